@@ -1,0 +1,174 @@
+/*
+ * sfdg.h -- C ABI of the B200-native Sparse Frequent Directions sketcher.
+ *
+ * Drop-in boundary for the reference's C++ sketch interface
+ * (/root/reference/proj/core/include/sfd/sketch.hpp:9-49,71 and shrink.hpp:26-41).
+ * Plain pointers and sizes only; no exceptions cross this boundary. Every entry
+ * point returns a status code that mirrors the reference's exception classes
+ * (core/include/sfd/common.hpp:14-17, mapped to exit codes in tools/sfd_main.cpp:289-298):
+ *
+ *   SFDG_OK (0), SFDG_INVALID_ARGUMENT (1) = std::invalid_argument,
+ *   SFDG_NUMERICAL_ERROR (2) = sfd::numerical_error, SFDG_CUDA_ERROR (3) = device fault.
+ *
+ * sfdg_last_error() returns the thread-local message of the last failure.
+ *
+ * Matrices are FP64 row-major like sfd::DenseMatrix (dense_matrix.hpp:10-30). Sparse
+ * inputs are CSR like sfd::SparseBuffer (sparse.hpp:52-57): int64 row offsets,
+ * uint32 strictly increasing column indices, FP64 values. Host pointers are read
+ * before the call returns; the caller keeps ownership.
+ *
+ * All compute runs on the selected CUDA device (sm_100a). There is no CPU path:
+ * without a usable device every compute entry point returns SFDG_CUDA_ERROR.
+ */
+#ifndef SFDG_H
+#define SFDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFDG_OK 0
+#define SFDG_INVALID_ARGUMENT 1
+#define SFDG_NUMERICAL_ERROR 2
+#define SFDG_CUDA_ERROR 3
+
+/* PowerConfig (randsvd.hpp:10-14). q_override < 0 means "not set". */
+typedef struct {
+    double epsilon;     /* default 0.25 */
+    double q_constant;  /* default 1.0  */
+    int64_t q_override; /* default -1   */
+} sfdg_power_config;
+
+/* SketchConfig (sketch.hpp:9-17). */
+typedef struct {
+    size_t ell;
+    size_t d;
+    double delta; /* default 0.1 */
+    sfdg_power_config power;
+    uint64_t seed;
+} sfdg_sketch_config;
+
+/* Draw state of sfd::Rng (rng.hpp:12-31): std::mt19937_64(seed) after `words` raw
+ * outputs, plus the cached Box-Muller spare. A fresh Rng(seed) is {seed, 0, 0, 0}. */
+typedef struct {
+    uint64_t seed;
+    uint64_t words;
+    int32_t has_spare;
+    double spare;
+} sfdg_rng_state;
+
+/* VerifierState (shrink.hpp:11-16). Fresh state: {0, delta, 2.0, 0.0}. */
+typedef struct {
+    size_t i;
+    double delta;
+    double c_verify;
+    double delta_spent;
+} sfdg_verifier_state;
+
+/* Accessor snapshot of SfdSketcher (sketch.hpp:35-48). */
+typedef struct {
+    size_t flush_count;   /* flush_count()   */
+    size_t attempt_total; /* attempt_total() */
+    sfdg_verifier_state verifier;
+    size_t buffer_rows; /* buffer().rows()    */
+    size_t buffer_nnz;  /* buffer().nnz()     */
+    double buffer_frob_sq;
+    sfdg_rng_state rng;
+} sfdg_stats;
+
+typedef struct sfdg_sketcher sfdg_sketcher;
+
+const char* sfdg_last_error(void);
+const char* sfdg_version(void);
+/* Number of visible CUDA devices (0 on a machine without a GPU; never an error). */
+int sfdg_device_count(int* count);
+
+/* ---- SfdSketcher (sketch.hpp:22-49; sketch.cpp:9-45) -------------------------- */
+
+/* SfdSketcher(const SketchConfig&): validates (1 <= ell <= d, 0 < delta < 1). */
+int sfdg_sketcher_create(const sfdg_sketch_config* cfg, int device, sfdg_sketcher** out);
+int sfdg_sketcher_destroy(sfdg_sketcher* h);
+
+/* append(const SparseRow&) for nrows rows at once. Row r is cols/vals[row_ptr[r] ..
+ * row_ptr[r+1]). Rows are committed in order exactly as repeated append() calls
+ * would: the flush trigger (nnz >= ell*d || rows == d, sketch.cpp:22) is evaluated
+ * after every row. A row failing validation (sparse.cpp:8-20) stops the batch with
+ * SFDG_INVALID_ARGUMENT; earlier rows stay committed; *rows_done (optional) reports
+ * how many were. */
+int sfdg_sketcher_append_csr(sfdg_sketcher* h, const int64_t* row_ptr, const uint32_t* cols,
+                             const double* vals, size_t nrows, size_t* rows_done);
+
+/* Same, for a CSR whose cols/vals already sit in device memory of this sketcher's
+ * GPU (d_cols/d_vals indexed by the host row offsets h_row_ptr). Validation and
+ * the Frobenius bookkeeping run on the device. */
+int sfdg_sketcher_append_csr_device(sfdg_sketcher* h, const int64_t* h_row_ptr, const uint32_t* d_cols,
+                                    const double* d_vals, size_t nrows, size_t* rows_done);
+
+/* finalize() (sketch.cpp:34-45): flushes or densify-merges the remainder, writes
+ * B (ell x d, row-major) to host `out` (may be NULL). */
+int sfdg_sketcher_finalize(sfdg_sketcher* h, double* out);
+/* sketch(): current B (ell x d row-major) to host memory. */
+int sfdg_sketcher_get_sketch(sfdg_sketcher* h, double* out);
+/* Device-side B^T (d x ell, row-major, leading dimension ld >= ell) for the merge tree. */
+int sfdg_sketcher_get_sketch_device(sfdg_sketcher* h, double* d_out, size_t ld);
+/* flush_count(), attempt_total(), verifier(), buffer() sizes, RNG position. */
+int sfdg_sketcher_stats(sfdg_sketcher* h, sfdg_stats* out);
+/* buffer() contents (CSR, host): row_ptr (rows+1), cols (nnz), vals (nnz). */
+int sfdg_sketcher_get_buffer(sfdg_sketcher* h, int64_t* row_ptr, uint32_t* cols, double* vals);
+/* Blocks until all queued device work of this sketcher finished. */
+int sfdg_sketcher_synchronize(sfdg_sketcher* h);
+
+/* ---- free functions (shrink.hpp:26-41, sketch.hpp:71, randsvd.hpp:18-26) ------- */
+
+/* merge(b1, b2, ell) = dense_shrink(vstack(b1, b2), ell)  (sketch.cpp:80-83). */
+int sfdg_merge(const double* b1, size_t rows1, const double* b2, size_t rows2, size_t d, size_t ell,
+               double* out, int device);
+/* Device-resident merge for the shard tree: inputs/outputs are B^T (d x ell, leading
+ * dimension ld) on `device`; `stream` is a cudaStream_t (NULL = legacy default). */
+int sfdg_merge_device(const double* d_b1t, const double* d_b2t, size_t ell, size_t d, size_t ld,
+                      double* d_outt, int device, void* stream);
+/* dense_shrink(a, ell) (shrink.cpp:30-61), host in/out. */
+int sfdg_dense_shrink(const double* a, size_t rows, size_t cols, size_t ell, double* out, int device);
+/* sparse_shrink(buffer, ell, power, rng) (shrink.cpp:63-73); rng advanced in place. */
+int sfdg_sparse_shrink(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t m, size_t d,
+                       size_t ell, const sfdg_power_config* power, sfdg_rng_state* rng, double* out,
+                       int device);
+/* boosted_sparse_shrink (shrink.cpp:104-131); verifier and rng advanced in place. */
+int sfdg_boosted_sparse_shrink(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t m,
+                               size_t d, size_t ell, sfdg_verifier_state* verifier,
+                               const sfdg_power_config* power, sfdg_rng_state* rng, double* out,
+                               double* delta_hat, size_t* attempts, int device);
+/* simultaneous_iteration (randsvd.cpp:18-51): orthonormal basis Z (m x k) of the
+ * dominant left subspace; rng advanced in place. */
+int sfdg_simultaneous_iteration(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t m,
+                                size_t d, size_t k, const sfdg_power_config* power, sfdg_rng_state* rng,
+                                double* z_out, int device);
+/* power_iteration_count (randsvd.cpp:10-16). */
+int sfdg_power_iteration_count(size_t m, const sfdg_power_config* power, size_t* q);
+
+/* ---- device kernels exposed for parity tests (la_core.hpp:23-41) --------------- */
+
+/* gaussian_matrix(rows, cols, rng) (la_core.cpp:167-172) generated on the device. */
+int sfdg_gaussian_matrix(sfdg_rng_state* rng, size_t rows, size_t cols, double* out, int device);
+/* jacobi_eigh contract (la_core.cpp:24-80): eigenvalues descending + eigenvectors
+ * (column k, n x n row-major) of a symmetric matrix, off-diagonal tolerance off_tol. */
+int sfdg_eigh(const double* sym, size_t n, double off_tol, double* values, double* vectors, int device);
+/* orthonormalize contract (la_core.cpp:130-165) via device CholeskyQR2 with the same
+ * column-drop rule (n x k, n >= k). */
+int sfdg_orthonormalize(const double* in, size_t n, size_t k, double* out, int device);
+/* Sparse products of SparseBuffer (sparse.cpp:32-69) on the device:
+ * y = A x (m x k, x: d x k), w = A^T z (d x k, z: m x k). Either output may be NULL. */
+int sfdg_csr_products(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t m, size_t d,
+                      size_t k, const double* x, double* y, const double* z, double* w, int device);
+
+/* Process-wide count of kernels this library launched (benchmark gpu_launches claim). */
+uint64_t sfdg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFDG_H */

@@ -130,6 +130,7 @@ class Oracle:
             f.argtypes = [C.c_void_p]
         L.or_rng_uniform_below.restype = C.c_uint64
         L.or_rng_uniform_below.argtypes = [C.c_void_p, C.c_uint64]
+        L.or_rng_state.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_int), _dp]
         L.or_last_error.restype = C.c_char_p
         L.or_power_iteration_count.argtypes = [C.c_size_t, C.c_double, C.c_double, C.c_longlong, _szp]
         L.or_jacobi_eigh.argtypes = [_dp, C.c_size_t, C.c_double, _dp, _dp]
@@ -266,6 +267,7 @@ class Rng:
 
     def __init__(self, lib: Oracle, seed: int):
         self.lib = lib
+        self.seed = seed
         self.h = lib.L.or_rng_new(C.c_uint64(seed))
 
     def __del__(self):
@@ -290,6 +292,12 @@ class Rng:
 
     def normals_drawn(self):
         return self.lib.L.or_rng_normals_drawn(self.h)
+
+    def state(self):
+        """(seed-relative raw words consumed, has_spare, spare) -- the full Rng draw state."""
+        w, hs, sp = C.c_uint64(), C.c_int(), C.c_double()
+        self.lib.L.or_rng_state(self.h, C.byref(w), C.byref(hs), C.byref(sp))
+        return w.value, bool(hs.value), sp.value
 
 
 class OracleSketcher:

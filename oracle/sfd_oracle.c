@@ -160,6 +160,7 @@ struct or_rng {
     double spare;
     int has_spare;
     uint64_t normals;
+    uint64_t words; /* raw engine outputs consumed */
 };
 
 /* std::mt19937_64(seed) state initialisation ([rand.eng.mers], f = 6364136223846793005). */
@@ -186,6 +187,7 @@ static uint64_t mt_next(or_rng* r) {
         r->mt[MT_N - 1] = r->mt[MT_M - 1] ^ (x >> 1) ^ ((x & 1ULL) ? MT_A : 0ULL);
         r->mti = 0;
     }
+    r->words += 1;
     uint64_t x = r->mt[r->mti++];
     x ^= (x >> 29) & 0x5555555555555555ULL;
     x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
@@ -232,6 +234,11 @@ double or_rng_normal(or_rng* r) {
     return rad * cos(theta);
 }
 uint64_t or_rng_normals_drawn(const or_rng* r) { return r->normals; }
+void or_rng_state(const or_rng* r, uint64_t* words, int* has_spare, double* spare) {
+    *words = r->words;
+    *has_spare = r->has_spare;
+    *spare = r->spare;
+}
 
 /* ------------------------------------------------------------------------- */
 /* la_core (core/src/la_core.cpp)                                              */
@@ -792,6 +799,7 @@ int or_sketcher_new(const or_sketch_cfg* cfg, or_sketcher** out) {
     mt_seed(&s->rng, cfg->seed);
     s->rng.has_spare = 0;
     s->rng.normals = 0;
+    s->rng.words = 0;
     *out = s;
     LEAVE();
 }

@@ -40,6 +40,8 @@ uint64_t or_rng_uniform_below(or_rng* r, uint64_t n);
 double or_rng_normal(or_rng* r);
 /* Number of normals drawn so far (offset into the normal stream). */
 uint64_t or_rng_normals_drawn(const or_rng* r);
+/* Full draw state: raw words consumed, cached Box-Muller spare. */
+void or_rng_state(const or_rng* r, uint64_t* words, int* has_spare, double* spare);
 
 /* ---- power_iteration_count (core/src/randsvd.cpp:10-16) ---- */
 /* q_override < 0 means "no override". */

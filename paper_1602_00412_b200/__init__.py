@@ -1,0 +1,465 @@
+"""B200-native Sparse Frequent Directions (arXiv 1602.00412) -- host-side mirror.
+
+The product is ``libsfdg.so`` (CUDA, sm_100a) behind the C ABI in ``include/sfdg.h``.
+This module binds that ABI with ctypes and mirrors the reference C++ interface
+(/root/reference/proj/core/include/sfd/sketch.hpp:9-71, shrink.hpp:11-41,
+randsvd.hpp:10-26, la_core.hpp:23-41) so parity tests read like the reference's own:
+
+    cfg = SketchConfig(ell=100, d=10_000, seed=1)
+    s = SfdSketcher(cfg)              # SfdSketcher(const SketchConfig&)
+    s.append(indices, values)         # append(const SparseRow&)
+    s.append_csr(row_ptr, cols, vals) # many rows, same per-row trigger semantics
+    B = s.finalize()                  # ell x d, float64
+
+Errors map to the reference's exception classes: ``InvalidArgument`` (ValueError) for
+std::invalid_argument, ``NumericalError`` (ArithmeticError) for sfd::numerical_error.
+There is no CPU fallback: importing works anywhere, but every compute call needs the
+CUDA library and a GPU and raises ``CudaError`` otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+__all__ = [
+    "SketchConfig", "PowerConfig", "VerifierState", "RngState", "SfdSketcher", "merge", "merge_device",
+    "dense_shrink", "sparse_shrink", "boosted_sparse_shrink", "simultaneous_iteration", "power_iteration_count",
+    "gaussian_matrix", "eigh", "orthonormalize", "csr_products", "device_count", "launch_count", "lib",
+    "InvalidArgument", "NumericalError", "CudaError", "KALPHA", "LIB_PATH",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsfdg.so")
+KALPHA = 6.0 / 41.0  # core/include/sfd/common.hpp:10
+
+
+class SfdError(Exception):
+    pass
+
+
+class InvalidArgument(SfdError, ValueError):
+    """std::invalid_argument (SFDG_INVALID_ARGUMENT)."""
+
+
+class NumericalError(SfdError, ArithmeticError):
+    """sfd::numerical_error (SFDG_NUMERICAL_ERROR)."""
+
+
+class CudaError(SfdError, RuntimeError):
+    """Device fault or no device (SFDG_CUDA_ERROR)."""
+
+
+_dp = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+_u32p = C.POINTER(C.c_uint32)
+_szp = C.POINTER(C.c_size_t)
+
+
+class _Power(C.Structure):
+    _fields_ = [("epsilon", C.c_double), ("q_constant", C.c_double), ("q_override", C.c_int64)]
+
+
+class _SketchCfg(C.Structure):
+    _fields_ = [("ell", C.c_size_t), ("d", C.c_size_t), ("delta", C.c_double), ("power", _Power),
+                ("seed", C.c_uint64)]
+
+
+class _Rng(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("words", C.c_uint64), ("has_spare", C.c_int32), ("spare", C.c_double)]
+
+
+class _Verifier(C.Structure):
+    _fields_ = [("i", C.c_size_t), ("delta", C.c_double), ("c_verify", C.c_double), ("delta_spent", C.c_double)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("flush_count", C.c_size_t), ("attempt_total", C.c_size_t), ("verifier", _Verifier),
+                ("buffer_rows", C.c_size_t), ("buffer_nnz", C.c_size_t), ("buffer_frob_sq", C.c_double),
+                ("rng", _Rng)]
+
+
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    """Load libsfdg.so (fails loudly when it was not built)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: build it with `make -C {HERE}` (or __graft_entry__.build())")
+    L = C.CDLL(LIB_PATH)
+    L.sfdg_last_error.restype = C.c_char_p
+    L.sfdg_version.restype = C.c_char_p
+    L.sfdg_launch_count.restype = C.c_uint64
+    L.sfdg_device_count.argtypes = [C.POINTER(C.c_int)]
+    L.sfdg_sketcher_create.argtypes = [C.POINTER(_SketchCfg), C.c_int, C.POINTER(C.c_void_p)]
+    L.sfdg_sketcher_destroy.argtypes = [C.c_void_p]
+    L.sfdg_sketcher_append_csr.argtypes = [C.c_void_p, _i64p, _u32p, _dp, C.c_size_t, _szp]
+    L.sfdg_sketcher_append_csr_device.argtypes = [C.c_void_p, _i64p, C.c_void_p, C.c_void_p, C.c_size_t, _szp]
+    L.sfdg_sketcher_finalize.argtypes = [C.c_void_p, _dp]
+    L.sfdg_sketcher_get_sketch.argtypes = [C.c_void_p, _dp]
+    L.sfdg_sketcher_get_sketch_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+    L.sfdg_sketcher_stats.argtypes = [C.c_void_p, C.POINTER(_Stats)]
+    L.sfdg_sketcher_get_buffer.argtypes = [C.c_void_p, _i64p, _u32p, _dp]
+    L.sfdg_sketcher_synchronize.argtypes = [C.c_void_p]
+    L.sfdg_merge.argtypes = [_dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_int]
+    L.sfdg_merge_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int,
+                                    C.c_void_p]
+    L.sfdg_dense_shrink.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_int]
+    csr = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t]
+    L.sfdg_sparse_shrink.argtypes = csr + [C.c_size_t, C.POINTER(_Power), C.POINTER(_Rng), _dp, C.c_int]
+    L.sfdg_boosted_sparse_shrink.argtypes = csr + [C.c_size_t, C.POINTER(_Verifier), C.POINTER(_Power),
+                                                   C.POINTER(_Rng), _dp, _dp, _szp, C.c_int]
+    L.sfdg_simultaneous_iteration.argtypes = csr + [C.c_size_t, C.POINTER(_Power), C.POINTER(_Rng), _dp, C.c_int]
+    L.sfdg_power_iteration_count.argtypes = [C.c_size_t, C.POINTER(_Power), _szp]
+    L.sfdg_gaussian_matrix.argtypes = [C.POINTER(_Rng), C.c_size_t, C.c_size_t, _dp, C.c_int]
+    L.sfdg_eigh.argtypes = [_dp, C.c_size_t, C.c_double, _dp, _dp, C.c_int]
+    L.sfdg_orthonormalize.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_int]
+    L.sfdg_csr_products.argtypes = csr + [C.c_size_t, _dp, _dp, _dp, _dp, C.c_int]
+    _LIB = L
+    return L
+
+
+def _check(code: int) -> None:
+    if code == 0:
+        return
+    msg = lib().sfdg_last_error().decode(errors="replace")
+    if code == 1:
+        raise InvalidArgument(msg)
+    if code == 2:
+        raise NumericalError(msg)
+    raise CudaError(msg)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def _csr(row_ptr, cols, vals):
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    cs = np.ascontiguousarray(cols, dtype=np.uint32)
+    vs = np.ascontiguousarray(vals, dtype=np.float64)
+    if cs.size == 0:  # keep valid pointers for empty inputs
+        cs, vs = np.zeros(1, np.uint32), np.zeros(1)
+    return rp, cs, vs
+
+
+class PowerConfig:
+    """randsvd.hpp:10-14 (q_override None = unset)."""
+
+    def __init__(self, epsilon: float = 0.25, q_constant: float = 1.0, q_override: int | None = None):
+        self.epsilon, self.q_constant, self.q_override = float(epsilon), float(q_constant), q_override
+
+    def _c(self) -> _Power:
+        return _Power(self.epsilon, self.q_constant, -1 if self.q_override is None else int(self.q_override))
+
+
+class SketchConfig:
+    """sketch.hpp:9-17."""
+
+    def __init__(self, ell: int = 0, d: int = 0, delta: float = 0.1, power: PowerConfig | None = None, seed: int = 0):
+        self.ell, self.d, self.delta, self.seed = int(ell), int(d), float(delta), int(seed)
+        self.power = power or PowerConfig()
+
+    def _c(self) -> _SketchCfg:
+        return _SketchCfg(self.ell, self.d, self.delta, self.power._c(), self.seed)
+
+
+class VerifierState:
+    """shrink.hpp:11-16."""
+
+    def __init__(self, delta: float = 0.1, i: int = 0, c_verify: float = 2.0, delta_spent: float = 0.0):
+        self.i, self.delta, self.c_verify, self.delta_spent = int(i), float(delta), float(c_verify), float(delta_spent)
+
+    def _c(self) -> _Verifier:
+        return _Verifier(self.i, self.delta, self.c_verify, self.delta_spent)
+
+    def _update(self, v: _Verifier) -> None:
+        self.i, self.delta_spent = int(v.i), float(v.delta_spent)
+
+    def __repr__(self):
+        return f"VerifierState(i={self.i}, delta={self.delta}, delta_spent={self.delta_spent})"
+
+
+class RngState:
+    """Position in sfd::Rng's stream (rng.hpp:12-31): Rng(seed) after `words` raw draws."""
+
+    def __init__(self, seed: int = 0, words: int = 0, has_spare: bool = False, spare: float = 0.0):
+        self.seed, self.words, self.has_spare, self.spare = int(seed), int(words), bool(has_spare), float(spare)
+
+    def _c(self) -> _Rng:
+        return _Rng(self.seed, self.words, 1 if self.has_spare else 0, self.spare)
+
+    def _update(self, r: _Rng) -> None:
+        self.words, self.has_spare, self.spare = int(r.words), bool(r.has_spare), float(r.spare)
+
+    def __repr__(self):
+        return f"RngState(seed={self.seed}, words={self.words}, has_spare={self.has_spare})"
+
+
+def device_count() -> int:
+    n = C.c_int()
+    lib().sfdg_device_count(C.byref(n))
+    return n.value
+
+
+def launch_count() -> int:
+    return int(lib().sfdg_launch_count())
+
+
+class SfdSketcher:
+    """sfd::SfdSketcher (sketch.hpp:22-49) running on one B200."""
+
+    def __init__(self, cfg: SketchConfig, device: int = 0):
+        self.cfg = cfg
+        self.device = device
+        self._h = C.c_void_p()
+        c = cfg._c()
+        _check(lib().sfdg_sketcher_create(C.byref(c), device, C.byref(self._h)))
+
+    def close(self) -> None:
+        if self._h:
+            lib().sfdg_sketcher_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- append ------------------------------------------------------------
+    def append(self, indices, values) -> None:
+        """append(const SparseRow&) (sketch.cpp:20-23)."""
+        idx = np.ascontiguousarray(indices, dtype=np.int64)
+        val = np.ascontiguousarray(values, dtype=np.float64)
+        if idx.shape != val.shape:
+            raise InvalidArgument("append_row: index/value length mismatch")
+        if idx.size and (idx.min() < 0 or idx.max() >= 2 ** 32):
+            raise InvalidArgument("append_row: column index out of range")
+        self.append_csr(np.array([0, idx.size], dtype=np.int64), idx.astype(np.uint32), val)
+
+    def append_csr(self, row_ptr, cols, vals) -> int:
+        """Append many rows; returns rows committed. Raises on the first bad row."""
+        rp, cs, vs = _csr(row_ptr, cols, vals)
+        done = C.c_size_t()
+        _check(lib().sfdg_sketcher_append_csr(self._h, _p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), len(rp) - 1,
+                                              C.byref(done)))
+        return done.value
+
+    def append_csr_device(self, h_row_ptr, d_cols_ptr: int, d_vals_ptr: int) -> int:
+        """Rows whose cols/vals already live in this GPU's memory (raw device pointers)."""
+        rp = np.ascontiguousarray(h_row_ptr, dtype=np.int64)
+        done = C.c_size_t()
+        _check(lib().sfdg_sketcher_append_csr_device(self._h, _p(rp, _i64p), C.c_void_p(d_cols_ptr),
+                                                     C.c_void_p(d_vals_ptr), len(rp) - 1, C.byref(done)))
+        return done.value
+
+    # ---- results / accessors -------------------------------------------------
+    def finalize(self) -> np.ndarray:
+        out = np.zeros((self.cfg.ell, self.cfg.d))
+        _check(lib().sfdg_sketcher_finalize(self._h, _p(out, _dp)))
+        return out
+
+    def sketch(self) -> np.ndarray:
+        out = np.zeros((self.cfg.ell, self.cfg.d))
+        _check(lib().sfdg_sketcher_get_sketch(self._h, _p(out, _dp)))
+        return out
+
+    def sketch_device_t(self, d_out_ptr: int, ld: int) -> None:
+        """B^T (d x ell, leading dimension ld) into device memory (merge tree input)."""
+        _check(lib().sfdg_sketcher_get_sketch_device(self._h, C.c_void_p(d_out_ptr), ld))
+
+    def _stats(self) -> _Stats:
+        s = _Stats()
+        _check(lib().sfdg_sketcher_stats(self._h, C.byref(s)))
+        return s
+
+    def flush_count(self) -> int:
+        return int(self._stats().flush_count)
+
+    def attempt_total(self) -> int:
+        return int(self._stats().attempt_total)
+
+    def verifier(self) -> VerifierState:
+        v = self._stats().verifier
+        return VerifierState(v.delta, v.i, v.c_verify, v.delta_spent)
+
+    def rng_state(self) -> RngState:
+        r = self._stats().rng
+        return RngState(r.seed, r.words, bool(r.has_spare), r.spare)
+
+    def stats(self) -> dict:
+        s = self._stats()
+        return {"flushes": s.flush_count, "attempts": s.attempt_total, "verifier_i": s.verifier.i,
+                "delta_spent": s.verifier.delta_spent, "buf_rows": s.buffer_rows, "buf_nnz": s.buffer_nnz,
+                "buf_frob_sq": s.buffer_frob_sq, "rng_words": s.rng.words, "rng_has_spare": bool(s.rng.has_spare)}
+
+    def buffer(self):
+        """buffer(): (row_ptr int64, cols uint32, vals float64) of the unflushed rows."""
+        s = self._stats()
+        rp = np.zeros(s.buffer_rows + 1, np.int64)
+        cs = np.zeros(max(1, s.buffer_nnz), np.uint32)
+        vs = np.zeros(max(1, s.buffer_nnz))
+        _check(lib().sfdg_sketcher_get_buffer(self._h, _p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp)))
+        return rp, cs[: s.buffer_nnz], vs[: s.buffer_nnz]
+
+    def buffer_dense(self) -> np.ndarray:
+        rp, cs, vs = self.buffer()
+        out = np.zeros((len(rp) - 1, self.cfg.d))
+        for i in range(len(rp) - 1):
+            out[i, cs[rp[i]:rp[i + 1]]] = vs[rp[i]:rp[i + 1]]
+        return out
+
+    def synchronize(self) -> None:
+        _check(lib().sfdg_sketcher_synchronize(self._h))
+
+
+# ---- free functions ------------------------------------------------------------
+
+def merge(b1, b2, ell: int, device: int = 0) -> np.ndarray:
+    """merge(b1, b2, ell) = dense_shrink(vstack(b1, b2), ell) (sketch.cpp:80-83)."""
+    b1, b2 = _f64(b1), _f64(b2)
+    if b1.ndim != 2 or b2.ndim != 2 or b1.shape[1] != b2.shape[1]:
+        raise InvalidArgument("merge: column mismatch")
+    d = b1.shape[1]
+    out = np.zeros((ell, d))
+    _check(lib().sfdg_merge(_p(b1, _dp), b1.shape[0], _p(b2, _dp), b2.shape[0], d, ell, _p(out, _dp), device))
+    return out
+
+
+def merge_device(d_b1t: int, d_b2t: int, ell: int, d: int, ld: int, d_outt: int, device: int = 0,
+                 stream: int = 0) -> None:
+    """Device merge of two B^T (d x ell, leading dim ld) into d_outt."""
+    _check(lib().sfdg_merge_device(C.c_void_p(d_b1t), C.c_void_p(d_b2t), ell, d, ld, C.c_void_p(d_outt), device,
+                                   C.c_void_p(stream) if stream else None))
+
+
+def dense_shrink(a, ell: int, device: int = 0) -> np.ndarray:
+    """dense_shrink(a, ell) (shrink.cpp:30-61)."""
+    a = _f64(a)
+    out = np.zeros((ell, a.shape[1]))
+    _check(lib().sfdg_dense_shrink(_p(a, _dp), a.shape[0], a.shape[1], ell, _p(out, _dp), device))
+    return out
+
+
+def _rng_arg(rng) -> RngState:
+    if isinstance(rng, RngState):
+        return rng
+    if hasattr(rng, "state") and hasattr(rng, "seed"):  # oracle Rng: adopt its draw position
+        w, hs, sp = rng.state()
+        return RngState(rng.seed, w, hs, sp)
+    return RngState(int(rng))
+
+
+def sparse_shrink(csr, d: int, ell: int, rng, power: PowerConfig | None = None, device: int = 0):
+    """sparse_shrink(buffer, ell, power, rng) (shrink.cpp:63-73). Returns (B', RngState after)."""
+    rp, cs, vs = _csr(*csr)
+    st = _rng_arg(rng)
+    c = st._c()
+    pw = (power or PowerConfig())._c()
+    out = np.zeros((ell, d))
+    _check(lib().sfdg_sparse_shrink(_p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), len(rp) - 1, d, ell, C.byref(pw),
+                                    C.byref(c), _p(out, _dp), device))
+    st = RngState(st.seed)
+    st._update(c)
+    return out, st
+
+
+def boosted_sparse_shrink(csr, d: int, ell: int, state: VerifierState, rng, power: PowerConfig | None = None,
+                          device: int = 0):
+    """boosted_sparse_shrink (shrink.cpp:104-131). Returns (B', delta_hat, attempts, RngState after)."""
+    rp, cs, vs = _csr(*csr)
+    st = _rng_arg(rng)
+    c = st._c()
+    v = state._c()
+    pw = (power or PowerConfig())._c()
+    out = np.zeros((ell, d))
+    dh = C.c_double()
+    att = C.c_size_t()
+    _check(lib().sfdg_boosted_sparse_shrink(_p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), len(rp) - 1, d, ell,
+                                            C.byref(v), C.byref(pw), C.byref(c), _p(out, _dp), C.byref(dh),
+                                            C.byref(att), device))
+    state._update(v)
+    st = RngState(st.seed)
+    st._update(c)
+    return out, dh.value, att.value, st
+
+
+def simultaneous_iteration(csr, d: int, k: int, rng, power: PowerConfig | None = None, device: int = 0):
+    """simultaneous_iteration (randsvd.cpp:18-51). Returns (Z m x k, RngState after)."""
+    rp, cs, vs = _csr(*csr)
+    st = _rng_arg(rng)
+    c = st._c()
+    pw = (power or PowerConfig())._c()
+    m = len(rp) - 1
+    out = np.zeros((m, k))
+    _check(lib().sfdg_simultaneous_iteration(_p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), m, d, k, C.byref(pw),
+                                             C.byref(c), _p(out, _dp), device))
+    st = RngState(st.seed)
+    st._update(c)
+    return out, st
+
+
+def power_iteration_count(m: int, power: PowerConfig | None = None) -> int:
+    pw = (power or PowerConfig())._c()
+    q = C.c_size_t()
+    _check(lib().sfdg_power_iteration_count(m, C.byref(pw), C.byref(q)))
+    return q.value
+
+
+def gaussian_matrix(rows: int, cols: int, rng, device: int = 0):
+    """gaussian_matrix (la_core.cpp:167-172) on the device. Returns (G, RngState after)."""
+    st = _rng_arg(rng)
+    c = st._c()
+    out = np.zeros((rows, cols))
+    _check(lib().sfdg_gaussian_matrix(C.byref(c), rows, cols, _p(out, _dp), device))
+    st = RngState(st.seed)
+    st._update(c)
+    return out, st
+
+
+def eigh(sym, off_tol: float, device: int = 0):
+    """jacobi_eigh contract (la_core.cpp:24-80): (values desc, vectors columns)."""
+    s = _f64(sym)
+    n = s.shape[0]
+    vals, vecs = np.zeros(n), np.zeros((n, n))
+    _check(lib().sfdg_eigh(_p(s, _dp), n, off_tol, _p(vals, _dp), _p(vecs, _dp), device))
+    return vals, vecs
+
+
+def orthonormalize(a, device: int = 0) -> np.ndarray:
+    """orthonormalize contract (la_core.cpp:130-165) via device CholeskyQR2."""
+    a = _f64(a)
+    out = np.zeros_like(a)
+    _check(lib().sfdg_orthonormalize(_p(a, _dp), a.shape[0], a.shape[1], _p(out, _dp), device))
+    return out
+
+
+def csr_products(csr, d: int, x=None, z=None, device: int = 0):
+    """(A x, A^T z) for panels x (d x k) and z (m x k) (sparse.cpp:32-69)."""
+    rp, cs, vs = _csr(*csr)
+    m = len(rp) - 1
+    k = (x if x is not None else z).shape[1]
+    y = np.zeros((m, k)) if x is not None else None
+    w = np.zeros((d, k)) if z is not None else None
+    xx = _f64(x) if x is not None else None
+    zz = _f64(z) if z is not None else None
+    _check(lib().sfdg_csr_products(_p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), m, d, k,
+                                   _p(xx, _dp) if xx is not None else None, _p(y, _dp) if y is not None else None,
+                                   _p(zz, _dp) if zz is not None else None, _p(w, _dp) if w is not None else None,
+                                   device))
+    return y, w

@@ -1,0 +1,63 @@
+// common.cuh -- shared host/device helpers for the sfdg library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace sfdg {
+
+// Error classes mirroring the reference (core/include/sfd/common.hpp:14-17); the
+// C-ABI maps them to SFDG_INVALID_ARGUMENT / SFDG_NUMERICAL_ERROR / SFDG_CUDA_ERROR.
+struct invalid_argument : std::invalid_argument {
+    explicit invalid_argument(const std::string& w) : std::invalid_argument(w) {}
+};
+struct numerical_error : std::runtime_error {
+    explicit numerical_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct cuda_error : std::runtime_error {
+    explicit cuda_error(const std::string& w) : std::runtime_error(w) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        char buf[512];
+        snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e),
+                 file, line, what);
+        throw cuda_error(buf);
+    }
+}
+#define CK(x) ::sfdg::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Every kernel launch goes through LAUNCH so the process-wide launch counter
+// (sfdg_launch_count) is exact and launch errors surface immediately.
+extern std::atomic<uint64_t> g_launches;
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                                   \
+    do {                                                                                 \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                      \
+        ::sfdg::g_launches.fetch_add(1, std::memory_order_relaxed);                      \
+        CK(cudaGetLastError());                                                          \
+    } while (0)
+
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
+inline unsigned ceil_div(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+// Device error flags (one int array per context); bits set by kernels, read by host.
+enum : int {
+    ERR_NONFINITE_ITER = 1,     // simultaneous_iteration non-finite intermediate (randsvd.cpp:46-47)
+    ERR_NONFINITE_PROJ = 2,     // sparse_shrink non-finite projection (shrink.cpp:70)
+    ERR_NONFINITE_VERIFY = 4,   // verify_spectral non-finite operator output (shrink.cpp:90)
+    ERR_JACOBI_NOCONV = 8,      // jacobi_eigh 100 sweeps (la_core.cpp:34-35)
+    ERR_RNG_U1_ZERO = 16,       // Box-Muller u1 == 0 rejection (rng.cpp:27-29), p = 2^-53
+    ERR_BAD_INDEX = 32,         // device-input validation: index out of range / not increasing
+    ERR_BAD_VALUE = 64,         // device-input validation: non-finite value
+    ERR_NONFINITE_INPUT = 128,  // dense_shrink non-finite input (shrink.cpp:32)
+};
+
+}  // namespace sfdg

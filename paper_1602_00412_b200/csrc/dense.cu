@@ -1,0 +1,279 @@
+// dense.cu -- FP64 tall-skinny dense kernels on the DMMA tensor-core path.
+//
+// tcgen05 has no f64 kind on sm_100a, so FP64 contractions use the
+// legacy mma.sync m8n8k4 f64 (SASS DMMA.884); on B200 it runs at the FP64 peak
+// (36.9 TFLOP/s measured, profiles/r01_fp64_peak.txt -- same as DFMA) while cutting
+// register/LSU traffic per flop 8x versus scalar DFMA.
+//
+//  * gram_tn: C = X^T X for a tall X (n x k, k <= 512). The reference forms these
+//    Grams in orthonormalize (la_core.cpp:144-156, as MGS dot products), svd_top
+//    (la_core.cpp:90-100) and dense_shrink's tall path (shrink.cpp:43-52). Split-K
+//    over n into fixed chunks + fixed-order reduction: deterministic, no atomics.
+//  * gemm_nn: C = X S for tall X and small S (k x c): the CholQR apply Y R^-1,
+//    the right-vector recovery V = A^T U / sigma (la_core.cpp:113-126) fused with the
+//    shrink row scale (shrink.cpp:15-26).
+#include <algorithm>
+
+#include "common.cuh"
+#include "dense.cuh"
+
+namespace sfdg {
+
+namespace {
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+constexpr int TB = 64;   // output tile
+constexpr int KT = 32;   // k-chunk staged in smem
+constexpr int LDT = TB + 4;  // 68: conflict-free fragment reads (68 mod 16 == 4)
+constexpr int LDK = KT + 4;  // 36
+
+// Partial Gram of rows [r0, r1) for the upper tile (ti, tj): partial[chunk] (k x k).
+__global__ void __launch_bounds__(128) gram_tn_kernel(const double* __restrict__ X, int n, int k, int ldx,
+                                                      int rows_per_chunk, int T, double* __restrict__ partial) {
+    __shared__ double As[KT][LDT];
+    __shared__ double Bs[KT][LDT];
+    int ti = 0, rem = blockIdx.x;  // linear upper-triangle tile index -> (ti, tj)
+    while (rem >= T - ti) {
+        rem -= T - ti;
+        ++ti;
+    }
+    const int tj = ti + rem;
+    const int i0 = ti * TB, j0 = tj * TB;
+    const int chunk = blockIdx.y;
+    const int r0 = chunk * rows_per_chunk;
+    const int r1 = min(n, r0 + rows_per_chunk);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = w & 1, wn = w >> 1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int kb = r0; kb < r1; kb += KT) {
+        for (int e = threadIdx.x; e < KT * TB; e += 128) {
+            const int r = e / TB, c = e % TB;
+            const int row = kb + r;
+            const bool rok = row < r1;
+            As[r][c] = (rok && i0 + c < k) ? X[(size_t)row * ldx + i0 + c] : 0.0;
+            Bs[r][c] = (rok && j0 + c < k) ? X[(size_t)row * ldx + j0 + c] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < KT; ks += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = As[ks + t][wm * 32 + mi * 8 + g];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[ks + t][wn * 32 + ni * 8 + g];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncthreads();
+    }
+    double* P = partial + (size_t)chunk * k * k;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const int row = i0 + wm * 32 + mi * 8 + g;
+            const int col = j0 + wn * 32 + ni * 8 + 2 * t;
+            if (row < k) {
+                if (col < k) P[(size_t)row * k + col] = acc[mi][ni][0];
+                if (col + 1 < k) P[(size_t)row * k + col + 1] = acc[mi][ni][1];
+            }
+        }
+}
+
+__global__ void gram_reduce_kernel(const double* __restrict__ partial, int nchunks, int k, double* __restrict__ out,
+                                   int ldo) {
+    const int total = k * k;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        int i = e / k, j = e % k;
+        if (i / TB > j / TB) {  // lower tiles were not computed: mirror
+            const int tmp = i;
+            i = j;
+            j = tmp;
+        }
+        double s = 0.0;
+        for (int c = 0; c < nchunks; ++c) s += partial[(size_t)c * total + (size_t)i * k + j];
+        out[(size_t)(e / k) * ldo + (e % k)] = s;
+    }
+}
+
+__global__ void __launch_bounds__(128) gemm_nn_kernel(const double* __restrict__ X, int n, int k, int ldx,
+                                                      const double* __restrict__ S, int c, int lds,
+                                                      double* __restrict__ C, int ldc) {
+    __shared__ double Xs[TB][LDK];
+    __shared__ double Ss[KT][LDT];
+    const int r0 = blockIdx.x * TB, c0 = blockIdx.y * TB;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = w & 1, wn = w >> 1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int kk = 0; kk < k; kk += KT) {
+        for (int e = threadIdx.x; e < TB * KT; e += 128) {
+            const int r = e / KT, q = e % KT;
+            Xs[r][q] = (r0 + r < n && kk + q < k) ? X[(size_t)(r0 + r) * ldx + kk + q] : 0.0;
+        }
+        for (int e = threadIdx.x; e < KT * TB; e += 128) {
+            const int q = e / TB, cc = e % TB;
+            Ss[q][cc] = (kk + q < k && c0 + cc < c) ? S[(size_t)(kk + q) * lds + c0 + cc] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < KT; ks += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = Xs[wm * 32 + mi * 8 + g][ks + t];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) b[ni] = Ss[ks + t][wn * 32 + ni * 8 + g];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const int row = r0 + wm * 32 + mi * 8 + g;
+            const int col = c0 + wn * 32 + ni * 8 + 2 * t;
+            if (row < n) {
+                if (col < c) C[(size_t)row * ldc + col] = acc[mi][ni][0];
+                if (col + 1 < c) C[(size_t)row * ldc + col + 1] = acc[mi][ni][1];
+            }
+        }
+}
+
+constexpr int kRedBlocks = 2 * kSMs;
+
+// Deterministic sum of squares: fixed grid, fixed per-thread stride order, fixed trees.
+__global__ void sumsq_partial_kernel(const double* __restrict__ X, int64_t rows, int cols, int ld,
+                                     double* __restrict__ partial, int* __restrict__ err, int err_bit) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    bool bad = false;
+    const int64_t total = rows * (int64_t)cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const double v = X[(e / cols) * ld + e % cols];
+        if (!isfinite(v)) bad = true;
+        s = fma(v, v, s);
+    }
+    if (bad && err) atomicOr(err, err_bit);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) partial[blockIdx.x] = s;
+    }
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ partial, int n, double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += partial[i];
+        *out = s;
+    }
+}
+
+__global__ void transpose_kernel(const double* __restrict__ in, int rows, int cols, int ldi, double* __restrict__ out,
+                                 int ldo) {
+    __shared__ double tile[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int r = by + j, c = bx + threadIdx.x;
+        if (r < rows && c < cols) tile[j][threadIdx.x] = in[(size_t)r * ldi + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int r = bx + j, c = by + threadIdx.x;  // out row = in col
+        if (r < cols && c < rows) out[(size_t)r * ldo + c] = tile[threadIdx.x][j];
+    }
+}
+
+__global__ void copy2d_kernel(const double* __restrict__ in, int rows, int cols, int ldi, double* __restrict__ out,
+                              int ldo) {
+    const int64_t total = (int64_t)rows * cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+        out[(e / cols) * ldo + e % cols] = in[(e / cols) * ldi + e % cols];
+}
+
+__global__ void fill2d_kernel(double* __restrict__ out, int rows, int cols, int ldo, double v) {
+    const int64_t total = (int64_t)rows * cols;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+        out[(e / cols) * ldo + e % cols] = v;
+}
+
+}  // namespace
+
+void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scratch& scr, cudaStream_t st) {
+    if (k <= 0) return;
+    if (n <= 0) {
+        fill2d(out, k, k, ldo, 0.0, st);
+        return;
+    }
+    const int T = (k + TB - 1) / TB;
+    const int ntiles = T * (T + 1) / 2;
+    int target_chunks = std::max(1, (2 * kSMs + ntiles - 1) / ntiles);
+    int rows_per_chunk = (int)round_up(std::max<int64_t>(KT * 4, ((int64_t)n + target_chunks - 1) / target_chunks), KT);
+    const int nchunks = (n + rows_per_chunk - 1) / rows_per_chunk;
+    double* partial = scr.take<double>((int64_t)nchunks * k * k);
+    LAUNCH(gram_tn_kernel, dim3(ntiles, nchunks), 128, 0, st, X, n, k, ldx, rows_per_chunk, T, partial);
+    LAUNCH(gram_reduce_kernel, std::max(1u, std::min(4u * kSMs, ceil_div((size_t)k * k, 256))), 256, 0, st, partial,
+           nchunks, k, out, ldo);
+}
+
+void gemm_nn(const double* X, int n, int k, int ldx, const double* S, int c, int lds, double* C, int ldc,
+             cudaStream_t st) {
+    if (n <= 0 || c <= 0) return;
+    if (k <= 0) {
+        fill2d(C, n, c, ldc, 0.0, st);
+        return;
+    }
+    LAUNCH(gemm_nn_kernel, dim3(ceil_div(n, TB), ceil_div(c, TB)), 128, 0, st, X, n, k, ldx, S, c, lds, C, ldc);
+}
+
+void sumsq(const double* X, int64_t rows, int cols, int ld, double* d_out, int* d_err, int err_bit, Scratch& scr,
+           cudaStream_t st) {
+    double* partial = scr.take<double>(kRedBlocks);
+    LAUNCH(sumsq_partial_kernel, kRedBlocks, 256, 0, st, X, rows, cols, ld, partial, d_err, err_bit);
+    LAUNCH(sum_partials_kernel, 1, 32, 0, st, partial, kRedBlocks, d_out);
+}
+
+void transpose(const double* in, int rows, int cols, int ldi, double* out, int ldo, cudaStream_t st) {
+    if (rows <= 0 || cols <= 0) return;
+    LAUNCH(transpose_kernel, dim3(ceil_div(cols, 32), ceil_div(rows, 32)), dim3(32, 8), 0, st, in, rows, cols, ldi, out,
+           ldo);
+}
+
+void copy2d(const double* in, int rows, int cols, int ldi, double* out, int ldo, cudaStream_t st) {
+    if (rows <= 0 || cols <= 0) return;
+    LAUNCH(copy2d_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)rows * cols, 256))), 256, 0, st, in, rows,
+           cols, ldi, out, ldo);
+}
+
+void fill2d(double* out, int rows, int cols, int ldo, double v, cudaStream_t st) {
+    if (rows <= 0 || cols <= 0) return;
+    LAUNCH(fill2d_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)rows * cols, 256))), 256, 0, st, out, rows,
+           cols, ldo, v);
+}
+
+}  // namespace sfdg

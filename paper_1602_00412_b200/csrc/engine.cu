@@ -1,0 +1,397 @@
+// engine.cu -- the SparseShrink flush on one B200, composed from the device kernels.
+//
+// Reference call stack:
+//   boosted_sparse_shrink (shrink.cpp:104-131)
+//     sparse_shrink (shrink.cpp:63-73)
+//       simultaneous_iteration (randsvd.cpp:18-51): G (rng.cu) -> Y = A'G (spmm) ->
+//         orth -> q x [W = A'^T Y, Y = A'W, orth]          orth = CholeskyQR2 (dense.cu, chol.cu)
+//       P = Z^T A'  kept transposed as W = A'^T Z (d x ell) (spmm over the CSC)
+//       svd_top(P) (la_core.cpp:82-128): PP^T = W^T W (gram_tn) -> eigh -> V = W U / sigma
+//       shrink_from_factors (shrink.cpp:15-26) folded into the V GEMM as a column scale
+//     drop / Delta / verify_spectral (verify.cu)
+//   dense_shrink([B; B']) (shrink.cpp:30-61): Gram of the stacked transpose -> eigh -> GEMM.
+//
+// Layout: every ell-wide matrix is stored transposed and padded, d x lp (lp = ell
+// rounded up to 8) row-major, so each row of B^T, B'^T, W, G is one contiguous lp*8-byte
+// line that the gather SpMM and the DMMA tiles read whole. B^T and B'^T sit side by side
+// in one d x 2lp buffer so [B; B'] never has to be materialised for dense_shrink.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "engine.cuh"
+
+namespace sfdg {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+
+// out (R x R) = K restricted to the index map a -> a < n1 ? a : off + (a - n1)
+__global__ void compact_kernel(const double* __restrict__ K, int ldk, int n1, int off, int R, double* __restrict__ out,
+                               double* __restrict__ trace_out) {
+    __shared__ double sh[32];
+    double tr = 0.0;
+    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < R * R; e += blockDim.x * gridDim.x) {
+        const int a = e / R, b = e % R;
+        const int ia = a < n1 ? a : off + (a - n1), ib = b < n1 ? b : off + (b - n1);
+        const double v = K[(size_t)ia * ldk + ib];
+        out[e] = v;
+        if (a == b) tr += v;
+    }
+    if (trace_out && gridDim.x == 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, o);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = tr;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+            *trace_out = s;
+        }
+    }
+}
+
+// svd_top right vectors + shrink_from_factors as one GEMM operand:
+// S[map(j)][i] = U[j][i] * w_i, w_i = sqrt(max(s_i^2 - s_{ell-1}^2, 0)) / s_i, with
+// s_i = sqrt(max(lambda_i, 0)); w_i = 0 when s_i < 1e-10 s_0 or s_i == 0 (la_core.cpp:109-126,
+// shrink.cpp:15-26). S is kcols x lds, zero elsewhere.
+__global__ void shrink_weights_kernel(const double* __restrict__ evals, const double* __restrict__ U, int R, int ell,
+                                      int n1, int off, double* __restrict__ S, int kcols, int lds) {
+    __shared__ double w[512];
+    const double s0 = sqrt(fmax(evals[0], 0.0));
+    const double sl = sqrt(fmax(evals[ell - 1], 0.0));
+    const double floor_sq = sl * sl;
+    const double cutoff = 1e-10 * s0;
+    for (int i = threadIdx.x; i < ell; i += blockDim.x) {
+        const double si = sqrt(fmax(evals[i], 0.0));
+        double wi = 0.0;
+        if (!(si < cutoff || si == 0.0)) {
+            const double shrunk = sqrt(fmax(si * si - floor_sq, 0.0));
+            wi = shrunk == 0.0 ? 0.0 : shrunk / si;
+        }
+        w[i] = wi;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kcols * lds; e += blockDim.x) {
+        const int row = e / lds, i = e % lds;
+        int j = -1;
+        if (row < n1) j = row;
+        else if (row >= off && row < off + (R - n1)) j = n1 + (row - off);
+        double v = 0.0;
+        if (j >= 0 && i < ell) v = U[(size_t)j * R + i] * w[i];
+        S[e] = v;
+    }
+}
+
+// dense_shrink tall path (shrink.cpp:53-60): B^T[t][i] = shrunk_i * V[t][i].
+__global__ void tall_shrink_kernel(const double* __restrict__ evals, const double* __restrict__ V, int dd, int ell,
+                                   double* __restrict__ bt, int ldo, int lp) {
+    const double sl = sqrt(fmax(evals[ell - 1], 0.0));
+    const double floor_sq = sl * sl;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < dd * lp; e += gridDim.x * blockDim.x) {
+        const int t = e / lp, i = e % lp;
+        double v = 0.0;
+        if (i < ell) {
+            const double si = sqrt(fmax(evals[i], 0.0));
+            const double shrunk = sqrt(fmax(si * si - floor_sq, 0.0));
+            v = shrunk * V[(size_t)t * dd + i];
+        }
+        bt[(size_t)t * ldo + i] = v;
+    }
+}
+
+// densify (sparse.cpp:71-78) straight into transposed columns: Tt[col][off + row] = val
+__global__ void densify_t_kernel(const int* __restrict__ row_ptr, const uint32_t* __restrict__ col,
+                                 const double* __restrict__ val, int m, double* __restrict__ Tt, int ld, int off) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = warp; r < m; r += nw)
+        for (int k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32) Tt[(size_t)col[k] * ld + off + r] = val[k];
+}
+
+}  // namespace
+
+size_t power_iteration_count(size_t m, const PowerCfg& cfg) {
+    if (cfg.q_override >= 0) return (size_t)cfg.q_override;
+    if (cfg.epsilon <= 0.0 || cfg.epsilon >= 1.0)
+        throw invalid_argument("power_iteration_count: epsilon must be in (0,1)");
+    const double q = cfg.q_constant * std::log(static_cast<double>(std::max<size_t>(m, 1)) / cfg.epsilon) / cfg.epsilon;
+    return std::max<size_t>(1, static_cast<size_t>(std::ceil(q)));
+}
+
+Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, int m_cap_)
+    : device(device_), d(d_), ell(ell_) {
+    if (ell < 1 || ell > kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 256] for this build");
+    lp = (int)round_up((size_t)ell, 8);
+    set_device();
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // the ring holds >= 3 attempts' worth of draws (G: d*ell, x: d)
+    const uint64_t per_attempt = 2 * ((uint64_t)d * ell + d) + 8;
+    rng.init(seed, std::max<uint64_t>(3 * per_attempt, 1 << 20), device);
+    a.reserve(std::max(1, m_cap_), std::max<int64_t>((int64_t)nnz_cap, 1));
+    ensure_rows(std::max(1, m_cap_));
+    const size_t wbytes = (size_t)d * lp * sizeof(double);
+    CK(cudaMalloc(&W, wbytes));
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaMalloc(&Mt[i], 2 * wbytes));
+        CK(cudaMemsetAsync(Mt[i], 0, 2 * wbytes, st));
+    }
+    const int kmax = std::max(2 * lp, 8);
+    CK(cudaMalloc(&gram, (size_t)kmax * kmax * sizeof(double)));
+    CK(cudaMalloc(&rinv, (size_t)lp * lp * sizeof(double)));
+    CK(cudaMalloc(&kc, (size_t)kmax * kmax * sizeof(double)));
+    CK(cudaMalloc(&evals, (size_t)kmax * sizeof(double)));
+    CK(cudaMalloc(&evecs, (size_t)kmax * kmax * sizeof(double)));
+    CK(cudaMalloc(&S, (size_t)kmax * lp * sizeof(double)));
+    CK(cudaMalloc(&x0, (size_t)d * sizeof(double)));
+    CK(cudaMalloc(&ybuf, 2 * (size_t)d * sizeof(double)));
+    verify_blocks = verify_grid_blocks(device);
+    CK(cudaMalloc(&tpart, (size_t)verify_blocks * lp * sizeof(double)));
+    CK(cudaMalloc(&tvec, (size_t)lp * sizeof(double)));
+    CK(cudaMalloc(&vpart, (size_t)verify_blocks * sizeof(double)));
+    CK(cudaMalloc(&vout, 4 * sizeof(double)));
+    CK(cudaMalloc(&bar, 2 * sizeof(unsigned)));
+    CK(cudaMalloc(&d_err, 4 * sizeof(int)));
+    CK(cudaMemsetAsync(d_err, 0, 4 * sizeof(int), st));
+    CK(cudaMalloc(&d_scal, 16 * sizeof(double)));
+    CK(cudaHostAlloc(&h_scal, 16 * sizeof(double), cudaHostAllocDefault));
+    CK(cudaHostAlloc(&h_err, 4 * sizeof(int), cudaHostAllocDefault));
+    CK(cudaStreamSynchronize(st));
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device);
+    if (st) cudaStreamSynchronize(st);
+    for (void* p : {(void*)Y, (void*)Yt, (void*)W, (void*)Mt[0], (void*)Mt[1], (void*)gram, (void*)rinv, (void*)kc,
+                    (void*)evals, (void*)evecs, (void*)S, (void*)x0, (void*)ybuf, (void*)u, (void*)tpart, (void*)tvec,
+                    (void*)vpart, (void*)vout, (void*)bar, (void*)d_err, (void*)d_scal})
+        if (p) cudaFree(p);
+    if (h_scal) cudaFreeHost(h_scal);
+    if (h_err) cudaFreeHost(h_err);
+    a.release();
+    plan_r.release();
+    plan_c.release();
+    scr.release();
+    rng.release();
+    if (st) cudaStreamDestroy(st);
+}
+
+void Engine::set_device() const { CK(cudaSetDevice(device)); }
+
+void Engine::ensure_rows(int m) {
+    if (m <= m_cap && Y) return;
+    m_cap = std::max(m, m_cap);
+    for (double** p : {&Y, &Yt}) {
+        if (*p) cudaFree(*p);
+        CK(cudaMalloc(p, (size_t)m_cap * lp * sizeof(double)));
+    }
+    if (u) cudaFree(u);
+    CK(cudaMalloc(&u, (size_t)m_cap * sizeof(double)));
+}
+
+void Engine::sync() { CK(cudaStreamSynchronize(st)); }
+
+double Engine::read_scalar(const double* dptr) {
+    CK(cudaMemcpyAsync(h_scal, dptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return h_scal[0];
+}
+
+void Engine::check_errors() {
+    CK(cudaMemcpyAsync(h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int e = h_err[0];
+    if (!e) return;
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+    CK(cudaStreamSynchronize(st));
+    if (e & ERR_NONFINITE_INPUT) throw invalid_argument("dense_shrink: non-finite input");
+    if (e & ERR_NONFINITE_ITER) throw numerical_error("simultaneous_iteration: non-finite intermediate");
+    if (e & ERR_NONFINITE_PROJ) throw numerical_error("sparse_shrink: non-finite projection");
+    if (e & ERR_NONFINITE_VERIFY) throw numerical_error("verify_spectral: non-finite operator output");
+    if (e & ERR_JACOBI_NOCONV) throw numerical_error("jacobi_eigh: no convergence after 100 sweeps");
+    if (e & ERR_RNG_U1_ZERO)
+        throw numerical_error("rng: Box-Muller u1 == 0 redraw (probability 2^-53) is not reproduced on device");
+    throw numerical_error("sfdg: device error flag " + std::to_string(e));
+}
+
+void Engine::load_csr(const int64_t* row_ptr, const uint32_t* cols, const double* vals, int m, int64_t nnz) {
+    ensure_rows(m);
+    a.set_shape(m, d, nnz);
+    std::vector<int> rp(m + 1);
+    for (int i = 0; i <= m; ++i) rp[i] = (int)(row_ptr[i] - row_ptr[0]);
+    CK(cudaMemcpyAsync(a.row_ptr, rp.data(), (m + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (nnz > 0) {
+        CK(cudaMemcpyAsync(a.col, cols + row_ptr[0], nnz * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(a.val, vals + row_ptr[0], nnz * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaStreamSynchronize(st));  // host vectors go out of scope
+}
+
+void Engine::prepare() {
+    build_transpose(a, scr, st);
+    plan_r.build(a.row_ptr, a.m, a.nnz, scr, st);
+    plan_c.build(a.col_ptr, a.d, a.nnz, scr, st);
+}
+
+void Engine::orthonormalize(double* Yp, int m, int err_bit) {
+    // Two CholeskyQR passes: Yp -> Yt -> Yp.
+    double* stats = d_scal + 8;
+    gram_tn(Yp, m, lp, lp, gram, lp, scr, st);
+    chol_rinv(gram, lp, lp, rinv, lp, stats, d_err, err_bit, scr, st);
+    gemm_nn(Yp, m, lp, lp, rinv, lp, lp, Yt, lp, st);
+    gram_tn(Yt, m, lp, lp, gram, lp, scr, st);
+    chol_rinv(gram, lp, lp, rinv, lp, stats, d_err, err_bit, scr, st);
+    gemm_nn(Yt, m, lp, lp, rinv, lp, lp, Yp, lp, st);
+}
+
+void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
+    const int m = a.m;
+    if (k < 1 || k > std::min(m, d)) throw invalid_argument("simultaneous_iteration: k out of range");
+    if (k != ell) throw invalid_argument("simultaneous_iteration: engine built for a different k");
+    const size_t q = power_iteration_count((size_t)m, cfg);
+    // G = gaussian_matrix(d, k) in W (la_core.cpp:167-172), pad columns zero
+    rng.normals(pos, (uint64_t)d * k, (uint64_t)k, (uint64_t)lp, W, d_err, st);
+    spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
+    orthonormalize(Y, m, ERR_NONFINITE_ITER);
+    for (size_t s = 0; s < q; ++s) {
+        spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st);
+        spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
+        orthonormalize(Y, m, ERR_NONFINITE_ITER);
+    }
+}
+
+void Engine::sparse_shrink(const PowerCfg& cfg, double* bpt, int ldb) {
+    if (ell < 1 || ell > a.m) throw invalid_argument("sparse_shrink: ell out of range");
+    if (ell > d) throw invalid_argument("sparse_shrink: ell exceeds column count");
+    simultaneous_iteration(ell, cfg);
+    // W = A'^T Z = P^T (d x lp): project_rows (sparse.cpp:57-69) without the transpose
+    spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st);
+    double* fsq = d_scal + 0;
+    sumsq(W, d, lp, lp, fsq, d_err, ERR_NONFINITE_PROJ, scr, st);  // all_finite(P) (shrink.cpp:70)
+    // svd_top(P, ell): PP^T = W^T W, eigen, right vectors and the shrink in one GEMM
+    gram_tn(W, d, lp, lp, gram, lp, scr, st);
+    LAUNCH(compact_kernel, 1, 1024, 0, st, gram, lp, ell, ell, ell, kc, (double*)nullptr);
+    eigh(kc, ell, ell, 0.0, fsq, evals, evecs, ell, d_err, scr, st);
+    LAUNCH(shrink_weights_kernel, 1, 1024, 0, st, evals, evecs, ell, ell, ell, ell, S, lp, lp);
+    gemm_nn(W, d, lp, lp, S, lp, lp, bpt, ldb, st);
+}
+
+bool Engine::verify(Verifier& v, double delta_hat, const double* bpt, int ldb) {
+    // shrink.cpp:76-82, host arithmetic identical to the reference
+    v.i += 1;
+    const double di = static_cast<double>(v.i);
+    const double delta_i = v.delta / (2.0 * di * di);
+    v.delta_spent += delta_i;
+    const size_t steps = static_cast<size_t>(std::ceil(v.c_verify * std::log2(static_cast<double>(d) / delta_i)));
+    rng.normals(pos, (uint64_t)d, (uint64_t)d, (uint64_t)d, x0, d_err, st);  // unit_sphere_vector draws
+    VerifyArgs args{};
+    args.row_ptr = a.row_ptr;
+    args.col = a.col;
+    args.val = a.val;
+    args.col_ptr = a.col_ptr;
+    args.row_idx = a.row_idx;
+    args.cval = a.cval;
+    args.m = a.m;
+    args.d = d;
+    args.bt = bpt;
+    args.ldb = ldb;
+    args.ell = ell;
+    args.scale = 2.0 / delta_hat;
+    args.steps = (int)steps;
+    args.x0 = x0;
+    args.u = u;
+    args.ybuf = ybuf;
+    args.tpart = tpart;
+    args.t = tvec;
+    args.part = vpart;
+    args.bar = bar;
+    args.err = d_err;
+    args.out = vout;
+    verify_launch(args, verify_blocks, st);
+    CK(cudaMemcpyAsync(h_scal, vout, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    check_errors();
+    return h_scal[0] != 0.0;
+}
+
+size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* delta_hat_out) {
+    if (ell < 1 || ell > a.m) throw invalid_argument("boosted_sparse_shrink: ell out of range");
+    double* bpt = Mt[cur] + lp;  // right half of [B^T | B'^T]
+    const int ldb = 2 * lp;
+    for (size_t attempt = 1; attempt <= kRetryCap; ++attempt) {
+        sparse_shrink(cfg, bpt, ldb);
+        double* bfsq = d_scal + 1;
+        sumsq(bpt, d, ell, ldb, bfsq, nullptr, 0, scr, st);
+        // prefetch the next attempt's draws while we wait (side stream)
+        rng.prefetch(pos.words + 2 * ((uint64_t)d * ell + 2 * d) + 8);
+        const double b_fsq = read_scalar(bfsq);
+        check_errors();
+        const double drop = a_fsq - b_fsq;  // shrink.cpp:112-113
+        const double delta_hat = drop / (kAlpha * static_cast<double>(ell));
+        if (drop <= 1e-12 * a_fsq) {  // exact recovery: Delta = 0, no verification (shrink.cpp:115-118)
+            *delta_hat_out = 0.0;
+            return attempt;
+        }
+        if (verify(v, delta_hat, bpt, ldb)) {
+            *delta_hat_out = delta_hat;
+            return attempt;
+        }
+    }
+    throw numerical_error("boosted_sparse_shrink: retry cap exceeded");
+}
+
+void Engine::dense_shrink_stack(const double* Xt, int ldx, int n1, int off, int n2, double* bt_out, int ldo) {
+    const int R = n1 + n2;
+    const int kcols = off + n2;
+    if (ell < 1 || ell > R) throw invalid_argument("dense_shrink: ell out of range");
+    double* fsq = d_scal + 2;
+    if (R <= d) {
+        // short-fat: Gram of the stacked rows = Xt^T Xt restricted to the stack's columns
+        if (R > 1024) throw invalid_argument("dense_shrink: more than 1024 stacked rows unsupported");
+        double* K = scr.take<double>((int64_t)kcols * kcols);
+        double* Kc = scr.take<double>((int64_t)R * R);
+        double* ev = scr.take<double>(R);
+        double* U = scr.take<double>((int64_t)R * R);
+        double* Sx = scr.take<double>((int64_t)kcols * lp);
+        gram_tn(Xt, d, kcols, ldx, K, kcols, scr, st);
+        LAUNCH(compact_kernel, 1, 1024, 0, st, K, kcols, n1, off, R, Kc, fsq);
+        eigh(Kc, R, R, 0.0, fsq, ev, U, R, d_err, scr, st);
+        LAUNCH(shrink_weights_kernel, 1, 1024, 0, st, ev, U, R, ell, n1, off, Sx, kcols, lp);
+        gemm_nn(Xt, d, kcols, ldx, Sx, lp, lp, bt_out, ldo, st);
+    } else {
+        // tall: eigendecompose the d x d Gram A^T A (shrink.cpp:39-60)
+        if (ell > d) throw invalid_argument("dense_shrink: ell exceeds column count");
+        double* X = scr.take<double>((int64_t)R * d);
+        double* Xc = scr.take<double>((int64_t)d * R);
+        // gather the stack's columns contiguously, then transpose to rows
+        copy2d(Xt, d, n1, ldx, Xc, R, st);
+        if (n2 > 0) copy2d(Xt + off, d, n2, ldx, Xc + n1, R, st);
+        transpose(Xc, d, R, R, X, d, st);
+        double* K = scr.take<double>((int64_t)d * d);
+        double* Kc = scr.take<double>((int64_t)d * d);
+        double* ev = scr.take<double>(d);
+        double* V = scr.take<double>((int64_t)d * d);
+        gram_tn(X, R, d, d, K, d, scr, st);
+        LAUNCH(compact_kernel, 1, 1024, 0, st, K, d, d, d, d, Kc, fsq);
+        eigh(Kc, d, d, 0.0, fsq, ev, V, d, d_err, scr, st);
+        LAUNCH(tall_shrink_kernel, std::max(1u, std::min(4u * kSMs, ceil_div((size_t)d * lp, 256))), 256, 0, st, ev, V,
+               d, ell, bt_out, ldo, lp);
+    }
+}
+
+void Engine::densify_into_stack(int off) {
+    fill2d(Mt[cur] + lp, d, lp, 2 * lp, 0.0, st);
+    if (a.m > 0)
+        LAUNCH(densify_t_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)a.m * 32, 256))), 256, 0, st,
+               a.row_ptr, a.col, a.val, a.m, Mt[cur], 2 * lp, off);
+}
+
+void Engine::sketch_to_host(double* out) {
+    double* tmp = scr.take<double>((int64_t)ell * d);
+    transpose(Mt[cur], d, ell, 2 * lp, tmp, d, st);
+    CK(cudaMemcpyAsync(out, tmp, (size_t)ell * d * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace sfdg

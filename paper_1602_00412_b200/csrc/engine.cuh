@@ -1,0 +1,95 @@
+// engine.cuh -- device implementation of the SFD flush (see engine.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+#include "dense.cuh"
+#include "rng.cuh"
+#include "sparse.cuh"
+#include "verify.cuh"
+
+namespace sfdg {
+
+constexpr double kAlpha = 6.0 / 41.0;  // core/include/sfd/common.hpp:10
+constexpr size_t kRetryCap = 64;       // core/src/shrink.cpp:12
+constexpr int kMaxEll = 256;           // 2*ell <= 512 fits every kernel's tile plan
+
+struct PowerCfg {  // randsvd.hpp:10-14
+    double epsilon = 0.25;
+    double q_constant = 1.0;
+    int64_t q_override = -1;
+};
+
+struct Verifier {  // shrink.hpp:11-16
+    size_t i = 0;
+    double delta = 0.1;
+    double c_verify = 2.0;
+    double delta_spent = 0.0;
+};
+
+size_t power_iteration_count(size_t m, const PowerCfg& cfg);  // randsvd.cpp:10-16
+
+// Per-device working set for one sketch stream (or one standalone call).
+class Engine {
+  public:
+    Engine(int device, int d, int ell, uint64_t seed, uint64_t nnz_cap, int m_cap);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    int device, d, ell, lp;
+    cudaStream_t st = nullptr;
+    Scratch scr;
+    RngStream rng;
+    RngPos pos;
+    DevCsr a;
+    SegPlan plan_r, plan_c;
+    int m_cap = 0;
+
+    double *Y = nullptr, *Yt = nullptr, *W = nullptr;  // m_cap x lp, m_cap x lp, d x lp
+    double* Mt[2] = {nullptr, nullptr};                 // d x 2lp : [B^T | B'^T]
+    int cur = 0;
+    double *gram = nullptr, *rinv = nullptr, *kc = nullptr, *evals = nullptr, *evecs = nullptr, *S = nullptr;
+    double *x0 = nullptr, *ybuf = nullptr, *u = nullptr, *tpart = nullptr, *tvec = nullptr, *vpart = nullptr;
+    double* vout = nullptr;
+    unsigned* bar = nullptr;
+    int* d_err = nullptr;
+    double* d_scal = nullptr;  // device scalars
+    double* h_scal = nullptr;  // pinned mirror
+    int* h_err = nullptr;
+    int verify_blocks = 0;
+
+    void set_device() const;
+    void ensure_rows(int m);
+    // Host CSR -> device A' (standalone entry points).
+    void load_csr(const int64_t* row_ptr, const uint32_t* cols, const double* vals, int m, int64_t nnz);
+    // CSC + long-row plans for the current A'.
+    void prepare();
+    // la_core.cpp:130-165 contract on Y (m x lp, first k columns meaningful): CholeskyQR2.
+    void orthonormalize(double* Yp, int m, int err_bit);
+    // randsvd.cpp:18-51: Z (m x lp) left in Y.
+    void simultaneous_iteration(int k, const PowerCfg& cfg);
+    // shrink.cpp:63-73 (+ la_core.cpp:82-128): B'^T (d x lp) into bpt (ld).
+    void sparse_shrink(const PowerCfg& cfg, double* bpt, int ldb);
+    // shrink.cpp:75-102 on diff_op (shrink.cpp:121-126); host syncs for the verdict.
+    bool verify(Verifier& v, double delta_hat, const double* bpt, int ldb);
+    // shrink.cpp:104-131; B'^T lands in Mt[cur] right half. Returns attempts.
+    size_t boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* delta_hat_out);
+    // dense_shrink (shrink.cpp:30-61) of the row stack whose transpose is Xt (d x kcols, ldx),
+    // rows = columns [0, n1) and [off, off + n2) of Xt; writes B^T (d x lp, ldo).
+    void dense_shrink_stack(const double* Xt, int ldx, int n1, int off, int n2, double* bt_out, int ldo);
+    // Zero the B'^T half of Mt[cur] and scatter the buffer rows of A' into columns
+    // [off, off + m) of Mt[cur] (densify, sparse.cpp:71-78, already transposed).
+    void densify_into_stack(int off);
+    // Copies the current B (ell x d row-major) to host.
+    void sketch_to_host(double* out);
+    double read_scalar(const double* dptr);
+    void check_errors();  // syncs; throws the reference's error class for any device flag
+    void sync();
+};
+
+}  // namespace sfdg

@@ -1,0 +1,55 @@
+// rng.cuh -- device reproduction of sfd::Rng's normal stream (see rng.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sfdg {
+
+// Position in the draw stream of sfd::Rng (rng.hpp:12-31): raw engine words consumed
+// and whether a Box-Muller spare is cached (its value lives on the device).
+struct RngPos {
+    uint64_t words = 0;
+    bool has_spare = false;
+};
+
+class RngStream {
+  public:
+    RngStream() = default;
+    RngStream(const RngStream&) = delete;
+    RngStream& operator=(const RngStream&) = delete;
+    ~RngStream() { release(); }
+
+    void init(uint64_t seed, uint64_t min_ring_words, int device);
+    void release();
+
+    // Draw n normals at `pos` into d_out (rows of `cols`, leading dimension ld).
+    void normals(RngPos& pos, uint64_t n, uint64_t cols, uint64_t ld, double* d_out, int* d_err,
+                 cudaStream_t stream);
+    // Generate ahead (side stream) up to raw word w_end.
+    void prefetch(uint64_t w_end);
+    double spare_value(cudaStream_t stream);
+    void set_spare(double v, cudaStream_t stream);
+    uint64_t ring_words() const { return ring_cap; }
+
+  private:
+    void reseed();
+    void generate_to(uint64_t words_end);
+    void ensure(uint64_t w_begin, uint64_t w_end, cudaStream_t consumer);
+    void mark_consumed(cudaStream_t consumer);
+
+    int device = 0;
+    uint64_t seed = 0;
+    uint64_t gen_words = 0;  // tempered output words produced so far
+    uint64_t ring_cap = 0;   // power of two
+    uint64_t* d_ring = nullptr;
+    uint64_t* d_window = nullptr;
+    double* d_spare = nullptr;  // two slots, alternating
+    unsigned spare_slot = 0;
+    cudaStream_t s_gen = nullptr;
+    cudaEvent_t ev_gen = nullptr;
+    cudaEvent_t ev_consumed = nullptr;
+};
+
+}  // namespace sfdg

@@ -1,0 +1,560 @@
+// sparse.cu -- device CSR buffer A' and its products (reference: core/src/sparse.cpp).
+//
+//  * csc_build: CSR -> CSC by a stable LSD radix sort on the column index (8-bit
+//    digits, warp-level match_any ranking). Stability keeps every column's entries in
+//    row order, so W = A'^T Y gathers in exactly the order rmatvec / project_rows
+//    scatter (sparse.cpp:45-69) and the result is deterministic (no FP atomics).
+//  * spmm: out[r, :] = sum_k val[k] * in[idx[k], :] over an ell-wide row-major panel.
+//    One warp per output row, lanes across the panel columns (double2 loads). Rows
+//    longer than kPiece*2 are split into kPiece-long pieces whose partial rows are
+//    summed in piece order by a fix-up kernel (deterministic load balancing for
+//    Zipf-skewed columns). Used for Y = A' X (matvec, sparse.cpp:32-43) and
+//    W = A'^T Y (rmatvec/project_rows, sparse.cpp:45-69).
+#include <algorithm>
+
+#include "common.cuh"
+#include "sparse.cuh"
+
+namespace sfdg {
+
+namespace {
+
+constexpr int kScanBlock = 1024;
+constexpr int kScanItems = 4;  // 4096 elements per block
+
+// ---------------------------------------------------------------- exclusive scan
+__global__ void scan_block_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
+                                  int64_t* __restrict__ block_sums) {
+    __shared__ int64_t warp_tot[32];
+    const int64_t base = (int64_t)blockIdx.x * kScanBlock * kScanItems;
+    int64_t v[kScanItems];
+    int64_t tsum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const int64_t idx = base + (int64_t)threadIdx.x * kScanItems + i;
+        v[i] = idx < n ? in[idx] : 0;
+        tsum += v[i];
+    }
+    // block exclusive scan of tsum
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t x = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int64_t t = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        warp_tot[lane] = t;  // inclusive
+    }
+    __syncthreads();
+    int64_t run = x - tsum + (w > 0 ? warp_tot[w - 1] : 0);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const int64_t idx = base + (int64_t)threadIdx.x * kScanItems + i;
+        if (idx < n) out[idx] = run;
+        run += v[i];
+    }
+    if (threadIdx.x == kScanBlock - 1 && block_sums) block_sums[blockIdx.x] = run;
+}
+
+__global__ void scan_add_kernel(int64_t* __restrict__ out, int64_t n, const int64_t* __restrict__ block_offs) {
+    const int64_t base = (int64_t)blockIdx.x * kScanBlock * kScanItems;
+    const int64_t add = block_offs[blockIdx.x];
+    for (int i = threadIdx.x; i < kScanBlock * kScanItems; i += kScanBlock) {
+        const int64_t idx = base + i;
+        if (idx < n) out[idx] += add;
+    }
+}
+
+// ---------------------------------------------------------------- radix sort
+constexpr int kRadixThreads = 256;
+constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixItemsPerWarp = 256;  // 8 rounds of 32
+constexpr int kRadixTile = kRadixWarps * kRadixItemsPerWarp;
+
+__global__ void radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift, int ntiles,
+                                  int64_t* __restrict__ hist /* [256][ntiles] */) {
+    __shared__ int cnt[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+    for (int i = threadIdx.x; i < kRadixTile; i += blockDim.x) {
+        const int64_t k = base + i;
+        if (k < n) atomicAdd(&cnt[(keys[k] >> shift) & 0xff], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[(int64_t)i * ntiles + blockIdx.x] = cnt[i];
+}
+
+__global__ void radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                                     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int64_t n,
+                                     int shift, int ntiles, const int64_t* __restrict__ offs /* [256][ntiles] */) {
+    __shared__ int cnt[kRadixWarps][256];
+    for (int i = threadIdx.x; i < kRadixWarps * 256; i += blockDim.x) (&cnt[0][0])[i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t wbase = (int64_t)blockIdx.x * kRadixTile + (int64_t)w * kRadixItemsPerWarp;
+    constexpr int R = kRadixItemsPerWarp / 32;
+    uint32_t key[R], val[R];
+    int dig[R], lpos[R];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t k = wbase + r * 32 + lane;
+        const bool ok = k < n;
+        key[r] = ok ? keys_in[k] : 0u;
+        val[r] = ok ? vals_in[k] : 0u;
+        dig[r] = ok ? (int)((key[r] >> shift) & 0xff) : 256;
+        const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
+        const int rank = __popc(peers & lt);
+        const int leader = __ffs(peers) - 1;
+        int before = 0;
+        if (ok) before = cnt[w][dig[r]];
+        __syncwarp();
+        if (ok && lane == leader) cnt[w][dig[r]] = before + __popc(peers);
+        __syncwarp();
+        lpos[r] = before + rank;
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps (tile-local offsets)
+    for (int dg = threadIdx.x; dg < 256; dg += blockDim.x) {
+        int run = 0;
+#pragma unroll
+        for (int ww = 0; ww < kRadixWarps; ++ww) {
+            const int t = cnt[ww][dg];
+            cnt[ww][dg] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (dig[r] < 256) {
+            const int64_t pos = offs[(int64_t)dig[r] * ntiles + blockIdx.x] + cnt[w][dig[r]] + lpos[r];
+            keys_out[pos] = key[r];
+            vals_out[pos] = val[r];
+        }
+    }
+}
+
+__global__ void iota_kernel(uint32_t* __restrict__ v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (uint32_t)i;
+}
+
+// row id of every stored entry (warp per row)
+__global__ void expand_rows_kernel(const int* __restrict__ row_ptr, int m, uint32_t* __restrict__ row_of) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = warp; r < m; r += nw)
+        for (int k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32) row_of[k] = (uint32_t)r;
+}
+
+__global__ void csc_fill_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ row_of,
+                                const double* __restrict__ val, int64_t n, int* __restrict__ row_idx,
+                                double* __restrict__ cval) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = perm[i];
+        row_idx[i] = (int)row_of[k];
+        cval[i] = val[k];
+    }
+}
+
+// col_ptr[c] = first position with key >= c (sorted keys)
+__global__ void col_ptr_kernel(const uint32_t* __restrict__ skeys, int64_t n, int d, int* __restrict__ col_ptr) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= d; c += gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (skeys[mid] < (uint32_t)c) lo = mid + 1;
+            else hi = mid;
+        }
+        col_ptr[c] = (int)lo;
+    }
+}
+
+// ---------------------------------------------------------------- segment plans
+__global__ void plan_count_kernel(const int* __restrict__ ptr, int nrows, int piece, int64_t* __restrict__ is_long,
+                                  int64_t* __restrict__ npieces) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+        const int len = ptr[r + 1] - ptr[r];
+        const bool lg = len > 2 * piece;
+        is_long[r] = lg ? 1 : 0;
+        npieces[r] = lg ? (len + piece - 1) / piece : 0;
+    }
+}
+
+__global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int piece, const int64_t* __restrict__ is_long,
+                                 const int64_t* __restrict__ long_off, const int64_t* __restrict__ piece_off,
+                                 int* __restrict__ long_rows, int* __restrict__ long_first, int* __restrict__ piece_beg,
+                                 int* __restrict__ piece_end, int* __restrict__ counts /* [nlong, npieces] */) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+        const int len = ptr[r + 1] - ptr[r];
+        if (len > 2 * piece) {
+            const int li = (int)long_off[r];
+            const int pf = (int)piece_off[r];
+            long_rows[li] = r;
+            long_first[li] = pf;
+            const int np = (len + piece - 1) / piece;
+            for (int p = 0; p < np; ++p) {
+                piece_beg[pf + p] = ptr[r] + p * piece;
+                piece_end[pf + p] = min(ptr[r] + (p + 1) * piece, ptr[r + 1]);
+            }
+        }
+        if (r == nrows - 1) {
+            counts[0] = (int)(long_off[r] + is_long[r]);
+            counts[1] = (int)(piece_off[r] + (len > 2 * piece ? (len + piece - 1) / piece : 0));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- SpMM
+// J = number of 64-column chunks (lane owns columns 2*lane + 64*j, +1).
+template <int J>
+__device__ __forceinline__ void gather_range(int kb, int ke, const int* __restrict__ idx, const double* __restrict__ val,
+                                             const double* __restrict__ in, int ld, int ncols, int lane,
+                                             double2 (&acc)[J]) {
+    for (int k0 = kb; k0 < ke; k0 += 32) {
+        const int kk = k0 + lane;
+        const int my_idx = kk < ke ? idx[kk] : 0;
+        const double my_val = kk < ke ? val[kk] : 0.0;
+        const int cnt = min(32, ke - k0);
+        int e = 0;
+        for (; e + 4 <= cnt; e += 4) {
+            int ci[4];
+            double cv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                ci[u] = __shfl_sync(0xffffffffu, my_idx, e + u);
+                cv[u] = __shfl_sync(0xffffffffu, my_val, e + u);
+            }
+            double2 x[4][J];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    const int c = 2 * lane + 64 * j;
+                    x[u][j] = c < ncols ? __ldg(reinterpret_cast<const double2*>(in + (size_t)ci[u] * ld + c))
+                                        : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    acc[j].x = fma(cv[u], x[u][j].x, acc[j].x);
+                    acc[j].y = fma(cv[u], x[u][j].y, acc[j].y);
+                }
+        }
+        for (; e < cnt; ++e) {
+            const int ci = __shfl_sync(0xffffffffu, my_idx, e);
+            const double cv = __shfl_sync(0xffffffffu, my_val, e);
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int c = 2 * lane + 64 * j;
+                if (c < ncols) {
+                    const double2 x = __ldg(reinterpret_cast<const double2*>(in + (size_t)ci * ld + c));
+                    acc[j].x = fma(cv, x.x, acc[j].x);
+                    acc[j].y = fma(cv, x.y, acc[j].y);
+                }
+            }
+        }
+    }
+}
+
+template <int J>
+__global__ void spmm_rows_kernel(const int* __restrict__ ptr, const int* __restrict__ idx, const double* __restrict__ val,
+                                 int nrows, int piece, const double* __restrict__ in, int ld, int ncols,
+                                 double* __restrict__ out, int ldo) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = warp; r < nrows; r += nw) {
+        const int kb = ptr[r], ke = ptr[r + 1];
+        if (ke - kb > 2 * piece) continue;  // handled by the piece kernels
+        double2 acc[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[j] = make_double2(0.0, 0.0);
+        gather_range<J>(kb, ke, idx, val, in, ld, ncols, lane, acc);
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int c = 2 * lane + 64 * j;
+            if (c < ncols) *reinterpret_cast<double2*>(out + (size_t)r * ldo + c) = acc[j];
+        }
+    }
+}
+
+template <int J>
+__global__ void spmm_pieces_kernel(const int* __restrict__ piece_beg, const int* __restrict__ piece_end,
+                                   const int* __restrict__ counts, const int* __restrict__ idx,
+                                   const double* __restrict__ val, const double* __restrict__ in, int ld, int ncols,
+                                   double* __restrict__ partial /* [npieces][ld] */) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int np = counts[1];
+    for (int p = warp; p < np; p += nw) {
+        double2 acc[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) acc[j] = make_double2(0.0, 0.0);
+        gather_range<J>(piece_beg[p], piece_end[p], idx, val, in, ld, ncols, lane, acc);
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int c = 2 * lane + 64 * j;
+            if (c < ncols) *reinterpret_cast<double2*>(partial + (size_t)p * ld + c) = acc[j];
+        }
+    }
+}
+
+__global__ void spmm_fixup_kernel(const int* __restrict__ long_rows, const int* __restrict__ long_first,
+                                  const int* __restrict__ counts, const double* __restrict__ partial, int ld,
+                                  int ncols, double* __restrict__ out, int ldo) {
+    const int nl = counts[0];
+    const int npieces = counts[1];
+    for (int li = blockIdx.x; li < nl; li += gridDim.x) {
+        const int first = long_first[li];
+        const int last = li + 1 < nl ? long_first[li + 1] : npieces;
+        const int r = long_rows[li];
+        for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+            double s = 0.0;
+            for (int p = first; p < last; ++p) s += partial[(size_t)p * ld + c];
+            out[(size_t)r * ldo + c] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- validation
+// Device-resident input rows (sfdg_sketcher_append_csr_device): first bad row
+// (index out of range / not strictly increasing / non-finite), sparse.cpp:8-20.
+__global__ void validate_rows_kernel(const int64_t* __restrict__ row_ptr, int64_t nrows, const uint32_t* __restrict__ cols,
+                                     const double* __restrict__ vals, uint32_t d, unsigned long long* __restrict__ first_bad,
+                                     int* __restrict__ kind) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < nrows; r += nw) {
+        bool bad_idx = false, bad_val = false;
+        for (int64_t k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32) {
+            const uint32_t c = cols[k];
+            if (c >= d) bad_idx = true;
+            if (k > row_ptr[r] && cols[k - 1] >= c) bad_idx = true;
+            if (!isfinite(vals[k])) bad_val = true;
+        }
+        const bool bi = __any_sync(0xffffffffu, bad_idx), bv = __any_sync(0xffffffffu, bad_val);
+        if ((bi || bv) && lane == 0) {
+            atomicMin(first_bad, (unsigned long long)r);
+            atomicOr(kind, bi ? ERR_BAD_INDEX : ERR_BAD_VALUE);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- misc
+__global__ void rebase_rows_kernel(const int64_t* __restrict__ src, int64_t base, int m, int* __restrict__ dst) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += gridDim.x * blockDim.x)
+        dst[i] = (int)(src[i] - base);
+}
+
+}  // namespace
+
+// ============================================================== host side
+
+void exclusive_scan(const int64_t* d_in, int64_t* d_out, int64_t n, Scratch& scr, cudaStream_t st) {
+    if (n <= 0) return;
+    const int64_t per = (int64_t)kScanBlock * kScanItems;
+    const int64_t nb = (n + per - 1) / per;
+    if (nb == 1) {
+        LAUNCH(scan_block_kernel, 1, kScanBlock, 0, st, d_in, d_out, n, (int64_t*)nullptr);
+        return;
+    }
+    int64_t* sums = scr.take<int64_t>(nb);
+    int64_t* offs = scr.take<int64_t>(nb);
+    LAUNCH(scan_block_kernel, (unsigned)nb, kScanBlock, 0, st, d_in, d_out, n, sums);
+    exclusive_scan(sums, offs, nb, scr, st);
+    LAUNCH(scan_add_kernel, (unsigned)nb, kScanBlock, 0, st, d_out, n, offs);
+}
+
+void DevCsr::reserve(int m_cap, int64_t nnz_cap_) {
+    if (m_cap > rows_cap) {
+        if (row_ptr) cudaFree(row_ptr);
+        CK(cudaMalloc(&row_ptr, (size_t)(m_cap + 1) * sizeof(int)));
+        rows_cap = m_cap;
+    }
+    if (nnz_cap_ > nnz_cap) {
+        nnz_cap = std::max<int64_t>(nnz_cap_, nnz_cap * 3 / 2);
+        for (void* p : {(void*)col, (void*)val, (void*)row_idx, (void*)cval})
+            if (p) cudaFree(p);
+        CK(cudaMalloc(&col, nnz_cap * sizeof(uint32_t)));
+        CK(cudaMalloc(&val, nnz_cap * sizeof(double)));
+        CK(cudaMalloc(&row_idx, nnz_cap * sizeof(int)));
+        CK(cudaMalloc(&cval, nnz_cap * sizeof(double)));
+    }
+}
+
+void DevCsr::release() {
+    for (void* p : {(void*)row_ptr, (void*)col, (void*)val, (void*)col_ptr, (void*)row_idx, (void*)cval})
+        if (p) cudaFree(p);
+    row_ptr = nullptr;
+    col = nullptr;
+    val = nullptr;
+    col_ptr = nullptr;
+    row_idx = nullptr;
+    cval = nullptr;
+    rows_cap = 0;
+    nnz_cap = 0;
+    d_cap = 0;
+}
+
+void DevCsr::set_shape(int m_, int d_, int64_t nnz_) {
+    if (nnz_ >= (int64_t)INT32_MAX) throw invalid_argument("buffer: more than 2^31-1 stored entries per flush");
+    m = m_;
+    d = d_;
+    nnz = nnz_;
+    reserve(m_, std::max<int64_t>(nnz_, 1));
+    if (d_ + 1 > d_cap) {
+        if (col_ptr) cudaFree(col_ptr);
+        CK(cudaMalloc(&col_ptr, (size_t)(d_ + 1) * sizeof(int)));
+        d_cap = d_ + 1;
+    }
+}
+
+void rebase_row_ptr(const int64_t* d_src, int64_t base, int m, int* d_dst, cudaStream_t st) {
+    LAUNCH(rebase_rows_kernel, ceil_div(m + 1, 256), 256, 0, st, d_src, base, m, d_dst);
+}
+
+// CSR -> CSC (stable in row order) + long-row plans for both orientations.
+void build_transpose(DevCsr& a, Scratch& scr, cudaStream_t st) {
+    const int64_t n = a.nnz;
+    const int d = a.d;
+    if (n == 0) {
+        CK(cudaMemsetAsync(a.col_ptr, 0, (size_t)(d + 1) * sizeof(int), st));
+        return;
+    }
+    uint32_t* k0 = scr.take<uint32_t>(n);
+    uint32_t* k1 = scr.take<uint32_t>(n);
+    uint32_t* v0 = scr.take<uint32_t>(n);
+    uint32_t* v1 = scr.take<uint32_t>(n);
+    uint32_t* row_of = scr.take<uint32_t>(n);
+    CK(cudaMemcpyAsync(k0, a.col, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    const unsigned g = (unsigned)std::min<int64_t>(8 * kSMs, (n + 255) / 256);
+    LAUNCH(iota_kernel, g, 256, 0, st, v0, n);
+    int bits = 0;
+    while (bits < 32 && (1ull << bits) < (unsigned long long)d) ++bits;
+    const int ntiles = (int)((n + kRadixTile - 1) / kRadixTile);
+    int64_t* hist = scr.take<int64_t>((int64_t)256 * ntiles);
+    int64_t* offs = scr.take<int64_t>((int64_t)256 * ntiles);
+    for (int shift = 0; shift < bits; shift += 8) {
+        LAUNCH(radix_hist_kernel, ntiles, kRadixThreads, 0, st, k0, n, shift, ntiles, hist);
+        exclusive_scan(hist, offs, (int64_t)256 * ntiles, scr, st);
+        LAUNCH(radix_scatter_kernel, ntiles, kRadixThreads, 0, st, k0, v0, k1, v1, n, shift, ntiles, offs);
+        std::swap(k0, k1);
+        std::swap(v0, v1);
+    }
+    LAUNCH(expand_rows_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)a.m * 32, 256))), 256, 0, st,
+           a.row_ptr, a.m, row_of);
+    LAUNCH(csc_fill_kernel, g, 256, 0, st, v0, row_of, a.val, n, a.row_idx, a.cval);
+    LAUNCH(col_ptr_kernel, ceil_div(d + 1, 256), 256, 0, st, k0, n, d, a.col_ptr);
+}
+
+void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st) {
+    rows = nrows;
+    reserve_pieces(nnz);
+    if (nrows > cap_rows) {
+        for (void* p : {(void*)long_rows, (void*)long_first}) if (p) cudaFree(p);
+        CK(cudaMalloc(&long_rows, (size_t)nrows * sizeof(int)));
+        CK(cudaMalloc(&long_first, (size_t)nrows * sizeof(int)));
+        cap_rows = nrows;
+    }
+    if (!counts) CK(cudaMalloc(&counts, 2 * sizeof(int)));
+    CK(cudaMemsetAsync(counts, 0, 2 * sizeof(int), st));
+    if (nrows == 0) return;
+    int64_t* is_long = scr.take<int64_t>(nrows);
+    int64_t* np = scr.take<int64_t>(nrows);
+    int64_t* long_off = scr.take<int64_t>(nrows);
+    int64_t* piece_off = scr.take<int64_t>(nrows);
+    const unsigned g = std::max(1u, std::min(8u * kSMs, ceil_div(nrows, 256)));
+    LAUNCH(plan_count_kernel, g, 256, 0, st, d_ptr, nrows, kPiece, is_long, np);
+    exclusive_scan(is_long, long_off, nrows, scr, st);
+    exclusive_scan(np, piece_off, nrows, scr, st);
+    // pieces <= nnz / kPiece + nrows; size the piece arrays for the worst case of this call
+    LAUNCH(plan_fill_kernel, g, 256, 0, st, d_ptr, nrows, kPiece, is_long, long_off, piece_off, long_rows, long_first,
+           piece_beg, piece_end, counts);
+}
+
+void SegPlan::reserve_pieces(int64_t nnz) {
+    const int64_t need = 2 * (nnz / kPiece) + 2;
+    if (need > cap_pieces) {
+        for (void* p : {(void*)piece_beg, (void*)piece_end}) if (p) cudaFree(p);
+        cap_pieces = need;
+        CK(cudaMalloc(&piece_beg, cap_pieces * sizeof(int)));
+        CK(cudaMalloc(&piece_end, cap_pieces * sizeof(int)));
+    }
+}
+
+void SegPlan::release() {
+    for (void* p : {(void*)long_rows, (void*)long_first, (void*)piece_beg, (void*)piece_end, (void*)counts})
+        if (p) cudaFree(p);
+    long_rows = long_first = piece_beg = piece_end = counts = nullptr;
+    cap_rows = 0;
+    cap_pieces = 0;
+}
+
+void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, const SegPlan& plan, int64_t nnz,
+          const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st) {
+    if (nrows == 0) return;
+    if (ncols % 2 != 0 || ld % 2 != 0 || ldo % 2 != 0) throw invalid_argument("spmm: panel widths must be even");
+    const int J = (ncols + 63) / 64;
+    const unsigned grid = std::max(1u, std::min(16u * kSMs, ceil_div((size_t)nrows * 32, 256)));
+    double* partial = scr.take<double>((2 * (nnz / kPiece) + 2) * (int64_t)ld);
+    const unsigned pgrid = 4 * kSMs;
+    switch (J) {
+#define SPMM_CASE(JJ)                                                                                              \
+    case JJ:                                                                                                       \
+        LAUNCH(spmm_rows_kernel<JJ>, grid, 256, 0, st, d_ptr, d_idx, d_val, nrows, kPiece, d_in, ld, ncols, d_out, \
+               ldo);                                                                                               \
+        LAUNCH(spmm_pieces_kernel<JJ>, pgrid, 256, 0, st, plan.piece_beg, plan.piece_end, plan.counts, d_idx,     \
+               d_val, d_in, ld, ncols, partial);                                                                   \
+        break;
+        SPMM_CASE(1)
+        SPMM_CASE(2)
+        SPMM_CASE(3)
+        SPMM_CASE(4)
+        SPMM_CASE(5)
+        SPMM_CASE(6)
+        SPMM_CASE(7)
+        SPMM_CASE(8)
+#undef SPMM_CASE
+        default:
+            throw invalid_argument("spmm: panel wider than 512 columns");
+    }
+    LAUNCH(spmm_fixup_kernel, 2 * kSMs, 128, 0, st, plan.long_rows, plan.long_first, plan.counts, partial, ld, ncols,
+           d_out, ldo);
+}
+
+int64_t validate_rows_device(const int64_t* d_row_ptr, int64_t nrows, const uint32_t* d_cols, const double* d_vals,
+                             uint32_t d, int* kind_out, Scratch& scr, cudaStream_t st) {
+    unsigned long long* first = scr.take<unsigned long long>(1);
+    int* kind = scr.take<int>(2);
+    const unsigned long long init = ~0ull;
+    CK(cudaMemcpyAsync(first, &init, sizeof init, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(kind, 0, sizeof(int), st));
+    if (nrows > 0)
+        LAUNCH(validate_rows_kernel, std::max(1u, std::min(16u * kSMs, ceil_div((size_t)nrows * 32, 256))), 256, 0, st,
+               d_row_ptr, nrows, d_cols, d_vals, d, first, kind);
+    unsigned long long h_first = 0;
+    int h_kind = 0;
+    CK(cudaMemcpyAsync(&h_first, first, sizeof h_first, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h_kind, kind, sizeof h_kind, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *kind_out = h_kind;
+    return h_first == ~0ull ? -1 : (int64_t)h_first;
+}
+
+}  // namespace sfdg

@@ -1,0 +1,101 @@
+// sparse.cuh -- device CSR/CSC buffer, scratch arena, sparse kernels (see sparse.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sfdg {
+
+// Stream-ordered bump arena over retained device chunks. reset() rewinds; callers
+// only reuse memory on the same stream, so earlier kernels are ordered before reuse.
+class Scratch {
+  public:
+    ~Scratch() { release(); }
+    template <class T>
+    T* take(int64_t n) {
+        const size_t bytes = round_up(std::max<int64_t>(n, 1) * sizeof(T), 256);
+        while (cur < chunks.size() && used + bytes > chunks[cur].size) {
+            ++cur;
+            used = 0;
+        }
+        if (cur == chunks.size()) {
+            size_t sz = std::max<size_t>(bytes, chunks.empty() ? (size_t)64 << 20 : chunks.back().size * 2);
+            Chunk c{nullptr, sz};
+            CK(cudaMalloc(&c.ptr, sz));
+            chunks.push_back(c);
+            used = 0;
+        }
+        T* p = reinterpret_cast<T*>(static_cast<char*>(chunks[cur].ptr) + used);
+        used += bytes;
+        return p;
+    }
+    void reset() {
+        cur = 0;
+        used = 0;
+    }
+    void release() {
+        for (auto& c : chunks) cudaFree(c.ptr);
+        chunks.clear();
+        reset();
+    }
+
+  private:
+    struct Chunk {
+        void* ptr;
+        size_t size;
+    };
+    std::vector<Chunk> chunks;
+    size_t cur = 0, used = 0;
+};
+
+// A' on the device (sparse.hpp:19-57): CSR with int32 offsets (nnz per flush < 2^31)
+// plus its stable transpose (CSC) built once per flush.
+struct DevCsr {
+    int m = 0, d = 0;
+    int64_t nnz = 0;
+    int* row_ptr = nullptr;  // m+1
+    uint32_t* col = nullptr; // nnz
+    double* val = nullptr;   // nnz
+    int* col_ptr = nullptr;  // d+1
+    int* row_idx = nullptr;  // nnz (CSC)
+    double* cval = nullptr;  // nnz (CSC)
+    int rows_cap = 0, d_cap = 0;
+    int64_t nnz_cap = 0;
+    void reserve(int m_cap, int64_t nnz_cap);
+    void set_shape(int m, int d, int64_t nnz);
+    void release();
+    ~DevCsr() { release(); }
+};
+
+// Long-row split plan for the gather SpMM (rows longer than 2*kPiece).
+constexpr int kPiece = 256;
+struct SegPlan {
+    int rows = 0;
+    int* long_rows = nullptr;
+    int* long_first = nullptr;
+    int* piece_beg = nullptr;
+    int* piece_end = nullptr;
+    int* counts = nullptr;  // device [nlong, npieces]
+    int cap_rows = 0;
+    int64_t cap_pieces = 0;
+    void build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st);
+    void reserve_pieces(int64_t nnz);
+    void release();
+    ~SegPlan() { release(); }
+};
+
+void exclusive_scan(const int64_t* d_in, int64_t* d_out, int64_t n, Scratch& scr, cudaStream_t st);
+void rebase_row_ptr(const int64_t* d_src, int64_t base, int m, int* d_dst, cudaStream_t st);
+void build_transpose(DevCsr& a, Scratch& scr, cudaStream_t st);
+// out (nrows x ncols, ldo) = sparse(ptr, idx, val) * in (ld), ncols even.
+void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, const SegPlan& plan, int64_t nnz,
+          const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st);
+// First invalid row (or -1) of a device-resident CSR batch; kind_out gets ERR_BAD_* bits.
+int64_t validate_rows_device(const int64_t* d_row_ptr, int64_t nrows, const uint32_t* d_cols, const double* d_vals,
+                             uint32_t d, int* kind_out, Scratch& scr, cudaStream_t st);
+
+}  // namespace sfdg

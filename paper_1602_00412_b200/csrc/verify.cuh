@@ -1,0 +1,40 @@
+// verify.cuh -- persistent verifier kernel arguments (see verify.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sfdg {
+
+struct VerifyArgs {
+    // A' as CSR (u = A' x) and CSC (A'^T u)
+    const int* row_ptr;
+    const uint32_t* col;
+    const double* val;
+    const int* col_ptr;
+    const int* row_idx;
+    const double* cval;
+    int64_t m, d;
+    // B'^T: d x ell, row stride ldb (the right half of the [B | B']^T stack)
+    const double* bt;
+    int64_t ldb;
+    int ell;
+    double scale;      // 2 / Delta
+    int steps;         // ceil(c_v log2(d / delta_i))   (shrink.cpp:81-82)
+    const double* x0;  // d raw normals (unit_sphere_vector draws)
+    // workspace
+    double* u;      // m
+    double* ybuf;   // 2 d
+    double* tpart;  // nblocks * ell
+    double* t;      // ell
+    double* part;   // nblocks
+    unsigned* bar;  // 2
+    int* err;
+    double* out;  // [accepted, log_mag, steps_run]
+};
+
+int verify_grid_blocks(int device);
+void verify_launch(const VerifyArgs& args, int nblocks, cudaStream_t st);
+
+}  // namespace sfdg

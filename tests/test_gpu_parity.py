@@ -1,0 +1,413 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the reference
+golden vectors, on the same seeded inputs and the same Gaussian draw stream.
+
+Tolerances (north_star): B^T B within 1e-8 relative Frobenius in FP64; counters
+(flush_count, attempt_total, verifier i, delta_spent) exact. Kernel-level checks use the
+reference's own gates (1e-12 for the sparse products, tests/test_sparse.cpp:36-72).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_1602_00412_b200 as P
+from oracle.oracle import KALPHA, PowerConfig as OPower, VerifierState as OVer
+from paper_1602_00412_b200 import synthetic as S
+
+pytestmark = pytest.mark.gpu
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
+BTB_TOL = 1e-8
+
+
+def btb_rel(b1, b2):
+    g1, g2 = b1.T @ b1, b2.T @ b2
+    den = max(np.linalg.norm(g2), 1e-300)
+    return np.linalg.norm(g1 - g2) / den
+
+
+def dense_of(rp, cs, vs, d):
+    a = np.zeros((len(rp) - 1, d))
+    for i in range(len(rp) - 1):
+        a[i, cs[rp[i]:rp[i + 1]]] = vs[rp[i]:rp[i + 1]]
+    return a
+
+
+# ---------------------------------------------------------------- draw stream
+def test_gaussian_stream_matches_rng(oracle):
+    for seed, pre in ((0, 0), (7, 3), (123, 10)):
+        r = oracle.rng(seed)
+        for _ in range(pre):
+            r.normal()  # leaves a spare when pre is odd
+        g, st = P.gaussian_matrix(37, 11, r)
+        want = np.array([r.normal() for _ in range(37 * 11)]).reshape(37, 11)
+        assert np.max(np.abs(g - want) / np.maximum(np.abs(want), 1e-300)) < 1e-13
+        w, hs, sp = r.state()
+        assert (st.words, st.has_spare) == (w, hs)
+        if hs:
+            assert abs(st.spare - sp) <= 1e-13 * abs(sp)
+
+
+def test_gaussian_stream_large_and_interleaved_uniforms(oracle):
+    r = oracle.rng(42)
+    for _ in range(5):
+        r.uniform()  # raw words consumed outside the normal pairs
+    g, st = P.gaussian_matrix(1000, 100, r)
+    want = np.array([r.normal() for _ in range(100_000)]).reshape(1000, 100)
+    assert np.max(np.abs(g - want)) < 1e-12
+    assert st.words == r.state()[0]
+
+
+# ---------------------------------------------------------------- sparse products
+@pytest.mark.parametrize("m,d,fill,k", [(50, 40, 0.2, 3), (300, 120, 0.05, 64), (200, 900, 0.01, 104), (40, 30, 0.9, 7)])
+def test_csr_products_vs_dense(oracle, m, d, fill, k):
+    rp, cs, vs = S.random_sparse(oracle.rng(m * d), m, d, fill)
+    a = dense_of(rp, cs, vs, d)
+    rng = np.random.default_rng(1)
+    x, z = rng.standard_normal((d, k)), rng.standard_normal((m, k))
+    y, w = P.csr_products((rp, cs, vs), d, x=x, z=z)
+    assert np.max(np.abs(y - a @ x)) <= 1e-12 * max(1.0, np.abs(a @ x).max())
+    assert np.max(np.abs(w - a.T @ z)) <= 1e-12 * max(1.0, np.abs(a.T @ z).max())
+
+
+def test_csr_products_long_rows_and_columns():
+    # rows/columns longer than 2*kPiece take the split-and-fixup path
+    rng = np.random.default_rng(5)
+    m, d = 40, 3000
+    rows = []
+    for i in range(m):
+        n = 2500 if i % 7 == 0 else 5
+        rows.append(np.sort(rng.choice(d, n, replace=False)))
+    hot = np.arange(0, 10)  # hot columns appear in every row -> long CSC columns
+    rows = [np.union1d(r, hot) for r in rows]
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    cs = np.concatenate(rows).astype(np.uint32)
+    vs = rng.standard_normal(cs.size)
+    a = dense_of(rp, cs, vs, d)
+    x, z = rng.standard_normal((d, 16)), rng.standard_normal((m, 16))
+    y, w = P.csr_products((rp, cs, vs), d, x=x, z=z)
+    assert np.max(np.abs(y - a @ x)) <= 1e-11 * np.abs(a @ x).max()
+    assert np.max(np.abs(w - a.T @ z)) <= 1e-11 * np.abs(a.T @ z).max()
+    # deterministic: identical bits on repeat
+    y2, w2 = P.csr_products((rp, cs, vs), d, x=x, z=z)
+    assert np.array_equal(y, y2) and np.array_equal(w, w2)
+
+
+def test_csr_products_empty_rows_and_buffer():
+    rp = np.array([0, 0, 2, 2, 3], np.int64)
+    cs = np.array([1, 4, 0], np.uint32)
+    vs = np.array([2.0, -1.0, 3.0])
+    a = dense_of(rp, cs, vs, 5)
+    x = np.arange(10.0).reshape(5, 2)
+    y, w = P.csr_products((rp, cs, vs), 5, x=x, z=np.ones((4, 2)))
+    assert np.array_equal(y, a @ x)
+    assert np.array_equal(w, a.T @ np.ones((4, 2)))
+
+
+# ---------------------------------------------------------------- dense kernels
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 33, 100, 200, 257])
+def test_eigh_vs_oracle(oracle, n):
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n + 3, n))
+    k = a.T @ a
+    tol = 1e-12 * max((a ** 2).sum(), 1.0)
+    vals, vecs = P.eigh(k, tol)
+    ov, oe = oracle.jacobi_eigh(k, tol)
+    scale = np.abs(ov).max()
+    assert np.max(np.abs(vals - ov)) <= 1e-12 * scale
+    assert np.all(np.diff(vals) <= 0)
+    assert np.max(np.abs(vecs.T @ vecs - np.eye(n))) <= 1e-12
+    assert np.max(np.abs(vecs @ np.diag(vals) @ vecs.T - k)) <= 1e-11 * scale
+
+
+def test_eigh_degenerate_and_diagonal():
+    k = np.diag([3.0, 1.0, 3.0, 0.0, 2.0])
+    vals, vecs = P.eigh(k, 1e-12)
+    assert list(vals) == [3.0, 3.0, 2.0, 1.0, 0.0]
+    k = np.ones((6, 6))
+    vals, vecs = P.eigh(k, 1e-12)
+    assert abs(vals[0] - 6.0) < 1e-12 and np.max(np.abs(vals[1:])) < 1e-12
+
+
+@pytest.mark.parametrize("n,k", [(50, 10), (1000, 104), (300, 64), (12, 12)])
+def test_orthonormalize_projector_vs_oracle(oracle, n, k):
+    a = np.random.default_rng(n + k).standard_normal((n, k))
+    q = P.orthonormalize(a)
+    qo = oracle.orthonormalize(a)
+    assert np.max(np.abs(q.T @ q - np.eye(k))) <= 1e-13
+    assert np.max(np.abs(q @ q.T - qo @ qo.T)) <= 1e-12
+
+
+def test_orthonormalize_drops_dependent_columns(oracle):
+    rng = np.random.default_rng(3)
+    base = rng.standard_normal((40, 3))
+    a = np.column_stack([base[:, 0], base[:, 1], base[:, 0] + 2 * base[:, 1], base[:, 2], np.zeros(40)])
+    q = P.orthonormalize(a)
+    qo = oracle.orthonormalize(a)
+    assert np.array_equal(np.abs(q).sum(axis=0) == 0, np.abs(qo).sum(axis=0) == 0)
+    assert np.max(np.abs(q @ q.T - qo @ qo.T)) <= 1e-12
+
+
+# ---------------------------------------------------------------- shrinks
+def test_dense_shrink_kat():
+    b = P.dense_shrink(GOLD["kat_dense_a"], 2)
+    assert abs(abs(b[0, 0]) - math.sqrt(5.0)) < 1e-10
+    assert np.all(np.abs(b[0, 1:]) < 1e-10) and np.all(b[1] == 0.0)
+
+
+def test_dense_shrink_rank_below_ell():
+    a = np.zeros((2, 3))
+    a[0, 0] = a[1, 0] = 1.0
+    b = P.dense_shrink(a, 2)
+    assert abs(abs(b[0, 0]) - math.sqrt(2.0)) < 1e-10
+    assert np.max(np.abs(a.T @ a - b.T @ b)) < 1e-10
+
+
+def test_dense_shrink_tall_path():
+    b = P.dense_shrink(GOLD["tall_a"], 4)
+    assert btb_rel(b, GOLD["tall_b"]) <= 1e-12
+
+
+@pytest.mark.parametrize("rows,cols,ell", [(20, 50, 10), (200, 1000, 100), (512, 700, 256), (9, 9, 4)])
+def test_dense_shrink_vs_oracle(oracle, rows, cols, ell):
+    a = np.random.default_rng(rows).standard_normal((rows, cols))
+    assert btb_rel(P.dense_shrink(a, ell), oracle.dense_shrink(a, ell)) <= 1e-11
+
+
+def test_dense_shrink_validation():
+    with pytest.raises(P.InvalidArgument):
+        P.dense_shrink(np.zeros((3, 4)), 0)
+    with pytest.raises(P.InvalidArgument):
+        P.dense_shrink(np.zeros((3, 4)), 4)
+    bad = np.ones((3, 4))
+    bad[1, 2] = np.inf
+    with pytest.raises(P.InvalidArgument):
+        P.dense_shrink(bad, 2)
+
+
+def test_merge_cases(oracle):
+    # tests/test_sketch.cpp:206-253
+    rng = oracle.rng(6)
+    r = np.array([[rng.normal() for _ in range(8)] for _ in range(4)])
+    b = oracle.dense_shrink(r, 4)
+    m = P.merge(b, np.zeros((4, 8)), 4)
+    assert np.max(np.abs(b.T @ b - m.T @ m)) < 1e-8 * (b ** 2).sum()
+    assert np.all(P.merge(np.zeros((4, 8)), np.zeros((4, 8)), 4) == 0.0)
+    with pytest.raises(P.InvalidArgument):
+        P.merge(np.zeros((2, 4)), np.zeros((2, 5)), 2)
+    x = np.random.default_rng(2).standard_normal((2, 50, 300))
+    assert btb_rel(P.merge(x[0], x[1], 50), oracle.merge(x[0], x[1], 50)) <= 1e-10
+
+
+def test_sparse_shrink_rank_one_kat():
+    # tests/test_shrink.cpp:60-70: rows 2e1, 1e1 -> B'^T B' = 5 e1 e1^T
+    rp = np.array([0, 1, 2], np.int64)
+    b, _ = P.sparse_shrink((rp, np.array([0, 0], np.uint32), np.array([2.0, 1.0])), 4, 2, P.RngState(2))
+    g = b.T @ b
+    want = np.zeros((4, 4))
+    want[0, 0] = 5.0
+    assert np.max(np.abs(g - want)) < 1e-8 * 5.0
+
+
+@pytest.mark.parametrize("m,d,fill,ell,seed", [(100, 60, 0.15, 8, 7000), (60, 30, 0.2, 6, 1300), (400, 200, 0.05, 24, 3)])
+def test_sparse_shrink_vs_oracle(oracle, m, d, fill, ell, seed):
+    g = oracle.rng(seed)
+    csr = S.random_sparse(g, m, d, fill)
+    r_gpu = oracle.rng(seed + 1)
+    r_or = oracle.rng(seed + 1)
+    b, st = P.sparse_shrink(csr, d, ell, r_gpu)
+    bo = oracle.sparse_shrink(csr, d, ell, r_or)
+    assert btb_rel(b, bo) <= BTB_TOL
+    assert (st.words, st.has_spare) == r_or.state()[:2]
+
+
+def test_simultaneous_iteration_projector(oracle):
+    g = oracle.rng(11)
+    csr = S.random_sparse(g, 25, 18, 0.3)
+    z, _ = P.simultaneous_iteration(csr, 18, 4, oracle.rng(5))
+    zo = oracle.simultaneous_iteration(csr, 18, 4, oracle.rng(5))
+    assert np.max(np.abs(z.T @ z - np.eye(4))) <= 1e-12
+    assert np.max(np.abs(z @ z.T - zo @ zo.T)) <= 1e-10
+
+
+def test_simultaneous_iteration_exact_rank2(oracle):
+    # tests/test_randsvd.cpp:49-65
+    r = oracle.rng(3)
+    rows = []
+    for _ in range(5):
+        a, b = r.normal(), r.normal()
+        rows.append([a * 1.0, b * -1.0, a * 2.0, b * 0.5])
+    rp = np.arange(0, 21, 4, dtype=np.int64)
+    cs = np.tile(np.arange(4, dtype=np.uint32), 5)
+    vs = np.array(rows).ravel()
+    z, _ = P.simultaneous_iteration((rp, cs, vs), 4, 2, r)
+    a = np.array(rows)
+    res = a - z @ (z.T @ a)
+    assert np.linalg.norm(res) <= 1e-8 * np.linalg.norm(a)
+
+
+def test_boosted_vs_reference_golden():
+    csr = (GOLD["boost_rp"], GOLD["boost_cs"], GOLD["boost_vs"])
+    st = P.VerifierState()
+    b, dh, att, _ = P.boosted_sparse_shrink(csr, 30, 6, st, P.RngState(99))
+    dh_ref, att_ref, i_ref, spent_ref = GOLD["boost_meta"]
+    assert btb_rel(b, GOLD["boost_b"]) <= BTB_TOL
+    assert (att, st.i) == (int(att_ref), int(i_ref)) and st.delta_spent == spent_ref
+    assert abs(dh - dh_ref) <= 1e-10 * dh_ref
+
+
+def test_boosted_exact_recovery_branch():
+    # tests/test_shrink.cpp:167-181: rank-1 buffer -> Delta = 0, no verification
+    rp = np.array([0, 2, 4, 6], np.int64)
+    cs = np.array([0, 1] * 3, np.uint32)
+    vs = np.array([1.0, 2.0, 2.0, 4.0, -1.0, -2.0])
+    st = P.VerifierState()
+    b, dh, att, _ = P.boosted_sparse_shrink((rp, cs, vs), 6, 3, st, P.RngState(3))
+    assert (att, dh, st.i) == (1, 0.0, 0)
+    a = dense_of(rp, cs, vs, 6)
+    assert np.max(np.abs(a.T @ a - b.T @ b)) < 1e-8 * (vs ** 2).sum()
+
+
+# ---------------------------------------------------------------- the sketcher
+def sketch_gpu(rp, cs, vs, d, ell, seed, per_row=False, **kw):
+    s = P.SfdSketcher(P.SketchConfig(ell=ell, d=d, seed=seed, **kw))
+    if per_row:
+        for i in range(len(rp) - 1):
+            s.append(cs[rp[i]:rp[i + 1]], vs[rp[i]:rp[i + 1]])
+    else:
+        s.append_csr(rp, cs, vs)
+    b = s.finalize()
+    st = s.stats()
+    s.close()
+    return b, st
+
+
+def test_small_stream_vs_reference_golden():
+    b, st = sketch_gpu(GOLD["small_rp"], GOLD["small_cs"], GOLD["small_vs"], 40, 12, 9000)
+    fl, at, vi, spent = GOLD["small_stats"]
+    assert btb_rel(b, GOLD["small_b"]) <= BTB_TOL
+    assert (st["flushes"], st["attempts"], st["verifier_i"]) == (fl, at, vi) and st["delta_spent"] == spent
+
+
+def test_c1_prefix_vs_reference_golden():
+    rp, cs, vs = S.generate("c1", (0, 3000))
+    b, st = sketch_gpu(rp, cs, vs, 1000, 50, 0)
+    fl, at, vi, spent = GOLD["c1p_stats"]
+    assert btb_rel(b, GOLD["c1p_b"]) <= BTB_TOL
+    assert (st["flushes"], st["attempts"], st["verifier_i"]) == (fl, at, vi) and st["delta_spent"] == spent
+
+
+def test_c1_full_stream_vs_oracle(oracle):
+    rp, cs, vs = S.generate("c1")
+    b, st = sketch_gpu(rp, cs, vs, 1000, 50, 0)
+    bo, so = oracle.sketch(rp, cs, vs, 1000, 50, seed=0)
+    assert btb_rel(b, bo) <= BTB_TOL
+    for key in ("flushes", "attempts", "verifier_i", "delta_spent"):
+        assert st[key] == so[key], key
+    # covariance bound at k = 0 with alpha = 6/41 (tests/acceptance.cpp:102-117)
+    a_fsq = (vs ** 2).sum()
+    import scipy.sparse as sp
+    A = sp.csr_matrix((vs, cs, rp), shape=(len(rp) - 1, 1000))
+    diff = (A.T @ A).toarray() - b.T @ b
+    assert np.linalg.norm(diff, 2) <= a_fsq / (KALPHA * 50)
+    assert np.linalg.eigvalsh(diff).min() >= -1e-8 * a_fsq  # PSD dominance (Property 1)
+
+
+def test_triggers_flush_count_after_every_row(oracle):
+    # tests/test_sketch.cpp:35-66
+    s = P.SfdSketcher(P.SketchConfig(ell=4, d=16, seed=0))
+    s.append([0], [1.0])
+    assert s.flush_count() == 0 and s.stats()["buf_rows"] == 1
+    assert np.all(s.sketch() == 0.0)
+    s = P.SfdSketcher(P.SketchConfig(ell=3, d=6, seed=0))
+    g = oracle.rng(1)
+    for i in range(3):
+        s.append(np.arange(6), [g.normal() for _ in range(6)])
+        assert s.flush_count() == (1 if i == 2 else 0)
+    assert s.stats()["buf_rows"] == 0
+    s = P.SfdSketcher(P.SketchConfig(ell=4, d=8, seed=0))
+    for i in range(8):
+        s.append([i], [1.0])
+        assert s.flush_count() == (1 if i == 7 else 0)
+
+
+def test_finalize_paths(oracle):
+    s = P.SfdSketcher(P.SketchConfig(ell=3, d=10, seed=7))
+    b = s.finalize()
+    assert b.shape == (3, 10) and np.all(b == 0.0)
+    # partial buffer below ell rows: densify path (tests/test_sketch.cpp:76-93)
+    s = P.SfdSketcher(P.SketchConfig(ell=5, d=9, seed=7))
+    s.append([0, 3], [1.5, -2.0])
+    s.append([2, 5], [0.5, 1.0])
+    b = s.finalize()
+    o = oracle.sketcher(5, 9, 7)
+    o.append([0, 3], [1.5, -2.0])
+    o.append([2, 5], [0.5, 1.0])
+    bo = o.finalize()
+    assert np.max(np.abs(b.T @ b - bo.T @ bo)) <= 1e-12 * max(1.0, np.abs(bo.T @ bo).max())
+    # partial buffer with rows >= ell flushes through the full path, ell + rows > d -> tall path
+    g = oracle.rng(12)
+    rp, cs, vs = S.random_sparse(g, 7, 6, 0.6)
+    b, st = sketch_gpu(rp, cs, vs, 6, 4, 3)
+    bo, so = oracle.sketch(rp, cs, vs, 6, 4, seed=3)
+    assert btb_rel(b, bo) <= BTB_TOL and st["flushes"] == so["flushes"]
+
+
+def test_determinism_and_batching_are_bit_identical(oracle):
+    g = oracle.rng(31)
+    rp, cs, vs = S.random_sparse(g, 80, 16, 0.3)
+    b1, _ = sketch_gpu(rp, cs, vs, 16, 5, 4242)
+    b2, _ = sketch_gpu(rp, cs, vs, 16, 5, 4242)
+    b3, _ = sketch_gpu(rp, cs, vs, 16, 5, 4242, per_row=True)
+    assert np.array_equal(b1, b2) and np.array_equal(b1, b3)
+
+
+def test_device_resident_append_matches_host(oracle):
+    torch = pytest.importorskip("torch")
+    rp, cs, vs = S.generate("c1", (0, 2500))
+    b_host, st_host = sketch_gpu(rp, cs, vs, 1000, 50, 0)
+    dc = torch.from_numpy(cs.astype(np.int32)).cuda()
+    dv = torch.from_numpy(vs).cuda()
+    s = P.SfdSketcher(P.SketchConfig(ell=50, d=1000, seed=0))
+    s.append_csr_device(rp, dc.data_ptr(), dv.data_ptr())
+    b_dev = s.finalize()
+    st_dev = s.stats()
+    assert btb_rel(b_dev, b_host) <= 1e-12
+    assert (st_dev["flushes"], st_dev["attempts"]) == (st_host["flushes"], st_host["attempts"])
+
+
+def test_row_validation_commits_prefix():
+    s = P.SfdSketcher(P.SketchConfig(ell=2, d=5, seed=0))
+    rp = np.array([0, 1, 2, 4, 5], np.int64)
+    cs = np.array([0, 1, 3, 3, 4], np.uint32)  # row 2 not strictly increasing
+    vs = np.ones(5)
+    with pytest.raises(P.InvalidArgument, match="strictly increasing"):
+        s.append_csr(rp, cs, vs)
+    assert s.stats()["buf_rows"] == 2
+    with pytest.raises(P.InvalidArgument, match="out of range"):
+        s.append([7], [1.0])
+    with pytest.raises(P.InvalidArgument, match="non-finite"):
+        s.append([1], [float("inf")])
+    rp_b, cs_b, vs_b = s.buffer()
+    assert list(rp_b) == [0, 1, 2] and list(cs_b) == [0, 1]
+
+
+def test_covariance_bound_random_streams(oracle):
+    # tests/test_sketch.cpp:96-121 (>= 19 of 20 seeds)
+    ok = 0
+    for seed in range(20):
+        gen = oracle.rng(9000 + seed)
+        rows_rp, rows_cs, rows_vs = [0], [], []
+        for _ in range(300):
+            for j in range(40):
+                if gen.uniform() < 0.2:
+                    rows_cs.append(j)
+                    rows_vs.append(gen.normal())
+            rows_rp.append(len(rows_cs))
+        rp, cs, vs = np.array(rows_rp), np.array(rows_cs, np.uint32), np.array(rows_vs)
+        b, _ = sketch_gpu(rp, cs, vs, 40, 12, 9000 + seed)
+        a = dense_of(rp, cs, vs, 40)
+        if np.linalg.norm(a.T @ a - b.T @ b, 2) <= (a ** 2).sum() / (KALPHA * 12):
+            ok += 1
+    assert ok >= 19
