@@ -118,6 +118,8 @@ int sfdg_sketcher_get_sketch_device(sfdg_sketcher* h, double* d_out, size_t ld);
 int sfdg_sketcher_stats(sfdg_sketcher* h, sfdg_stats* out);
 /* buffer() contents (CSR, host): row_ptr (rows+1), cols (nnz), vals (nnz). */
 int sfdg_sketcher_get_buffer(sfdg_sketcher* h, int64_t* row_ptr, uint32_t* cols, double* vals);
+/* Returns the sketcher to its just-constructed state with a new seed (allocations kept). */
+int sfdg_sketcher_reset(sfdg_sketcher* h, uint64_t seed);
 /* Blocks until all queued device work of this sketcher finished. */
 int sfdg_sketcher_synchronize(sfdg_sketcher* h);
 
@@ -163,6 +165,11 @@ int sfdg_orthonormalize(const double* in, size_t n, size_t k, double* out, int d
  * y = A x (m x k, x: d x k), w = A^T z (d x k, z: m x k). Either output may be NULL. */
 int sfdg_csr_products(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t m, size_t d,
                       size_t k, const double* x, double* y, const double* z, double* w, int device);
+
+/* Per-kernel-class device timing with CUDA events on the launching stream (off by
+ * default). profile_end writes {"class": [total_ms, launches], ...} into buf. */
+int sfdg_profile_begin(void);
+int sfdg_profile_end(char* buf, size_t n);
 
 /* Process-wide count of kernels this library launched (benchmark gpu_launches claim). */
 uint64_t sfdg_launch_count(void);

@@ -105,6 +105,7 @@ def lib() -> C.CDLL:
     L.sfdg_sketcher_stats.argtypes = [C.c_void_p, C.POINTER(_Stats)]
     L.sfdg_sketcher_get_buffer.argtypes = [C.c_void_p, _i64p, _u32p, _dp]
     L.sfdg_sketcher_synchronize.argtypes = [C.c_void_p]
+    L.sfdg_sketcher_reset.argtypes = [C.c_void_p, C.c_uint64]
     L.sfdg_merge.argtypes = [_dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_int]
     L.sfdg_merge_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int,
                                     C.c_void_p]
@@ -119,8 +120,22 @@ def lib() -> C.CDLL:
     L.sfdg_eigh.argtypes = [_dp, C.c_size_t, C.c_double, _dp, _dp, C.c_int]
     L.sfdg_orthonormalize.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp, C.c_int]
     L.sfdg_csr_products.argtypes = csr + [C.c_size_t, _dp, _dp, _dp, _dp, C.c_int]
+    L.sfdg_profile_end.argtypes = [C.c_char_p, C.c_size_t]
     _LIB = L
     return L
+
+
+def profile_begin() -> None:
+    """Start per-kernel-class CUDA-event timing inside the library."""
+    lib().sfdg_profile_begin()
+
+
+def profile_end() -> dict:
+    """Stop timing; returns {kernel_class: (total_ms, launches)}."""
+    import json
+    buf = C.create_string_buffer(1 << 16)
+    lib().sfdg_profile_end(buf, len(buf))
+    return {k: (v[0], v[1]) for k, v in json.loads(buf.value.decode()).items()}
 
 
 def _check(code: int) -> None:
@@ -326,6 +341,16 @@ class SfdSketcher:
 
     def synchronize(self) -> None:
         _check(lib().sfdg_sketcher_synchronize(self._h))
+
+    def reset(self, seed: int | None = None) -> None:
+        """Back to the just-constructed state (optionally with a new seed); keeps allocations."""
+        if seed is not None:
+            self.cfg.seed = int(seed)
+        _check(lib().sfdg_sketcher_reset(self._h, C.c_uint64(self.cfg.seed)))
+
+    def finalize_device(self) -> None:
+        """finalize() leaving B on the device (no host copy)."""
+        _check(lib().sfdg_sketcher_finalize(self._h, None))
 
 
 # ---- free functions ------------------------------------------------------------

@@ -198,6 +198,24 @@ class Sketcher {
         eng->sync();
     }
 
+    // Back to a freshly constructed sketcher with `seed`, reusing every allocation.
+    void reset(uint64_t seed) {
+        eng->set_device();
+        eng->sync();
+        cfg.seed = seed;
+        eng->rng.restart(seed);
+        eng->pos = RngPos{};
+        for (int i = 0; i < 2; ++i)
+            CK(cudaMemsetAsync(eng->Mt[i], 0, (size_t)cfg.d * 2 * eng->lp * sizeof(double), eng->st));
+        eng->cur = 0;
+        CK(cudaMemsetAsync(eng->d_err, 0, sizeof(int), eng->st));
+        eng->sync();
+        ver = Verifier{};
+        ver.delta = cfg.delta;
+        clear_buffer();
+        flushes = attempts = 0;
+    }
+
   private:
     size_t buf_rows() const { return buf_rp.size() - 1; }
 
@@ -446,6 +464,10 @@ int sfdg_sketcher_stats(sfdg_sketcher* h, sfdg_stats* out) {
 
 int sfdg_sketcher_get_buffer(sfdg_sketcher* h, int64_t* row_ptr, uint32_t* cols, double* vals) {
     return guard([&] { impl_of(h)->get_buffer(row_ptr, cols, vals); });
+}
+
+int sfdg_sketcher_reset(sfdg_sketcher* h, uint64_t seed) {
+    return guard([&] { impl_of(h)->reset(seed); });
 }
 
 int sfdg_sketcher_synchronize(sfdg_sketcher* h) {

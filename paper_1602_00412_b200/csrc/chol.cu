@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(kCholThreads) chol_rinv_kernel(const double* _
 
     // Rinv: warp per column c solves R x = e_c by back substitution.
     const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-    for (int q = warp; q < k; q += nw) {
+    const int qend = ((k + nw - 1) / nw) * nw;
+    for (int q = warp; q < qend; q += nw) {
         // snake order balances the O(c) column costs across warps
         const int round = q / nw, pos = q % nw;
         const int c = (round & 1) ? round * nw + (nw - 1 - pos) : q;
@@ -149,6 +150,7 @@ void chol_rinv(const double* G, int k, int ldg, double* Rinv, int ldr, double* s
                Scratch& scr, cudaStream_t st) {
     if (k <= 0) return;
     if (k > 512) throw invalid_argument("chol_rinv: k > 512 unsupported");
+    ProfScope prof("chol", st);
     const bool use_smem = k <= 128;
     double* gscr = nullptr;
     size_t smem = 0;
@@ -159,7 +161,7 @@ void chol_rinv(const double* G, int k, int ldg, double* Rinv, int ldr, double* s
     }
     static bool attr_set = false;
     if (!attr_set) {
-        CK(cudaFuncSetAttribute(chol_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        allow_max_dynamic_smem(chol_rinv_kernel);
         attr_set = true;
     }
     LAUNCH(chol_rinv_kernel, 1, kCholThreads, smem, st, G, k, ldg, Rinv, ldr, stats, d_err, err_bit, gscr,

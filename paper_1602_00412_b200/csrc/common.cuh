@@ -43,7 +43,36 @@ extern std::atomic<uint64_t> g_launches;
         CK(cudaGetLastError());                                                          \
     } while (0)
 
+// Times everything a launcher enqueues on `st` between construction and destruction
+// under the kernel class `cls` when profiling is on (prof.cu); a no-op otherwise.
+extern std::atomic<bool> g_prof_on;
+class ProfScope {
+  public:
+    ProfScope(const char* cls, cudaStream_t st);
+    ~ProfScope();
+    ProfScope(const ProfScope&) = delete;
+    ProfScope& operator=(const ProfScope&) = delete;
+
+  private:
+    const char* cls_ = nullptr;
+    cudaStream_t st_;
+    cudaEvent_t e0_ = nullptr, e1_ = nullptr;
+};
+
 constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+// Opt a kernel into the largest dynamic shared memory the device allows next to its
+// static shared memory (227 KB per CTA on sm_100a).
+template <class F>
+inline void allow_max_dynamic_smem(F* func) {
+    cudaFuncAttributes attr;
+    CK(cudaFuncGetAttributes(&attr, (const void*)func));
+    int dev = 0, optin = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CK(cudaFuncSetAttribute((const void*)func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            optin - (int)attr.sharedSizeBytes));
+}
 
 inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 inline unsigned ceil_div(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }

@@ -230,6 +230,7 @@ void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scrat
         fill2d(out, k, k, ldo, 0.0, st);
         return;
     }
+    ProfScope prof("gram", st);
     const int T = (k + TB - 1) / TB;
     const int ntiles = T * (T + 1) / 2;
     int target_chunks = std::max(1, (2 * kSMs + ntiles - 1) / ntiles);
@@ -248,11 +249,13 @@ void gemm_nn(const double* X, int n, int k, int ldx, const double* S, int c, int
         fill2d(C, n, c, ldc, 0.0, st);
         return;
     }
+    ProfScope prof("gemm", st);
     LAUNCH(gemm_nn_kernel, dim3(ceil_div(n, TB), ceil_div(c, TB)), 128, 0, st, X, n, k, ldx, S, c, lds, C, ldc);
 }
 
 void sumsq(const double* X, int64_t rows, int cols, int ld, double* d_out, int* d_err, int err_bit, Scratch& scr,
            cudaStream_t st) {
+    ProfScope prof("reduce", st);
     double* partial = scr.take<double>(kRedBlocks);
     LAUNCH(sumsq_partial_kernel, kRedBlocks, 256, 0, st, X, rows, cols, ld, partial, d_err, err_bit);
     LAUNCH(sum_partials_kernel, 1, 32, 0, st, partial, kRedBlocks, d_out);

@@ -233,17 +233,23 @@ void eigh(const double* K, int n, int ldk, double off_tol, const double* d_fsq, 
     double* V = scr.take<double>((int64_t)n * n);
     static bool attr = false;
     if (!attr) {
-        CK(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        CK(cudaFuncSetAttribute(vapply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        allow_max_dynamic_smem(jacobi_kernel);
+        allow_max_dynamic_smem(vapply_kernel);
         attr = true;
     }
     const size_t smem = use_smem ? packed * sizeof(double) : 0;
-    LAUNCH(jacobi_kernel, 1, kJacThreads, smem, st, K, n, ldk, off_tol * off_tol, d_fsq, gpk, use_smem ? 1 : 0,
-           rotlog, nrounds, diag, d_err);
+    {
+        ProfScope prof("eigh_jacobi", st);
+        LAUNCH(jacobi_kernel, 1, kJacThreads, smem, st, K, n, ldk, off_tol * off_tol, d_fsq, gpk, use_smem ? 1 : 0,
+               rotlog, nrounds, diag, d_err);
+    }
     const int rows_per_block = 8;
-    LAUNCH(vapply_kernel, ceil_div(n, rows_per_block), 32 * rows_per_block, rows_per_block * N * sizeof(double), st, n,
-           rotlog, nrounds, V, n);
-    LAUNCH(sort_kernel, 1, 1024, 0, st, n, diag, V, n, values, vectors, ldv);
+    {
+        ProfScope prof("eigh_vectors", st);
+        LAUNCH(vapply_kernel, ceil_div(n, rows_per_block), 32 * rows_per_block, rows_per_block * N * sizeof(double),
+               st, n, rotlog, nrounds, V, n);
+        LAUNCH(sort_kernel, 1, 1024, 0, st, n, diag, V, n, values, vectors, ldv);
+    }
 }
 
 }  // namespace sfdg

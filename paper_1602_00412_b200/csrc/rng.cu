@@ -131,6 +131,13 @@ void RngStream::reseed() {
     gen_words = 0;
 }
 
+void RngStream::restart(uint64_t seed_) {
+    CK(cudaStreamSynchronize(s_gen));
+    seed = seed_;
+    spare_slot = 0;
+    reseed();
+}
+
 void RngStream::release() {
     if (d_ring) cudaFree(d_ring);
     if (d_window) cudaFree(d_window);
@@ -150,6 +157,7 @@ void RngStream::generate_to(uint64_t words_end) {
     if (words_end <= gen_words) return;
     // Never overwrite words a queued consumer may still read.
     CK(cudaStreamWaitEvent(s_gen, ev_consumed, 0));
+    ProfScope prof("rng_gen", s_gen);
     const uint64_t need = words_end - gen_words;
     const int steps = (int)((need + MT_M - 1) / MT_M);
     LAUNCH(mt_generate_kernel, 1, MT_M, 0, s_gen, d_window, d_ring, ring_cap - 1, gen_words, steps);
@@ -189,6 +197,7 @@ void RngStream::normals(RngPos& st, uint64_t n, uint64_t cols, uint64_t ld, doub
     double* spare_in = d_spare + (spare_slot & 1);
     double* spare_out = d_spare + ((spare_slot + 1) & 1);
     const bool new_spare = (rest % 2) == 1;
+    ProfScope prof("box_muller", stream);
     const unsigned blocks = (unsigned)std::min<uint64_t>(4 * kSMs, (pairs + 255) / 256 + 1);
     LAUNCH(box_muller_kernel, blocks, 256, 0, stream, d_ring, ring_cap - 1, st.words, (int)st.has_spare, spare_in, n,
            cols, ld, d_out, new_spare ? spare_out : nullptr, d_err);

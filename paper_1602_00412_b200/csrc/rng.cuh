@@ -22,6 +22,7 @@ class RngStream {
     ~RngStream() { release(); }
 
     void init(uint64_t seed, uint64_t min_ring_words, int device);
+    void restart(uint64_t seed);  // back to Rng(seed), keeping the allocations
     void release();
 
     // Draw n normals at `pos` into d_out (rows of `cols`, leading dimension ld).

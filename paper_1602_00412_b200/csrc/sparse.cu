@@ -431,6 +431,7 @@ void rebase_row_ptr(const int64_t* d_src, int64_t base, int m, int* d_dst, cudaS
 
 // CSR -> CSC (stable in row order) + long-row plans for both orientations.
 void build_transpose(DevCsr& a, Scratch& scr, cudaStream_t st) {
+    ProfScope prof("csc_build", st);
     const int64_t n = a.nnz;
     const int d = a.d;
     if (n == 0) {
@@ -464,6 +465,7 @@ void build_transpose(DevCsr& a, Scratch& scr, cudaStream_t st) {
 }
 
 void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st) {
+    ProfScope prof("csc_build", st);
     rows = nrows;
     reserve_pieces(nnz);
     if (nrows > cap_rows) {
@@ -510,6 +512,7 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
           const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st) {
     if (nrows == 0) return;
     if (ncols % 2 != 0 || ld % 2 != 0 || ldo % 2 != 0) throw invalid_argument("spmm: panel widths must be even");
+    ProfScope prof("spmm", st);
     const int J = (ncols + 63) / 64;
     const unsigned grid = std::max(1u, std::min(16u * kSMs, ceil_div((size_t)nrows * 32, 256)));
     double* partial = scr.take<double>((2 * (nnz / kPiece) + 2) * (int64_t)ld);

@@ -199,6 +199,7 @@ int verify_grid_blocks(int device) {
 }
 
 void verify_launch(const VerifyArgs& args, int nblocks, cudaStream_t st) {
+    ProfScope prof("verify", st);
     CK(cudaMemsetAsync(args.bar, 0, 2 * sizeof(unsigned), st));
     void* params[] = {(void*)&args};
     CK(cudaLaunchCooperativeKernel((const void*)verify_kernel, dim3(nblocks), dim3(kVThreads), params, 0, st));

@@ -165,14 +165,15 @@ def _heavy(cfg: StreamConfig, r0: int, r1: int):
     return np.concatenate(rps), np.concatenate(css).astype(np.uint32), np.concatenate(vss)
 
 
-def generate(name: str, rows: tuple[int, int] | None = None):
-    """CSR of rows [r0, r1) of config `name` (default: the whole stream)."""
-    cfg = CONFIGS[name]
+def generate(name: str | StreamConfig, rows: tuple[int, int] | None = None):
+    """CSR of rows [r0, r1) of config `name` (default: the whole stream). A StreamConfig
+    selects the family by its name with its own seed (e.g. per-shard seeds)."""
+    cfg = name if isinstance(name, StreamConfig) else CONFIGS[name]
     r0, r1 = rows if rows is not None else (0, cfg.n)
     r1 = min(r1, cfg.n)
-    if name == "c1":
+    if cfg.name == "c1":
         return _bernoulli_lowrank(cfg, 10, 0.8, 0.01, r0, r1)
-    if name == "c2":
+    if cfg.name == "c2":
         return _bernoulli_lowrank(cfg, 20, 0.9, 0.001, r0, r1)
     return _heavy(cfg, r0, r1)
 
