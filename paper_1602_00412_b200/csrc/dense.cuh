@@ -24,9 +24,11 @@ void fill2d(double* out, int rows, int cols, int ldo, double v, cudaStream_t st)
 // CholeskyQR factor step (chol.cu): from the Gram G (k x k) of a tall Y, the upper
 // triangular Rinv with Y Rinv orthonormal; columns whose residual pivot falls below
 // the drop rule are zeroed (la_core.cpp:141,157-162). stats[0] = min relative pivot
-// of the kept columns, stats[1] = number of dropped columns.
+// of the kept columns, stats[1] = number of dropped columns, stats[2] = max|G - I|.
+// polar = true (second CholeskyQR pass): T = I - (G - I)/2 when max|G - I| <= 1e-6,
+// otherwise the full Cholesky path.
 void chol_rinv(const double* G, int k, int ldg, double* Rinv, int ldr, double* stats, int* d_err, int err_bit,
-               Scratch& scr, cudaStream_t st);
+               Scratch& scr, cudaStream_t st, bool polar = false);
 
 // Symmetric eigensolver (eigh.cu), the jacobi_eigh contract (la_core.cpp:24-80):
 // values descending (n), vectors column k (n x n, ldv). off_tol is absolute, or, when

@@ -242,7 +242,7 @@ void Engine::orthonormalize(double* Yp, int m, int err_bit) {
     chol_rinv(gram, lp, lp, rinv, lp, stats, d_err, err_bit, scr, st);
     gemm_nn(Yp, m, lp, lp, rinv, lp, lp, Yt, lp, st);
     gram_tn(Yt, m, lp, lp, gram, lp, scr, st);
-    chol_rinv(gram, lp, lp, rinv, lp, stats, d_err, err_bit, scr, st);
+    chol_rinv(gram, lp, lp, rinv, lp, stats, d_err, err_bit, scr, st, /*polar=*/true);
     gemm_nn(Yt, m, lp, lp, rinv, lp, lp, Yp, lp, st);
 }
 
