@@ -1,4 +1,4 @@
-// chol.cu -- CholeskyQR factor step with the reference's column-drop rule.
+// chol.cu -- CholeskyQR factor + apply with the reference's column-drop rule.
 //
 // Reference: orthonormalize (core/src/la_core.cpp:130-165) runs modified Gram-Schmidt
 // with one re-orthogonalisation pass and zeroes a column whose residual norm falls
@@ -9,13 +9,16 @@
 // carries O(k u G_jj) cancellation error, so a pivot below kRelDrop * G_jj is treated as
 // numerically dependent and dropped as well.
 //
-// Second pass (mode kPolar): after one CholeskyQR pass, G = Q^T Q = I + E with tiny E.
-// Then T = I - E/2 gives (QT)^T(QT) = I - 3/4 E^2 + O(E^3): orthonormal to O(|E|^2)
-// with the same span, without a sequential factorisation. When max|E| > kPolarMax the
-// kernel falls back to the full Cholesky path, so accuracy never depends on the guess.
-//
-// One CTA; the k x k Gram lives in shared memory (k <= 160) or L2-resident scratch.
-// Layout: upper triangle = R, strictly lower triangle = off-diagonal of Rinv^T, dinv[k].
+//  * chol_factor_kernel (1 CTA): R (upper, k x k) with a one-barrier-per-pivot right-
+//    looking loop (warp 0 carries the pivot chain, the other warps the trailing update),
+//    plus the inverse of every 8 x 8 diagonal block of R.
+//  * trsm_apply_kernel (many CTAs): Q = Y R^-1 without ever forming R^-1: each warp owns
+//    16 rows and forward-substitutes them block column by block column with DMMA
+//    (X_b = (Y_b - X_<b R_<b,b) inv(R_bb)); rows are independent, so no CTA barrier.
+//  * Second pass (polar): after one CholeskyQR pass, G = Q^T Q = I + E with tiny E, and
+//    T = I - E/2 gives (QT)^T(QT) = I - 3/4 E^2 + O(E^3) with the same span. The kernel
+//    emits T for gemm_nn when max|E| <= kPolarMax and otherwise falls back to the
+//    Cholesky path, so accuracy never depends on the guess.
 #include <algorithm>
 
 #include "common.cuh"
@@ -30,22 +33,26 @@ constexpr double kPolarMax = 1e-6;  // |E|^2 <= 1e-12 relative -> far below the 
 constexpr int kCholThreads = 512;
 constexpr int kSmemMaxK = 160;
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kCholThreads) chol_rinv_kernel(const double* __restrict__ G, int k, int ldg,
-                                                                 double* __restrict__ Rinv, int ldr,
-                                                                 double* __restrict__ stats, int* __restrict__ err,
-                                                                 int err_bit, double* __restrict__ gscratch,
-                                                                 int use_smem, int polar) {
+// out: R (k x k row-major, upper; dropped rows = e_j), dinv8 (k x 8: inverse of the
+// 8 x 8 diagonal block containing row i, row i of that inverse, zero columns for dropped),
+// stats[0] = min relative pivot, [1] = dropped count, [2] = max|G - I|,
+// [3] = max R_jj / min R_jj over kept columns, [4] = 1 when the polar path was taken.
+__global__ void __launch_bounds__(kCholThreads) chol_factor_kernel(const double* __restrict__ G, int k, int ldg,
+                                                                   double* __restrict__ Rout, double* __restrict__ dinv8,
+                                                                   double* __restrict__ T, int ldt,
+                                                                   double* __restrict__ stats, int* __restrict__ err,
+                                                                   int err_bit, double* __restrict__ gscratch,
+                                                                   int use_smem, int polar) {
     extern __shared__ double sm[];
-    const int lda = use_smem ? k + 1 : k;
+    const int lda = use_smem ? k + 4 : k;
     double* A = use_smem ? sm : gscratch;
     double* d0 = A + (size_t)k * lda;  // original diagonal
-    double* dinv = d0 + k;             // 1 / R_jj (0 for dropped)
     __shared__ double s_thr, s_emax;
     __shared__ int s_bad, s_dropped;
     __shared__ double red[32];
@@ -60,23 +67,23 @@ __global__ void __launch_bounds__(kCholThreads) chol_rinv_kernel(const double* _
     for (int j = tid; j < k; j += nt) s_drop[j] = 0;
     __syncthreads();
     double mx = 0.0, emax = 0.0;
-    for (int e = tid; e < k * k; e += nt) {
-        const int i = e / k, j = e % k;
-        const double v = G[(size_t)i * ldg + j];
-        if (!isfinite(v)) s_bad = 1;
-        if (j >= i) A[(size_t)i * lda + j] = v;
-        if (i == j) {
-            d0[i] = v;
-            mx = fmax(mx, v);
+    for (int i = warp; i < k; i += nw)
+        for (int j = i + lane; j < k; j += 32) {
+            const double v = G[(size_t)i * ldg + j];
+            if (!isfinite(v)) s_bad = 1;
+            A[(size_t)i * lda + j] = v;
+            if (i == j) {
+                d0[i] = v;
+                mx = fmax(mx, v);
+            }
         }
-    }
     __syncthreads();
     if (polar) {  // max |G - I| over the kept (nonzero-diagonal) columns
-        for (int e = tid; e < k * k; e += nt) {
-            const int i = e / k, j = e % k;
-            if (j < i || d0[i] == 0.0 || d0[j] == 0.0) continue;
-            emax = fmax(emax, fabs(A[(size_t)i * lda + j] - (i == j ? 1.0 : 0.0)));
-        }
+        for (int i = warp; i < k; i += nw)
+            for (int j = i + lane; j < k; j += 32) {
+                if (d0[i] == 0.0 || d0[j] == 0.0) continue;
+                emax = fmax(emax, fabs(A[(size_t)i * lda + j] - (i == j ? 1.0 : 0.0)));
+            }
     }
     for (int o = 16; o > 0; o >>= 1) {
         mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -99,33 +106,40 @@ __global__ void __launch_bounds__(kCholThreads) chol_rinv_kernel(const double* _
     }
     __syncthreads();
     if (s_bad) {
-        for (int e = tid; e < k * k; e += nt) Rinv[(size_t)(e / k) * ldr + e % k] = 0.0;
         if (tid == 0) atomicOr(err, err_bit);
+        if (polar)
+            for (int e = tid; e < k * k; e += nt) T[(size_t)(e / k) * ldt + e % k] = 0.0;
+        for (int e = tid; e < k * k; e += nt) Rout[e] = (e / k == e % k) ? 1.0 : 0.0;
+        for (int e = tid; e < k * 8; e += nt) dinv8[e] = 0.0;
+        if (tid == 0) {
+            stats[0] = 0.0;
+            stats[3] = 1e300;
+            stats[4] = 0.0;
+        }
         return;
     }
-
     if (polar && s_emax <= kPolarMax) {
         // T = I - E/2 on kept columns, zero rows/columns for dropped ones (Q_j = 0 stays 0)
-        for (int e = tid; e < k * k; e += nt) {
-            const int i = e / k, j = e % k;
-            double v = 0.0;
-            if (d0[i] != 0.0 && d0[j] != 0.0) {
-                const double g = i <= j ? A[(size_t)i * lda + j] : A[(size_t)j * lda + i];
-                v = (i == j ? 1.0 : 0.0) - 0.5 * (g - (i == j ? 1.0 : 0.0));
+        for (int i = warp; i < k; i += nw)
+            for (int j = lane; j < k; j += 32) {
+                double v = 0.0;
+                if (d0[i] != 0.0 && d0[j] != 0.0) {
+                    const double g = i <= j ? A[(size_t)i * lda + j] : A[(size_t)j * lda + i];
+                    v = (i == j ? 1.0 : 0.0) - 0.5 * (g - (i == j ? 1.0 : 0.0));
+                }
+                T[(size_t)i * ldt + j] = v;
             }
-            Rinv[(size_t)i * ldr + j] = v;
-        }
         if (tid == 0) {
             stats[0] = 1.0;
             stats[1] = 0.0;
             stats[2] = s_emax;
+            stats[3] = 1.0;
+            stats[4] = 1.0;
         }
         return;
     }
 
-    // ---- right-looking Cholesky, one barrier per column. Warp 0 owns the pivot chain:
-    // it updates row j+1 with row j, then pivots and scales row j+1, while the other
-    // warps update rows j+2.. with row j.
+    // ---- right-looking Cholesky, one barrier per pivot
     auto pivot_row = [&](int j) {  // warp 0 only
         const double piv = A[(size_t)j * lda + j];
         const bool keep = isfinite(piv) && piv > s_thr && piv > kRelDrop * d0[j] && piv > 0.0;
@@ -137,7 +151,6 @@ __global__ void __launch_bounds__(kCholThreads) chol_rinv_kernel(const double* _
         }
         if (lane == 0) {
             A[(size_t)j * lda + j] = r;
-            dinv[j] = keep ? ri : 0.0;
             if (!keep) {
                 s_drop[j] = 1;
                 s_dropped += 1;
@@ -145,6 +158,77 @@ __global__ void __launch_bounds__(kCholThreads) chol_rinv_kernel(const double* _
         }
         __syncwarp();
     };
+    if (use_smem && k % 8 == 0 && k <= 128) {
+        // Blocked right-looking Cholesky: warp 0 factors an 8-row panel entirely in
+        // registers (pivots via shuffles, no barrier), then all warps apply the rank-8
+        // trailing update R_p^T R_p with DMMA on 8 x 8 tiles. Two barriers per 8 pivots.
+        const int g = lane >> 2, t4 = lane & 3;
+        for (int jb = 0; jb < k; jb += 8) {
+            if (warp == 0) {
+                double p[8][4];
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = jb + lane + 32 * q;
+                        p[r][q] = c < k ? A[(size_t)(jb + r) * lda + c] : 0.0;
+                    }
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int j = jb + jj;
+                    const double piv = __shfl_sync(0xffffffffu, p[jj][0], jj);
+                    const bool keep = isfinite(piv) && piv > s_thr && piv > kRelDrop * d0[j] && piv > 0.0;
+                    const double r = keep ? sqrt(piv) : 1.0;
+                    const double ri = 1.0 / r;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = jb + lane + 32 * q;
+                        if (c > j) p[jj][q] = keep ? p[jj][q] * ri : 0.0;
+                        else if (c == j) p[jj][q] = r;
+                    }
+                    if (!keep && lane == 0) {
+                        s_drop[j] = 1;
+                        s_dropped += 1;
+                    }
+#pragma unroll
+                    for (int ii = jj + 1; ii < 8; ++ii) {
+                        const double coef = __shfl_sync(0xffffffffu, p[jj][0], ii);  // R[j][jb + ii]
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) p[ii][q] -= coef * p[jj][q];
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = jb + lane + 32 * q;
+                        if (c < k && c >= jb + r) A[(size_t)(jb + r) * lda + c] = p[r][q];
+                    }
+            }
+            __syncthreads();
+            const int t0 = jb / 8 + 1, nrem = k / 8 - t0;
+            const int ntiles = nrem * (nrem + 1) / 2;
+            for (int tile = warp; tile < ntiles; tile += nw) {
+                int ti = 0, rem = tile;
+                while (rem >= nrem - ti) {
+                    rem -= nrem - ti;
+                    ++ti;
+                }
+                const int i0 = (t0 + ti) * 8, c0 = (t0 + ti + rem) * 8;
+                double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < 8; ks += 4) {
+                    const double av = A[(size_t)(jb + ks + t4) * lda + i0 + g];
+                    const double bv = A[(size_t)(jb + ks + t4) * lda + c0 + g];
+                    dmma884(v0, v1, av, bv);
+                }
+                double* dst = A + (size_t)(i0 + g) * lda + c0 + 2 * t4;
+                dst[0] -= v0;
+                dst[1] -= v1;
+            }
+            __syncthreads();
+        }
+    } else {
     if (warp == 0) pivot_row(0);
     __syncthreads();
     for (int j = 0; j + 1 < k; ++j) {
@@ -158,81 +242,163 @@ __global__ void __launch_bounds__(kCholThreads) chol_rinv_kernel(const double* _
             __syncwarp();
             pivot_row(j + 1);
         } else if (kept) {
-            // rows i >= j+2, columns c >= i: flattened over the trailing block
-            const int base = j + 2, rem = k - base;
-            for (int e = tid - 32; e < rem * rem; e += nt - 32) {
-                const int i = base + e / rem, c = base + e % rem;
-                if (c >= i) A[(size_t)i * lda + c] -= rj[i] * rj[c];
+            for (int i = j + 1 + warp; i < k; i += nw - 1) {  // rows j+2.. (warp w >= 1)
+                const double rji = rj[i];
+                if (rji == 0.0) continue;
+                double* ai = A + (size_t)i * lda;
+                for (int c = i + lane; c < k; c += 32) ai[c] -= rji * rj[c];
             }
         }
         __syncthreads();
     }
-
-    // ---- Rinv = R^-1. Column c of Rinv by back substitution, one warp per column,
-    // x_i (i < c) stored in the strictly lower triangle row c: A[c][i].
-    const int qend = ((k + nw - 1) / nw) * nw;
-    for (int q = warp; q < qend; q += nw) {
-        const int round = q / nw, pos = q % nw;
-        const int c = (round & 1) ? round * nw + (nw - 1 - pos) : q;  // snake order balances cost
-        if (c >= k) continue;
-        const double xc = dinv[c];
-        for (int i = c - 1; i >= 0; --i) {
-            double s = 0.0;
-            for (int l = i + 1 + lane; l <= c; l += 32) {
-                const double xl = (l == c) ? xc : A[(size_t)c * lda + l];
-                s = fma(A[(size_t)i * lda + l], xl, s);
+    }
+    // ---- outputs: R, and the inverse of every 8 x 8 diagonal block (one thread per
+    // column of each block solves the 8 x 8 triangular system by back substitution)
+    for (int i = warp; i < k; i += nw)
+        for (int c = lane; c < k; c += 32) Rout[(size_t)i * k + c] = c >= i ? A[(size_t)i * lda + c] : 0.0;
+    for (int t = tid; t < k; t += nt) {
+        const int c = t;  // column c of block b = c / 8
+        const int b0 = (c / 8) * 8, b1 = min(b0 + 8, k);
+        double x[8];
+        for (int i = 0; i < 8; ++i) x[i] = 0.0;
+        if (!s_drop[c]) {
+            for (int i = c; i >= b0; --i) {
+                double s = (i == c) ? 1.0 : 0.0;
+                for (int l = i + 1; l <= c; ++l) s -= A[(size_t)i * lda + l] * x[l - b0];
+                x[i - b0] = s / A[(size_t)i * lda + i];
             }
-            s = warp_sum(s);
-            if (lane == 0) A[(size_t)c * lda + i] = -s * dinv[i];
-            __syncwarp();
         }
+        // dinv8 row i (i in block) column (c - b0): inv(R_bb)[i][c]
+        for (int i = b0; i < b1; ++i) dinv8[(size_t)i * 8 + (c - b0)] = x[i - b0];
     }
     __syncthreads();
-    // Dropped j: dinv[j] = 0 zeroes column j (Q_j = 0, la_core.cpp:158-159) and row j
-    // of R is zero, so no kept column sees y_j.
-    for (int e = tid; e < k * k; e += nt) {
-        const int i = e / k, c = e % k;
-        double v = 0.0;
-        if (i == c) v = dinv[c];
-        else if (i < c) v = s_drop[c] ? 0.0 : A[(size_t)c * lda + i];
-        Rinv[(size_t)i * ldr + c] = v;
-    }
     if (tid == 0) {
-        double mn = 1.0;
+        double mn = 1.0, rmax = 0.0, rmin = 1e300;
         for (int j = 0; j < k; ++j)
             if (!s_drop[j] && d0[j] > 0.0) {
                 const double r = A[(size_t)j * lda + j];
                 mn = fmin(mn, r * r / d0[j]);
+                rmax = fmax(rmax, r);
+                rmin = fmin(rmin, r);
             }
         stats[0] = mn;
         stats[1] = (double)s_dropped;
         stats[2] = s_emax;
+        stats[3] = rmin > 0.0 && rmin < 1e300 ? rmax / rmin : 1.0;
+        stats[4] = 0.0;
+    }
+}
+
+// Q = Y R^-1 (m x k, ld). Warp w of the CTA owns rows [64*blk + 16w, +16) as two 8-row
+// DMMA tiles; block columns b = 0..nb-1 of 8: acc = Y_b - X_<b R_<b,b ; X_b = acc inv(R_bb).
+// R (k x k) and inv(R_bb) (k x 8) are staged in shared memory once per CTA. When the
+// second-pass polar path was taken (stats[4] == 1) the kernel is a no-op (gemm applies T).
+constexpr int kTrsmRows = 64;
+constexpr int kTrsmSmemK = 128;
+__global__ void __launch_bounds__(128) trsm_apply_kernel(const double* __restrict__ Y, int m, int k, int ld,
+                                                         const double* __restrict__ R, const double* __restrict__ dinv8,
+                                                         double* __restrict__ X, int ldx,
+                                                         const double* __restrict__ stats) {
+    if (stats && stats[4] != 0.0) return;
+    extern __shared__ double sm[];
+    const int kp = (k + 7) / 8 * 8;
+    const bool rsm = kp <= kTrsmSmemK;  // R staged in shared memory, else read through L1
+    const int ldr = rsm ? kp + 4 : k;   // conflict-free B-fragment reads (ldr % 16 == 4 or 12)
+    const int ldy = kp + 4;
+    double* Rs = sm;                                     // kp x ldr (when rsm)
+    double* Ds = Rs + (rsm ? (size_t)kp * ldr : 0);      // kp x 8 (+4 pad)
+    double* Xs = Ds + (size_t)kp * 12;                   // 64 x ldy : Y tile, overwritten by X
+    const double* Rr = rsm ? Rs : R;
+    const int r0 = blockIdx.x * kTrsmRows;
+    if (rsm)
+        for (int e = threadIdx.x; e < kp * kp; e += blockDim.x) {
+            const int i = e / kp, c = e % kp;
+            Rs[(size_t)i * ldr + c] = (i < k && c < k) ? R[(size_t)i * k + c] : (i == c ? 1.0 : 0.0);
+        }
+    for (int e = threadIdx.x; e < kp * 8; e += blockDim.x) {
+        const int i = e / 8, c = e % 8;
+        Ds[(size_t)i * 12 + c] = (i < k) ? dinv8[(size_t)i * 8 + c] : 0.0;
+    }
+    for (int e = threadIdx.x; e < kTrsmRows * kp; e += blockDim.x) {
+        const int i = e / kp, c = e % kp;
+        Xs[(size_t)i * ldy + c] = (r0 + i < m && c < k) ? Y[(size_t)(r0 + i) * ld + c] : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int nb = kp / 8;
+    for (int mt = 0; mt < 2; ++mt) {
+        double* xr = Xs + (size_t)(w * 16 + mt * 8) * ldy;  // this warp's 8-row tile
+        for (int b = 0; b < nb; ++b) {
+            double c0 = 0.0, c1 = 0.0;  // acc = X_<b R_<b,b (subtracted below)
+            for (int kk = 0; kk < 8 * b; kk += 4) {
+                const double av = xr[(size_t)g * ldy + kk + t];
+                const int rr = kk + t, cc = 8 * b + g;
+                const double bv = rsm ? Rr[(size_t)rr * ldr + cc] : (rr < k && cc < k ? __ldg(Rr + (size_t)rr * ldr + cc) : 0.0);
+                dmma884(c0, c1, av, bv);
+            }
+            // acc = Y_b - acc, laid out as C fragment: row g, cols 2t, 2t+1 of block b
+            double* yb = xr + (size_t)g * ldy + 8 * b + 2 * t;
+            const double a0 = yb[0] - c0, a1 = yb[1] - c1;
+            __syncwarp();
+            yb[0] = a0;
+            yb[1] = a1;
+            __syncwarp();
+            // X_b = acc inv(R_bb): A frag from xr (row g, col 4ks + t), B frag from Ds
+            double x0 = 0.0, x1 = 0.0;
+            for (int ks = 0; ks < 8; ks += 4) {
+                const double av = xr[(size_t)g * ldy + 8 * b + ks + t];
+                const double bv = Ds[(size_t)(8 * b + ks + t) * 12 + g];
+                dmma884(x0, x1, av, bv);
+            }
+            __syncwarp();
+            yb[0] = x0;
+            yb[1] = x1;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTrsmRows * k; e += blockDim.x) {
+        const int i = e / k, c = e % k;
+        if (r0 + i < m) X[(size_t)(r0 + i) * ldx + c] = Xs[(size_t)i * ldy + c];
     }
 }
 
 }  // namespace
 
-void chol_rinv(const double* G, int k, int ldg, double* Rinv, int ldr, double* stats, int* d_err, int err_bit,
-               Scratch& scr, cudaStream_t st, bool polar) {
+void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, double* T, int ldt, double* stats,
+                 int* d_err, int err_bit, Scratch& scr, cudaStream_t st, bool polar) {
     if (k <= 0) return;
-    if (k > 512) throw invalid_argument("chol_rinv: k > 512 unsupported");
+    if (k > 512) throw invalid_argument("chol_factor: k > 512 unsupported");
     ProfScope prof(polar ? "chol_polar" : "chol", st);
     const bool use_smem = k <= kSmemMaxK;
     double* gscr = nullptr;
-    size_t smem = 3 * (size_t)k * sizeof(double);
+    size_t smem = 2 * (size_t)k * sizeof(double);
     if (use_smem) {
-        smem += (size_t)k * (k + 1) * sizeof(double);
+        smem += (size_t)k * (k + 4) * sizeof(double);
     } else {
         gscr = scr.take<double>((int64_t)k * k + 2 * k);
         smem = 0;
     }
     static bool attr_set = false;
     if (!attr_set) {
-        allow_max_dynamic_smem(chol_rinv_kernel);
+        allow_max_dynamic_smem(chol_factor_kernel);
+        allow_max_dynamic_smem(trsm_apply_kernel);
         attr_set = true;
     }
-    LAUNCH(chol_rinv_kernel, 1, kCholThreads, smem, st, G, k, ldg, Rinv, ldr, stats, d_err, err_bit, gscr,
+    LAUNCH(chol_factor_kernel, 1, kCholThreads, smem, st, G, k, ldg, R, dinv8, T, ldt, stats, d_err, err_bit, gscr,
            use_smem ? 1 : 0, polar ? 1 : 0);
+}
+
+void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const double* dinv8, double* X, int ldx,
+                const double* stats, cudaStream_t st) {
+    if (m <= 0 || k <= 0) return;
+    const int kp = (k + 7) / 8 * 8;
+    if (kp > 512) throw invalid_argument("trsm_apply: k > 512 unsupported");
+    ProfScope prof("trsm", st);
+    const size_t rs = kp <= kTrsmSmemK ? (size_t)kp * (kp + 4) : 0;
+    const size_t smem = (rs + (size_t)kp * 12 + (size_t)kTrsmRows * (kp + 4)) * sizeof(double);
+    LAUNCH(trsm_apply_kernel, ceil_div(m, kTrsmRows), 128, smem, st, Y, m, k, ld, R, dinv8, X, ldx, stats);
 }
 
 }  // namespace sfdg

@@ -110,7 +110,9 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int nchun
 
 __global__ void __launch_bounds__(128) gemm_nn_kernel(const double* __restrict__ X, int n, int k, int ldx,
                                                       const double* __restrict__ S, int c, int lds,
-                                                      double* __restrict__ C, int ldc) {
+                                                      double* __restrict__ C, int ldc,
+                                                      const double* __restrict__ pred) {
+    if (pred && *pred == 0.0) return;
     __shared__ double Xs[TB][LDK];
     __shared__ double Ss[KT][LDT];
     const int r0 = blockIdx.x * TB, c0 = blockIdx.y * TB;
@@ -243,14 +245,14 @@ void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scrat
 }
 
 void gemm_nn(const double* X, int n, int k, int ldx, const double* S, int c, int lds, double* C, int ldc,
-             cudaStream_t st) {
+             cudaStream_t st, const double* pred) {
     if (n <= 0 || c <= 0) return;
     if (k <= 0) {
         fill2d(C, n, c, ldc, 0.0, st);
         return;
     }
     ProfScope prof("gemm", st);
-    LAUNCH(gemm_nn_kernel, dim3(ceil_div(n, TB), ceil_div(c, TB)), 128, 0, st, X, n, k, ldx, S, c, lds, C, ldc);
+    LAUNCH(gemm_nn_kernel, dim3(ceil_div(n, TB), ceil_div(c, TB)), 128, 0, st, X, n, k, ldx, S, c, lds, C, ldc, pred);
 }
 
 void sumsq(const double* X, int64_t rows, int cols, int ld, double* d_out, int* d_err, int err_bit, Scratch& scr,

@@ -12,8 +12,9 @@ namespace sfdg {
 // out (k x k, ldo) = X^T X, X: n x k row-major (ldx). Deterministic.
 void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scratch& scr, cudaStream_t st);
 // C (n x c, ldc) = X (n x k, ldx) * S (k x c, lds). C must not alias X or S.
+// pred (optional, device): the kernel only runs when *pred != 0.
 void gemm_nn(const double* X, int n, int k, int ldx, const double* S, int c, int lds, double* C, int ldc,
-             cudaStream_t st);
+             cudaStream_t st, const double* pred = nullptr);
 // *d_out = sum of squares of X (rows x cols, ld); sets err_bit in *d_err on non-finite.
 void sumsq(const double* X, int64_t rows, int cols, int ld, double* d_out, int* d_err, int err_bit, Scratch& scr,
            cudaStream_t st);
@@ -21,14 +22,17 @@ void transpose(const double* in, int rows, int cols, int ldi, double* out, int l
 void copy2d(const double* in, int rows, int cols, int ldi, double* out, int ldo, cudaStream_t st);
 void fill2d(double* out, int rows, int cols, int ldo, double v, cudaStream_t st);
 
-// CholeskyQR factor step (chol.cu): from the Gram G (k x k) of a tall Y, the upper
-// triangular Rinv with Y Rinv orthonormal; columns whose residual pivot falls below
-// the drop rule are zeroed (la_core.cpp:141,157-162). stats[0] = min relative pivot
-// of the kept columns, stats[1] = number of dropped columns, stats[2] = max|G - I|.
-// polar = true (second CholeskyQR pass): T = I - (G - I)/2 when max|G - I| <= 1e-6,
-// otherwise the full Cholesky path.
-void chol_rinv(const double* G, int k, int ldg, double* Rinv, int ldr, double* stats, int* d_err, int err_bit,
-               Scratch& scr, cudaStream_t st, bool polar = false);
+// CholeskyQR (chol.cu). chol_factor: from the Gram G (k x k) of a tall Y, the upper
+// Cholesky factor R (k x k) and the inverses of its 8 x 8 diagonal blocks (dinv8, k x 8);
+// columns whose residual pivot falls below the drop rule get a zero row in R and a zero
+// column in dinv8 (la_core.cpp:141,157-162). stats (5 doubles): [0] min relative pivot,
+// [1] dropped columns, [2] max|G - I|, [3] max R_jj / min R_jj, [4] polar path taken.
+// polar = true (second pass): T = I - (G - I)/2 into T (k x k, ldt) when max|G - I| <=
+// 1e-6, else the Cholesky path. trsm_apply: X = Y R^-1 (skipped when stats[4] != 0).
+void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, double* T, int ldt, double* stats,
+                 int* d_err, int err_bit, Scratch& scr, cudaStream_t st, bool polar);
+void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const double* dinv8, double* X, int ldx,
+                const double* stats, cudaStream_t st);
 
 // Symmetric eigensolver (eigh.cu), the jacobi_eigh contract (la_core.cpp:24-80):
 // values descending (n), vectors column k (n x n, ldv). off_tol is absolute, or, when

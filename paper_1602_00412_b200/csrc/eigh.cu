@@ -30,7 +30,6 @@ namespace {
 constexpr int kJacThreads = 1024;
 constexpr int kMaxSweeps = 100;  // la_core.cpp:31
 constexpr int kPackedSmemMax = 232;
-constexpr int kRowsPerAcc = kJacThreads / 32;
 
 __device__ __forceinline__ int pidx(int i, int j) {  // packed upper, i <= j
     return j * (j + 1) / 2 + i;
@@ -73,53 +72,13 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(JacArgs a) {
     const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const int N = a.N, P = N / 2, n = a.n;
 
-    if (blockIdx.x > 0) {
-        // ---------------- accumulator CTA: rows of V
-        const int row = (blockIdx.x - 1) * kRowsPerAcc + warp;
-        double* v = sm + (size_t)warp * N;
-        for (int j = lane; j < N; j += 32) v[j] = (j == row) ? 1.0 : 0.0;
-        __syncwarp();
-        volatile int* prog = a.progress;
-        int r = 0;
-        for (;;) {
-            int avail = prog[0];
-            const int done = prog[1];
-            if (r >= avail) {
-                if (done) {
-                    avail = prog[0];
-                    if (r >= avail) break;
-                } else {
-                    __nanosleep(64);
-                    continue;
-                }
-            }
-            __threadfence();
-            for (; r < avail; ++r) {
-                if (row < N) {
-                    const int rr = r % (N - 1);
-                    const double2* lg = a.rotlog + (size_t)r * P;
-                    for (int k = lane; k < P; k += 32) {
-                        const double2 cs = __ldcg(lg + k);
-                        if (cs.y == 0.0) continue;
-                        int p, q;
-                        pair_of(rr, k, N, p, q);
-                        const double vp = v[p], vq = v[q];
-                        v[p] = cs.x * vp - cs.y * vq;
-                        v[q] = cs.y * vp + cs.x * vq;
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        if (row < N)
-            for (int j = lane; j < N; j += 32) a.V[(size_t)row * N + j] = v[j];
-        return;
-    }
-
     // ---------------- rotator CTA
     double* A = a.use_smem ? sm : a.gpacked;
     __shared__ double2 cs[512];
     __shared__ int pp[512], qq[512];
+    __shared__ int tri[1024];  // tri[j] = j (j + 1) / 2: packed column offsets
+    const int nblk = P * (P + 1) / 2;
+    for (int j = tid; j < N; j += nt) tri[j] = j * (j + 1) / 2;
     __shared__ double red[32];
     __shared__ int s_go;
     double tol_sq = a.tol_sq;
@@ -173,60 +132,96 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(JacArgs a) {
                 }
                 cs[k] = make_double2(c, s);
                 a.rotlog[(size_t)rounds * P + k] = make_double2(c, s);
-                __threadfence();  // log visible device-wide before the round is published
             }
             __syncthreads();
-            // block rows K in snake order over warps; lanes sweep L >= K
-            const int kend = ((P + nw - 1) / nw) * nw;
-            for (int qk = warp; qk < kend; qk += nw) {
-                const int rnd = qk / nw, pos = qk % nw;
-                const int Kb = (rnd & 1) ? rnd * nw + (nw - 1 - pos) : qk;
-                if (Kb >= P) continue;
-                const double2 rk = cs[Kb];
+            // all P(P+1)/2 independent 2x2 blocks (K <= L), one per thread in turn
+            for (int bidx = tid; bidx < nblk; bidx += nt) {
+                // linear upper-triangle index -> (Kb, Lb): row Kb holds P - Kb blocks
+                int Kb = (int)floorf((2.0f * P + 1.0f - sqrtf((2.0f * P + 1.0f) * (2.0f * P + 1.0f) - 8.0f * bidx)) * 0.5f);
+                while (Kb > 0 && Kb * P - Kb * (Kb - 1) / 2 > bidx) --Kb;
+                while ((Kb + 1) * P - (Kb + 1) * Kb / 2 <= bidx) ++Kb;
+                const int Lb = Kb + (bidx - (Kb * P - Kb * (Kb - 1) / 2));
+                const double2 rk = cs[Kb], rl = cs[Lb];
+                if (rk.y == 0.0 && rl.y == 0.0) continue;  // identity on both sides
                 const int pK = pp[Kb], qK = qq[Kb];
-                for (int Lb = Kb + lane; Lb < P; Lb += 32) {
-                    const double2 rl = cs[Lb];
-                    if (rk.y == 0.0 && rl.y == 0.0) continue;
-                    if (Lb == Kb) {
-                        double& app = A[pidx(pK, pK)];
-                        double& aqq = A[pidx(qK, qK)];
-                        double& apq = A[pidx(pK, qK)];
-                        const double c = rk.x, s = rk.y;
-                        const double y11 = c * app - s * apq, y12 = s * app + c * apq;
-                        const double y21 = c * apq - s * aqq, y22 = s * apq + c * aqq;
-                        app = c * y11 - s * y21;
-                        apq = c * y12 - s * y22;
-                        aqq = s * y12 + c * y22;
-                    } else {
-                        const int pL = pp[Lb], qL = qq[Lb];
-                        double& x11 = at(A, pK, pL);
-                        double& x12 = at(A, pK, qL);
-                        double& x21 = at(A, qK, pL);
-                        double& x22 = at(A, qK, qL);
-                        const double cl = rl.x, sl = rl.y, ck = rk.x, sk = rk.y;
-                        const double y11 = cl * x11 - sl * x12, y12 = sl * x11 + cl * x12;
-                        const double y21 = cl * x21 - sl * x22, y22 = sl * x21 + cl * x22;
-                        x11 = ck * y11 - sk * y21;
-                        x21 = sk * y11 + ck * y21;
-                        x12 = ck * y12 - sk * y22;
-                        x22 = sk * y12 + ck * y22;
-                    }
+                if (Lb == Kb) {
+                    double* app = A + tri[pK] + pK;
+                    double* aqq = A + tri[qK] + qK;
+                    double* apq = A + tri[qK] + pK;
+                    const double c = rk.x, s = rk.y;
+                    const double y11 = c * *app - s * *apq, y12 = s * *app + c * *apq;
+                    const double y21 = c * *apq - s * *aqq, y22 = s * *apq + c * *aqq;
+                    *app = c * y11 - s * y21;
+                    *apq = c * y12 - s * y22;
+                    *aqq = s * y12 + c * y22;
+                } else {
+                    const int pL = pp[Lb], qL = qq[Lb];
+                    double* p11 = A + (pK <= pL ? tri[pL] + pK : tri[pK] + pL);
+                    double* p12 = A + (pK <= qL ? tri[qL] + pK : tri[pK] + qL);
+                    double* p21 = A + (qK <= pL ? tri[pL] + qK : tri[qK] + pL);
+                    double* p22 = A + (qK <= qL ? tri[qL] + qK : tri[qK] + qL);
+                    const double x11 = *p11, x12 = *p12, x21 = *p21, x22 = *p22;
+                    const double cl = rl.x, sl = rl.y, ck = rk.x, sk = rk.y;
+                    const double y11 = cl * x11 - sl * x12, y12 = sl * x11 + cl * x12;
+                    const double y21 = cl * x21 - sl * x22, y22 = sl * x21 + cl * x22;
+                    *p11 = ck * y11 - sk * y21;
+                    *p21 = sk * y11 + ck * y21;
+                    *p12 = ck * y12 - sk * y22;
+                    *p22 = sk * y12 + ck * y22;
                 }
             }
             ++rounds;
             __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                atomicExch(a.progress, rounds);  // publish this round to the accumulators
-            }
         }
     }
     for (int i = tid; i < N; i += nt) a.diag[i] = A[pidx(i, i)];
-    if (tid == 0) {
-        __threadfence();
-        atomicExch(a.progress, rounds);
-        atomicExch(a.progress + 1, 1);
+    if (tid == 0) *a.progress = rounds;
+}
+
+// V = I J_1 J_2 ... J_R. Each warp owns one row of V in shared memory (rows evolve
+// independently); the CTA stages kChunk rounds of (c, s) from the log into shared memory
+// with one coalesced pass, then every warp applies them to its row.
+constexpr int kVRows = 16;
+constexpr int kChunk = 8;
+__global__ void __launch_bounds__(kVRows * 32) vapply_kernel(int n, int N, const double2* __restrict__ rotlog,
+                                                             const int* __restrict__ nrounds, double* __restrict__ V) {
+    extern __shared__ double sm[];
+    const int P = N / 2;
+    double2* cs = reinterpret_cast<double2*>(sm);            // kChunk x P
+    short2* pq = reinterpret_cast<short2*>(cs + kChunk * P);  // kChunk x P
+    double* rows = reinterpret_cast<double*>(pq + kChunk * P + 2);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int row = blockIdx.x * kVRows + w;
+    double* v = rows + (size_t)w * N;
+    for (int j = lane; j < N; j += 32) v[j] = (j == row) ? 1.0 : 0.0;
+    const int R = *nrounds;
+    for (int r0 = 0; r0 < R; r0 += kChunk) {
+        const int rc = min(kChunk, R - r0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < rc * P; e += blockDim.x) {
+            const int rr = e / P, k = e % P;
+            cs[e] = __ldg(rotlog + (size_t)(r0 + rr) * P + k);
+            int p, q;
+            pair_of((r0 + rr) % (N - 1), k, N, p, q);
+            pq[e] = make_short2((short)p, (short)q);
+        }
+        __syncthreads();
+        if (row < N) {
+            for (int rr = 0; rr < rc; ++rr) {
+                for (int k = lane; k < P; k += 32) {
+                    const double2 c = cs[rr * P + k];
+                    if (c.y == 0.0) continue;
+                    const short2 ij = pq[rr * P + k];
+                    const double vp = v[ij.x], vq = v[ij.y];
+                    v[ij.x] = c.x * vp - c.y * vq;
+                    v[ij.y] = c.y * vp + c.x * vq;
+                }
+                __syncwarp();
+            }
+        }
     }
+    if (row < N)
+        for (int j = lane; j < N; j += 32) V[(size_t)row * N + j] = v[j];
 }
 
 // Stable descending sort of eigenpairs (la_core.cpp:67-78); V (N x N) -> out (n x n).
@@ -278,17 +273,18 @@ void eigh(const double* K, int n, int ldk, double off_tol, const double* d_fsq, 
     static bool attr = false;
     if (!attr) {
         allow_max_dynamic_smem(jacobi_kernel);
+        allow_max_dynamic_smem(vapply_kernel);
         attr = true;
     }
-    const size_t smem = std::max(use_smem ? packed * sizeof(double) : 0, (size_t)kRowsPerAcc * N * sizeof(double));
-    const int nacc = (N + kRowsPerAcc - 1) / kRowsPerAcc;
-    CK(cudaMemsetAsync(a.progress, 0, 2 * sizeof(int), st));
+    const size_t smem = use_smem ? packed * sizeof(double) : 0;
+    const size_t vsmem = (size_t)kChunk * P * (sizeof(double2) + sizeof(short2)) + 8 + (size_t)kVRows * N * sizeof(double);
     {
-        ProfScope prof("eigh", st);
-        void* params[] = {(void*)&a};
-        CK(cudaLaunchCooperativeKernel((const void*)jacobi_kernel, dim3(1 + nacc), dim3(kJacThreads), params, smem,
-                                       st));
-        g_launches.fetch_add(1, std::memory_order_relaxed);
+        ProfScope prof("eigh_jacobi", st);
+        LAUNCH(jacobi_kernel, 1, kJacThreads, smem, st, a);
+    }
+    {
+        ProfScope prof("eigh_vectors", st);
+        LAUNCH(vapply_kernel, ceil_div(N, kVRows), kVRows * 32, vsmem, st, n, N, a.rotlog, a.progress, a.V);
         LAUNCH(sort_kernel, 1, 1024, 0, st, n, N, a.diag, a.V, values, vectors, ldv);
     }
 }

@@ -141,6 +141,8 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     const int kmax = std::max(2 * lp, 8);
     CK(cudaMalloc(&gram, (size_t)kmax * kmax * sizeof(double)));
     CK(cudaMalloc(&rinv, (size_t)lp * lp * sizeof(double)));
+    CK(cudaMalloc(&rfac, (size_t)lp * lp * sizeof(double)));
+    CK(cudaMalloc(&dinv8, (size_t)lp * 8 * sizeof(double)));
     CK(cudaMalloc(&kc, (size_t)kmax * kmax * sizeof(double)));
     CK(cudaMalloc(&evals, (size_t)kmax * sizeof(double)));
     CK(cudaMalloc(&evecs, (size_t)kmax * kmax * sizeof(double)));
@@ -155,8 +157,9 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     CK(cudaMalloc(&bar, 2 * sizeof(unsigned)));
     CK(cudaMalloc(&d_err, 4 * sizeof(int)));
     CK(cudaMemsetAsync(d_err, 0, 4 * sizeof(int), st));
-    CK(cudaMalloc(&d_scal, 16 * sizeof(double)));
-    CK(cudaHostAlloc(&h_scal, 16 * sizeof(double), cudaHostAllocDefault));
+    CK(cudaMalloc(&d_scal, 64 * sizeof(double)));
+    CK(cudaMemsetAsync(d_scal, 0, 64 * sizeof(double), st));
+    CK(cudaHostAlloc(&h_scal, 64 * sizeof(double), cudaHostAllocDefault));
     CK(cudaHostAlloc(&h_err, 4 * sizeof(int), cudaHostAllocDefault));
     CK(cudaStreamSynchronize(st));
 }
@@ -164,7 +167,8 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
 Engine::~Engine() {
     cudaSetDevice(device);
     if (st) cudaStreamSynchronize(st);
-    for (void* p : {(void*)Y, (void*)Yt, (void*)W, (void*)Mt[0], (void*)Mt[1], (void*)gram, (void*)rinv, (void*)kc,
+    for (void* p : {(void*)Y, (void*)Yt, (void*)W, (void*)Mt[0], (void*)Mt[1], (void*)gram, (void*)rinv, (void*)rfac,
+                    (void*)dinv8, (void*)kc,
                     (void*)evals, (void*)evecs, (void*)S, (void*)x0, (void*)ybuf, (void*)u, (void*)tpart, (void*)tvec,
                     (void*)vpart, (void*)vout, (void*)bar, (void*)d_err, (void*)d_scal})
         if (p) cudaFree(p);
@@ -236,14 +240,17 @@ void Engine::prepare() {
 }
 
 void Engine::orthonormalize(double* Yp, int m, int err_bit) {
-    // Two CholeskyQR passes: Yp -> Yt -> Yp.
-    double* stats = d_scal + 8;
+    // CholeskyQR2: pass 1 Cholesky + blocked forward substitution (Yp -> Yt); pass 2 the
+    // polar correction T = I - E/2 (or Cholesky again if Yt is not yet orthonormal enough).
+    double* st1 = d_scal + 16;
+    double* st2 = d_scal + 24;
     gram_tn(Yp, m, lp, lp, gram, lp, scr, st);
-    chol_rinv(gram, lp, lp, rinv, lp, stats, d_err, err_bit, scr, st);
-    gemm_nn(Yp, m, lp, lp, rinv, lp, lp, Yt, lp, st);
+    chol_factor(gram, lp, lp, rfac, dinv8, nullptr, 0, st1, d_err, err_bit, scr, st, false);
+    trsm_apply(Yp, m, lp, lp, rfac, dinv8, Yt, lp, nullptr, st);
     gram_tn(Yt, m, lp, lp, gram, lp, scr, st);
-    chol_rinv(gram, lp, lp, rinv, lp, stats, d_err, err_bit, scr, st, /*polar=*/true);
-    gemm_nn(Yt, m, lp, lp, rinv, lp, lp, Yp, lp, st);
+    chol_factor(gram, lp, lp, rfac, dinv8, rinv, lp, st2, d_err, err_bit, scr, st, true);
+    trsm_apply(Yt, m, lp, lp, rfac, dinv8, Yp, lp, st2, st);
+    gemm_nn(Yt, m, lp, lp, rinv, lp, lp, Yp, lp, st, st2 + 4);
 }
 
 void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {

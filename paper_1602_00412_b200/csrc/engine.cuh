@@ -53,7 +53,7 @@ class Engine {
     double *Y = nullptr, *Yt = nullptr, *W = nullptr;  // m_cap x lp, m_cap x lp, d x lp
     double* Mt[2] = {nullptr, nullptr};                 // d x 2lp : [B^T | B'^T]
     int cur = 0;
-    double *gram = nullptr, *rinv = nullptr, *kc = nullptr, *evals = nullptr, *evecs = nullptr, *S = nullptr;
+    double *gram = nullptr, *rinv = nullptr, *rfac = nullptr, *dinv8 = nullptr, *kc = nullptr, *evals = nullptr, *evecs = nullptr, *S = nullptr;
     double *x0 = nullptr, *ybuf = nullptr, *u = nullptr, *tpart = nullptr, *tvec = nullptr, *vpart = nullptr;
     double* vout = nullptr;
     unsigned* bar = nullptr;
