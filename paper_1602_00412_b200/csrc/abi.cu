@@ -139,6 +139,8 @@ class Sketcher {
 
     void finalize(double* out) {  // sketch.cpp:34-45
         eng->set_device();
+        eng->sync();
+        eng->check_errors();
         if (buf_rows() > 0) {
             if (buf_rows() >= cfg.ell) {
                 flush();
@@ -159,18 +161,23 @@ class Sketcher {
 
     void get_sketch(double* out) {
         eng->set_device();
+        eng->sync();
+        eng->check_errors();
         eng->scr.reset();
         eng->sketch_to_host(out);
     }
 
     void get_sketch_device(double* d_out, size_t ld) {
         eng->set_device();
+        eng->sync();
+        eng->check_errors();
         copy2d(eng->Mt[eng->cur], (int)cfg.d, (int)cfg.ell, 2 * eng->lp, d_out, (int)ld, eng->st);
         eng->sync();
     }
 
     void stats(sfdg_stats* s) {
         eng->set_device();
+        eng->sync();
         s->flush_count = flushes;
         s->attempt_total = attempts;
         s->verifier = {ver.i, ver.delta, ver.c_verify, ver.delta_spent};
@@ -278,11 +285,18 @@ class Sketcher {
         eng->scr.reset();
         upload_row_ptr();
         eng->prepare();
+        // B'_f goes into the right half of Mt[cur]: first wait for the shrink that last read it
+        CK(cudaStreamWaitEvent(eng->st, eng->ev_read_done[eng->cur], 0));
         double delta_hat = 0.0;
         const size_t att = eng->boosted(ver, cfg.power, buf_frob, &delta_hat);
+        // B = dense_shrink([B; B']) on the shrink stream: it overlaps the next flush's power
+        // iteration. Errors it raises (Jacobi non-convergence) surface at the next sync point.
+        CK(cudaEventRecord(eng->ev_bprime, eng->st));
+        CK(cudaStreamWaitEvent(eng->st2, eng->ev_bprime, 0));
+        eng->scr2.reset();
         eng->dense_shrink_stack(eng->Mt[eng->cur], 2 * eng->lp, (int)cfg.ell, eng->lp, (int)cfg.ell,
-                                eng->Mt[eng->cur ^ 1], 2 * eng->lp);
-        eng->check_errors();  // a failed dense_shrink leaves B and the buffer untouched
+                                eng->Mt[eng->cur ^ 1], 2 * eng->lp, /*side=*/true);
+        CK(cudaEventRecord(eng->ev_read_done[eng->cur], eng->st2));
         eng->cur ^= 1;
         clear_buffer();
         flushes += 1;

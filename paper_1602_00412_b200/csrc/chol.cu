@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kCholThreads) chol_factor_kernel(const double*
             stats[0] = 0.0;
             stats[3] = 1e300;
             stats[4] = 0.0;
+            stats[5] = 1e300;
         }
         return;
     }
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(kCholThreads) chol_factor_kernel(const double*
         stats[2] = s_emax;
         stats[3] = rmin > 0.0 && rmin < 1e300 ? rmax / rmin : 1.0;
         stats[4] = 0.0;
+        stats[5] = fmax(stats[5], stats[3]);  // running max over the calls sharing `stats`
     }
 }
 

@@ -17,6 +17,7 @@
 // in one d x 2lp buffer so [B; B'] never has to be materialised for dense_shrink.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -125,8 +126,12 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     : device(device_), d(d_), ell(ell_) {
     if (ell < 1 || ell > kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 256] for this build");
     lp = (int)round_up((size_t)ell, 8);
+    if (const char* e = std::getenv("SFDG_ORTH_EVERY_SWEEP")) adaptive = std::atoi(e) == 0;
     set_device();
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&ev_read_done[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_bprime, cudaEventDisableTiming));
     // the ring holds >= 3 attempts' worth of draws (G: d*ell, x: d)
     const uint64_t per_attempt = 2 * ((uint64_t)d * ell + d) + 8;
     rng.init(seed, std::max<uint64_t>(3 * per_attempt, 1 << 20), device);
@@ -177,8 +182,14 @@ Engine::~Engine() {
     a.release();
     plan_r.release();
     plan_c.release();
+    if (st2) cudaStreamSynchronize(st2);
     scr.release();
+    scr2.release();
     rng.release();
+    for (int i = 0; i < 2; ++i)
+        if (ev_read_done[i]) cudaEventDestroy(ev_read_done[i]);
+    if (ev_bprime) cudaEventDestroy(ev_bprime);
+    if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
 }
 
@@ -195,7 +206,10 @@ void Engine::ensure_rows(int m) {
     CK(cudaMalloc(&u, (size_t)m_cap * sizeof(double)));
 }
 
-void Engine::sync() { CK(cudaStreamSynchronize(st)); }
+void Engine::sync() {
+    CK(cudaStreamSynchronize(st2));
+    CK(cudaStreamSynchronize(st));
+}
 
 double Engine::read_scalar(const double* dptr) {
     CK(cudaMemcpyAsync(h_scal, dptr, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -262,10 +276,20 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     rng.normals(pos, (uint64_t)d * k, (uint64_t)k, (uint64_t)lp, W, d_err, st);
     spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
     orthonormalize(Y, m, ERR_NONFINITE_ITER);
+    // Only span(Y) matters for B' (it enters through Z Z^T), so CholeskyQR2 runs every
+    // `interval` sweeps (adaptive, see boosted()) and always after the last sweep; in
+    // between Y <- A'(A'^T Y) unnormalised. interval = 1 is the reference's schedule
+    // (randsvd.cpp:38-49).
+    const int interval = adaptive ? orth_interval : 1;
+    int since = 0;
     for (size_t s = 0; s < q; ++s) {
         spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st);
         spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
-        orthonormalize(Y, m, ERR_NONFINITE_ITER);
+        if (++since >= interval || s + 1 == q) {
+            orthonormalize(Y, m, ERR_NONFINITE_ITER);
+            last_since = since;
+            since = 0;
+        }
     }
 }
 
@@ -327,12 +351,35 @@ size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* d
     double* bpt = Mt[cur] + lp;  // right half of [B^T | B'^T]
     const int ldb = 2 * lp;
     for (size_t attempt = 1; attempt <= kRetryCap; ++attempt) {
+        const RngPos pos0 = pos;
+        const int interval_used = adaptive ? orth_interval : 1;
+        last_since = 1;
+        CK(cudaMemsetAsync(d_scal + 16, 0, 16 * sizeof(double), st));  // pass-1 stats incl. running max kappa
         sparse_shrink(cfg, bpt, ldb);
         double* bfsq = d_scal + 1;
         sumsq(bpt, d, ell, ldb, bfsq, nullptr, 0, scr, st);
         // prefetch the next attempt's draws while we wait (side stream)
         rng.prefetch(pos.words + 2 * ((uint64_t)d * ell + 2 * d) + 8);
-        const double b_fsq = read_scalar(bfsq);
+        CK(cudaMemcpyAsync(h_scal + 1, bfsq, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h_scal + 16, d_scal + 16, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double b_fsq = h_scal[1];
+        const double kappa_last = h_scal[16 + 3], kappa_max = h_scal[16 + 5];
+        if (interval_used > 1 && (kappa_max > kKappaUnsafe || (h_err[0] & ERR_NONFINITE_ITER))) {
+            // the skipped-orthonormalisation schedule lost too much conditioning: redo this
+            // attempt from the same draws with the reference's every-sweep schedule
+            CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+            pos = pos0;
+            orth_interval = 1;
+            --attempt;
+            continue;
+        }
+        if (adaptive && kappa_last >= 1.0) {  // per-sweep growth of cond(Y) -> next interval
+            const double g = std::pow(std::max(kappa_last, 1.0), 1.0 / std::max(last_since, 1));
+            int iv = g <= 1.001 ? kMaxInterval : (int)std::floor(std::log(kKappaTarget) / std::log(g));
+            orth_interval = std::max(1, std::min(kMaxInterval, iv));
+        }
         check_errors();
         const double drop = a_fsq - b_fsq;  // shrink.cpp:112-113
         const double delta_hat = drop / (kAlpha * static_cast<double>(ell));
@@ -348,41 +395,44 @@ size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* d
     throw numerical_error("boosted_sparse_shrink: retry cap exceeded");
 }
 
-void Engine::dense_shrink_stack(const double* Xt, int ldx, int n1, int off, int n2, double* bt_out, int ldo) {
+void Engine::dense_shrink_stack(const double* Xt, int ldx, int n1, int off, int n2, double* bt_out, int ldo,
+                                bool side) {
+    cudaStream_t ss = side ? st2 : st;
+    Scratch& sc = side ? scr2 : scr;
     const int R = n1 + n2;
     const int kcols = off + n2;
     if (ell < 1 || ell > R) throw invalid_argument("dense_shrink: ell out of range");
-    double* fsq = d_scal + 2;
+    double* fsq = d_scal + (side ? 4 : 2);
     if (R <= d) {
         // short-fat: Gram of the stacked rows = Xt^T Xt restricted to the stack's columns
         if (R > 1024) throw invalid_argument("dense_shrink: more than 1024 stacked rows unsupported");
-        double* K = scr.take<double>((int64_t)kcols * kcols);
-        double* Kc = scr.take<double>((int64_t)R * R);
-        double* ev = scr.take<double>(R);
-        double* U = scr.take<double>((int64_t)R * R);
-        double* Sx = scr.take<double>((int64_t)kcols * lp);
-        gram_tn(Xt, d, kcols, ldx, K, kcols, scr, st);
-        LAUNCH(compact_kernel, 1, 1024, 0, st, K, kcols, n1, off, R, Kc, fsq);
-        eigh(Kc, R, R, 0.0, fsq, ev, U, R, d_err, scr, st);
-        LAUNCH(shrink_weights_kernel, 1, 1024, 0, st, ev, U, R, ell, n1, off, Sx, kcols, lp);
-        gemm_nn(Xt, d, kcols, ldx, Sx, lp, lp, bt_out, ldo, st);
+        double* K = sc.take<double>((int64_t)kcols * kcols);
+        double* Kc = sc.take<double>((int64_t)R * R);
+        double* ev = sc.take<double>(R);
+        double* U = sc.take<double>((int64_t)R * R);
+        double* Sx = sc.take<double>((int64_t)kcols * lp);
+        gram_tn(Xt, d, kcols, ldx, K, kcols, sc, ss);
+        LAUNCH(compact_kernel, 1, 1024, 0, ss, K, kcols, n1, off, R, Kc, fsq);
+        eigh(Kc, R, R, 0.0, fsq, ev, U, R, d_err, sc, ss);
+        LAUNCH(shrink_weights_kernel, 1, 1024, 0, ss, ev, U, R, ell, n1, off, Sx, kcols, lp);
+        gemm_nn(Xt, d, kcols, ldx, Sx, lp, lp, bt_out, ldo, ss);
     } else {
         // tall: eigendecompose the d x d Gram A^T A (shrink.cpp:39-60)
         if (ell > d) throw invalid_argument("dense_shrink: ell exceeds column count");
-        double* X = scr.take<double>((int64_t)R * d);
-        double* Xc = scr.take<double>((int64_t)d * R);
+        double* X = sc.take<double>((int64_t)R * d);
+        double* Xc = sc.take<double>((int64_t)d * R);
         // gather the stack's columns contiguously, then transpose to rows
-        copy2d(Xt, d, n1, ldx, Xc, R, st);
-        if (n2 > 0) copy2d(Xt + off, d, n2, ldx, Xc + n1, R, st);
-        transpose(Xc, d, R, R, X, d, st);
-        double* K = scr.take<double>((int64_t)d * d);
-        double* Kc = scr.take<double>((int64_t)d * d);
-        double* ev = scr.take<double>(d);
-        double* V = scr.take<double>((int64_t)d * d);
-        gram_tn(X, R, d, d, K, d, scr, st);
-        LAUNCH(compact_kernel, 1, 1024, 0, st, K, d, d, d, d, Kc, fsq);
-        eigh(Kc, d, d, 0.0, fsq, ev, V, d, d_err, scr, st);
-        LAUNCH(tall_shrink_kernel, std::max(1u, std::min(4u * kSMs, ceil_div((size_t)d * lp, 256))), 256, 0, st, ev, V,
+        copy2d(Xt, d, n1, ldx, Xc, R, ss);
+        if (n2 > 0) copy2d(Xt + off, d, n2, ldx, Xc + n1, R, ss);
+        transpose(Xc, d, R, R, X, d, ss);
+        double* K = sc.take<double>((int64_t)d * d);
+        double* Kc = sc.take<double>((int64_t)d * d);
+        double* ev = sc.take<double>(d);
+        double* V = sc.take<double>((int64_t)d * d);
+        gram_tn(X, R, d, d, K, d, sc, ss);
+        LAUNCH(compact_kernel, 1, 1024, 0, ss, K, d, d, d, d, Kc, fsq);
+        eigh(Kc, d, d, 0.0, fsq, ev, V, d, d_err, sc, ss);
+        LAUNCH(tall_shrink_kernel, std::max(1u, std::min(4u * kSMs, ceil_div((size_t)d * lp, 256))), 256, 0, ss, ev, V,
                d, ell, bt_out, ldo, lp);
     }
 }

@@ -17,6 +17,9 @@ namespace sfdg {
 constexpr double kAlpha = 6.0 / 41.0;  // core/include/sfd/common.hpp:10
 constexpr size_t kRetryCap = 64;       // core/src/shrink.cpp:12
 constexpr int kMaxEll = 256;           // 2*ell <= 512 fits every kernel's tile plan
+constexpr double kKappaTarget = 1e4;   // cond(Y) allowed to build up between CholeskyQR2 passes
+constexpr double kKappaUnsafe = 1e7;   // above this CholeskyQR2 may lose orthogonality: redo
+constexpr int kMaxInterval = 8;
 
 struct PowerCfg {  // randsvd.hpp:10-14
     double epsilon = 0.25;
@@ -44,6 +47,12 @@ class Engine {
     int device, d, ell, lp;
     cudaStream_t st = nullptr;
     Scratch scr;
+    // dense_shrink of flush f runs on st2 while flush f+1's power iteration runs on st:
+    // ev_read_done[i] = the shrink that reads Mt[i] finished; ev_bprime = B' of this flush ready
+    cudaStream_t st2 = nullptr;
+    Scratch scr2;
+    cudaEvent_t ev_read_done[2] = {nullptr, nullptr};
+    cudaEvent_t ev_bprime = nullptr;
     RngStream rng;
     RngPos pos;
     DevCsr a;
@@ -62,6 +71,10 @@ class Engine {
     double* h_scal = nullptr;  // pinned mirror
     int* h_err = nullptr;
     int verify_blocks = 0;
+    // adaptive orthonormalisation schedule (simultaneous_iteration)
+    bool adaptive = true;   // SFDG_ORTH_EVERY_SWEEP=1 forces the reference schedule
+    int orth_interval = 1;  // sweeps per CholeskyQR2
+    int last_since = 1;     // sweeps folded into the last pass-1 factorisation
 
     void set_device() const;
     void ensure_rows(int m);
@@ -81,7 +94,9 @@ class Engine {
     size_t boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* delta_hat_out);
     // dense_shrink (shrink.cpp:30-61) of the row stack whose transpose is Xt (d x kcols, ldx),
     // rows = columns [0, n1) and [off, off + n2) of Xt; writes B^T (d x lp, ldo).
-    void dense_shrink_stack(const double* Xt, int ldx, int n1, int off, int n2, double* bt_out, int ldo);
+    // side = true: on the shrink stream st2 with its own scratch (overlaps the next flush).
+    void dense_shrink_stack(const double* Xt, int ldx, int n1, int off, int n2, double* bt_out, int ldo,
+                            bool side = false);
     // Zero the B'^T half of Mt[cur] and scatter the buffer rows of A' into columns
     // [off, off + m) of Mt[cur] (densify, sparse.cpp:71-78, already transposed).
     void densify_into_stack(int off);

@@ -138,10 +138,12 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
         }
         grid_sync(bar, nb);
         // ---- phase 2: t[j] = sum_b tpart[b][j] in block order
-        for (int j = blockIdx.x * kVThreads + threadIdx.x; j < L; j += nb * kVThreads) {
+        for (int j = (int)blockIdx.x * (kVThreads / 32) + wib; j < L; j += (int)nb * (kVThreads / 32)) {
             double s = 0.0;
-            for (unsigned b = 0; b < nb; ++b) s += __ldcg(a.tpart + (size_t)b * L + j);
-            a.t[j] = s;
+            for (unsigned b = lane; b < nb; b += 32) s += __ldcg(a.tpart + (size_t)b * L + j);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) a.t[j] = s;
         }
         grid_sync(bar, nb);
         for (int j = threadIdx.x; j < L; j += kVThreads) tloc[j] = __ldcg(a.t + j);
@@ -207,7 +209,9 @@ int verify_grid_blocks(int device) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, verify_kernel, kVThreads, 0));
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    const int nb = std::max(1, std::min(per_sm, 1)) * sms;
+    // one block per SM, leaving two SMs for a concurrently running shrink (eigh) CTA so the
+    // cooperative grid never waits for it to drain
+    const int nb = std::max(1, std::min(per_sm, 1) * sms - 2);
     if (device >= 0 && device < 64) cached[device] = nb;
     return nb;
 }
