@@ -38,7 +38,10 @@ void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const do
 // values descending (n), vectors column k (n x n, ldv). off_tol is absolute, or, when
 // d_fsq != nullptr, 1e-12 * max(*d_fsq, 1) read on the device (svd_top's rule,
 // la_core.cpp:103). A non-converged solve after 100 sweeps sets ERR_JACOBI_NOCONV.
+// nval: only the top nval eigenpairs are required (the default n = all). The fast path is
+// eigh_tri.cu (tridiagonal + bisection + inverse iteration); the Jacobi solver runs as a
+// device-predicated fallback or when SFDG_EIGH=jacobi.
 void eigh(const double* K, int n, int ldk, double off_tol, const double* d_fsq, double* values, double* vectors,
-          int ldv, int* d_err, Scratch& scr, cudaStream_t st);
+          int ldv, int* d_err, Scratch& scr, cudaStream_t st, int nval = 0);
 
 }  // namespace sfdg

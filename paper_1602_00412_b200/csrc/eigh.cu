@@ -19,6 +19,8 @@
 //    runs concurrently on other SMs instead of after the sweeps.
 // A final pass sorts eigenpairs (stable, descending; la_core.cpp:67-78).
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "dense.cuh"
@@ -50,7 +52,6 @@ __device__ __forceinline__ void pair_of(int r, int k, int N, int& p, int& q) {
     q = max(a, b);
 }
 
-__device__ __forceinline__ double& at(double* A, int i, int j) { return i <= j ? A[pidx(i, j)] : A[pidx(j, i)]; }
 
 struct JacArgs {
     const double* K;
@@ -64,32 +65,41 @@ struct JacArgs {
     double* diag;
     double* V;  // N x N accumulated rotations (row-major)
     int* err;
+    const int* only_if;  // optional: run only when *only_if != 0 (fallback after eigh_tri)
 };
 
+// Rotator CTA. SMEM: the packed upper triangle lives in shared memory (else L2 scratch).
+// TABLE: the (K, L) block list of a round is precomputed in shared memory (else derived
+// from the linear block index). Per pair k the round keeps {p, q, tri[p], tri[q]} so the
+// packed index of any element of a 2 x 2 block costs one compare and one add.
+template <bool SMEM, bool TABLE>
 __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(JacArgs a) {
+    if (a.only_if && *a.only_if == 0) return;
     extern __shared__ double sm[];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const int N = a.N, P = N / 2, n = a.n;
-
-    // ---------------- rotator CTA
-    double* A = a.use_smem ? sm : a.gpacked;
+    const size_t packed = (size_t)N * (N + 1) / 2;
+    double* A = SMEM ? sm : a.gpacked;
+    uint32_t* kl = reinterpret_cast<uint32_t*>(sm + (SMEM ? packed : 0));  // TABLE only
     __shared__ double2 cs[512];
-    __shared__ int pp[512], qq[512];
-    __shared__ int tri[1024];  // tri[j] = j (j + 1) / 2: packed column offsets
-    const int nblk = P * (P + 1) / 2;
-    for (int j = tid; j < N; j += nt) tri[j] = j * (j + 1) / 2;
+    __shared__ int4 pq[512];  // p, q, tri[p], tri[q]
     __shared__ double red[32];
     __shared__ int s_go;
+    const int nblk = P * (P + 1) / 2;
     double tol_sq = a.tol_sq;
     if (a.d_fsq) {  // svd_top / dense_shrink tolerance 1e-12 * max(|a|_F^2, 1) (la_core.cpp:103, shrink.cpp:53)
         const double off_tol = 1e-12 * fmax(*a.d_fsq, 1.0);
         tol_sq = off_tol * off_tol;
     }
-    for (int e = tid; e < N * N; e += nt) {  // odd n: index n is a zero pad row/column
-        const int i = e / N, j = e % N;
-        if (i <= j) A[pidx(i, j)] = (i < n && j < n) ? a.K[(size_t)i * a.ldk + j] : 0.0;
-    }
+    for (int j = warp; j < N; j += nw)  // odd n: index n is a zero pad row/column
+        for (int i = lane; i <= j; i += 32)
+            A[j * (j + 1) / 2 + i] = (i < n && j < n) ? a.K[(size_t)i * a.ldk + j] : 0.0;
+    if (TABLE)
+        for (int K = warp; K < P; K += nw) {
+            const int base = K * P - K * (K - 1) / 2;
+            for (int L = K + lane; L < P; L += 32) kl[base + (L - K)] = ((uint32_t)K << 16) | (uint32_t)L;
+        }
     __syncthreads();
     int rounds = 0;
     for (int sweep = 0;; ++sweep) {
@@ -97,7 +107,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(JacArgs a) {
         double acc = 0.0;
         for (int j = warp; j < N; j += nw)
             for (int i = lane; i < j; i += 32) {
-                const double x = A[pidx(i, j)];
+                const double x = A[j * (j + 1) / 2 + i];
                 acc += 2.0 * x * x;
             }
 #pragma unroll
@@ -120,12 +130,12 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(JacArgs a) {
             for (int k = tid; k < P; k += nt) {
                 int p, q;
                 pair_of(r, k, N, p, q);
-                pp[k] = p;
-                qq[k] = q;
+                const int tp = p * (p + 1) / 2, tq = q * (q + 1) / 2;
+                pq[k] = make_int4(p, q, tp, tq);
                 double c = 1.0, s = 0.0;
-                const double apq = A[pidx(p, q)];
-                if (apq != 0.0) {
-                    const double theta = (A[pidx(q, q)] - A[pidx(p, p)]) / (2.0 * apq);
+                const double apq = A[tq + p];
+                if (apq != 0.0) {  // la_core.cpp:39-44
+                    const double theta = (A[tq + q] - A[tp + p]) / (2.0 * apq);
                     const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
                     c = 1.0 / sqrt(t * t + 1.0);
                     s = t * c;
@@ -134,32 +144,40 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(JacArgs a) {
                 a.rotlog[(size_t)rounds * P + k] = make_double2(c, s);
             }
             __syncthreads();
-            // all P(P+1)/2 independent 2x2 blocks (K <= L), one per thread in turn
             for (int bidx = tid; bidx < nblk; bidx += nt) {
-                // linear upper-triangle index -> (Kb, Lb): row Kb holds P - Kb blocks
-                int Kb = (int)floorf((2.0f * P + 1.0f - sqrtf((2.0f * P + 1.0f) * (2.0f * P + 1.0f) - 8.0f * bidx)) * 0.5f);
-                while (Kb > 0 && Kb * P - Kb * (Kb - 1) / 2 > bidx) --Kb;
-                while ((Kb + 1) * P - (Kb + 1) * Kb / 2 <= bidx) ++Kb;
-                const int Lb = Kb + (bidx - (Kb * P - Kb * (Kb - 1) / 2));
+                int Kb, Lb;
+                if (TABLE) {
+                    const uint32_t e = kl[bidx];
+                    Kb = (int)(e >> 16);
+                    Lb = (int)(e & 0xffff);
+                } else {
+                    Kb = (int)floorf((2.0f * P + 1.0f - sqrtf((2.0f * P + 1.0f) * (2.0f * P + 1.0f) - 8.0f * bidx)) *
+                                     0.5f);
+                    while (Kb > 0 && Kb * P - Kb * (Kb - 1) / 2 > bidx) --Kb;
+                    while ((Kb + 1) * P - (Kb + 1) * Kb / 2 <= bidx) ++Kb;
+                    Lb = Kb + (bidx - (Kb * P - Kb * (Kb - 1) / 2));
+                }
                 const double2 rk = cs[Kb], rl = cs[Lb];
                 if (rk.y == 0.0 && rl.y == 0.0) continue;  // identity on both sides
-                const int pK = pp[Kb], qK = qq[Kb];
+                const int4 K4 = pq[Kb];
                 if (Lb == Kb) {
-                    double* app = A + tri[pK] + pK;
-                    double* aqq = A + tri[qK] + qK;
-                    double* apq = A + tri[qK] + pK;
+                    double* app = A + K4.z + K4.x;
+                    double* aqq = A + K4.w + K4.y;
+                    double* apq = A + K4.w + K4.x;
                     const double c = rk.x, s = rk.y;
-                    const double y11 = c * *app - s * *apq, y12 = s * *app + c * *apq;
-                    const double y21 = c * *apq - s * *aqq, y22 = s * *apq + c * *aqq;
+                    const double xpp = *app, xqq = *aqq, xpq = *apq;
+                    const double y11 = c * xpp - s * xpq, y12 = s * xpp + c * xpq;
+                    const double y21 = c * xpq - s * xqq, y22 = s * xpq + c * xqq;
                     *app = c * y11 - s * y21;
                     *apq = c * y12 - s * y22;
                     *aqq = s * y12 + c * y22;
                 } else {
-                    const int pL = pp[Lb], qL = qq[Lb];
-                    double* p11 = A + (pK <= pL ? tri[pL] + pK : tri[pK] + pL);
-                    double* p12 = A + (pK <= qL ? tri[qL] + pK : tri[pK] + qL);
-                    double* p21 = A + (qK <= pL ? tri[pL] + qK : tri[qK] + pL);
-                    double* p22 = A + (qK <= qL ? tri[qL] + qK : tri[qK] + qL);
+                    const int4 L4 = pq[Lb];
+                    // element (i, j) of the symmetric matrix: i <= j ? tri[j] + i : tri[i] + j
+                    double* p11 = A + (K4.x <= L4.x ? L4.z + K4.x : K4.z + L4.x);
+                    double* p12 = A + (K4.x <= L4.y ? L4.w + K4.x : K4.z + L4.y);
+                    double* p21 = A + (K4.y <= L4.x ? L4.z + K4.y : K4.w + L4.x);
+                    double* p22 = A + (K4.y <= L4.y ? L4.w + K4.y : K4.w + L4.y);
                     const double x11 = *p11, x12 = *p12, x21 = *p21, x22 = *p22;
                     const double cl = rl.x, sl = rl.y, ck = rk.x, sk = rk.y;
                     const double y11 = cl * x11 - sl * x12, y12 = sl * x11 + cl * x12;
@@ -174,7 +192,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(JacArgs a) {
             __syncthreads();
         }
     }
-    for (int i = tid; i < N; i += nt) a.diag[i] = A[pidx(i, i)];
+    for (int i = tid; i < N; i += nt) a.diag[i] = A[i * (i + 1) / 2 + i];
     if (tid == 0) *a.progress = rounds;
 }
 
@@ -184,7 +202,9 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(JacArgs a) {
 constexpr int kVRows = 16;
 constexpr int kChunk = 8;
 __global__ void __launch_bounds__(kVRows * 32) vapply_kernel(int n, int N, const double2* __restrict__ rotlog,
-                                                             const int* __restrict__ nrounds, double* __restrict__ V) {
+                                                             const int* __restrict__ nrounds, double* __restrict__ V,
+                                                             const int* __restrict__ only_if) {
+    if (only_if && *only_if == 0) return;
     extern __shared__ double sm[];
     const int P = N / 2;
     double2* cs = reinterpret_cast<double2*>(sm);            // kChunk x P
@@ -226,7 +246,9 @@ __global__ void __launch_bounds__(kVRows * 32) vapply_kernel(int n, int N, const
 
 // Stable descending sort of eigenpairs (la_core.cpp:67-78); V (N x N) -> out (n x n).
 __global__ void sort_kernel(int n, int N, const double* __restrict__ diag, const double* __restrict__ V,
-                            double* __restrict__ values, double* __restrict__ out, int ldo) {
+                            double* __restrict__ values, double* __restrict__ out, int ldo,
+                            const int* __restrict__ only_if) {
+    if (only_if && *only_if == 0) return;
     __shared__ int rank[1024];
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double di = diag[i];
@@ -247,10 +269,25 @@ __global__ void sort_kernel(int n, int N, const double* __restrict__ diag, const
 
 }  // namespace
 
+void eigh_tri(const double* K, int n, int ldk, double off_tol, const double* d_fsq, int nval, double* values,
+              double* vectors, int ldv, int* fallback, Scratch& scr, cudaStream_t st);
+
 void eigh(const double* K, int n, int ldk, double off_tol, const double* d_fsq, double* values, double* vectors,
-          int ldv, int* d_err, Scratch& scr, cudaStream_t st) {
+          int ldv, int* d_err, Scratch& scr, cudaStream_t st, int nval) {
     if (n <= 0) return;
     if (n > 1024) throw invalid_argument("eigh: n > 1024 unsupported");
+    if (nval <= 0 || nval > n) nval = n;
+    static const int force_jacobi = [] {
+        const char* e = std::getenv("SFDG_EIGH");
+        return (e && std::string(e) == "jacobi") ? 1 : 0;
+    }();
+    int* fallback = scr.take<int>(1);
+    if (force_jacobi) {
+        CK(cudaMemsetAsync(fallback, 0xff, sizeof(int), st));
+    } else {
+        CK(cudaMemsetAsync(fallback, 0, sizeof(int), st));
+        eigh_tri(K, n, ldk, off_tol, d_fsq, nval, values, vectors, ldv, fallback, scr, st);
+    }
     const int N = n + (n & 1);
     const int P = N / 2;
     const bool use_smem = N <= kPackedSmemMax;
@@ -270,22 +307,29 @@ void eigh(const double* K, int n, int ldk, double off_tol, const double* d_fsq, 
     a.diag = scr.take<double>(N);
     a.V = scr.take<double>((int64_t)N * N);
     a.err = d_err;
+    a.only_if = fallback;
     static bool attr = false;
     if (!attr) {
-        allow_max_dynamic_smem(jacobi_kernel);
+        allow_max_dynamic_smem(jacobi_kernel<true, true>);
+        allow_max_dynamic_smem(jacobi_kernel<true, false>);
         allow_max_dynamic_smem(vapply_kernel);
         attr = true;
     }
-    const size_t smem = use_smem ? packed * sizeof(double) : 0;
+    const size_t table = (size_t)P * (P + 1) / 2 * sizeof(uint32_t);
+    const bool use_table = use_smem && packed * sizeof(double) + table <= 200 * 1024;
+    const size_t smem = use_smem ? packed * sizeof(double) + (use_table ? table : 0) : 0;
     const size_t vsmem = (size_t)kChunk * P * (sizeof(double2) + sizeof(short2)) + 8 + (size_t)kVRows * N * sizeof(double);
     {
         ProfScope prof("eigh_jacobi", st);
-        LAUNCH(jacobi_kernel, 1, kJacThreads, smem, st, a);
+        if (use_table) LAUNCH((jacobi_kernel<true, true>), 1, kJacThreads, smem, st, a);
+        else if (use_smem) LAUNCH((jacobi_kernel<true, false>), 1, kJacThreads, smem, st, a);
+        else LAUNCH((jacobi_kernel<false, false>), 1, kJacThreads, smem, st, a);
     }
     {
         ProfScope prof("eigh_vectors", st);
-        LAUNCH(vapply_kernel, ceil_div(N, kVRows), kVRows * 32, vsmem, st, n, N, a.rotlog, a.progress, a.V);
-        LAUNCH(sort_kernel, 1, 1024, 0, st, n, N, a.diag, a.V, values, vectors, ldv);
+        LAUNCH(vapply_kernel, ceil_div(N, kVRows), kVRows * 32, vsmem, st, n, N, a.rotlog, a.progress, a.V,
+               fallback);
+        LAUNCH(sort_kernel, 1, 1024, 0, st, n, N, a.diag, a.V, values, vectors, ldv, fallback);
     }
 }
 

@@ -251,6 +251,13 @@ void Engine::prepare() {
     build_transpose(a, scr, st);
     plan_r.build(a.row_ptr, a.m, a.nnz, scr, st);
     plan_c.build(a.col_ptr, a.d, a.nnz, scr, st);
+    // one small read-back per flush lets every SpMM skip the long-row kernels when unused
+    int h[4];
+    CK(cudaMemcpyAsync(h, plan_r.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h + 2, plan_c.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    plan_r.host_long = h[0];
+    plan_c.host_long = h[2];
 }
 
 void Engine::orthonormalize(double* Yp, int m, int err_bit) {
@@ -413,7 +420,7 @@ void Engine::dense_shrink_stack(const double* Xt, int ldx, int n1, int off, int 
         double* Sx = sc.take<double>((int64_t)kcols * lp);
         gram_tn(Xt, d, kcols, ldx, K, kcols, sc, ss);
         LAUNCH(compact_kernel, 1, 1024, 0, ss, K, kcols, n1, off, R, Kc, fsq);
-        eigh(Kc, R, R, 0.0, fsq, ev, U, R, d_err, sc, ss);
+        eigh(Kc, R, R, 0.0, fsq, ev, U, R, d_err, sc, ss, ell);
         LAUNCH(shrink_weights_kernel, 1, 1024, 0, ss, ev, U, R, ell, n1, off, Sx, kcols, lp);
         gemm_nn(Xt, d, kcols, ldx, Sx, lp, lp, bt_out, ldo, ss);
     } else {
@@ -431,7 +438,7 @@ void Engine::dense_shrink_stack(const double* Xt, int ldx, int n1, int off, int 
         double* V = sc.take<double>((int64_t)d * d);
         gram_tn(X, R, d, d, K, d, sc, ss);
         LAUNCH(compact_kernel, 1, 1024, 0, ss, K, d, d, d, d, Kc, fsq);
-        eigh(Kc, d, d, 0.0, fsq, ev, V, d, d_err, sc, ss);
+        eigh(Kc, d, d, 0.0, fsq, ev, V, d, d_err, sc, ss, ell);
         LAUNCH(tall_shrink_kernel, std::max(1u, std::min(4u * kSMs, ceil_div((size_t)d * lp, 256))), 256, 0, ss, ev, V,
                d, ell, bt_out, ldo, lp);
     }

@@ -467,6 +467,7 @@ void build_transpose(DevCsr& a, Scratch& scr, cudaStream_t st) {
 void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st) {
     ProfScope prof("csc_build", st);
     rows = nrows;
+    host_long = -1;
     reserve_pieces(nnz);
     if (nrows > cap_rows) {
         for (void* p : {(void*)long_rows, (void*)long_first}) if (p) cudaFree(p);
@@ -522,8 +523,9 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
     case JJ:                                                                                                       \
         LAUNCH(spmm_rows_kernel<JJ>, grid, 256, 0, st, d_ptr, d_idx, d_val, nrows, kPiece, d_in, ld, ncols, d_out, \
                ldo);                                                                                               \
-        LAUNCH(spmm_pieces_kernel<JJ>, pgrid, 256, 0, st, plan.piece_beg, plan.piece_end, plan.counts, d_idx,     \
-               d_val, d_in, ld, ncols, partial);                                                                   \
+        if (plan.host_long != 0)                                                                                   \
+            LAUNCH(spmm_pieces_kernel<JJ>, pgrid, 256, 0, st, plan.piece_beg, plan.piece_end, plan.counts, d_idx, \
+                   d_val, d_in, ld, ncols, partial);                                                               \
         break;
         SPMM_CASE(1)
         SPMM_CASE(2)
@@ -537,8 +539,9 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
         default:
             throw invalid_argument("spmm: panel wider than 512 columns");
     }
-    LAUNCH(spmm_fixup_kernel, 2 * kSMs, 128, 0, st, plan.long_rows, plan.long_first, plan.counts, partial, ld, ncols,
-           d_out, ldo);
+    if (plan.host_long != 0)
+        LAUNCH(spmm_fixup_kernel, 2 * kSMs, 128, 0, st, plan.long_rows, plan.long_first, plan.counts, partial, ld,
+               ncols, d_out, ldo);
 }
 
 int64_t validate_rows_device(const int64_t* d_row_ptr, int64_t nrows, const uint32_t* d_cols, const double* d_vals,

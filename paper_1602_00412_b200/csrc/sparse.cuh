@@ -80,6 +80,7 @@ struct SegPlan {
     int* piece_beg = nullptr;
     int* piece_end = nullptr;
     int* counts = nullptr;  // device [nlong, npieces]
+    int host_long = -1;     // long rows as known on the host (-1: unknown -> always run the piece path)
     int cap_rows = 0;
     int64_t cap_pieces = 0;
     void build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st);

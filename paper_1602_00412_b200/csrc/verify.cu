@@ -11,8 +11,8 @@
 //   phase 3: y = scale (A'^T u - B'^T t) (CSC gather + dense row), per-block |y|^2
 //   phase 4: every block sums the |y|^2 partials in the same fixed order, so all
 //            blocks take the same accept/reject/continue decision without a sync.
-// x_{k+1} = y_k / |y_k| is never materialised: phase 1 reads y_k and divides on the fly
-// (exactly the reference's x[i] = y[i] / nrm).
+// x_{k+1} = y_k / |y_k| is never materialised: phase 1 reads y_k and scales it on the fly
+// by 1/|y_k| (the reference divides; the two differ by at most one ulp per entry).
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -23,6 +23,7 @@ namespace sfdg {
 namespace {
 
 constexpr int kVThreads = 512;
+constexpr int kXStage = 4096;  // rows of B'^T staged in shared memory per chunk
 
 struct GridBar {
     unsigned* count;
@@ -82,6 +83,7 @@ __device__ __forceinline__ double grid_total(const double* part, unsigned nb, do
 __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     __shared__ double sh[33];
     __shared__ double tloc[512];
+    __shared__ double xl[kXStage];
     const unsigned nb = gridDim.x;
     const GridBar bar{a.bar, a.bar + 1};
     const int lane = threadIdx.x & 31;
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     }
     const double inv0 = 1.0 / sqrt(nsq0);
     const double* xsrc = a.x0;
-    double xmul = inv0, xdiv = 1.0;
+    double xscale = inv0;
     double log_mag = 0.0;
     int verdict = -1;  // -1 running, 0 reject, 1 accept
     int step = 0;
@@ -120,21 +122,29 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
             double s = 0.0;
             for (int k = a.row_ptr[r] + lane; k < a.row_ptr[r + 1]; k += 32) {
                 const int c = (int)a.col[k];
-                s = fma(a.val[k], (__ldcg(xsrc + c) * xmul) / xdiv, s);
+                s = fma(a.val[k], __ldcg(xsrc + c) * xscale, s);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             if (lane == 0) a.u[r] = s;
         }
         {
+            // this block's rows of B'^T: stage x once in shared memory, then one column j
+            // per thread (coalesced across j) accumulates over the rows in order
             const int64_t per = (a.d + nb - 1) / nb;
             const int64_t t0 = (int64_t)blockIdx.x * per;
             const int64_t t1 = min((int64_t)a.d, t0 + per);
-            for (int j = threadIdx.x; j < L; j += kVThreads) {
-                double s = 0.0;
-                for (int64_t t = t0; t < t1; ++t) s = fma(a.bt[t * a.ldb + j], (__ldcg(xsrc + t) * xmul) / xdiv, s);
-                a.tpart[(size_t)blockIdx.x * L + j] = s;
+            const int j = threadIdx.x;  // ell <= 256 < kVThreads: one column per thread
+            double s = 0.0;
+            for (int64_t c0 = t0; c0 < t1; c0 += kXStage) {
+                const int64_t c1 = min(t1, c0 + kXStage);
+                for (int64_t t = c0 + threadIdx.x; t < c1; t += kVThreads) xl[t - c0] = __ldcg(xsrc + t) * xscale;
+                __syncthreads();
+                if (j < L)
+                    for (int64_t t = c0; t < c1; ++t) s = fma(a.bt[t * a.ldb + j], xl[t - c0], s);
+                __syncthreads();
             }
+            if (j < L) a.tpart[(size_t)blockIdx.x * L + j] = s;
         }
         grid_sync(bar, nb);
         // ---- phase 2: t[j] = sum_b tpart[b][j] in block order
@@ -189,8 +199,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
             break;
         }
         xsrc = y;
-        xmul = 1.0;
-        xdiv = nrm;
+        xscale = 1.0 / nrm;
     }
     if (verdict < 0) verdict = log_mag <= 0.0 ? 1 : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
