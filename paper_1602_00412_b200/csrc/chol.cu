@@ -291,68 +291,87 @@ __global__ void __launch_bounds__(kCholThreads) chol_factor_kernel(const double*
     }
 }
 
-// Q = Y R^-1 (m x k, ld). Warp w of the CTA owns rows [64*blk + 16w, +16) as two 8-row
-// DMMA tiles; block columns b = 0..nb-1 of 8: acc = Y_b - X_<b R_<b,b ; X_b = acc inv(R_bb).
-// R (k x k) and inv(R_bb) (k x 8) are staged in shared memory once per CTA. When the
-// second-pass polar path was taken (stats[4] == 1) the kernel is a no-op (gemm applies T).
-constexpr int kTrsmRows = 64;
+// Q = Y R^-1 (m x k, ld). Each warp owns 16 rows (two 8-row DMMA tiles) and forward-
+// substitutes them block column by block column: acc = Y_b - X_<b R_<b,b ; X_b = acc inv(R_bb).
+// Rows are independent, so after the cp.async staging of R, inv(R_bb) and the row tile there
+// is no CTA barrier. When the second-pass polar path was taken (stats[4] == 1) the kernel
+// is a no-op (gemm_nn applies T instead).
+__device__ __forceinline__ void cpa8(double* smem, const double* gmem, bool ok) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 8 : 0));
+}
+constexpr int kTrsmThreads = 256;
 constexpr int kTrsmSmemK = 128;
-__global__ void __launch_bounds__(128) trsm_apply_kernel(const double* __restrict__ Y, int m, int k, int ld,
-                                                         const double* __restrict__ R, const double* __restrict__ dinv8,
-                                                         double* __restrict__ X, int ldx,
-                                                         const double* __restrict__ stats) {
+__global__ void __launch_bounds__(kTrsmThreads) trsm_apply_kernel(const double* __restrict__ Y, int m, int k, int ld,
+                                                                  const double* __restrict__ R,
+                                                                  const double* __restrict__ dinv8,
+                                                                  double* __restrict__ X, int ldx,
+                                                                  const double* __restrict__ stats, int rows) {
     if (stats && stats[4] != 0.0) return;
     extern __shared__ double sm[];
     const int kp = (k + 7) / 8 * 8;
     const bool rsm = kp <= kTrsmSmemK;  // R staged in shared memory, else read through L1
     const int ldr = rsm ? kp + 4 : k;   // conflict-free B-fragment reads (ldr % 16 == 4 or 12)
     const int ldy = kp + 4;
-    double* Rs = sm;                                     // kp x ldr (when rsm)
-    double* Ds = Rs + (rsm ? (size_t)kp * ldr : 0);      // kp x 8 (+4 pad)
-    double* Xs = Ds + (size_t)kp * 12;                   // 64 x ldy : Y tile, overwritten by X
+    double* Rs = sm;                                 // kp x ldr (when rsm)
+    double* Ds = Rs + (rsm ? (size_t)kp * ldr : 0);  // kp x 12
+    double* Xs = Ds + (size_t)kp * 12;               // rows x ldy : Y tile, overwritten by X
     const double* Rr = rsm ? Rs : R;
-    const int r0 = blockIdx.x * kTrsmRows;
+    const int r0 = blockIdx.x * rows;
     if (rsm)
         for (int e = threadIdx.x; e < kp * kp; e += blockDim.x) {
             const int i = e / kp, c = e % kp;
-            Rs[(size_t)i * ldr + c] = (i < k && c < k) ? R[(size_t)i * k + c] : (i == c ? 1.0 : 0.0);
+            const bool ok = i < k && c < k;
+            cpa8(Rs + (size_t)i * ldr + c, ok ? R + (size_t)i * k + c : R, ok);
         }
     for (int e = threadIdx.x; e < kp * 8; e += blockDim.x) {
         const int i = e / 8, c = e % 8;
-        Ds[(size_t)i * 12 + c] = (i < k) ? dinv8[(size_t)i * 8 + c] : 0.0;
+        cpa8(Ds + (size_t)i * 12 + c, i < k ? dinv8 + (size_t)i * 8 + c : dinv8, i < k);
     }
-    for (int e = threadIdx.x; e < kTrsmRows * kp; e += blockDim.x) {
+    for (int e = threadIdx.x; e < rows * kp; e += blockDim.x) {
         const int i = e / kp, c = e % kp;
-        Xs[(size_t)i * ldy + c] = (r0 + i < m && c < k) ? Y[(size_t)(r0 + i) * ld + c] : 0.0;
+        const bool ok = r0 + i < m && c < k;
+        cpa8(Xs + (size_t)i * ldy + c, ok ? Y + (size_t)(r0 + i) * ld + c : Y, ok);
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    if (rsm)  // pad rows/cols beyond k: identity so padded columns stay exactly zero
+        for (int i = k + threadIdx.x; i < kp; i += blockDim.x) Rs[(size_t)i * ldr + i] = 1.0;
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int nb = kp / 8;
-    for (int mt = 0; mt < 2; ++mt) {
-        double* xr = Xs + (size_t)(w * 16 + mt * 8) * ldy;  // this warp's 8-row tile
+    const int ntile = rows / 8;
+    for (int mt = w; mt < ntile; mt += blockDim.x / 32) {
+        double* xr = Xs + (size_t)(mt * 8) * ldy;  // this warp's 8-row tile
         for (int b = 0; b < nb; ++b) {
-            double c0 = 0.0, c1 = 0.0;  // acc = X_<b R_<b,b (subtracted below)
-            for (int kk = 0; kk < 8 * b; kk += 4) {
-                const double av = xr[(size_t)g * ldy + kk + t];
-                const int rr = kk + t, cc = 8 * b + g;
-                const double bv = rsm ? Rr[(size_t)rr * ldr + cc] : (rr < k && cc < k ? __ldg(Rr + (size_t)rr * ldr + cc) : 0.0);
-                dmma884(c0, c1, av, bv);
+            double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;  // two chains: X_<b R_<b,b
+            int kk = 0;
+            for (; kk + 4 < 8 * b; kk += 8) {
+                const int r1 = kk + t, r2 = kk + 4 + t, cc = 8 * b + g;
+                const double bv1 = rsm ? Rr[(size_t)r1 * ldr + cc] : (r1 < k && cc < k ? __ldg(Rr + (size_t)r1 * ldr + cc) : 0.0);
+                const double bv2 = rsm ? Rr[(size_t)r2 * ldr + cc] : (r2 < k && cc < k ? __ldg(Rr + (size_t)r2 * ldr + cc) : 0.0);
+                dmma884(c0, c1, xr[(size_t)g * ldy + r1], bv1);
+                dmma884(e0, e1, xr[(size_t)g * ldy + r2], bv2);
             }
-            // acc = Y_b - acc, laid out as C fragment: row g, cols 2t, 2t+1 of block b
+            for (; kk < 8 * b; kk += 4) {
+                const int r1 = kk + t, cc = 8 * b + g;
+                const double bv1 = rsm ? Rr[(size_t)r1 * ldr + cc] : (r1 < k && cc < k ? __ldg(Rr + (size_t)r1 * ldr + cc) : 0.0);
+                dmma884(c0, c1, xr[(size_t)g * ldy + r1], bv1);
+            }
+            c0 += e0;
+            c1 += e1;
+            // acc = Y_b - acc, as a C fragment: row g, cols 2t, 2t+1 of block b
             double* yb = xr + (size_t)g * ldy + 8 * b + 2 * t;
             const double a0 = yb[0] - c0, a1 = yb[1] - c1;
             __syncwarp();
             yb[0] = a0;
             yb[1] = a1;
             __syncwarp();
-            // X_b = acc inv(R_bb): A frag from xr (row g, col 4ks + t), B frag from Ds
-            double x0 = 0.0, x1 = 0.0;
-            for (int ks = 0; ks < 8; ks += 4) {
-                const double av = xr[(size_t)g * ldy + 8 * b + ks + t];
-                const double bv = Ds[(size_t)(8 * b + ks + t) * 12 + g];
-                dmma884(x0, x1, av, bv);
-            }
+            double x0 = 0.0, x1 = 0.0;  // X_b = acc inv(R_bb)
+#pragma unroll
+            for (int ks = 0; ks < 8; ks += 4)
+                dmma884(x0, x1, xr[(size_t)g * ldy + 8 * b + ks + t], Ds[(size_t)(8 * b + ks + t) * 12 + g]);
             __syncwarp();
             yb[0] = x0;
             yb[1] = x1;
@@ -360,7 +379,7 @@ __global__ void __launch_bounds__(128) trsm_apply_kernel(const double* __restric
         }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < kTrsmRows * k; e += blockDim.x) {
+    for (int e = threadIdx.x; e < rows * k; e += blockDim.x) {
         const int i = e / k, c = e % k;
         if (r0 + i < m) X[(size_t)(r0 + i) * ldx + c] = Xs[(size_t)i * ldy + c];
     }
@@ -399,8 +418,11 @@ void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const do
     if (kp > 512) throw invalid_argument("trsm_apply: k > 512 unsupported");
     ProfScope prof("trsm", st);
     const size_t rs = kp <= kTrsmSmemK ? (size_t)kp * (kp + 4) : 0;
-    const size_t smem = (rs + (size_t)kp * 12 + (size_t)kTrsmRows * (kp + 4)) * sizeof(double);
-    LAUNCH(trsm_apply_kernel, ceil_div(m, kTrsmRows), 128, smem, st, Y, m, k, ld, R, dinv8, X, ldx, stats);
+    int rows = 128;
+    auto bytes = [&](int r) { return (rs + (size_t)kp * 12 + (size_t)r * (kp + 4)) * sizeof(double); };
+    while (rows > 16 && bytes(rows) > 220 * 1024) rows /= 2;
+    LAUNCH(trsm_apply_kernel, ceil_div(m, rows), kTrsmThreads, bytes(rows), st, Y, m, k, ld, R, dinv8, X, ldx, stats,
+           rows);
 }
 
 }  // namespace sfdg

@@ -32,11 +32,25 @@ constexpr int KT = 32;   // k-chunk staged in smem
 constexpr int LDT = TB + 4;  // 68: conflict-free fragment reads (68 mod 16 == 4)
 constexpr int LDK = KT + 4;  // 36
 
+// cp.async (LDGSTS) with zero fill: `bytes` = 0 writes zeros, so tile edges need no branches.
+template <int VEC>
+__device__ __forceinline__ void cp_async(double* smem, const double* gmem, bool ok) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    if (VEC == 2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 16 : 0));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 // Partial Gram of rows [r0, r1) for the upper tile (ti, tj): partial[chunk] (k x k).
+// Two-stage cp.async pipeline: the next 32-row chunk streams in while DMMA consumes this one.
+template <int VEC>
 __global__ void __launch_bounds__(128) gram_tn_kernel(const double* __restrict__ X, int n, int k, int ldx,
                                                       int rows_per_chunk, int T, double* __restrict__ partial) {
-    __shared__ double As[KT][LDT];
-    __shared__ double Bs[KT][LDT];
+    extern __shared__ double smg[];  // [stage][A|B][KT][LDT]
     int ti = 0, rem = blockIdx.x;  // linear upper-triangle tile index -> (ti, tj)
     while (rem >= T - ti) {
         rem -= T - ti;
@@ -50,33 +64,51 @@ __global__ void __launch_bounds__(128) gram_tn_kernel(const double* __restrict__
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm = w & 1, wn = w >> 1;
+    auto tile = [&](int stage, int ab) { return smg + (size_t)((stage * 2 + ab) * KT) * LDT; };
+    auto load = [&](int stage, int kb) {
+        double* As = tile(stage, 0);
+        double* Bs = tile(stage, 1);
+        for (int e = threadIdx.x; e < KT * (TB / VEC); e += 128) {
+            const int r = e / (TB / VEC), c = (e % (TB / VEC)) * VEC;
+            const int row = kb + r;
+            const bool rok = row < r1;
+            const bool oa = rok && i0 + c < k, ob = rok && j0 + c < k;
+            cp_async<VEC>(As + r * LDT + c, oa ? X + (size_t)row * ldx + i0 + c : X, oa);
+            cp_async<VEC>(Bs + r * LDT + c, ob ? X + (size_t)row * ldx + j0 + c : X, ob);
+        }
+        cp_commit();
+    };
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    int stage = 0;
+    if (r0 < r1) load(0, r0);
     for (int kb = r0; kb < r1; kb += KT) {
-        for (int e = threadIdx.x; e < KT * TB; e += 128) {
-            const int r = e / TB, c = e % TB;
-            const int row = kb + r;
-            const bool rok = row < r1;
-            As[r][c] = (rok && i0 + c < k) ? X[(size_t)row * ldx + i0 + c] : 0.0;
-            Bs[r][c] = (rok && j0 + c < k) ? X[(size_t)row * ldx + j0 + c] : 0.0;
+        if (kb + KT < r1) {
+            load(stage ^ 1, kb + KT);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
         }
         __syncthreads();
+        const double* As = tile(stage, 0);
+        const double* Bs = tile(stage, 1);
 #pragma unroll
         for (int ks = 0; ks < KT; ks += 4) {
             double a[4], b[4];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) a[mi] = As[ks + t][wm * 32 + mi * 8 + g];
+            for (int mi = 0; mi < 4; ++mi) a[mi] = As[(ks + t) * LDT + wm * 32 + mi * 8 + g];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[ks + t][wn * 32 + ni * 8 + g];
+            for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(ks + t) * LDT + wn * 32 + ni * 8 + g];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         }
         __syncthreads();
+        stage ^= 1;
     }
     double* P = partial + (size_t)chunk * k * k;
 #pragma unroll
@@ -108,45 +140,64 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int nchun
     }
 }
 
+template <int VEC>
 __global__ void __launch_bounds__(128) gemm_nn_kernel(const double* __restrict__ X, int n, int k, int ldx,
                                                       const double* __restrict__ S, int c, int lds,
                                                       double* __restrict__ C, int ldc,
                                                       const double* __restrict__ pred) {
     if (pred && *pred == 0.0) return;
-    __shared__ double Xs[TB][LDK];
-    __shared__ double Ss[KT][LDT];
+    extern __shared__ double smg[];  // [stage][Xs TB x LDK | Ss KT x LDT]
+    constexpr int XS = TB * LDK, SS = KT * LDT;
     const int r0 = blockIdx.x * TB, c0 = blockIdx.y * TB;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm = w & 1, wn = w >> 1;
+    auto load = [&](int stage, int kk) {
+        double* Xs = smg + stage * (XS + SS);
+        double* Ss = Xs + XS;
+        for (int e = threadIdx.x; e < TB * (KT / VEC); e += 128) {
+            const int r = e / (KT / VEC), q = (e % (KT / VEC)) * VEC;
+            const bool ok = r0 + r < n && kk + q < k;
+            cp_async<VEC>(Xs + r * LDK + q, ok ? X + (size_t)(r0 + r) * ldx + kk + q : X, ok);
+        }
+        for (int e = threadIdx.x; e < KT * (TB / VEC); e += 128) {
+            const int q = e / (TB / VEC), cc = (e % (TB / VEC)) * VEC;
+            const bool ok = kk + q < k && c0 + cc < c;
+            cp_async<VEC>(Ss + q * LDT + cc, ok ? S + (size_t)(kk + q) * lds + c0 + cc : S, ok);
+        }
+        cp_commit();
+    };
     double acc[4][4][2];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    int stage = 0;
+    load(0, 0);
     for (int kk = 0; kk < k; kk += KT) {
-        for (int e = threadIdx.x; e < TB * KT; e += 128) {
-            const int r = e / KT, q = e % KT;
-            Xs[r][q] = (r0 + r < n && kk + q < k) ? X[(size_t)(r0 + r) * ldx + kk + q] : 0.0;
-        }
-        for (int e = threadIdx.x; e < KT * TB; e += 128) {
-            const int q = e / TB, cc = e % TB;
-            Ss[q][cc] = (kk + q < k && c0 + cc < c) ? S[(size_t)(kk + q) * lds + c0 + cc] : 0.0;
+        if (kk + KT < k) {
+            load(stage ^ 1, kk + KT);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
         }
         __syncthreads();
+        const double* Xs = smg + stage * (XS + SS);
+        const double* Ss = Xs + XS;
 #pragma unroll
         for (int ks = 0; ks < KT; ks += 4) {
             double a[4], b[4];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) a[mi] = Xs[wm * 32 + mi * 8 + g][ks + t];
+            for (int mi = 0; mi < 4; ++mi) a[mi] = Xs[(wm * 32 + mi * 8 + g) * LDK + ks + t];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) b[ni] = Ss[ks + t][wn * 32 + ni * 8 + g];
+            for (int ni = 0; ni < 4; ++ni) b[ni] = Ss[(ks + t) * LDT + wn * 32 + ni * 8 + g];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
                 for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         }
         __syncthreads();
+        stage ^= 1;
     }
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
@@ -226,6 +277,8 @@ __global__ void fill2d_kernel(double* __restrict__ out, int rows, int cols, int 
 
 }  // namespace
 
+static bool vec16(const double* p, int ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); }
+
 void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scratch& scr, cudaStream_t st) {
     if (k <= 0) return;
     if (n <= 0) {
@@ -239,7 +292,17 @@ void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scrat
     int rows_per_chunk = (int)round_up(std::max<int64_t>(KT * 4, ((int64_t)n + target_chunks - 1) / target_chunks), KT);
     const int nchunks = (n + rows_per_chunk - 1) / rows_per_chunk;
     double* partial = scr.take<double>((int64_t)nchunks * k * k);
-    LAUNCH(gram_tn_kernel, dim3(ntiles, nchunks), 128, 0, st, X, n, k, ldx, rows_per_chunk, T, partial);
+    const size_t smem = 2 * 2 * KT * LDT * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        allow_max_dynamic_smem(gram_tn_kernel<2>);
+        allow_max_dynamic_smem(gram_tn_kernel<1>);
+        attr = true;
+    }
+    if (vec16(X, ldx) && k % 2 == 0)
+        LAUNCH(gram_tn_kernel<2>, dim3(ntiles, nchunks), 128, smem, st, X, n, k, ldx, rows_per_chunk, T, partial);
+    else
+        LAUNCH(gram_tn_kernel<1>, dim3(ntiles, nchunks), 128, smem, st, X, n, k, ldx, rows_per_chunk, T, partial);
     LAUNCH(gram_reduce_kernel, std::max(1u, std::min(4u * kSMs, ceil_div((size_t)k * k, 256))), 256, 0, st, partial,
            nchunks, k, out, ldo);
 }
@@ -252,7 +315,19 @@ void gemm_nn(const double* X, int n, int k, int ldx, const double* S, int c, int
         return;
     }
     ProfScope prof("gemm", st);
-    LAUNCH(gemm_nn_kernel, dim3(ceil_div(n, TB), ceil_div(c, TB)), 128, 0, st, X, n, k, ldx, S, c, lds, C, ldc, pred);
+    const size_t smem = 2 * (TB * LDK + KT * LDT) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        allow_max_dynamic_smem(gemm_nn_kernel<2>);
+        allow_max_dynamic_smem(gemm_nn_kernel<1>);
+        attr = true;
+    }
+    if (vec16(X, ldx) && vec16(S, lds) && k % 2 == 0 && c % 2 == 0)
+        LAUNCH(gemm_nn_kernel<2>, dim3(ceil_div(n, TB), ceil_div(c, TB)), 128, smem, st, X, n, k, ldx, S, c, lds, C,
+               ldc, pred);
+    else
+        LAUNCH(gemm_nn_kernel<1>, dim3(ceil_div(n, TB), ceil_div(c, TB)), 128, smem, st, X, n, k, ldx, S, c, lds, C,
+               ldc, pred);
 }
 
 void sumsq(const double* X, int64_t rows, int cols, int ld, double* d_out, int* d_err, int err_bit, Scratch& scr,
