@@ -3,18 +3,19 @@
 // Reference: verify_spectral (core/src/shrink.cpp:75-102) runs `steps` power-method
 // steps on diff_op(x) = (2/Delta)(A'^T A' x - B'^T B' x) (shrink.cpp:121-126) from a
 // random unit vector (la_core.cpp:174-189), tracking log|y| and exiting early on
-// annihilation (accept) or on growth past 1 (reject). Every step depends on the last,
-// and each has a global norm, so a host loop would pay a launch + round trip per step.
-// Here all steps run inside one cooperative grid: per step
-//   phase 1: u = A' x (CSR, warp/row) and per-block partials of t = B' x
-//   phase 2: t reduced (block b owns entries j = b mod nblocks)
-//   phase 3: y = scale (A'^T u - B'^T t) (CSC gather + dense row), per-block |y|^2
-//   phase 4: every block sums the |y|^2 partials in the same fixed order, so all
-//            blocks take the same accept/reject/continue decision without a sync.
-// x_{k+1} = y_k / |y_k| is never materialised: phase 1 reads y_k and scales it on the fly
-// by 1/|y_k| (the reference divides; the two differ by at most one ulp per entry).
-#include <cooperative_groups.h>
-
+// annihilation (accept) or on growth past 1 (reject). Every step depends on the last and
+// has a global norm, so a host loop would pay a launch + round trip per step. Here all
+// steps run in one cooperative grid; block b owns a contiguous chunk of rows of A' (for
+// u = A'x) and a contiguous chunk of columns (for y and the rows of B'^T). Per step:
+//   phase A: u = A' x                                     (CSR, warp per row)  | barrier
+//   phase B: y_c = scale (A'^T u - B'^T t)_c for own columns (CSC + B'^T row), and, from the
+//            same B'^T rows still in registers, the partials of next t = B' y and |y|^2
+//                                                                              | barrier
+//   phase C: every block reduces |y|^2 and t in the same fixed order, so all blocks take
+//            the same accept / reject / continue decision with no further sync.
+// B'^T is therefore streamed once per step (it is the bulk: d x ell FP64), not twice.
+// x = y / |y| is never materialised: it is y scaled by 1/|y| on the fly (the reference
+// divides; the two differ by at most one ulp per entry).
 #include "common.cuh"
 #include "verify.cuh"
 
@@ -23,82 +24,133 @@ namespace sfdg {
 namespace {
 
 constexpr int kVThreads = 512;
-constexpr int kXStage = 4096;  // rows of B'^T staged in shared memory per chunk
+constexpr int kVWarps = kVThreads / 32;
+constexpr int kMaxQ = 8;  // ell <= 256 = 32 lanes x 8
 
 struct GridBar {
     unsigned* count;
     unsigned* gen;
 };
 
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Generation barrier: the last arriving block resets the count and bumps the generation;
+// the others spin on an acquire load.
 __device__ __forceinline__ void grid_sync(const GridBar& b, unsigned nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* vgen = b.gen;
-        const unsigned g = *vgen;
+        const unsigned g = ld_acquire(b.gen);
         __threadfence();
         if (atomicAdd(b.count, 1u) == nblocks - 1) {
             atomicExch(b.count, 0u);
             __threadfence();
             atomicAdd(b.gen, 1u);
         } else {
-            while (*vgen == g) __nanosleep(20);
+            while (ld_acquire(b.gen) == g) __nanosleep(32);
         }
-        __threadfence();
     }
     __syncthreads();
 }
 
-__device__ __forceinline__ double block_sum(double v, double* sh) {
+__device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double s = 0.0;
-    if (threadIdx.x == 0) {
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
-        sh[32] = s;
-    }
-    __syncthreads();
-    s = sh[32];
-    __syncthreads();
-    return s;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
 }
 
-// Sum of the nb per-block partials in a fixed order (lane-strided then a fixed shuffle
-// tree): every block computes the identical value.
+// Sum of the nb per-block partials in a fixed order: every block gets the identical value.
 __device__ __forceinline__ double grid_total(const double* part, unsigned nb, double* sh) {
     if (threadIdx.x < 32) {
         double s = 0.0;
         for (unsigned b = threadIdx.x; b < nb; b += 32) s += __ldcg(part + b);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (threadIdx.x == 0) sh[32] = s;
+        s = warp_sum(s);
+        if (threadIdx.x == 0) sh[0] = s;
     }
     __syncthreads();
-    const double t = sh[32];
+    const double t = sh[0];
     __syncthreads();
     return t;
 }
 
+// t[j] = scale * sum_b tp[b][j] for all j < L, reduced identically in every block: kSplit
+// threads per entry each sum a fixed stride of blocks (all loads in flight at once), then
+// the kSplit partials are combined in a fixed order.
+constexpr int kSplit = 4;
+__device__ __forceinline__ void reduce_t(const double* tp, unsigned nb, int L, double scale, double* tloc,
+                                         double* scratch /* kSplit * 256 */) {
+    for (int e = threadIdx.x; e < L * kSplit; e += kVThreads) {
+        const int j = e / kSplit, sidx = e % kSplit;
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+        int u = 0;
+        for (unsigned b = sidx; b < nb; b += kSplit, u = (u + 1) & 7) acc[u] += __ldcg(tp + (size_t)b * L + j);
+        double s = 0.0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) s += acc[v];
+        scratch[sidx * 256 + j] = s;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < L; j += kVThreads) {
+        double s = 0.0;
+        for (int sidx = 0; sidx < kSplit; ++sidx) s += scratch[sidx * 256 + j];
+        tloc[j] = s * scale;
+    }
+    __syncthreads();
+}
+
+// Per-warp partials (registers) -> block partial (fixed warp order) -> tp[blockIdx] and
+// part[blockIdx] (the |.|^2 slot).
+__device__ __forceinline__ void block_partials(double (&tn)[kMaxQ], double ns, int L, double (*wpart)[257],
+                                               double* tp, double* part) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q)
+        if (lane + 32 * q < L) wpart[wib][lane + 32 * q] = tn[q];
+    if (lane == 0) wpart[wib][256] = ns;
+    __syncthreads();
+    for (int j = threadIdx.x; j <= 256; j += kVThreads) {
+        if (j < L || j == 256) {
+            double s = 0.0;
+            for (int w = 0; w < kVWarps; ++w) s += wpart[w][j];
+            if (j < L) tp[(size_t)blockIdx.x * L + j] = s;
+            else part[blockIdx.x] = s;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
-    __shared__ double sh[33];
-    __shared__ double tloc[512];
-    __shared__ double xl[kXStage];
+    __shared__ double sh[8];
+    __shared__ double tloc[256];             // current t = B' x
+    __shared__ double wpart[kVWarps][257];   // per-warp partials of the next t, and |.|^2
     const unsigned nb = gridDim.x;
     const GridBar bar{a.bar, a.bar + 1};
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    const int64_t gwarp = (int64_t)blockIdx.x * (kVThreads / 32) + wib;
-    const int64_t nwarps = (int64_t)nb * (kVThreads / 32);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int L = a.ell;
+    const int64_t rper = (a.m + nb - 1) / nb, cper = (a.d + nb - 1) / nb;
+    const int64_t r0 = blockIdx.x * rper, r1 = min((int64_t)a.m, r0 + rper);
+    const int64_t c0 = blockIdx.x * cper, c1 = min((int64_t)a.d, c0 + cper);
 
-    // phase 0: |x0|^2 for the unit-sphere normalisation (la_core.cpp:177-186)
+    // ---- init: |x0|^2 (la_core.cpp:177-186) and the partials of B' x0 over own columns
     {
-        double s = 0.0;
-        for (int64_t i = blockIdx.x * (int64_t)kVThreads + threadIdx.x; i < a.d; i += (int64_t)nb * kVThreads)
-            s = fma(a.x0[i], a.x0[i], s);
-        s = block_sum(s, sh);
-        if (threadIdx.x == 0) a.part[blockIdx.x] = s;
+        double tn[kMaxQ];
+#pragma unroll
+        for (int q = 0; q < kMaxQ; ++q) tn[q] = 0.0;
+        double ns = 0.0;
+        for (int64_t c = c0 + wib; c < c1; c += kVWarps) {
+            const double xc = a.x0[c];
+            ns = fma(xc, xc, ns);
+#pragma unroll
+            for (int q = 0; q < kMaxQ; ++q) {
+                const int j = lane + 32 * q;
+                if (j < L) tn[q] = fma(a.bt[c * a.ldb + j], xc, tn[q]);
+            }
+        }
+        block_partials(tn, ns, L, wpart, a.tpart, a.part);
     }
     grid_sync(bar, nb);
     const double nsq0 = grid_total(a.part, nb, sh);
@@ -109,79 +161,65 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
         }
         return;
     }
-    const double inv0 = 1.0 / sqrt(nsq0);
+    double xscale = 1.0 / sqrt(nsq0);
+    reduce_t(a.tpart, nb, L, xscale, tloc, &wpart[0][0]);  // t = B' x0 / |x0|
     const double* xsrc = a.x0;
-    double xscale = inv0;
     double log_mag = 0.0;
     int verdict = -1;  // -1 running, 0 reject, 1 accept
     int step = 0;
     for (; step < a.steps; ++step) {
         double* y = a.ybuf + (size_t)(step & 1) * a.d;
-        // ---- phase 1: u = A' x ; t partials = B' x (B't is d x ell, row stride ldb)
-        for (int64_t r = gwarp; r < a.m; r += nwarps) {
-            double s = 0.0;
-            for (int k = a.row_ptr[r] + lane; k < a.row_ptr[r + 1]; k += 32) {
-                const int c = (int)a.col[k];
-                s = fma(a.val[k], __ldcg(xsrc + c) * xscale, s);
+        double* tp = a.tpart + (size_t)((step + 1) & 1) * nb * L;  // partials of the next t
+        // ---- phase A: u = A' x over this block's rows
+        for (int64_t r = r0 + wib; r < r1; r += 2 * kVWarps) {
+            const int64_t r2 = r + kVWarps;
+            const bool has2 = r2 < r1;
+            double s = 0.0, s2 = 0.0;
+            const int k0 = a.row_ptr[r], k1 = a.row_ptr[r + 1];
+            const int q0 = has2 ? a.row_ptr[r2] : 0, q1 = has2 ? a.row_ptr[r2 + 1] : 0;
+            for (int k = k0 + lane, q = q0 + lane; k < k1 || q < q1; k += 32, q += 32) {
+                if (k < k1) s = fma(a.val[k], __ldcg(xsrc + a.col[k]) * xscale, s);
+                if (q < q1) s2 = fma(a.val[q], __ldcg(xsrc + a.col[q]) * xscale, s2);
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) a.u[r] = s;
-        }
-        {
-            // this block's rows of B'^T: stage x once in shared memory, then one column j
-            // per thread (coalesced across j) accumulates over the rows in order
-            const int64_t per = (a.d + nb - 1) / nb;
-            const int64_t t0 = (int64_t)blockIdx.x * per;
-            const int64_t t1 = min((int64_t)a.d, t0 + per);
-            const int j = threadIdx.x;  // ell <= 256 < kVThreads: one column per thread
-            double s = 0.0;
-            for (int64_t c0 = t0; c0 < t1; c0 += kXStage) {
-                const int64_t c1 = min(t1, c0 + kXStage);
-                for (int64_t t = c0 + threadIdx.x; t < c1; t += kVThreads) xl[t - c0] = __ldcg(xsrc + t) * xscale;
-                __syncthreads();
-                if (j < L)
-                    for (int64_t t = c0; t < c1; ++t) s = fma(a.bt[t * a.ldb + j], xl[t - c0], s);
-                __syncthreads();
+            s = warp_sum(s);
+            s2 = warp_sum(s2);
+            if (lane == 0) {
+                a.u[r] = s;
+                if (has2) a.u[r2] = s2;
             }
-            if (j < L) a.tpart[(size_t)blockIdx.x * L + j] = s;
         }
         grid_sync(bar, nb);
-        // ---- phase 2: t[j] = sum_b tpart[b][j] in block order
-        for (int j = (int)blockIdx.x * (kVThreads / 32) + wib; j < L; j += (int)nb * (kVThreads / 32)) {
-            double s = 0.0;
-            for (unsigned b = lane; b < nb; b += 32) s += __ldcg(a.tpart + (size_t)b * L + j);
+        // ---- phase B: y over own columns; next-t partials and |y|^2 from the same rows
+        double tn[kMaxQ];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) a.t[j] = s;
-        }
-        grid_sync(bar, nb);
-        for (int j = threadIdx.x; j < L; j += kVThreads) tloc[j] = __ldcg(a.t + j);
-        __syncthreads();
-        // ---- phase 3: y = scale * (A'^T u - B'^T t), per-warp |y|^2 in fixed order
+        for (int q = 0; q < kMaxQ; ++q) tn[q] = 0.0;
         double nsq = 0.0;
         bool bad = false;
-        for (int64_t c = gwarp; c < a.d; c += nwarps) {
+        for (int64_t c = c0 + wib; c < c1; c += kVWarps) {
             double s = 0.0;
-            for (int k = a.col_ptr[c] + lane; k < a.col_ptr[c + 1]; k += 32) s = fma(a.cval[k], __ldcg(a.u + a.row_idx[k]), s);
+            for (int k = a.col_ptr[c] + lane; k < a.col_ptr[c + 1]; k += 32)
+                s = fma(a.cval[k], __ldcg(a.u + a.row_idx[k]), s);
+            double brow[kMaxQ];
             double bsum = 0.0;
-            for (int j = lane; j < L; j += 32) bsum = fma(a.bt[c * a.ldb + j], tloc[j], bsum);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                s += __shfl_xor_sync(0xffffffffu, s, o);
-                bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+            for (int q = 0; q < kMaxQ; ++q) {
+                const int j = lane + 32 * q;
+                brow[q] = j < L ? a.bt[c * a.ldb + j] : 0.0;
+                bsum = fma(brow[q], j < L ? tloc[j] : 0.0, bsum);
             }
+            s = warp_sum(s);
+            bsum = warp_sum(bsum);
             const double yc = a.scale * (s - bsum);  // shrink.cpp:124
             if (!isfinite(yc)) bad = true;
             if (lane == 0) y[c] = yc;
             nsq = fma(yc, yc, nsq);
+#pragma unroll
+            for (int q = 0; q < kMaxQ; ++q) tn[q] = fma(brow[q], yc, tn[q]);
         }
         if (bad) atomicOr(a.err, ERR_NONFINITE_VERIFY);
-        if (lane != 0) nsq = 0.0;
-        nsq = block_sum(nsq, sh);
-        if (threadIdx.x == 0) a.part[blockIdx.x] = nsq;
+        block_partials(tn, nsq, L, wpart, tp, a.part);
         grid_sync(bar, nb);
-        // ---- phase 4: identical decision in every block (shrink.cpp:88-99)
+        // ---- phase C: identical decision in every block (shrink.cpp:88-99)
         const double tot = grid_total(a.part, nb, sh);
         if (*((volatile int*)a.err) & ERR_NONFINITE_VERIFY) {
             verdict = 0;
@@ -200,6 +238,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
         }
         xsrc = y;
         xscale = 1.0 / nrm;
+        reduce_t(tp, nb, L, xscale, tloc, &wpart[0][0]);
     }
     if (verdict < 0) verdict = log_mag <= 0.0 ? 1 : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
