@@ -164,24 +164,29 @@ def run_reference(a):
 
 # ------------------------------------------------------------------ our arm
 def merge_tree(P, torch, dist, s, d, ell, device, rank, world):
-    """log2 tree: at level L, rank r with r % 2^(L+1) == 2^L sends its
-    B^T (d x ell) to r - 2^L, which merge-shrinks (sketch.cpp:80-83) lower-rank first."""
+    """log2 tree (paper_1602_00412_b200/shards.py): at level L, rank r with
+    r % 2^(L+1) == 2^L sends its B^T (d x ell, FP64) to r - 2^L, which merge-shrinks it
+    (sketch.cpp:80-83, sfdg_merge_device) with its own, lower rank stacked first."""
+    from paper_1602_00412_b200 import shards
+    host = dist.get_backend() == "gloo"  # gloo (CI / single-GPU dry runs) moves host tensors
     bt = torch.empty((d, ell), dtype=torch.float64, device=f"cuda:{device}")
     s.sketch_device_t(bt.data_ptr(), ell)
-    other = torch.empty_like(bt)
-    out = torch.empty_like(bt)
-    step = 1
-    while step < world:
-        if rank % (2 * step) == step:
-            dist.send(bt, dst=rank - step)
-            break
-        if rank % (2 * step) == 0 and rank + step < world:
-            dist.recv(other, src=rank + step)
-            torch.cuda.synchronize(device)
-            P.merge_device(bt.data_ptr(), other.data_ptr(), ell, d, ell, out.data_ptr(), device)
-            bt, out = out, bt
-        step *= 2
-    return bt
+
+    def send(t, peer):
+        dist.send(t.cpu() if host else t, dst=peer)
+
+    def recv(peer):
+        o = torch.empty((d, ell), dtype=torch.float64, device="cpu" if host else f"cuda:{device}")
+        dist.recv(o, src=peer)
+        return o.to(f"cuda:{device}") if host else o
+
+    def merge(lo, hi):
+        out = torch.empty_like(lo)
+        torch.cuda.synchronize(device)
+        P.merge_device(lo.data_ptr(), hi.data_ptr(), ell, d, ell, out.data_ptr(), device)
+        return out
+
+    return shards.merge_tree(bt, rank, world, send, recv, merge)
 
 
 def main():
@@ -199,8 +204,13 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
+        local = local % max(1, torch.cuda.device_count())  # dry runs may put several ranks on one GPU
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("SFDG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     device = local
     torch.cuda.set_device(device)
 
@@ -237,7 +247,10 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[device])
+            if dist.get_backend() == "nccl":
+                dist.barrier(device_ids=[device])
+            else:
+                dist.barrier()
 
     def timed(fn, k):
         total = 0.0
@@ -255,7 +268,8 @@ def main():
             e1.synchronize()
             barrier()
             total += e0.elapsed_time(e1)
-        t = torch.tensor([total], dtype=torch.float64, device=f"cuda:{device}")
+        t = torch.tensor([total], dtype=torch.float64,
+                         device=f"cuda:{device}" if world == 1 or dist.get_backend() == "nccl" else "cpu")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()) / 1e3

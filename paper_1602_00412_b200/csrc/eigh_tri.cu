@@ -96,15 +96,16 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(TriArgs a) {
         return;
     }
     if (tid == 0) *a.trivial = 0;
+    __shared__ double wred[32];
     for (int k = 0; k + 2 < n; ++k) {
-        // x_j = A(k, j), j = k+1..n-1 ; Householder (dlarfg) on x
-        double xs = 0.0;
-        for (int j = k + 2 + tid; j < n; j += nt) {
-            const double x = A[tri[j] + k];
-            xs += x * x;
-        }
-        xs = block_sum(xs, red);
-        if (tid == 0) {
+        // warp 0: Householder (dlarfg) on x_j = A(k, j), j = k+1..n-1, and the vector v
+        if (warp == 0) {
+            double xs = 0.0;
+            for (int j = k + 2 + lane; j < n; j += 32) {
+                const double x = A[tri[j] + k];
+                xs += x * x;
+            }
+            xs = warp_sum(xs);
             const double alpha = A[tri[k + 1] + k];
             double tau = 0.0, beta = alpha, scal = 0.0;
             if (xs > 0.0) {
@@ -112,32 +113,35 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(TriArgs a) {
                 tau = (beta - alpha) / beta;
                 scal = 1.0 / (alpha - beta);
             }
-            s_tau = tau;
-            s_scal = scal;
-            a.d[k] = A[tri[k] + k];
-            a.e[k] = beta;
-            a.tau[k] = tau;
+            for (int j = k + 1 + lane; j < n; j += 32) {
+                const double v = (j == k + 1) ? 1.0 : A[tri[j] + k] * scal;
+                vs[j] = v;
+                a.vh[(size_t)k * n + j] = v;
+            }
+            if (lane == 0) {
+                s_tau = tau;
+                a.d[k] = A[tri[k] + k];
+                a.e[k] = beta;
+                a.tau[k] = tau;
+            }
         }
         __syncthreads();
-        const double tau = s_tau, scal = s_scal;
-        for (int j = k + 1 + tid; j < n; j += nt) {
-            const double v = (j == k + 1) ? 1.0 : A[tri[j] + k] * scal;
-            vs[j] = v;
-            a.vh[(size_t)k * n + j] = v;
-        }
-        __syncthreads();
+        const double tau = s_tau;
         if (tau == 0.0) continue;
-        // p = tau A22 v (warp per row), then kk = tau/2 p^T v, w = p - kk v
+        // p = tau A22 v (warp per row) and per-warp partials of p^T v
         double pv = 0.0;
         for (int i = k + 1 + warp; i < n; i += nw) {
             double s = 0.0;
             for (int j = k + 1 + lane; j < n; j += 32) s += A[i <= j ? tri[j] + i : tri[i] + j] * vs[j];
             s = warp_sum(s) * tau;
             if (lane == 0) ws[i] = s;
-            pv += (lane == 0) ? s * vs[i] : 0.0;
+            pv += s * vs[i];
         }
-        pv = block_sum(pv, red);
-        const double kk = 0.5 * tau * pv;
+        if (lane == 0) wred[warp] = pv;
+        __syncthreads();
+        double kk = 0.0;
+        for (int w2 = 0; w2 < nw; ++w2) kk += wred[w2];  // fixed order, same in every thread
+        kk *= 0.5 * tau;
         for (int i = k + 1 + tid; i < n; i += nt) ws[i] -= kk * vs[i];
         __syncthreads();
         // A22 -= v w^T + w v^T (upper triangle)
@@ -227,9 +231,13 @@ __global__ void bisect_kernel(const double* __restrict__ dg, const double* __res
 // (T - lambda I) (LAPACK dgttrf/dgttrs algebra); X is n x ldx (column t = vector t).
 __global__ void inviter_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int nval,
                                const double* __restrict__ lam, const int* __restrict__ trivial,
-                               double* __restrict__ X, int ldx, double* __restrict__ work) {
+                               double* __restrict__ X, int ldx, double* __restrict__ work_g) {
+    extern __shared__ double work_s[];
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nval) return;
+    // per-thread LU bands + vector: shared memory when they fit (n <= 320), else global
+    double* work = work_g ? work_g : work_s;
+    const int slot = work_g ? t : threadIdx.x;
     if (*trivial) {  // identity eigenvectors in the stable descending order of the diagonal
         int idx = 0;
         for (int i = 0; i < n; ++i) {
@@ -240,7 +248,7 @@ __global__ void inviter_kernel(const double* __restrict__ dg, const double* __re
         for (int i = 0; i < n; ++i) X[(size_t)i * ldx + t] = (i == idx) ? 1.0 : 0.0;
         return;
     }
-    double* U0 = work + (size_t)t * 5 * n;  // diag of U
+    double* U0 = work + (size_t)slot * 5 * n;  // diag of U
     double* U1 = U0 + n;                    // 1st super
     double* U2 = U1 + n;                    // 2nd super
     double* Lm = U2 + n;                    // multipliers
@@ -435,19 +443,24 @@ __global__ void cluster_kernel(const double* __restrict__ dg, const double* __re
 __global__ void backtransform_kernel(const double* __restrict__ vh, const double* __restrict__ tau, int n, int nval,
                                      const int* __restrict__ trivial, double* __restrict__ X, int ldx) {
     if (*trivial) return;
+    extern __shared__ double colbuf[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int col = blockIdx.x * (blockDim.x >> 5) + w;  // warp per column
+    const int col = blockIdx.x * (blockDim.x >> 5) + w;  // warp per column, kept in shared memory
     if (col >= nval) return;
+    double* x = colbuf + (size_t)w * n;
+    for (int j = lane; j < n; j += 32) x[j] = X[(size_t)j * ldx + col];
+    __syncwarp();
     for (int k = n - 3; k >= 0; --k) {
         const double tk = tau[k];
         if (tk == 0.0) continue;
-        double s = 0.0;
         const double* v = vh + (size_t)k * n;
-        for (int j = k + 1 + lane; j < n; j += 32) s += v[j] * X[(size_t)j * ldx + col];
+        double s = 0.0;
+        for (int j = k + 1 + lane; j < n; j += 32) s += v[j] * x[j];
         s = warp_sum(s) * tk;
-        for (int j = k + 1 + lane; j < n; j += 32) X[(size_t)j * ldx + col] -= s * v[j];
+        for (int j = k + 1 + lane; j < n; j += 32) x[j] -= s * v[j];
         __syncwarp();
     }
+    for (int j = lane; j < n; j += 32) X[(size_t)j * ldx + col] = x[j];
 }
 
 }  // namespace
@@ -478,6 +491,8 @@ void eigh_tri(const double* K, int n, int ldk, double off_tol, const double* d_f
     static bool attr = false;
     if (!attr) {
         allow_max_dynamic_smem(tridiag_kernel<true>);
+        allow_max_dynamic_smem(inviter_kernel);
+        allow_max_dynamic_smem(backtransform_kernel);
         attr = true;
     }
     {
@@ -493,9 +508,17 @@ void eigh_tri(const double* K, int n, int ldk, double off_tol, const double* d_f
     }
     {
         ProfScope prof("eigh_vectors", st);
-        LAUNCH(inviter_kernel, ceil_div(nval, 64), 64, 0, st, a.d, a.e, n, nval, values, a.trivial, vectors, ldv, work);
+        const int ith = 8;  // threads per block: 8 x 5n doubles of LU bands in shared memory
+        const size_t ismem = (size_t)ith * 5 * n * sizeof(double);
+        if (ismem <= 96 * 1024)
+            LAUNCH(inviter_kernel, ceil_div(nval, ith), ith, ismem, st, a.d, a.e, n, nval, values, a.trivial, vectors,
+                   ldv, (double*)nullptr);
+        else
+            LAUNCH(inviter_kernel, ceil_div(nval, 64), 64, 0, st, a.d, a.e, n, nval, values, a.trivial, vectors, ldv,
+                   work);
         LAUNCH(cluster_kernel, nval, 32, 0, st, a.d, a.e, n, nval, values, a.trivial, vectors, ldv, fallback);
-        LAUNCH(backtransform_kernel, ceil_div(nval, 8), 256, 0, st, a.vh, a.tau, n, nval, a.trivial, vectors, ldv);
+        LAUNCH(backtransform_kernel, ceil_div(nval, 8), 256, 8 * (size_t)n * sizeof(double), st, a.vh, a.tau, n, nval,
+               a.trivial, vectors, ldv);
     }
 }
 

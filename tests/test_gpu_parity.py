@@ -411,3 +411,30 @@ def test_covariance_bound_random_streams(oracle):
         if np.linalg.norm(a.T @ a - b.T @ b, 2) <= (a ** 2).sum() / (KALPHA * 12):
             ok += 1
     assert ok >= 19
+
+
+# ---------------------------------------------------------------- BASELINE families at reduced d
+@pytest.mark.parametrize("family,d,ell,rows", [("c3", 1500, 40, 3000), ("c4", 1200, 32, 2400), ("c5", 2000, 48, 4000),
+                                               ("c2", 3000, 60, 6000)])
+def test_baseline_family_streams_vs_oracle(oracle, family, d, ell, rows):
+    """Same generator family (Zipf / power-law columns, skewed row lengths, centred ratings,
+    planted signal) at a d the CPU oracle finishes in seconds; two full flushes each."""
+    cfg = S.StreamConfig(family, rows, d, ell, 7)
+    rp, cs, vs = S.generate(cfg, (0, rows))
+    b, st = sketch_gpu(rp, cs, vs, d, ell, 11)
+    bo, so = oracle.sketch(rp, cs, vs, d, ell, seed=11)
+    assert btb_rel(b, bo) <= BTB_TOL
+    for key in ("flushes", "attempts", "verifier_i", "delta_spent"):
+        assert st[key] == so[key], key
+
+
+def test_every_sweep_schedule_matches_adaptive(oracle, monkeypatch):
+    """The adaptive CholeskyQR2 schedule and the reference's every-sweep schedule give the
+    same sketch to roundoff (only span(Z) matters)."""
+    rp, cs, vs = S.generate("c1", (0, 2000))
+    b_adapt, _ = sketch_gpu(rp, cs, vs, 1000, 50, 0)
+    monkeypatch.setenv("SFDG_ORTH_EVERY_SWEEP", "1")
+    b_every, _ = sketch_gpu(rp, cs, vs, 1000, 50, 0)
+    bo, _ = oracle.sketch(rp, cs, vs, 1000, 50, seed=0)
+    assert btb_rel(b_every, bo) <= 1e-10
+    assert btb_rel(b_adapt, b_every) <= 1e-10
