@@ -162,6 +162,231 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(TriArgs a) {
     }
 }
 
+// Row-distributed Householder tridiagonalisation, one CTA or a cluster of C CTAs.
+//
+// The full symmetric matrix lives in shared memory, row i on CTA (i % C), local row
+// i / C, owned by warp (i / C) % NW. Step k is fused with the update of step k-1:
+//   S1 (owner warp of row k): c_{k-1} = tau_{k-1}/2 p_{k-1}^T v_{k-1}; apply the rank-2
+//      update of step k-1 to row k; Householder (dlarfg) on row k -> v_k, tau_k; broadcast
+//      v_k, tau_k, c_{k-1} into every CTA of the cluster.
+//   S2 (every warp, rows i > k): a_ij -= v_i w_j + w_i v_j (step k-1, w = p - c v) and in
+//      the same pass p_k,i = tau_k sum_j a_ij v_k,j; broadcast p_k,i.
+// Two (cluster) barriers per step; each element is read and written once per step, with
+// lanes over columns (conflict-free rows). Algebra as tridiag_kernel (dsytd2).
+struct TriRowsArgs {
+    TriArgs a;
+    int C;      // CTAs in the cluster
+    int rows;   // ceil(n / C): local rows per CTA
+};
+
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <class T>
+__device__ __forceinline__ T* cluster_map(T* p, unsigned rank) {
+    unsigned long long out;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(p), "r"(rank));
+    return reinterpret_cast<T*>(out);
+}
+
+template <int C, int NT, int NTHR>
+__global__ void __launch_bounds__(NTHR) tridiag_rows_kernel(TriRowsArgs ra) {
+    constexpr int NW = NTHR / 32;
+    extern __shared__ double sm[];
+    __shared__ double s_sc[2][2];  // [k & 1] = {tau_k, c_{k-1}}
+    __shared__ double s_off[16];
+    __shared__ double red[32];
+    const TriArgs& a = ra.a;
+    const int n = a.n;
+    const unsigned rank = C > 1 ? cluster_rank() : 0u;
+    const int tid = threadIdx.x, lane = tid & 31, wl = tid >> 5;
+    const int nloc = (n - (int)rank + C - 1) / C;  // rows rank, rank + C, ...
+    double* A = sm;                                // rows x n
+    double* vbuf = sm + (size_t)ra.rows * n;       // 2 x n
+    double* pbuf = vbuf + 2 * n;                   // 2 x n
+    auto bar = [&]() {
+        if (C > 1) cluster_barrier();
+        else __syncthreads();
+    };
+    // load the owned rows; off-diagonal sum of squares over them
+    double off = 0.0;
+    for (int li = wl; li < nloc; li += NW) {
+        const int i = (int)rank + C * li;
+        for (int j = lane; j < n; j += 32) {
+            const double v = a.K[(size_t)i * a.ldk + j];
+            A[(size_t)li * n + j] = v;
+            if (j != i) off += v * v;
+        }
+    }
+    for (int j = tid; j < 4 * n; j += NTHR) vbuf[j] = 0.0;
+    if (tid < 4) (&s_sc[0][0])[tid] = 0.0;
+    off = block_sum(off, red);
+    if (tid == 0)
+        for (int r = 0; r < C; ++r) (C > 1 ? cluster_map(s_off, r) : s_off)[rank] = off;
+    bar();
+    off = 0.0;
+    for (int r = 0; r < C; ++r) off += s_off[r];  // same order on every CTA
+    double tol_sq = a.tol_sq;
+    if (a.d_fsq) {
+        const double ot = 1e-12 * fmax(*a.d_fsq, 1.0);
+        tol_sq = ot * ot;
+    }
+    if (!(off > tol_sq) || n == 1) {  // the reference's Jacobi would not rotate at all (la_core.cpp:33)
+        for (int li = wl; li < nloc; li += NW)
+            if (lane == 0) {
+                const int i = (int)rank + C * li;
+                a.d[i] = A[(size_t)li * n + i];
+                if (i + 1 < n) a.e[i] = 0.0;
+            }
+        if (rank == 0 && tid == 0) *a.trivial = 1;
+        return;
+    }
+    if (rank == 0 && tid == 0) *a.trivial = 0;
+    for (int k = 0; k + 1 < n; ++k) {
+        const int cur = k & 1, prv = cur ^ 1;
+        const double* vp = vbuf + prv * n;
+        const double* pp = pbuf + prv * n;
+        // ---- S1: owner warp of row k
+        if ((int)rank == k % C && wl == (k / C) % NW) {
+            double dsum = 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = 32 * t + lane;
+                if (j >= k && j < n) dsum += pp[j] * vp[j];
+            }
+            dsum = warp_sum(dsum);
+            const double cprev = 0.5 * s_sc[prv][0] * dsum;
+            const double vk = vp[k], wk = pp[k] - cprev * vp[k];
+            double* Ak = A + (size_t)(k / C) * n;
+            double x[NT];
+            double xs = 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = 32 * t + lane;
+                x[t] = 0.0;
+                if (j >= k && j < n) {
+                    const double vj = vp[j];
+                    const double val = Ak[j] - vk * (pp[j] - cprev * vj) - wk * vj;
+                    Ak[j] = val;
+                    x[t] = val;
+                    if (j >= k + 2) xs += val * val;
+                }
+            }
+            xs = warp_sum(xs);
+            __syncwarp();
+            const double alpha = Ak[k + 1];
+            double tau = 0.0, beta = alpha, scal = 0.0;
+            if (xs > 0.0) {
+                beta = -copysign(sqrt(alpha * alpha + xs), alpha);
+                tau = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = 32 * t + lane;
+                if (j >= k + 1 && j < n) {
+                    const double v = (j == k + 1) ? 1.0 : x[t] * scal;
+                    for (int r = 0; r < C; ++r) (C > 1 ? cluster_map(vbuf, r) : vbuf)[cur * n + j] = v;
+                    a.vh[(size_t)k * n + j] = v;
+                }
+            }
+            if (lane == 0) {
+                for (int r = 0; r < C; ++r) {
+                    double* sc = C > 1 ? cluster_map(&s_sc[cur][0], r) : &s_sc[cur][0];
+                    sc[0] = tau;
+                    sc[1] = cprev;
+                }
+                a.d[k] = Ak[k];
+                a.e[k] = beta;
+                a.tau[k] = tau;
+            }
+        }
+        bar();
+        // ---- S2: rows i > k: update of step k-1, p_k = tau_k A v_k
+        {
+            const double tau = s_sc[cur][0], cprev = s_sc[cur][1];
+            const double* vc = vbuf + cur * n;
+            double rv[NT], rw[NT], rc[NT];
+            const int t0 = (k + 1) >> 5;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = 32 * t + lane;
+                const bool on = t >= t0 && j > k && j < n;
+                rv[t] = on ? vp[j] : 0.0;
+                rw[t] = on ? pp[j] - cprev * vp[j] : 0.0;
+                rc[t] = on ? vc[j] : 0.0;
+            }
+            int li = wl;
+            {  // first local row index with global row > k owned by this warp
+                const int need = (k + 1 - (int)rank + C - 1) / C;  // smallest li with rank + C li > k
+                if (need > li) li += (need - li + NW - 1) / NW * NW;
+            }
+            // four rows per pass: independent accumulators, one 6-shuffle transposed reduction
+            for (; li < nloc; li += 4 * NW) {
+                double sr[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int lr = li + r * NW;
+                    sr[r] = 0.0;
+                    if (lr < nloc) {
+                        const int i = (int)rank + C * lr;
+                        const double vi = vp[i], wi = pp[i] - cprev * vp[i];
+                        double* Ai = A + (size_t)lr * n;
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) {
+                            const int j = 32 * t + lane;
+                            if (t >= t0 && j > k && j < n) {
+                                const double val = Ai[j] - vi * rw[t] - wi * rv[t];
+                                Ai[j] = val;
+                                sr[r] += val * rc[t];
+                            }
+                        }
+                    }
+                }
+                const bool h16 = lane & 16, h8 = lane & 8;
+                double a0 = h16 ? sr[2] : sr[0], a1 = h16 ? sr[3] : sr[1];
+                a0 += __shfl_xor_sync(0xffffffffu, h16 ? sr[0] : sr[2], 16);
+                a1 += __shfl_xor_sync(0xffffffffu, h16 ? sr[1] : sr[3], 16);
+                double c0 = h8 ? a1 : a0;
+                c0 += __shfl_xor_sync(0xffffffffu, h8 ? a0 : a1, 8);
+                c0 += __shfl_xor_sync(0xffffffffu, c0, 4);
+                c0 += __shfl_xor_sync(0xffffffffu, c0, 2);
+                c0 += __shfl_xor_sync(0xffffffffu, c0, 1);
+                // lanes 0, 8, 16, 24 hold rows 0..3; lanes +1..+C-1 of each group fan out to the cluster
+                const int r = lane >> 3, sub = lane & 7;
+                const int lr = li + r * NW;
+                if (lr < nloc) {
+                    const int i = (int)rank + C * lr;
+                    for (int q = sub; q < C; q += 8) (C > 1 ? cluster_map(pbuf, q) : pbuf)[cur * n + i] = c0 * tau;
+                }
+            }
+        }
+        bar();
+    }
+    if ((int)rank == (n - 1) % C && tid == 0) {
+        a.d[n - 1] = A[(size_t)((n - 1) / C) * n + n - 1];
+        a.tau[n - 1] = 0.0;
+        if (n >= 2) a.tau[n - 2] = 0.0;
+    }
+}
+
+// Branch-free double reciprocal: MUFU seed (rcp.approx.ftz.f64, ~2^-23) + two Newton
+// steps (~1 ulp). IEEE division carries a slow-path branch per divide, which serialises
+// the interleaved Sturm chains below; this keeps them independent.
+__device__ __forceinline__ double fast_rcp(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    double e = fma(-q, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-q, r, 1.0);
+    return fma(r, e, r);
+}
+
 // Sturm count: eigenvalues of T smaller than x (dlaebz recurrence with pivmin guard).
 __device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
     double q = d[0] - x;
@@ -175,7 +400,10 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
     return c;
 }
 
-// Warp per eigenvalue: the top `nval` eigenvalues, written in descending order.
+// Warp per eigenvalue: the top `nval` eigenvalues, written in descending order. Each lane
+// runs kShifts interleaved Sturm chains (independent divides overlap), so one step splits
+// the bracket into 32 * kShifts + 1 pieces (~7 bits per step instead of 5).
+constexpr int kShifts = 4;
 __global__ void bisect_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int nval,
                               const int* __restrict__ trivial, double* __restrict__ lam_desc) {
     extern __shared__ double sh[];
@@ -190,37 +418,65 @@ __global__ void bisect_kernel(const double* __restrict__ dg, const double* __res
     const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // descending index
     if (t >= nval) return;
     if (*trivial) {  // diagonal: eigenvalues are the sorted diagonal (stable, descending)
-        if (lane == 0) {
-            // t-th largest with stable tie order: value with rank t
-            for (int i = 0; i < n; ++i) {
-                int r = 0;
-                for (int j = 0; j < n; ++j) r += (d[j] > d[i] || (d[j] == d[i] && j < i));
-                if (r == t) lam_desc[t] = d[i];
-            }
+        for (int i = lane; i < n; i += 32) {
+            int r = 0;
+            for (int j = 0; j < n; ++j) r += (d[j] > d[i] || (d[j] == d[i] && j < i));
+            if (r == t) lam_desc[t] = d[i];
         }
         return;
     }
     double lo = 1e300, hi = -1e300, emax = 0.0;
-    for (int j = 0; j < n; ++j) {
+    for (int j = lane; j < n; j += 32) {
         const double r = (j > 0 ? sqrt(e2[j - 1]) : 0.0) + (j + 1 < n ? sqrt(e2[j]) : 0.0);
         lo = fmin(lo, d[j] - r);
         hi = fmax(hi, d[j] + r);
         emax = fmax(emax, e2[j]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
     }
     const double tnorm = fmax(fabs(lo), fabs(hi));
     const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax) * 1e3;
     lo -= 2.0 * 2.2e-16 * tnorm + pivmin;
     hi += 2.0 * 2.2e-16 * tnorm + pivmin;
     const int want = n - 1 - t;  // ascending index of the eigenvalue
-    double a = lo, b = hi;       // count(a) <= want < count(b)
-    for (int it = 0; it < 80; ++it) {
+    constexpr int P = 32 * kShifts;
+    constexpr double inv = 1.0 / (P + 1);
+    double a = lo, b = hi;  // count(a) <= want < count(b)
+    for (int it = 0; it < 40; ++it) {
         if (b - a <= 2.0 * 2.2e-16 * fmax(fabs(a), fabs(b)) + pivmin) break;
-        const double x = a + (b - a) * (double)(lane + 1) / 33.0;
-        const int c = sturm_count(d, e2, n, x, pivmin);
-        const unsigned above = __ballot_sync(0xffffffffu, c > want);  // lanes whose x is past the eigenvalue
-        const int first = above ? __ffs(above) - 1 : 32;
-        const double na = first > 0 ? a + (b - a) * (double)first / 33.0 : a;
-        const double nb = first < 32 ? a + (b - a) * (double)(first + 1) / 33.0 : b;
+        const double w = b - a;
+        double x[kShifts], q[kShifts];
+        int c[kShifts];
+#pragma unroll
+        for (int s = 0; s < kShifts; ++s) {
+            x[s] = a + w * ((double)(lane * kShifts + s + 1) * inv);
+            q[s] = d[0] - x[s];
+            if (fabs(q[s]) < pivmin) q[s] = -pivmin;
+            c[s] = q[s] < 0.0;
+        }
+        for (int j = 1; j < n; ++j) {
+            const double dj = d[j], ej = e2[j - 1];
+#pragma unroll
+            for (int s = 0; s < kShifts; ++s) {
+                q[s] = fma(-ej, fast_rcp(q[s]), dj - x[s]);
+                if (fabs(q[s]) < pivmin) q[s] = -pivmin;
+                c[s] += q[s] < 0.0;
+            }
+        }
+        int f = kShifts;  // first local shift past the eigenvalue
+#pragma unroll
+        for (int s = kShifts - 1; s >= 0; --s)
+            if (c[s] > want) f = s;
+        const unsigned above = __ballot_sync(0xffffffffu, f < kShifts);
+        const int L = above ? __ffs(above) - 1 : 32;
+        const int fL = __shfl_sync(0xffffffffu, f, L & 31);
+        const int m = L < 32 ? L * kShifts + fL : P;  // first point index with count > want
+        const double na = m > 0 ? a + w * ((double)m * inv) : a;
+        const double nb = m < P ? a + w * ((double)(m + 1) * inv) : b;
         a = na;
         b = nb;
     }
@@ -229,96 +485,145 @@ __global__ void bisect_kernel(const double* __restrict__ dg, const double* __res
 
 // Thread per eigenvalue: 3 steps of inverse iteration with a partially pivoted LU of
 // (T - lambda I) (LAPACK dgttrf/dgttrs algebra); X is n x ldx (column t = vector t).
+// T is staged in shared memory; the per-thread LU bands live in shared memory (or global
+// for large n) interleaved by thread; the solves carry their recurrences in registers and
+// multiply by stored pivot reciprocals, so the only divides are the n of the factorisation.
 __global__ void inviter_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int nval,
                                const double* __restrict__ lam, const int* __restrict__ trivial,
                                double* __restrict__ X, int ldx, double* __restrict__ work_g) {
-    extern __shared__ double work_s[];
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    extern __shared__ double sh_inv[];
+    __shared__ double s_tn;
+    double* d = sh_inv;
+    double* e = sh_inv + n;
+    const int nb = blockDim.x;
+    for (int j = threadIdx.x; j < n; j += nb) {
+        d[j] = dg[j];
+        e[j] = j + 1 < n ? eg[j] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tn = 0.0;
+        for (int j = 0; j < n; ++j) tn = fmax(tn, fabs(d[j]) + (j > 0 ? fabs(e[j - 1]) : 0.0) + fabs(e[j]));
+        s_tn = tn;
+    }
+    __syncthreads();
+    const int t = blockIdx.x * nb + threadIdx.x;
     if (t >= nval) return;
-    // per-thread LU bands + vector: shared memory when they fit (n <= 320), else global
-    double* work = work_g ? work_g : work_s;
-    const int slot = work_g ? t : threadIdx.x;
     if (*trivial) {  // identity eigenvectors in the stable descending order of the diagonal
         int idx = 0;
         for (int i = 0; i < n; ++i) {
             int r = 0;
-            for (int j = 0; j < n; ++j) r += (dg[j] > dg[i] || (dg[j] == dg[i] && j < i));
+            for (int j = 0; j < n; ++j) r += (d[j] > d[i] || (d[j] == d[i] && j < i));
             if (r == t) idx = i;
         }
         for (int i = 0; i < n; ++i) X[(size_t)i * ldx + t] = (i == idx) ? 1.0 : 0.0;
         return;
     }
-    double* U0 = work + (size_t)slot * 5 * n;  // diag of U
-    double* U1 = U0 + n;                    // 1st super
-    double* U2 = U1 + n;                    // 2nd super
-    double* Lm = U2 + n;                    // multipliers
-    double* x = Lm + n;
-    double tn = 0.0;
-    for (int j = 0; j < n; ++j) tn = fmax(tn, fabs(dg[j]) + (j > 0 ? fabs(eg[j - 1]) : 0.0) + (j + 1 < n ? fabs(eg[j]) : 0.0));
-    const double tiny = 2.2e-16 * fmax(tn, 1e-300);
+    // interleaved per-thread arrays: element j of thread s at [j * S + s]
+    const bool glob = work_g != nullptr;
+    const int S = glob ? gridDim.x * nb : nb;
+    const int slot = glob ? t : threadIdx.x;
+    double* base = glob ? work_g : sh_inv + 2 * n;
+    double* Ui = base;                      // 1 / diag(U)
+    double* U1 = base + (size_t)n * S;      // 1st super
+    double* U2 = base + 2 * (size_t)n * S;  // 2nd super (0 unless a swap)
+    double* Lm = base + 3 * (size_t)n * S;  // multipliers
+    double* x = base + 4 * (size_t)n * S;
+#define AT(arr, j) arr[(size_t)(j) * S + slot]
+    const double tiny = 2.2e-16 * fmax(s_tn, 1e-300);
     const double l = lam[t];
-    // factor (T - l I) = P L U ; pivot flags packed in the sign of Lm via a separate array
-    // (we store swaps in U2 >= 0 convention: keep a small local bitmask per 64 rows)
-    unsigned long long swaps[16];  // n <= 1024
-    for (int i = 0; i < 16; ++i) swaps[i] = 0ull;
-    double a = dg[0] - l;  // current diagonal
-    double b = n > 1 ? eg[0] : 0.0;  // current super
+    unsigned swapw = 0;  // row-swap flags of the current 32-row word
+    double a = d[0] - l;
+    double b = n > 1 ? e[0] : 0.0;
+    unsigned* flags = reinterpret_cast<unsigned*>(base + 5 * (size_t)n * S);  // ceil(n/32) words per thread
     for (int j = 0; j + 1 < n; ++j) {
-        const double c = eg[j];               // sub-diagonal below a
-        const double dn = dg[j + 1] - l;      // next diagonal
-        const double bn = j + 2 < n ? eg[j + 1] : 0.0;  // next super
+        const double c = e[j];
+        const double dn = d[j + 1] - l;
+        const double bn = j + 2 < n ? e[j + 1] : 0.0;
+        double u0;
         if (fabs(a) >= fabs(c)) {
-            const double m = (a != 0.0) ? c / a : 0.0;
-            U0[j] = a;
-            U1[j] = b;
-            U2[j] = 0.0;
-            Lm[j] = m;
+            const double r = a != 0.0 ? fast_rcp(a) : 0.0;
+            const double m = c * r;
+            u0 = a;
+            AT(U1, j) = b;
+            AT(U2, j) = 0.0;
+            AT(Lm, j) = m;
             a = dn - m * b;
             b = bn;
         } else {
-            const double m = a / c;
-            U0[j] = c;
-            U1[j] = dn;
-            U2[j] = bn;
-            Lm[j] = m;
-            swaps[j >> 6] |= 1ull << (j & 63);
+            const double m = a * fast_rcp(c);
+            u0 = c;
+            AT(U1, j) = dn;
+            AT(U2, j) = bn;
+            AT(Lm, j) = m;
+            swapw |= 1u << (j & 31);
             a = b - m * dn;
             b = -m * bn;
         }
-    }
-    U0[n - 1] = a;
-    for (int j = 0; j < n; ++j)
-        if (fabs(U0[j]) < tiny) U0[j] = U0[j] < 0.0 ? -tiny : tiny;
-    // deterministic distinct start vector
-    uint64_t s = 0x9E3779B97F4A7C15ull * (uint64_t)(t + 1);
-    for (int j = 0; j < n; ++j) {
-        s ^= s >> 12;
-        s ^= s << 25;
-        s ^= s >> 27;
-        x[j] = (double)((s * 2685821657736338717ull) >> 11) * 0x1.0p-53 - 0.5;
-    }
-    for (int it = 0; it < 3; ++it) {
-        // forward: apply P and L
-        for (int j = 0; j + 1 < n; ++j) {
-            const bool sw = (swaps[j >> 6] >> (j & 63)) & 1ull;
-            if (sw) {
-                const double tmp = x[j];
-                x[j] = x[j + 1];
-                x[j + 1] = tmp - Lm[j] * x[j];
-            } else {
-                x[j + 1] -= Lm[j] * x[j];
-            }
+        if (fabs(u0) < tiny) u0 = u0 < 0.0 ? -tiny : tiny;
+        AT(Ui, j) = fast_rcp(u0);
+        if ((j & 31) == 31) {
+            flags[(size_t)(j >> 5) * S + slot] = swapw;
+            swapw = 0;
         }
-        // backward: U x = y
-        x[n - 1] /= U0[n - 1];
-        if (n >= 2) x[n - 2] = (x[n - 2] - U1[n - 2] * x[n - 1]) / U0[n - 2];
-        for (int j = n - 3; j >= 0; --j) x[j] = (x[j] - U1[j] * x[j + 1] - U2[j] * x[j + 2]) / U0[j];
-        double nrm = 0.0;
-        for (int j = 0; j < n; ++j) nrm += x[j] * x[j];
-        nrm = 1.0 / sqrt(nrm);
-        for (int j = 0; j < n; ++j) x[j] *= nrm;
     }
-    for (int j = 0; j < n; ++j) X[(size_t)j * ldx + t] = x[j];
+    if (n >= 1) {
+        if (((n - 2) & 31) != 31 && n >= 2) flags[(size_t)((n - 2) >> 5) * S + slot] = swapw;
+        double u0 = a;
+        if (fabs(u0) < tiny) u0 = u0 < 0.0 ? -tiny : tiny;
+        AT(Ui, n - 1) = 1.0 / u0;
+    }
+    // deterministic distinct start vector
+    uint64_t sd = 0x9E3779B97F4A7C15ull * (uint64_t)(t + 1);
+    for (int j = 0; j < n; ++j) {
+        sd ^= sd >> 12;
+        sd ^= sd << 25;
+        sd ^= sd >> 27;
+        AT(x, j) = (double)((sd * 2685821657736338717ull) >> 11) * 0x1.0p-53 - 0.5;
+    }
+    double scale = 1.0;
+    for (int it = 0; it < 3; ++it) {
+        // forward: apply P and L (scaled by the previous normalisation)
+        double xj = AT(x, 0) * scale;
+        unsigned fw = 0;
+        for (int j = 0; j + 1 < n; ++j) {
+            if ((j & 31) == 0) fw = flags[(size_t)(j >> 5) * S + slot];
+            const double xn = AT(x, j + 1) * scale;
+            const double m = AT(Lm, j);
+            double keep, carry;
+            if ((fw >> (j & 31)) & 1u) {
+                keep = xn;
+                carry = xj - m * xn;
+            } else {
+                keep = xj;
+                carry = xn - m * xj;
+            }
+            AT(x, j) = keep;
+            xj = carry;
+        }
+        // backward: U x = y, with the squared norm on the side
+        double x1 = xj * AT(Ui, n - 1);
+        AT(x, n - 1) = x1;
+        double nrm = x1 * x1;
+        double x0 = x1, x2 = 0.0;
+        if (n >= 2) {
+            x0 = (AT(x, n - 2) - AT(U1, n - 2) * x1) * AT(Ui, n - 2);
+            AT(x, n - 2) = x0;
+            nrm += x0 * x0;
+            x2 = x1;
+            x1 = x0;
+        }
+        for (int j = n - 3; j >= 0; --j) {
+            const double v = (AT(x, j) - AT(U1, j) * x1 - AT(U2, j) * x2) * AT(Ui, j);
+            AT(x, j) = v;
+            nrm += v * v;
+            x2 = x1;
+            x1 = v;
+        }
+        scale = 1.0 / sqrt(nrm);
+    }
+    for (int j = 0; j < n; ++j) X[(size_t)j * ldx + t] = AT(x, j) * scale;
+#undef AT
 }
 
 // Warp per cluster start: orthonormalise the cluster's vectors (MGS twice) and resolve the
@@ -438,29 +743,134 @@ __global__ void cluster_kernel(const double* __restrict__ dg, const double* __re
         for (int a = 0; a < c; ++a) lam[t0 + a] = C[a * c + a];
 }
 
-// U = Q X with Q = H_0 H_1 ... H_{n-3}: apply reflectors last-to-first. One CTA per
-// 32 columns of X; the reflector loop is sequential, each step a dot + axpy per column.
-__global__ void backtransform_kernel(const double* __restrict__ vh, const double* __restrict__ tau, int n, int nval,
-                                     const int* __restrict__ trivial, double* __restrict__ X, int ldx) {
+// U = Q X with Q = H_0 H_1 ... H_{n-3}: apply reflectors last-to-first. Warp per column
+// of X, the column in registers (lane owns rows lane + 32 t); the reflectors are staged
+// through shared memory in chunks of R rows (coalesced), one block barrier per chunk.
+template <int NT>
+__global__ void __launch_bounds__(256) backtransform_kernel(const double* __restrict__ vh,
+                                                            const double* __restrict__ tau, int n, int nval,
+                                                            const int* __restrict__ trivial, double* __restrict__ X,
+                                                            int ldx, int R) {
     if (*trivial) return;
-    extern __shared__ double colbuf[];
+    extern __shared__ double vs[];  // R x n reflector rows, then R taus
+    double* ts = vs + (size_t)R * n;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int col = blockIdx.x * (blockDim.x >> 5) + w;  // warp per column, kept in shared memory
-    if (col >= nval) return;
-    double* x = colbuf + (size_t)w * n;
-    for (int j = lane; j < n; j += 32) x[j] = X[(size_t)j * ldx + col];
-    __syncwarp();
-    for (int k = n - 3; k >= 0; --k) {
-        const double tk = tau[k];
-        if (tk == 0.0) continue;
-        const double* v = vh + (size_t)k * n;
-        double s = 0.0;
-        for (int j = k + 1 + lane; j < n; j += 32) s += v[j] * x[j];
-        s = warp_sum(s) * tk;
-        for (int j = k + 1 + lane; j < n; j += 32) x[j] -= s * v[j];
-        __syncwarp();
+    const int col = blockIdx.x * (blockDim.x >> 5) + w;
+    const bool active = col < nval;
+    double x[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const int j = 32 * t + lane;
+        x[t] = (active && j < n) ? X[(size_t)j * ldx + col] : 0.0;
     }
-    for (int j = lane; j < n; j += 32) X[(size_t)j * ldx + col] = x[j];
+    for (int hi = n - 3; hi >= 0; hi -= R) {  // chunk of reflectors k = lo .. hi
+        const int lo = max(0, hi - R + 1);
+        __syncthreads();
+        for (int r = 0; r <= hi - lo; ++r) {
+            const double* src = vh + (size_t)(lo + r) * n;
+            for (int j = lo + r + 1 + threadIdx.x; j < n; j += blockDim.x) vs[(size_t)r * n + j] = src[j];
+        }
+        for (int r = threadIdx.x; r <= hi - lo; r += blockDim.x) ts[r] = tau[lo + r];
+        __syncthreads();
+        if (!active) continue;
+        for (int k = hi; k >= lo; --k) {
+            const double tk = ts[k - lo];
+            if (tk == 0.0) continue;
+            const double* v = vs + (size_t)(k - lo) * n;
+            double s = 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = 32 * t + lane;
+                if (j > k && j < n) s += v[j] * x[t];
+            }
+            s = warp_sum(s) * tk;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = 32 * t + lane;
+                if (j > k && j < n) x[t] -= s * v[j];
+            }
+        }
+    }
+    if (!active) return;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const int j = 32 * t + lane;
+        if (j < n) X[(size_t)j * ldx + col] = x[t];
+    }
+}
+
+template <int NT>
+void launch_backtransform(const double* vh, const double* tau, int n, int nval, const int* trivial, double* X,
+                          int ldx, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        allow_max_dynamic_smem(backtransform_kernel<NT>);
+        attr = true;
+    }
+    const int R = std::max(1, std::min(n, (int)((96 * 1024) / (sizeof(double) * (n + 1)))));
+    const size_t smem = (size_t)R * (n + 1) * sizeof(double);
+    LAUNCH(backtransform_kernel<NT>, ceil_div(nval, 8), 256, smem, st, vh, tau, n, nval, trivial, X, ldx, R);
+}
+
+void backtransform(const double* vh, const double* tau, int n, int nval, const int* trivial, double* X, int ldx,
+                   cudaStream_t st) {
+    const int nt = (n + 31) / 32;
+    if (nt <= 4) launch_backtransform<4>(vh, tau, n, nval, trivial, X, ldx, st);
+    else if (nt <= 8) launch_backtransform<8>(vh, tau, n, nval, trivial, X, ldx, st);
+    else if (nt <= 16) launch_backtransform<16>(vh, tau, n, nval, trivial, X, ldx, st);
+    else launch_backtransform<32>(vh, tau, n, nval, trivial, X, ldx, st);
+}
+
+template <int C, int NT, int NTHR>
+void launch_rows(const TriRowsArgs& ra, size_t smem, cudaStream_t st) {
+    auto* fn = tridiag_rows_kernel<C, NT, NTHR>;
+    static bool attr = false;
+    if (!attr) {
+        allow_max_dynamic_smem(fn);
+        CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ra.C);
+    cfg.blockDim = dim3(NTHR);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ra.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, fn, ra));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// Row-distributed tridiagonalisation when the full matrix fits the shared memory of a
+// cluster of <= 16 CTAs (n <= ~670); false -> the caller uses the packed kernel.
+bool launch_tridiag_rows(const TriArgs& a, cudaStream_t st) {
+    static const char* env = getenv("SFDG_TRIDIAG");
+    if (env && env[0] == 'p') return false;  // packed single-CTA kernel (A/B testing)
+    const int n = a.n;
+    const int nt = (n + 31) / 32;
+    for (int C = 1; C <= 16; C *= 2) {
+        const int rows = (n + C - 1) / C;
+        const size_t smem = ((size_t)rows * n + 4 * (size_t)n) * sizeof(double);
+        if (smem > 220 * 1024) continue;
+        TriRowsArgs ra{a, C, rows};
+        if (C == 1 && nt <= 4) launch_rows<1, 4, 512>(ra, smem, st);
+        else if (C == 1 && nt <= 8) launch_rows<1, 8, 512>(ra, smem, st);
+        else if (C == 2 && nt <= 8) launch_rows<2, 8, 512>(ra, smem, st);
+        else if (C == 4 && nt <= 8) launch_rows<4, 8, 512>(ra, smem, st);
+        else if (C == 4 && nt <= 12) launch_rows<4, 12, 256>(ra, smem, st);
+        else if (C == 8 && nt <= 12) launch_rows<8, 12, 256>(ra, smem, st);
+        else if (C == 8 && nt <= 16) launch_rows<8, 16, 256>(ra, smem, st);
+        else if (C == 16 && nt <= 16) launch_rows<16, 16, 256>(ra, smem, st);
+        else if (C == 16 && nt <= 21) launch_rows<16, 21, 256>(ra, smem, st);
+        else return false;
+        return true;
+    }
+    return false;
 }
 
 }  // namespace
@@ -487,38 +897,41 @@ void eigh_tri(const double* K, int n, int ldk, double off_tol, const double* d_f
     a.vh = scr.take<double>((int64_t)n * n);
     a.tau = scr.take<double>(n);
     a.trivial = scr.take<int>(1);
-    double* work = scr.take<double>((int64_t)nval * 5 * n);
+    const int64_t inv_slots = (int64_t)ceil_div(nval, 64) * 64;
+    double* work = scr.take<double>(inv_slots * (5 * (int64_t)n + (n + 31) / 32 + 1));
     static bool attr = false;
     if (!attr) {
         allow_max_dynamic_smem(tridiag_kernel<true>);
         allow_max_dynamic_smem(inviter_kernel);
-        allow_max_dynamic_smem(backtransform_kernel);
         attr = true;
     }
     {
         ProfScope prof("eigh_tridiag", st);
-        const size_t smem = use_smem ? (packed + 2 * (size_t)n) * sizeof(double) : 0;
-        if (use_smem) LAUNCH(tridiag_kernel<true>, 1, kTriThreads, smem, st, a);
-        else LAUNCH(tridiag_kernel<false>, 1, kTriThreads, 0, st, a);
+        if (!launch_tridiag_rows(a, st)) {
+            const size_t smem = use_smem ? (packed + 2 * (size_t)n) * sizeof(double) : 0;
+            if (use_smem) LAUNCH(tridiag_kernel<true>, 1, kTriThreads, smem, st, a);
+            else LAUNCH(tridiag_kernel<false>, 1, kTriThreads, 0, st, a);
+        }
     }
     {
         ProfScope prof("eigh_bisect", st);
-        LAUNCH(bisect_kernel, ceil_div(nval, 8), 256, 2 * (size_t)n * sizeof(double), st, a.d, a.e, n, nval, a.trivial,
-               values);
+        LAUNCH(bisect_kernel, ceil_div(nval, 4), 128, 2 * (size_t)n * sizeof(double), st, a.d, a.e, n, nval,
+               a.trivial, values);
     }
     {
         ProfScope prof("eigh_vectors", st);
-        const int ith = 8;  // threads per block: 8 x 5n doubles of LU bands in shared memory
-        const size_t ismem = (size_t)ith * 5 * n * sizeof(double);
+        // per thread: 5n doubles of LU bands + ceil(n/32) flag words; T staged (2n doubles)
+        const int ith = 8;
+        const size_t per = 5 * (size_t)n * sizeof(double) + (size_t)((n + 31) / 32) * sizeof(unsigned);
+        const size_t ismem = 2 * (size_t)n * sizeof(double) + ith * per;
         if (ismem <= 96 * 1024)
             LAUNCH(inviter_kernel, ceil_div(nval, ith), ith, ismem, st, a.d, a.e, n, nval, values, a.trivial, vectors,
                    ldv, (double*)nullptr);
         else
-            LAUNCH(inviter_kernel, ceil_div(nval, 64), 64, 0, st, a.d, a.e, n, nval, values, a.trivial, vectors, ldv,
-                   work);
+            LAUNCH(inviter_kernel, ceil_div(nval, 64), 64, 2 * (size_t)n * sizeof(double), st, a.d, a.e, n, nval,
+                   values, a.trivial, vectors, ldv, work);
         LAUNCH(cluster_kernel, nval, 32, 0, st, a.d, a.e, n, nval, values, a.trivial, vectors, ldv, fallback);
-        LAUNCH(backtransform_kernel, ceil_div(nval, 8), 256, 8 * (size_t)n * sizeof(double), st, a.vh, a.tau, n, nval,
-               a.trivial, vectors, ldv);
+        backtransform(a.vh, a.tau, n, nval, a.trivial, vectors, ldv, st);
     }
 }
 

@@ -106,7 +106,7 @@ def test_csr_products_empty_rows_and_buffer():
 
 
 # ---------------------------------------------------------------- dense kernels
-@pytest.mark.parametrize("n", [1, 2, 3, 7, 33, 100, 200, 257])
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 33, 100, 129, 200, 257])
 def test_eigh_vs_oracle(oracle, n):
     rng = np.random.default_rng(n)
     a = rng.standard_normal((n + 3, n))
@@ -119,6 +119,37 @@ def test_eigh_vs_oracle(oracle, n):
     assert np.all(np.diff(vals) <= 0)
     assert np.max(np.abs(vecs.T @ vecs - np.eye(n))) <= 1e-12
     assert np.max(np.abs(vecs @ np.diag(vals) @ vecs.T - k)) <= 1e-11 * scale
+
+
+@pytest.mark.parametrize("n", [160, 300, 400, 520, 700])
+def test_eigh_large_cluster_tridiag(n):
+    """Sizes that take the 2/4/8/16-CTA cluster tridiagonalisation (and n = 700 the packed
+    fallback); checked against numpy's LAPACK eigh (the Jacobi oracle is too slow here)."""
+    rng = np.random.default_rng(1000 + n)
+    a = rng.standard_normal((n + 5, n))
+    k = a.T @ a
+    vals, vecs = P.eigh(k, 1e-12 * (a ** 2).sum())
+    ref = np.linalg.eigvalsh(k)[::-1]
+    scale = np.abs(ref).max()
+    assert np.max(np.abs(vals - ref)) <= 1e-12 * scale
+    assert np.max(np.abs(vecs.T @ vecs - np.eye(n))) <= 1e-11
+    assert np.max(np.abs(vecs @ np.diag(vals) @ vecs.T - k)) <= 1e-11 * scale
+
+
+@pytest.mark.parametrize("n", [100, 200])
+def test_eigh_clustered_spectrum(n):
+    """Repeated and near-repeated eigenvalues (cluster Rayleigh-Ritz path) at both sizes
+    the c2 flush uses."""
+    rng = np.random.default_rng(n)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.repeat(np.linspace(10.0, 1.0, n // 4), 4)[:n].copy()
+    lam[::7] += 1e-9
+    k = (q * lam) @ q.T
+    k = 0.5 * (k + k.T)
+    vals, vecs = P.eigh(k, 1e-12)
+    assert np.max(np.abs(vals - np.sort(lam)[::-1])) <= 1e-12 * 10
+    assert np.max(np.abs(vecs.T @ vecs - np.eye(n))) <= 1e-11
+    assert np.max(np.abs(vecs @ np.diag(vals) @ vecs.T - k)) <= 1e-11 * 10
 
 
 def test_eigh_degenerate_and_diagonal():

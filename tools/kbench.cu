@@ -124,6 +124,10 @@ int main(int argc, char** argv) {
                    s2.reset();
                    eigh(K, n, n, 1e-12 * 1e4 * n, nullptr, vals_d, vecs, n, err, s2, st);
                }));
+        printf("eigh n=%-4d top %d %8.2f us\n", n, ell, time_us(st, r, [&] {
+                   s2.reset();
+                   eigh(K, n, n, 1e-12 * 1e4 * n, nullptr, vals_d, vecs, n, err, s2, st, ell);
+               }));
     }
     int herr = 0;
     cudaMemcpy(&herr, err, 4, cudaMemcpyDeviceToHost);
