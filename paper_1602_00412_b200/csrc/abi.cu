@@ -8,7 +8,9 @@
 // and each segment is copied to the device buffer in one transfer.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <new>
 #include <string>
@@ -70,19 +72,70 @@ double csr_frob(const int64_t* row_ptr, const double* vals, size_t m) {
 
 }  // namespace
 
+// Position in the reference's state sequence at a flush boundary: the Rng stream and the
+// verifier (sketch.cpp:25-32 threads both through every flush).
+struct FlushState {
+    RngPos pos;
+    Verifier ver;
+};
+
+bool same_state(const FlushState& a, const FlushState& b) {
+    return a.pos.words == b.pos.words && a.pos.has_spare == b.pos.has_spare && a.ver.i == b.ver.i &&
+           a.ver.delta_spent == b.ver.delta_spent;
+}
+
+// Flush pipeline.
+//
+// Flushes are independent SparseShrink problems except for (1) the Rng / verifier state
+// they inherit and (2) the dense_shrink chain B_f = dense_shrink([B_{f-1}; B'_f]). So the
+// sketcher keeps up to 4 flushes in flight, each on its own lane (engine, stream,
+// buffers): a flush starts from the state its predecessor is predicted to end in (one
+// attempt that verifies), and is re-run from the true state if the prediction was wrong
+// (a retry or an exact-recovery flush upstream). Flushes commit strictly in order; a commit
+// queues the dense shrink on the chain stream. Results do not depend on the lane count or
+// on timing: every flush is computed from its true start state, and the adaptive
+// orthonormalisation interval of flush f depends only on flush f - kLag, which has always
+// committed when f starts.
 class Sketcher {
   public:
     Sketcher(const SketchCfg& c, int device) : cfg(c) {
         validate_cfg(cfg);
         nnz_trigger = (int64_t)(cfg.ell * cfg.d);
-        eng = std::make_unique<Engine>(device, (int)cfg.d, (int)cfg.ell, cfg.seed, (uint64_t)nnz_trigger + cfg.d,
-                                       (int)cfg.d);
-        ver.delta = cfg.delta;
-        buf_rp.assign(1, 0);
+        CK(cudaSetDevice(device));
+        const int lanes_n = lane_count();
+        const uint64_t per_flush = (uint64_t)cfg.d * cfg.ell + cfg.d + 16;  // raw words drawn per attempt
+        rng.init(cfg.seed, std::max<uint64_t>((uint64_t)(lanes_n + 3) * per_flush, 1 << 20), device);
+        chain = std::make_unique<Engine>(device, (int)cfg.d, (int)cfg.ell, cfg.seed, 1, 1, &rng, true);
+        lanes.resize(lanes_n);
+        for (auto& L : lanes) {
+            L.eng = std::make_unique<Engine>(device, (int)cfg.d, (int)cfg.ell, cfg.seed, (uint64_t)nnz_trigger + cfg.d,
+                                             (int)cfg.d, &rng, false);
+            CK(cudaEventCreateWithFlags(&L.ev, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&L.ev_bp_free, cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&ev_verify, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_verify, chain->st));
+        hist.assign(kLag, Hist{});
+        committed.ver.delta = cfg.delta;
+        fill = 0;
+        lanes[0].phase = Lane::Filling;
+        lanes[0].clear_rows();
+    }
+
+    ~Sketcher() {
+        try {
+            sync_all();
+        } catch (...) {
+        }
+        for (auto& L : lanes) {
+            if (L.ev) cudaEventDestroy(L.ev);
+            if (L.ev_bp_free) cudaEventDestroy(L.ev_bp_free);
+        }
+        if (ev_verify) cudaEventDestroy(ev_verify);
     }
 
     void append_host(const int64_t* rp, const uint32_t* cols, const double* vals, size_t nrows, size_t* done) {
-        eng->set_device();
+        chain->set_device();
         if (done) *done = 0;
         size_t r = 0;
         while (r < nrows) {
@@ -103,26 +156,31 @@ class Sketcher {
             if (good > 0) commit_host(rp, cols, vals, r, good);
             if (good < take) {
                 if (done) *done = r + good;
+                finish_copies();
                 throw invalid_argument(err);
             }
             r += take;
             if (done) *done = r;
             maybe_flush();
         }
+        finish_copies();  // the caller may reuse its (possibly pinned) buffers on return
+        pump();
     }
 
     void append_device(const int64_t* h_rp, const uint32_t* d_cols, const double* d_vals, size_t nrows, size_t* done) {
-        eng->set_device();
+        chain->set_device();
         if (done) *done = 0;
         if (nrows == 0) return;
         for (size_t i = 0; i < nrows; ++i)
             if (h_rp[i + 1] < h_rp[i]) throw invalid_argument("append_row: index/value length mismatch");
-        int64_t* d_rp = eng->scr.take<int64_t>((int64_t)nrows + 1);
-        CK(cudaMemcpyAsync(d_rp, h_rp, (nrows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, eng->st));
+        Engine& E = *lanes[fill].eng;  // idle apart from row copies
+        E.scr.reset();
+        int64_t* d_rp = E.scr.take<int64_t>((int64_t)nrows + 1);
+        CK(cudaMemcpyAsync(d_rp, h_rp, (nrows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, E.st));
         int kind = 0;
-        const int64_t bad = validate_rows_device(d_rp, (int64_t)nrows, d_cols, d_vals, (uint32_t)cfg.d, &kind,
-                                                 eng->scr, eng->st);
-        eng->scr.reset();
+        const int64_t bad = validate_rows_device(d_rp, (int64_t)nrows, d_cols, d_vals, (uint32_t)cfg.d, &kind, E.scr,
+                                                 E.st);
+        E.scr.reset();
         const size_t limit = bad < 0 ? nrows : (size_t)bad;
         size_t r = 0;
         while (r < limit) {
@@ -132,104 +190,170 @@ class Sketcher {
             if (done) *done = r;
             maybe_flush();
         }
+        finish_copies();
+        pump();
         if (bad >= 0)
             throw invalid_argument((kind & ERR_BAD_INDEX) ? "append_row: column index out of range or not increasing"
                                                           : "append_row: non-finite value");
     }
 
     void finalize(double* out) {  // sketch.cpp:34-45
-        eng->set_device();
-        eng->sync();
-        eng->check_errors();
-        if (buf_rows() > 0) {
-            if (buf_rows() >= cfg.ell) {
+        chain->set_device();
+        drain();
+        Lane& F = lanes[fill];
+        if (F.rows() > 0) {
+            if (F.rows() >= cfg.ell) {
                 flush();
+                drain();
             } else {
-                upload_row_ptr();
-                const int m = (int)buf_rows();
-                eng->densify_into_stack(eng->lp);
-                eng->scr.reset();
-                eng->dense_shrink_stack(eng->Mt[eng->cur], 2 * eng->lp, (int)cfg.ell, eng->lp, m,
-                                        eng->Mt[eng->cur ^ 1], 2 * eng->lp);
-                eng->check_errors();
-                eng->cur ^= 1;
-                clear_buffer();
+                upload_row_ptr(F);
+                CK(cudaStreamSynchronize(F.eng->st));
+                const int m = (int)F.rows();
+                Engine& C = *chain;
+                C.scr.reset();
+                C.densify_into_stack(F.eng->a, C.lp);
+                C.dense_shrink_stack(C.Mt[C.cur], 2 * C.lp, (int)cfg.ell, C.lp, m, C.Mt[C.cur ^ 1], 2 * C.lp);
+                C.check_errors();
+                C.cur ^= 1;
+                F.clear_rows();
             }
         }
         if (out) get_sketch(out);
     }
 
     void get_sketch(double* out) {
-        eng->set_device();
-        eng->sync();
-        eng->check_errors();
-        eng->scr.reset();
-        eng->sketch_to_host(out);
+        chain->set_device();
+        drain();
+        chain->sync();
+        chain->check_errors();
+        chain->scr.reset();
+        chain->sketch_to_host(out);
     }
 
     void get_sketch_device(double* d_out, size_t ld) {
-        eng->set_device();
-        eng->sync();
-        eng->check_errors();
-        copy2d(eng->Mt[eng->cur], (int)cfg.d, (int)cfg.ell, 2 * eng->lp, d_out, (int)ld, eng->st);
-        eng->sync();
+        chain->set_device();
+        drain();
+        chain->sync();
+        chain->check_errors();
+        copy2d(chain->Mt[chain->cur], (int)cfg.d, (int)cfg.ell, 2 * chain->lp, d_out, (int)ld, chain->st);
+        chain->sync();
     }
 
     void stats(sfdg_stats* s) {
-        eng->set_device();
-        eng->sync();
+        chain->set_device();
+        drain();
+        chain->sync();
+        const Lane& F = lanes[fill];
         s->flush_count = flushes;
         s->attempt_total = attempts;
-        s->verifier = {ver.i, ver.delta, ver.c_verify, ver.delta_spent};
-        s->buffer_rows = buf_rows();
-        s->buffer_nnz = (size_t)buf_nnz;
-        s->buffer_frob_sq = buf_frob;
+        s->verifier = {committed.ver.i, committed.ver.delta, committed.ver.c_verify, committed.ver.delta_spent};
+        s->buffer_rows = F.rows();
+        s->buffer_nnz = (size_t)F.nnz;
+        s->buffer_frob_sq = F.frob;
         s->rng.seed = cfg.seed;
-        s->rng.words = eng->pos.words;
-        s->rng.has_spare = eng->pos.has_spare ? 1 : 0;
-        s->rng.spare = eng->pos.has_spare ? eng->rng.spare_value(eng->st) : 0.0;
+        s->rng.words = committed.pos.words;
+        s->rng.has_spare = committed.pos.has_spare ? 1 : 0;
+        s->rng.spare = committed.pos.has_spare ? rng.spare_value(committed.pos, chain->st) : 0.0;
     }
 
     void get_buffer(int64_t* rp, uint32_t* cols, double* vals) {
-        eng->set_device();
-        if (rp) std::memcpy(rp, buf_rp.data(), buf_rp.size() * sizeof(int64_t));
-        if (buf_nnz > 0) {
-            if (cols) CK(cudaMemcpyAsync(cols, eng->a.col, buf_nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost, eng->st));
-            if (vals) CK(cudaMemcpyAsync(vals, eng->a.val, buf_nnz * sizeof(double), cudaMemcpyDeviceToHost, eng->st));
+        chain->set_device();
+        Lane& F = lanes[fill];
+        CK(cudaStreamSynchronize(F.eng->st));
+        if (rp) std::memcpy(rp, F.rp.data(), F.rp.size() * sizeof(int64_t));
+        if (F.nnz > 0) {
+            if (cols) CK(cudaMemcpyAsync(cols, F.eng->a.col, F.nnz * sizeof(uint32_t), cudaMemcpyDeviceToHost, F.eng->st));
+            if (vals) CK(cudaMemcpyAsync(vals, F.eng->a.val, F.nnz * sizeof(double), cudaMemcpyDeviceToHost, F.eng->st));
         }
-        eng->sync();
+        CK(cudaStreamSynchronize(F.eng->st));
     }
 
     void synchronize() {
-        eng->set_device();
-        eng->sync();
+        chain->set_device();
+        drain();
+        chain->sync();
     }
 
     // Back to a freshly constructed sketcher with `seed`, reusing every allocation.
     void reset(uint64_t seed) {
-        eng->set_device();
-        eng->sync();
+        chain->set_device();
+        abort_inflight();
         cfg.seed = seed;
-        eng->rng.restart(seed);
-        eng->pos = RngPos{};
+        rng.restart(seed);
         for (int i = 0; i < 2; ++i)
-            CK(cudaMemsetAsync(eng->Mt[i], 0, (size_t)cfg.d * 2 * eng->lp * sizeof(double), eng->st));
-        eng->cur = 0;
-        CK(cudaMemsetAsync(eng->d_err, 0, sizeof(int), eng->st));
-        eng->sync();
-        ver = Verifier{};
-        ver.delta = cfg.delta;
-        clear_buffer();
+            CK(cudaMemsetAsync(chain->Mt[i], 0, (size_t)cfg.d * 2 * chain->lp * sizeof(double), chain->st));
+        chain->cur = 0;
+        CK(cudaMemsetAsync(chain->d_err, 0, sizeof(int), chain->st));
+        chain->sync();
+        for (auto& L : lanes) {
+            CK(cudaMemsetAsync(L.eng->d_err, 0, sizeof(int), L.eng->st));
+            CK(cudaStreamSynchronize(L.eng->st));
+            L.phase = Lane::Idle;
+            L.clear_rows();
+        }
+        committed = FlushState{};
+        committed.ver.delta = cfg.delta;
+        hist.assign(kLag, Hist{});
+        next_id = 0;
+        fill = 0;
+        lanes[0].phase = Lane::Filling;
         flushes = attempts = 0;
     }
 
   private:
-    size_t buf_rows() const { return buf_rp.size() - 1; }
+    struct Lane {
+        std::unique_ptr<Engine> eng;
+        enum Phase { Idle, Filling, Preparing, Shrinking, Verifying, Done } phase = Idle;
+        std::vector<int64_t> rp{0};
+        std::vector<int> rp32;
+        int64_t nnz = 0;
+        double frob = 0.0;
+        uint64_t id = 0;
+        FlushState start, cur;
+        int interval = 1, interval_base = 1, interval_used = 1;
+        RngPos pos0;
+        size_t attempt = 0;
+        double delta_hat = 0.0, kappa_last = 0.0;
+        int last_since = 1;
+        cudaEvent_t ev = nullptr;          // completion of the queued phase
+        cudaEvent_t ev_bp_free = nullptr;  // the chain finished reading Bp
+        bool bp_pending = false;
+        size_t rows() const { return rp.size() - 1; }
+        void clear_rows() {
+            rp.assign(1, 0);
+            nnz = 0;
+            frob = 0.0;
+        }
+    };
+    // The orthonormalisation interval of flush f comes from flush f - kLag (>= the lane
+    // count, so committed when f starts): the same schedule for every lane count.
+    static constexpr uint64_t kLag = 4;
+    struct Hist {
+        double kappa_last = 0.0;
+        int last_since = 1;
+        bool valid = false;
+    };
+
+    // Flushes in flight: 4, or fewer when 4 lanes' working sets (CSR + CSC of ell*d nnz,
+    // Y/Yt of d x lp, W/B' of d x lp, a share of the Rng ring) would exceed 30% of the HBM.
+    // SFDG_LANES overrides (1 = one flush at a time); the results are the same either way.
+    int lane_count() const {
+        if (const char* e = std::getenv("SFDG_LANES")) return std::max(1, std::min(8, std::atoi(e)));
+        const double lp = (double)round_up(cfg.ell, 8);
+        const double per_lane = 24.0 * ((double)cfg.ell * cfg.d + cfg.d) + 32.0 * cfg.d * lp + 8.0 * cfg.d * (cfg.ell + 1);
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const int fit = (int)std::floor(0.3 * (double)total_b / std::max(per_lane, 1.0));
+        return std::max(1, std::min((int)kLag, fit));
+    }
+
+    size_t buf_rows() const { return lanes[fill].rows(); }
 
     // rows [r, r+take) such that the trigger can fire only after the last one
     size_t segment(const int64_t* rp, size_t r, size_t nrows) const {
-        size_t take = std::min(nrows - r, cfg.d - buf_rows());
-        const int64_t need = nnz_trigger - buf_nnz;  // > 0 while the buffer is below the trigger
+        const Lane& F = lanes[fill];
+        size_t take = std::min(nrows - r, cfg.d - F.rows());
+        const int64_t need = nnz_trigger - F.nnz;  // > 0 while the buffer is below the trigger
         // first j in [r, r+take) with rp[j+1] - rp[r] >= need
         size_t lo = r, hi = r + take;
         while (lo < hi) {
@@ -242,81 +366,274 @@ class Sketcher {
     }
 
     void commit_host(const int64_t* rp, const uint32_t* cols, const double* vals, size_t r, size_t n) {
-        const int64_t b = rp[r], e = rp[r + n];
-        if (e > b) {
-            CK(cudaMemcpyAsync(eng->a.col + buf_nnz, cols + b, (e - b) * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                               eng->st));
-            CK(cudaMemcpyAsync(eng->a.val + buf_nnz, vals + b, (e - b) * sizeof(double), cudaMemcpyHostToDevice,
-                               eng->st));
+        Lane& F = lanes[fill];
+        Engine& e = *F.eng;
+        const int64_t b = rp[r], end = rp[r + n];
+        if (end > b) {
+            CK(cudaMemcpyAsync(e.a.col + F.nnz, cols + b, (end - b) * sizeof(uint32_t), cudaMemcpyHostToDevice, e.st));
+            CK(cudaMemcpyAsync(e.a.val + F.nnz, vals + b, (end - b) * sizeof(double), cudaMemcpyHostToDevice, e.st));
         }
-        for (int64_t k = b; k < e; ++k) buf_frob += vals[k] * vals[k];  // sparse.cpp:22, row order
-        for (size_t i = 1; i <= n; ++i) buf_rp.push_back(buf_nnz + (rp[r + i] - b));
-        buf_nnz += e - b;
+        for (int64_t k = b; k < end; ++k) F.frob += vals[k] * vals[k];  // sparse.cpp:22, row order
+        for (size_t i = 1; i <= n; ++i) F.rp.push_back(F.nnz + (rp[r + i] - b));
+        F.nnz += end - b;
+        copies_on.push_back(fill);
     }
 
     void commit_device(const int64_t* rp, const uint32_t* d_cols, const double* d_vals, size_t r, size_t n) {
-        const int64_t b = rp[r], e = rp[r + n];
-        if (e > b) {
-            CK(cudaMemcpyAsync(eng->a.col + buf_nnz, d_cols + b, (e - b) * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
-                               eng->st));
-            CK(cudaMemcpyAsync(eng->a.val + buf_nnz, d_vals + b, (e - b) * sizeof(double), cudaMemcpyDeviceToDevice,
-                               eng->st));
-            eng->scr.reset();
-            sumsq(eng->a.val + buf_nnz, e - b, 1, 1, eng->d_scal + 3, nullptr, 0, eng->scr, eng->st);
-            buf_frob += eng->read_scalar(eng->d_scal + 3);
+        Lane& F = lanes[fill];
+        Engine& e = *F.eng;
+        const int64_t b = rp[r], end = rp[r + n];
+        if (end > b) {
+            CK(cudaMemcpyAsync(e.a.col + F.nnz, d_cols + b, (end - b) * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                               e.st));
+            CK(cudaMemcpyAsync(e.a.val + F.nnz, d_vals + b, (end - b) * sizeof(double), cudaMemcpyDeviceToDevice, e.st));
+            e.scr.reset();
+            sumsq(e.a.val + F.nnz, end - b, 1, 1, e.d_scal + 3, nullptr, 0, e.scr, e.st);
+            F.frob += e.read_scalar(e.d_scal + 3);
         }
-        for (size_t i = 1; i <= n; ++i) buf_rp.push_back(buf_nnz + (rp[r + i] - b));
-        buf_nnz += e - b;
+        for (size_t i = 1; i <= n; ++i) F.rp.push_back(F.nnz + (rp[r + i] - b));
+        F.nnz += end - b;
+    }
+
+    // The host->device row copies of this call are on the streams in copies_on.
+    void finish_copies() {
+        for (int i : copies_on) CK(cudaStreamSynchronize(lanes[i].eng->st));
+        copies_on.clear();
     }
 
     void maybe_flush() {  // sketch.cpp:22
-        if (buf_nnz >= nnz_trigger || buf_rows() == cfg.d) flush();
+        const Lane& F = lanes[fill];
+        if (F.nnz >= nnz_trigger || F.rows() == cfg.d) flush();
     }
 
-    void upload_row_ptr() {
-        const int m = (int)buf_rows();
-        eng->a.set_shape(m, (int)cfg.d, buf_nnz);
-        h_rp32.resize(m + 1);
-        for (int i = 0; i <= m; ++i) h_rp32[i] = (int)buf_rp[i];
-        CK(cudaMemcpyAsync(eng->a.row_ptr, h_rp32.data(), (m + 1) * sizeof(int), cudaMemcpyHostToDevice, eng->st));
+    void upload_row_ptr(Lane& L) {
+        const int m = (int)L.rows();
+        L.eng->a.set_shape(m, (int)cfg.d, L.nnz);
+        L.rp32.resize(m + 1);
+        for (int i = 0; i <= m; ++i) L.rp32[i] = (int)L.rp[i];
+        CK(cudaMemcpyAsync(L.eng->a.row_ptr, L.rp32.data(), (m + 1) * sizeof(int), cudaMemcpyHostToDevice, L.eng->st));
     }
 
-    void flush() {  // sketch.cpp:25-32
-        eng->scr.reset();
-        upload_row_ptr();
-        eng->prepare();
-        // B'_f goes into the right half of Mt[cur]: first wait for the shrink that last read it
-        CK(cudaStreamWaitEvent(eng->st, eng->ev_read_done[eng->cur], 0));
-        double delta_hat = 0.0;
-        const size_t att = eng->boosted(ver, cfg.power, buf_frob, &delta_hat);
-        // B = dense_shrink([B; B']) on the shrink stream: it overlaps the next flush's power
-        // iteration. Errors it raises (Jacobi non-convergence) surface at the next sync point.
-        CK(cudaEventRecord(eng->ev_bprime, eng->st));
-        CK(cudaStreamWaitEvent(eng->st2, eng->ev_bprime, 0));
-        eng->scr2.reset();
-        eng->dense_shrink_stack(eng->Mt[eng->cur], 2 * eng->lp, (int)cfg.ell, eng->lp, (int)cfg.ell,
-                                eng->Mt[eng->cur ^ 1], 2 * eng->lp, /*side=*/true);
-        CK(cudaEventRecord(eng->ev_read_done[eng->cur], eng->st2));
-        eng->cur ^= 1;
-        clear_buffer();
+    // sketch.cpp:25-32: the filling lane's buffer becomes a flush in flight.
+    void flush() {
+        Lane& L = lanes[fill];
+        L.id = next_id++;
+        L.eng->scr.reset();
+        upload_row_ptr(L);
+        L.eng->prepare_async();
+        CK(cudaEventRecord(L.ev, L.eng->st));
+        L.phase = Lane::Preparing;
+        inflight.push_back(fill);
+        // the next filling lane: an idle one, committing older flushes until one frees up
+        for (;;) {
+            int idle = -1;
+            for (int i = 0; i < (int)lanes.size(); ++i)
+                if (lanes[i].phase == Lane::Idle) {
+                    idle = i;
+                    break;
+                }
+            if (idle >= 0) {
+                fill = idle;
+                break;
+            }
+            step(true);
+        }
+        Lane& F = lanes[fill];
+        F.clear_rows();
+        F.phase = Lane::Filling;
+        // the new filling lane's previous B' must be consumed before rows overwrite nothing of
+        // it (rows and B' are separate buffers), so no wait is needed here
+    }
+
+    FlushState predicted_end(const Lane& P) const {
+        if (P.phase == Lane::Done) return P.cur;
+        FlushState s = P.start;
+        s.pos = rng_advance(rng_advance(s.pos, (uint64_t)cfg.d * cfg.ell), (uint64_t)cfg.d);
+        s.ver.i += 1;
+        const double di = static_cast<double>(s.ver.i);
+        s.ver.delta_spent += s.ver.delta / (2.0 * di * di);
+        return s;
+    }
+
+    void start_flush(Lane& L, const FlushState& st) {
+        L.start = st;
+        L.cur = st;
+        L.attempt = 0;
+        L.interval = L.interval_base;
+        CK(cudaMemsetAsync(L.eng->d_err, 0, sizeof(int), L.eng->st));
+        enqueue_attempt(L);
+    }
+
+    void enqueue_attempt(Lane& L) {
+        if (++L.attempt > kRetryCap) throw numerical_error("boosted_sparse_shrink: retry cap exceeded");
+        Engine& e = *L.eng;
+        L.pos0 = L.cur.pos;
+        L.interval_used = e.adaptive ? L.interval : 1;
+        e.orth_interval = L.interval_used;
+        e.pos = L.cur.pos;
+        e.scr.reset();
+        if (L.bp_pending) {  // the chain's dense shrink of this lane's previous B'
+            CK(cudaStreamWaitEvent(e.st, L.ev_bp_free, 0));
+            L.bp_pending = false;
+        }
+        e.attempt_enqueue(cfg.power, e.Bp, e.lp);
+        L.cur.pos = e.pos;
+        CK(cudaEventRecord(L.ev, e.st));
+        L.phase = Lane::Shrinking;
+    }
+
+    // Advance one lane whose queued phase has completed.
+    void advance(Lane& L, size_t idx_in_flight) {
+        Engine& e = *L.eng;
+        switch (L.phase) {
+            case Lane::Preparing: {
+                e.prepare_finish();
+                const uint64_t lag = kLag;
+                const Hist& h = hist[L.id % lag];
+                L.interval_base = (L.id >= lag && h.valid) ? next_orth_interval(h.kappa_last, h.last_since) : 1;
+                const FlushState st = idx_in_flight == 0 ? committed : predicted_end(lanes[inflight[idx_in_flight - 1]]);
+                start_flush(L, st);
+                break;
+            }
+            case Lane::Shrinking: {
+                const double b_fsq = e.h_scal[1];
+                const double kappa_last = e.h_scal[16 + 3], kappa_max = e.h_scal[16 + 5];
+                const int err = e.h_err[0];
+                if (L.interval_used > 1 && (kappa_max > kKappaUnsafe || (err & ERR_NONFINITE_ITER))) {
+                    // redo from the same draws with the every-sweep schedule (as Engine::boosted)
+                    CK(cudaMemsetAsync(e.d_err, 0, sizeof(int), e.st));
+                    L.cur.pos = L.pos0;
+                    L.interval = 1;
+                    --L.attempt;
+                    enqueue_attempt(L);
+                    break;
+                }
+                raise_device_flags(err);
+                L.kappa_last = kappa_last;
+                L.last_since = e.last_since;
+                const double drop = L.frob - b_fsq;  // shrink.cpp:112-113
+                const double delta_hat = drop / (kAlpha * static_cast<double>(cfg.ell));
+                if (drop <= 1e-12 * L.frob) {  // exact recovery (shrink.cpp:115-118)
+                    L.delta_hat = 0.0;
+                    L.phase = Lane::Done;
+                    break;
+                }
+                L.delta_hat = delta_hat;
+                e.pos = L.cur.pos;
+                e.verify_enqueue(L.cur.ver, delta_hat, e.Bp, e.lp, ev_verify);
+                L.cur.pos = e.pos;
+                CK(cudaEventRecord(L.ev, e.st));
+                L.phase = Lane::Verifying;
+                break;
+            }
+            case Lane::Verifying: {
+                if (e.verify_result()) L.phase = Lane::Done;
+                else enqueue_attempt(L);
+                break;
+            }
+            default:
+                break;
+        }
+    }
+
+    void commit(Lane& L) {
+        committed = L.cur;
+        if (e_adaptive(L)) hist[L.id % kLag] = Hist{L.kappa_last, L.last_since, true};
         flushes += 1;
-        attempts += att;
+        attempts += L.attempt;
+        Engine& C = *chain;
+        const int lp = C.lp;
+        // B = dense_shrink([B; B']) on the chain stream (the lane's work is complete: its
+        // event was observed); errors surface at the next chain sync.
+        C.scr.reset();
+        copy2d(L.eng->Bp, (int)cfg.d, lp, lp, C.Mt[C.cur] + lp, 2 * lp, C.st);
+        CK(cudaEventRecord(L.ev_bp_free, C.st));
+        L.bp_pending = true;
+        C.dense_shrink_stack(C.Mt[C.cur], 2 * lp, (int)cfg.ell, lp, (int)cfg.ell, C.Mt[C.cur ^ 1], 2 * lp);
+        C.cur ^= 1;
+        L.phase = Lane::Idle;
+        L.clear_rows();
     }
 
-    void clear_buffer() {
-        buf_rp.assign(1, 0);
-        buf_nnz = 0;
-        buf_frob = 0.0;
+    static bool e_adaptive(const Lane& L) { return L.eng->adaptive; }
+
+    // One round of progress; blocking = wait for the oldest pending phase if nothing moved.
+    void step(bool blocking) {
+        bool moved = false;
+        try {
+            for (size_t k = 0; k < inflight.size(); ++k) {
+                Lane& L = lanes[inflight[k]];
+                if (L.phase == Lane::Done) continue;
+                const cudaError_t q = cudaEventQuery(L.ev);
+                if (q == cudaErrorNotReady) continue;
+                CK(q);
+                advance(L, k);
+                moved = true;
+            }
+            while (!inflight.empty()) {
+                Lane& L = lanes[inflight.front()];
+                if (L.phase != Lane::Done) break;
+                if (!same_state(L.start, committed)) {  // mispredicted start: recompute from the truth
+                    start_flush(L, committed);
+                    moved = true;
+                    break;
+                }
+                commit(L);
+                inflight.pop_front();
+                moved = true;
+            }
+        } catch (...) {
+            abort_inflight();
+            throw;
+        }
+        if (!moved && blocking) {
+            for (int i : inflight)
+                if (lanes[i].phase != Lane::Done) {
+                    CK(cudaEventSynchronize(lanes[i].ev));
+                    break;
+                }
+        }
+    }
+
+    void pump() { step(false); }
+
+    void drain() {
+        while (!inflight.empty()) step(true);
+    }
+
+    void sync_all() {
+        for (auto& L : lanes) CK(cudaStreamSynchronize(L.eng->st));
+        chain->sync();
+    }
+
+    // Drop every in-flight flush (after an error, or on reset); committed state stays.
+    void abort_inflight() {
+        for (auto& L : lanes) cudaStreamSynchronize(L.eng->st);
+        chain->sync();
+        for (int i : inflight) {
+            lanes[i].phase = Lane::Idle;
+            lanes[i].clear_rows();
+            CK(cudaMemsetAsync(lanes[i].eng->d_err, 0, sizeof(int), lanes[i].eng->st));
+        }
+        inflight.clear();
+        if (lanes[fill].phase != Lane::Filling) {
+            lanes[fill].phase = Lane::Filling;
+            lanes[fill].clear_rows();
+        }
     }
 
     SketchCfg cfg;
-    std::unique_ptr<Engine> eng;
-    Verifier ver;
-    std::vector<int64_t> buf_rp;
-    std::vector<int> h_rp32;
-    int64_t buf_nnz = 0;
+    RngStream rng;
+    std::unique_ptr<Engine> chain;  // B (= Mt[cur] left half), the dense-shrink stream
+    std::vector<Lane> lanes;
+    std::deque<int> inflight;  // lane indices in flush order
+    std::vector<int> copies_on;
+    std::vector<Hist> hist;
+    cudaEvent_t ev_verify = nullptr;
+    FlushState committed;
+    int fill = 0;
+    uint64_t next_id = 0;
     int64_t nnz_trigger = 0;
-    double buf_frob = 0.0;
     size_t flushes = 0, attempts = 0;
 };
 
@@ -357,13 +674,13 @@ void require_device(int device) {
 void rng_in(Engine& e, const sfdg_rng_state* r) {
     e.pos.words = r->words;
     e.pos.has_spare = r->has_spare != 0;
-    if (e.pos.has_spare) e.rng.set_spare(r->spare, e.st);
+    if (e.pos.has_spare) e.rng->set_spare(e.pos, r->spare, e.st);
 }
 
 void rng_out(Engine& e, sfdg_rng_state* r) {
     r->words = e.pos.words;
     r->has_spare = e.pos.has_spare ? 1 : 0;
-    r->spare = e.pos.has_spare ? e.rng.spare_value(e.st) : 0.0;
+    r->spare = e.pos.has_spare ? e.rng->spare_value(e.pos, e.st) : 0.0;
 }
 
 // B'^T (d x lp, ldb) on device -> B' (ell x d) on host
@@ -607,7 +924,7 @@ int sfdg_gaussian_matrix(sfdg_rng_state* rng, size_t rows, size_t cols, double* 
         RngStream rs;
         rs.init(rng->seed, 2 * rows * cols + 64, device);
         RngPos pos{rng->words, rng->has_spare != 0};
-        if (pos.has_spare) rs.set_spare(rng->spare, st);
+        if (pos.has_spare) rs.set_spare(pos, rng->spare, st);
         double* dout = nullptr;
         int* derr = nullptr;
         CK(cudaMalloc(&dout, rows * cols * sizeof(double)));
@@ -620,7 +937,7 @@ int sfdg_gaussian_matrix(sfdg_rng_state* rng, size_t rows, size_t cols, double* 
         CK(cudaStreamSynchronize(st));
         rng->words = pos.words;
         rng->has_spare = pos.has_spare ? 1 : 0;
-        rng->spare = pos.has_spare ? rs.spare_value(st) : 0.0;
+        rng->spare = pos.has_spare ? rs.spare_value(pos, st) : 0.0;
         cudaFree(dout);
         cudaFree(derr);
         cudaStreamDestroy(st);

@@ -122,7 +122,27 @@ size_t power_iteration_count(size_t m, const PowerCfg& cfg) {
     return std::max<size_t>(1, static_cast<size_t>(std::ceil(q)));
 }
 
-Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, int m_cap_)
+int next_orth_interval(double kappa_last, int last_since) {
+    if (!(kappa_last >= 1.0)) return 1;
+    const double g = std::pow(std::max(kappa_last, 1.0), 1.0 / std::max(last_since, 1));
+    const int iv = g <= 1.001 ? kMaxInterval : (int)std::floor(std::log(kKappaTarget) / std::log(g));
+    return std::max(1, std::min(kMaxInterval, iv));
+}
+
+void raise_device_flags(int e) {
+    if (!e) return;
+    if (e & ERR_NONFINITE_INPUT) throw invalid_argument("dense_shrink: non-finite input");
+    if (e & ERR_NONFINITE_ITER) throw numerical_error("simultaneous_iteration: non-finite intermediate");
+    if (e & ERR_NONFINITE_PROJ) throw numerical_error("sparse_shrink: non-finite projection");
+    if (e & ERR_NONFINITE_VERIFY) throw numerical_error("verify_spectral: non-finite operator output");
+    if (e & ERR_JACOBI_NOCONV) throw numerical_error("jacobi_eigh: no convergence after 100 sweeps");
+    if (e & ERR_RNG_U1_ZERO)
+        throw numerical_error("rng: Box-Muller u1 == 0 redraw (probability 2^-53) is not reproduced on device");
+    throw numerical_error("sfdg: device error flag " + std::to_string(e));
+}
+
+Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, int m_cap_, RngStream* shared_rng,
+               bool stack)
     : device(device_), d(d_), ell(ell_) {
     if (ell < 1 || ell > kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 256] for this build");
     lp = (int)round_up((size_t)ell, 8);
@@ -132,16 +152,27 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&ev_read_done[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_bprime, cudaEventDisableTiming));
-    // the ring holds >= 3 attempts' worth of draws (G: d*ell, x: d)
-    const uint64_t per_attempt = 2 * ((uint64_t)d * ell + d) + 8;
-    rng.init(seed, std::max<uint64_t>(3 * per_attempt, 1 << 20), device);
+    if (shared_rng) {
+        rng = shared_rng;
+    } else {
+        // the ring holds >= 3 attempts' worth of draws (G: d*ell, x: d)
+        const uint64_t per_attempt = 2 * ((uint64_t)d * ell + d) + 8;
+        own_rng = std::make_unique<RngStream>();
+        own_rng->init(seed, std::max<uint64_t>(3 * per_attempt, 1 << 20), device);
+        rng = own_rng.get();
+    }
     a.reserve(std::max(1, m_cap_), std::max<int64_t>((int64_t)nnz_cap, 1));
     ensure_rows(std::max(1, m_cap_));
     const size_t wbytes = (size_t)d * lp * sizeof(double);
     CK(cudaMalloc(&W, wbytes));
-    for (int i = 0; i < 2; ++i) {
-        CK(cudaMalloc(&Mt[i], 2 * wbytes));
-        CK(cudaMemsetAsync(Mt[i], 0, 2 * wbytes, st));
+    if (stack) {
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaMalloc(&Mt[i], 2 * wbytes));
+            CK(cudaMemsetAsync(Mt[i], 0, 2 * wbytes, st));
+        }
+    } else {
+        CK(cudaMalloc(&Bp, wbytes));
+        CK(cudaMemsetAsync(Bp, 0, wbytes, st));
     }
     const int kmax = std::max(2 * lp, 8);
     CK(cudaMalloc(&gram, (size_t)kmax * kmax * sizeof(double)));
@@ -166,26 +197,29 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     CK(cudaMemsetAsync(d_scal, 0, 64 * sizeof(double), st));
     CK(cudaHostAlloc(&h_scal, 64 * sizeof(double), cudaHostAllocDefault));
     CK(cudaHostAlloc(&h_err, 4 * sizeof(int), cudaHostAllocDefault));
+    CK(cudaHostAlloc(&h_counts, 4 * sizeof(int), cudaHostAllocDefault));
     CK(cudaStreamSynchronize(st));
 }
 
 Engine::~Engine() {
     cudaSetDevice(device);
     if (st) cudaStreamSynchronize(st);
-    for (void* p : {(void*)Y, (void*)Yt, (void*)W, (void*)Mt[0], (void*)Mt[1], (void*)gram, (void*)rinv, (void*)rfac,
+    for (void* p : {(void*)Y, (void*)Yt, (void*)W, (void*)Mt[0], (void*)Mt[1], (void*)Bp, (void*)gram, (void*)rinv,
+                    (void*)rfac,
                     (void*)dinv8, (void*)kc,
                     (void*)evals, (void*)evecs, (void*)S, (void*)x0, (void*)ybuf, (void*)u, (void*)tpart, (void*)tvec,
                     (void*)vpart, (void*)vout, (void*)bar, (void*)d_err, (void*)d_scal})
         if (p) cudaFree(p);
     if (h_scal) cudaFreeHost(h_scal);
     if (h_err) cudaFreeHost(h_err);
+    if (h_counts) cudaFreeHost(h_counts);
     a.release();
     plan_r.release();
     plan_c.release();
     if (st2) cudaStreamSynchronize(st2);
     scr.release();
     scr2.release();
-    rng.release();
+    own_rng.reset();
     for (int i = 0; i < 2; ++i)
         if (ev_read_done[i]) cudaEventDestroy(ev_read_done[i]);
     if (ev_bprime) cudaEventDestroy(ev_bprime);
@@ -224,14 +258,7 @@ void Engine::check_errors() {
     if (!e) return;
     CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
     CK(cudaStreamSynchronize(st));
-    if (e & ERR_NONFINITE_INPUT) throw invalid_argument("dense_shrink: non-finite input");
-    if (e & ERR_NONFINITE_ITER) throw numerical_error("simultaneous_iteration: non-finite intermediate");
-    if (e & ERR_NONFINITE_PROJ) throw numerical_error("sparse_shrink: non-finite projection");
-    if (e & ERR_NONFINITE_VERIFY) throw numerical_error("verify_spectral: non-finite operator output");
-    if (e & ERR_JACOBI_NOCONV) throw numerical_error("jacobi_eigh: no convergence after 100 sweeps");
-    if (e & ERR_RNG_U1_ZERO)
-        throw numerical_error("rng: Box-Muller u1 == 0 redraw (probability 2^-53) is not reproduced on device");
-    throw numerical_error("sfdg: device error flag " + std::to_string(e));
+    raise_device_flags(e);
 }
 
 void Engine::load_csr(const int64_t* row_ptr, const uint32_t* cols, const double* vals, int m, int64_t nnz) {
@@ -247,17 +274,24 @@ void Engine::load_csr(const int64_t* row_ptr, const uint32_t* cols, const double
     CK(cudaStreamSynchronize(st));  // host vectors go out of scope
 }
 
-void Engine::prepare() {
+void Engine::prepare_async() {
     build_transpose(a, scr, st);
     plan_r.build(a.row_ptr, a.m, a.nnz, scr, st);
     plan_c.build(a.col_ptr, a.d, a.nnz, scr, st);
     // one small read-back per flush lets every SpMM skip the long-row kernels when unused
-    int h[4];
-    CK(cudaMemcpyAsync(h, plan_r.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h + 2, plan_c.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_counts, plan_r.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_counts + 2, plan_c.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+}
+
+void Engine::prepare_finish() {
+    plan_r.host_long = h_counts[0];
+    plan_c.host_long = h_counts[2];
+}
+
+void Engine::prepare() {
+    prepare_async();
     CK(cudaStreamSynchronize(st));
-    plan_r.host_long = h[0];
-    plan_c.host_long = h[2];
+    prepare_finish();
 }
 
 void Engine::orthonormalize(double* Yp, int m, int err_bit) {
@@ -280,7 +314,7 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     if (k != ell) throw invalid_argument("simultaneous_iteration: engine built for a different k");
     const size_t q = power_iteration_count((size_t)m, cfg);
     // G = gaussian_matrix(d, k) in W (la_core.cpp:167-172), pad columns zero
-    rng.normals(pos, (uint64_t)d * k, (uint64_t)k, (uint64_t)lp, W, d_err, st);
+    rng->normals(pos, (uint64_t)d * k, (uint64_t)k, (uint64_t)lp, W, d_err, st);
     spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
     orthonormalize(Y, m, ERR_NONFINITE_ITER);
     // Only span(Y) matters for B' (it enters through Z Z^T), so CholeskyQR2 runs every
@@ -316,14 +350,14 @@ void Engine::sparse_shrink(const PowerCfg& cfg, double* bpt, int ldb) {
     gemm_nn(W, d, lp, lp, S, lp, lp, bpt, ldb, st);
 }
 
-bool Engine::verify(Verifier& v, double delta_hat, const double* bpt, int ldb) {
+void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, int ldb, cudaEvent_t serial) {
     // shrink.cpp:76-82, host arithmetic identical to the reference
     v.i += 1;
     const double di = static_cast<double>(v.i);
     const double delta_i = v.delta / (2.0 * di * di);
     v.delta_spent += delta_i;
     const size_t steps = static_cast<size_t>(std::ceil(v.c_verify * std::log2(static_cast<double>(d) / delta_i)));
-    rng.normals(pos, (uint64_t)d, (uint64_t)d, (uint64_t)d, x0, d_err, st);  // unit_sphere_vector draws
+    rng->normals(pos, (uint64_t)d, (uint64_t)d, (uint64_t)d, x0, d_err, st);  // unit_sphere_vector draws
     VerifyArgs args{};
     args.row_ptr = a.row_ptr;
     args.col = a.col;
@@ -347,10 +381,37 @@ bool Engine::verify(Verifier& v, double delta_hat, const double* bpt, int ldb) {
     args.bar = bar;
     args.err = d_err;
     args.out = vout;
+    if (serial) CK(cudaStreamWaitEvent(st, serial, 0));
     verify_launch(args, verify_blocks, st);
-    CK(cudaMemcpyAsync(h_scal, vout, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    check_errors();
-    return h_scal[0] != 0.0;
+    if (serial) CK(cudaEventRecord(serial, st));
+    CK(cudaMemcpyAsync(h_scal + 32, vout, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_err + 1, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+}
+
+bool Engine::verify_result() const {
+    raise_device_flags(h_err[1]);
+    return h_scal[32] != 0.0;
+}
+
+bool Engine::verify(Verifier& v, double delta_hat, const double* bpt, int ldb) {
+    verify_enqueue(v, delta_hat, bpt, ldb, nullptr);
+    CK(cudaStreamSynchronize(st));
+    if (h_err[1]) {
+        CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+        CK(cudaStreamSynchronize(st));
+    }
+    return verify_result();
+}
+
+void Engine::attempt_enqueue(const PowerCfg& cfg, double* bpt, int ldb) {
+    last_since = 1;
+    CK(cudaMemsetAsync(d_scal + 16, 0, 16 * sizeof(double), st));  // pass-1 stats incl. running max kappa
+    sparse_shrink(cfg, bpt, ldb);
+    double* bfsq = d_scal + 1;
+    sumsq(bpt, d, ell, ldb, bfsq, nullptr, 0, scr, st);
+    CK(cudaMemcpyAsync(h_scal + 1, bfsq, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_scal + 16, d_scal + 16, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
 }
 
 size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* delta_hat_out) {
@@ -360,16 +421,9 @@ size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* d
     for (size_t attempt = 1; attempt <= kRetryCap; ++attempt) {
         const RngPos pos0 = pos;
         const int interval_used = adaptive ? orth_interval : 1;
-        last_since = 1;
-        CK(cudaMemsetAsync(d_scal + 16, 0, 16 * sizeof(double), st));  // pass-1 stats incl. running max kappa
-        sparse_shrink(cfg, bpt, ldb);
-        double* bfsq = d_scal + 1;
-        sumsq(bpt, d, ell, ldb, bfsq, nullptr, 0, scr, st);
+        attempt_enqueue(cfg, bpt, ldb);
         // prefetch the next attempt's draws while we wait (side stream)
-        rng.prefetch(pos.words + 2 * ((uint64_t)d * ell + 2 * d) + 8);
-        CK(cudaMemcpyAsync(h_scal + 1, bfsq, sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(h_scal + 16, d_scal + 16, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+        rng->prefetch(pos.words + 2 * ((uint64_t)d * ell + 2 * d) + 8);
         CK(cudaStreamSynchronize(st));
         const double b_fsq = h_scal[1];
         const double kappa_last = h_scal[16 + 3], kappa_max = h_scal[16 + 5];
@@ -382,11 +436,7 @@ size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* d
             --attempt;
             continue;
         }
-        if (adaptive && kappa_last >= 1.0) {  // per-sweep growth of cond(Y) -> next interval
-            const double g = std::pow(std::max(kappa_last, 1.0), 1.0 / std::max(last_since, 1));
-            int iv = g <= 1.001 ? kMaxInterval : (int)std::floor(std::log(kKappaTarget) / std::log(g));
-            orth_interval = std::max(1, std::min(kMaxInterval, iv));
-        }
+        if (adaptive && kappa_last >= 1.0) orth_interval = next_orth_interval(kappa_last, last_since);
         check_errors();
         const double drop = a_fsq - b_fsq;  // shrink.cpp:112-113
         const double delta_hat = drop / (kAlpha * static_cast<double>(ell));
@@ -444,11 +494,13 @@ void Engine::dense_shrink_stack(const double* Xt, int ldx, int n1, int off, int 
     }
 }
 
-void Engine::densify_into_stack(int off) {
+void Engine::densify_into_stack(int off) { densify_into_stack(a, off); }
+
+void Engine::densify_into_stack(const DevCsr& src, int off) {
     fill2d(Mt[cur] + lp, d, lp, 2 * lp, 0.0, st);
-    if (a.m > 0)
-        LAUNCH(densify_t_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)a.m * 32, 256))), 256, 0, st,
-               a.row_ptr, a.col, a.val, a.m, Mt[cur], 2 * lp, off);
+    if (src.m > 0)
+        LAUNCH(densify_t_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)src.m * 32, 256))), 256, 0, st,
+               src.row_ptr, src.col, src.val, src.m, Mt[cur], 2 * lp, off);
 }
 
 void Engine::sketch_to_host(double* out) {

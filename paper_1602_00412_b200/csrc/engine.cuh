@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -36,10 +37,20 @@ struct Verifier {  // shrink.hpp:11-16
 
 size_t power_iteration_count(size_t m, const PowerCfg& cfg);  // randsvd.cpp:10-16
 
+// Adaptive CholeskyQR2 schedule: sweeps between passes so that cond(Y) grows by at most
+// kKappaTarget, from the condition number seen after the last pass-1 factorisation.
+int next_orth_interval(double kappa_last, int last_since);
+
+// Throws the reference's error class for a set of device error flags (0 = no-op).
+void raise_device_flags(int flags);
+
 // Per-device working set for one sketch stream (or one standalone call).
 class Engine {
   public:
-    Engine(int device, int d, int ell, uint64_t seed, uint64_t nnz_cap, int m_cap);
+    // shared_rng: draw from a sketcher-wide generator (flush pipeline lanes) instead of an
+    // own one. stack: allocate Mt[2] (= [B^T | B'^T] pairs); lanes only need Bp (d x lp).
+    Engine(int device, int d, int ell, uint64_t seed, uint64_t nnz_cap, int m_cap, RngStream* shared_rng = nullptr,
+           bool stack = true);
     ~Engine();
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -53,7 +64,8 @@ class Engine {
     Scratch scr2;
     cudaEvent_t ev_read_done[2] = {nullptr, nullptr};
     cudaEvent_t ev_bprime = nullptr;
-    RngStream rng;
+    std::unique_ptr<RngStream> own_rng;
+    RngStream* rng = nullptr;
     RngPos pos;
     DevCsr a;
     SegPlan plan_r, plan_c;
@@ -61,6 +73,7 @@ class Engine {
 
     double *Y = nullptr, *Yt = nullptr, *W = nullptr;  // m_cap x lp, m_cap x lp, d x lp
     double* Mt[2] = {nullptr, nullptr};                 // d x 2lp : [B^T | B'^T]
+    double* Bp = nullptr;                               // d x lp : this lane's B'^T (no stack)
     int cur = 0;
     double *gram = nullptr, *rinv = nullptr, *rfac = nullptr, *dinv8 = nullptr, *kc = nullptr, *evals = nullptr, *evecs = nullptr, *S = nullptr;
     double *x0 = nullptr, *ybuf = nullptr, *u = nullptr, *tpart = nullptr, *tvec = nullptr, *vpart = nullptr;
@@ -80,8 +93,12 @@ class Engine {
     void ensure_rows(int m);
     // Host CSR -> device A' (standalone entry points).
     void load_csr(const int64_t* row_ptr, const uint32_t* cols, const double* vals, int m, int64_t nnz);
-    // CSC + long-row plans for the current A'.
+    // CSC + long-row plans for the current A'. prepare_async queues the build and the
+    // read-back of the long-row counts; prepare_finish consumes them once the stream got there.
     void prepare();
+    void prepare_async();
+    void prepare_finish();
+    int* h_counts = nullptr;  // pinned [4]
     // la_core.cpp:130-165 contract on Y (m x lp, first k columns meaningful): CholeskyQR2.
     void orthonormalize(double* Yp, int m, int err_bit);
     // randsvd.cpp:18-51: Z (m x lp) left in Y.
@@ -90,6 +107,14 @@ class Engine {
     void sparse_shrink(const PowerCfg& cfg, double* bpt, int ldb);
     // shrink.cpp:75-102 on diff_op (shrink.cpp:121-126); host syncs for the verdict.
     bool verify(Verifier& v, double delta_hat, const double* bpt, int ldb);
+    // Asynchronous halves: queue the verification (optionally ordered after the event
+    // `serial`, re-recorded after it: verify is a persistent grid-barrier kernel, and two of
+    // them must never share the GPU) and read its verdict once the stream is past it.
+    void verify_enqueue(Verifier& v, double delta_hat, const double* bpt, int ldb, cudaEvent_t serial);
+    bool verify_result() const;
+    // One sparse_shrink attempt + ||B'||_F^2 + schedule statistics, read back into h_scal
+    // (b_fsq at [1], pass-1 stats at [16..23]) and h_err[0] without a host sync.
+    void attempt_enqueue(const PowerCfg& cfg, double* bpt, int ldb);
     // shrink.cpp:104-131; B'^T lands in Mt[cur] right half. Returns attempts.
     size_t boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* delta_hat_out);
     // dense_shrink (shrink.cpp:30-61) of the row stack whose transpose is Xt (d x kcols, ldx),
@@ -100,6 +125,8 @@ class Engine {
     // Zero the B'^T half of Mt[cur] and scatter the buffer rows of A' into columns
     // [off, off + m) of Mt[cur] (densify, sparse.cpp:71-78, already transposed).
     void densify_into_stack(int off);
+    // Same from another engine's buffer (the sketcher's filling lane).
+    void densify_into_stack(const DevCsr& src, int off);
     // Copies the current B (ell x d row-major) to host.
     void sketch_to_host(double* out);
     double read_scalar(const double* dptr);

@@ -62,38 +62,53 @@ __global__ void __launch_bounds__(MT_M) mt_generate_kernel(uint64_t* __restrict_
     window[t + MT_M] = r[(base + t + MT_M) % (2 * MT_N)];
 }
 
-// Normals j = 0 .. n-1 of the stream starting at raw word w0 with an optional carried
-// spare (j == 0 when has_spare). Output element j goes to out[(j / cols) * ld + j % cols];
-// columns cols..ld-1 of every row are zero-filled when pad != 0.
+__device__ __forceinline__ void box_muller_pair(uint64_t e1, uint64_t e2, double& c, double& sn, int* err) {
+    const double u1 = (double)(e1 >> 11) * 0x1.0p-53;  // rng.hpp:19
+    const double u2 = (double)(e2 >> 11) * 0x1.0p-53;
+    if (u1 <= 0.0) atomicOr(err, ERR_RNG_U1_ZERO);  // rng.cpp:27-29 redraw: p = 2^-53
+    const double rad = sqrt(-2.0 * log(u1));
+    const double theta = 6.283185307179586476925286766559 * u2;  // (2.0 * pi) * u2
+    double s, cs;
+    sincos(theta, &s, &cs);
+    c = rad * cs;
+    sn = rad * s;
+}
+
+// Normals j = 0 .. n-1 of the stream at raw word w0 with an optional carried spare (j == 0
+// when has_spare): from *spare_in when given, else the sin half of ring words (w0-2, w0-1).
+// Output element j goes to out[(j / cols) * ld + j % cols].
 __global__ void box_muller_kernel(const uint64_t* __restrict__ ring, uint64_t ring_mask, uint64_t w0,
                                   int has_spare, const double* __restrict__ spare_in, uint64_t n, uint64_t cols,
-                                  uint64_t ld, double* __restrict__ out, double* __restrict__ spare_out,
-                                  int* __restrict__ err) {
+                                  uint64_t ld, double* __restrict__ out, int* __restrict__ err) {
     const uint64_t s = has_spare ? 1 : 0;
     const uint64_t rest = n > s ? n - s : 0;
     const uint64_t pairs = (rest + 1) / 2;
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    if (tid == 0 && s && n > 0) out[0] = *spare_in;
-    for (uint64_t p = tid; p < pairs; p += stride) {
-        const uint64_t e1 = ring[(w0 + 2 * p) & ring_mask];
-        const uint64_t e2 = ring[(w0 + 2 * p + 1) & ring_mask];
-        const double u1 = (double)(e1 >> 11) * 0x1.0p-53;  // rng.hpp:19
-        const double u2 = (double)(e2 >> 11) * 0x1.0p-53;
-        if (u1 <= 0.0) atomicOr(err, ERR_RNG_U1_ZERO);  // rng.cpp:27-29 redraw: p = 2^-53
-        const double rad = sqrt(-2.0 * log(u1));
-        const double theta = 6.283185307179586476925286766559 * u2;  // (2.0 * pi) * u2
-        double sn, cs;
-        sincos(theta, &sn, &cs);
-        const uint64_t j0 = s + 2 * p;
-        out[(j0 / cols) * ld + j0 % cols] = rad * cs;
-        const uint64_t j1 = j0 + 1;
-        if (j1 < n) {
-            out[(j1 / cols) * ld + j1 % cols] = rad * sn;
-        } else if (spare_out) {
-            *spare_out = rad * sn;  // becomes the cached spare (rng.cpp:30-31)
+    if (tid == 0 && s && n > 0) {
+        if (spare_in) {
+            out[0] = *spare_in;
+        } else {
+            double c, sn;
+            box_muller_pair(ring[(w0 - 2) & ring_mask], ring[(w0 - 1) & ring_mask], c, sn, err);
+            out[0] = sn;
         }
     }
+    for (uint64_t p = tid; p < pairs; p += stride) {
+        double c, sn;
+        box_muller_pair(ring[(w0 + 2 * p) & ring_mask], ring[(w0 + 2 * p + 1) & ring_mask], c, sn, err);
+        const uint64_t j0 = s + 2 * p;
+        out[(j0 / cols) * ld + j0 % cols] = c;
+        const uint64_t j1 = j0 + 1;
+        if (j1 < n) out[(j1 / cols) * ld + j1 % cols] = sn;
+    }
+}
+
+__global__ void spare_kernel(const uint64_t* __restrict__ ring, uint64_t ring_mask, uint64_t w, double* __restrict__ out,
+                             int* __restrict__ err) {
+    double c, sn;
+    box_muller_pair(ring[(w - 2) & ring_mask], ring[(w - 1) & ring_mask], c, sn, err);
+    *out = sn;
 }
 
 __global__ void zero_pad_kernel(double* __restrict__ out, uint64_t rows, uint64_t cols, uint64_t ld) {
@@ -104,6 +119,15 @@ __global__ void zero_pad_kernel(double* __restrict__ out, uint64_t rows, uint64_
 }
 
 }  // namespace
+
+RngPos rng_advance(RngPos p, uint64_t n) {
+    if (n == 0) return p;
+    const uint64_t s = p.has_spare ? 1 : 0;
+    const uint64_t rest = n > s ? n - s : 0;
+    p.words += 2 * ((rest + 1) / 2);
+    p.has_spare = rest > 0 && (rest % 2) == 1;
+    return p;
+}
 
 void RngStream::init(uint64_t seed_, uint64_t min_ring_words, int device_) {
     release();
@@ -116,9 +140,9 @@ void RngStream::init(uint64_t seed_, uint64_t min_ring_words, int device_) {
     CK(cudaMalloc(&d_window, MT_N * sizeof(uint64_t)));
     CK(cudaMalloc(&d_spare, 2 * sizeof(double)));
     CK(cudaMemset(d_spare, 0, 2 * sizeof(double)));
+    d_tmp = d_spare + 1;
     CK(cudaStreamCreateWithFlags(&s_gen, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&ev_gen, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ev_consumed, cudaEventDisableTiming));
     reseed();
 }
 
@@ -127,51 +151,69 @@ void RngStream::reseed() {
     uint64_t mt[MT_N];
     mt[0] = seed;
     for (int i = 1; i < MT_N; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+    // every queued reader of the old stream must be done before the ring is rewritten
+    for (auto& c : live) {
+        CK(cudaEventSynchronize(c.ev));
+        pool.push_back(c.ev);
+    }
+    live.clear();
+    CK(cudaStreamSynchronize(s_gen));
     CK(cudaMemcpy(d_window, mt, sizeof mt, cudaMemcpyHostToDevice));
     gen_words = 0;
 }
 
 void RngStream::restart(uint64_t seed_) {
-    CK(cudaStreamSynchronize(s_gen));
     seed = seed_;
-    spare_slot = 0;
+    explicit_at = ~0ull;
     reseed();
 }
 
 void RngStream::release() {
+    for (auto& c : live) cudaEventDestroy(c.ev);
+    for (auto e : pool) cudaEventDestroy(e);
+    live.clear();
+    pool.clear();
     if (d_ring) cudaFree(d_ring);
     if (d_window) cudaFree(d_window);
     if (d_spare) cudaFree(d_spare);
     if (s_gen) cudaStreamDestroy(s_gen);
     if (ev_gen) cudaEventDestroy(ev_gen);
-    if (ev_consumed) cudaEventDestroy(ev_consumed);
     d_ring = nullptr;
     d_window = nullptr;
     d_spare = nullptr;
+    d_tmp = nullptr;
     s_gen = nullptr;
     ev_gen = nullptr;
-    ev_consumed = nullptr;
 }
 
 void RngStream::generate_to(uint64_t words_end) {
     if (words_end <= gen_words) return;
-    // Never overwrite words a queued consumer may still read.
-    CK(cudaStreamWaitEvent(s_gen, ev_consumed, 0));
-    ProfScope prof("rng_gen", s_gen);
     const uint64_t need = words_end - gen_words;
     const int steps = (int)((need + MT_M - 1) / MT_M);
+    const uint64_t new_end = gen_words + (uint64_t)steps * MT_M;
+    // Never overwrite words a queued reader may still need: writing word p replaces p - ring_cap.
+    if (new_end > ring_cap) {
+        const uint64_t limit = new_end - ring_cap;
+        size_t keep = 0;
+        for (auto& c : live) {
+            if (c.begin < limit) {
+                CK(cudaStreamWaitEvent(s_gen, c.ev, 0));
+                pool.push_back(c.ev);
+            } else {
+                live[keep++] = c;
+            }
+        }
+        live.resize(keep);
+    }
+    ProfScope prof("rng_gen", s_gen);
     LAUNCH(mt_generate_kernel, 1, MT_M, 0, s_gen, d_window, d_ring, ring_cap - 1, gen_words, steps);
-    gen_words += (uint64_t)steps * MT_M;
+    gen_words = new_end;
     CK(cudaEventRecord(ev_gen, s_gen));
 }
 
 void RngStream::ensure(uint64_t w_begin, uint64_t w_end, cudaStream_t consumer) {
     if (w_end - w_begin > ring_cap) throw invalid_argument("rng: request exceeds the device ring");
-    if (w_begin + ring_cap < gen_words) {
-        // Requested words fell out of the ring (only in standalone calls): restart.
-        CK(cudaStreamSynchronize(s_gen));
-        reseed();
-    }
+    if (w_begin + ring_cap < gen_words) reseed();  // fell out of the ring (standalone calls): regenerate
     generate_to(w_end);
     CK(cudaStreamWaitEvent(consumer, ev_gen, 0));
 }
@@ -182,50 +224,64 @@ void RngStream::prefetch(uint64_t w_end) {
     generate_to(cap_end);
 }
 
-void RngStream::mark_consumed(cudaStream_t consumer) { CK(cudaEventRecord(ev_consumed, consumer)); }
+void RngStream::mark_consumed(uint64_t w_begin, cudaStream_t consumer) {
+    cudaEvent_t ev;
+    if (!pool.empty()) {
+        ev = pool.back();
+        pool.pop_back();
+    } else {
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ev, consumer));
+    live.push_back({w_begin, ev});
+}
 
 // Draws n normals (rng.cpp:19-34 semantics) into out (rows of `cols` values, leading
-// dimension ld, zero padding beyond cols), advancing st.
-void RngStream::normals(RngPos& st, uint64_t n, uint64_t cols, uint64_t ld, double* d_out, int* d_err,
+// dimension ld, zero padding beyond cols), advancing pos.
+void RngStream::normals(RngPos& pos, uint64_t n, uint64_t cols, uint64_t ld, double* d_out, int* d_err,
                         cudaStream_t stream) {
     if (n == 0) return;
-    const uint64_t s = st.has_spare ? 1 : 0;
-    const uint64_t rest = n > s ? n - s : 0;
-    const uint64_t pairs = (rest + 1) / 2;
-    ensure(st.words, st.words + 2 * pairs, stream);
-    // spare slots alternate so a kernel never reads and writes the same scalar
-    double* spare_in = d_spare + (spare_slot & 1);
-    double* spare_out = d_spare + ((spare_slot + 1) & 1);
-    const bool new_spare = (rest % 2) == 1;
+    const RngPos next = rng_advance(pos, n);
+    const bool from_ring = pos.has_spare && explicit_at != pos.words;
+    const uint64_t w_begin = from_ring ? pos.words - 2 : pos.words;
+    ensure(w_begin, std::max(next.words, pos.words), stream);
     ProfScope prof("box_muller", stream);
+    const uint64_t s = pos.has_spare ? 1 : 0;
+    const uint64_t pairs = ((n > s ? n - s : 0) + 1) / 2;
     const unsigned blocks = (unsigned)std::min<uint64_t>(4 * kSMs, (pairs + 255) / 256 + 1);
-    LAUNCH(box_muller_kernel, blocks, 256, 0, stream, d_ring, ring_cap - 1, st.words, (int)st.has_spare, spare_in, n,
-           cols, ld, d_out, new_spare ? spare_out : nullptr, d_err);
+    LAUNCH(box_muller_kernel, blocks, 256, 0, stream, d_ring, ring_cap - 1, pos.words, (int)pos.has_spare,
+           from_ring ? (const double*)nullptr : (const double*)d_spare, n, cols, ld, d_out, d_err);
     if (ld > cols) {
         const uint64_t rows = (n + cols - 1) / cols;
         LAUNCH(zero_pad_kernel, (unsigned)std::min<uint64_t>(4 * kSMs, (rows * (ld - cols) + 255) / 256), 256, 0,
                stream, d_out, rows, cols, ld);
     }
-    mark_consumed(stream);
-    st.words += 2 * pairs;
-    if (rest == 0) {
-        st.has_spare = false;  // consumed the carried spare only
-    } else {
-        st.has_spare = new_spare;
-        if (new_spare) spare_slot += 1;
-    }
+    mark_consumed(w_begin, stream);
+    pos = next;
 }
 
-double RngStream::spare_value(cudaStream_t stream) {
+double RngStream::spare_value(const RngPos& pos, cudaStream_t stream) {
+    if (!pos.has_spare) return 0.0;
     double v = 0.0;
-    CK(cudaMemcpyAsync(&v, d_spare + (spare_slot & 1), sizeof v, cudaMemcpyDeviceToHost, stream));
+    if (explicit_at == pos.words) {
+        CK(cudaMemcpyAsync(&v, d_spare, sizeof v, cudaMemcpyDeviceToHost, stream));
+    } else {
+        ensure(pos.words - 2, pos.words, stream);
+        int* err = nullptr;
+        CK(cudaMallocAsync(&err, sizeof(int), stream));
+        LAUNCH(spare_kernel, 1, 1, 0, stream, d_ring, ring_cap - 1, pos.words, d_tmp, err);
+        mark_consumed(pos.words - 2, stream);
+        CK(cudaMemcpyAsync(&v, d_tmp, sizeof v, cudaMemcpyDeviceToHost, stream));
+        CK(cudaFreeAsync(err, stream));
+    }
     CK(cudaStreamSynchronize(stream));
     return v;
 }
 
-void RngStream::set_spare(double v, cudaStream_t stream) {
-    CK(cudaMemcpyAsync(d_spare + (spare_slot & 1), &v, sizeof v, cudaMemcpyHostToDevice, stream));
+void RngStream::set_spare(const RngPos& pos, double v, cudaStream_t stream) {
+    CK(cudaMemcpyAsync(d_spare, &v, sizeof v, cudaMemcpyHostToDevice, stream));
     CK(cudaStreamSynchronize(stream));
+    explicit_at = pos.words;
 }
 
 }  // namespace sfdg

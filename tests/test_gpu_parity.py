@@ -469,3 +469,53 @@ def test_every_sweep_schedule_matches_adaptive(oracle, monkeypatch):
     bo, _ = oracle.sketch(rp, cs, vs, 1000, 50, seed=0)
     assert btb_rel(b_every, bo) <= 1e-10
     assert btb_rel(b_adapt, b_every) <= 1e-10
+
+
+# ---------------------------------------------------------------- flush pipeline
+def _mixed_rank_stream(seed, d=40, ell=6, flushes=9):
+    """Flush buffers (40 rows of 6 nnz: the nnz and rows triggers coincide) that alternate
+    between rank 3 -- exact recovery, no verification, fewer draws than the pipeline
+    predicts -- and full-rank random rows, so speculative flushes must be re-run."""
+    g = np.random.default_rng(seed)
+    rps, css, vss = [0], [], []
+    for f in range(flushes):
+        low = f % 3 != 2
+        for _ in range(d):
+            if low:
+                coef = g.standard_normal(3)
+                cols = np.arange(6)
+                vals = np.repeat(coef, 2) * np.array([1.0, 0.5, 1.0, -0.5, 2.0, 1.0])
+            else:
+                cols = np.sort(g.choice(d, 6, replace=False))
+                vals = g.standard_normal(6)
+            css.append(cols)
+            vss.append(vals)
+            rps.append(rps[-1] + 6)
+    return np.array(rps, np.int64), np.concatenate(css).astype(np.uint32), np.concatenate(vss)
+
+
+def test_pipeline_mispredictions_match_sequential_reference(oracle, monkeypatch):
+    """Exact-recovery flushes consume fewer draws than predicted; the in-flight flushes
+    behind them restart from the true state. Counters and B must match the oracle, and
+    one lane (no speculation) must give the bit-identical sketch."""
+    rp, cs, vs = _mixed_rank_stream(5)
+    b4, st4 = sketch_gpu(rp, cs, vs, 40, 6, 77)
+    bo, so = oracle.sketch(rp, cs, vs, 40, 6, seed=77)
+    assert btb_rel(b4, bo) <= BTB_TOL
+    assert (st4["flushes"], st4["attempts"], st4["verifier_i"]) == (so["flushes"], so["attempts"], so["verifier_i"])
+    assert st4["delta_spent"] == so["delta_spent"]
+    monkeypatch.setenv("SFDG_LANES", "1")
+    b1, st1 = sketch_gpu(rp, cs, vs, 40, 6, 77)
+    assert np.array_equal(b1, b4) and st1 == st4
+
+
+def test_lane_count_does_not_change_results(monkeypatch):
+    """c1 rows 0..9000 at d = 1000 -> 9 flushes: beyond the 4-flush lag of the adaptive
+    schedule. 1, 2 and 4 lanes give bit-identical sketches and identical counters."""
+    rp, cs, vs = S.generate("c1", (0, 9000))
+    out = []
+    for lanes in ("1", "2", "4"):
+        monkeypatch.setenv("SFDG_LANES", lanes)
+        out.append(sketch_gpu(rp, cs, vs, 1000, 50, 0))
+    for b, st in out[1:]:
+        assert np.array_equal(b, out[0][0]) and st == out[0][1]
