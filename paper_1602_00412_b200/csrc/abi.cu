@@ -10,7 +10,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 #include <deque>
+#include <thread>
 #include <memory>
 #include <new>
 #include <string>
@@ -115,6 +117,17 @@ class Sketcher {
         }
         CK(cudaEventCreateWithFlags(&ev_verify, cudaEventDisableTiming));
         CK(cudaEventRecord(ev_verify, chain->st));
+        if (const char* t = std::getenv("SFDG_TRACE")) {
+            trace_path = t;
+            CK(cudaEventCreate(&tr_epoch));
+            CK(cudaEventRecord(tr_epoch, chain->st));
+            CK(cudaStreamSynchronize(chain->st));
+            tr_host0 = host_us();
+            for (auto& L : lanes) {
+                CK(cudaEventCreate(&L.tr0));
+                CK(cudaEventCreate(&L.tr1));
+            }
+        }
         hist.assign(kLag, Hist{});
         committed.ver.delta = cfg.delta;
         fill = 0;
@@ -125,6 +138,7 @@ class Sketcher {
     ~Sketcher() {
         try {
             sync_all();
+            if (!trace_path.empty()) dump_trace();
         } catch (...) {
         }
         for (auto& L : lanes) {
@@ -317,6 +331,8 @@ class Sketcher {
         int last_since = 1;
         cudaEvent_t ev = nullptr;          // completion of the queued phase
         cudaEvent_t ev_bp_free = nullptr;  // the chain finished reading Bp
+        cudaEvent_t tr0 = nullptr, tr1 = nullptr;  // SFDG_TRACE: timed bounds of the queued phase
+        double tr_enq = 0.0;
         bool bp_pending = false;
         size_t rows() const { return rp.size() - 1; }
         void clear_rows() {
@@ -328,6 +344,10 @@ class Sketcher {
     // The orthonormalisation interval of flush f comes from flush f - kLag (>= the lane
     // count, so committed when f starts): the same schedule for every lane count.
     static constexpr uint64_t kLag = 4;
+    // Flushes without history start at a moderate interval; a conditioning blow-up
+    // (kappa > kKappaUnsafe) replays that attempt with the every-sweep schedule.
+    static constexpr int kFirstInterval = 4;
+    static constexpr int kDefaultLanes = 4;
     struct Hist {
         double kappa_last = 0.0;
         int last_since = 1;
@@ -338,13 +358,13 @@ class Sketcher {
     // Y/Yt of d x lp, W/B' of d x lp, a share of the Rng ring) would exceed 30% of the HBM.
     // SFDG_LANES overrides (1 = one flush at a time); the results are the same either way.
     int lane_count() const {
-        if (const char* e = std::getenv("SFDG_LANES")) return std::max(1, std::min(8, std::atoi(e)));
+        if (const char* e = std::getenv("SFDG_LANES")) return std::max(1, std::min((int)kLag, std::atoi(e)));
         const double lp = (double)round_up(cfg.ell, 8);
         const double per_lane = 24.0 * ((double)cfg.ell * cfg.d + cfg.d) + 32.0 * cfg.d * lp + 8.0 * cfg.d * (cfg.ell + 1);
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
         const int fit = (int)std::floor(0.3 * (double)total_b / std::max(per_lane, 1.0));
-        return std::max(1, std::min((int)kLag, fit));
+        return std::max(1, std::min(kDefaultLanes, fit));
     }
 
     size_t buf_rows() const { return lanes[fill].rows(); }
@@ -419,8 +439,10 @@ class Sketcher {
         Lane& L = lanes[fill];
         L.id = next_id++;
         L.eng->scr.reset();
+        trace_begin(L);
         upload_row_ptr(L);
         L.eng->prepare_async();
+        trace_end(L);
         CK(cudaEventRecord(L.ev, L.eng->st));
         L.phase = Lane::Preparing;
         inflight.push_back(fill);
@@ -476,7 +498,9 @@ class Sketcher {
             CK(cudaStreamWaitEvent(e.st, L.ev_bp_free, 0));
             L.bp_pending = false;
         }
+        trace_begin(L);
         e.attempt_enqueue(cfg.power, e.Bp, e.lp);
+        trace_end(L);
         L.cur.pos = e.pos;
         CK(cudaEventRecord(L.ev, e.st));
         L.phase = Lane::Shrinking;
@@ -490,7 +514,8 @@ class Sketcher {
                 e.prepare_finish();
                 const uint64_t lag = kLag;
                 const Hist& h = hist[L.id % lag];
-                L.interval_base = (L.id >= lag && h.valid) ? next_orth_interval(h.kappa_last, h.last_since) : 1;
+                L.interval_base =
+                    (L.id >= lag && h.valid) ? next_orth_interval(h.kappa_last, h.last_since) : kFirstInterval;
                 const FlushState st = idx_in_flight == 0 ? committed : predicted_end(lanes[inflight[idx_in_flight - 1]]);
                 start_flush(L, st);
                 break;
@@ -520,7 +545,9 @@ class Sketcher {
                 }
                 L.delta_hat = delta_hat;
                 e.pos = L.cur.pos;
-                e.verify_enqueue(L.cur.ver, delta_hat, e.Bp, e.lp, ev_verify);
+                trace_begin(L);
+                e.verify_enqueue(L.cur.ver, delta_hat, e.Bp, e.lp, serial_verify ? ev_verify : nullptr);
+                trace_end(L);
                 L.cur.pos = e.pos;
                 CK(cudaEventRecord(L.ev, e.st));
                 L.phase = Lane::Verifying;
@@ -546,10 +573,20 @@ class Sketcher {
         // B = dense_shrink([B; B']) on the chain stream (the lane's work is complete: its
         // event was observed); errors surface at the next chain sync.
         C.scr.reset();
+        cudaEvent_t c0 = nullptr, c1 = nullptr;
+        if (!trace_path.empty()) {
+            CK(cudaEventCreate(&c0));
+            CK(cudaEventCreate(&c1));
+            CK(cudaEventRecord(c0, C.st));
+        }
         copy2d(L.eng->Bp, (int)cfg.d, lp, lp, C.Mt[C.cur] + lp, 2 * lp, C.st);
         CK(cudaEventRecord(L.ev_bp_free, C.st));
         L.bp_pending = true;
         C.dense_shrink_stack(C.Mt[C.cur], 2 * lp, (int)cfg.ell, lp, (int)cfg.ell, C.Mt[C.cur ^ 1], 2 * lp);
+        if (c1) {
+            CK(cudaEventRecord(c1, C.st));
+            tr_chain.push_back({L.id, c0, c1, host_us()});
+        }
         C.cur ^= 1;
         L.phase = Lane::Idle;
         L.clear_rows();
@@ -567,6 +604,7 @@ class Sketcher {
                 const cudaError_t q = cudaEventQuery(L.ev);
                 if (q == cudaErrorNotReady) continue;
                 CK(q);
+                trace_observe(L, inflight[k]);
                 advance(L, k);
                 moved = true;
             }
@@ -586,16 +624,59 @@ class Sketcher {
             abort_inflight();
             throw;
         }
-        if (!moved && blocking) {
-            for (int i : inflight)
-                if (lanes[i].phase != Lane::Done) {
-                    CK(cudaEventSynchronize(lanes[i].ev));
-                    break;
-                }
-        }
+        // Nothing moved: the caller spins. Polling every lane (rather than blocking on one
+        // event) lets whichever lane finishes first get its next phase queued at once.
+        if (!moved && blocking) std::this_thread::yield();
     }
 
     void pump() { step(false); }
+
+    // ---- SFDG_TRACE=<path>: per-phase device intervals and host reaction times (JSON lines)
+    static double host_us() {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
+    void trace_begin(Lane& L) {
+        if (trace_path.empty()) return;
+        CK(cudaEventRecord(L.tr0, L.eng->st));
+        L.tr_enq = host_us();
+    }
+    void trace_end(Lane& L) {
+        if (trace_path.empty()) return;
+        CK(cudaEventRecord(L.tr1, L.eng->st));
+    }
+    void trace_observe(Lane& L, int lane_idx) {
+        if (trace_path.empty()) return;
+        float a = 0.f, b = 0.f;
+        CK(cudaEventElapsedTime(&a, tr_epoch, L.tr0));
+        CK(cudaEventElapsedTime(&b, tr_epoch, L.tr1));
+        static const char* names[] = {"idle", "filling", "prepare", "shrink", "verify", "done"};
+        char buf[256];
+        snprintf(buf, sizeof buf,
+                 "{\"lane\": %d, \"flush\": %llu, \"phase\": \"%s\", \"gpu_start_us\": %.1f, \"gpu_end_us\": %.1f, "
+                 "\"host_enqueue_us\": %.1f, \"host_observe_us\": %.1f}",
+                 lane_idx, (unsigned long long)L.id, names[L.phase], 1e3 * a, 1e3 * b, L.tr_enq - tr_host0,
+                 host_us() - tr_host0);
+        tr_lines.push_back(buf);
+    }
+    void dump_trace() {
+        FILE* f = fopen(trace_path.c_str(), "a");
+        if (!f) return;
+        for (auto& l : tr_lines) fprintf(f, "%s\n", l.c_str());
+        for (auto& c : tr_chain) {
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, tr_epoch, c.e0);
+            cudaEventElapsedTime(&b, tr_epoch, c.e1);
+            fprintf(f,
+                    "{\"lane\": -1, \"flush\": %llu, \"phase\": \"dense_shrink\", \"gpu_start_us\": %.1f, "
+                    "\"gpu_end_us\": %.1f, \"host_enqueue_us\": %.1f}\n",
+                    (unsigned long long)c.id, 1e3 * a, 1e3 * b, c.host - tr_host0);
+            cudaEventDestroy(c.e0);
+            cudaEventDestroy(c.e1);
+        }
+        fclose(f);
+        tr_lines.clear();
+        tr_chain.clear();
+    }
 
     void drain() {
         while (!inflight.empty()) step(true);
@@ -629,7 +710,18 @@ class Sketcher {
     std::deque<int> inflight;  // lane indices in flush order
     std::vector<int> copies_on;
     std::vector<Hist> hist;
+    std::string trace_path;
+    cudaEvent_t tr_epoch = nullptr;
+    double tr_host0 = 0.0;
+    std::vector<std::string> tr_lines;
+    struct ChainTrace {
+        uint64_t id;
+        cudaEvent_t e0, e1;
+        double host;
+    };
+    std::vector<ChainTrace> tr_chain;
     cudaEvent_t ev_verify = nullptr;
+    bool serial_verify = !(std::getenv("SFDG_VERIFY_SERIAL") && std::atoi(std::getenv("SFDG_VERIFY_SERIAL")) == 0);
     FlushState committed;
     int fill = 0;
     uint64_t next_id = 0;

@@ -124,19 +124,29 @@ __global__ void __launch_bounds__(128) gram_tn_kernel(const double* __restrict__
         }
 }
 
-__global__ void gram_reduce_kernel(const double* __restrict__ partial, int nchunks, int k, double* __restrict__ out,
-                                   int ldo) {
+// Sum of the split-K partials (fixed order: warp w takes chunks w, w+8, ..., then the 8
+// warp sums in warp order). A block owns 32 consecutive entries of the k x k output; only
+// computed (upper) tiles are read -- coalesced -- and mirrored on write.
+constexpr int kRedWarps = 8;
+__global__ void __launch_bounds__(32 * kRedWarps) gram_reduce_kernel(const double* __restrict__ partial, int nchunks,
+                                                                     int k, double* __restrict__ out, int ldo) {
+    __shared__ double sh[kRedWarps][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int total = k * k;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        int i = e / k, j = e % k;
-        if (i / TB > j / TB) {  // lower tiles were not computed: mirror
-            const int tmp = i;
-            i = j;
-            j = tmp;
-        }
-        double s = 0.0;
-        for (int c = 0; c < nchunks; ++c) s += partial[(size_t)c * total + (size_t)i * k + j];
-        out[(size_t)(e / k) * ldo + (e % k)] = s;
+    const int e = blockIdx.x * 32 + lane;
+    const int i = e / k, j = e % k;
+    const bool on = e < total && i / TB <= j / TB;
+    double s = 0.0;
+    if (on)
+        for (int c = w; c < nchunks; c += kRedWarps) s += __ldcg(partial + (size_t)c * total + e);
+    sh[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && on) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < kRedWarps; ++q) t += sh[q][lane];
+        out[(size_t)i * ldo + j] = t;
+        if (i / TB < j / TB) out[(size_t)j * ldo + i] = t;
     }
 }
 
@@ -303,8 +313,7 @@ void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scrat
         LAUNCH(gram_tn_kernel<2>, dim3(ntiles, nchunks), 128, smem, st, X, n, k, ldx, rows_per_chunk, T, partial);
     else
         LAUNCH(gram_tn_kernel<1>, dim3(ntiles, nchunks), 128, smem, st, X, n, k, ldx, rows_per_chunk, T, partial);
-    LAUNCH(gram_reduce_kernel, std::max(1u, std::min(4u * kSMs, ceil_div((size_t)k * k, 256))), 256, 0, st, partial,
-           nchunks, k, out, ldo);
+    LAUNCH(gram_reduce_kernel, ceil_div((size_t)k * k, 32), 32 * kRedWarps, 0, st, partial, nchunks, k, out, ldo);
 }
 
 void gemm_nn(const double* X, int n, int k, int ldx, const double* S, int c, int lds, double* C, int ldc,

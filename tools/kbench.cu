@@ -48,7 +48,8 @@ int main(int argc, char** argv) {
         for (int j = ell; j < lp; ++j) hY[(size_t)i * lp + j] = 0.0;
     double *Y, *Y2, *W, *G, *R, *st4, *K;
     int* err;
-    cudaMalloc(&Y, hY.size() * 8);
+    cudaMalloc(&Y, 2 * hY.size() * 8);  // eigh test Grams read 2 lp columns
+    cudaMemset(Y, 0, 2 * hY.size() * 8);
     cudaMalloc(&Y2, hY.size() * 8);
     cudaMalloc(&W, (size_t)d * lp * 8);
     cudaMalloc(&G, (size_t)4 * lp * lp * 8);
