@@ -123,6 +123,23 @@ int sfdg_sketcher_reset(sfdg_sketcher* h, uint64_t seed);
 /* Blocks until all queued device work of this sketcher finished. */
 int sfdg_sketcher_synchronize(sfdg_sketcher* h);
 
+/* ---- FdSketcher: dense Frequent Directions (sketch.hpp:53-67, sketch.cpp:47-78) ---
+ * The paper's baseline: a 2ell x d buffer shrunk to ell rows whenever it fills. */
+typedef struct sfdg_fd_sketcher sfdg_fd_sketcher;
+/* FdSketcher(ell, d) (sketch.cpp:47-50); 1 <= ell <= d else SFDG_INVALID_ARGUMENT. */
+int sfdg_fd_create(size_t ell, size_t d, int device, sfdg_fd_sketcher** out);
+int sfdg_fd_destroy(sfdg_fd_sketcher* h);
+/* append(row) for nrows dense rows (nrows x d row-major), sketch.cpp:52-63. A non-finite
+ * value fails the shrink that would consume it (dense_shrink, shrink.cpp:32). */
+int sfdg_fd_append(sfdg_fd_sketcher* h, const double* rows, size_t nrows);
+/* Same rows given as CSR (densified on the device). */
+int sfdg_fd_append_csr(sfdg_fd_sketcher* h, const int64_t* row_ptr, const uint32_t* cols, const double* vals,
+                       size_t nrows);
+/* finalize() (sketch.cpp:65-78): ell x d row-major into out. */
+int sfdg_fd_finalize(sfdg_fd_sketcher* h, double* out);
+/* shrink_count() (sketch.hpp:60). */
+int sfdg_fd_shrink_count(sfdg_fd_sketcher* h, size_t* count);
+
 /* ---- free functions (shrink.hpp:26-41, sketch.hpp:71, randsvd.hpp:18-26) ------- */
 
 /* merge(b1, b2, ell) = dense_shrink(vstack(b1, b2), ell)  (sketch.cpp:80-83). */
@@ -132,6 +149,16 @@ int sfdg_merge(const double* b1, size_t rows1, const double* b2, size_t rows2, s
  * dimension ld) on `device`; `stream` is a cudaStream_t (NULL = legacy default). */
 int sfdg_merge_device(const double* d_b1t, const double* d_b2t, size_t ell, size_t d, size_t ld,
                       double* d_outt, int device, void* stream);
+/* Row-sharded sketch of one stream (the multi-GPU entry). Shard g holds the
+ * contiguous rows [g*ceil(n/G), (g+1)*ceil(n/G)) and is sketched with seed + g on
+ * devices[g % ndev] (one host thread per shard); the shard sketches then meet in the
+ * log2 tree -- at level L shard r (r % 2^(L+1) == 2^L) is peer-copied to r - 2^L, which
+ * computes merge(B_lo, B_hi) (sketch.cpp:80-83) -- and `out` (ell x d) receives the root.
+ * Replaces the caller-side loop of tests/acceptance.cpp:420-445 (shard, sketch, merge).
+ * shard_stats (nullable) receives the G per-shard counters. */
+int sfdg_sharded_sketch(const sfdg_sketch_config* cfg, const int64_t* row_ptr, const uint32_t* cols,
+                        const double* vals, size_t nrows, int shards, const int* devices, int ndev, double* out,
+                        sfdg_stats* shard_stats);
 /* dense_shrink(a, ell) (shrink.cpp:30-61), host in/out. */
 int sfdg_dense_shrink(const double* a, size_t rows, size_t cols, size_t ell, double* out, int device);
 /* sparse_shrink(buffer, ell, power, rng) (shrink.cpp:63-73); rng advanced in place. */

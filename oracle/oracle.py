@@ -137,6 +137,7 @@ class Oracle:
         L.or_svd_top.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp, _dp, C.POINTER(C.c_int)]
         L.or_orthonormalize.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp]
         L.or_dense_shrink.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp]
+        L.or_fd_sketch.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.POINTER(C.c_size_t)]
         L.or_simultaneous_iteration.argtypes = [C.POINTER(_OrCsr), C.c_size_t, C.POINTER(_OrPower), C.c_void_p, _dp]
         L.or_sparse_shrink.argtypes = [C.POINTER(_OrCsr), C.c_size_t, C.POINTER(_OrPower), C.c_void_p, _dp]
         L.or_verify_spectral.argtypes = [_SYMOP, C.c_void_p, C.c_size_t, C.POINTER(_OrVerifier), C.c_void_p,
@@ -250,6 +251,15 @@ class Oracle:
         out = np.zeros((ell, d))
         self._chk(self.L.or_merge(_ptr(b1, _dp), b1.shape[0], _ptr(b2, _dp), b2.shape[0], d, ell, _ptr(out, _dp)))
         return out
+
+    def fd_sketch(self, rows, ell):
+        """FdSketcher whole-stream run (sketch.cpp:47-78): (B ell x d, shrink_count)."""
+        a = _f64(np.atleast_2d(rows))
+        n, d = a.shape
+        out = np.zeros((ell, d))
+        cnt = C.c_size_t()
+        self._chk(self.L.or_fd_sketch(_ptr(a, _dp), n, d, ell, _ptr(out, _dp), C.byref(cnt)))
+        return out, cnt.value
 
     def sketcher(self, ell, d, seed=0, delta=0.1, power: PowerConfig | None = None) -> "OracleSketcher":
         return OracleSketcher(self, ell, d, seed, delta, power or PowerConfig())
@@ -450,6 +460,15 @@ class Reference:
         self._chk(self.L.ref_merge(_ptr(b1, _dp), b1.shape[0], _ptr(b2, _dp), b2.shape[0], b1.shape[1], ell,
                                    _ptr(out, _dp)))
         return out
+
+    def fd_sketch(self, rows, ell):
+        a = _f64(np.atleast_2d(rows))
+        n, d = a.shape
+        out = np.zeros((ell, d))
+        cnt = C.c_size_t()
+        self._chk(self.L.ref_fd_sketch(_ptr(a, _dp), C.c_size_t(n), C.c_size_t(d), C.c_size_t(ell), _ptr(out, _dp),
+                                       C.byref(cnt)))
+        return out, cnt.value
 
     def sketch(self, row_ptr, cols, vals, d, ell, seed=0, delta=0.1, power: PowerConfig | None = None):
         args, keep = self._csr(row_ptr, cols, vals, d)

@@ -142,6 +142,20 @@ int ref_merge(const double* b1, size_t r1, const double* b2, size_t r2, size_t d
     });
 }
 
+// Whole-stream FdSketcher run (sketch.cpp:47-78) over n dense rows.
+int ref_fd_sketch(const double* rows, size_t n, size_t d, size_t ell, double* out, size_t* shrink_count) {
+    return guarded([&] {
+        sfd::FdSketcher f(ell, d);
+        std::vector<double> r(d);
+        for (size_t i = 0; i < n; ++i) {
+            std::memcpy(r.data(), rows + i * d, d * sizeof(double));
+            f.append(r);
+        }
+        put(f.finalize(), out);
+        *shrink_count = f.shrink_count();
+    });
+}
+
 // Whole-stream SfdSketcher run: append every row, finalize. stats = [flushes, attempts, verifier_i,
 // delta_spent].
 int ref_sketch(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d,

@@ -758,6 +758,41 @@ int or_merge(const double* b1, size_t r1, const double* b2, size_t r2, size_t d,
 }
 
 /* ------------------------------------------------------------------------- */
+/* FdSketcher (core/src/sketch.cpp:47-78): dense Frequent Directions baseline. */
+/* Whole-stream run over n dense rows (n x d row-major).                       */
+/* ------------------------------------------------------------------------- */
+
+int or_fd_sketch(const double* rows, size_t n, size_t d, size_t ell, double* out /* ell x d */,
+                 size_t* shrink_count) {
+    ENTER();
+    if (ell < 1 || ell > d) THROW_INVALID("FdSketcher: requires 1 <= ell <= d"); /* sketch.cpp:48-49 */
+    mat work = mat_new(2 * ell, d);
+    size_t fill = 0, shrinks = 0;
+    for (size_t i = 0; i < n; ++i) { /* append (sketch.cpp:52-63) */
+        memcpy(work.data + fill * d, rows + i * d, d * sizeof(double));
+        fill += 1;
+        if (fill == 2 * ell) {
+            mat shrunk = dense_shrink(&work, ell);
+            memset(work.data, 0, 2 * ell * d * sizeof(double));
+            memcpy(work.data, shrunk.data, ell * d * sizeof(double));
+            fill = ell;
+            shrinks += 1;
+        }
+    }
+    if (fill > ell) { /* finalize (sketch.cpp:65-78) */
+        mat live = {fill, d, work.data};
+        mat shrunk = dense_shrink(&live, ell);
+        memset(work.data, 0, 2 * ell * d * sizeof(double));
+        memcpy(work.data, shrunk.data, ell * d * sizeof(double));
+        fill = ell;
+        shrinks += 1;
+    }
+    memcpy(out, work.data, ell * d * sizeof(double));
+    *shrink_count = shrinks;
+    LEAVE();
+}
+
+/* ------------------------------------------------------------------------- */
 /* SfdSketcher (core/src/sketch.cpp:9-45)                                      */
 /* ------------------------------------------------------------------------- */
 

@@ -93,6 +93,10 @@ int or_boosted_sparse_shrink(const or_csr* a, size_t ell, or_verifier* st, const
 int or_merge(const double* b1, size_t r1, const double* b2, size_t r2, size_t d, size_t ell,
              double* out);
 
+/* ---- FdSketcher (core/include/sfd/sketch.hpp:53-67, core/src/sketch.cpp:47-78) ----
+ * Whole-stream dense FD: n rows (n x d row-major) -> B (ell x d), shrink count. */
+int or_fd_sketch(const double* rows, size_t n, size_t d, size_t ell, double* out, size_t* shrink_count);
+
 /* ---- SfdSketcher (core/include/sfd/sketch.hpp:22-49, core/src/sketch.cpp:9-45) ---- */
 typedef struct or_sketcher or_sketcher;
 typedef struct {

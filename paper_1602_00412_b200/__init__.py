@@ -110,6 +110,14 @@ def lib() -> C.CDLL:
     L.sfdg_merge_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int,
                                     C.c_void_p]
     L.sfdg_dense_shrink.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_int]
+    L.sfdg_fd_create.argtypes = [C.c_size_t, C.c_size_t, C.c_int, C.POINTER(C.c_void_p)]
+    L.sfdg_fd_destroy.argtypes = [C.c_void_p]
+    L.sfdg_fd_append.argtypes = [C.c_void_p, _dp, C.c_size_t]
+    L.sfdg_fd_append_csr.argtypes = [C.c_void_p, _i64p, _u32p, _dp, C.c_size_t]
+    L.sfdg_fd_finalize.argtypes = [C.c_void_p, _dp]
+    L.sfdg_fd_shrink_count.argtypes = [C.c_void_p, C.POINTER(C.c_size_t)]
+    L.sfdg_sharded_sketch.argtypes = [C.POINTER(_SketchCfg), _i64p, _u32p, _dp, C.c_size_t, C.c_int,
+                                      C.POINTER(C.c_int), C.c_int, _dp, C.POINTER(_Stats)]
     csr = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t]
     L.sfdg_sparse_shrink.argtypes = csr + [C.c_size_t, C.POINTER(_Power), C.POINTER(_Rng), _dp, C.c_int]
     L.sfdg_boosted_sparse_shrink.argtypes = csr + [C.c_size_t, C.POINTER(_Verifier), C.POINTER(_Power),
@@ -364,6 +372,65 @@ def merge(b1, b2, ell: int, device: int = 0) -> np.ndarray:
     out = np.zeros((ell, d))
     _check(lib().sfdg_merge(_p(b1, _dp), b1.shape[0], _p(b2, _dp), b2.shape[0], d, ell, _p(out, _dp), device))
     return out
+
+
+class FdSketcher:
+    """FdSketcher (sketch.hpp:53-67): dense Frequent Directions on the device."""
+
+    def __init__(self, ell: int, d: int, device: int = 0):
+        self.ell, self.d = int(ell), int(d)
+        self._h = C.c_void_p()
+        _check(lib().sfdg_fd_create(self.ell, self.d, device, C.byref(self._h)))
+
+    def append(self, row) -> None:
+        self.append_rows(np.atleast_2d(row))
+
+    def append_rows(self, rows) -> None:
+        a = _f64(np.atleast_2d(rows))
+        if a.shape[1] != self.d:
+            raise InvalidArgument("FdSketcher: row dimension mismatch")
+        _check(lib().sfdg_fd_append(self._h, _p(a, _dp), a.shape[0]))
+
+    def append_csr(self, row_ptr, cols, vals) -> None:
+        rp, cs, vs = _csr(row_ptr, cols, vals)
+        _check(lib().sfdg_fd_append_csr(self._h, _p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), len(rp) - 1))
+
+    def finalize(self) -> np.ndarray:
+        out = np.zeros((self.ell, self.d))
+        _check(lib().sfdg_fd_finalize(self._h, _p(out, _dp)))
+        return out
+
+    def shrink_count(self) -> int:
+        c = C.c_size_t()
+        _check(lib().sfdg_fd_shrink_count(self._h, C.byref(c)))
+        return c.value
+
+    def close(self) -> None:
+        if self._h:
+            lib().sfdg_fd_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sharded_sketch(row_ptr, cols, vals, cfg: "SketchConfig", shards: int, devices=(0,)):
+    """sfdg_sharded_sketch: G contiguous row shards sketched with seed + g on
+    devices[g % len(devices)], merged in the log2 tree (shards.py order). Returns
+    (B ell x d, [per-shard stats dicts])."""
+    rp, cs, vs = _csr(row_ptr, cols, vals)
+    devs = np.ascontiguousarray(np.asarray(devices, dtype=np.int32))
+    out = np.zeros((cfg.ell, cfg.d))
+    st = (_Stats * shards)()
+    c = cfg._c()
+    _check(lib().sfdg_sharded_sketch(C.byref(c), _p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), len(rp) - 1, shards,
+                                     devs.ctypes.data_as(C.POINTER(C.c_int)), len(devs), _p(out, _dp), st))
+    stats = [{"flushes": s.flush_count, "attempts": s.attempt_total, "verifier_i": s.verifier.i,
+              "delta_spent": s.verifier.delta_spent} for s in st]
+    return out, stats
 
 
 def merge_device(d_b1t: int, d_b2t: int, ell: int, d: int, ld: int, d_outt: int, device: int = 0,

@@ -314,6 +314,29 @@ class Sketcher {
         flushes = attempts = 0;
     }
 
+    // Shard tree (sfdg_sharded_sketch): B^T lives in the left half of chain Mt[cur].
+    Engine& chain_engine() { return *chain; }
+    // this <- merge(this, other) = dense_shrink([B_this; B_other]) (sketch.cpp:80-83);
+    // `other` may live on another device (peer copy).
+    void merge_from(Sketcher& other) {
+        drain();
+        other.drain();
+        other.chain->sync();
+        Engine& C = *chain;
+        Engine& O = *other.chain;
+        C.set_device();
+        const int lp = C.lp;
+        const size_t bytes = (size_t)cfg.d * 2 * lp * sizeof(double);
+        C.scr.reset();
+        double* tmp = C.scr.take<double>((int64_t)cfg.d * 2 * lp);
+        if (O.device == C.device) CK(cudaMemcpyAsync(tmp, O.Mt[O.cur], bytes, cudaMemcpyDeviceToDevice, C.st));
+        else CK(cudaMemcpyPeerAsync(tmp, C.device, O.Mt[O.cur], O.device, bytes, C.st));
+        copy2d(tmp, (int)cfg.d, lp, 2 * lp, C.Mt[C.cur] + lp, 2 * lp, C.st);
+        C.dense_shrink_stack(C.Mt[C.cur], 2 * lp, (int)cfg.ell, lp, (int)cfg.ell, C.Mt[C.cur ^ 1], 2 * lp);
+        C.check_errors();
+        C.cur ^= 1;
+    }
+
   private:
     struct Lane {
         std::unique_ptr<Engine> eng;
@@ -332,7 +355,7 @@ class Sketcher {
         cudaEvent_t ev = nullptr;          // completion of the queued phase
         cudaEvent_t ev_bp_free = nullptr;  // the chain finished reading Bp
         cudaEvent_t tr0 = nullptr, tr1 = nullptr;  // SFDG_TRACE: timed bounds of the queued phase
-        double tr_enq = 0.0;
+        double tr_enq = 0.0, tr_enq_end = 0.0;
         bool bp_pending = false;
         size_t rows() const { return rp.size() - 1; }
         void clear_rows() {
@@ -343,7 +366,7 @@ class Sketcher {
     };
     // The orthonormalisation interval of flush f comes from flush f - kLag (>= the lane
     // count, so committed when f starts): the same schedule for every lane count.
-    static constexpr uint64_t kLag = 4;
+    static constexpr uint64_t kLag = 8;
     // Flushes without history start at a moderate interval; a conditioning blow-up
     // (kappa > kKappaUnsafe) replays that attempt with the every-sweep schedule.
     static constexpr int kFirstInterval = 4;
@@ -643,6 +666,7 @@ class Sketcher {
     void trace_end(Lane& L) {
         if (trace_path.empty()) return;
         CK(cudaEventRecord(L.tr1, L.eng->st));
+        L.tr_enq_end = host_us();
     }
     void trace_observe(Lane& L, int lane_idx) {
         if (trace_path.empty()) return;
@@ -650,12 +674,12 @@ class Sketcher {
         CK(cudaEventElapsedTime(&a, tr_epoch, L.tr0));
         CK(cudaEventElapsedTime(&b, tr_epoch, L.tr1));
         static const char* names[] = {"idle", "filling", "prepare", "shrink", "verify", "done"};
-        char buf[256];
+        char buf[384];
         snprintf(buf, sizeof buf,
                  "{\"lane\": %d, \"flush\": %llu, \"phase\": \"%s\", \"gpu_start_us\": %.1f, \"gpu_end_us\": %.1f, "
-                 "\"host_enqueue_us\": %.1f, \"host_observe_us\": %.1f}",
+                 "\"host_enqueue_us\": %.1f, \"host_enqueue_end_us\": %.1f, \"host_observe_us\": %.1f}",
                  lane_idx, (unsigned long long)L.id, names[L.phase], 1e3 * a, 1e3 * b, L.tr_enq - tr_host0,
-                 host_us() - tr_host0);
+                 L.tr_enq_end - tr_host0, host_us() - tr_host0);
         tr_lines.push_back(buf);
     }
     void dump_trace() {
@@ -727,6 +751,95 @@ class Sketcher {
     uint64_t next_id = 0;
     int64_t nnz_trigger = 0;
     size_t flushes = 0, attempts = 0;
+};
+
+// FdSketcher (core/include/sfd/sketch.hpp:53-67, core/src/sketch.cpp:47-78): dense
+// Frequent Directions, the paper's baseline. The 2ell x d work buffer is the engine's
+// [B^T | B'^T] pair (d x 2lp): rows 0..ell-1 are columns of the left half, rows
+// ell..2ell-1 of the right half, so a full buffer is exactly the dense_shrink stack the
+// sketcher uses. Appends are batched: rows are copied to the device and transposed (or,
+// for sparse input, scattered) into their columns; a shrink runs whenever the buffer fills.
+class FdSketch {
+  public:
+    FdSketch(size_t ell_, size_t d_, int device) : ell(ell_), d(d_) {
+        if (ell < 1 || ell > d) throw invalid_argument("FdSketcher: requires 1 <= ell <= d");  // sketch.cpp:48-49
+        if (ell > (size_t)kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 256] for this build");
+        if (d >= (size_t)INT32_MAX) throw invalid_argument("FdSketcher: d must be < 2^31");
+        e = std::make_unique<Engine>(device, (int)d, (int)ell, 0, 1, 1);
+    }
+
+    // n dense rows, row-major (append, sketch.cpp:52-63)
+    void append_dense(const double* rows, size_t n) {
+        e->set_device();
+        size_t r = 0;
+        while (r < n) {
+            const size_t take = chunk(n - r);
+            for (size_t i = r; i < r + take; ++i)
+                for (size_t j = 0; j < d; ++j)
+                    if (!std::isfinite(rows[i * d + j])) bad = true;
+            e->scr.reset();
+            double* tmp = e->scr.take<double>((int64_t)take * d);
+            CK(cudaMemcpyAsync(tmp, rows + r * d, take * d * sizeof(double), cudaMemcpyHostToDevice, e->st));
+            transpose(tmp, (int)take, (int)d, (int)d, e->Mt[e->cur] + col_of(fill), 2 * e->lp, e->st);
+            advance(take);
+            r += take;
+        }
+        CK(cudaStreamSynchronize(e->st));
+    }
+
+    // n sparse rows (CSR, row_ptr absolute into cols/vals), densified on the device
+    void append_csr(const int64_t* rp, const uint32_t* cols, const double* vals, size_t n) {
+        e->set_device();
+        validate_csr(rp, cols, vals, n, d);
+        size_t r = 0;
+        while (r < n) {
+            const size_t take = chunk(n - r);
+            e->ensure_rows((int)take);
+            e->load_csr(rp + r, cols, vals, (int)take, rp[r + take] - rp[r]);
+            e->scr.reset();
+            e->scatter_rows_t(e->Mt[e->cur], 2 * e->lp, col_of(fill));
+            advance(take);
+            r += take;
+        }
+        CK(cudaStreamSynchronize(e->st));
+    }
+
+    void finalize(double* out) {  // sketch.cpp:65-78
+        e->set_device();
+        if (fill > ell) shrink(fill - ell);
+        e->sync();
+        e->check_errors();
+        e->scr.reset();
+        e->sketch_to_host(out);
+    }
+
+    size_t shrink_count() const { return shrinks; }
+
+  private:
+    // rows appended in one transfer: up to the next shrink, never across the ell boundary
+    size_t chunk(size_t left) const {
+        size_t take = std::min(left, 2 * ell - fill);
+        if (fill < ell) take = std::min(take, ell - fill);
+        return take;
+    }
+    int col_of(size_t row) const { return row < ell ? (int)row : e->lp + (int)(row - ell); }
+    void advance(size_t take) {
+        fill += take;
+        if (fill == 2 * ell) shrink(ell);
+    }
+    void shrink(size_t n2) {
+        if (bad) throw invalid_argument("dense_shrink: non-finite input");  // shrink.cpp:32
+        e->scr.reset();
+        e->dense_shrink_stack(e->Mt[e->cur], 2 * e->lp, (int)ell, e->lp, (int)n2, e->Mt[e->cur ^ 1], 2 * e->lp);
+        e->cur ^= 1;
+        fill = ell;
+        shrinks += 1;
+    }
+
+    size_t ell, d;
+    std::unique_ptr<Engine> e;
+    size_t fill = 0, shrinks = 0;
+    bool bad = false;
 };
 
 namespace {
@@ -809,6 +922,10 @@ using namespace sfdg;
 
 struct sfdg_sketcher {
     std::unique_ptr<Sketcher> impl;
+};
+
+struct sfdg_fd_sketcher {
+    std::unique_ptr<FdSketch> impl;
 };
 
 static Sketcher* impl_of(sfdg_sketcher* h) {
@@ -895,6 +1012,100 @@ int sfdg_sketcher_reset(sfdg_sketcher* h, uint64_t seed) {
 
 int sfdg_sketcher_synchronize(sfdg_sketcher* h) {
     return guard([&] { impl_of(h)->synchronize(); });
+}
+
+int sfdg_fd_create(size_t ell, size_t d, int device, sfdg_fd_sketcher** out) {
+    return guard([&] {
+        if (!out) throw invalid_argument("sfdg_fd_create: null argument");
+        if (ell < 1 || ell > d) throw invalid_argument("FdSketcher: requires 1 <= ell <= d");
+        require_device(device);
+        auto h = std::make_unique<sfdg_fd_sketcher>();
+        h->impl = std::make_unique<FdSketch>(ell, d, device);
+        *out = h.release();
+    });
+}
+
+int sfdg_fd_destroy(sfdg_fd_sketcher* h) {
+    return guard([&] { delete h; });
+}
+
+int sfdg_fd_append(sfdg_fd_sketcher* h, const double* rows, size_t nrows) {
+    return guard([&] {
+        if (!h || !h->impl) throw invalid_argument("null FD sketcher");
+        h->impl->append_dense(rows, nrows);
+    });
+}
+
+int sfdg_fd_append_csr(sfdg_fd_sketcher* h, const int64_t* row_ptr, const uint32_t* cols, const double* vals,
+                       size_t nrows) {
+    return guard([&] {
+        if (!h || !h->impl) throw invalid_argument("null FD sketcher");
+        h->impl->append_csr(row_ptr, cols, vals, nrows);
+    });
+}
+
+int sfdg_fd_finalize(sfdg_fd_sketcher* h, double* out) {
+    return guard([&] {
+        if (!h || !h->impl) throw invalid_argument("null FD sketcher");
+        h->impl->finalize(out);
+    });
+}
+
+int sfdg_fd_shrink_count(sfdg_fd_sketcher* h, size_t* count) {
+    return guard([&] {
+        if (!h || !h->impl || !count) throw invalid_argument("null FD sketcher");
+        *count = h->impl->shrink_count();
+    });
+}
+
+int sfdg_sharded_sketch(const sfdg_sketch_config* cfg, const int64_t* row_ptr, const uint32_t* cols,
+                        const double* vals, size_t nrows, int shards, const int* devices, int ndev, double* out,
+                        sfdg_stats* shard_stats) {
+    return guard([&] {
+        if (!cfg || !row_ptr || !devices) throw invalid_argument("sharded_sketch: null argument");
+        if (shards < 1) throw invalid_argument("sharded_sketch: shards must be >= 1");
+        if (ndev < 1) throw invalid_argument("sharded_sketch: needs at least one device");
+        SketchCfg c;
+        c.ell = cfg->ell;
+        c.d = cfg->d;
+        c.delta = cfg->delta;
+        c.power = to_power(&cfg->power);
+        c.seed = cfg->seed;
+        validate_cfg(c);
+        for (int i = 0; i < ndev; ++i) require_device(devices[i]);
+        const size_t per = (nrows + shards - 1) / shards;
+        std::vector<std::unique_ptr<Sketcher>> sk(shards);
+        std::vector<std::string> errs(shards);
+        std::vector<int> codes(shards, SFDG_OK);
+        std::vector<std::thread> th;
+        for (int g = 0; g < shards; ++g)
+            th.emplace_back([&, g] {
+                codes[g] = guard([&] {
+                    const int dev = devices[g % ndev];
+                    CK(cudaSetDevice(dev));
+                    SketchCfg cg = c;
+                    cg.seed = c.seed + (uint64_t)g;  // per-shard seed
+                    sk[g] = std::make_unique<Sketcher>(cg, dev);
+                    const size_t r0 = std::min(nrows, g * per), r1 = std::min(nrows, (g + 1) * per);
+                    if (r1 > r0) sk[g]->append_host(row_ptr + r0, cols, vals, r1 - r0, nullptr);
+                    sk[g]->finalize(nullptr);
+                });
+                if (codes[g] != SFDG_OK) errs[g] = g_last_error;
+            });
+        for (auto& t : th) t.join();
+        for (int g = 0; g < shards; ++g)
+            if (codes[g] != SFDG_OK) {
+                g_last_error = errs[g];
+                if (codes[g] == SFDG_INVALID_ARGUMENT) throw invalid_argument(errs[g]);
+                if (codes[g] == SFDG_NUMERICAL_ERROR) throw numerical_error(errs[g]);
+                throw cuda_error(errs[g]);
+            }
+        if (shard_stats)
+            for (int g = 0; g < shards; ++g) sk[g]->stats(&shard_stats[g]);
+        for (int step = 1; step < shards; step *= 2)  // shards.py tree order, lower rank first
+            for (int r = 0; r + step < shards; r += 2 * step) sk[r]->merge_from(*sk[r + step]);
+        sk[0]->get_sketch(out);
+    });
 }
 
 int sfdg_merge(const double* b1, size_t rows1, const double* b2, size_t rows2, size_t d, size_t ell, double* out,

@@ -503,6 +503,13 @@ void Engine::densify_into_stack(const DevCsr& src, int off) {
                src.row_ptr, src.col, src.val, src.m, Mt[cur], 2 * lp, off);
 }
 
+void Engine::scatter_rows_t(double* dst, int ld, int col0) {
+    if (a.m <= 0) return;
+    fill2d(dst + col0, d, a.m, ld, 0.0, st);
+    LAUNCH(densify_t_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)a.m * 32, 256))), 256, 0, st, a.row_ptr,
+           a.col, a.val, a.m, dst, ld, col0);
+}
+
 void Engine::sketch_to_host(double* out) {
     double* tmp = scr.take<double>((int64_t)ell * d);
     transpose(Mt[cur], d, ell, 2 * lp, tmp, d, st);

@@ -127,6 +127,9 @@ class Engine {
     void densify_into_stack(int off);
     // Same from another engine's buffer (the sketcher's filling lane).
     void densify_into_stack(const DevCsr& src, int off);
+    // Rows of this engine's CSR buffer into columns [col0, col0 + m) of dst (d x ld), those
+    // columns zeroed first (FdSketcher appends of sparse rows).
+    void scatter_rows_t(double* dst, int ld, int col0);
     // Copies the current B (ell x d row-major) to host.
     void sketch_to_host(double* out);
     double read_scalar(const double* dptr);

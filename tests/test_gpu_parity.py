@@ -519,3 +519,63 @@ def test_lane_count_does_not_change_results(monkeypatch):
         out.append(sketch_gpu(rp, cs, vs, 1000, 50, 0))
     for b, st in out[1:]:
         assert np.array_equal(b, out[0][0]) and st == out[0][1]
+
+
+# ---------------------------------------------------------------- sharded sketch (8(e))
+@pytest.mark.parametrize("shards", [1, 2, 3, 4])
+def test_sharded_sketch_matches_oracle_tree(oracle, shards):
+    """sfdg_sharded_sketch against the oracle replaying the same shards, seeds (seed + g)
+    and merge-tree order (each shard count has its own oracle answer)."""
+    from paper_1602_00412_b200 import shards as SH
+    rp, cs, vs = S.generate("c1", (0, 3000))
+    cfg = P.SketchConfig(ell=50, d=1000, seed=11)
+    b, st = P.sharded_sketch(rp, cs, vs, cfg, shards, devices=[0])
+    n = len(rp) - 1
+    per = (n + shards - 1) // shards
+    parts, ostats = [], []
+    for g in range(shards):
+        r0, r1 = min(n, g * per), min(n, (g + 1) * per)
+        srp = rp[r0:r1 + 1] - rp[r0]
+        bo, so = oracle.sketch(srp, cs[rp[r0]:rp[r1]], vs[rp[r0]:rp[r1]], 1000, 50, seed=11 + g)
+        parts.append(bo)
+        ostats.append(so)
+    want = SH.replay_tree(parts, lambda a, c: oracle.merge(a, c, 50))
+    assert btb_rel(b, want) <= BTB_TOL
+    for s, so in zip(st, ostats):
+        assert (s["flushes"], s["attempts"], s["verifier_i"]) == (so["flushes"], so["attempts"], so["verifier_i"])
+        assert s["delta_spent"] == so["delta_spent"]
+
+
+# ---------------------------------------------------------------- FdSketcher (8(f) rank 1)
+@pytest.mark.parametrize("n,d,ell", [(7, 5, 2), (40, 12, 4), (3, 6, 3), (250, 300, 20), (61, 9, 6), (900, 1000, 50)])
+def test_fd_sketcher_vs_oracle(oracle, n, d, ell):
+    g = np.random.default_rng(n + d)
+    a = g.standard_normal((n, d))
+    bo, co = oracle.fd_sketch(a, ell)
+    f = P.FdSketcher(ell, d)
+    f.append_rows(a)
+    b = f.finalize()
+    assert f.shrink_count() == co
+    assert btb_rel(b, bo) <= BTB_TOL
+    # one row at a time: bit-identical to the batched appends
+    f1 = P.FdSketcher(ell, d)
+    for i in range(n):
+        f1.append(a[i])
+    assert np.array_equal(f1.finalize(), b)
+
+
+def test_fd_sketcher_sparse_rows_and_errors(oracle):
+    rp, cs, vs = S.generate("c1", (0, 700))
+    a = dense_of(rp, cs, vs, 1000)
+    bo, co = oracle.fd_sketch(a, 50)
+    f = P.FdSketcher(50, 1000)
+    f.append_csr(rp, cs, vs)
+    assert f.shrink_count() == co and btb_rel(f.finalize(), bo) <= BTB_TOL
+    with pytest.raises(P.InvalidArgument):
+        P.FdSketcher(0, 5)
+    with pytest.raises(P.InvalidArgument):
+        P.FdSketcher(6, 5)
+    f = P.FdSketcher(2, 3)
+    f.append([1.0, float("nan"), 0.0])
+    with pytest.raises(P.InvalidArgument, match="non-finite"):
+        f.append_rows(np.ones((3, 3)))

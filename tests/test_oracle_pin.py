@@ -168,3 +168,15 @@ def test_retry_cap_is_a_numerical_error(oracle):
     assert att >= 1
     with pytest.raises((NumericalError, InvalidArgument)):
         oracle.boosted_sparse_shrink(csr, 30, 0, VerifierState(), oracle.rng(1))
+
+
+def test_fd_sketcher_oracle_matches_reference(oracle, reference):
+    """FdSketcher restatement (sketch.cpp:47-78) against the compiled reference: buffer
+    fills, the finalize partial shrink, the tall (2 ell > d) stack and < ell rows."""
+    g = np.random.default_rng(3)
+    for n, d, ell in [(7, 5, 2), (40, 12, 4), (3, 6, 3), (25, 30, 5), (61, 9, 6), (1, 4, 4)]:
+        a = g.standard_normal((n, d))
+        bo, co = oracle.fd_sketch(a, ell)
+        br, cr = reference.fd_sketch(a, ell)
+        assert co == cr
+        assert np.array_equal(bo, br)
