@@ -11,7 +11,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
+#include <condition_variable>
 #include <deque>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <memory>
 #include <new>
@@ -74,6 +77,71 @@ double csr_frob(const int64_t* row_ptr, const double* vals, size_t m) {
 
 }  // namespace
 
+// One host thread per lane: a lane's phase (a few hundred launches) is enqueued off the
+// coordinating thread, so the coordinator keeps reacting to the other lanes. Tasks run one
+// at a time; busy() is true from post() until the task returned.
+class Worker {
+  public:
+    explicit Worker(int device) : dev(device), th([this] { loop(); }) {}
+    ~Worker() {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            stop = true;
+        }
+        cv.notify_one();
+        th.join();
+    }
+    void post(std::function<void()> f) {
+        busy_.store(true, std::memory_order_release);
+        {
+            std::lock_guard<std::mutex> g(mu);
+            task = std::move(f);
+            has = true;
+        }
+        cv.notify_one();
+    }
+    bool busy() const { return busy_.load(std::memory_order_acquire); }
+    void wait() const {
+        while (busy()) std::this_thread::yield();
+    }
+    std::exception_ptr take_error() {
+        std::lock_guard<std::mutex> g(mu);
+        std::exception_ptr e = err;
+        err = nullptr;
+        return e;
+    }
+
+  private:
+    void loop() {
+        cudaSetDevice(dev);
+        for (;;) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return has || stop; });
+                if (!has) return;
+                f = std::move(task);
+                has = false;
+            }
+            try {
+                f();
+            } catch (...) {
+                std::lock_guard<std::mutex> g(mu);
+                err = std::current_exception();
+            }
+            busy_.store(false, std::memory_order_release);
+        }
+    }
+    int dev;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::function<void()> task;
+    bool has = false, stop = false;
+    std::atomic<bool> busy_{false};
+    std::exception_ptr err;
+    std::thread th;  // last: starts after the members above exist
+};
+
 // Position in the reference's state sequence at a flush boundary: the Rng stream and the
 // verifier (sketch.cpp:25-32 threads both through every flush).
 struct FlushState {
@@ -114,6 +182,7 @@ class Sketcher {
                                              (int)cfg.d, &rng, false);
             CK(cudaEventCreateWithFlags(&L.ev, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&L.ev_bp_free, cudaEventDisableTiming));
+            if (use_workers()) L.worker = std::make_unique<Worker>(device);
         }
         CK(cudaEventCreateWithFlags(&ev_verify, cudaEventDisableTiming));
         CK(cudaEventRecord(ev_verify, chain->st));
@@ -137,6 +206,8 @@ class Sketcher {
 
     ~Sketcher() {
         try {
+            for (auto& L : lanes)
+                if (L.worker) L.worker->wait();
             sync_all();
             if (!trace_path.empty()) dump_trace();
         } catch (...) {
@@ -354,6 +425,7 @@ class Sketcher {
         int last_since = 1;
         cudaEvent_t ev = nullptr;          // completion of the queued phase
         cudaEvent_t ev_bp_free = nullptr;  // the chain finished reading Bp
+        std::unique_ptr<Worker> worker;            // null: enqueue on the calling thread
         cudaEvent_t tr0 = nullptr, tr1 = nullptr;  // SFDG_TRACE: timed bounds of the queued phase
         double tr_enq = 0.0, tr_enq_end = 0.0;
         bool bp_pending = false;
@@ -461,13 +533,15 @@ class Sketcher {
     void flush() {
         Lane& L = lanes[fill];
         L.id = next_id++;
-        L.eng->scr.reset();
-        trace_begin(L);
-        upload_row_ptr(L);
-        L.eng->prepare_async();
-        trace_end(L);
-        CK(cudaEventRecord(L.ev, L.eng->st));
         L.phase = Lane::Preparing;
+        run(L, [this, &L] {
+            L.eng->scr.reset();
+            trace_begin(L);
+            upload_row_ptr(L);
+            L.eng->prepare_async();
+            trace_end(L);
+            CK(cudaEventRecord(L.ev, L.eng->st));
+        });
         inflight.push_back(fill);
         // the next filling lane: an idle one, committing older flushes until one frees up
         for (;;) {
@@ -511,22 +585,36 @@ class Sketcher {
 
     void enqueue_attempt(Lane& L) {
         if (++L.attempt > kRetryCap) throw numerical_error("boosted_sparse_shrink: retry cap exceeded");
-        Engine& e = *L.eng;
         L.pos0 = L.cur.pos;
-        L.interval_used = e.adaptive ? L.interval : 1;
-        e.orth_interval = L.interval_used;
-        e.pos = L.cur.pos;
-        e.scr.reset();
-        if (L.bp_pending) {  // the chain's dense shrink of this lane's previous B'
-            CK(cudaStreamWaitEvent(e.st, L.ev_bp_free, 0));
-            L.bp_pending = false;
-        }
-        trace_begin(L);
-        e.attempt_enqueue(cfg.power, e.Bp, e.lp);
-        trace_end(L);
-        L.cur.pos = e.pos;
-        CK(cudaEventRecord(L.ev, e.st));
+        L.interval_used = L.eng->adaptive ? L.interval : 1;
+        const bool wait_bp = L.bp_pending;  // the chain's dense shrink of this lane's previous B'
+        L.bp_pending = false;
         L.phase = Lane::Shrinking;
+        run(L, [this, &L, wait_bp] {
+            Engine& e = *L.eng;
+            e.orth_interval = L.interval_used;
+            e.pos = L.cur.pos;
+            e.scr.reset();
+            if (wait_bp) CK(cudaStreamWaitEvent(e.st, L.ev_bp_free, 0));
+            trace_begin(L);
+            e.attempt_enqueue(cfg.power, e.Bp, e.lp);
+            trace_end(L);
+            L.cur.pos = e.pos;
+            CK(cudaEventRecord(L.ev, e.st));
+        });
+    }
+
+    // Enqueue a phase on the lane's worker thread (or inline without workers).
+    void run(Lane& L, std::function<void()> f) {
+        if (L.worker) L.worker->post(std::move(f));
+        else f();
+    }
+
+    // Off by default: measured no gain on c2 (212.5 vs 211.1 ms per stream) -- the device,
+    // not the enqueueing thread, is the bottleneck with 4 lanes. SFDG_WORKERS=1 enables.
+    static bool use_workers() {
+        const char* e = std::getenv("SFDG_WORKERS");
+        return e && std::atoi(e) != 0;
     }
 
     // Advance one lane whose queued phase has completed.
@@ -567,13 +655,19 @@ class Sketcher {
                     break;
                 }
                 L.delta_hat = delta_hat;
-                e.pos = L.cur.pos;
-                trace_begin(L);
-                e.verify_enqueue(L.cur.ver, delta_hat, e.Bp, e.lp, serial_verify ? ev_verify : nullptr);
-                trace_end(L);
-                L.cur.pos = e.pos;
-                CK(cudaEventRecord(L.ev, e.st));
                 L.phase = Lane::Verifying;
+                run(L, [this, &L, delta_hat] {
+                    Engine& e = *L.eng;
+                    e.pos = L.cur.pos;
+                    trace_begin(L);
+                    {
+                        std::lock_guard<std::mutex> g(verify_mu);  // keeps the ev_verify chain in order
+                        e.verify_enqueue(L.cur.ver, delta_hat, e.Bp, e.lp, serial_verify ? ev_verify : nullptr);
+                    }
+                    trace_end(L);
+                    L.cur.pos = e.pos;
+                    CK(cudaEventRecord(L.ev, e.st));
+                });
                 break;
             }
             case Lane::Verifying: {
@@ -624,6 +718,10 @@ class Sketcher {
             for (size_t k = 0; k < inflight.size(); ++k) {
                 Lane& L = lanes[inflight[k]];
                 if (L.phase == Lane::Done) continue;
+                if (L.worker) {
+                    if (L.worker->busy()) continue;  // its phase is still being enqueued
+                    if (std::exception_ptr ep = L.worker->take_error()) std::rethrow_exception(ep);
+                }
                 const cudaError_t q = cudaEventQuery(L.ev);
                 if (q == cudaErrorNotReady) continue;
                 CK(q);
@@ -707,12 +805,19 @@ class Sketcher {
     }
 
     void sync_all() {
+        for (auto& L : lanes)
+            if (L.worker) L.worker->wait();
         for (auto& L : lanes) CK(cudaStreamSynchronize(L.eng->st));
         chain->sync();
     }
 
     // Drop every in-flight flush (after an error, or on reset); committed state stays.
     void abort_inflight() {
+        for (auto& L : lanes)
+            if (L.worker) {
+                L.worker->wait();
+                L.worker->take_error();
+            }
         for (auto& L : lanes) cudaStreamSynchronize(L.eng->st);
         chain->sync();
         for (int i : inflight) {
@@ -745,6 +850,7 @@ class Sketcher {
     };
     std::vector<ChainTrace> tr_chain;
     cudaEvent_t ev_verify = nullptr;
+    std::mutex verify_mu;
     bool serial_verify = !(std::getenv("SFDG_VERIFY_SERIAL") && std::atoi(std::getenv("SFDG_VERIFY_SERIAL")) == 0);
     FlushState committed;
     int fill = 0;

@@ -163,6 +163,7 @@ void RngStream::reseed() {
 }
 
 void RngStream::restart(uint64_t seed_) {
+    std::lock_guard<std::recursive_mutex> lk(mu);
     seed = seed_;
     explicit_at = ~0ull;
     reseed();
@@ -219,6 +220,7 @@ void RngStream::ensure(uint64_t w_begin, uint64_t w_end, cudaStream_t consumer) 
 }
 
 void RngStream::prefetch(uint64_t w_end) {
+    std::lock_guard<std::recursive_mutex> lk(mu);
     uint64_t cap_end = w_end;
     if (cap_end > gen_words + ring_cap / 2) cap_end = gen_words + ring_cap / 2;
     generate_to(cap_end);
@@ -240,6 +242,7 @@ void RngStream::mark_consumed(uint64_t w_begin, cudaStream_t consumer) {
 // dimension ld, zero padding beyond cols), advancing pos.
 void RngStream::normals(RngPos& pos, uint64_t n, uint64_t cols, uint64_t ld, double* d_out, int* d_err,
                         cudaStream_t stream) {
+    std::lock_guard<std::recursive_mutex> lk(mu);
     if (n == 0) return;
     const RngPos next = rng_advance(pos, n);
     const bool from_ring = pos.has_spare && explicit_at != pos.words;
@@ -261,6 +264,7 @@ void RngStream::normals(RngPos& pos, uint64_t n, uint64_t cols, uint64_t ld, dou
 }
 
 double RngStream::spare_value(const RngPos& pos, cudaStream_t stream) {
+    std::lock_guard<std::recursive_mutex> lk(mu);
     if (!pos.has_spare) return 0.0;
     double v = 0.0;
     if (explicit_at == pos.words) {
@@ -279,6 +283,7 @@ double RngStream::spare_value(const RngPos& pos, cudaStream_t stream) {
 }
 
 void RngStream::set_spare(const RngPos& pos, double v, cudaStream_t stream) {
+    std::lock_guard<std::recursive_mutex> lk(mu);
     CK(cudaMemcpyAsync(d_spare, &v, sizeof v, cudaMemcpyHostToDevice, stream));
     CK(cudaStreamSynchronize(stream));
     explicit_at = pos.words;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 namespace sfdg {
@@ -66,6 +67,7 @@ class RngStream {
     };
     std::vector<Consumer> live;       // readers not yet known to be done
     std::vector<cudaEvent_t> pool;    // recycled events
+    std::recursive_mutex mu;          // lanes enqueue from their own host threads
 };
 
 }  // namespace sfdg

@@ -271,7 +271,9 @@ __device__ __forceinline__ void gather_range(int kb, int ke, const int* __restri
 }
 
 template <int J>
-__global__ void spmm_rows_kernel(const int* __restrict__ ptr, const int* __restrict__ idx, const double* __restrict__ val,
+__global__ void __launch_bounds__(256, (J <= 2 ? 5 : 1)) spmm_rows_kernel(const int* __restrict__ ptr,
+                                                                        const int* __restrict__ idx,
+                                                                        const double* __restrict__ val,
                                  int nrows, int piece, const double* __restrict__ in, int ld, int ncols,
                                  double* __restrict__ out, int ldo) {
     const int lane = threadIdx.x & 31;

@@ -125,7 +125,25 @@ __device__ __forceinline__ void block_partials(double (&tn)[kMaxQ], double ns, i
     }
 }
 
+// Sum of four per-lane partials across the warp in 6 shuffles (transposed butterfly):
+// afterwards lanes 8u .. 8u+7 hold the total of partial u.
+__device__ __forceinline__ double warp_sum4(const double (&v)[4]) {
+    const int lane = threadIdx.x & 31;
+    const bool h16 = lane & 16, h8 = lane & 8;
+    double a0 = h16 ? v[2] : v[0], a1 = h16 ? v[3] : v[1];
+    a0 += __shfl_xor_sync(0xffffffffu, h16 ? v[0] : v[2], 16);
+    a1 += __shfl_xor_sync(0xffffffffu, h16 ? v[1] : v[3], 16);
+    double c = h8 ? a1 : a0;
+    c += __shfl_xor_sync(0xffffffffu, h8 ? a0 : a1, 8);
+    c += __shfl_xor_sync(0xffffffffu, c, 4);
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    return c;
+}
+
+template <int Q>
 __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
+    extern __shared__ __align__(16) unsigned char vsm[];
     __shared__ double sh[8];
     __shared__ double tloc[256];             // current t = B' x
     __shared__ double wpart[kVWarps][257];   // per-warp partials of the next t, and |.|^2
@@ -136,6 +154,44 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     const int64_t rper = (a.m + nb - 1) / nb, cper = (a.d + nb - 1) / nb;
     const int64_t r0 = blockIdx.x * rper, r1 = min((int64_t)a.m, r0 + rper);
     const int64_t c0 = blockIdx.x * cper, c1 = min((int64_t)a.d, c0 + cper);
+    // The block's slices of A' (CSR rows r0..r1, CSC columns c0..c1) do not change across
+    // the power-method steps: stage them in shared memory when they fit, so each step pays
+    // one dependent round trip (the x / u gather) instead of three.
+    const int nr = (int)max((int64_t)0, r1 - r0), nc = (int)max((int64_t)0, c1 - c0);
+    const int rbase = nr > 0 ? a.row_ptr[r0] : 0, knr = nr > 0 ? a.row_ptr[r1] - rbase : 0;
+    const int cbase = nc > 0 ? a.col_ptr[c0] : 0, knc = nc > 0 ? a.col_ptr[c1] - cbase : 0;
+    const size_t need = 12 * ((size_t)knr + knc) + 4 * ((size_t)nr + nc + 2);
+    const bool staged = need <= (size_t)a.stage_bytes;
+    const int *RP = a.row_ptr + r0, *CP = a.col_ptr + c0, *RI = a.row_idx + cbase;
+    const uint32_t* CI = a.col + rbase;
+    const double *RV = a.val + rbase, *CV = a.cval + cbase;
+    int rsub = rbase, csub = cbase;
+    if (staged) {
+        double* s_rv = reinterpret_cast<double*>(vsm);
+        double* s_cv = s_rv + knr;
+        uint32_t* s_ci = reinterpret_cast<uint32_t*>(s_cv + knc);
+        int* s_ri = reinterpret_cast<int*>(s_ci + knr);
+        int* s_rp = s_ri + knc;
+        int* s_cp = s_rp + nr + 1;
+        for (int i = threadIdx.x; i < knr; i += kVThreads) {
+            s_rv[i] = RV[i];
+            s_ci[i] = CI[i];
+        }
+        for (int i = threadIdx.x; i < knc; i += kVThreads) {
+            s_cv[i] = CV[i];
+            s_ri[i] = RI[i];
+        }
+        for (int i = threadIdx.x; i <= nr; i += kVThreads) s_rp[i] = RP[i] - rbase;
+        for (int i = threadIdx.x; i <= nc; i += kVThreads) s_cp[i] = CP[i] - cbase;
+        RP = s_rp;
+        CP = s_cp;
+        RI = s_ri;
+        CI = s_ci;
+        RV = s_rv;
+        CV = s_cv;
+        rsub = csub = 0;
+        __syncthreads();
+    }
 
     // ---- init: |x0|^2 (la_core.cpp:177-186) and the partials of B' x0 over own columns
     {
@@ -147,7 +203,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
             const double xc = a.x0[c];
             ns = fma(xc, xc, ns);
 #pragma unroll
-            for (int q = 0; q < kMaxQ; ++q) {
+            for (int q = 0; q < Q; ++q) {
                 const int j = lane + 32 * q;
                 if (j < L) tn[q] = fma(a.bt[c * a.ldb + j], xc, tn[q]);
             }
@@ -172,51 +228,84 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     for (; step < a.steps; ++step) {
         double* y = a.ybuf + (size_t)(step & 1) * a.d;
         double* tp = a.tpart + (size_t)((step + 1) & 1) * nb * L;  // partials of the next t
-        // ---- phase A: u = A' x over this block's rows
-        for (int64_t r = r0 + wib; r < r1; r += 2 * kVWarps) {
-            const int64_t r2 = r + kVWarps;
-            const bool has2 = r2 < r1;
-            double s = 0.0, s2 = 0.0;
-            const int k0 = a.row_ptr[r], k1 = a.row_ptr[r + 1];
-            const int q0 = has2 ? a.row_ptr[r2] : 0, q1 = has2 ? a.row_ptr[r2 + 1] : 0;
-            for (int k = k0 + lane, q = q0 + lane; k < k1 || q < q1; k += 32, q += 32) {
-                if (k < k1) s = fma(a.val[k], __ldcg(xsrc + a.col[k]) * xscale, s);
-                if (q < q1) s2 = fma(a.val[q], __ldcg(xsrc + a.col[q]) * xscale, s2);
+        // ---- phase A: u = A' x over this block's rows, four rows per warp in flight
+        for (int64_t rb = r0 + wib; rb < r1; rb += 4 * kVWarps) {
+            int k0[4], k1[4];
+            int len = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t r = rb + q * kVWarps;
+                k0[q] = r < r1 ? RP[r - r0] - rsub : 0;
+                k1[q] = r < r1 ? RP[r - r0 + 1] - rsub : 0;
+                len = max(len, k1[q] - k0[q]);
             }
-            s = warp_sum(s);
-            s2 = warp_sum(s2);
-            if (lane == 0) {
-                a.u[r] = s;
-                if (has2) a.u[r2] = s2;
+            double sp[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int off = lane; off < len; off += 32) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int k = k0[q] + off;
+                    if (k < k1[q]) sp[q] = fma(RV[k], __ldcg(xsrc + CI[k]) * xscale, sp[q]);
+                }
             }
+            const double tot = warp_sum4(sp);
+            const int q = lane >> 3;
+            const int64_t r = rb + q * kVWarps;
+            if ((lane & 7) == 0 && r < r1) a.u[r] = tot;
         }
         grid_sync(bar, nb);
-        // ---- phase B: y over own columns; next-t partials and |y|^2 from the same rows
+        // ---- phase B: y over own columns (four per warp in flight); next-t partials and
+        // |y|^2 from the same B'^T rows
+        double tl[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) tl[q] = (lane + 32 * q < L) ? tloc[lane + 32 * q] : 0.0;
         double tn[kMaxQ];
 #pragma unroll
         for (int q = 0; q < kMaxQ; ++q) tn[q] = 0.0;
         double nsq = 0.0;
         bool bad = false;
-        for (int64_t c = c0 + wib; c < c1; c += kVWarps) {
-            double s = 0.0;
-            for (int k = a.col_ptr[c] + lane; k < a.col_ptr[c + 1]; k += 32)
-                s = fma(a.cval[k], __ldcg(a.u + a.row_idx[k]), s);
-            double brow[kMaxQ];
-            double bsum = 0.0;
+        for (int64_t cb = c0 + wib; cb < c1; cb += 4 * kVWarps) {
+            int k0[4], k1[4];
+            int len = 0;
 #pragma unroll
-            for (int q = 0; q < kMaxQ; ++q) {
-                const int j = lane + 32 * q;
-                brow[q] = j < L ? a.bt[c * a.ldb + j] : 0.0;
-                bsum = fma(brow[q], j < L ? tloc[j] : 0.0, bsum);
+            for (int q = 0; q < 4; ++q) {
+                const int64_t c = cb + q * kVWarps;
+                k0[q] = c < c1 ? CP[c - c0] - csub : 0;
+                k1[q] = c < c1 ? CP[c - c0 + 1] - csub : 0;
+                len = max(len, k1[q] - k0[q]);
             }
-            s = warp_sum(s);
-            bsum = warp_sum(bsum);
-            const double yc = a.scale * (s - bsum);  // shrink.cpp:124
-            if (!isfinite(yc)) bad = true;
-            if (lane == 0) y[c] = yc;
-            nsq = fma(yc, yc, nsq);
+            double brow[4][Q];
+            double dp[4];
 #pragma unroll
-            for (int q = 0; q < kMaxQ; ++q) tn[q] = fma(brow[q], yc, tn[q]);
+            for (int q = 0; q < 4; ++q) {
+                const int64_t c = cb + q * kVWarps;
+                dp[q] = 0.0;
+#pragma unroll
+                for (int w = 0; w < Q; ++w) {
+                    const int j = lane + 32 * w;
+                    brow[q][w] = (c < c1 && j < L) ? a.bt[c * a.ldb + j] : 0.0;
+                    dp[q] = fma(-brow[q][w], tl[w], dp[q]);  // - (B'^T t)_c partial
+                }
+            }
+            for (int off = lane; off < len; off += 32) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int k = k0[q] + off;
+                    if (k < k1[q]) dp[q] = fma(CV[k], __ldcg(a.u + RI[k]), dp[q]);
+                }
+            }
+            const double tot = warp_sum4(dp);  // (A'^T u - B'^T t)_c on lanes 8q..8q+7
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t c = cb + q * kVWarps;
+                const double yc = a.scale * __shfl_sync(0xffffffffu, tot, 8 * q);  // shrink.cpp:124
+                if (c < c1) {
+                    if (!isfinite(yc)) bad = true;
+                    if (lane == 0) y[c] = yc;
+                    nsq = fma(yc, yc, nsq);
+#pragma unroll
+                    for (int w = 0; w < Q; ++w) tn[w] = fma(brow[q][w], yc, tn[w]);
+                }
+            }
         }
         if (bad) atomicOr(a.err, ERR_NONFINITE_VERIFY);
         block_partials(tn, nsq, L, wpart, tp, a.part);
@@ -250,29 +339,59 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     }
 }
 
+typedef void (*VerifyFn)(VerifyArgs);
+VerifyFn verify_fn(int ell) {
+    switch ((ell + 31) / 32) {
+        case 1: return verify_kernel<1>;
+        case 2: return verify_kernel<2>;
+        case 3: return verify_kernel<3>;
+        case 4: return verify_kernel<4>;
+        case 5: return verify_kernel<5>;
+        case 6: return verify_kernel<6>;
+        case 7: return verify_kernel<7>;
+        default: return verify_kernel<8>;
+    }
+}
+
 }  // namespace
 
 int verify_grid_blocks(int device) {
     static int cached[64] = {0};
     if (device >= 0 && device < 64 && cached[device]) return cached[device];
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, verify_kernel, kVThreads, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, verify_kernel<8>, kVThreads, 0));
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    // One block per SM on half the SMs: the power method is latency bound (two grid
-    // barriers per step), and with several flushes in flight the other half keeps running
-    // their SpMM / orthonormalisation kernels (measured: 322 -> 249 ms per c2 stream).
-    int nb = std::max(1, std::min(per_sm, 1) * sms / 2);
+    // 32 blocks: the power method is latency bound (two grid barriers per step), and with
+    // several flushes in flight the other SMs keep running their SpMM / orthonormalisation
+    // kernels (measured on c2: 146 blocks 322, 74 blocks 199, 32 blocks 182 ms per stream).
+    int nb = std::max(1, std::min(std::min(per_sm, 1) * sms, 32));
     if (const char* e = std::getenv("SFDG_VERIFY_BLOCKS")) nb = std::max(1, std::min(nb, std::atoi(e)));
     if (device >= 0 && device < 64) cached[device] = nb;
     return nb;
 }
 
-void verify_launch(const VerifyArgs& args, int nblocks, cudaStream_t st) {
+void verify_launch(const VerifyArgs& args_in, int nblocks, cudaStream_t st) {
     ProfScope prof("verify", st);
+    VerifyFn fn = verify_fn(args_in.ell);
+    static int stage = -1;
+    if (stage < 0) {
+        for (VerifyFn f : {verify_kernel<1>, verify_kernel<2>, verify_kernel<3>, verify_kernel<4>, verify_kernel<5>,
+                           verify_kernel<6>, verify_kernel<7>, verify_kernel<8>})
+            allow_max_dynamic_smem(f);
+        cudaFuncAttributes attr;
+        CK(cudaFuncGetAttributes(&attr, (const void*)verify_kernel<8>));
+        int dev = 0, optin = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        stage = optin - (int)attr.sharedSizeBytes - 1024;
+        if (const char* e = std::getenv("SFDG_VERIFY_STAGE")) stage = std::atoi(e) ? stage : 0;
+    }
+    VerifyArgs args = args_in;
+    args.stage_bytes = stage;
     CK(cudaMemsetAsync(args.bar, 0, 2 * sizeof(unsigned), st));
     void* params[] = {(void*)&args};
-    CK(cudaLaunchCooperativeKernel((const void*)verify_kernel, dim3(nblocks), dim3(kVThreads), params, 0, st));
+    CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(nblocks), dim3(kVThreads), params, (size_t)stage, st));
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

@@ -32,6 +32,7 @@ struct VerifyArgs {
     unsigned* bar;  // 2
     int* err;
     double* out;  // [accepted, log_mag, steps_run]
+    int stage_bytes;  // dynamic shared memory for the block's CSR/CSC slices (0 = read from global)
 };
 
 int verify_grid_blocks(int device);
