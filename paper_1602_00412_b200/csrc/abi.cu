@@ -175,7 +175,9 @@ class Sketcher {
         const int lanes_n = lane_count();
         const uint64_t per_flush = (uint64_t)cfg.d * cfg.ell + cfg.d + 16;  // raw words drawn per attempt
         rng.init(cfg.seed, std::max<uint64_t>((uint64_t)(lanes_n + 3) * per_flush, 1 << 20), device);
-        chain = std::make_unique<Engine>(device, (int)cfg.d, (int)cfg.ell, cfg.seed, 1, 1, &rng, true);
+        chain = std::make_unique<Engine>(device, (int)cfg.d, (int)cfg.ell, cfg.seed, 1, 1, &rng, true,
+                                         std::getenv("SFDG_CHAIN_PRIORITY") != nullptr &&
+                                             std::atoi(std::getenv("SFDG_CHAIN_PRIORITY")) != 0);
         lanes.resize(lanes_n);
         for (auto& L : lanes) {
             L.eng = std::make_unique<Engine>(device, (int)cfg.d, (int)cfg.ell, cfg.seed, (uint64_t)nnz_trigger + cfg.d,

@@ -142,14 +142,20 @@ void raise_device_flags(int e) {
 }
 
 Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, int m_cap_, RngStream* shared_rng,
-               bool stack)
+               bool stack, bool high_priority)
     : device(device_), d(d_), ell(ell_) {
     if (ell < 1 || ell > kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 256] for this build");
     lp = (int)round_up((size_t)ell, 8);
     if (const char* e = std::getenv("SFDG_ORTH_EVERY_SWEEP")) adaptive = std::atoi(e) == 0;
     set_device();
-    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    int prio = 0;
+    if (high_priority) {
+        int least = 0, greatest = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        prio = greatest;
+    }
+    CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio));
+    CK(cudaStreamCreateWithPriority(&st2, cudaStreamNonBlocking, prio));
     for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&ev_read_done[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_bprime, cudaEventDisableTiming));
     if (shared_rng) {
@@ -308,6 +314,18 @@ void Engine::orthonormalize(double* Yp, int m, int err_bit) {
     gemm_nn(Yt, m, lp, lp, rinv, lp, lp, Yp, lp, st, st2 + 4);
 }
 
+void Engine::orthonormalize_light(int m, int err_bit) {
+    // One CholeskyQR pass, Y <- Y R^{-1} (into Yt, then the buffers swap). Used between
+    // sweeps of the adaptive schedule, where Y only has to stay well conditioned: the
+    // interval keeps cond(Y) <= kKappaTarget, so one pass leaves Y orthonormal to
+    // O(kappa^2 eps) with its span unchanged. The last pass is always the full CholeskyQR2.
+    double* st1 = d_scal + 16;
+    gram_tn(Y, m, lp, lp, gram, lp, scr, st);
+    chol_factor(gram, lp, lp, rfac, dinv8, nullptr, 0, st1, d_err, err_bit, scr, st, false);
+    trsm_apply(Y, m, lp, lp, rfac, dinv8, Yt, lp, nullptr, st);
+    std::swap(Y, Yt);
+}
+
 void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     const int m = a.m;
     if (k < 1 || k > std::min(m, d)) throw invalid_argument("simultaneous_iteration: k out of range");
@@ -316,7 +334,8 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     // G = gaussian_matrix(d, k) in W (la_core.cpp:167-172), pad columns zero
     rng->normals(pos, (uint64_t)d * k, (uint64_t)k, (uint64_t)lp, W, d_err, st);
     spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
-    orthonormalize(Y, m, ERR_NONFINITE_ITER);
+    if (adaptive && q > 0) orthonormalize_light(m, ERR_NONFINITE_ITER);
+    else orthonormalize(Y, m, ERR_NONFINITE_ITER);
     // Only span(Y) matters for B' (it enters through Z Z^T), so CholeskyQR2 runs every
     // `interval` sweeps (adaptive, see boosted()) and always after the last sweep; in
     // between Y <- A'(A'^T Y) unnormalised. interval = 1 is the reference's schedule
@@ -327,7 +346,8 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
         spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st);
         spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
         if (++since >= interval || s + 1 == q) {
-            orthonormalize(Y, m, ERR_NONFINITE_ITER);
+            if (adaptive && s + 1 < q) orthonormalize_light(m, ERR_NONFINITE_ITER);
+            else orthonormalize(Y, m, ERR_NONFINITE_ITER);
             last_since = since;
             since = 0;
         }

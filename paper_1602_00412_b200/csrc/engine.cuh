@@ -49,8 +49,10 @@ class Engine {
   public:
     // shared_rng: draw from a sketcher-wide generator (flush pipeline lanes) instead of an
     // own one. stack: allocate Mt[2] (= [B^T | B'^T] pairs); lanes only need Bp (d x lp).
+    // high_priority: streams at the device's greatest priority (the sketcher's dense-shrink
+    // chain, a serial dependency that the lanes' kernels must not starve).
     Engine(int device, int d, int ell, uint64_t seed, uint64_t nnz_cap, int m_cap, RngStream* shared_rng = nullptr,
-           bool stack = true);
+           bool stack = true, bool high_priority = false);
     ~Engine();
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -101,6 +103,8 @@ class Engine {
     int* h_counts = nullptr;  // pinned [4]
     // la_core.cpp:130-165 contract on Y (m x lp, first k columns meaningful): CholeskyQR2.
     void orthonormalize(double* Yp, int m, int err_bit);
+    // Single CholeskyQR pass on Y (between sweeps of the adaptive schedule; swaps Y/Yt).
+    void orthonormalize_light(int m, int err_bit);
     // randsvd.cpp:18-51: Z (m x lp) left in Y.
     void simultaneous_iteration(int k, const PowerCfg& cfg);
     // shrink.cpp:63-73 (+ la_core.cpp:82-128): B'^T (d x lp) into bpt (ld).
