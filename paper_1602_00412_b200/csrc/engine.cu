@@ -401,6 +401,13 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
     args.bar = bar;
     args.err = d_err;
     args.out = vout;
+    args.has_long = plan_c.host_long != 0 ? 1 : 0;
+    args.long_cols = plan_c.long_rows;
+    args.long_first = plan_c.long_first;
+    args.piece_beg = plan_c.piece_beg;
+    args.piece_end = plan_c.piece_end;
+    args.counts = plan_c.counts;
+    args.lpart = scr.take<double>(std::max<int64_t>(1, plan_c.cap_pieces));
     if (serial) CK(cudaStreamWaitEvent(st, serial, 0));
     verify_launch(args, verify_blocks, st);
     if (serial) CK(cudaEventRecord(serial, st));

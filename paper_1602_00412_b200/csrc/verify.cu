@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "sparse.cuh"
 #include "verify.cuh"
 
 namespace sfdg {
@@ -253,6 +254,19 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
             if ((lane & 7) == 0 && r < r1) a.u[r] = tot;
         }
         grid_sync(bar, nb);
+        // ---- phase B0 (skewed columns only): pieces of the long columns over the whole grid
+        if (a.has_long) {
+            const int np = a.counts[1];
+            const int gw = blockIdx.x * kVWarps + wib, tw = nb * kVWarps;
+            for (int p = gw; p < np; p += tw) {
+                double sp = 0.0;
+                for (int k = a.piece_beg[p] + lane; k < a.piece_end[p]; k += 32)
+                    sp = fma(a.cval[k], __ldcg(a.u + a.row_idx[k]), sp);
+                sp = warp_sum(sp);
+                if (lane == 0) a.lpart[p] = sp;
+            }
+            grid_sync(bar, nb);
+        }
         // ---- phase B: y over own columns (four per warp in flight); next-t partials and
         // |y|^2 from the same B'^T rows
         double tl[Q];
@@ -266,11 +280,25 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
         for (int64_t cb = c0 + wib; cb < c1; cb += 4 * kVWarps) {
             int k0[4], k1[4];
             int len = 0;
+            double lsum[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int64_t c = cb + q * kVWarps;
                 k0[q] = c < c1 ? CP[c - c0] - csub : 0;
                 k1[q] = c < c1 ? CP[c - c0 + 1] - csub : 0;
+                if (a.has_long && k1[q] - k0[q] > 2 * kPiece) {  // its pieces were summed in B0
+                    int lo = 0, hi = a.counts[0];
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (a.long_cols[mid] < c) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    const int first = a.long_first[lo];
+                    const int npc = (k1[q] - k0[q] + kPiece - 1) / kPiece;
+                    if (lane == 0)
+                        for (int p = 0; p < npc; ++p) lsum[q] += __ldcg(a.lpart + first + p);
+                    k1[q] = k0[q];
+                }
                 len = max(len, k1[q] - k0[q]);
             }
             double brow[4][Q];
@@ -278,7 +306,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int64_t c = cb + q * kVWarps;
-                dp[q] = 0.0;
+                dp[q] = lsum[q];
 #pragma unroll
                 for (int w = 0; w < Q; ++w) {
                     const int j = lane + 32 * w;

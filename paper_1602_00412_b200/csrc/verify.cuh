@@ -33,6 +33,15 @@ struct VerifyArgs {
     int* err;
     double* out;  // [accepted, log_mag, steps_run]
     int stage_bytes;  // dynamic shared memory for the block's CSR/CSC slices (0 = read from global)
+    // Columns longer than 2 kPiece (skewed data: Zipf columns) are split into pieces that every
+    // warp of the grid shares (the CSC SegPlan of the SpMM), summed per column in fixed order.
+    int has_long;
+    const int* long_cols;   // ascending column ids
+    const int* long_first;  // first piece of each long column
+    const int* piece_beg;
+    const int* piece_end;
+    const int* counts;      // [n_long, n_pieces] (device)
+    double* lpart;          // n_pieces partial sums
 };
 
 int verify_grid_blocks(int device);
