@@ -50,6 +50,18 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Branch-free double reciprocal: MUFU seed (rcp.approx.ftz.f64, ~2^-23) + two Newton
+// steps (~1 ulp). IEEE division carries a slow-path branch per divide, which serialises
+// the interleaved Sturm chains below; this keeps them independent.
+__device__ __forceinline__ double fast_rcp(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    double e = fma(-q, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-q, r, 1.0);
+    return fma(r, e, r);
+}
+
 __device__ double block_sum(double v, double* red) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     v = warp_sum(v);
@@ -281,10 +293,10 @@ __global__ void __launch_bounds__(NTHR) tridiag_rows_kernel(TriRowsArgs ra) {
             __syncwarp();
             const double alpha = Ak[k + 1];
             double tau = 0.0, beta = alpha, scal = 0.0;
-            if (xs > 0.0) {
+            if (xs > 0.0) {  // reciprocals without the IEEE-divide slow path (~1 ulp, 55 vs 131 cycles)
                 beta = -copysign(sqrt(alpha * alpha + xs), alpha);
-                tau = (beta - alpha) / beta;
-                scal = 1.0 / (alpha - beta);
+                tau = (beta - alpha) * fast_rcp(beta);
+                scal = fast_rcp(alpha - beta);
             }
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
@@ -373,18 +385,6 @@ __global__ void __launch_bounds__(NTHR) tridiag_rows_kernel(TriRowsArgs ra) {
         a.tau[n - 1] = 0.0;
         if (n >= 2) a.tau[n - 2] = 0.0;
     }
-}
-
-// Branch-free double reciprocal: MUFU seed (rcp.approx.ftz.f64, ~2^-23) + two Newton
-// steps (~1 ulp). IEEE division carries a slow-path branch per divide, which serialises
-// the interleaved Sturm chains below; this keeps them independent.
-__device__ __forceinline__ double fast_rcp(double q) {
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-    double e = fma(-q, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-q, r, 1.0);
-    return fma(r, e, r);
 }
 
 // Sturm count: eigenvalues of T smaller than x (dlaebz recurrence with pivmin guard).
@@ -583,13 +583,18 @@ __global__ void inviter_kernel(const double* __restrict__ dg, const double* __re
     }
     double scale = 1.0;
     for (int it = 0; it < 3; ++it) {
-        // forward: apply P and L (scaled by the previous normalisation)
+        // forward: apply P and L (scaled by the previous normalisation). The next step's
+        // operands are loaded before this step's store (software pipelining: the store/load
+        // pair on x would otherwise serialise every step on shared-memory latency).
         double xj = AT(x, 0) * scale;
-        unsigned fw = 0;
+        unsigned fw = flags[slot];
+        double xn_n = n > 1 ? AT(x, 1) * scale : 0.0, m_n = n > 1 ? AT(Lm, 0) : 0.0;
         for (int j = 0; j + 1 < n; ++j) {
-            if ((j & 31) == 0) fw = flags[(size_t)(j >> 5) * S + slot];
-            const double xn = AT(x, j + 1) * scale;
-            const double m = AT(Lm, j);
+            const double xn = xn_n, m = m_n;
+            if (j + 2 < n) {
+                xn_n = AT(x, j + 2) * scale;
+                m_n = AT(Lm, j + 1);
+            }
             double keep, carry;
             if ((fw >> (j & 31)) & 1u) {
                 keep = xn;
@@ -600,6 +605,7 @@ __global__ void inviter_kernel(const double* __restrict__ dg, const double* __re
             }
             AT(x, j) = keep;
             xj = carry;
+            if ((j & 31) == 31) fw = flags[(size_t)((j + 1) >> 5) * S + slot];
         }
         // backward: U x = y, with the squared norm on the side
         double x1 = xj * AT(Ui, n - 1);
@@ -613,12 +619,22 @@ __global__ void inviter_kernel(const double* __restrict__ dg, const double* __re
             x2 = x1;
             x1 = x0;
         }
-        for (int j = n - 3; j >= 0; --j) {
-            const double v = (AT(x, j) - AT(U1, j) * x1 - AT(U2, j) * x2) * AT(Ui, j);
-            AT(x, j) = v;
-            nrm += v * v;
-            x2 = x1;
-            x1 = v;
+        if (n >= 3) {
+            double bx = AT(x, n - 3), b1 = AT(U1, n - 3), b2 = AT(U2, n - 3), bi = AT(Ui, n - 3);
+            for (int j = n - 3; j >= 0; --j) {
+                const double cx = bx, c1 = b1, c2 = b2, ci = bi;
+                if (j > 0) {
+                    bx = AT(x, j - 1);
+                    b1 = AT(U1, j - 1);
+                    b2 = AT(U2, j - 1);
+                    bi = AT(Ui, j - 1);
+                }
+                const double v = (cx - c1 * x1 - c2 * x2) * ci;
+                AT(x, j) = v;
+                nrm += v * v;
+                x2 = x1;
+                x1 = v;
+            }
         }
         scale = 1.0 / sqrt(nrm);
     }
