@@ -159,6 +159,12 @@ int sfdg_merge_device(const double* d_b1t, const double* d_b2t, size_t ell, size
 int sfdg_sharded_sketch(const sfdg_sketch_config* cfg, const int64_t* row_ptr, const uint32_t* cols,
                         const double* vals, size_t nrows, int shards, const int* devices, int ndev, double* out,
                         sfdg_stats* shard_stats);
+/* cov_err(a, sketch, rng, iterations) (bench.hpp:62-64, bench.cpp:171-183):
+ * |A^T A - B^T B|_2 / |A|_F^2 by `iterations` power steps (la_core.cpp:191-211) from
+ * unit_sphere_vector(d, rng); A is n x d CSR (host), B is ell x d row-major (host). The
+ * whole-stream evaluation metric of SURVEY 8(f); rng advanced in place. */
+int sfdg_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d,
+                 const double* b, size_t ell, size_t iterations, sfdg_rng_state* rng, double* out, int device);
 /* dense_shrink(a, ell) (shrink.cpp:30-61), host in/out. */
 int sfdg_dense_shrink(const double* a, size_t rows, size_t cols, size_t ell, double* out, int device);
 /* sparse_shrink(buffer, ell, power, rng) (shrink.cpp:63-73); rng advanced in place. */

@@ -138,6 +138,7 @@ class Oracle:
         L.or_orthonormalize.argtypes = [_dp, C.c_size_t, C.c_size_t, _dp]
         L.or_dense_shrink.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp]
         L.or_fd_sketch.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.POINTER(C.c_size_t)]
+        L.or_cov_err.argtypes = [C.POINTER(_OrCsr), _dp, C.c_size_t, C.c_void_p, C.c_size_t, C.POINTER(C.c_double)]
         L.or_simultaneous_iteration.argtypes = [C.POINTER(_OrCsr), C.c_size_t, C.POINTER(_OrPower), C.c_void_p, _dp]
         L.or_sparse_shrink.argtypes = [C.POINTER(_OrCsr), C.c_size_t, C.POINTER(_OrPower), C.c_void_p, _dp]
         L.or_verify_spectral.argtypes = [_SYMOP, C.c_void_p, C.c_size_t, C.POINTER(_OrVerifier), C.c_void_p,
@@ -251,6 +252,14 @@ class Oracle:
         out = np.zeros((ell, d))
         self._chk(self.L.or_merge(_ptr(b1, _dp), b1.shape[0], _ptr(b2, _dp), b2.shape[0], d, ell, _ptr(out, _dp)))
         return out
+
+    def cov_err(self, row_ptr, cols, vals, d, sketch, rng: "Rng", iterations=1000):
+        """cov_err (bench.cpp:171-183): |A^T A - B^T B|_2 / |A|_F^2; rng advanced."""
+        keep = self._csr(row_ptr, cols, vals, d)
+        b = _f64(sketch)
+        out = C.c_double()
+        self._chk(self.L.or_cov_err(C.byref(keep[0]), _ptr(b, _dp), b.shape[0], rng.h, iterations, C.byref(out)))
+        return out.value
 
     def fd_sketch(self, rows, ell):
         """FdSketcher whole-stream run (sketch.cpp:47-78): (B ell x d, shrink_count)."""
@@ -397,6 +406,7 @@ class Reference:
         L.ref_boosted_sparse_shrink.argtypes = csr + [C.c_size_t, _dp] + pw + [C.c_void_p, _dp, _dp, _szp]
         L.ref_merge.argtypes = [_dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp]
         L.ref_sketch.argtypes = csr + [C.c_size_t, C.c_double] + pw + [C.c_uint64, _dp, _dp]
+        L.ref_cov_err.argtypes = csr + [_dp, C.c_size_t, C.c_void_p, C.c_size_t, C.POINTER(C.c_double)]
 
     def _chk(self, code):
         if code:
@@ -469,6 +479,13 @@ class Reference:
         self._chk(self.L.ref_fd_sketch(_ptr(a, _dp), C.c_size_t(n), C.c_size_t(d), C.c_size_t(ell), _ptr(out, _dp),
                                        C.byref(cnt)))
         return out, cnt.value
+
+    def cov_err(self, row_ptr, cols, vals, d, sketch, rng, iterations=1000):
+        args, keep = self._csr(row_ptr, cols, vals, d)
+        b = _f64(sketch)
+        out = C.c_double()
+        self._chk(self.L.ref_cov_err(*args, _ptr(b, _dp), b.shape[0], rng.h, iterations, C.byref(out)))
+        return out.value
 
     def sketch(self, row_ptr, cols, vals, d, ell, seed=0, delta=0.1, power: PowerConfig | None = None):
         args, keep = self._csr(row_ptr, cols, vals, d)

@@ -10,6 +10,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "sfd/bench.hpp"
 #include "sfd/common.hpp"
 #include "sfd/la_core.hpp"
 #include "sfd/randsvd.hpp"
@@ -139,6 +140,17 @@ int ref_merge(const double* b1, size_t r1, const double* b2, size_t r2, size_t d
         std::memcpy(m1.data.data(), b1, r1 * d * sizeof(double));
         std::memcpy(m2.data.data(), b2, r2 * d * sizeof(double));
         put(sfd::merge(m1, m2, ell), out);
+    });
+}
+
+// cov_err (bench.cpp:171-183) of a sketch (ell x d) against CSR A, rng advanced in place.
+int ref_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t m, size_t d,
+                const double* sketch, size_t ell, void* rng, size_t iterations, double* out) {
+    return guarded([&] {
+        sfd::SparseBuffer a = to_buffer(row_ptr, cols, vals, m, d);
+        sfd::DenseMatrix b(ell, d);
+        std::memcpy(b.data.data(), sketch, ell * d * sizeof(double));
+        *out = sfd::cov_err(a, b, *static_cast<sfd::Rng*>(rng), iterations);
     });
 }
 

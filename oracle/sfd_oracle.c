@@ -758,6 +758,53 @@ int or_merge(const double* b1, size_t r1, const double* b2, size_t r2, size_t d,
 }
 
 /* ------------------------------------------------------------------------- */
+/* Evaluation metric: cov_err (core/src/bench.cpp:171-183) over                */
+/* spectral_norm_sym (core/src/la_core.cpp:191-211).                           */
+/* ------------------------------------------------------------------------- */
+
+/* la_core.cpp:191-211: Rayleigh quotient after `iterations` normalised power steps */
+static double spectral_norm_sym(or_symop op, void* ctx, size_t d, size_t iterations, or_rng* rng) {
+    if (iterations < 1) THROW_INVALID("spectral_norm_sym: iterations must be >= 1");
+    double* x = unit_sphere_vector(d, rng);
+    double* y = (double*)az(d * sizeof(double));
+    double rayleigh = 0.0;
+    for (size_t it = 0; it < iterations; ++it) {
+        op(x, y, d, ctx);
+        double dot = 0.0, nrm_sq = 0.0;
+        for (size_t i = 0; i < d; ++i) {
+            if (!isfinite(y[i])) THROW_NUMERICAL("spectral_norm_sym: non-finite operator output");
+            dot += x[i] * y[i];
+            nrm_sq += y[i] * y[i];
+        }
+        rayleigh = dot;
+        if (nrm_sq == 0.0) return 0.0; /* operator annihilated the iterate */
+        const double inv = 1.0 / sqrt(nrm_sq);
+        for (size_t i = 0; i < d; ++i) x[i] = y[i] * inv;
+    }
+    return rayleigh;
+}
+
+/* bench.cpp:171-183: |A^T A - B^T B|_2 / |A|_F^2 */
+int or_cov_err(const or_csr* a, const double* sketch, size_t ell, or_rng* rng, size_t iterations, double* out) {
+    ENTER();
+    const double fsq = csr_frob_sq(a);
+    if (fsq == 0.0) {
+        *out = 0.0;
+        LEAVE();
+    }
+    mat b = {ell, a->d, (double*)sketch};
+    diff_ctx c;
+    c.a = a;
+    c.b = &b;
+    c.scale = 1.0;
+    c.tm = (double*)az(a->m * sizeof(double));
+    c.tl = (double*)az(ell * sizeof(double));
+    c.t2 = (double*)az(a->d * sizeof(double));
+    *out = spectral_norm_sym(diff_op, &c, a->d, iterations, rng) / fsq;
+    LEAVE();
+}
+
+/* ------------------------------------------------------------------------- */
 /* FdSketcher (core/src/sketch.cpp:47-78): dense Frequent Directions baseline. */
 /* Whole-stream run over n dense rows (n x d row-major).                       */
 /* ------------------------------------------------------------------------- */

@@ -93,6 +93,10 @@ int or_boosted_sparse_shrink(const or_csr* a, size_t ell, or_verifier* st, const
 int or_merge(const double* b1, size_t r1, const double* b2, size_t r2, size_t d, size_t ell,
              double* out);
 
+/* ---- cov_err (core/include/sfd/bench.hpp:62-64, core/src/bench.cpp:171-183) ----
+ * |A^T A - B^T B|_2 / |A|_F^2 by `iterations` power steps from unit_sphere_vector(d, rng). */
+int or_cov_err(const or_csr* a, const double* sketch, size_t ell, or_rng* rng, size_t iterations, double* out);
+
 /* ---- FdSketcher (core/include/sfd/sketch.hpp:53-67, core/src/sketch.cpp:47-78) ----
  * Whole-stream dense FD: n rows (n x d row-major) -> B (ell x d), shrink count. */
 int or_fd_sketch(const double* rows, size_t n, size_t d, size_t ell, double* out, size_t* shrink_count);

@@ -110,6 +110,8 @@ def lib() -> C.CDLL:
     L.sfdg_merge_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int,
                                     C.c_void_p]
     L.sfdg_dense_shrink.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_int]
+    L.sfdg_cov_err.argtypes = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, C.c_size_t,
+                               C.POINTER(_Rng), C.POINTER(C.c_double), C.c_int]
     L.sfdg_fd_create.argtypes = [C.c_size_t, C.c_size_t, C.c_int, C.POINTER(C.c_void_p)]
     L.sfdg_fd_destroy.argtypes = [C.c_void_p]
     L.sfdg_fd_append.argtypes = [C.c_void_p, _dp, C.c_size_t]
@@ -469,6 +471,23 @@ def sparse_shrink(csr, d: int, ell: int, rng, power: PowerConfig | None = None, 
     st = RngState(st.seed)
     st._update(c)
     return out, st
+
+
+def cov_err(csr, d: int, sketch, rng, iterations: int = 1000, device: int = 0):
+    """cov_err(a, sketch, rng, iterations) (bench.cpp:171-183): |A^T A - B^T B|_2 / |A|_F^2 over
+    the whole CSR stream, on the device. Returns (value, RngState after)."""
+    rp, cs, vs = _csr(*csr)
+    b = _f64(np.atleast_2d(sketch))
+    if b.shape[1] != d:
+        raise InvalidArgument("cov_err: dimension mismatch")
+    st = _rng_arg(rng)
+    c = st._c()
+    out = C.c_double()
+    _check(lib().sfdg_cov_err(_p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), len(rp) - 1, d, _p(b, _dp), b.shape[0],
+                              iterations, C.byref(c), C.byref(out), device))
+    st = RngState(st.seed)
+    st._update(c)
+    return out.value, st
 
 
 def boosted_sparse_shrink(csr, d: int, ell: int, state: VerifierState, rng, power: PowerConfig | None = None,

@@ -1321,6 +1321,24 @@ int sfdg_simultaneous_iteration(const int64_t* row_ptr, const uint32_t* cols, co
     });
 }
 
+int sfdg_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d, const double* b,
+                 size_t ell, size_t iterations, sfdg_rng_state* rng, double* out, int device) {
+    return guard([&] {
+        if (!row_ptr || !b || !rng || !out) throw invalid_argument("cov_err: null argument");
+        if (ell < 1 || ell > (size_t)kMaxEll) throw invalid_argument("cov_err: sketch rows must be in [1, 256]");
+        if (d < 1 || d >= (size_t)INT32_MAX) throw invalid_argument("cov_err: dimension mismatch");
+        validate_csr(row_ptr, cols, vals, n, d);
+        require_device(device);
+        const int64_t nnz = row_ptr[n] - row_ptr[0];
+        Engine e(device, (int)d, (int)ell, rng->seed, (uint64_t)std::max<int64_t>(nnz, 1), 1);
+        rng_in(e, rng);
+        e.load_csr(row_ptr, cols, vals, (int)n, nnz, /*panels=*/false);
+        e.prepare();
+        *out = device_cov_err(e, b, (int)ell, iterations, csr_frob(row_ptr, vals, n));
+        rng_out(e, rng);
+    });
+}
+
 int sfdg_power_iteration_count(size_t m, const sfdg_power_config* power, size_t* q) {
     return guard([&] { *q = power_iteration_count(m, to_power(power)); });
 }

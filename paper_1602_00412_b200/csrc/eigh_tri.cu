@@ -846,6 +846,18 @@ void launch_rows(const TriRowsArgs& ra, size_t smem, cudaStream_t st) {
         CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         attr = true;
     }
+    // Exclusive SMs: asking for all the shared memory an SM has keeps other kernels' blocks
+    // (the lanes' SpMMs) off the SMs this latency-bound chain kernel runs on.
+    static int excl = -1;
+    if (excl < 0) {
+        const char* e = getenv("SFDG_TRIDIAG_EXCLUSIVE");
+        excl = e ? atoi(e) : 1;
+    }
+    if (excl) {
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, (const void*)fn));
+        smem = std::max(smem, (size_t)fa.maxDynamicSharedSizeBytes);
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ra.C);
     cfg.blockDim = dim3(NTHR);

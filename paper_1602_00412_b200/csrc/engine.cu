@@ -267,8 +267,9 @@ void Engine::check_errors() {
     raise_device_flags(e);
 }
 
-void Engine::load_csr(const int64_t* row_ptr, const uint32_t* cols, const double* vals, int m, int64_t nnz) {
-    ensure_rows(m);
+void Engine::load_csr(const int64_t* row_ptr, const uint32_t* cols, const double* vals, int m, int64_t nnz,
+                      bool panels) {
+    if (panels) ensure_rows(m);
     a.set_shape(m, d, nnz);
     std::vector<int> rp(m + 1);
     for (int i = 0; i <= m; ++i) rp[i] = (int)(row_ptr[i] - row_ptr[0]);

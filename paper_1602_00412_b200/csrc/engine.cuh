@@ -93,8 +93,10 @@ class Engine {
 
     void set_device() const;
     void ensure_rows(int m);
-    // Host CSR -> device A' (standalone entry points).
-    void load_csr(const int64_t* row_ptr, const uint32_t* cols, const double* vals, int m, int64_t nnz);
+    // Host CSR -> device A' (standalone entry points); panels = false skips the m-row Y panels
+    // (metrics over a whole stream only need the CSR/CSC).
+    void load_csr(const int64_t* row_ptr, const uint32_t* cols, const double* vals, int m, int64_t nnz,
+                  bool panels = true);
     // CSC + long-row plans for the current A'. prepare_async queues the build and the
     // read-back of the long-row counts; prepare_finish consumes them once the stream got there.
     void prepare();
@@ -140,5 +142,9 @@ class Engine {
     void check_errors();  // syncs; throws the reference's error class for any device flag
     void sync();
 };
+
+// cov_err (bench.cpp:171-183) of B (ell x d, host row-major) against the A held by e
+// (load_csr + prepare done); draws unit_sphere_vector(d) at e.pos (metrics.cu).
+double device_cov_err(Engine& e, const double* b_host, int ell, size_t iterations, double a_fsq);
 
 }  // namespace sfdg

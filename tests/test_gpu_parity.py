@@ -579,3 +579,22 @@ def test_fd_sketcher_sparse_rows_and_errors(oracle):
     f.append([1.0, float("nan"), 0.0])
     with pytest.raises(P.InvalidArgument, match="non-finite"):
         f.append_rows(np.ones((3, 3)))
+
+
+# ---------------------------------------------------------------- cov_err metric (8(f) rank 2)
+def test_cov_err_device_vs_oracle(oracle):
+    """Device cov_err (whole-stream power iteration, graph-replayed steps) against the oracle
+    from the same start draw: the same iterates up to roundoff; and the alpha-bound holds."""
+    rp, cs, vs = S.generate("c1", (0, 3000))
+    b, _ = sketch_gpu(rp, cs, vs, 1000, 50, 0)
+    got, st = P.cov_err((rp, cs, vs), 1000, b, P.RngState(77), iterations=300)
+    g = oracle.rng(77)
+    want = oracle.cov_err(rp, cs, vs, 1000, b, g, 300)
+    assert abs(got - want) <= 1e-9 * abs(want)
+    assert st.words == g.state()[0]
+    assert got <= 1.0 / (KALPHA * 50)  # |A^T A - B^T B|_2 <= |A|_F^2 / (alpha ell)  (k = 0)
+    # a zero sketch measures |A^T A|_2 / |A|_F^2, the top squared singular value share
+    z, _ = P.cov_err((rp, cs, vs), 1000, np.zeros((3, 1000)), P.RngState(5), iterations=400)
+    a = dense_of(rp, cs, vs, 1000)
+    top = np.linalg.norm(a, 2) ** 2 / (a ** 2).sum()
+    assert abs(z - top) <= 1e-6 * top

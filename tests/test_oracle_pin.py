@@ -180,3 +180,19 @@ def test_fd_sketcher_oracle_matches_reference(oracle, reference):
         br, cr = reference.fd_sketch(a, ell)
         assert co == cr
         assert np.array_equal(bo, br)
+
+
+def test_cov_err_oracle_matches_reference(oracle, reference):
+    """cov_err restatement (bench.cpp:171-183 over la_core.cpp:191-211) bit-exact against
+    the compiled reference, same draws (rng advanced identically)."""
+    from paper_1602_00412_b200 import synthetic as S
+    rp, cs, vs = S.generate("c1", (0, 1200))
+    b, _ = oracle.sketch(rp, cs, vs, 1000, 50, seed=0)
+    g1, g2 = oracle.rng(77), reference.rng(77)
+    assert oracle.cov_err(rp, cs, vs, 1000, b, g1, 150) == reference.cov_err(rp, cs, vs, 1000, b, g2, 150)
+    # a zero sketch measures |A^T A|_2 / |A|_F^2 (power iteration converged by 400 steps)
+    a = np.zeros((len(rp) - 1, 1000))
+    for i in range(len(rp) - 1):
+        a[i, cs[rp[i]:rp[i + 1]]] = vs[rp[i]:rp[i + 1]]
+    top = np.linalg.norm(a, 2) ** 2 / (a ** 2).sum()
+    assert abs(oracle.cov_err(rp, cs, vs, 1000, np.zeros((5, 1000)), oracle.rng(1), 400) - top) <= 1e-6 * top
