@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--rows", type=int, default=0, help="limit rows per stream (debug only)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-accuracy", action="store_true", help="skip the whole-stream cov_err check")
     return p.parse_args()
 
 
@@ -298,6 +299,19 @@ def main():
     step_device()
     prof = P.profile_end()
     pstats = sk.stats()
+    accuracy = None
+    if rank == 0 and world == 1 and not a.no_accuracy:
+        # the paper's guarantee checked on the whole stream, on the device (SURVEY 8(d) accuracy
+        # gate; cov_err = bench.cpp:171-183 with its default 1000 power steps, untimed)
+        b = sk.sketch()
+        t0 = time.time()
+        ce, _ = P.cov_err((rp, cs, vs), d, b, P.RngState(4242), iterations=1000, device=device)
+        alpha = 6.0 / 41.0
+        accuracy = {"cov_err": ce, "definition": "|A^T A - B^T B|_2 / |A|_F^2 over the whole stream (1000 "
+                                                 "power steps on the device, bench.cpp:171-183)",
+                    "alpha_bound_k0": 1.0 / (alpha * ell), "within_alpha_bound": bool(ce <= 1.0 / (alpha * ell)),
+                    "fd_bound_k0": 1.0 / ell, "within_fd_bound": bool(ce <= 1.0 / ell),
+                    "seconds": round(time.time() - t0, 3)}
 
     value = world * nnz * a.steps / t_dev
     ms_step = 1e3 * t_dev / a.steps
@@ -315,6 +329,8 @@ def main():
                        "h2d_bytes_per_step": int(nnz * 12 + (n + stats["flushes"]) * 4),
                        "d2h_bytes_per_step": int(ell * d * 8)}
     line.update(roofline_from_profile(prof, pstats, n, d, ell, nnz))
+    if accuracy is not None:
+        line["accuracy"] = accuracy
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
             t, nz, rows = reference_sample(a.config, 1, d)
