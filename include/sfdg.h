@@ -159,6 +159,19 @@ int sfdg_merge_device(const double* d_b1t, const double* d_b2t, size_t ell, size
 int sfdg_sharded_sketch(const sfdg_sketch_config* cfg, const int64_t* row_ptr, const uint32_t* cols,
                         const double* vals, size_t nrows, int shards, const int* devices, int ndev, double* out,
                         sfdg_stats* shard_stats);
+/* ---- ingestion (io.hpp:13-33, io.cpp:21-189) ----------------
+ * Sketch a row-stream file: MatrixMarket "matrix coordinate real general" (1-based,
+ * entries grouped by nondecreasing row) or, with plain_cols > 0, the plain "col:value"
+ * format -- the reference's open_row_stream + run_sketch (tools/sfd_main.cpp:65-69).
+ * cfg->d = 0 takes the file's column count (else it must match). The file is memory-mapped
+ * and parsed by all host threads window by window while the device sketches the previous
+ * window. out: ell x d (row-major); stats and *d_out optional. */
+int sfdg_sketch_file(const char* path, size_t plain_cols, const sfdg_sketch_config* cfg, int device, double* out,
+                     sfdg_stats* stats, size_t* d_out);
+/* The parsed rows themselves (CSR, absolute row_ptr): call with NULL arrays to get the
+ * sizes, then with arrays of nrows + 1, nnz, nnz entries. */
+int sfdg_read_row_stream(const char* path, size_t plain_cols, size_t* nrows, size_t* d, size_t* nnz,
+                         int64_t* row_ptr, uint32_t* cols, double* vals);
 /* cov_err(a, sketch, rng, iterations) (bench.hpp:62-64, bench.cpp:171-183):
  * |A^T A - B^T B|_2 / |A|_F^2 by `iterations` power steps (la_core.cpp:191-211) from
  * unit_sphere_vector(d, rng); A is n x d CSR (host), B is ell x d row-major (host). The

@@ -480,6 +480,23 @@ class Reference:
                                        C.byref(cnt)))
         return out, cnt.value
 
+    def read_row_stream(self, path, plain_cols=0):
+        """open_row_stream (io.cpp:170-189) read to the end by the compiled reference reader
+        (oracle/_ref/refio): (row_ptr, cols, vals, d, error message or None)."""
+        import subprocess
+        exe = os.path.join(os.path.dirname(LIB_REF), "refio")
+        raw = subprocess.run([exe, path, str(plain_cols)], capture_output=True, check=True).stdout
+        n, d, z, err, ml = np.frombuffer(raw[:40], np.int64)
+        off = 40
+        msg = raw[off:off + ml].decode()
+        off += ml
+        rp = np.frombuffer(raw[off:off + 8 * (n + 1)], np.int64).copy()
+        off += 8 * (n + 1)
+        cs = np.frombuffer(raw[off:off + 4 * z], np.uint32).copy()
+        off += 4 * z
+        vs = np.frombuffer(raw[off:off + 8 * z], np.float64).copy()
+        return rp, cs, vs, int(d), (msg if err else None)
+
     def cov_err(self, row_ptr, cols, vals, d, sketch, rng, iterations=1000):
         args, keep = self._csr(row_ptr, cols, vals, d)
         b = _f64(sketch)

@@ -110,6 +110,9 @@ def lib() -> C.CDLL:
     L.sfdg_merge_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int,
                                     C.c_void_p]
     L.sfdg_dense_shrink.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_int]
+    L.sfdg_sketch_file.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(_SketchCfg), C.c_int, _dp, C.POINTER(_Stats),
+                                   _szp]
+    L.sfdg_read_row_stream.argtypes = [C.c_char_p, C.c_size_t, _szp, _szp, _szp, _i64p, _u32p, _dp]
     L.sfdg_cov_err.argtypes = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, C.c_size_t,
                                C.POINTER(_Rng), C.POINTER(C.c_double), C.c_int]
     L.sfdg_fd_create.argtypes = [C.c_size_t, C.c_size_t, C.c_int, C.POINTER(C.c_void_p)]
@@ -471,6 +474,46 @@ def sparse_shrink(csr, d: int, ell: int, rng, power: PowerConfig | None = None, 
     st = RngState(st.seed)
     st._update(c)
     return out, st
+
+
+def read_row_stream(path: str, plain_cols: int = 0):
+    """open_row_stream (io.cpp:170-189) through the parallel reader: (row_ptr, cols, vals, d).
+    Host-only (no GPU needed)."""
+    n, d, z = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    _check(lib().sfdg_read_row_stream(path.encode(), plain_cols, C.byref(n), C.byref(d), C.byref(z), None, None,
+                                      None))
+    rp = np.zeros(n.value + 1, np.int64)
+    cs = np.zeros(max(1, z.value), np.uint32)
+    vs = np.zeros(max(1, z.value))
+    _check(lib().sfdg_read_row_stream(path.encode(), plain_cols, C.byref(n), C.byref(d), C.byref(z), _p(rp, _i64p),
+                                      _p(cs, _u32p), _p(vs, _dp)))
+    return rp, cs[: z.value], vs[: z.value], d.value
+
+
+def sketch_file(path: str, cfg: "SketchConfig", plain_cols: int = 0, device: int = 0):
+    """sfdg_sketch_file: the reference's run_sketch over a file (tools/sfd_main.cpp:65-69).
+    cfg.d = 0 takes the file's width. Returns (B, stats dict)."""
+    d = C.c_size_t()
+    # the sketch width is the file's; read the header first when cfg.d is 0
+    width = cfg.d or read_row_stream_width(path, plain_cols)
+    out = np.zeros((cfg.ell, width))
+    st = _Stats()
+    c = cfg._c()
+    _check(lib().sfdg_sketch_file(path.encode(), plain_cols, C.byref(c), device, _p(out, _dp), C.byref(st),
+                                  C.byref(d)))
+    return out, {"flushes": st.flush_count, "attempts": st.attempt_total, "verifier_i": st.verifier.i,
+                 "delta_spent": st.verifier.delta_spent}
+
+
+def read_row_stream_width(path: str, plain_cols: int = 0) -> int:
+    if plain_cols:
+        return plain_cols
+    with open(path) as f:
+        for line in f:
+            if line.startswith("%") or not line.strip():
+                continue
+            return int(line.split()[1])
+    raise InvalidArgument(path + ": missing MatrixMarket size line")
 
 
 def cov_err(csr, d: int, sketch, rng, iterations: int = 1000, device: int = 0):

@@ -23,6 +23,7 @@
 
 #include "../../include/sfdg.h"
 #include "engine.cuh"
+#include "io.cuh"
 
 namespace sfdg {
 
@@ -1163,6 +1164,68 @@ int sfdg_fd_shrink_count(sfdg_fd_sketcher* h, size_t* count) {
     return guard([&] {
         if (!h || !h->impl || !count) throw invalid_argument("null FD sketcher");
         *count = h->impl->shrink_count();
+    });
+}
+
+int sfdg_sketch_file(const char* path, size_t plain_cols, const sfdg_sketch_config* cfg, int device, double* out,
+                     sfdg_stats* stats, size_t* d_out) {
+    return guard([&] {
+        if (!path || !cfg) throw invalid_argument("sfdg_sketch_file: null argument");
+        require_device(device);
+        CK(cudaSetDevice(device));
+        SketchCfg c;
+        c.ell = cfg->ell;
+        c.d = cfg->d;
+        c.delta = cfg->delta;
+        c.power = to_power(&cfg->power);
+        c.seed = cfg->seed;
+        std::unique_ptr<Sketcher> sk;
+        size_t d = 0;
+        auto make = [&] {
+            if (sk) return;
+            if (c.d == 0) c.d = d;  // tools/sfd_main.cpp:65-69: cfg.d = stream->cols()
+            if (c.d != d) throw invalid_argument("sfdg_sketch_file: config d does not match the file's columns");
+            validate_cfg(c);
+            sk = std::make_unique<Sketcher>(c, device);
+        };
+        try {
+            read_row_stream(path, plain_cols, 0, &d, [&](const int64_t* rp, const uint32_t* cs, const double* vs,
+                                                         size_t nrows) {
+                make();
+                sk->append_host(rp, cs, vs, nrows, nullptr);
+            });
+        } catch (...) {
+            if (d_out) *d_out = d;
+            throw;
+        }
+        make();
+        sk->finalize(out);
+        if (stats) sk->stats(stats);
+        if (d_out) *d_out = d;
+    });
+}
+
+int sfdg_read_row_stream(const char* path, size_t plain_cols, size_t* nrows, size_t* d, size_t* nnz,
+                         int64_t* row_ptr, uint32_t* cols, double* vals) {
+    return guard([&] {
+        if (!path || !nrows || !d || !nnz) throw invalid_argument("sfdg_read_row_stream: null argument");
+        std::vector<int64_t> rp{0};
+        std::vector<uint32_t> cs;
+        std::vector<double> vs;
+        size_t dd = 0;
+        read_row_stream(path, plain_cols, 0, &dd, [&](const int64_t* r, const uint32_t* c, const double* v,
+                                                      size_t n) {
+            const int64_t base = rp.back();
+            for (size_t i = 1; i <= n; ++i) rp.push_back(base + (r[i] - r[0]));
+            cs.insert(cs.end(), c + r[0], c + r[n]);
+            vs.insert(vs.end(), v + r[0], v + r[n]);
+        });
+        *nrows = rp.size() - 1;
+        *d = dd;
+        *nnz = cs.size();
+        if (row_ptr) std::memcpy(row_ptr, rp.data(), rp.size() * sizeof(int64_t));
+        if (cols) std::memcpy(cols, cs.data(), cs.size() * sizeof(uint32_t));
+        if (vals) std::memcpy(vals, vs.data(), vs.size() * sizeof(double));
     });
 }
 

@@ -598,3 +598,29 @@ def test_cov_err_device_vs_oracle(oracle):
     a = dense_of(rp, cs, vs, 1000)
     top = np.linalg.norm(a, 2) ** 2 / (a ** 2).sum()
     assert abs(z - top) <= 1e-6 * top
+
+
+# ---------------------------------------------------------------- file ingestion (8(f) rank 3)
+def test_sketch_file_matches_oracle(oracle, tmp_path):
+    """sfdg_sketch_file (parallel mmap reader -> device sketcher) on MatrixMarket and plain
+    files of the c1 prefix: same rows as the in-memory path, so the same sketch and counters
+    as the oracle (tools/sfd_main.cpp:65-69 run_sketch contract, cfg.d from the file)."""
+    rp, cs, vs = S.generate("c1", (0, 2500))
+    n = len(rp) - 1
+    mm = str(tmp_path / "c1.mtx")
+    with open(mm, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real general\n% c1 prefix\n")
+        f.write(f"{n} 1000 {int(rp[-1])}\n")
+        for i in range(n):
+            for k in range(rp[i + 1] - 1, rp[i] - 1, -1):  # reversed within rows: the reader sorts
+                f.write(f"{i + 1} {int(cs[k]) + 1} {float(vs[k])!r}\n")
+    plain = str(tmp_path / "c1.txt")
+    with open(plain, "w") as f:
+        for i in range(n):
+            f.write(" ".join(f"{int(cs[k])}:{float(vs[k])!r}" for k in range(rp[i], rp[i + 1])) + "\n")
+    bo, so = oracle.sketch(rp, cs, vs, 1000, 50, seed=3)
+    for path, pc in ((mm, 0), (plain, 1000)):
+        b, st = P.sketch_file(path, P.SketchConfig(ell=50, d=0, seed=3), plain_cols=pc)
+        assert b.shape == (50, 1000)
+        assert btb_rel(b, bo) <= BTB_TOL
+        assert (st["flushes"], st["attempts"], st["verifier_i"]) == (so["flushes"], so["attempts"], so["verifier_i"])
