@@ -624,3 +624,50 @@ def test_sketch_file_matches_oracle(oracle, tmp_path):
         assert b.shape == (50, 1000)
         assert btb_rel(b, bo) <= BTB_TOL
         assert (st["flushes"], st["attempts"], st["verifier_i"]) == (so["flushes"], so["attempts"], so["verifier_i"])
+
+
+# ---------------------------------------------------------------- CLI (8(f) rank 4)
+def test_cli_sketch_csv_manifest_and_determinism(oracle, tmp_path):
+    """`sfdg sketch` (tools/sfdg_main.cpp, the reference CLI's sketch command): CSV with 17
+    significant digits round-trips the sketch, the manifest records the run, equal seeds give
+    byte-identical CSVs (acceptance criterion 9 for this implementation), bad input exits 1."""
+    import json
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "..", "tools", "sfdg")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", os.path.join(os.path.dirname(__file__), "..", "tools"), "sfdg"], check=True)
+    rp, cs, vs = S.generate("c1", (0, 1500))
+    n = len(rp) - 1
+    mm = str(tmp_path / "a.mtx")
+    with open(mm, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real general\n")
+        f.write(f"{n} 1000 {int(rp[-1])}\n")
+        for i in range(n):
+            for k in range(rp[i], rp[i + 1]):
+                f.write(f"{i + 1} {int(cs[k]) + 1} {float(vs[k])!r}\n")
+    outs = []
+    for run in range(2):
+        out = str(tmp_path / f"b{run}.csv")
+        r = subprocess.run([exe, "sketch", "--input", mm, "--output", out, "--ell", "50", "--seed", "4"],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        outs.append(open(out, "rb").read())
+    assert outs[0] == outs[1]
+    b = np.loadtxt(str(tmp_path / "b0.csv"), delimiter=",")
+    bo, _ = oracle.sketch(rp, cs, vs, 1000, 50, seed=4)
+    assert btb_rel(b, bo) <= BTB_TOL
+    man = json.load(open(str(tmp_path / "b0.csv") + ".manifest.json"))
+    assert man["command"] == "sketch" and man["ell"] == 50 and man["d"] == 1000 and man["seed"] == 4
+    fd_out = str(tmp_path / "fd.csv")
+    r = subprocess.run([exe, "sketch", "--input", mm, "--output", fd_out, "--ell", "50", "--algo", "fd"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    bf = np.loadtxt(fd_out, delimiter=",")
+    bfo, _ = oracle.fd_sketch(dense_of(rp, cs, vs, 1000), 50)
+    assert btb_rel(bf, bfo) <= BTB_TOL
+    bad = str(tmp_path / "bad.mtx")
+    with open(bad, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate real general\n2 3 1\n1 9 1.0\n")
+    r = subprocess.run([exe, "sketch", "--input", bad, "--output", str(tmp_path / "x.csv")], capture_output=True,
+                       text=True)
+    assert r.returncode == 1 and "out of range" in r.stderr
