@@ -10,8 +10,10 @@
 //     packed upper triangle in shared memory; n-2 steps of symv + rank-2 update.
 //  2. bisect_kernel (warp per eigenvalue): Sturm-count multisection on T, 32 shifts per
 //     step (5 bits per iteration) to full double precision.
-//  3. inviter_kernel (thread per eigenvalue): inverse iteration with a partially pivoted
-//     tridiagonal LU, distinct deterministic start vectors.
+//  3. twisted_kernel (lane pair per eigenvalue): eigenvector from the forward/backward
+//     twisted factorisations in one pass; inviter_kernel (thread per eigenvalue: inverse
+//     iteration with a partially pivoted tridiagonal LU, distinct deterministic start
+//     vectors) redoes the eigenvalues in clusters, which need independent start vectors.
 //  4. cluster_kernel (warp per cluster of eigenvalues closer than 1e-6 |T|): modified
 //     Gram-Schmidt twice, then Rayleigh-Ritz with a small Jacobi inside the cluster so each
 //     vector is the right eigenvector, not just a basis of the cluster's space.
@@ -490,7 +492,8 @@ __global__ void bisect_kernel(const double* __restrict__ dg, const double* __res
 // multiply by stored pivot reciprocals, so the only divides are the n of the factorisation.
 __global__ void inviter_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int nval,
                                const double* __restrict__ lam, const int* __restrict__ trivial,
-                               double* __restrict__ X, int ldx, double* __restrict__ work_g) {
+                               double* __restrict__ X, int ldx, double* __restrict__ work_g,
+                               const int* __restrict__ need) {
     extern __shared__ double sh_inv[];
     __shared__ double s_tn;
     double* d = sh_inv;
@@ -509,6 +512,7 @@ __global__ void inviter_kernel(const double* __restrict__ dg, const double* __re
     __syncthreads();
     const int t = blockIdx.x * nb + threadIdx.x;
     if (t >= nval) return;
+    if (need && !need[t]) return;  // already done by the twisted factorisation
     if (*trivial) {  // identity eigenvectors in the stable descending order of the diagonal
         int idx = 0;
         for (int i = 0; i < n; ++i) {
@@ -640,6 +644,133 @@ __global__ void inviter_kernel(const double* __restrict__ dg, const double* __re
     }
     for (int j = 0; j < n; ++j) X[(size_t)j * ldx + t] = AT(x, j) * scale;
 #undef AT
+}
+
+// Eigenvectors by twisted factorisations (Dhillon's "getvec"): for each eigenvalue l the
+// stationary forward factorisation T - l I = L+ D+ L+^T and the backward one U- D- U-^T
+// run at once on a lane pair (same recurrence q' = (a - l) - b^2 / q, indexed up vs down);
+// the twist r = argmin |gamma_k| (gamma_k = D+_k + D-_k - (a_k - l)) then gives the vector
+// z_r = 1, z_i = -L_i z_{i+1} above and z_i = -U_{i-1} z_{i-1} below. One pass, no
+// iteration: with l accurate to bisection precision the residual is |gamma_r| / |z| ~ u |T|.
+// kEPW eigenvalues per warp (lane 2p forward, 2p+1 backward); the factors live in shared
+// memory, four n-vectors per eigenvalue.
+constexpr int kEPW = 16;
+__global__ void twisted_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int nval,
+                               const double* __restrict__ lam, const int* __restrict__ trivial,
+                               double* __restrict__ X, int ldx, int* __restrict__ need) {
+    extern __shared__ double tw_s[];
+    double* a = tw_s;          // n diagonal
+    double* b2 = tw_s + n;     // n-1 squared off-diagonals
+    double* bo = tw_s + 2 * n; // n-1 off-diagonals
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        a[j] = dg[j];
+        const double e = j + 1 < n ? eg[j] : 0.0;
+        bo[j] = e;
+        b2[j] = e * e;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int pr = lane >> 1, dir = lane & 1;
+    const int t = (blockIdx.x * nw + w) * kEPW + pr;
+    const bool act = pr < kEPW && t < nval;
+    if (*trivial) {  // identity vectors in the stable descending order of the diagonal
+        if (act && dir == 0) {
+            int idx = 0;
+            for (int i = 0; i < n; ++i) {
+                int r = 0;
+                for (int j = 0; j < n; ++j) r += (a[j] > a[i] || (a[j] == a[i] && j < i));
+                if (r == t) idx = i;
+            }
+            for (int i = 0; i < n; ++i) X[(size_t)i * ldx + t] = (i == idx) ? 1.0 : 0.0;
+        }
+        return;
+    }
+    // per-eigenvalue factor storage: D (n) and 1/D (n) for this lane's direction
+    double* base = tw_s + 3 * n + (size_t)(w * kEPW + (pr < kEPW ? pr : 0)) * 4 * n;
+    double* D = base + (size_t)dir * 2 * n;  // D+ (dir 0) or D- (dir 1)
+    double* R = D + n;                       // 1/D+ or 1/D-
+    double tn = 0.0, emax = 0.0;
+    for (int j = 0; j < n; ++j) {
+        tn = fmax(tn, fabs(a[j]) + (j > 0 ? fabs(bo[j - 1]) : 0.0) + fabs(bo[j]));
+        emax = fmax(emax, b2[j]);
+    }
+    const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax) * 1e3;
+    const double l = act ? lam[t] : 0.0;
+    // both factorisations: step s computes index j from j -/+ 1
+    {
+        int j = dir ? n - 1 : 0;
+        double q = a[j] - l;
+        if (fabs(q) < pivmin) q = -pivmin;
+        D[j] = q;
+        for (int s = 0; s + 1 < n; ++s) {
+            const int jn = dir ? n - 2 - s : s + 1;
+            const int o = dir ? n - 2 - s : s;  // off-diagonal between j and jn
+            const double r = fast_rcp(q);
+            R[j] = r;
+            q = fma(-b2[o], r, a[jn] - l);
+            if (fabs(q) < pivmin) q = -pivmin;
+            D[jn] = q;
+            j = jn;
+        }
+        R[j] = fast_rcp(q);
+    }
+    __syncwarp();
+    // twist: argmin |gamma_k| over the pair (lane 2p: k < n/2, lane 2p+1: k >= n/2)
+    const double* Dp = base;
+    const double* Dm = base + 2 * n;
+    int kbest = -1;
+    double gbest = 1e300;
+    const int k0 = dir ? n / 2 : 0, k1 = dir ? n : n / 2;
+    for (int k = k0; k < k1; ++k) {
+        const double g = fabs(Dp[k] + Dm[k] - (a[k] - l));
+        if (g < gbest) {
+            gbest = g;
+            kbest = k;
+        }
+    }
+    {
+        const double go = __shfl_xor_sync(0xffffffffu, gbest, 1);
+        const int ko = __shfl_xor_sync(0xffffffffu, kbest, 1);
+        if (go < gbest || (go == gbest && ko >= 0 && (kbest < 0 || ko < kbest))) {
+            gbest = go;
+            kbest = ko;
+        }
+    }
+    const int r = kbest < 0 ? 0 : kbest;
+    __syncwarp();
+    // z into the D+ slot (no longer needed): up from r on lane 2p, down from r on lane 2p+1
+    double* z = base;
+    const double* Rp = base + n;
+    const double* Rm = base + 3 * n;
+    double nrm = 0.0;
+    {
+        double zc = 1.0;
+        const int len = dir ? n - 1 - r : r;
+        for (int s = 0; s < n; ++s) {
+            if (s < len) {
+                const int i = dir ? r + 1 + s : r - 1 - s;
+                // z_i = -L_i z_{i+1} = -b_i/D+_i z_{i+1}  |  z_i = -U_{i-1} z_{i-1} = -b_{i-1}/D-_i z_{i-1}
+                zc = dir ? -bo[i - 1] * Rm[i] * zc : -bo[i] * Rp[i] * zc;
+                nrm = fma(zc, zc, nrm);
+                z[i] = zc;  // lane 2p writes i < r, lane 2p+1 writes i > r: disjoint
+            }
+        }
+    }
+    nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+    nrm += 1.0;  // z_r
+    if (dir == 0) z[r] = 1.0;
+    __syncwarp();
+    const double inv = 1.0 / sqrt(nrm);
+    if (act)
+        for (int i = dir; i < n; i += 2) X[(size_t)i * ldx + t] = z[i] * inv;
+    // eigenvalues in a cluster (gap <= the cluster kernel's 1e-6 |T|) need distinct start
+    // vectors for the Rayleigh-Ritz step, and an overflowed twist needs a redo: both go to
+    // inverse iteration (inviter_kernel with this mask)
+    if (act && dir == 0) {
+        const double ctol = 1e-6 * tn;
+        const bool clus = (t > 0 && lam[t - 1] - l <= ctol) || (t + 1 < nval && l - lam[t + 1] <= ctol);
+        need[t] = (clus || !isfinite(inv) || !(nrm < 1e300)) ? 1 : 0;
+    }
 }
 
 // Warp per cluster start: orthonormalise the cluster's vectors (MGS twice) and resolve the
@@ -931,6 +1062,7 @@ void eigh_tri(const double* K, int n, int ldk, double off_tol, const double* d_f
     if (!attr) {
         allow_max_dynamic_smem(tridiag_kernel<true>);
         allow_max_dynamic_smem(inviter_kernel);
+        allow_max_dynamic_smem(twisted_kernel);
         attr = true;
     }
     {
@@ -948,16 +1080,25 @@ void eigh_tri(const double* K, int n, int ldk, double off_tol, const double* d_f
     }
     {
         ProfScope prof("eigh_vectors", st);
+        // twisted factorisations (one warp per kEPW eigenvalues, 4n doubles each) when they fit
+        static const bool twisted = !(getenv("SFDG_EIGVEC") && getenv("SFDG_EIGVEC")[0] == 'i');
+        const size_t tsmem = (3 * (size_t)n + (size_t)kEPW * 4 * n) * sizeof(double);
         // per thread: 5n doubles of LU bands + ceil(n/32) flag words; T staged (2n doubles)
         const int ith = 8;
         const size_t per = 5 * (size_t)n * sizeof(double) + (size_t)((n + 31) / 32) * sizeof(unsigned);
         const size_t ismem = 2 * (size_t)n * sizeof(double) + ith * per;
+        int* need = nullptr;
+        if (twisted && tsmem <= 200 * 1024) {
+            need = scr.take<int>(nval);
+            LAUNCH(twisted_kernel, ceil_div(nval, kEPW), 32, tsmem, st, a.d, a.e, n, nval, values, a.trivial,
+                   vectors, ldv, need);
+        }
         if (ismem <= 96 * 1024)
             LAUNCH(inviter_kernel, ceil_div(nval, ith), ith, ismem, st, a.d, a.e, n, nval, values, a.trivial, vectors,
-                   ldv, (double*)nullptr);
+                   ldv, (double*)nullptr, (const int*)need);
         else
             LAUNCH(inviter_kernel, ceil_div(nval, 64), 64, 2 * (size_t)n * sizeof(double), st, a.d, a.e, n, nval,
-                   values, a.trivial, vectors, ldv, work);
+                   values, a.trivial, vectors, ldv, work, (const int*)need);
         LAUNCH(cluster_kernel, nval, 32, 0, st, a.d, a.e, n, nval, values, a.trivial, vectors, ldv, fallback);
         backtransform(a.vh, a.tau, n, nval, a.trivial, vectors, ldv, st);
     }
