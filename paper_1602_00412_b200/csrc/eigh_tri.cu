@@ -405,7 +405,10 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
 // Warp per eigenvalue: the top `nval` eigenvalues, written in descending order. Each lane
 // runs kShifts interleaved Sturm chains (independent divides overlap), so one step splits
 // the bracket into 32 * kShifts + 1 pieces (~7 bits per step instead of 5).
-constexpr int kShifts = 4;
+#ifndef SFDG_BISECT_SHIFTS
+#define SFDG_BISECT_SHIFTS 2  // measured: 1 -> 49/91 us, 2 -> 48/88, 3 -> 52/96, 4 -> 106/206 (n = 100 / 200)
+#endif
+constexpr int kShifts = SFDG_BISECT_SHIFTS;
 __global__ void bisect_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int nval,
                               const int* __restrict__ trivial, double* __restrict__ lam_desc) {
     extern __shared__ double sh[];
