@@ -916,10 +916,10 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double* __rest
     for (int hi = n - 3; hi >= 0; hi -= R) {  // chunk of reflectors k = lo .. hi
         const int lo = max(0, hi - R + 1);
         __syncthreads();
-        for (int r = 0; r <= hi - lo; ++r) {
-            const double* src = vh + (size_t)(lo + r) * n;
-            for (int j = lo + r + 1 + threadIdx.x; j < n; j += blockDim.x) vs[(size_t)r * n + j] = src[j];
-        }
+        // one flat, independent load per element (the chunk arrives in a few L2 round trips)
+        const int cnt = (hi - lo + 1) * n;
+        const double* src = vh + (size_t)lo * n;
+        for (int e = threadIdx.x; e < cnt; e += blockDim.x) vs[e] = src[e];
         for (int r = threadIdx.x; r <= hi - lo; r += blockDim.x) ts[r] = tau[lo + r];
         __syncthreads();
         if (!active) continue;
@@ -927,13 +927,16 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double* __rest
             const double tk = ts[k - lo];
             if (tk == 0.0) continue;
             const double* v = vs + (size_t)(k - lo) * n;
-            double s = 0.0;
+            double s0 = 0.0, s1 = 0.0;  // two chains: the dot's FMA latency halves
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
                 const int j = 32 * t + lane;
-                if (j > k && j < n) s += v[j] * x[t];
+                if (j > k && j < n) {
+                    if (t & 1) s1 = fma(v[j], x[t], s1);
+                    else s0 = fma(v[j], x[t], s0);
+                }
             }
-            s = warp_sum(s) * tk;
+            const double s = warp_sum(s0 + s1) * tk;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
                 const int j = 32 * t + lane;
