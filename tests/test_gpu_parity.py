@@ -671,3 +671,18 @@ def test_cli_sketch_csv_manifest_and_determinism(oracle, tmp_path):
     r = subprocess.run([exe, "sketch", "--input", bad, "--output", str(tmp_path / "x.csv")], capture_output=True,
                        text=True)
     assert r.returncode == 1 and "out of range" in r.stderr
+
+
+# ---------------------------------------------------------------- wide sketches (c3 / c5 ell)
+@pytest.mark.parametrize("family,d,ell,rows", [("c3", 900, 200, 1800), ("c5", 600, 256, 1200)])
+def test_wide_ell_streams_vs_oracle(oracle, family, d, ell, rows):
+    """The ell of c3 (200) and c5 (256, the build's maximum): 2 ell = 400 / 512 stacked rows
+    take the 8 / 16-CTA cluster tridiagonalisation in the dense-shrink chain, lp = 200 / 256
+    panels the 4-chunk SpMM and the Q = 7 / 8 verifier."""
+    cfg = S.StreamConfig(family, rows, d, ell, 5)
+    rp, cs, vs = S.generate(cfg, (0, rows))
+    b, st = sketch_gpu(rp, cs, vs, d, ell, 21)
+    bo, so = oracle.sketch(rp, cs, vs, d, ell, seed=21)
+    assert btb_rel(b, bo) <= BTB_TOL
+    for key in ("flushes", "attempts", "verifier_i", "delta_spent"):
+        assert st[key] == so[key], key
