@@ -563,8 +563,8 @@ class Sketcher {
         Lane& F = lanes[fill];
         F.clear_rows();
         F.phase = Lane::Filling;
-        // the new filling lane's previous B' must be consumed before rows overwrite nothing of
-        // it (rows and B' are separate buffers), so no wait is needed here
+        // no wait here: rows go to the lane's CSR buffer, while the chain may still be reading
+        // its previous B' (a separate buffer; the next attempt waits on ev_bp_free)
     }
 
     FlushState predicted_end(const Lane& P) const {
