@@ -166,28 +166,23 @@ def run_reference(a):
 # ------------------------------------------------------------------ our arm
 def merge_tree(P, torch, dist, s, d, ell, device, rank, world):
     """log2 tree (paper_1602_00412_b200/shards.py): at level L, rank r with
-    r % 2^(L+1) == 2^L sends its B^T (d x ell, FP64) to r - 2^L, which merge-shrinks it
-    (sketch.cpp:80-83, sfdg_merge_device) with its own, lower rank stacked first."""
+    r % 2^(L+1) == 2^L sends its B^T (d x ell, FP64) to r - 2^L, which merge-shrinks it into
+    its own sketch (sketch.cpp:80-83, sfdg_sketcher_merge_device: no allocation on the timed
+    path), lower rank stacked first. Rank 0 ends with the merged sketch."""
     from paper_1602_00412_b200 import shards
     host = dist.get_backend() == "gloo"  # gloo (CI / single-GPU dry runs) moves host tensors
-    bt = torch.empty((d, ell), dtype=torch.float64, device=f"cuda:{device}")
-    s.sketch_device_t(bt.data_ptr(), ell)
-
-    def send(t, peer):
-        dist.send(t.cpu() if host else t, dst=peer)
-
-    def recv(peer):
+    for _step, role, peer in shards.tree_plan(rank, world):
+        if role == "send":
+            bt = torch.empty((d, ell), dtype=torch.float64, device=f"cuda:{device}")
+            s.sketch_device_t(bt.data_ptr(), ell)
+            dist.send(bt.cpu() if host else bt, dst=peer)
+            return
         o = torch.empty((d, ell), dtype=torch.float64, device="cpu" if host else f"cuda:{device}")
         dist.recv(o, src=peer)
-        return o.to(f"cuda:{device}") if host else o
-
-    def merge(lo, hi):
-        out = torch.empty_like(lo)
+        if host:
+            o = o.to(f"cuda:{device}")
         torch.cuda.synchronize(device)
-        P.merge_device(lo.data_ptr(), hi.data_ptr(), ell, d, ell, out.data_ptr(), device)
-        return out
-
-    return shards.merge_tree(bt, rank, world, send, recv, merge)
+        s.merge_device(o.data_ptr(), ell)
 
 
 def main():

@@ -118,6 +118,10 @@ int sfdg_sketcher_get_sketch_device(sfdg_sketcher* h, double* d_out, size_t ld);
 int sfdg_sketcher_stats(sfdg_sketcher* h, sfdg_stats* out);
 /* buffer() contents (CSR, host): row_ptr (rows+1), cols (nnz), vals (nnz). */
 int sfdg_sketcher_get_buffer(sfdg_sketcher* h, int64_t* row_ptr, uint32_t* cols, double* vals);
+/* B <- merge(B, B_other) = dense_shrink(vstack(B, B_other), ell) (sketch.cpp:80-83), with
+ * B_other given as B_other^T (d x ell, leading dimension ld) in device memory of this
+ * sketcher's device: the receiving side of the multi-GPU merge tree, without allocation. */
+int sfdg_sketcher_merge_device(sfdg_sketcher* h, const double* d_other_bt, size_t ld);
 /* Returns the sketcher to its just-constructed state with a new seed (allocations kept). */
 int sfdg_sketcher_reset(sfdg_sketcher* h, uint64_t seed);
 /* Blocks until all queued device work of this sketcher finished. */

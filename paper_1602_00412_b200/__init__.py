@@ -106,6 +106,7 @@ def lib() -> C.CDLL:
     L.sfdg_sketcher_get_buffer.argtypes = [C.c_void_p, _i64p, _u32p, _dp]
     L.sfdg_sketcher_synchronize.argtypes = [C.c_void_p]
     L.sfdg_sketcher_reset.argtypes = [C.c_void_p, C.c_uint64]
+    L.sfdg_sketcher_merge_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
     L.sfdg_merge.argtypes = [_dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.c_int]
     L.sfdg_merge_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p, C.c_int,
                                     C.c_void_p]
@@ -360,6 +361,10 @@ class SfdSketcher:
         if seed is not None:
             self.cfg.seed = int(seed)
         _check(lib().sfdg_sketcher_reset(self._h, C.c_uint64(self.cfg.seed)))
+
+    def merge_device(self, d_other_bt: int, ld: int) -> None:
+        """B <- merge(B, other) with other's B^T (d x ell, leading dim ld) on this device."""
+        _check(lib().sfdg_sketcher_merge_device(self._h, C.c_void_p(d_other_bt), ld))
 
     def finalize_device(self) -> None:
         """finalize() leaving B on the device (no host copy)."""

@@ -388,6 +388,22 @@ class Sketcher {
         flushes = attempts = 0;
     }
 
+    // this <- merge(this, other) with other's B^T (d x ell, leading dimension ld) already on
+    // this sketcher's device (the torchrun shard tree receives it over NCCL). No allocation:
+    // the chain's own [B^T | B'^T] pair holds the stack.
+    void merge_device(const double* d_bt, size_t ld) {
+        chain->set_device();
+        drain();
+        Engine& C = *chain;
+        const int lp = C.lp;
+        copy2d(d_bt, (int)cfg.d, (int)cfg.ell, (int)ld, C.Mt[C.cur] + lp, 2 * lp, C.st);
+        if (lp > (int)cfg.ell) fill2d(C.Mt[C.cur] + lp + cfg.ell, (int)cfg.d, lp - (int)cfg.ell, 2 * lp, 0.0, C.st);
+        C.scr.reset();
+        C.dense_shrink_stack(C.Mt[C.cur], 2 * lp, (int)cfg.ell, lp, (int)cfg.ell, C.Mt[C.cur ^ 1], 2 * lp);
+        C.check_errors();
+        C.cur ^= 1;
+    }
+
     // Shard tree (sfdg_sharded_sketch): B^T lives in the left half of chain Mt[cur].
     Engine& chain_engine() { return *chain; }
     // this <- merge(this, other) = dense_shrink([B_this; B_other]) (sketch.cpp:80-83);
@@ -1113,6 +1129,13 @@ int sfdg_sketcher_stats(sfdg_sketcher* h, sfdg_stats* out) {
 
 int sfdg_sketcher_get_buffer(sfdg_sketcher* h, int64_t* row_ptr, uint32_t* cols, double* vals) {
     return guard([&] { impl_of(h)->get_buffer(row_ptr, cols, vals); });
+}
+
+int sfdg_sketcher_merge_device(sfdg_sketcher* h, const double* d_other_bt, size_t ld) {
+    return guard([&] {
+        if (!d_other_bt) throw invalid_argument("sfdg_sketcher_merge_device: null argument");
+        impl_of(h)->merge_device(d_other_bt, ld);
+    });
 }
 
 int sfdg_sketcher_reset(sfdg_sketcher* h, uint64_t seed) {

@@ -686,3 +686,23 @@ def test_wide_ell_streams_vs_oracle(oracle, family, d, ell, rows):
     assert btb_rel(b, bo) <= BTB_TOL
     for key in ("flushes", "attempts", "verifier_i", "delta_spent"):
         assert st[key] == so[key], key
+
+
+def test_sketcher_merge_device_matches_oracle_merge(oracle):
+    """sfdg_sketcher_merge_device (the receiving side of the torchrun tree): B <- merge(B,
+    B_other) against the oracle's merge of the same two sketches."""
+    torch = pytest.importorskip("torch")
+    rp, cs, vs = S.generate("c1", (0, 2400))
+    half = 1200
+    b1, _ = sketch_gpu(rp[:half + 1], cs, vs, 1000, 50, 1)
+    rp2 = rp[half:] - rp[half]
+    b2, _ = sketch_gpu(rp2, cs[rp[half]:], vs[rp[half]:], 1000, 50, 2)
+    s = P.SfdSketcher(P.SketchConfig(ell=50, d=1000, seed=1))
+    s.append_csr(rp[:half + 1], cs, vs)
+    s.finalize_device()
+    other = torch.from_numpy(np.ascontiguousarray(b2.T)).cuda()
+    s.merge_device(other.data_ptr(), 50)
+    got = s.sketch()
+    s.close()
+    want = oracle.merge(b1, b2, 50)
+    assert btb_rel(got, want) <= BTB_TOL
