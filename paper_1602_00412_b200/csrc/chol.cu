@@ -385,6 +385,88 @@ __global__ void __launch_bounds__(kTrsmThreads) trsm_apply_kernel(const double* 
     }
 }
 
+// k > 128: R no longer fits shared memory next to the row tile, and reading its B fragments
+// through L1/L2 serialises every DMMA on an L2 round trip (19 ms for 1e6 x 256 at c5). Here
+// the CTA walks the block columns b in lockstep and stages only the panel R[0 : 8b+8, 8b :
+// 8b+8] it needs (double-buffered with cp.async while the previous block column computes).
+constexpr int kPanelLd = 12;  // 8 columns + 4: conflict-free fragment reads
+__global__ void __launch_bounds__(kTrsmThreads) trsm_panel_kernel(const double* __restrict__ Y, int m, int k, int ld,
+                                                                  const double* __restrict__ R,
+                                                                  const double* __restrict__ dinv8,
+                                                                  double* __restrict__ X, int ldx,
+                                                                  const double* __restrict__ stats, int rows) {
+    if (stats && stats[4] != 0.0) return;
+    extern __shared__ double sm[];
+    const int kp = (k + 7) / 8 * 8;
+    const int ldy = kp + 4;
+    double* Ps = sm;                                  // 2 x kp x kPanelLd : panels of R
+    double* Ds = Ps + 2 * (size_t)kp * kPanelLd;      // kp x 12
+    double* Xs = Ds + (size_t)kp * 12;                // rows x ldy
+    const int r0 = blockIdx.x * rows;
+    auto stage_panel = [&](int b, int buf) {
+        double* P = Ps + (size_t)buf * kp * kPanelLd;
+        const int nr = 8 * b + 8;
+        for (int e = threadIdx.x; e < nr * 8; e += blockDim.x) {
+            const int i = e / 8, c = e % 8, cc = 8 * b + c;
+            const bool ok = i < k && cc < k;
+            cpa8(P + (size_t)i * kPanelLd + c, ok ? R + (size_t)i * k + cc : R, ok);
+        }
+    };
+    for (int e = threadIdx.x; e < kp * 8; e += blockDim.x) {
+        const int i = e / 8, c = e % 8;
+        cpa8(Ds + (size_t)i * 12 + c, i < k ? dinv8 + (size_t)i * 8 + c : dinv8, i < k);
+    }
+    for (int e = threadIdx.x; e < rows * kp; e += blockDim.x) {
+        const int i = e / kp, c = e % kp;
+        const bool ok = r0 + i < m && c < k;
+        cpa8(Xs + (size_t)i * ldy + c, ok ? Y + (size_t)(r0 + i) * ld + c : Y, ok);
+    }
+    stage_panel(0, 0);
+    asm volatile("cp.async.commit_group;\n" ::);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int nb = kp / 8;
+    const int ntile = rows / 8;
+    for (int b = 0; b < nb; ++b) {
+        if (b + 1 < nb) stage_panel(b + 1, (b + 1) & 1);
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 1;\n" ::);  // panel b (and the tiles) landed
+        __syncthreads();
+        const double* P = Ps + (size_t)(b & 1) * kp * kPanelLd;
+        for (int mt = w; mt < ntile; mt += blockDim.x / 32) {
+            double* xr = Xs + (size_t)(mt * 8) * ldy;
+            double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+            int kk = 0;
+            for (; kk + 4 < 8 * b; kk += 8) {
+                dmma884(c0, c1, xr[(size_t)g * ldy + kk + t], P[(size_t)(kk + t) * kPanelLd + g]);
+                dmma884(e0, e1, xr[(size_t)g * ldy + kk + 4 + t], P[(size_t)(kk + 4 + t) * kPanelLd + g]);
+            }
+            for (; kk < 8 * b; kk += 4) dmma884(c0, c1, xr[(size_t)g * ldy + kk + t], P[(size_t)(kk + t) * kPanelLd + g]);
+            c0 += e0;
+            c1 += e1;
+            double* yb = xr + (size_t)g * ldy + 8 * b + 2 * t;
+            const double a0 = yb[0] - c0, a1 = yb[1] - c1;
+            __syncwarp();
+            yb[0] = a0;
+            yb[1] = a1;
+            __syncwarp();
+            double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 8; ks += 4)
+                dmma884(x0, x1, xr[(size_t)g * ldy + 8 * b + ks + t], Ds[(size_t)(8 * b + ks + t) * 12 + g]);
+            __syncwarp();
+            yb[0] = x0;
+            yb[1] = x1;
+            __syncwarp();
+        }
+        __syncthreads();  // the buffer of panel b is refilled two iterations later
+    }
+    for (int e = threadIdx.x; e < rows * k; e += blockDim.x) {
+        const int i = e / k, c = e % k;
+        if (r0 + i < m) X[(size_t)(r0 + i) * ldx + c] = Xs[(size_t)i * ldy + c];
+    }
+}
+
 }  // namespace
 
 void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, double* T, int ldt, double* stats,
@@ -417,7 +499,22 @@ void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const do
     const int kp = (k + 7) / 8 * 8;
     if (kp > 512) throw invalid_argument("trsm_apply: k > 512 unsupported");
     ProfScope prof("trsm", st);
-    const size_t rs = kp <= kTrsmSmemK ? (size_t)kp * (kp + 4) : 0;
+    if (kp > kTrsmSmemK) {  // R streamed through shared memory one block-column panel at a time
+        static bool pattr = false;
+        if (!pattr) {
+            allow_max_dynamic_smem(trsm_panel_kernel);
+            pattr = true;
+        }
+        int rows = 128;
+        auto pbytes = [&](int r) {
+            return (2 * (size_t)kp * kPanelLd + (size_t)kp * 12 + (size_t)r * (kp + 4)) * sizeof(double);
+        };
+        while (rows > 16 && pbytes(rows) > 220 * 1024) rows /= 2;
+        LAUNCH(trsm_panel_kernel, ceil_div(m, rows), kTrsmThreads, pbytes(rows), st, Y, m, k, ld, R, dinv8, X, ldx,
+               stats, rows);
+        return;
+    }
+    const size_t rs = (size_t)kp * (kp + 4);
     int rows = 128;
     auto bytes = [&](int r) { return (rs + (size_t)kp * 12 + (size_t)r * (kp + 4)) * sizeof(double); };
     while (rows > 16 && bytes(rows) > 220 * 1024) rows /= 2;

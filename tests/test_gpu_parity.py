@@ -161,7 +161,7 @@ def test_eigh_degenerate_and_diagonal():
     assert abs(vals[0] - 6.0) < 1e-12 and np.max(np.abs(vals[1:])) < 1e-12
 
 
-@pytest.mark.parametrize("n,k", [(50, 10), (1000, 104), (300, 64), (12, 12)])
+@pytest.mark.parametrize("n,k", [(50, 10), (1000, 104), (300, 64), (12, 12), (1500, 200), (700, 256)])
 def test_orthonormalize_projector_vs_oracle(oracle, n, k):
     a = np.random.default_rng(n + k).standard_normal((n, k))
     q = P.orthonormalize(a)
