@@ -191,7 +191,7 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     CK(cudaMalloc(&S, (size_t)kmax * lp * sizeof(double)));
     CK(cudaMalloc(&x0, (size_t)d * sizeof(double)));
     CK(cudaMalloc(&ybuf, 2 * (size_t)d * sizeof(double)));
-    verify_blocks = verify_grid_blocks(device);
+    verify_blocks = verify_grid_blocks(device, d, lp);
     CK(cudaMalloc(&tpart, 2 * (size_t)verify_blocks * lp * sizeof(double)));
     CK(cudaMalloc(&tvec, (size_t)lp * sizeof(double)));
     CK(cudaMalloc(&vpart, (size_t)verify_blocks * sizeof(double)));

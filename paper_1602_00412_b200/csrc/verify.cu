@@ -383,19 +383,21 @@ VerifyFn verify_fn(int ell) {
 
 }  // namespace
 
-int verify_grid_blocks(int device) {
-    static int cached[64] = {0};
-    if (device >= 0 && device < 64 && cached[device]) return cached[device];
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, verify_kernel<8>, kVThreads, 0));
-    int sms = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    // 32 blocks: the power method is latency bound (two grid barriers per step), and with
-    // several flushes in flight the other SMs keep running their SpMM / orthonormalisation
-    // kernels (measured on c2: 146 blocks 322, 74 blocks 199, 32 blocks 182 ms per stream).
-    int nb = std::max(1, std::min(std::min(per_sm, 1) * sms, 32));
-    if (const char* e = std::getenv("SFDG_VERIFY_BLOCKS")) nb = std::max(1, std::min(nb, std::atoi(e)));
-    if (device >= 0 && device < 64) cached[device] = nb;
+int verify_grid_blocks(int device, int64_t d, int lp) {
+    static int cached_sms[64] = {0};
+    int sms = device >= 0 && device < 64 ? cached_sms[device] : 0;
+    if (!sms) {
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        if (device >= 0 && device < 64) cached_sms[device] = sms;
+    }
+    // Each step streams B'^T (8 d lp bytes) once over the grid. Small B' (c2: 8 MB): the power
+    // method is latency bound (two grid barriers per step), so 32 blocks -- with several
+    // flushes in flight the other SMs keep running SpMM / orthonormalisation (measured on c2:
+    // 146 blocks 322, 74 blocks 199, 32 blocks 182 ms per stream). Large B' (c3-c5: 0.16-2 GB
+    // per step) is bandwidth bound per SM: one block per 512 KB of B', up to every SM.
+    const int64_t by_size = (8 * d * (int64_t)lp) / (512 * 1024);
+    int nb = (int)std::max<int64_t>(32, std::min<int64_t>(sms, by_size));
+    if (const char* e = std::getenv("SFDG_VERIFY_BLOCKS")) nb = std::max(1, std::min(sms, std::atoi(e)));
     return nb;
 }
 

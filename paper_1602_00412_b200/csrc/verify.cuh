@@ -44,7 +44,7 @@ struct VerifyArgs {
     double* lpart;          // n_pieces partial sums
 };
 
-int verify_grid_blocks(int device);
+int verify_grid_blocks(int device, int64_t d, int lp);  // cooperative grid for this B' size
 void verify_launch(const VerifyArgs& args, int nblocks, cudaStream_t st);
 
 }  // namespace sfdg
