@@ -147,6 +147,7 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     if (ell < 1 || ell > kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 256] for this build");
     lp = (int)round_up((size_t)ell, 8);
     if (const char* e = std::getenv("SFDG_ORTH_EVERY_SWEEP")) adaptive = std::atoi(e) == 0;
+    if (const char* e = std::getenv("SFDG_GRAPHS")) use_graphs = std::atoi(e) != 0;
     set_device();
     int prio = 0;
     if (high_priority) {
@@ -210,6 +211,8 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
 Engine::~Engine() {
     cudaSetDevice(device);
     if (st) cudaStreamSynchronize(st);
+    for (auto& kv : graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     for (void* p : {(void*)Y, (void*)Yt, (void*)W, (void*)Mt[0], (void*)Mt[1], (void*)Bp, (void*)gram, (void*)rinv,
                     (void*)rfac,
                     (void*)dinv8, (void*)kc,
@@ -327,6 +330,46 @@ void Engine::orthonormalize_light(int m, int err_bit) {
     std::swap(Y, Yt);
 }
 
+void Engine::sweep_block(int interval, int m) {
+    const std::array<uintptr_t, 12> key{(uintptr_t)interval,   (uintptr_t)m,          (uintptr_t)Y,
+                                        (uintptr_t)Yt,         (uintptr_t)W,          (uintptr_t)a.row_ptr,
+                                        (uintptr_t)a.col,      (uintptr_t)a.val,      (uintptr_t)a.col_ptr,
+                                        (uintptr_t)a.row_idx,  (uintptr_t)a.cval,     (uintptr_t)d};
+    auto body = [&] {
+        for (int i = 0; i < interval; ++i) {
+            spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st);
+            spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
+        }
+        orthonormalize_light(m, ERR_NONFINITE_ITER);  // swaps Y and Yt (host side)
+    };
+    auto it = graphs.find(key);
+    if (it == graphs.end()) {
+        // capture once: the kernels read only fixed buffers and device scalars (no long rows,
+        // checked by the caller), so the same graph serves every later flush of this lane
+        const uint64_t l0 = g_launches.load();
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            body();
+        } catch (...) {
+            cudaStreamEndCapture(st, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        CK(cudaStreamEndCapture(st, &graph));
+        GraphEntry g;
+        CK(cudaGraphInstantiate(&g.exec, graph, 0));
+        CK(cudaGraphDestroy(graph));
+        g.kernels = g_launches.load() - l0;
+        g_launches.fetch_sub(g.kernels, std::memory_order_relaxed);  // counted at launch below
+        it = graphs.emplace(key, g).first;
+        std::swap(Y, Yt);  // body() swapped them while recording; the replay below is the real run
+    }
+    CK(cudaGraphLaunch(it->second.exec, st));
+    g_launches.fetch_add(it->second.kernels, std::memory_order_relaxed);
+    std::swap(Y, Yt);
+}
+
 void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     const int m = a.m;
     if (k < 1 || k > std::min(m, d)) throw invalid_argument("simultaneous_iteration: k out of range");
@@ -342,8 +385,18 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     // between Y <- A'(A'^T Y) unnormalised. interval = 1 is the reference's schedule
     // (randsvd.cpp:38-49).
     const int interval = adaptive ? orth_interval : 1;
+    // whole blocks (interval sweeps closed by a light pass) replay as a CUDA graph when no
+    // long-row piece kernels are involved and profiling (per-launch events) is off
+    const bool graphs_ok = use_graphs && adaptive && plan_r.host_long == 0 && plan_c.host_long == 0 &&
+                           !g_prof_on.load(std::memory_order_relaxed);
     int since = 0;
-    for (size_t s = 0; s < q; ++s) {
+    for (size_t s = 0; s < q;) {
+        if (graphs_ok && since == 0 && s + (size_t)interval < q) {
+            sweep_block(interval, m);
+            s += (size_t)interval;
+            last_since = interval;
+            continue;
+        }
         spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st);
         spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
         if (++since >= interval || s + 1 == q) {
@@ -352,6 +405,7 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
             last_since = since;
             since = 0;
         }
+        ++s;
     }
 }
 

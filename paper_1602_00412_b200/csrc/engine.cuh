@@ -3,7 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <vector>
 
@@ -107,6 +109,15 @@ class Engine {
     void orthonormalize(double* Yp, int m, int err_bit);
     // Single CholeskyQR pass on Y (between sweeps of the adaptive schedule; swaps Y/Yt).
     void orthonormalize_light(int m, int err_bit);
+    // `interval` sweeps + the light orthonormalisation that closes them, as one CUDA graph
+    // (captured on first use per shape and buffer set, replayed after: ~20 launches -> 1).
+    void sweep_block(int interval, int m);
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t kernels = 0;
+    };
+    std::map<std::array<uintptr_t, 12>, GraphEntry> graphs;
+    bool use_graphs = true;  // SFDG_GRAPHS=0 disables
     // randsvd.cpp:18-51: Z (m x lp) left in Y.
     void simultaneous_iteration(int k, const PowerCfg& cfg);
     // shrink.cpp:63-73 (+ la_core.cpp:82-128): B'^T (d x lp) into bpt (ld).
