@@ -248,19 +248,25 @@ def main():
             else:
                 dist.barrier()
 
+    prange = os.environ.get("SFDG_PROFILE_RANGE") == "1"  # ncu --replay-mode app-range around step 1
+
     def timed(fn, k):
         total = 0.0
-        for _ in range(k):
+        for it in range(k):
             sk.reset(seed)
             flush_buf.random_(0, 255)  # evict L2 between timed steps (outside the timed region)
             torch.cuda.synchronize(device)
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize(device)
+            if prange and it == 0:
+                torch.cuda.profiler.start()
             e0.record()
             fn()
             torch.cuda.synchronize(device)
             e1.record()
+            if prange and it == 0:
+                torch.cuda.profiler.stop()
             e1.synchronize()
             barrier()
             total += e0.elapsed_time(e1)
