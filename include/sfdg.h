@@ -182,6 +182,12 @@ int sfdg_read_row_stream(const char* path, size_t plain_cols, size_t* nrows, siz
  * whole-stream evaluation metric of SURVEY 8(f); rng advanced in place. */
 int sfdg_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d,
                  const double* b, size_t ell, size_t iterations, sfdg_rng_state* rng, double* out, int device);
+/* exact_tail(a, k, rng) (bench.hpp:51-55, bench.cpp:68-137): the ground-truth tail
+ * |A - A_k|_F^2 and the top-k singular values of the whole stream by block power iteration
+ * (block k + 10 <= 256, <= 1000 sweeps, the reference's convergence tests); *sweeps_out = the
+ * sweeps run (nullable). k = 0 returns |A|_F^2. rng advanced in place. */
+int sfdg_exact_tail(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d, size_t k,
+                    sfdg_rng_state* rng, double* sigma_out, double* tail_out, size_t* sweeps_out, int device);
 /* dense_shrink(a, ell) (shrink.cpp:30-61), host in/out. */
 int sfdg_dense_shrink(const double* a, size_t rows, size_t cols, size_t ell, double* out, int device);
 /* sparse_shrink(buffer, ell, power, rng) (shrink.cpp:63-73); rng advanced in place. */

@@ -139,6 +139,8 @@ class Oracle:
         L.or_dense_shrink.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp]
         L.or_fd_sketch.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.POINTER(C.c_size_t)]
         L.or_cov_err.argtypes = [C.POINTER(_OrCsr), _dp, C.c_size_t, C.c_void_p, C.c_size_t, C.POINTER(C.c_double)]
+        L.or_exact_tail.argtypes = [C.POINTER(_OrCsr), C.c_size_t, C.c_void_p, _dp, C.POINTER(C.c_double),
+                                    C.POINTER(C.c_size_t)]
         L.or_simultaneous_iteration.argtypes = [C.POINTER(_OrCsr), C.c_size_t, C.POINTER(_OrPower), C.c_void_p, _dp]
         L.or_sparse_shrink.argtypes = [C.POINTER(_OrCsr), C.c_size_t, C.POINTER(_OrPower), C.c_void_p, _dp]
         L.or_verify_spectral.argtypes = [_SYMOP, C.c_void_p, C.c_size_t, C.POINTER(_OrVerifier), C.c_void_p,
@@ -260,6 +262,15 @@ class Oracle:
         out = C.c_double()
         self._chk(self.L.or_cov_err(C.byref(keep[0]), _ptr(b, _dp), b.shape[0], rng.h, iterations, C.byref(out)))
         return out.value
+
+    def exact_tail(self, row_ptr, cols, vals, d, k, rng: "Rng"):
+        """exact_tail (bench.cpp:68-137): (tail_sq, sigma[k], sweeps); rng advanced."""
+        keep = self._csr(row_ptr, cols, vals, d)
+        sig = np.zeros(max(1, k))
+        tail = C.c_double()
+        sw = C.c_size_t()
+        self._chk(self.L.or_exact_tail(C.byref(keep[0]), k, rng.h, _ptr(sig, _dp), C.byref(tail), C.byref(sw)))
+        return tail.value, sig[:k], sw.value
 
     def fd_sketch(self, rows, ell):
         """FdSketcher whole-stream run (sketch.cpp:47-78): (B ell x d, shrink_count)."""
@@ -407,6 +418,7 @@ class Reference:
         L.ref_merge.argtypes = [_dp, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp]
         L.ref_sketch.argtypes = csr + [C.c_size_t, C.c_double] + pw + [C.c_uint64, _dp, _dp]
         L.ref_cov_err.argtypes = csr + [_dp, C.c_size_t, C.c_void_p, C.c_size_t, C.POINTER(C.c_double)]
+        L.ref_exact_tail.argtypes = csr + [C.c_size_t, C.c_void_p, _dp, C.POINTER(C.c_double)]
 
     def _chk(self, code):
         if code:
@@ -496,6 +508,13 @@ class Reference:
         off += 4 * z
         vs = np.frombuffer(raw[off:off + 8 * z], np.float64).copy()
         return rp, cs, vs, int(d), (msg if err else None)
+
+    def exact_tail(self, row_ptr, cols, vals, d, k, rng):
+        args, keep = self._csr(row_ptr, cols, vals, d)
+        sig = np.zeros(max(1, k))
+        tail = C.c_double()
+        self._chk(self.L.ref_exact_tail(*args, k, rng.h, _ptr(sig, _dp), C.byref(tail)))
+        return tail.value, sig[:k]
 
     def cov_err(self, row_ptr, cols, vals, d, sketch, rng, iterations=1000):
         args, keep = self._csr(row_ptr, cols, vals, d)

@@ -154,6 +154,17 @@ int ref_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* vals
     });
 }
 
+// exact_tail (bench.cpp:68-137): tail and the top-k singular values.
+int ref_exact_tail(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t m, size_t d, size_t k,
+                   void* rng, double* sigma_out, double* tail_out) {
+    return guarded([&] {
+        sfd::SparseBuffer a = to_buffer(row_ptr, cols, vals, m, d);
+        sfd::TailResult r = sfd::exact_tail(a, k, *static_cast<sfd::Rng*>(rng));
+        *tail_out = r.tail_sq;
+        for (size_t i = 0; i < r.sigma.size(); ++i) sigma_out[i] = r.sigma[i];
+    });
+}
+
 // Whole-stream FdSketcher run (sketch.cpp:47-78) over n dense rows.
 int ref_fd_sketch(const double* rows, size_t n, size_t d, size_t ell, double* out, size_t* shrink_count) {
     return guarded([&] {

@@ -784,6 +784,79 @@ static double spectral_norm_sym(or_symop op, void* ctx, size_t d, size_t iterati
     return rayleigh;
 }
 
+/* bench.cpp:68-137: |A - A_k|_F^2 by block power iteration (block k + 10, <= 1000 sweeps) */
+int or_exact_tail(const or_csr* a, size_t k, or_rng* rng, double* sigma_out /* k */, double* tail_out,
+                  size_t* sweeps_out) {
+    ENTER();
+    const double fsq = csr_frob_sq(a);
+    *sweeps_out = 0;
+    if (k == 0) {
+        *tail_out = fsq;
+        LEAVE();
+    }
+    const size_t m = a->m, d = a->d;
+    if (k > (m < d ? m : d)) THROW_INVALID("exact_tail: k exceeds matrix rank bound");
+    size_t block = k + 10;
+    if (block > (m < d ? m : d)) block = m < d ? m : d;
+    mat g = gaussian_matrix(d, block, rng);
+    double* col = (double*)az(d * sizeof(double));
+    double* yc = (double*)az(m * sizeof(double));
+    mat y = mat_new(m, block);
+    for (size_t j = 0; j < block; ++j) {
+        for (size_t i = 0; i < d; ++i) col[i] = AT(g, i, j);
+        sp_matvec(a, col, yc);
+        for (size_t i = 0; i < m; ++i) AT(y, i, j) = yc[i];
+    }
+    y = orthonormalize(&y);
+    double* prev = (double*)az(k * sizeof(double));
+    for (size_t i = 0; i < k; ++i) prev[i] = -1.0;
+    double prev_energy = -1.0;
+    double* ycol = (double*)az(m * sizeof(double));
+    double* wc = (double*)az(d * sizeof(double));
+    double* est = (double*)az(k * sizeof(double));
+    for (size_t sweep = 0; sweep < 1000; ++sweep) {
+        mat w = mat_new(d, block);
+        mat next = mat_new(m, block);
+        for (size_t j = 0; j < block; ++j) {
+            for (size_t i = 0; i < m; ++i) ycol[i] = AT(y, i, j);
+            sp_rmatvec(a, ycol, wc);
+            for (size_t i = 0; i < d; ++i) AT(w, i, j) = wc[i];
+            sp_matvec(a, wc, yc);
+            for (size_t i = 0; i < m; ++i) AT(next, i, j) = yc[i];
+        }
+        mat small = mat_new(block, block);
+        for (size_t p = 0; p < block; ++p)
+            for (size_t q = p; q < block; ++q) {
+                double s = 0.0;
+                for (size_t i = 0; i < d; ++i) s += AT(w, i, p) * AT(w, i, q);
+                AT(small, p, q) = s;
+                AT(small, q, p) = s;
+            }
+        eigh_t eig = jacobi_eigh(&small, 1e-14 * (fsq > 1.0 ? fsq : 1.0));
+        for (size_t i = 0; i < k; ++i) est[i] = sqrt(eig.values[i] > 0.0 ? eig.values[i] : 0.0);
+        double change = 0.0;
+        for (size_t i = 0; i < k; ++i) {
+            const double c = fabs(est[i] - prev[i]);
+            if (c > change) change = c;
+        }
+        const double scale = est[0] > 1.0 ? est[0] : 1.0;
+        double head = 0.0;
+        for (size_t i = 0; i < k; ++i) head += est[i] * est[i];
+        const int values_done = sweep > 0 && change <= 1e-10 * scale;
+        const int energy_done = sweep >= 30 && fabs(head - prev_energy) <= 1e-9 * (head > 1.0 ? head : 1.0);
+        if (values_done || energy_done) {
+            memcpy(sigma_out, est, k * sizeof(double));
+            *tail_out = fsq - head > 0.0 ? fsq - head : 0.0;
+            *sweeps_out = sweep + 1;
+            LEAVE();
+        }
+        memcpy(prev, est, k * sizeof(double));
+        prev_energy = head;
+        y = orthonormalize(&next);
+    }
+    THROW_NUMERICAL("exact_tail: no convergence within 1000 sweeps");
+}
+
 /* bench.cpp:171-183: |A^T A - B^T B|_2 / |A|_F^2 */
 int or_cov_err(const or_csr* a, const double* sketch, size_t ell, or_rng* rng, size_t iterations, double* out) {
     ENTER();

@@ -97,6 +97,10 @@ int or_merge(const double* b1, size_t r1, const double* b2, size_t r2, size_t d,
  * |A^T A - B^T B|_2 / |A|_F^2 by `iterations` power steps from unit_sphere_vector(d, rng). */
 int or_cov_err(const or_csr* a, const double* sketch, size_t ell, or_rng* rng, size_t iterations, double* out);
 
+/* ---- exact_tail (core/include/sfd/bench.hpp:51-55, core/src/bench.cpp:68-137) ----
+ * |A - A_k|_F^2 and the top-k singular values; *sweeps_out = block sweeps run. */
+int or_exact_tail(const or_csr* a, size_t k, or_rng* rng, double* sigma_out, double* tail_out, size_t* sweeps_out);
+
 /* ---- FdSketcher (core/include/sfd/sketch.hpp:53-67, core/src/sketch.cpp:47-78) ----
  * Whole-stream dense FD: n rows (n x d row-major) -> B (ell x d), shrink count. */
 int or_fd_sketch(const double* rows, size_t n, size_t d, size_t ell, double* out, size_t* shrink_count);

@@ -114,6 +114,8 @@ def lib() -> C.CDLL:
     L.sfdg_sketch_file.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(_SketchCfg), C.c_int, _dp, C.POINTER(_Stats),
                                    _szp]
     L.sfdg_read_row_stream.argtypes = [C.c_char_p, C.c_size_t, _szp, _szp, _szp, _i64p, _u32p, _dp]
+    L.sfdg_exact_tail.argtypes = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t, C.c_size_t, C.POINTER(_Rng), _dp,
+                                  C.POINTER(C.c_double), _szp, C.c_int]
     L.sfdg_cov_err.argtypes = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, C.c_size_t,
                                C.POINTER(_Rng), C.POINTER(C.c_double), C.c_int]
     L.sfdg_fd_create.argtypes = [C.c_size_t, C.c_size_t, C.c_int, C.POINTER(C.c_void_p)]
@@ -519,6 +521,21 @@ def read_row_stream_width(path: str, plain_cols: int = 0) -> int:
                 continue
             return int(line.split()[1])
     raise InvalidArgument(path + ": missing MatrixMarket size line")
+
+
+def exact_tail(csr, d: int, k: int, rng, device: int = 0):
+    """exact_tail(a, k, rng) (bench.cpp:68-137) on the device: (tail_sq, sigma[k], sweeps, RngState)."""
+    rp, cs, vs = _csr(*csr)
+    st = _rng_arg(rng)
+    c = st._c()
+    sig = np.zeros(max(1, k))
+    tail = C.c_double()
+    sw = C.c_size_t()
+    _check(lib().sfdg_exact_tail(_p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), len(rp) - 1, d, k, C.byref(c),
+                                 _p(sig, _dp), C.byref(tail), C.byref(sw), device))
+    st = RngState(st.seed)
+    st._update(c)
+    return tail.value, sig[:k], sw.value, st
 
 
 def cov_err(csr, d: int, sketch, rng, iterations: int = 1000, device: int = 0):

@@ -1425,6 +1425,35 @@ int sfdg_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* val
     });
 }
 
+int sfdg_exact_tail(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d, size_t k,
+                    sfdg_rng_state* rng, double* sigma_out, double* tail_out, size_t* sweeps_out, int device) {
+    return guard([&] {
+        if (!row_ptr || !rng || !tail_out) throw invalid_argument("exact_tail: null argument");
+        validate_csr(row_ptr, cols, vals, n, d);
+        const double fsq = csr_frob(row_ptr, vals, n);
+        size_t sweeps = 0;
+        if (k == 0) {  // bench.cpp:70-73
+            *tail_out = fsq;
+            if (sweeps_out) *sweeps_out = 0;
+            return;
+        }
+        if (k > std::min(n, d)) throw invalid_argument("exact_tail: k exceeds matrix rank bound");
+        const size_t block = std::min(k + 10, std::min(n, d));
+        if (block > (size_t)kMaxEll) throw invalid_argument("exact_tail: k + 10 must be <= 256 for this build");
+        require_device(device);
+        const int64_t nnz = row_ptr[n] - row_ptr[0];
+        Engine e(device, (int)d, (int)block, rng->seed, (uint64_t)std::max<int64_t>(nnz, 1), (int)n);
+        rng_in(e, rng);
+        e.load_csr(row_ptr, cols, vals, (int)n, nnz);
+        e.prepare();
+        std::vector<double> sig(k);
+        device_exact_tail(e, (int)k, fsq, sig.data(), tail_out, &sweeps);
+        if (sigma_out) std::memcpy(sigma_out, sig.data(), k * sizeof(double));
+        if (sweeps_out) *sweeps_out = sweeps;
+        rng_out(e, rng);
+    });
+}
+
 int sfdg_power_iteration_count(size_t m, const sfdg_power_config* power, size_t* q) {
     return guard([&] { *q = power_iteration_count(m, to_power(power)); });
 }

@@ -1,4 +1,4 @@
-// metrics.cu -- device evaluation metric cov_err.
+// metrics.cu -- device evaluation metrics cov_err and exact_tail.
 //
 // Reference: cov_err (core/src/bench.cpp:171-183) = spectral_norm_sym (la_core.cpp:191-211)
 // of x -> A^T(A x) - B^T(B x), divided by |A|_F^2. On the CPU it is 1000 power steps over
@@ -6,7 +6,9 @@
 // stream's CSR/CSC (the flush SpMM kernels with a 2-wide panel), two passes over B^T and
 // fixed-order reductions, captured once as a CUDA graph and replayed `iterations` times.
 // The start vector is unit_sphere_vector(d, rng) from the same draw stream as the CPU.
+#include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "common.cuh"
 #include "dense.cuh"
@@ -187,6 +189,56 @@ double device_cov_err(Engine& e, const double* b_host, int ell, size_t iteration
     if (h[3] != 0.0) throw numerical_error("spectral_norm_sym: non-finite operator output");
     if (h[2] != 0.0) return 0.0;
     return h[0] / a_fsq;
+}
+
+// exact_tail (core/src/bench.cpp:68-137): |A - A_k|_F^2 by block power iteration with block
+// = k + 10 columns (the engine's ell), <= 1000 sweeps, the reference's convergence tests on
+// the top-k Ritz values of W^T W (W = A^T Y). A (whole stream) is held by e (load_csr with
+// panels + prepare done); the Gaussian start block is drawn at e.pos.
+void device_exact_tail(Engine& e, int k, double a_fsq, double* sigma_out, double* tail_out, size_t* sweeps_out) {
+    *sweeps_out = 0;
+    if (k == 0) {
+        *tail_out = a_fsq;
+        return;
+    }
+    const int m = e.a.m, d = e.d, lp = e.lp, block = e.ell;
+    cudaStream_t st = e.st;
+    e.scr.reset();
+    e.rng->normals(e.pos, (uint64_t)d * block, (uint64_t)block, (uint64_t)lp, e.W, e.d_err, st);  // la_core.cpp:167
+    spmm(e.a.row_ptr, (const int*)e.a.col, e.a.val, m, e.plan_r, e.a.nnz, e.W, lp, lp, e.Y, lp, e.scr, st);
+    e.orthonormalize(e.Y, m, ERR_NONFINITE_ITER);
+    std::vector<double> prev(k, -1.0), est(k), vals(block);
+    double prev_energy = -1.0;
+    const double tol = 1e-14 * std::max(a_fsq, 1.0);
+    for (size_t sweep = 0; sweep < 1000; ++sweep) {
+        e.scr.reset();
+        spmm(e.a.col_ptr, e.a.row_idx, e.a.cval, d, e.plan_c, e.a.nnz, e.Y, lp, lp, e.W, lp, e.scr, st);  // W = A^T Y
+        spmm(e.a.row_ptr, (const int*)e.a.col, e.a.val, m, e.plan_r, e.a.nnz, e.W, lp, lp, e.Y, lp, e.scr, st);  // next
+        gram_tn(e.W, d, lp, lp, e.gram, lp, e.scr, st);  // small = W^T W (block x block leading part)
+        eigh(e.gram, block, lp, tol, nullptr, e.evals, e.evecs, block, e.d_err, e.scr, st, k);
+        CK(cudaMemcpyAsync(vals.data(), e.evals, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        double change = 0.0, head = 0.0;
+        for (int i = 0; i < k; ++i) {
+            est[i] = std::sqrt(std::max(vals[i], 0.0));
+            change = std::max(change, std::abs(est[i] - prev[i]));
+            head += est[i] * est[i];
+        }
+        const double scale = std::max(est[0], 1.0);
+        const bool values_done = sweep > 0 && change <= 1e-10 * scale;
+        const bool energy_done = sweep >= 30 && std::abs(head - prev_energy) <= 1e-9 * std::max(head, 1.0);
+        if (values_done || energy_done) {
+            for (int i = 0; i < k; ++i) sigma_out[i] = est[i];
+            *tail_out = std::max(a_fsq - head, 0.0);
+            *sweeps_out = sweep + 1;
+            e.check_errors();
+            return;
+        }
+        prev = est;
+        prev_energy = head;
+        e.orthonormalize(e.Y, m, ERR_NONFINITE_ITER);
+    }
+    throw numerical_error("exact_tail: no convergence within 1000 sweeps");
 }
 
 }  // namespace sfdg

@@ -706,3 +706,20 @@ def test_sketcher_merge_device_matches_oracle_merge(oracle):
     s.close()
     want = oracle.merge(b1, b2, 50)
     assert btb_rel(got, want) <= BTB_TOL
+
+
+def test_exact_tail_device_vs_oracle(oracle):
+    """Device exact_tail (whole-stream block power iteration) against the oracle from the same
+    draws: tail |A - A_k|_F^2 and sigma agree to the convergence tolerance; then the paper's
+    bound |A^T A - B^T B|_2 <= |A - A_k|_F^2 / (alpha ell - k) holds for the GPU sketch."""
+    rp, cs, vs = S.generate("c1", (0, 3000))
+    for k in (0, 7, 10):
+        tail, sig, sweeps, st = P.exact_tail((rp, cs, vs), 1000, k, P.RngState(9))
+        to, so, _ = oracle.exact_tail(rp, cs, vs, 1000, k, oracle.rng(9))
+        assert abs(tail - to) <= 1e-7 * to
+        assert np.max(np.abs(sig - so)) <= 1e-7 * max(1.0, so.max() if k else 1.0)
+    b, _ = sketch_gpu(rp, cs, vs, 1000, 50, 0)
+    ce, _ = P.cov_err((rp, cs, vs), 1000, b, P.RngState(77), iterations=400)
+    fsq = float((vs ** 2).sum())
+    tail7, _, _, _ = P.exact_tail((rp, cs, vs), 1000, 7, P.RngState(9))
+    assert ce * fsq <= tail7 / (KALPHA * 50 - 7)  # k = 7 < alpha ell = 7.3

@@ -196,3 +196,14 @@ def test_cov_err_oracle_matches_reference(oracle, reference):
         a[i, cs[rp[i]:rp[i + 1]]] = vs[rp[i]:rp[i + 1]]
     top = np.linalg.norm(a, 2) ** 2 / (a ** 2).sum()
     assert abs(oracle.cov_err(rp, cs, vs, 1000, np.zeros((5, 1000)), oracle.rng(1), 400) - top) <= 1e-6 * top
+
+
+def test_exact_tail_oracle_matches_reference(oracle, reference):
+    """exact_tail restatement (bench.cpp:68-137: block k+10, MGS, Jacobi, the two convergence
+    tests) bit-exact against the compiled reference for k = 0, 5, 10."""
+    from paper_1602_00412_b200 import synthetic as S
+    rp, cs, vs = S.generate("c1", (0, 1500))
+    for k in (0, 5, 10):
+        t1, s1, _ = oracle.exact_tail(rp, cs, vs, 1000, k, oracle.rng(9))
+        t2, s2 = reference.exact_tail(rp, cs, vs, 1000, k, reference.rng(9))
+        assert t1 == t2 and np.array_equal(s1, s2)
