@@ -308,10 +308,18 @@ def main():
         t0 = time.time()
         ce, _ = P.cov_err((rp, cs, vs), d, b, P.RngState(4242), iterations=1000, device=device)
         alpha = 6.0 / 41.0
+        fsq = float(np.dot(vs, vs))
+        # the north_star bound at k = the planted rank: |A^T A - B^T B|_2 <= |A - A_k|_F^2 / (ell - k),
+        # with |A - A_k|_F^2 from exact_tail (bench.cpp:68-137) on the device
+        kp = {"c1": 10, "c2": 20, "c5": 32}.get(a.config, 0)
+        tail, _, sweeps, _ = P.exact_tail((rp, cs, vs), d, kp, P.RngState(4243), device=device)
         accuracy = {"cov_err": ce, "definition": "|A^T A - B^T B|_2 / |A|_F^2 over the whole stream (1000 "
                                                  "power steps on the device, bench.cpp:171-183)",
                     "alpha_bound_k0": 1.0 / (alpha * ell), "within_alpha_bound": bool(ce <= 1.0 / (alpha * ell)),
                     "fd_bound_k0": 1.0 / ell, "within_fd_bound": bool(ce <= 1.0 / ell),
+                    "k_planted": kp, "tail_k_over_fsq": tail / fsq, "exact_tail_sweeps": sweeps,
+                    "north_star_bound_k": tail / fsq / (ell - kp),
+                    "within_north_star_bound": bool(ce <= tail / fsq / (ell - kp)),
                     "seconds": round(time.time() - t0, 3)}
 
     value = world * nnz * a.steps / t_dev
