@@ -188,6 +188,11 @@ int sfdg_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* val
  * sweeps run (nullable). k = 0 returns |A|_F^2. rng advanced in place. */
 int sfdg_exact_tail(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d, size_t k,
                     sfdg_rng_state* rng, double* sigma_out, double* tail_out, size_t* sweeps_out, int device);
+/* proj_err(a, sketch, k, tail) (bench.hpp:57-60, bench.cpp:139-169): |A - A V_k V_k^T|_F^2 /
+ * tail_sq with V_k the sketch's top-k right singular vectors; *has_value = 0 for the
+ * reference's nullopt cases (rank <= k input, sketch without a k-dimensional span). */
+int sfdg_proj_err(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d, const double* b,
+                  size_t ell, size_t k, double tail_sq, double* out, int* has_value, int device);
 /* dense_shrink(a, ell) (shrink.cpp:30-61), host in/out. */
 int sfdg_dense_shrink(const double* a, size_t rows, size_t cols, size_t ell, double* out, int device);
 /* sparse_shrink(buffer, ell, power, rng) (shrink.cpp:63-73); rng advanced in place. */

@@ -139,6 +139,8 @@ class Oracle:
         L.or_dense_shrink.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp]
         L.or_fd_sketch.argtypes = [_dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, C.POINTER(C.c_size_t)]
         L.or_cov_err.argtypes = [C.POINTER(_OrCsr), _dp, C.c_size_t, C.c_void_p, C.c_size_t, C.POINTER(C.c_double)]
+        L.or_proj_err.argtypes = [C.POINTER(_OrCsr), _dp, C.c_size_t, C.c_size_t, C.c_double,
+                                  C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.or_exact_tail.argtypes = [C.POINTER(_OrCsr), C.c_size_t, C.c_void_p, _dp, C.POINTER(C.c_double),
                                     C.POINTER(C.c_size_t)]
         L.or_simultaneous_iteration.argtypes = [C.POINTER(_OrCsr), C.c_size_t, C.POINTER(_OrPower), C.c_void_p, _dp]
@@ -262,6 +264,15 @@ class Oracle:
         out = C.c_double()
         self._chk(self.L.or_cov_err(C.byref(keep[0]), _ptr(b, _dp), b.shape[0], rng.h, iterations, C.byref(out)))
         return out.value
+
+    def proj_err(self, row_ptr, cols, vals, d, sketch, k, tail_sq):
+        """proj_err (bench.cpp:139-169): value or None (the reference's nullopt)."""
+        keep = self._csr(row_ptr, cols, vals, d)
+        b = _f64(sketch)
+        out, has = C.c_double(), C.c_int()
+        self._chk(self.L.or_proj_err(C.byref(keep[0]), _ptr(b, _dp), b.shape[0], k, tail_sq, C.byref(out),
+                                     C.byref(has)))
+        return out.value if has.value else None
 
     def exact_tail(self, row_ptr, cols, vals, d, k, rng: "Rng"):
         """exact_tail (bench.cpp:68-137): (tail_sq, sigma[k], sweeps); rng advanced."""
@@ -419,6 +430,8 @@ class Reference:
         L.ref_sketch.argtypes = csr + [C.c_size_t, C.c_double] + pw + [C.c_uint64, _dp, _dp]
         L.ref_cov_err.argtypes = csr + [_dp, C.c_size_t, C.c_void_p, C.c_size_t, C.POINTER(C.c_double)]
         L.ref_exact_tail.argtypes = csr + [C.c_size_t, C.c_void_p, _dp, C.POINTER(C.c_double)]
+        L.ref_proj_err.argtypes = csr + [_dp, C.c_size_t, C.c_size_t, C.c_double, C.POINTER(C.c_double),
+                                         C.POINTER(C.c_int)]
 
     def _chk(self, code):
         if code:
@@ -508,6 +521,13 @@ class Reference:
         off += 4 * z
         vs = np.frombuffer(raw[off:off + 8 * z], np.float64).copy()
         return rp, cs, vs, int(d), (msg if err else None)
+
+    def proj_err(self, row_ptr, cols, vals, d, sketch, k, tail_sq):
+        args, keep = self._csr(row_ptr, cols, vals, d)
+        b = _f64(sketch)
+        out, has = C.c_double(), C.c_int()
+        self._chk(self.L.ref_proj_err(*args, _ptr(b, _dp), b.shape[0], k, tail_sq, C.byref(out), C.byref(has)))
+        return out.value if has.value else None
 
     def exact_tail(self, row_ptr, cols, vals, d, k, rng):
         args, keep = self._csr(row_ptr, cols, vals, d)

@@ -165,6 +165,21 @@ int ref_exact_tail(const int64_t* row_ptr, const uint32_t* cols, const double* v
     });
 }
 
+// proj_err (bench.cpp:139-169); *has_value = 0 for nullopt.
+int ref_proj_err(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t m, size_t d,
+                 const double* sketch, size_t ell, size_t k, double tail_sq, double* out, int* has_value) {
+    return guarded([&] {
+        sfd::SparseBuffer a = to_buffer(row_ptr, cols, vals, m, d);
+        sfd::DenseMatrix b(ell, d);
+        std::memcpy(b.data.data(), sketch, ell * d * sizeof(double));
+        sfd::TailResult t;
+        t.tail_sq = tail_sq;
+        auto r = sfd::proj_err(a, b, k, t);
+        *has_value = r ? 1 : 0;
+        *out = r ? *r : 0.0;
+    });
+}
+
 // Whole-stream FdSketcher run (sketch.cpp:47-78) over n dense rows.
 int ref_fd_sketch(const double* rows, size_t n, size_t d, size_t ell, double* out, size_t* shrink_count) {
     return guarded([&] {

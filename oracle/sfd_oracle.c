@@ -857,6 +857,42 @@ int or_exact_tail(const or_csr* a, size_t k, or_rng* rng, double* sigma_out /* k
     THROW_NUMERICAL("exact_tail: no convergence within 1000 sweeps");
 }
 
+/* bench.cpp:139-169: |A - A V_k V_k^T|_F^2 / tail (V_k from svd_top of the sketch);
+ * *has_value = 0 for the reference's nullopt cases. */
+int or_proj_err(const or_csr* a, const double* sketch, size_t ell, size_t k, double tail_sq, double* out,
+                int* has_value) {
+    ENTER();
+    *has_value = 0;
+    *out = 0.0;
+    if (k < 1 || k > ell) THROW_INVALID("proj_err: k out of range");
+    if (tail_sq < 1e-12 * csr_frob_sq(a)) { /* rank <= k input */
+        LEAVE();
+    }
+    mat b = {ell, a->d, (double*)sketch};
+    svd_t svd = svd_top(&b, k);
+    if (svd.singular[0] == 0.0 || svd.singular[k - 1] < 1e-10 * svd.singular[0]) {
+        LEAVE();
+    }
+    double num = 0.0;
+    double* proj = (double*)az(k * sizeof(double));
+    for (size_t i = 0; i < a->m; ++i) {
+        for (size_t t = 0; t < k; ++t) proj[t] = 0.0;
+        double row_sq = 0.0;
+        for (int64_t p = a->row_ptr[i]; p < a->row_ptr[i + 1]; ++p) {
+            const double v = a->vals[p];
+            row_sq += v * v;
+            const uint32_t j = a->cols[p];
+            for (size_t t = 0; t < k; ++t) proj[t] += AT(svd.right, j, t) * v;
+        }
+        double proj_sq = 0.0;
+        for (size_t t = 0; t < k; ++t) proj_sq += proj[t] * proj[t];
+        num += row_sq - proj_sq;
+    }
+    *out = (num > 0.0 ? num : 0.0) / tail_sq;
+    *has_value = 1;
+    LEAVE();
+}
+
 /* bench.cpp:171-183: |A^T A - B^T B|_2 / |A|_F^2 */
 int or_cov_err(const or_csr* a, const double* sketch, size_t ell, or_rng* rng, size_t iterations, double* out) {
     ENTER();

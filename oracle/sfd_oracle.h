@@ -101,6 +101,10 @@ int or_cov_err(const or_csr* a, const double* sketch, size_t ell, or_rng* rng, s
  * |A - A_k|_F^2 and the top-k singular values; *sweeps_out = block sweeps run. */
 int or_exact_tail(const or_csr* a, size_t k, or_rng* rng, double* sigma_out, double* tail_out, size_t* sweeps_out);
 
+/* ---- proj_err (core/include/sfd/bench.hpp:57-60, core/src/bench.cpp:139-169) ---- */
+int or_proj_err(const or_csr* a, const double* sketch, size_t ell, size_t k, double tail_sq, double* out,
+                int* has_value);
+
 /* ---- FdSketcher (core/include/sfd/sketch.hpp:53-67, core/src/sketch.cpp:47-78) ----
  * Whole-stream dense FD: n rows (n x d row-major) -> B (ell x d), shrink count. */
 int or_fd_sketch(const double* rows, size_t n, size_t d, size_t ell, double* out, size_t* shrink_count);

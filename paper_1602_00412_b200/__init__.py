@@ -114,6 +114,8 @@ def lib() -> C.CDLL:
     L.sfdg_sketch_file.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(_SketchCfg), C.c_int, _dp, C.POINTER(_Stats),
                                    _szp]
     L.sfdg_read_row_stream.argtypes = [C.c_char_p, C.c_size_t, _szp, _szp, _szp, _i64p, _u32p, _dp]
+    L.sfdg_proj_err.argtypes = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, C.c_size_t, C.c_double,
+                                C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_int]
     L.sfdg_exact_tail.argtypes = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t, C.c_size_t, C.POINTER(_Rng), _dp,
                                   C.POINTER(C.c_double), _szp, C.c_int]
     L.sfdg_cov_err.argtypes = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t, _dp, C.c_size_t, C.c_size_t,
@@ -521,6 +523,16 @@ def read_row_stream_width(path: str, plain_cols: int = 0) -> int:
                 continue
             return int(line.split()[1])
     raise InvalidArgument(path + ": missing MatrixMarket size line")
+
+
+def proj_err(csr, d: int, sketch, k: int, tail_sq: float, device: int = 0):
+    """proj_err (bench.cpp:139-169) on the device: value or None (the reference's nullopt)."""
+    rp, cs, vs = _csr(*csr)
+    b = _f64(np.atleast_2d(sketch))
+    out, has = C.c_double(), C.c_int()
+    _check(lib().sfdg_proj_err(_p(rp, _i64p), _p(cs, _u32p), _p(vs, _dp), len(rp) - 1, d, _p(b, _dp), b.shape[0], k,
+                               tail_sq, C.byref(out), C.byref(has), device))
+    return out.value if has.value else None
 
 
 def exact_tail(csr, d: int, k: int, rng, device: int = 0):

@@ -1454,6 +1454,24 @@ int sfdg_exact_tail(const int64_t* row_ptr, const uint32_t* cols, const double* 
     });
 }
 
+int sfdg_proj_err(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d, const double* b,
+                  size_t ell, size_t k, double tail_sq, double* out, int* has_value, int device) {
+    return guard([&] {
+        if (!row_ptr || !b || !out || !has_value) throw invalid_argument("proj_err: null argument");
+        if (k < 1 || k > ell) throw invalid_argument("proj_err: k out of range");
+        if (ell > (size_t)kMaxEll) throw invalid_argument("proj_err: sketch rows must be in [1, 256]");
+        if (ell > d) throw invalid_argument("svd_top: expects m <= d");
+        validate_csr(row_ptr, cols, vals, n, d);
+        require_device(device);
+        const int64_t nnz = row_ptr[n] - row_ptr[0];
+        Engine e(device, (int)d, (int)ell, 0, (uint64_t)std::max<int64_t>(nnz, 1), 1);
+        e.load_csr(row_ptr, cols, vals, (int)n, nnz, /*panels=*/false);
+        e.prepare();
+        *has_value = device_proj_err(e, b, (int)ell, (int)k, csr_frob(row_ptr, vals, n), tail_sq, out) ? 1 : 0;
+        if (!*has_value) *out = 0.0;
+    });
+}
+
 int sfdg_power_iteration_count(size_t m, const sfdg_power_config* power, size_t* q) {
     return guard([&] { *q = power_iteration_count(m, to_power(power)); });
 }

@@ -157,6 +157,8 @@ class Engine {
 // cov_err (bench.cpp:171-183) of B (ell x d, host row-major) against the A held by e
 // (load_csr + prepare done); draws unit_sphere_vector(d) at e.pos (metrics.cu).
 double device_cov_err(Engine& e, const double* b_host, int ell, size_t iterations, double a_fsq);
+// proj_err (bench.cpp:139-169); false = the reference's nullopt (metrics.cu).
+bool device_proj_err(Engine& e, const double* b_host, int ell, int k, double a_fsq, double tail_sq, double* out);
 // exact_tail (bench.cpp:68-137) with block = e.ell = min(k + 10, m, d) (metrics.cu).
 void device_exact_tail(Engine& e, int k, double a_fsq, double* sigma_out, double* tail_out, size_t* sweeps_out);
 

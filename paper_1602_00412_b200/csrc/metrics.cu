@@ -191,6 +191,51 @@ double device_cov_err(Engine& e, const double* b_host, int ell, size_t iteration
     return h[0] / a_fsq;
 }
 
+// proj_err (core/src/bench.cpp:139-169): |A - A V_k V_k^T|_F^2 / tail with V_k the top-k
+// right singular vectors of the sketch (svd_top, la_core.cpp:82-128: Gram B B^T, eigen,
+// v = B^T u / s). Device: Gram + eigh, V_k = B^T S (S = U diag(1/s)) by GEMM, then
+// |A V_k|_F^2 by one SpMM over the stream, num = |A|_F^2 - |A V_k|_F^2 (the reference sums the
+// same per row). Returns false for the reference's nullopt cases.
+bool device_proj_err(Engine& e, const double* b_host, int ell, int k, double a_fsq, double tail_sq, double* out) {
+    if (k < 1 || k > ell) throw invalid_argument("proj_err: k out of range");
+    if (tail_sq < 1e-12 * a_fsq) return false;  // rank <= k input
+    const int d = e.d, m = e.a.m, lp = e.lp;
+    const int kp = (k + 1) / 2 * 2;
+    cudaStream_t st = e.st;
+    e.scr.reset();
+    double* bdev = e.scr.take<double>((int64_t)ell * d);
+    CK(cudaMemcpyAsync(bdev, b_host, (size_t)ell * d * sizeof(double), cudaMemcpyHostToDevice, st));
+    fill2d(e.W, d, lp, lp, 0.0, st);
+    transpose(bdev, ell, d, d, e.W, lp, st);  // B^T (d x lp)
+    double* fsq = e.d_scal + 6;
+    sumsq(e.W, d, lp, lp, fsq, nullptr, 0, e.scr, st);
+    gram_tn(e.W, d, lp, lp, e.gram, lp, e.scr, st);  // B B^T
+    eigh(e.gram, ell, lp, 0.0, fsq, e.evals, e.evecs, ell, e.d_err, e.scr, st, k);  // tol 1e-12 max(|B|^2, 1)
+    std::vector<double> lam(k), U((size_t)ell * ell);
+    CK(cudaMemcpyAsync(lam.data(), e.evals, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(U.data(), e.evecs, (size_t)ell * ell * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    e.check_errors();
+    std::vector<double> sig(k);
+    for (int t = 0; t < k; ++t) sig[t] = std::sqrt(std::max(lam[t], 0.0));
+    if (sig[0] == 0.0 || sig[k - 1] < 1e-10 * sig[0]) return false;  // no k-dimensional span
+    // S (lp x kp): S[i][t] = U[i][t] / s_t
+    std::vector<double> S((size_t)lp * kp, 0.0);
+    for (int i = 0; i < ell; ++i)
+        for (int t = 0; t < k; ++t) S[(size_t)i * kp + t] = U[(size_t)i * ell + t] / sig[t];
+    double* Sd = e.scr.take<double>((int64_t)lp * kp);
+    double* V = e.scr.take<double>((int64_t)d * kp);
+    double* P = e.scr.take<double>((int64_t)std::max(m, 1) * kp);
+    CK(cudaMemcpyAsync(Sd, S.data(), S.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    gemm_nn(e.W, d, lp, lp, Sd, kp, kp, V, kp, st);  // V_k = B^T U / s  (d x kp)
+    spmm(e.a.row_ptr, (const int*)e.a.col, e.a.val, m, e.plan_r, e.a.nnz, V, kp, kp, P, kp, e.scr, st);  // A V_k
+    double* pe = e.d_scal + 7;
+    sumsq(P, m, kp, kp, pe, nullptr, 0, e.scr, st);
+    const double proj = e.read_scalar(pe);
+    *out = std::max(a_fsq - proj, 0.0) / tail_sq;
+    return true;
+}
+
 // exact_tail (core/src/bench.cpp:68-137): |A - A_k|_F^2 by block power iteration with block
 // = k + 10 columns (the engine's ell), <= 1000 sweeps, the reference's convergence tests on
 // the top-k Ritz values of W^T W (W = A^T Y). A (whole stream) is held by e (load_csr with

@@ -724,3 +724,16 @@ def test_exact_tail_device_vs_oracle(oracle):
     fsq = float((vs ** 2).sum())
     tail7, _, _, _ = P.exact_tail((rp, cs, vs), 1000, 7, P.RngState(9))
     assert ce * fsq <= tail7 / (KALPHA * 50 - 7)  # k = 7 < alpha ell = 7.3
+
+
+def test_proj_err_device_vs_oracle(oracle):
+    """Device proj_err (svd_top of the sketch, V_k by GEMM, |A V_k|_F^2 by one SpMM) against the
+    oracle for k = 1, 7, 10, and the nullopt case."""
+    rp, cs, vs = S.generate("c1", (0, 3000))
+    b, _ = sketch_gpu(rp, cs, vs, 1000, 50, 0)
+    for k in (1, 7, 10):
+        t, _, _ = oracle.exact_tail(rp, cs, vs, 1000, k, oracle.rng(9))
+        got = P.proj_err((rp, cs, vs), 1000, b, k, t)
+        want = oracle.proj_err(rp, cs, vs, 1000, b, k, t)
+        assert got is not None and abs(got - want) <= 1e-9 * want
+    assert P.proj_err((rp, cs, vs), 1000, b, 5, 1e-30) is None

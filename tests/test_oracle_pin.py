@@ -207,3 +207,15 @@ def test_exact_tail_oracle_matches_reference(oracle, reference):
         t1, s1, _ = oracle.exact_tail(rp, cs, vs, 1000, k, oracle.rng(9))
         t2, s2 = reference.exact_tail(rp, cs, vs, 1000, k, reference.rng(9))
         assert t1 == t2 and np.array_equal(s1, s2)
+
+
+def test_proj_err_oracle_matches_reference(oracle, reference):
+    """proj_err restatement (bench.cpp:139-169) bit-exact against the reference, including
+    the nullopt case (tail below 1e-12 |A|_F^2)."""
+    from paper_1602_00412_b200 import synthetic as S
+    rp, cs, vs = S.generate("c1", (0, 1500))
+    b, _ = oracle.sketch(rp, cs, vs, 1000, 50, seed=0)
+    for k in (1, 7, 10):
+        t, _, _ = oracle.exact_tail(rp, cs, vs, 1000, k, oracle.rng(9))
+        assert oracle.proj_err(rp, cs, vs, 1000, b, k, t) == reference.proj_err(rp, cs, vs, 1000, b, k, t)
+    assert oracle.proj_err(rp, cs, vs, 1000, b, 5, 1e-30) is None
