@@ -438,6 +438,8 @@ class Sketcher {
         uint64_t id = 0;
         FlushState start, cur;
         int interval = 1, interval_base = 1, interval_used = 1;
+        bool checked = false, checked_base = false;  // Engine::exact_check for the attempt / flush start
+        bool uncertain_seen = false;                 // a checked attempt met uncertain drops
         RngPos pos0;
         size_t attempt = 0;
         double delta_hat = 0.0, kappa_last = 0.0;
@@ -466,6 +468,7 @@ class Sketcher {
         double kappa_last = 0.0;
         int last_since = 1;
         bool valid = false;
+        bool checked = false;  // the flush needed exact drop decisions: start checked
     };
 
     // Flushes in flight: 4, or fewer when 4 lanes' working sets (CSR + CSC of ell*d nnz,
@@ -598,6 +601,8 @@ class Sketcher {
         L.cur = st;
         L.attempt = 0;
         L.interval = L.interval_base;
+        L.checked = L.checked_base;
+        L.uncertain_seen = false;
         CK(cudaMemsetAsync(L.eng->d_err, 0, sizeof(int), L.eng->st));
         enqueue_attempt(L);
     }
@@ -605,6 +610,7 @@ class Sketcher {
     void enqueue_attempt(Lane& L) {
         if (++L.attempt > kRetryCap) throw numerical_error("boosted_sparse_shrink: retry cap exceeded");
         L.pos0 = L.cur.pos;
+        if (L.checked) L.interval = 1;
         L.interval_used = L.eng->adaptive ? L.interval : 1;
         const bool wait_bp = L.bp_pending;  // the chain's dense shrink of this lane's previous B'
         L.bp_pending = false;
@@ -612,6 +618,7 @@ class Sketcher {
         run(L, [this, &L, wait_bp] {
             Engine& e = *L.eng;
             e.orth_interval = L.interval_used;
+            e.exact_check = L.checked;
             e.pos = L.cur.pos;
             e.scr.reset();
             if (wait_bp) CK(cudaStreamWaitEvent(e.st, L.ev_bp_free, 0));
@@ -646,6 +653,7 @@ class Sketcher {
                 const Hist& h = hist[L.id % lag];
                 L.interval_base =
                     (L.id >= lag && h.valid) ? next_orth_interval(h.kappa_last, h.last_since) : kFirstInterval;
+                L.checked_base = L.id >= lag && h.valid && h.checked;
                 const FlushState st = idx_in_flight == 0 ? committed : predicted_end(lanes[inflight[idx_in_flight - 1]]);
                 start_flush(L, st);
                 break;
@@ -654,15 +662,20 @@ class Sketcher {
                 const double b_fsq = e.h_scal[1];
                 const double kappa_last = e.h_scal[16 + 3], kappa_max = e.h_scal[16 + 5];
                 const int err = e.h_err[0];
-                if (L.interval_used > 1 && (kappa_max > kKappaUnsafe || (err & ERR_NONFINITE_ITER))) {
-                    // redo from the same draws with the every-sweep schedule (as Engine::boosted)
+                const double uncertain = e.h_scal[16 + 7] + e.h_scal[24 + 7];
+                if (!L.checked && (uncertain > 0.0 || (L.interval_used > 1 && (kappa_max > kKappaUnsafe ||
+                                                                                 (err & ERR_NONFINITE_ITER))))) {
+                    // redo from the same draws with the every-sweep schedule and exact drop
+                    // decisions (as Engine::boosted)
                     CK(cudaMemsetAsync(e.d_err, 0, sizeof(int), e.st));
                     L.cur.pos = L.pos0;
                     L.interval = 1;
+                    L.checked = true;
                     --L.attempt;
                     enqueue_attempt(L);
                     break;
                 }
+                if (L.checked && uncertain > 0.0) L.uncertain_seen = true;
                 raise_device_flags(err);
                 L.kappa_last = kappa_last;
                 L.last_since = e.last_since;
@@ -701,7 +714,7 @@ class Sketcher {
 
     void commit(Lane& L) {
         committed = L.cur;
-        if (e_adaptive(L)) hist[L.id % kLag] = Hist{L.kappa_last, L.last_since, true};
+        if (e_adaptive(L)) hist[L.id % kLag] = Hist{L.kappa_last, L.last_since, true, L.uncertain_seen};
         flushes += 1;
         attempts += L.attempt;
         Engine& C = *chain;
@@ -1347,6 +1360,7 @@ int sfdg_sparse_shrink(const int64_t* row_ptr, const uint32_t* cols, const doubl
         require_device(device);
         Engine e(device, (int)d, (int)ell, rng->seed, (uint64_t)(row_ptr[m] - row_ptr[0]), (int)m);
         rng_in(e, rng);
+        e.exact_check = true;  // the reference's orthonormalize decisions on every pass
         e.load_csr(row_ptr, cols, vals, (int)m, row_ptr[m] - row_ptr[0]);
         e.prepare();
         double* bt = e.Mt[0] + e.lp;
@@ -1395,6 +1409,7 @@ int sfdg_simultaneous_iteration(const int64_t* row_ptr, const uint32_t* cols, co
         require_device(device);
         Engine e(device, (int)d, (int)k, rng->seed, (uint64_t)(row_ptr[m] - row_ptr[0]), (int)m);
         rng_in(e, rng);
+        e.exact_check = true;
         e.load_csr(row_ptr, cols, vals, (int)m, row_ptr[m] - row_ptr[0]);
         e.prepare();
         e.simultaneous_iteration((int)k, to_power(power));
@@ -1533,6 +1548,7 @@ int sfdg_orthonormalize(const double* in, size_t n, size_t k, double* out, int d
         double* tmp = e.scr.take<double>((int64_t)n * k);
         CK(cudaMemcpyAsync(tmp, in, n * k * sizeof(double), cudaMemcpyHostToDevice, e.st));
         copy2d(tmp, (int)n, (int)k, (int)k, e.Y, e.lp, e.st);
+        e.exact_check = true;
         e.orthonormalize(e.Y, (int)n, ERR_NONFINITE_ITER);
         copy2d(e.Y, (int)n, (int)k, e.lp, tmp, (int)k, e.st);
         CK(cudaMemcpyAsync(out, tmp, n * k * sizeof(double), cudaMemcpyDeviceToHost, e.st));

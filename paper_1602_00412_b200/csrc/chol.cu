@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kCholThreads) chol_factor_kernel(const double*
                                                                    double* __restrict__ T, int ldt,
                                                                    double* __restrict__ stats, int* __restrict__ err,
                                                                    int err_bit, double* __restrict__ gscratch,
-                                                                   int use_smem, int polar) {
+                                                                   int use_smem, int polar, int* __restrict__ udrop) {
     extern __shared__ double sm[];
     const int lda = use_smem ? k + 4 : k;
     double* A = use_smem ? sm : gscratch;
@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(kCholThreads) chol_factor_kernel(const double*
             stats[3] = 1e300;
             stats[4] = 0.0;
             stats[5] = 1e300;
+            stats[6] = 0.0;
         }
+        if (udrop)
+            for (int j = tid; j < k; j += nt) udrop[j] = 0;
         return;
     }
     if (polar && s_emax <= kPolarMax) {
@@ -136,7 +139,10 @@ __global__ void __launch_bounds__(kCholThreads) chol_factor_kernel(const double*
             stats[2] = s_emax;
             stats[3] = 1.0;
             stats[4] = 1.0;
+            stats[6] = 0.0;
         }
+        if (udrop)
+            for (int j = tid; j < k; j += nt) udrop[j] = 0;
         return;
     }
 
@@ -288,6 +294,23 @@ __global__ void __launch_bounds__(kCholThreads) chol_factor_kernel(const double*
         stats[3] = rmin > 0.0 && rmin < 1e300 ? rmax / rmin : 1.0;
         stats[4] = 0.0;
         stats[5] = fmax(stats[5], stats[3]);  // running max over the calls sharing `stats`
+    }
+    // Uncertain drops: columns of non-negligible norm dropped by the relative pivot test
+    // alone. The Gram cannot tell whether their residual is above the reference's absolute
+    // threshold (exact_orth_kernel can); udrop[j] marks them, stats[6] counts them and
+    // stats[7] accumulates the count over the calls sharing `stats`.
+    if (warp == 0) {
+        int cnt = 0;
+        for (int j = lane; j < k; j += 32) {
+            const int u = s_drop[j] && d0[j] > s_thr;
+            if (udrop) udrop[j] = u;
+            cnt += u;
+        }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0) {
+            stats[6] = (double)cnt;
+            stats[7] += (double)cnt;
+        }
     }
 }
 
@@ -467,10 +490,163 @@ __global__ void __launch_bounds__(kTrsmThreads) trsm_panel_kernel(const double* 
     }
 }
 
+
+// ---- exact_orth_kernel: the reference's Gram-Schmidt decisions (la_core.cpp:130-165)
+// One 8-CTA cluster; CTA r owns rows [r * chunk, (r + 1) * chunk). Column reductions go
+// through the CTAs' shared memory: each CTA writes its partial vector, a cluster barrier,
+// then every CTA sums the 8 partials in rank order (identical totals everywhere).
+// Per column j: sweep A (h = Q_<j^T t), sweep B (t -= Q_<j h, h2 = Q_<j^T t), sweep C
+// (t -= Q_<j h2, |t|^2): classical Gram-Schmidt twice, accurate to O(u |t|) like the
+// reference's re-orthogonalised MGS.
+constexpr int kXC = 8;
+constexpr int kXThreads = 512;
+constexpr int kXWarps = kXThreads / 32;
+constexpr int kXMaxK = 256;
+
+__global__ void __cluster_dims__(kXC, 1, 1) __launch_bounds__(kXThreads)
+    exact_orth_kernel(const double* __restrict__ Y, int ldy, double* __restrict__ Q, int ldq, int m, int k,
+                      const int* __restrict__ udrop, const double* __restrict__ stats, double* __restrict__ tmp,
+                      int force) {
+    if (!force && !(stats[6] > 0.0)) return;  // uniform over the cluster
+    __shared__ double wred[kXWarps][kXMaxK];
+    __shared__ double part[2][kXMaxK];
+    __shared__ double h[kXMaxK];
+    const unsigned rank = cluster_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int chunk = (m + kXC - 1) / kXC;
+    const int r0 = min(m, (int)rank * chunk), r1 = min(m, r0 + chunk);
+    int pb = 0;
+
+    // per-lane column accumulators acc[c] <-> column 32 c + lane  ->  h[0, n) (cluster totals)
+    auto reduce = [&](const double* acc, int n) {
+        const int nc = (n + 31) / 32;
+        for (int c = 0; c < nc; ++c)
+            if (32 * c + lane < n) wred[warp][32 * c + lane] = acc[c];
+        __syncthreads();
+        for (int p = tid; p < n; p += kXThreads) {
+            double v = 0.0;
+            for (int w = 0; w < kXWarps; ++w) v += wred[w][p];
+            part[pb][p] = v;
+        }
+        cluster_barrier();
+        for (int p = tid; p < n; p += kXThreads) {
+            double v = 0.0;
+            for (unsigned r = 0; r < kXC; ++r) v += cluster_map(&part[pb][0], r)[p];
+            h[p] = v;
+        }
+        pb ^= 1;
+        __syncthreads();
+    };
+    // (sum_p<j h_p Q_ip) for row i, lanes over p; every lane gets the total
+    auto hq = [&](int i, int j) {
+        double s = 0.0;
+        for (int p = lane; p < j; p += 32) s += h[p] * Q[(size_t)i * ldq + p];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        return s;
+    };
+    // residual of target column t (t(i) = tgt[i * ts]) against Q_<j; returns |t|
+    auto residual = [&](double* tgt, size_t ts, int j) {
+        double acc[kXMaxK / 32];
+        const int nc = (j + 31) / 32;
+        if (j > 0) {
+            for (int c = 0; c < kXMaxK / 32; ++c) acc[c] = 0.0;
+            for (int i = r0 + warp; i < r1; i += kXWarps) {  // sweep A
+                const double t = tgt[(size_t)i * ts];
+                for (int c = 0; c < nc; ++c) {
+                    const int p = 32 * c + lane;
+                    if (p < j) acc[c] += Q[(size_t)i * ldq + p] * t;
+                }
+            }
+            reduce(acc, j);
+            for (int c = 0; c < kXMaxK / 32; ++c) acc[c] = 0.0;
+            for (int i = r0 + warp; i < r1; i += kXWarps) {  // sweep B
+                const double t = tgt[(size_t)i * ts] - hq(i, j);
+                __syncwarp();
+                if (lane == 0) tgt[(size_t)i * ts] = t;
+                for (int c = 0; c < nc; ++c) {
+                    const int p = 32 * c + lane;
+                    if (p < j) acc[c] += Q[(size_t)i * ldq + p] * t;
+                }
+            }
+            reduce(acc, j);
+        }
+        double nrm = 0.0;
+        for (int i = r0 + warp; i < r1; i += kXWarps) {  // sweep C
+            const double t = j > 0 ? tgt[(size_t)i * ts] - hq(i, j) : tgt[(size_t)i * ts];
+            __syncwarp();
+            if (lane == 0) {
+                tgt[(size_t)i * ts] = t;
+                nrm += t * t;
+            }
+        }
+        for (int c = 0; c < kXMaxK / 32; ++c) acc[c] = 0.0;
+        acc[0] = nrm;  // lane 0 of each warp carries the warp's share
+        reduce(acc, 1);
+        return sqrt(h[0]);
+    };
+
+    // drop_tol = 1e-12 * max_j |y_j| over the input columns (la_core.cpp:135-141)
+    {
+        double acc[kXMaxK / 32];
+        for (int c = 0; c < kXMaxK / 32; ++c) acc[c] = 0.0;
+        const int nc = (k + 31) / 32;
+        for (int i = r0 + warp; i < r1; i += kXWarps)
+            for (int c = 0; c < nc; ++c) {
+                const int p = 32 * c + lane;
+                if (p < k) {
+                    const double v = Y[(size_t)i * ldy + p];
+                    acc[c] += v * v;
+                }
+            }
+        reduce(acc, k);
+    }
+    __shared__ double s_tol;
+    __shared__ int s_redo;
+    if (tid == 0) {
+        double mx = 0.0;
+        for (int p = 0; p < k; ++p) mx = fmax(mx, h[p]);
+        s_tol = 1e-12 * sqrt(mx);
+        s_redo = force;
+    }
+    __syncthreads();
+    const double tol = s_tol;
+
+    // confirm CholeskyQR's uncertain drops against the threshold
+    if (!s_redo)
+        for (int j = 0; j < k; ++j) {
+            if (!udrop[j]) continue;
+            for (int i = r0 + tid; i < r1; i += kXThreads) tmp[i] = Y[(size_t)i * ldy + j];
+            __syncthreads();
+            const double nrm = residual(tmp, 1, j);
+            if (!(nrm < tol || nrm == 0.0)) {  // the reference keeps column j
+                if (tid == 0) s_redo = 1;
+                __syncthreads();
+                break;
+            }
+        }
+    __syncthreads();
+    if (s_redo) {
+        // Gram-Schmidt with re-orthogonalisation on a copy of Y (la_core.cpp:143-163)
+        for (int i = r0 + warp; i < r1; i += kXWarps)
+            for (int p = lane; p < k; p += 32) Q[(size_t)i * ldq + p] = Y[(size_t)i * ldy + p];
+        __syncthreads();
+        for (int j = 0; j < k; ++j) {
+            const double nrm = residual(Q + j, (size_t)ldq, j);
+            const bool keep = !(nrm < tol || nrm == 0.0);
+            const double inv = keep ? 1.0 / nrm : 0.0;
+            for (int i = r0 + tid; i < r1; i += kXThreads) {
+                double* q = Q + (size_t)i * ldq + j;
+                *q = keep ? *q * inv : 0.0;
+            }
+            __syncthreads();
+        }
+    }
+    cluster_barrier();  // no CTA leaves while a peer may still read its partials
+}
 }  // namespace
 
 void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, double* T, int ldt, double* stats,
-                 int* d_err, int err_bit, Scratch& scr, cudaStream_t st, bool polar) {
+                 int* d_err, int err_bit, Scratch& scr, cudaStream_t st, bool polar, int* udrop) {
     if (k <= 0) return;
     if (k > 512) throw invalid_argument("chol_factor: k > 512 unsupported");
     ProfScope prof(polar ? "chol_polar" : "chol", st);
@@ -490,7 +666,7 @@ void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, doub
         attr_set = true;
     }
     LAUNCH(chol_factor_kernel, 1, kCholThreads, smem, st, G, k, ldg, R, dinv8, T, ldt, stats, d_err, err_bit, gscr,
-           use_smem ? 1 : 0, polar ? 1 : 0);
+           use_smem ? 1 : 0, polar ? 1 : 0, udrop);
 }
 
 void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const double* dinv8, double* X, int ldx,
@@ -520,6 +696,14 @@ void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const do
     while (rows > 16 && bytes(rows) > 220 * 1024) rows /= 2;
     LAUNCH(trsm_apply_kernel, ceil_div(m, rows), kTrsmThreads, bytes(rows), st, Y, m, k, ld, R, dinv8, X, ldx, stats,
            rows);
+}
+
+void exact_orth(const double* Y, int ldy, double* Q, int ldq, int m, int k, const int* udrop, const double* stats,
+                double* tmp, cudaStream_t st, bool force) {
+    if (m <= 0 || k <= 0) return;
+    if (k > kXMaxK) throw invalid_argument("exact_orth: k > 256 unsupported");
+    ProfScope prof("exact_orth", st);
+    LAUNCH(exact_orth_kernel, kXC, kXThreads, 0, st, Y, ldy, Q, ldq, m, k, udrop, stats, tmp, force ? 1 : 0);
 }
 
 }  // namespace sfdg

@@ -33,6 +33,26 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 }
 #define CK(x) ::sfdg::cuda_check((x), #x, __FILE__, __LINE__)
 
+#ifdef __CUDACC__
+// Thread-block cluster helpers (sm_90+): rank in the cluster, a full cluster barrier with
+// release/acquire semantics for shared::cluster accesses, and the DSMEM address of `p` in
+// the CTA of cluster rank `rank`.
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <class T>
+__device__ __forceinline__ T* cluster_map(T* p, unsigned rank) {
+    unsigned long long out;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(p), "r"(rank));
+    return reinterpret_cast<T*>(out);
+}
+#endif
+
 // Every kernel launch goes through LAUNCH so the process-wide launch counter
 // (sfdg_launch_count) is exact and launch errors surface immediately.
 extern std::atomic<uint64_t> g_launches;

@@ -193,21 +193,6 @@ struct TriRowsArgs {
     int rows;   // ceil(n / C): local rows per CTA
 };
 
-__device__ __forceinline__ unsigned cluster_rank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_barrier() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-template <class T>
-__device__ __forceinline__ T* cluster_map(T* p, unsigned rank) {
-    unsigned long long out;
-    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(p), "r"(rank));
-    return reinterpret_cast<T*>(out);
-}
-
 template <int C, int NT, int NTHR>
 __global__ void __launch_bounds__(NTHR) tridiag_rows_kernel(TriRowsArgs ra) {
     constexpr int NW = NTHR / 32;

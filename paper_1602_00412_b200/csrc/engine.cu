@@ -198,6 +198,7 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     CK(cudaMalloc(&vpart, (size_t)verify_blocks * sizeof(double)));
     CK(cudaMalloc(&vout, 4 * sizeof(double)));
     CK(cudaMalloc(&bar, 2 * sizeof(unsigned)));
+    CK(cudaMalloc(&d_udrop, 512 * sizeof(int)));
     CK(cudaMalloc(&d_err, 4 * sizeof(int)));
     CK(cudaMemsetAsync(d_err, 0, 4 * sizeof(int), st));
     CK(cudaMalloc(&d_scal, 64 * sizeof(double)));
@@ -217,7 +218,7 @@ Engine::~Engine() {
                     (void*)rfac,
                     (void*)dinv8, (void*)kc,
                     (void*)evals, (void*)evecs, (void*)S, (void*)x0, (void*)ybuf, (void*)u, (void*)tpart, (void*)tvec,
-                    (void*)vpart, (void*)vout, (void*)bar, (void*)d_err, (void*)d_scal})
+                    (void*)vpart, (void*)vout, (void*)bar, (void*)d_err, (void*)d_scal, (void*)xtmp, (void*)d_udrop})
         if (p) cudaFree(p);
     if (h_scal) cudaFreeHost(h_scal);
     if (h_err) cudaFreeHost(h_err);
@@ -245,8 +246,10 @@ void Engine::ensure_rows(int m) {
         if (*p) cudaFree(*p);
         CK(cudaMalloc(p, (size_t)m_cap * lp * sizeof(double)));
     }
-    if (u) cudaFree(u);
-    CK(cudaMalloc(&u, (size_t)m_cap * sizeof(double)));
+    for (double** p : {&u, &xtmp}) {
+        if (*p) cudaFree(*p);
+        CK(cudaMalloc(p, (size_t)m_cap * sizeof(double)));
+    }
 }
 
 void Engine::sync() {
@@ -310,8 +313,10 @@ void Engine::orthonormalize(double* Yp, int m, int err_bit) {
     double* st1 = d_scal + 16;
     double* st2 = d_scal + 24;
     gram_tn(Yp, m, lp, lp, gram, lp, scr, st);
-    chol_factor(gram, lp, lp, rfac, dinv8, nullptr, 0, st1, d_err, err_bit, scr, st, false);
+    chol_factor(gram, lp, lp, rfac, dinv8, nullptr, 0, st1, d_err, err_bit, scr, st, false,
+                exact_check ? d_udrop : nullptr);
     trsm_apply(Yp, m, lp, lp, rfac, dinv8, Yt, lp, nullptr, st);
+    if (exact_check) exact_orth(Yp, lp, Yt, lp, m, lp, d_udrop, st1, xtmp, st);
     gram_tn(Yt, m, lp, lp, gram, lp, scr, st);
     chol_factor(gram, lp, lp, rfac, dinv8, rinv, lp, st2, d_err, err_bit, scr, st, true);
     trsm_apply(Yt, m, lp, lp, rfac, dinv8, Yp, lp, st2, st);
@@ -325,8 +330,10 @@ void Engine::orthonormalize_light(int m, int err_bit) {
     // O(kappa^2 eps) with its span unchanged. The last pass is always the full CholeskyQR2.
     double* st1 = d_scal + 16;
     gram_tn(Y, m, lp, lp, gram, lp, scr, st);
-    chol_factor(gram, lp, lp, rfac, dinv8, nullptr, 0, st1, d_err, err_bit, scr, st, false);
+    chol_factor(gram, lp, lp, rfac, dinv8, nullptr, 0, st1, d_err, err_bit, scr, st, false,
+                exact_check ? d_udrop : nullptr);
     trsm_apply(Y, m, lp, lp, rfac, dinv8, Yt, lp, nullptr, st);
+    if (exact_check) exact_orth(Y, lp, Yt, lp, m, lp, d_udrop, st1, xtmp, st);
     std::swap(Y, Yt);
 }
 
@@ -387,7 +394,7 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     const int interval = adaptive ? orth_interval : 1;
     // whole blocks (interval sweeps closed by a light pass) replay as a CUDA graph when no
     // long-row piece kernels are involved and profiling (per-launch events) is off
-    const bool graphs_ok = use_graphs && adaptive && plan_r.host_long == 0 && plan_c.host_long == 0 &&
+    const bool graphs_ok = use_graphs && adaptive && !exact_check && plan_r.host_long == 0 && plan_c.host_long == 0 &&
                            !g_prof_on.load(std::memory_order_relaxed);
     int since = 0;
     for (size_t s = 0; s < q;) {
@@ -492,7 +499,7 @@ void Engine::attempt_enqueue(const PowerCfg& cfg, double* bpt, int ldb) {
     double* bfsq = d_scal + 1;
     sumsq(bpt, d, ell, ldb, bfsq, nullptr, 0, scr, st);
     CK(cudaMemcpyAsync(h_scal + 1, bfsq, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_scal + 16, d_scal + 16, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_scal + 16, d_scal + 16, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
 }
 
@@ -500,8 +507,10 @@ size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* d
     if (ell < 1 || ell > a.m) throw invalid_argument("boosted_sparse_shrink: ell out of range");
     double* bpt = Mt[cur] + lp;  // right half of [B^T | B'^T]
     const int ldb = 2 * lp;
+    exact_check = false;
     for (size_t attempt = 1; attempt <= kRetryCap; ++attempt) {
         const RngPos pos0 = pos;
+        if (exact_check) orth_interval = 1;
         const int interval_used = adaptive ? orth_interval : 1;
         attempt_enqueue(cfg, bpt, ldb);
         // prefetch the next attempt's draws while we wait (side stream)
@@ -509,12 +518,16 @@ size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* d
         CK(cudaStreamSynchronize(st));
         const double b_fsq = h_scal[1];
         const double kappa_last = h_scal[16 + 3], kappa_max = h_scal[16 + 5];
-        if (interval_used > 1 && (kappa_max > kKappaUnsafe || (h_err[0] & ERR_NONFINITE_ITER))) {
-            // the skipped-orthonormalisation schedule lost too much conditioning: redo this
-            // attempt from the same draws with the reference's every-sweep schedule
+        const double uncertain = h_scal[16 + 7] + h_scal[24 + 7];
+        if (!exact_check && (uncertain > 0.0 || (interval_used > 1 && (kappa_max > kKappaUnsafe ||
+                                                                        (h_err[0] & ERR_NONFINITE_ITER))))) {
+            // the skipped-orthonormalisation schedule lost too much conditioning, or CholeskyQR
+            // dropped a column it cannot vouch for: redo this attempt from the same draws with
+            // the reference's every-sweep schedule and exact drop decisions
             CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
             pos = pos0;
             orth_interval = 1;
+            exact_check = true;
             --attempt;
             continue;
         }

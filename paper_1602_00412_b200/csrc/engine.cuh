@@ -82,6 +82,8 @@ class Engine {
     double *gram = nullptr, *rinv = nullptr, *rfac = nullptr, *dinv8 = nullptr, *kc = nullptr, *evals = nullptr, *evecs = nullptr, *S = nullptr;
     double *x0 = nullptr, *ybuf = nullptr, *u = nullptr, *tpart = nullptr, *tvec = nullptr, *vpart = nullptr;
     double* vout = nullptr;
+    double* xtmp = nullptr;  // m_cap: exact_orth's residual column
+    int* d_udrop = nullptr;  // 512: CholeskyQR's uncertain drops
     unsigned* bar = nullptr;
     int* d_err = nullptr;
     double* d_scal = nullptr;  // device scalars
@@ -92,6 +94,10 @@ class Engine {
     bool adaptive = true;   // SFDG_ORTH_EVERY_SWEEP=1 forces the reference schedule
     int orth_interval = 1;  // sweeps per CholeskyQR2
     int last_since = 1;     // sweeps folded into the last pass-1 factorisation
+    // Every pass-1 factorisation followed by exact_orth (chol.cu): CholeskyQR's uncertain
+    // column drops re-decided by the reference's rule. Set for attempts replayed after an
+    // uncertain drop (with orth_interval = 1, the reference's schedule).
+    bool exact_check = false;
 
     void set_device() const;
     void ensure_rows(int m);

@@ -248,6 +248,7 @@ void device_exact_tail(Engine& e, int k, double a_fsq, double* sigma_out, double
     }
     const int m = e.a.m, d = e.d, lp = e.lp, block = e.ell;
     cudaStream_t st = e.st;
+    e.exact_check = true;  // the reference's orthonormalize decisions (rank-deficient blocks)
     e.scr.reset();
     e.rng->normals(e.pos, (uint64_t)d * block, (uint64_t)block, (uint64_t)lp, e.W, e.d_err, st);  // la_core.cpp:167
     spmm(e.a.row_ptr, (const int*)e.a.col, e.a.val, m, e.plan_r, e.a.nnz, e.W, lp, lp, e.Y, lp, e.scr, st);

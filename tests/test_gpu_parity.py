@@ -180,6 +180,61 @@ def test_orthonormalize_drops_dependent_columns(oracle):
     assert np.max(np.abs(q @ q.T - qo @ qo.T)) <= 1e-12
 
 
+def test_orthonormalize_nearly_dependent_column_kept(oracle):
+    """A column whose residual is 1e-9 of its norm: above the reference's absolute threshold
+    (1e-12 max |y_j|, la_core.cpp:141,158) so MGS keeps it, but below what a Gram-based
+    pivot can resolve -- CholeskyQR marks it uncertain and exact_orth keeps it."""
+    rng = np.random.default_rng(8)
+    base = rng.standard_normal((60, 4))
+    a = np.column_stack([base[:, 0], base[:, 1], base[:, 0] - base[:, 1] + 1e-9 * base[:, 2], base[:, 3],
+                         base[:, 0] + base[:, 3]])
+    q = P.orthonormalize(a)
+    qo = oracle.orthonormalize(a)
+    assert np.array_equal(np.abs(q).sum(axis=0) == 0, np.abs(qo).sum(axis=0) == 0)
+    assert np.abs(q[:, 2]).sum() > 0 and np.abs(q[:, 4]).sum() == 0
+    assert np.max(np.abs(q @ q.T - qo @ qo.T)) <= 1e-6  # column 2 carries u / 1e-9 in both
+
+
+def test_simultaneous_iteration_near_rank_deficient(oracle):
+    """A buffer whose 4th singular value is 1e-7 of the top: the first orthonormalisation
+    (Y = A G) leaves that column a residual CholeskyQR cannot resolve (uncertain; the
+    reference keeps it), the first sweep then drops it in both (lambda ratio 1e-14 <
+    1e-12): the same zero column and span as the reference."""
+    g = np.random.default_rng(4)
+    u = np.linalg.qr(g.standard_normal((30, 4)))[0]
+    v = np.linalg.qr(g.standard_normal((12, 4)))[0]
+    a = (u * np.array([3.0, 2.0, 1.5, 3e-7])) @ v.T
+    rp = np.arange(0, 30 * 12 + 1, 12, dtype=np.int64)
+    cs = np.tile(np.arange(12, dtype=np.uint32), 30)
+    csr = (rp, cs, a.ravel())
+    z, _ = P.simultaneous_iteration(csr, 12, 4, oracle.rng(2))
+    zo = oracle.simultaneous_iteration(csr, 12, 4, oracle.rng(2))
+    assert np.array_equal(np.abs(z).sum(axis=0) == 0, np.abs(zo).sum(axis=0) == 0)
+    assert np.max(np.abs(z @ z.T - zo @ zo.T)) <= 1e-6
+
+
+def test_widely_spread_spectrum_stream_vs_oracle(oracle):
+    """+-1 rows with two nonzeros (the CLI generator, n 1000, d 100, z 2, seed 2): per-flush
+    spectra with lambda_4 / lambda_1 ~ 0.03. Skipping orthonormalisations let CholeskyQR drop
+    columns 4-5 that the reference keeps; the uncertain drop now replays the attempt with the
+    every-sweep schedule and exact decisions."""
+    import subprocess
+    import tempfile
+    exe = os.path.join(os.path.dirname(__file__), "..", "tools", "sfdg")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", os.path.join(os.path.dirname(__file__), "..", "tools"), "sfdg"], check=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        mtx = os.path.join(tmp, "a.mtx")
+        subprocess.run([exe, "generate", "--n", "1000", "--d", "100", "--z", "2", "--seed", "2", "--output", mtx],
+                       check=True)
+        rp, cs, vs, d = P.read_row_stream(mtx)
+    b, st = sketch_gpu(rp, cs, vs, d, 5, 2)
+    bo, so = oracle.sketch(rp, cs, vs, d, 5, seed=2)
+    assert btb_rel(b, bo) <= BTB_TOL
+    for key in ("flushes", "attempts", "verifier_i", "delta_spent"):
+        assert st[key] == so[key], key
+
+
 # ---------------------------------------------------------------- shrinks
 def test_dense_shrink_kat():
     b = P.dense_shrink(GOLD["kat_dense_a"], 2)
@@ -668,8 +723,8 @@ def test_cli_sketch_csv_manifest_and_determinism(oracle, tmp_path):
     bad = str(tmp_path / "bad.mtx")
     with open(bad, "w") as f:
         f.write("%%MatrixMarket matrix coordinate real general\n2 3 1\n1 9 1.0\n")
-    r = subprocess.run([exe, "sketch", "--input", bad, "--output", str(tmp_path / "x.csv")], capture_output=True,
-                       text=True)
+    r = subprocess.run([exe, "sketch", "--input", bad, "--output", str(tmp_path / "x.csv"), "--ell", "2"],
+                       capture_output=True, text=True)
     assert r.returncode == 1 and "out of range" in r.stderr
 
 

@@ -1,16 +1,34 @@
-// sfdg_main.cpp -- `sfdg sketch`: the reference CLI's sketch command (tools/sfd_main.cpp:38-88)
-// over the device library. Reads a MatrixMarket or plain "col:value"
-// file (--cols for plain), sketches it with SFD (or the dense FD baseline), writes the
-// sketch as CSV with 17 significant digits (io.cpp:232-245) and a JSON manifest next to it
-// (io.cpp:296-301). Exit codes follow tools/sfd_main.cpp:289-298: 1 = invalid argument,
-// 2 = numerical error (3 = device fault).
+// sfdg_main.cpp -- the reference CLI (tools/sfd_main.cpp) over the device library
+// (SURVEY 8(f) rank 4). Four commands, same options, outputs and exit codes:
 //
-//   sfdg sketch --input A.mtx --output B.csv [--algo sfd|fd] [--ell 50] [--delta 0.1]
-//               [--seed 0] [--epsilon 0.25] [--q-const 1] [--fast-q] [--q-override N]
-//               [--cols d] [--device 0]
+//   sfdg sketch   --input A --output B.csv --ell N [--algo sfd|fd] [--delta X] [--seed N]
+//                 [--epsilon X] [--q-const X] [--fast-q] [--q-override N] [--cols D]
+//                 (sfd_main.cpp:38-88): SFD or the dense FD baseline over a MatrixMarket or
+//                 plain "col:value" file; sketch CSV with 17 significant digits (io.cpp:232-245)
+//   sfdg generate --output A.mtx [--n 10000] [--d 1000] [--z 100] [--seed 0]
+//                 (sfd_main.cpp:90-111): the synthetic +-1 head/tail row stream
+//                 (bench.cpp:13-66), MatrixMarket with %.17g values (io.cpp:191-230)
+//   sfdg eval     --matrix A --sketch B.csv --output M.csv [--k 10] [--cols D] [--seed 0]
+//                 (sfd_main.cpp:123-155): exact_tail -> proj_err -> cov_err with one Rng,
+//                 all three on the device; metrics CSV (io.cpp:265-292)
+//   sfdg bench    --sweep n|d|ell|nnz --out-csv M.csv [--scale X] [--seed N] [--fast-q]
+//                 (sfd_main.cpp:157-228, timed_run bench.cpp:185-237): fd vs sfd per cell,
+//                 wall-clock seconds of the sketch, metrics untimed
+//
+// Every command also takes --device N. Each writes <output>.manifest.json (io.cpp:296-301)
+// with the reference's keys, formatted like nlohmann::json::dump(2) (keys sorted, shortest
+// round-trip doubles). Exit codes (sfd_main.cpp:285-298): 0 ok, 1 invalid argument / usage,
+// 2 numerical failure, 3 device fault (no reference counterpart).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <random>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -18,48 +36,114 @@
 
 namespace {
 
-struct Args {
-    std::string input, output, algo = "sfd";
-    size_t ell = 50;
-    double delta = 0.1;
-    unsigned long long seed = 0;
-    double epsilon = 0.25, q_const = 1.0;
-    bool fast_q = false;
-    long long q_override = -1, cols = -1;
-    int device = 0;
+const char* kUsage =
+    "usage: sfdg <command> [options]\n"
+    "  sketch   --input FILE --output CSV --ell N [--algo sfd|fd] [--delta X] [--seed N]\n"
+    "           [--epsilon X] [--q-const X] [--fast-q] [--q-override N] [--cols D]\n"
+    "  generate --output MTX [--n N] [--d D] [--z Z] [--seed N]\n"
+    "  eval     --matrix FILE --sketch CSV --output CSV [--k K] [--cols D] [--seed N]\n"
+    "  bench    --sweep n|d|ell|nnz --out-csv CSV [--scale X] [--seed N] [--fast-q]\n"
+    "  (every command: [--device N])\n";
+
+// Failure classes of the reference CLI's catch blocks (sfd_main.cpp:285-298).
+struct Usage : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct Invalid : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct Lib {
+    int code;
 };
 
-int usage(const char* msg) {
-    std::fprintf(stderr, "sfdg: %s\nusage: sfdg sketch --input FILE --output CSV [--algo sfd|fd] [--ell N] "
-                         "[--delta X] [--seed N] [--epsilon X] [--q-const X] [--fast-q] [--q-override N] "
-                         "[--cols D] [--device N]\n", msg);
-    return 1;
+void check(int rc) {
+    if (rc != SFDG_OK) throw Lib{rc};
 }
 
-int fail(int code) {
-    std::fprintf(stderr, "sfdg: %s\n", sfdg_last_error());
-    return code;
-}
+// ---------------------------------------------------------------- options
+struct Opts {
+    std::map<std::string, std::string> kv;
+    std::map<std::string, bool> flags;
 
-void write_csv(const std::string& path, const std::vector<double>& b, size_t rows, size_t cols) {
-    FILE* f = std::fopen(path.c_str(), "w");
-    if (!f) throw 1;
-    char buf[64];
-    for (size_t i = 0; i < rows; ++i) {
-        for (size_t j = 0; j < cols; ++j) {
-            std::snprintf(buf, sizeof buf, "%.17g", b[i * cols + j]);
-            std::fputs(buf, f);
-            if (j + 1 < cols) std::fputc(',', f);
-        }
-        std::fputc('\n', f);
+    bool has(const char* k) const { return kv.count(k) != 0; }
+    std::string str(const char* k, const std::string& dflt = "") const {
+        auto it = kv.find(k);
+        return it == kv.end() ? dflt : it->second;
     }
-    std::fclose(f);
+    std::string req(const char* k) const {
+        if (!has(k)) throw Usage(std::string(k) + " is required");
+        return kv.at(k);
+    }
+    unsigned long long u64(const char* k, unsigned long long dflt) const {
+        if (!has(k)) return dflt;
+        const std::string& s = kv.at(k);
+        size_t pos = 0;
+        unsigned long long v = 0;
+        try {
+            if (!s.empty() && s[0] == '-') throw 0;
+            v = std::stoull(s, &pos);
+        } catch (...) {
+            pos = 0;
+        }
+        if (pos == 0 || pos != s.size()) throw Usage(std::string(k) + ": bad value '" + s + "'");
+        return v;
+    }
+    long long i64(const char* k, long long dflt) const {
+        if (!has(k)) return dflt;
+        const std::string& s = kv.at(k);
+        size_t pos = 0;
+        long long v = 0;
+        try {
+            v = std::stoll(s, &pos);
+        } catch (...) {
+            pos = 0;
+        }
+        if (pos == 0 || pos != s.size()) throw Usage(std::string(k) + ": bad value '" + s + "'");
+        return v;
+    }
+    double f64(const char* k, double dflt) const {
+        if (!has(k)) return dflt;
+        const std::string& s = kv.at(k);
+        size_t pos = 0;
+        double v = 0;
+        try {
+            v = std::stod(s, &pos);
+        } catch (...) {
+            pos = 0;
+        }
+        if (pos == 0 || pos != s.size()) throw Usage(std::string(k) + ": bad value '" + s + "'");
+        return v;
+    }
+};
+
+Opts parse(int argc, char** argv, const std::vector<std::string>& valued, const std::vector<std::string>& flags) {
+    Opts o;
+    for (int i = 2; i < argc; ++i) {
+        const std::string k = argv[i];
+        if (std::find(flags.begin(), flags.end(), k) != flags.end()) {
+            o.flags[k] = true;
+        } else if (std::find(valued.begin(), valued.end(), k) != valued.end()) {
+            if (i + 1 >= argc) throw Usage(k + " requires an argument");
+            o.kv[k] = argv[++i];
+        } else {
+            throw Usage("unexpected argument " + k);
+        }
+    }
+    return o;
 }
 
+// ---------------------------------------------------------------- manifest (nlohmann dump(2) layout)
+// Shortest decimal that round-trips, with ".0" on integral values (how nlohmann prints doubles).
 std::string jnum(double v) {
     char buf[64];
-    std::snprintf(buf, sizeof buf, "%.17g", v);
-    return buf;
+    for (int p = 1; p <= 17; ++p) {
+        std::snprintf(buf, sizeof buf, "%.*g", p, v);
+        if (std::strtod(buf, nullptr) == v) break;
+    }
+    std::string s = buf;
+    if (s.find_first_of(".eE") == std::string::npos && s.find_first_of("0123456789") != std::string::npos)
+        s += ".0";
+    return s;
 }
 
 std::string jstr(const std::string& s) {
@@ -71,101 +155,512 @@ std::string jstr(const std::string& s) {
     return o + "\"";
 }
 
+// A JSON object of pre-rendered scalars and nested objects; std::map keeps the keys sorted
+// like nlohmann::json's default object type.
+struct JObj {
+    struct Entry {
+        std::string scalar;
+        std::vector<JObj> nested;  // 0 or 1 element
+    };
+    std::map<std::string, Entry> v;
+    JObj& num(const std::string& k, double x) { return v[k] = {jnum(x), {}}, *this; }
+    JObj& uint(const std::string& k, unsigned long long x) { return v[k] = {std::to_string(x), {}}, *this; }
+    JObj& str(const std::string& k, const std::string& x) { return v[k] = {jstr(x), {}}, *this; }
+    JObj& boolean(const std::string& k, bool x) { return v[k] = {x ? "true" : "false", {}}, *this; }
+    JObj& obj(const std::string& k, const JObj& o) { return v[k] = {"", {o}}, *this; }
+    std::string dump(int level = 1) const {
+        if (v.empty()) return "{}";
+        const std::string pad(2 * level, ' ');
+        std::string out = "{\n";
+        size_t i = 0;
+        for (const auto& [k, e] : v) {
+            out += pad + jstr(k) + ": " + (e.nested.empty() ? e.scalar : e.nested[0].dump(level + 1));
+            out += ++i < v.size() ? ",\n" : "\n";
+        }
+        return out + std::string(2 * (level - 1), ' ') + "}";
+    }
+};
+
+void write_manifest(const std::string& output, const JObj& m) {
+    const std::string path = output + ".manifest.json";
+    FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw Invalid(path + ": cannot open manifest output");
+    const std::string text = m.dump() + "\n";
+    std::fwrite(text.data(), 1, text.size(), f);
+    std::fclose(f);
+}
+
+JObj power_json(const sfdg_power_config& p) {
+    JObj j;
+    j.num("epsilon", p.epsilon).num("q_constant", p.q_constant);
+    if (p.q_override >= 0) j.uint("q_override", (unsigned long long)p.q_override);
+    return j;
+}
+
+// ---------------------------------------------------------------- data
+struct Csr {
+    size_t n = 0, d = 0;
+    std::vector<int64_t> rp{0};
+    std::vector<uint32_t> cols;
+    std::vector<double> vals;
+    size_t nnz() const { return cols.size(); }
+};
+
+// open_row_stream(path, plain_cols) read to the end (io.cpp:170-189), parsed by the library.
+Csr load_matrix(const std::string& path, long long plain_cols) {
+    const size_t pc = plain_cols >= 0 ? (size_t)plain_cols : 0;
+    Csr a;
+    size_t nnz = 0;
+    check(sfdg_read_row_stream(path.c_str(), pc, &a.n, &a.d, &nnz, nullptr, nullptr, nullptr));
+    a.rp.assign(a.n + 1, 0);
+    a.cols.resize(nnz);
+    a.vals.resize(nnz);
+    check(sfdg_read_row_stream(path.c_str(), pc, &a.n, &a.d, &nnz, a.rp.data(), a.cols.data(), a.vals.data()));
+    return a;
+}
+
+// The synthetic row stream of SyntheticSpec / SyntheticStream (bench.hpp:9-36,
+// bench.cpp:13-66): every row has exactly z distinct columns with +-1 values; the first
+// min(ceil(1.5 z), d) columns form the "head", drawn with probability p_head per slot. The
+// draws are sfd::Rng's fixed formulas over std::mt19937_64 (rng.hpp:12-31): uniform() =
+// (w >> 11) 2^-53, uniform_below(n) by rejection above the largest multiple of n
+// (rng.cpp:9-17). Per slot: one uniform() picks the group (a full group redirects to the
+// other), uniform_below redraws until an unused column of that group comes up, one uniform()
+// picks the sign; the row is emitted sorted by column. Same seed -> the same rows as the
+// reference, bit for bit.
+class SyntheticRows {
+  public:
+    SyntheticRows(size_t n, size_t d, size_t z, double p_head, uint64_t seed)
+        : n_(n), d_(d), z_(z), p_head_(p_head), eng_(seed) {
+        if (d == 0 || z == 0 || z > d) throw Invalid("SyntheticSpec: requires 1 <= z <= d");
+        if (!(p_head >= 0.0 && p_head <= 1.0)) throw Invalid("SyntheticSpec: p_head out of range");
+        head_ = std::min((size_t)std::ceil(1.5 * (double)z), d);
+        tail_ = d - head_;
+        stamp_.assign(d, 0);
+    }
+    bool more() const { return made_ < n_; }
+    // Appends the next row's sorted (col, value) pairs to `out`.
+    void next(std::vector<std::pair<uint32_t, double>>& out) {
+        ++made_;
+        out.clear();
+        size_t in_head = 0, in_tail = 0;
+        while (out.size() < z_) {
+            bool head = uniform() < p_head_;
+            if (tail_ == 0 || in_tail == tail_) head = true;
+            if (in_head == head_) head = false;
+            uint64_t c;
+            do c = head ? below(head_) : head_ + below(tail_);
+            while (stamp_[c] == made_);
+            stamp_[c] = made_;
+            ++(head ? in_head : in_tail);
+            out.emplace_back((uint32_t)c, uniform() < 0.5 ? 1.0 : -1.0);
+        }
+        std::sort(out.begin(), out.end(),
+                  [](const std::pair<uint32_t, double>& a, const std::pair<uint32_t, double>& b) {
+                      return a.first < b.first;
+                  });
+    }
+
+  private:
+    double uniform() { return (double)(eng_() >> 11) * 0x1.0p-53; }
+    uint64_t below(uint64_t m) {
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % m;
+        uint64_t w;
+        do w = eng_();
+        while (w >= limit);
+        return w % m;
+    }
+    size_t n_, d_, z_, head_ = 0, tail_ = 0, made_ = 0;
+    double p_head_;
+    std::mt19937_64 eng_;
+    std::vector<size_t> stamp_;  // stamp_[c] == row number: column c used in this row
+};
+
+Csr synthetic_csr(size_t n, size_t d, size_t z, uint64_t seed) {
+    SyntheticRows g(n, d, z, 0.9, seed);
+    Csr a;
+    a.n = n;
+    a.d = d;
+    a.cols.reserve(n * z);
+    a.vals.reserve(n * z);
+    std::vector<std::pair<uint32_t, double>> row;
+    while (g.more()) {
+        g.next(row);
+        for (const auto& [c, v] : row) {
+            a.cols.push_back(c);
+            a.vals.push_back(v);
+        }
+        a.rp.push_back((int64_t)a.cols.size());
+    }
+    return a;
+}
+
+// read_sketch_csv (io.cpp:247-263): comma-separated rows, blank lines skipped.
+std::vector<double> read_sketch_csv(const std::string& path, size_t& rows, size_t& cols) {
+    FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) throw Invalid(path + ": cannot open sketch file");
+    std::vector<double> m;
+    rows = cols = 0;
+    std::string line;
+    int ch;
+    bool eof = false;
+    while (!eof) {
+        line.clear();
+        while ((ch = std::fgetc(f)) != EOF && ch != '\n') line += (char)ch;
+        eof = ch == EOF;
+        if (line.empty()) continue;
+        size_t count = 0, start = 0;
+        for (;;) {
+            const size_t comma = line.find(',', start);
+            const std::string cell = line.substr(start, comma == std::string::npos ? std::string::npos : comma - start);
+            size_t pos = 0;
+            double v = 0;
+            try {
+                v = std::stod(cell, &pos);
+            } catch (...) {
+                std::fclose(f);
+                throw Invalid("stod");  // std::stod's own what() in the reference
+            }
+            m.push_back(v);
+            ++count;
+            if (comma == std::string::npos || comma + 1 == line.size()) break;
+            start = comma + 1;
+        }
+        if (rows && count != cols) {
+            std::fclose(f);
+            throw Invalid(path + ": ragged sketch file");
+        }
+        cols = count;
+        ++rows;
+    }
+    std::fclose(f);
+    if (!rows) throw Invalid(path + ": empty sketch file");
+    return m;
+}
+
+void write_sketch_csv(const std::string& path, const std::vector<double>& b, size_t rows, size_t cols) {
+    FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw Invalid(path + ": cannot open output");
+    char buf[32];
+    std::string line;
+    for (size_t i = 0; i < rows; ++i) {
+        line.clear();
+        for (size_t j = 0; j < cols; ++j) {
+            std::snprintf(buf, sizeof buf, "%.17g", b[i * cols + j]);
+            line += buf;
+            if (j + 1 < cols) line += ',';
+        }
+        line += '\n';
+        std::fwrite(line.data(), 1, line.size(), f);
+    }
+    std::fclose(f);
+}
+
+// MetricsRow + write_metrics_csv (bench.hpp:38-45, io.cpp:265-292).
+struct MetricsRow {
+    std::string algo;
+    size_t n = 0, d = 0, ell = 0, z = 0, k = 0;
+    bool has_proj = false;
+    double proj_err = 0, cov_err = 0, wall_seconds = 0;
+    uint64_t seed = 0;
+};
+
+void write_metrics_csv(const std::string& path, const std::vector<MetricsRow>& rows) {
+    FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw Invalid(path + ": cannot open output");
+    std::fputs("algo,n,d,ell,z,k,proj_err,cov_err,wall_seconds,seed\n", f);
+    for (const MetricsRow& r : rows) {
+        std::fprintf(f, "%s,%zu,%zu,%zu,%zu,%zu,", r.algo.c_str(), r.n, r.d, r.ell, r.z, r.k);
+        if (r.has_proj) std::fprintf(f, "%.9f", r.proj_err);
+        else std::fputs("nan", f);
+        std::fprintf(f, ",%.9f,%.6f,%llu\n", r.cov_err, r.wall_seconds, (unsigned long long)r.seed);
+    }
+    std::fclose(f);
+}
+
+// ---------------------------------------------------------------- sketching and metrics
+std::vector<double> sketch_sfd(const Csr& a, const sfdg_sketch_config& cfg, int device) {
+    sfdg_sketcher* h = nullptr;
+    check(sfdg_sketcher_create(&cfg, device, &h));
+    std::vector<double> b(cfg.ell * a.d, 0.0);
+    int rc = sfdg_sketcher_append_csr(h, a.rp.data(), a.cols.data(), a.vals.data(), a.n, nullptr);
+    if (rc == SFDG_OK) rc = sfdg_sketcher_finalize(h, b.data());
+    sfdg_sketcher_destroy(h);
+    check(rc);
+    return b;
+}
+
+std::vector<double> sketch_fd(const Csr& a, size_t ell, int device) {
+    sfdg_fd_sketcher* h = nullptr;
+    check(sfdg_fd_create(ell, a.d, device, &h));
+    std::vector<double> b(ell * a.d, 0.0);
+    int rc = sfdg_fd_append_csr(h, a.rp.data(), a.cols.data(), a.vals.data(), a.n);
+    if (rc == SFDG_OK) rc = sfdg_fd_finalize(h, b.data());
+    sfdg_fd_destroy(h);
+    check(rc);
+    return b;
+}
+
+struct Tail {
+    double tail_sq = 0;
+    std::vector<double> sigma;
+};
+
+Tail exact_tail(const Csr& a, size_t k, sfdg_rng_state& rng, int device) {
+    Tail t;
+    t.sigma.assign(k ? k : 1, 0.0);
+    check(sfdg_exact_tail(a.rp.data(), a.cols.data(), a.vals.data(), a.n, a.d, k, &rng, t.sigma.data(), &t.tail_sq,
+                          nullptr, device));
+    t.sigma.resize(k);
+    return t;
+}
+
+void metrics(const Csr& a, const std::vector<double>& b, size_t ell, size_t k, const Tail& tail, sfdg_rng_state& rng,
+             int device, MetricsRow& row) {
+    if (k >= 1) {
+        int has = 0;
+        check(sfdg_proj_err(a.rp.data(), a.cols.data(), a.vals.data(), a.n, a.d, b.data(), ell, k, tail.tail_sq,
+                            &row.proj_err, &has, device));
+        row.has_proj = has != 0;
+    }
+    check(sfdg_cov_err(a.rp.data(), a.cols.data(), a.vals.data(), a.n, a.d, b.data(), ell, 1000, &rng, &row.cov_err,
+                       device));
+}
+
+// ---------------------------------------------------------------- commands
+int run_sketch(int argc, char** argv) {
+    const Opts o = parse(argc, argv,
+                         {"--input", "--output", "--algo", "--ell", "--delta", "--seed", "--epsilon", "--q-const",
+                          "--q-override", "--cols", "--device"},
+                         {"--fast-q"});
+    const std::string input = o.req("--input"), output = o.req("--output");
+    const std::string algo = o.str("--algo", "sfd");
+    if (algo != "sfd" && algo != "fd") throw Usage("--algo: " + algo + " not in {fd,sfd}");
+    const size_t ell = (size_t)o.u64("--ell", 0);
+    if (!o.has("--ell")) throw Usage("--ell is required");
+    const int device = (int)o.i64("--device", 0);
+
+    sfdg_sketch_config cfg{};
+    cfg.ell = ell;
+    cfg.delta = o.f64("--delta", 0.1);
+    cfg.seed = o.u64("--seed", 0);
+    cfg.power.epsilon = o.f64("--epsilon", 0.25);
+    cfg.power.q_constant = o.f64("--q-const", 1.0);
+    cfg.power.q_override = o.flags.count("--fast-q") ? 8 : -1;
+    const long long qo = o.i64("--q-override", -1);
+    if (qo >= 0) cfg.power.q_override = qo;
+
+    const long long cols = o.i64("--cols", -1);
+    std::vector<double> b;
+    size_t d = 0;
+    if (algo == "fd") {
+        // FdSketcher(ell, d) (sketch.cpp:47-52) validates 1 <= ell <= d itself
+        const Csr a = load_matrix(input, cols);
+        d = a.d;
+        b = sketch_fd(a, ell, device);
+    } else {
+        // streamed: the library parses the file window by window into the sketcher
+        size_t n = 0, nnz = 0;
+        const size_t pc = cols >= 0 ? (size_t)cols : 0;
+        check(sfdg_read_row_stream(input.c_str(), pc, &n, &d, &nnz, nullptr, nullptr, nullptr));
+        b.assign(ell * d, 0.0);
+        check(sfdg_sketch_file(input.c_str(), pc, &cfg, device, b.data(), nullptr, &d));
+    }
+    cfg.d = d;  // from the stream (sfd_main.cpp:52)
+    write_sketch_csv(output, b, ell, d);
+
+    JObj m;
+    m.str("command", "sketch").str("version", sfdg_version()).str("input", input).str("output", output);
+    m.str("algo", algo).uint("ell", ell).uint("d", d).num("delta", cfg.delta).uint("seed", cfg.seed);
+    m.obj("power", power_json(cfg.power));
+    write_manifest(output, m);
+    return 0;
+}
+
+int run_generate(int argc, char** argv) {
+    const Opts o = parse(argc, argv, {"--n", "--d", "--z", "--seed", "--output", "--device"}, {});
+    const std::string output = o.req("--output");
+    const size_t n = o.u64("--n", 10000), d = o.u64("--d", 1000), z = o.u64("--z", 100);
+    const uint64_t seed = o.u64("--seed", 0);
+    SyntheticRows g(n, d, z, 0.9, seed);
+
+    FILE* f = std::fopen(output.c_str(), "w");
+    if (!f) throw Invalid(output + ": cannot open output");
+    std::string text = "%%MatrixMarket matrix coordinate real general\n";
+    text += std::to_string(n) + " " + std::to_string(d) + " " + std::to_string(n * z) + "\n";
+    std::vector<std::pair<uint32_t, double>> row;
+    char buf[96];
+    for (size_t i = 0; g.more(); ++i) {
+        g.next(row);
+        for (const auto& [c, v] : row) {
+            const int len = std::snprintf(buf, sizeof buf, "%zu %zu %.17g\n", i + 1, (size_t)c + 1, v);
+            text.append(buf, (size_t)len);
+        }
+        if (text.size() > (1u << 20)) {
+            std::fwrite(text.data(), 1, text.size(), f);
+            text.clear();
+        }
+    }
+    std::fwrite(text.data(), 1, text.size(), f);
+    std::fclose(f);
+
+    JObj m;
+    m.str("command", "generate").str("version", sfdg_version()).str("output", output);
+    m.uint("n", n).uint("d", d).uint("z", z).num("p_head", 0.9).uint("seed", seed);
+    write_manifest(output, m);
+    return 0;
+}
+
+int run_eval(int argc, char** argv) {
+    const Opts o = parse(argc, argv, {"--matrix", "--sketch", "--k", "--output", "--cols", "--seed", "--device"}, {});
+    const std::string mpath = o.req("--matrix"), spath = o.req("--sketch"), output = o.req("--output");
+    const size_t k = o.u64("--k", 10);
+    const uint64_t seed = o.u64("--seed", 0);
+    const int device = (int)o.i64("--device", 0);
+
+    const Csr a = load_matrix(mpath, o.i64("--cols", -1));
+    size_t ell = 0, cols = 0;
+    const std::vector<double> b = read_sketch_csv(spath, ell, cols);
+    if (cols != a.d) throw Invalid("eval: matrix and sketch dimensions are incompatible");
+
+    sfdg_rng_state rng{seed, 0, 0, 0.0};  // Rng rng(seed), shared by exact_tail and cov_err
+    const Tail tail = exact_tail(a, k, rng, device);
+    MetricsRow row;
+    row.algo = "eval";
+    row.n = a.n;
+    row.d = a.d;
+    row.ell = ell;
+    row.z = a.n ? a.nnz() / a.n : 0;
+    row.k = k;
+    row.seed = seed;
+    metrics(a, b, ell, k, tail, rng, device, row);
+    write_metrics_csv(output, {row});
+
+    JObj m;
+    m.str("command", "eval").str("version", sfdg_version()).str("matrix", mpath).str("sketch", spath);
+    m.str("output", output).uint("k", k).uint("seed", seed);
+    write_manifest(output, m);
+    return 0;
+}
+
+size_t scaled(size_t v, double scale, size_t lo) {
+    return std::max(lo, (size_t)std::llround((double)v * scale));
+}
+
+int run_bench(int argc, char** argv) {
+    const Opts o = parse(argc, argv, {"--sweep", "--out-csv", "--scale", "--seed", "--device"}, {"--fast-q"});
+    const std::string sweep = o.req("--sweep"), out_csv = o.req("--out-csv");
+    if (sweep != "n" && sweep != "d" && sweep != "ell" && sweep != "nnz")
+        throw Usage("--sweep: " + sweep + " not in {d,ell,n,nnz}");
+    const double scale = o.f64("--scale", 1.0);
+    const uint64_t seed = o.u64("--seed", 0);
+    const bool fast_q = o.flags.count("--fast-q") != 0;
+    const int device = (int)o.i64("--device", 0);
+
+    const size_t def_n = scaled(10000, scale, 50), def_d = scaled(1000, scale, 20);
+    const size_t def_ell = scaled(50, scale, 4), def_z = scaled(100, scale, 2);
+    std::vector<size_t> values;
+    if (sweep == "n") {
+        for (size_t v : {10000, 20000, 30000, 40000, 50000, 60000}) values.push_back(scaled(v, scale, 50));
+    } else if (sweep == "d") {
+        for (size_t v : {1000, 2000, 3000, 4000, 5000, 6000}) values.push_back(scaled(v, scale, 20));
+    } else if (sweep == "ell") {
+        for (size_t v : {5, 10, 25, 50, 75, 100}) values.push_back(scaled(v, scale, 2));
+    } else {
+        for (size_t v : {5, 25, 50, 100, 250, 500}) values.push_back(scaled(v, scale, 2));
+    }
+
+    // bring the device context up before the first timed sketch
+    {
+        sfdg_fd_sketcher* h = nullptr;
+        check(sfdg_fd_create(1, 1, device, &h));
+        sfdg_fd_destroy(h);
+    }
+
+    std::vector<MetricsRow> rows;
+    for (size_t cell = 0; cell < values.size(); ++cell) {
+        const size_t v = values[cell];
+        size_t n = def_n, d = def_d, ell = def_ell, z = def_z;
+        if (sweep == "n") n = v;
+        else if (sweep == "d") d = v;
+        else if (sweep == "ell") ell = v;
+        else z = v;
+        z = std::min(z, d);
+        ell = std::min(ell, d);
+        const size_t k = std::max<size_t>(1, std::min<size_t>(10, ell - 1));
+        const uint64_t cseed = seed + 1000 * cell;
+        const Csr a = synthetic_csr(n, d, z, cseed);
+
+        sfdg_sketch_config cfg{};
+        cfg.ell = ell;
+        cfg.d = d;
+        cfg.delta = 0.1;
+        cfg.seed = cseed;
+        cfg.power.epsilon = 0.25;
+        cfg.power.q_constant = 1.0;
+        cfg.power.q_override = fast_q ? 8 : -1;
+
+        sfdg_rng_state tail_rng{cseed ^ 0x5bf03635ULL, 0, 0, 0.0};
+        const Tail tail = exact_tail(a, k, tail_rng, device);
+        for (const char* algo : {"fd", "sfd"}) {
+            // timed_run (bench.cpp:185-237): the sketch is timed, the metrics are not
+            MetricsRow row;
+            row.algo = algo;
+            row.n = n;
+            row.d = d;
+            row.ell = ell;
+            row.z = z;
+            row.k = k;
+            row.seed = cseed;
+            const auto t0 = std::chrono::steady_clock::now();
+            const std::vector<double> b = row.algo == "fd" ? sketch_fd(a, ell, device) : sketch_sfd(a, cfg, device);
+            row.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            sfdg_rng_state mrng{cseed ^ 0x9e3779b97f4a7c15ULL, 0, 0, 0.0};
+            metrics(a, b, ell, k, tail, mrng, device, row);
+            rows.push_back(row);
+        }
+        std::fprintf(stderr, "bench: %s=%zu done\n", sweep.c_str(), v);
+    }
+    write_metrics_csv(out_csv, rows);
+
+    JObj m;
+    m.str("command", "bench").str("version", sfdg_version()).str("sweep", sweep).num("scale", scale);
+    m.uint("seed", seed).boolean("fast_q", fast_q).str("out_csv", out_csv);
+    write_manifest(out_csv, m);
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-    if (argc < 2 || std::strcmp(argv[1], "sketch") != 0) return usage("expected the 'sketch' command");
-    Args a;
-    for (int i = 2; i < argc; ++i) {
-        const std::string k = argv[i];
-        auto val = [&]() -> const char* {
-            if (i + 1 >= argc) throw 0;
-            return argv[++i];
-        };
-        try {
-            if (k == "--input") a.input = val();
-            else if (k == "--output") a.output = val();
-            else if (k == "--algo") a.algo = val();
-            else if (k == "--ell") a.ell = std::stoull(val());
-            else if (k == "--delta") a.delta = std::stod(val());
-            else if (k == "--seed") a.seed = std::stoull(val());
-            else if (k == "--epsilon") a.epsilon = std::stod(val());
-            else if (k == "--q-const") a.q_const = std::stod(val());
-            else if (k == "--fast-q") a.fast_q = true;
-            else if (k == "--q-override") a.q_override = std::stoll(val());
-            else if (k == "--cols") a.cols = std::stoll(val());
-            else if (k == "--device") a.device = std::atoi(val());
-            else return usage(("unknown option " + k).c_str());
-        } catch (...) {
-            return usage(("bad value for " + k).c_str());
-        }
+    const std::string cmd = argc >= 2 ? argv[1] : "";
+    if (cmd == "--help" || cmd == "-h") {
+        std::fputs(kUsage, stdout);
+        return 0;
     }
-    if (a.input.empty() || a.output.empty()) return usage("--input and --output are required");
-    if (a.algo != "sfd" && a.algo != "fd") return usage("sketch: --algo must be fd or sfd");
-    const size_t plain = a.cols >= 0 ? (size_t)a.cols : 0;
-
-    sfdg_sketch_config cfg{};
-    cfg.ell = a.ell;
-    cfg.d = 0;  // from the file (tools/sfd_main.cpp:52)
-    cfg.delta = a.delta;
-    cfg.power.epsilon = a.epsilon;
-    cfg.power.q_constant = a.q_const;
-    cfg.power.q_override = a.fast_q ? 8 : -1;
-    if (a.q_override >= 0) cfg.power.q_override = a.q_override;
-    cfg.seed = a.seed;
-
-    size_t n = 0, d = 0, nnz = 0;
-    std::vector<double> b;
-    if (a.algo == "sfd") {
-        // the width is needed for the output buffer: parse the header (cheap) first
-        int rc = sfdg_read_row_stream(a.input.c_str(), plain, &n, &d, &nnz, nullptr, nullptr, nullptr);
-        if (rc != SFDG_OK) return fail(rc);
-        b.assign(a.ell * d, 0.0);
-        size_t dd = 0;
-        rc = sfdg_sketch_file(a.input.c_str(), plain, &cfg, a.device, b.data(), nullptr, &dd);
-        if (rc != SFDG_OK) return fail(rc);
-    } else {
-        int rc = sfdg_read_row_stream(a.input.c_str(), plain, &n, &d, &nnz, nullptr, nullptr, nullptr);
-        if (rc != SFDG_OK) return fail(rc);
-        std::vector<int64_t> rp(n + 1);
-        std::vector<uint32_t> cs(nnz ? nnz : 1);
-        std::vector<double> vs(nnz ? nnz : 1);
-        rc = sfdg_read_row_stream(a.input.c_str(), plain, &n, &d, &nnz, rp.data(), cs.data(), vs.data());
-        if (rc != SFDG_OK) return fail(rc);
-        sfdg_fd_sketcher* h = nullptr;
-        rc = sfdg_fd_create(a.ell, d, a.device, &h);
-        if (rc != SFDG_OK) return fail(rc);
-        b.assign(a.ell * d, 0.0);
-        if ((rc = sfdg_fd_append_csr(h, rp.data(), cs.data(), vs.data(), n)) != SFDG_OK ||
-            (rc = sfdg_fd_finalize(h, b.data())) != SFDG_OK) {
-            const int code = fail(rc);
-            sfdg_fd_destroy(h);
-            return code;
+    for (int i = 2; i < argc; ++i)
+        if (!std::strcmp(argv[i], "--help") || !std::strcmp(argv[i], "-h")) {
+            std::fputs(kUsage, stdout);
+            return 0;
         }
-        sfdg_fd_destroy(h);
-    }
     try {
-        write_csv(a.output, b, a.ell, d);
-    } catch (...) {
-        std::fprintf(stderr, "sfdg: %s: cannot open output\n", a.output.c_str());
+        if (cmd == "sketch") return run_sketch(argc, argv);
+        if (cmd == "generate") return run_generate(argc, argv);
+        if (cmd == "eval") return run_eval(argc, argv);
+        if (cmd == "bench") return run_bench(argc, argv);
+        throw Usage(cmd.empty() ? "a subcommand is required" : "unknown subcommand " + cmd);
+    } catch (const Usage& e) {
+        std::fprintf(stderr, "%s\n%s", e.what(), kUsage);
+        return 1;
+    } catch (const Invalid& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    } catch (const Lib& e) {
+        if (e.code == SFDG_NUMERICAL_ERROR) std::fprintf(stderr, "numerical failure: %s\n", sfdg_last_error());
+        else std::fprintf(stderr, "error: %s\n", sfdg_last_error());
+        return e.code == SFDG_NUMERICAL_ERROR ? 2 : e.code == SFDG_CUDA_ERROR ? 3 : 1;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
         return 1;
     }
-    // manifest (tools/sfd_main.cpp:73-85)
-    std::string m = "{\n";
-    m += "  \"command\": \"sketch\",\n  \"version\": " + jstr(sfdg_version()) + ",\n";
-    m += "  \"input\": " + jstr(a.input) + ",\n  \"output\": " + jstr(a.output) + ",\n";
-    m += "  \"algo\": " + jstr(a.algo) + ",\n  \"ell\": " + std::to_string(a.ell) + ",\n";
-    m += "  \"d\": " + std::to_string(d) + ",\n  \"delta\": " + jnum(a.delta) + ",\n";
-    m += "  \"seed\": " + std::to_string(a.seed) + ",\n";
-    m += "  \"power\": {\"epsilon\": " + jnum(a.epsilon) + ", \"q_constant\": " + jnum(a.q_const);
-    if (cfg.power.q_override >= 0) m += ", \"q_override\": " + std::to_string(cfg.power.q_override);
-    m += "}\n}\n";
-    FILE* f = std::fopen((a.output + ".manifest.json").c_str(), "w");
-    if (!f) {
-        std::fprintf(stderr, "sfdg: %s.manifest.json: cannot open manifest output\n", a.output.c_str());
-        return 1;
-    }
-    std::fputs(m.c_str(), f);
-    std::fclose(f);
-    return 0;
 }
