@@ -783,9 +783,18 @@ __global__ void cluster_kernel(const double* __restrict__ dg, const double* __re
         if (lane == 0) atomicExch(fallback, 1);  // eigh() then runs the Jacobi solver instead
         return;
     }
-    // MGS, two passes
+    // MGS, two passes. The cluster's inverse-iteration vectors must span its invariant
+    // subspace: when one of them is (nearly) dependent on the earlier ones -- e.g. equal
+    // eigenvalues from different diagonal blocks of a split T all converge to the same
+    // vector -- the normalised remainder is rounding noise, not an eigenvector. That case is
+    // handed to the Jacobi solver (eigh() runs it when *fallback is set).
     for (int pass = 0; pass < 2; ++pass)
         for (int a = 0; a < c; ++a) {
+            double s0 = 0.0;
+            if (pass == 0) {
+                for (int j = lane; j < n; j += 32) s0 += X[(size_t)j * ldx + t0 + a] * X[(size_t)j * ldx + t0 + a];
+                s0 = warp_sum(s0);
+            }
             for (int b = 0; b < a; ++b) {
                 double s = 0.0;
                 for (int j = lane; j < n; j += 32) s += X[(size_t)j * ldx + t0 + a] * X[(size_t)j * ldx + t0 + b];
@@ -795,7 +804,12 @@ __global__ void cluster_kernel(const double* __restrict__ dg, const double* __re
             }
             double s = 0.0;
             for (int j = lane; j < n; j += 32) s += X[(size_t)j * ldx + t0 + a] * X[(size_t)j * ldx + t0 + a];
-            s = 1.0 / sqrt(warp_sum(s));
+            s = warp_sum(s);
+            if (pass == 0 && !(s > 1e-6 * s0)) {  // lost > 99.9% of its norm: dependent
+                if (lane == 0) atomicExch(fallback, 1);
+                return;
+            }
+            s = 1.0 / sqrt(s);
             for (int j = lane; j < n; j += 32) X[(size_t)j * ldx + t0 + a] *= s;
             __syncwarp();
         }

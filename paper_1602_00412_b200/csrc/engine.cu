@@ -63,13 +63,14 @@ __global__ void shrink_weights_kernel(const double* __restrict__ evals, const do
     __shared__ double w[512];
     const double s0 = sqrt(fmax(evals[0], 0.0));
     const double sl = sqrt(fmax(evals[ell - 1], 0.0));
-    const double floor_sq = sl * sl;
+    const double floor_sq = __dmul_rn(sl, sl);
     const double cutoff = 1e-10 * s0;
     for (int i = threadIdx.x; i < ell; i += blockDim.x) {
         const double si = sqrt(fmax(evals[i], 0.0));
         double wi = 0.0;
         if (!(si < cutoff || si == 0.0)) {
-            const double shrunk = sqrt(fmax(si * si - floor_sq, 0.0));
+            // rounded product, no FMA contraction: s_i = s_ell must give exactly 0 (shrink.cpp:19-21)
+            const double shrunk = sqrt(fmax(__dsub_rn(__dmul_rn(si, si), floor_sq), 0.0));
             wi = shrunk == 0.0 ? 0.0 : shrunk / si;
         }
         w[i] = wi;
@@ -90,13 +91,13 @@ __global__ void shrink_weights_kernel(const double* __restrict__ evals, const do
 __global__ void tall_shrink_kernel(const double* __restrict__ evals, const double* __restrict__ V, int dd, int ell,
                                    double* __restrict__ bt, int ldo, int lp) {
     const double sl = sqrt(fmax(evals[ell - 1], 0.0));
-    const double floor_sq = sl * sl;
+    const double floor_sq = __dmul_rn(sl, sl);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < dd * lp; e += gridDim.x * blockDim.x) {
         const int t = e / lp, i = e % lp;
         double v = 0.0;
         if (i < ell) {
             const double si = sqrt(fmax(evals[i], 0.0));
-            const double shrunk = sqrt(fmax(si * si - floor_sq, 0.0));
+            const double shrunk = sqrt(fmax(__dsub_rn(__dmul_rn(si, si), floor_sq), 0.0));
             v = shrunk * V[(size_t)t * dd + i];
         }
         bt[(size_t)t * ldo + i] = v;

@@ -1,6 +1,8 @@
 // sparse.cuh -- device CSR/CSC buffer, scratch arena, sparse kernels (see sparse.cu).
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,6 +33,7 @@ class Scratch {
         }
         T* p = reinterpret_cast<T*>(static_cast<char*>(chunks[cur].ptr) + used);
         used += bytes;
+        if (poison()) CK(cudaMemset(p, 0xff, bytes));  // debugging aid: NaN-fill (SFDG_POISON=1)
         return p;
     }
     void reset() {
@@ -44,6 +47,10 @@ class Scratch {
     }
 
   private:
+    static bool poison() {
+        static const bool on = std::getenv("SFDG_POISON") && std::getenv("SFDG_POISON")[0] == '1';
+        return on;
+    }
     struct Chunk {
         void* ptr;
         size_t size;

@@ -242,6 +242,61 @@ def test_dense_shrink_kat():
     assert np.all(np.abs(b[0, 1:]) < 1e-10) and np.all(b[1] == 0.0)
 
 
+def test_dense_shrink_ell1_is_exactly_zero(oracle):
+    """ell = 1 shrinks by the top singular value itself: s_0^2 - s_0^2 is exactly 0 in the
+    reference (shrink.cpp:19-21), so B = 0 exactly -- no FMA-contracted rounding residue."""
+    g = np.random.default_rng(12)
+    for rows, d in ((2, 50), (3, 40), (2, 199), (2, 1)):
+        a = g.standard_normal((rows, d))
+        b = P.dense_shrink(a, 1)
+        assert np.all(b == 0.0) and np.all(oracle.dense_shrink(a, 1) == 0.0)
+
+
+def test_eigh_equal_eigenvalues_across_split_blocks():
+    """A Gram whose tridiagonal form splits into blocks that share the eigenvalue 0 (two zero
+    rows and a rank-one 2 x 2 coupled at 1e-27): the inverse-iteration vectors of that cluster
+    coincide, so the cluster is handed to the Jacobi solver; values and an orthonormal basis
+    must come out right."""
+    a, b = -3.2311742677852644e-27, -1.6155871338926322e-27
+    k = np.array([[0, 0, 0, 0, 0], [0, 16, 0, 8, a], [0, 0, 0, 0, 0], [0, 8, 0, 4, b], [0, a, 0, b, 1.0]])
+    vals, vecs = P.eigh(k, 1e-12 * 21.0)
+    assert np.allclose(vals, [20, 1, 0, 0, 0], atol=1e-12)
+    assert np.max(np.abs(vecs.T @ vecs - np.eye(5))) <= 1e-12
+    assert np.max(np.abs(k @ vecs - vecs * vals)) <= 1e-12
+    bp = np.zeros((5, 5))
+    bp[0, 1], bp[0, 3], bp[1, 4] = -4.0, -2.0, 1.0
+    bp[0, 4] = 1e-28  # the rounding residue that split the blocks in a sketch stream
+    out = P.dense_shrink(np.vstack([np.zeros((5, 5)), bp]), 5)
+    want = np.zeros((5, 5))
+    want[0, 1], want[0, 3], want[1, 4] = 4.0, 2.0, 1.0
+    assert np.max(np.abs(out.T @ out - want.T @ want)) <= 1e-12
+
+
+def test_small_d_integer_duplicate_stream_vs_oracle(oracle):
+    """ell = d = 5, rows of two small integers with duplicates (found by tools/fuzz_parity.py):
+    every flush is rank-deficient and its Gram has multiple zero eigenvalues."""
+    g = np.random.default_rng(1134232088)
+    rows = []
+    for i in range(400):
+        if rows and g.random() < 0.5:
+            rows.append(rows[int(g.integers(0, len(rows)))])
+            continue
+        z = int(g.integers(1, 3))
+        idx = np.sort(g.choice(5, size=z, replace=False))
+        v = g.integers(-3, 4, size=z).astype(float)
+        rows.append((idx[v != 0].astype(np.uint32), v[v != 0]))
+    rp = np.zeros(len(rows) + 1, np.int64)
+    rp[1:] = np.cumsum([len(r[0]) for r in rows])
+    cs = np.concatenate([r[0] for r in rows]).astype(np.uint32)
+    vs = np.concatenate([r[1] for r in rows])
+    for q in (8, None):
+        b, st = sketch_gpu(rp, cs, vs, 5, 5, 3, power=P.PowerConfig(q_override=q))
+        bo, so = oracle.sketch(rp, cs, vs, 5, 5, seed=3, power=OPower(q_override=q))
+        assert btb_rel(b, bo) <= BTB_TOL
+        for key in ("flushes", "attempts", "verifier_i", "delta_spent"):
+            assert st[key] == so[key], key
+
+
 def test_dense_shrink_rank_below_ell():
     a = np.zeros((2, 3))
     a[0, 0] = a[1, 0] = 1.0
