@@ -6,7 +6,7 @@ cover (+-1 and integer values, head/tail and Zipf columns, duplicated rows, exac
 low-rank rows, tiny d, ell = 1 and ell = d, delta / power overrides) and checks every run with
 the north_star gates: B^T B within 1e-8 relative Frobenius of the oracle's, counters exact.
 
-    python tools/fuzz_parity.py [--cases 200] [--seed 0] [--max-d 300] [--out report.json]
+    python tools/fuzz_parity.py [--cases 200] [--seed 0] [--max-d 300] [--big] [--out report.json]
 
 Test infrastructure (uses oracle/); prints one line per failure and a JSON summary.
 """
@@ -30,7 +30,16 @@ def btb_rel(b1, b2):
     return float(np.linalg.norm(g1 - g2) / max(np.linalg.norm(g2), 1e-300))
 
 
-def draw_case(g: np.random.Generator, max_d: int):
+def draw_case(g: np.random.Generator, max_d: int, big: bool = False):
+    if big:  # wide sketches: ell 65..256 (trsm panels, 4-chunk SpMM, Q 3..8 verify, cluster tridiag)
+        d = int(g.integers(300, max_d + 1))
+        ell = int(g.integers(65, min(256, d) + 1))
+        n = int(g.integers(ell, 3 * d))
+        kind = str(g.choice(["gauss", "pm1", "int", "lognormal"]))
+        return {"d": d, "ell": ell, "n": n, "kind": kind, "cols": str(g.choice(["uniform", "headtail", "zipf"])),
+                "structure": str(g.choice(["none", "dups", "lowrank", "nearlow"])),
+                "zmax": int(g.choice([3, 10, 40])), "seed": int(g.integers(0, 2**31)),
+                "delta": float(g.choice([0.1, 0.01])), "q_override": int(g.choice([1, 2, 3, 4]))}
     d = int(g.choice([int(g.integers(2, 12)), int(g.integers(12, 80)), int(g.integers(80, max_d + 1))]))
     ell = int(g.choice([1, int(g.integers(1, min(d, 64) + 1)), min(d, int(g.integers(2, 9)))]))
     if g.random() < 0.05:
@@ -137,12 +146,13 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--max-d", type=int, default=300)
     ap.add_argument("--out", default="")
+    ap.add_argument("--big", action="store_true", help="ell 65..256, d 300..max-d, q 1..4")
     a = ap.parse_args()
     O = Oracle()
     g = np.random.default_rng(a.seed)
     fails, worst, t0 = [], 0.0, time.time()
     for i in range(a.cases):
-        c = draw_case(g, a.max_d)
+        c = draw_case(g, a.max_d, a.big)
         r = run_case(O, c)
         worst = max(worst, r.get("btb", 0.0))
         if not r["ok"]:
