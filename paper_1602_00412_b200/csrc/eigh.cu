@@ -31,7 +31,7 @@ namespace {
 
 constexpr int kJacThreads = 1024;
 constexpr int kMaxSweeps = 100;  // la_core.cpp:31
-constexpr int kPackedSmemMax = 232;
+constexpr int kPackedSmemMax = 230;  // N(N+1)/2 doubles + 16.3 KB static smem <= 227 KB
 
 __device__ __forceinline__ int pidx(int i, int j) {  // packed upper, i <= j
     return j * (j + 1) / 2 + i;

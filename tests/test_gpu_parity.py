@@ -272,6 +272,23 @@ def test_eigh_equal_eigenvalues_across_split_blocks():
     assert np.max(np.abs(out.T @ out - want.T @ want)) <= 1e-12
 
 
+@pytest.mark.parametrize("n", [230, 232, 464])
+def test_eigh_jacobi_fallback_sizes(n):
+    """A 40-fold eigenvalue (cluster > 32) sends the whole matrix to the Jacobi solver: the
+    shared-memory variant up to N = 230 (N(N+1)/2 doubles + its static shared memory within
+    227 KB), the global-memory variant above (found by tools/fuzz_parity.py --big at 2 ell = 464)."""
+    g = np.random.default_rng(n)
+    q = np.linalg.qr(g.standard_normal((n, n)))[0]
+    lam = np.sort(g.uniform(1.0, 10.0, n))[::-1]
+    lam[20:60] = 5.0
+    k = (q * lam) @ q.T
+    k = 0.5 * (k + k.T)
+    vals, vecs = P.eigh(k, 1e-12 * max(float((k ** 2).sum()), 1.0))
+    assert np.max(np.abs(vals - np.sort(lam)[::-1])) <= 1e-10 * lam.max()
+    assert np.max(np.abs(vecs.T @ vecs - np.eye(n))) <= 1e-10
+    assert np.max(np.abs(k @ vecs - vecs * vals)) <= 1e-9 * lam.max()
+
+
 def test_small_d_integer_duplicate_stream_vs_oracle(oracle):
     """ell = d = 5, rows of two small integers with duplicates (found by tools/fuzz_parity.py):
     every flush is rank-deficient and its Gram has multiple zero eigenvalues."""

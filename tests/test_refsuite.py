@@ -1,0 +1,46 @@
+"""The reference's OWN unit tests run against the device build.
+
+oracle/_ref/refsuite is /root/reference/proj/tests/test_{sketch,shrink,randsvd,bench}.cpp,
+unmodified, compiled by `make -C oracle refsuite` against the compat layer tests/refsuite/
+(a doctest-compatible runner, and sfd::SfdSketcher / FdSketcher / merge / dense_shrink /
+sparse_shrink / boosted_sparse_shrink / simultaneous_iteration / exact_tail / proj_err /
+cov_err / timed_run / Rng implemented over the sfdg C ABI). The binary is built in the build
+container (the reference sources are not on the GPU box) and travels with the repo snapshot.
+
+Excluded: the two verify_spectral cases, which drive the verifier with arbitrary host
+std::function operators; the device verifier runs on the difference operator inside
+boosted_sparse_shrink (covered by the boosted_* cases here and the parity tests).
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXE = os.path.join(ROOT, "oracle", "_ref", "refsuite")
+EXCLUDE = "verify_spectral"
+
+
+def _run(*args, timeout=900):
+    if not os.path.exists(EXE):
+        pytest.skip("oracle/_ref/refsuite not built (needs the reference sources: make -C oracle refsuite)")
+    return subprocess.run([EXE, *args], capture_output=True, text=True, timeout=timeout)
+
+
+def test_refsuite_lists_the_reference_cases():
+    r = _run("--list", f"--exclude={EXCLUDE}")
+    names = r.stdout.splitlines()
+    assert r.returncode == 0 and len(names) == 35
+    assert sum("(excluded)" in n for n in names) == 2
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_pass_on_device():
+    r = _run(f"--exclude={EXCLUDE}")
+    m = re.search(r"test cases: (\d+) passed, (\d+) failed, (\d+) skipped \| assertions: (\d+), (\d+) failed",
+                  r.stdout)
+    assert m, r.stdout + r.stderr
+    passed, failed, skipped, asserts, afail = map(int, m.groups())
+    assert r.returncode == 0 and failed == 0 and afail == 0, r.stderr[-4000:]
+    assert passed == 33 and skipped == 2 and asserts > 3000

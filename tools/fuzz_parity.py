@@ -147,8 +147,13 @@ def main():
     ap.add_argument("--max-d", type=int, default=300)
     ap.add_argument("--out", default="")
     ap.add_argument("--big", action="store_true", help="ell 65..256, d 300..max-d, q 1..4")
+    ap.add_argument("--case", default="", help="rerun one case given as its JSON dict")
     a = ap.parse_args()
     O = Oracle()
+    if a.case:
+        r = run_case(O, json.loads(a.case))
+        print(json.dumps(r, default=str))
+        return 0 if r["ok"] else 1
     g = np.random.default_rng(a.seed)
     fails, worst, t0 = [], 0.0, time.time()
     for i in range(a.cases):
