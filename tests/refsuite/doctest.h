@@ -5,6 +5,7 @@
 // subset those files use, with doctest's semantics, so they compile unchanged:
 //   TEST_CASE, single-level SUBCASE (the test body re-runs once per subcase, entering one
 //   subcase per run), CHECK, CHECK_FALSE, REQUIRE (aborts the test case), CHECK_THROWS_AS,
+//   CHECK_THROWS_WITH_AS with doctest::Contains,
 //   doctest::Approx(v).epsilon(e) (|a - b| < eps * (1 + max(|a|, |b|)), default eps =
 //   100 * FLT_EPSILON), DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN.
 // The runner takes --exclude=pat1,pat2 (substring match on test-case names) and --list.
@@ -42,6 +43,13 @@ class Approx {
     double eps_ = static_cast<double>(std::numeric_limits<float>::epsilon()) * 100.0;
     double scale_ = 1.0;
 };
+// String matcher for CHECK_THROWS_WITH_AS: the exception's what() contains the text.
+struct Contains {
+    explicit Contains(const char* s) : text(s) {}
+    std::string text;
+    bool matches(const char* what) const { return std::strstr(what, text.c_str()) != nullptr; }
+};
+
 inline bool operator==(double x, const Approx& a) { return a.matches(x); }
 inline bool operator==(const Approx& a, double x) { return a.matches(x); }
 inline bool operator!=(double x, const Approx& a) { return !a.matches(x); }
@@ -186,6 +194,19 @@ inline int run(int argc, char** argv) {
         }                                                                                          \
         ::doctest_lite::check(doctest_lite_ok, __FILE__, __LINE__, "CHECK_THROWS_AS( " #expr ", " #__VA_ARGS__ " )", \
                               false);                                                              \
+    } while (0)
+
+#define CHECK_THROWS_WITH_AS(expr, matcher, ...)                                                   \
+    do {                                                                                           \
+        bool doctest_lite_ok = false;                                                              \
+        try {                                                                                      \
+            static_cast<void>(expr);                                                               \
+        } catch (const __VA_ARGS__& doctest_lite_e) {                                              \
+            doctest_lite_ok = (matcher).matches(doctest_lite_e.what());                            \
+        } catch (...) {                                                                            \
+        }                                                                                          \
+        ::doctest_lite::check(doctest_lite_ok, __FILE__, __LINE__,                                 \
+                              "CHECK_THROWS_WITH_AS( " #expr ", " #matcher ", " #__VA_ARGS__ " )", false); \
     } while (0)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN

@@ -1,10 +1,11 @@
 """The reference's OWN unit tests run against the device build.
 
-oracle/_ref/refsuite is /root/reference/proj/tests/test_{sketch,shrink,randsvd,bench}.cpp,
+oracle/_ref/refsuite is /root/reference/proj/tests/test_{sketch,shrink,randsvd,bench,io}.cpp,
 unmodified, compiled by `make -C oracle refsuite` against the compat layer tests/refsuite/
 (a doctest-compatible runner, and sfd::SfdSketcher / FdSketcher / merge / dense_shrink /
 sparse_shrink / boosted_sparse_shrink / simultaneous_iteration / exact_tail / proj_err /
-cov_err / timed_run / Rng implemented over the sfdg C ABI). The binary is built in the build
+cov_err / timed_run / Rng implemented over the sfdg C ABI; open_row_stream over the library's
+parallel reader and the CLI's writers for io.hpp). The binary is built in the build
 container (the reference sources are not on the GPU box) and travels with the repo snapshot.
 
 Excluded: the two verify_spectral cases, which drive the verifier with arbitrary host
@@ -31,7 +32,7 @@ def _run(*args, timeout=900):
 def test_refsuite_lists_the_reference_cases():
     r = _run("--list", f"--exclude={EXCLUDE}")
     names = r.stdout.splitlines()
-    assert r.returncode == 0 and len(names) == 35
+    assert r.returncode == 0 and len(names) == 43
     assert sum("(excluded)" in n for n in names) == 2
 
 
@@ -43,7 +44,7 @@ def test_reference_unit_tests_pass_on_device():
     assert m, r.stdout + r.stderr
     passed, failed, skipped, asserts, afail = map(int, m.groups())
     assert r.returncode == 0 and failed == 0 and afail == 0, r.stderr[-4000:]
-    assert passed == 33 and skipped == 2 and asserts > 3000
+    assert passed == 41 and skipped == 2 and asserts > 3000
 
 
 ACCEPT = os.path.join(ROOT, "oracle", "_ref", "refaccept")

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "../include/sfdg.h"
+#include "sfdg_host_io.hpp"
 #include "synthetic_rows.hpp"
 
 namespace {
@@ -182,14 +183,7 @@ struct JObj {
     }
 };
 
-void write_manifest(const std::string& output, const JObj& m) {
-    const std::string path = output + ".manifest.json";
-    FILE* f = std::fopen(path.c_str(), "w");
-    if (!f) throw Invalid(path + ": cannot open manifest output");
-    const std::string text = m.dump() + "\n";
-    std::fwrite(text.data(), 1, text.size(), f);
-    std::fclose(f);
-}
+void write_manifest(const std::string& output, const JObj& m) { sfdg_tools::write_manifest(output, m.dump()); }
 
 JObj power_json(const sfdg_power_config& p) {
     JObj j;
@@ -239,87 +233,11 @@ Csr synthetic_csr(size_t n, size_t d, size_t z, uint64_t seed) {
     return a;
 }
 
-// read_sketch_csv (io.cpp:247-263): comma-separated rows, blank lines skipped.
-std::vector<double> read_sketch_csv(const std::string& path, size_t& rows, size_t& cols) {
-    FILE* f = std::fopen(path.c_str(), "r");
-    if (!f) throw Invalid(path + ": cannot open sketch file");
-    std::vector<double> m;
-    rows = cols = 0;
-    std::string line;
-    int ch;
-    bool eof = false;
-    while (!eof) {
-        line.clear();
-        while ((ch = std::fgetc(f)) != EOF && ch != '\n') line += (char)ch;
-        eof = ch == EOF;
-        if (line.empty()) continue;
-        size_t count = 0, start = 0;
-        for (;;) {
-            const size_t comma = line.find(',', start);
-            const std::string cell = line.substr(start, comma == std::string::npos ? std::string::npos : comma - start);
-            size_t pos = 0;
-            double v = 0;
-            try {
-                v = std::stod(cell, &pos);
-            } catch (...) {
-                std::fclose(f);
-                throw Invalid("stod");  // std::stod's own what() in the reference
-            }
-            m.push_back(v);
-            ++count;
-            if (comma == std::string::npos || comma + 1 == line.size()) break;
-            start = comma + 1;
-        }
-        if (rows && count != cols) {
-            std::fclose(f);
-            throw Invalid(path + ": ragged sketch file");
-        }
-        cols = count;
-        ++rows;
-    }
-    std::fclose(f);
-    if (!rows) throw Invalid(path + ": empty sketch file");
-    return m;
-}
+using sfdg_tools::read_sketch_csv;
+using MetricsRow = sfdg_tools::MetricsLine;
 
 void write_sketch_csv(const std::string& path, const std::vector<double>& b, size_t rows, size_t cols) {
-    FILE* f = std::fopen(path.c_str(), "w");
-    if (!f) throw Invalid(path + ": cannot open output");
-    char buf[32];
-    std::string line;
-    for (size_t i = 0; i < rows; ++i) {
-        line.clear();
-        for (size_t j = 0; j < cols; ++j) {
-            std::snprintf(buf, sizeof buf, "%.17g", b[i * cols + j]);
-            line += buf;
-            if (j + 1 < cols) line += ',';
-        }
-        line += '\n';
-        std::fwrite(line.data(), 1, line.size(), f);
-    }
-    std::fclose(f);
-}
-
-// MetricsRow + write_metrics_csv (bench.hpp:38-45, io.cpp:265-292).
-struct MetricsRow {
-    std::string algo;
-    size_t n = 0, d = 0, ell = 0, z = 0, k = 0;
-    bool has_proj = false;
-    double proj_err = 0, cov_err = 0, wall_seconds = 0;
-    uint64_t seed = 0;
-};
-
-void write_metrics_csv(const std::string& path, const std::vector<MetricsRow>& rows) {
-    FILE* f = std::fopen(path.c_str(), "w");
-    if (!f) throw Invalid(path + ": cannot open output");
-    std::fputs("algo,n,d,ell,z,k,proj_err,cov_err,wall_seconds,seed\n", f);
-    for (const MetricsRow& r : rows) {
-        std::fprintf(f, "%s,%zu,%zu,%zu,%zu,%zu,", r.algo.c_str(), r.n, r.d, r.ell, r.z, r.k);
-        if (r.has_proj) std::fprintf(f, "%.9f", r.proj_err);
-        else std::fputs("nan", f);
-        std::fprintf(f, ",%.9f,%.6f,%llu\n", r.cov_err, r.wall_seconds, (unsigned long long)r.seed);
-    }
-    std::fclose(f);
+    sfdg_tools::write_sketch_csv(path, b.data(), rows, cols);
 }
 
 // ---------------------------------------------------------------- sketching and metrics
@@ -428,25 +346,21 @@ int run_generate(int argc, char** argv) {
     const uint64_t seed = o.u64("--seed", 0);
     sfdg_tools::SyntheticRows g(n, d, z, 0.9, seed);
 
-    FILE* f = std::fopen(output.c_str(), "w");
-    if (!f) throw Invalid(output + ": cannot open output");
-    std::string text = "%%MatrixMarket matrix coordinate real general\n";
-    text += std::to_string(n) + " " + std::to_string(d) + " " + std::to_string(n * z) + "\n";
+    sfdg_tools::MmWriter writer(output, n, d, n * z);
     std::vector<std::pair<uint32_t, double>> row;
-    char buf[96];
+    std::vector<uint32_t> idx;
+    std::vector<double> val;
     for (size_t i = 0; g.more(); ++i) {
         g.next(row);
+        idx.clear();
+        val.clear();
         for (const auto& [c, v] : row) {
-            const int len = std::snprintf(buf, sizeof buf, "%zu %zu %.17g\n", i + 1, (size_t)c + 1, v);
-            text.append(buf, (size_t)len);
+            idx.push_back(c);
+            val.push_back(v);
         }
-        if (text.size() > (1u << 20)) {
-            std::fwrite(text.data(), 1, text.size(), f);
-            text.clear();
-        }
+        writer.append_row(i, idx.data(), val.data(), idx.size());
     }
-    std::fwrite(text.data(), 1, text.size(), f);
-    std::fclose(f);
+    writer.close();
 
     JObj m;
     m.str("command", "generate").str("version", sfdg_version()).str("output", output);
@@ -478,7 +392,7 @@ int run_eval(int argc, char** argv) {
     row.k = k;
     row.seed = seed;
     metrics(a, b, ell, k, tail, rng, device, row);
-    write_metrics_csv(output, {row});
+    sfdg_tools::write_metrics_csv(output, {row});
 
     JObj m;
     m.str("command", "eval").str("version", sfdg_version()).str("matrix", mpath).str("sketch", spath);
@@ -565,7 +479,7 @@ int run_bench(int argc, char** argv) {
         }
         std::fprintf(stderr, "bench: %s=%zu done\n", sweep.c_str(), v);
     }
-    write_metrics_csv(out_csv, rows);
+    sfdg_tools::write_metrics_csv(out_csv, rows);
 
     JObj m;
     m.str("command", "bench").str("version", sfdg_version()).str("sweep", sweep).num("scale", scale);
