@@ -694,7 +694,9 @@ class Sketcher {
                     trace_begin(L);
                     {
                         std::lock_guard<std::mutex> g(verify_mu);  // keeps the ev_verify chain in order
-                        e.verify_enqueue(L.cur.ver, delta_hat, e.Bp, e.lp, serial_verify ? ev_verify : nullptr);
+                        // cluster verifiers run concurrently; grid ones are chained (co-residency)
+                        e.verify_enqueue(L.cur.ver, delta_hat, e.Bp, e.lp,
+                                         serial_verify && e.verify_cluster == 0 ? ev_verify : nullptr);
                     }
                     trace_end(L);
                     L.cur.pos = e.pos;

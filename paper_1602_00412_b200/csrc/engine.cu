@@ -193,7 +193,8 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     CK(cudaMalloc(&S, (size_t)kmax * lp * sizeof(double)));
     CK(cudaMalloc(&x0, (size_t)d * sizeof(double)));
     CK(cudaMalloc(&ybuf, 2 * (size_t)d * sizeof(double)));
-    verify_blocks = verify_grid_blocks(device, d, lp);
+    verify_cluster = verify_cluster_size(d, lp);
+    verify_blocks = verify_cluster > 0 ? verify_cluster : verify_grid_blocks(device, d, lp);
     CK(cudaMalloc(&tpart, 2 * (size_t)verify_blocks * lp * sizeof(double)));
     CK(cudaMalloc(&tvec, (size_t)lp * sizeof(double)));
     CK(cudaMalloc(&vpart, (size_t)verify_blocks * sizeof(double)));
@@ -472,7 +473,7 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
     args.counts = plan_c.counts;
     args.lpart = scr.take<double>(std::max<int64_t>(1, plan_c.cap_pieces));
     if (serial) CK(cudaStreamWaitEvent(st, serial, 0));
-    verify_launch(args, verify_blocks, st);
+    verify_launch(args, verify_blocks, verify_cluster, st);
     if (serial) CK(cudaEventRecord(serial, st));
     CK(cudaMemcpyAsync(h_scal + 32, vout, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_err + 1, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -90,6 +90,7 @@ class Engine {
     double* h_scal = nullptr;  // pinned mirror
     int* h_err = nullptr;
     int verify_blocks = 0;
+    int verify_cluster = 0;  // > 0: the verifier is one cluster of this many CTAs (no grid barrier)
     // adaptive orthonormalisation schedule (simultaneous_iteration)
     bool adaptive = true;   // SFDG_ORTH_EVERY_SWEEP=1 forces the reference schedule
     int orth_interval = 1;  // sweeps per CholeskyQR2

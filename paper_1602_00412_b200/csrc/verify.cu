@@ -142,7 +142,12 @@ __device__ __forceinline__ double warp_sum4(const double (&v)[4]) {
     return c;
 }
 
-template <int Q>
+// CL = true: the grid is ONE thread-block cluster (8 or 16 CTAs) and the step barriers are
+// hardware cluster barriers (release/acquire at cluster scope, covering the global-memory
+// exchanges) instead of the software grid barrier. A cluster is scheduled atomically, so
+// verifications of different flushes can run concurrently without the co-residency hazard
+// of two spinning grids.
+template <int Q, bool CL>
 __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     extern __shared__ __align__(16) unsigned char vsm[];
     __shared__ double sh[8];
@@ -150,6 +155,10 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     __shared__ double wpart[kVWarps][257];   // per-warp partials of the next t, and |.|^2
     const unsigned nb = gridDim.x;
     const GridBar bar{a.bar, a.bar + 1};
+    auto step_sync = [&]() {
+        if constexpr (CL) cluster_barrier();
+        else grid_sync(bar, nb);
+    };
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int L = a.ell;
     const int64_t rper = (a.m + nb - 1) / nb, cper = (a.d + nb - 1) / nb;
@@ -211,7 +220,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
         }
         block_partials(tn, ns, L, wpart, a.tpart, a.part);
     }
-    grid_sync(bar, nb);
+    step_sync();
     const double nsq0 = grid_total(a.part, nb, sh);
     if (!(nsq0 > 0.0)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
             const int64_t r = rb + q * kVWarps;
             if ((lane & 7) == 0 && r < r1) a.u[r] = tot;
         }
-        grid_sync(bar, nb);
+        step_sync();
         // ---- phase B0 (skewed columns only): pieces of the long columns over the whole grid
         if (a.has_long) {
             const int np = a.counts[1];
@@ -265,7 +274,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
                 sp = warp_sum(sp);
                 if (lane == 0) a.lpart[p] = sp;
             }
-            grid_sync(bar, nb);
+            step_sync();
         }
         // ---- phase B: y over own columns (four per warp in flight); next-t partials and
         // |y|^2 from the same B'^T rows
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
         }
         if (bad) atomicOr(a.err, ERR_NONFINITE_VERIFY);
         block_partials(tn, nsq, L, wpart, tp, a.part);
-        grid_sync(bar, nb);
+        step_sync();
         // ---- phase C: identical decision in every block (shrink.cpp:88-99)
         const double tot = grid_total(a.part, nb, sh);
         if (*((volatile int*)a.err) & ERR_NONFINITE_VERIFY) {
@@ -368,16 +377,17 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
 }
 
 typedef void (*VerifyFn)(VerifyArgs);
-VerifyFn verify_fn(int ell) {
+template <bool CL>
+VerifyFn verify_fn_t(int ell) {
     switch ((ell + 31) / 32) {
-        case 1: return verify_kernel<1>;
-        case 2: return verify_kernel<2>;
-        case 3: return verify_kernel<3>;
-        case 4: return verify_kernel<4>;
-        case 5: return verify_kernel<5>;
-        case 6: return verify_kernel<6>;
-        case 7: return verify_kernel<7>;
-        default: return verify_kernel<8>;
+        case 1: return verify_kernel<1, CL>;
+        case 2: return verify_kernel<2, CL>;
+        case 3: return verify_kernel<3, CL>;
+        case 4: return verify_kernel<4, CL>;
+        case 5: return verify_kernel<5, CL>;
+        case 6: return verify_kernel<6, CL>;
+        case 7: return verify_kernel<7, CL>;
+        default: return verify_kernel<8, CL>;
     }
 }
 
@@ -401,16 +411,34 @@ int verify_grid_blocks(int device, int64_t d, int lp) {
     return nb;
 }
 
-void verify_launch(const VerifyArgs& args_in, int nblocks, cudaStream_t st) {
+int verify_cluster_size(int64_t d, int lp) {
+    // Opt-in (SFDG_VERIFY_CLUSTER=8|16): one cluster per verification, so the flushes in
+    // flight verify concurrently (hardware barriers, no co-residency hazard). Measured on c2
+    // (ms per 100-flush stream): grid 165.8, cluster-16 168.2, cluster-8 228.9 -- a 16-CTA
+    // cluster streams 512 KB of B'^T per CTA per step and waits for 16 free SMs in a GPC, which
+    // cancels the concurrency. Large B' (c3-c5) needs the whole grid's bandwidth anyway.
+    (void)d;
+    (void)lp;
+    int c = 0;
+    if (const char* e = std::getenv("SFDG_VERIFY_CLUSTER")) {
+        const int v = std::atoi(e);
+        c = v >= 16 ? 16 : v >= 8 ? 8 : 0;
+    }
+    return c;
+}
+
+void verify_launch(const VerifyArgs& args_in, int nblocks, int cluster, cudaStream_t st) {
     ProfScope prof("verify", st);
-    VerifyFn fn = verify_fn(args_in.ell);
     static int stage = -1;
     if (stage < 0) {
-        for (VerifyFn f : {verify_kernel<1>, verify_kernel<2>, verify_kernel<3>, verify_kernel<4>, verify_kernel<5>,
-                           verify_kernel<6>, verify_kernel<7>, verify_kernel<8>})
-            allow_max_dynamic_smem(f);
+        for (int ell = 32; ell <= 256; ell += 32) {
+            allow_max_dynamic_smem(verify_fn_t<false>(ell));
+            allow_max_dynamic_smem(verify_fn_t<true>(ell));
+            CK(cudaFuncSetAttribute((const void*)verify_fn_t<true>(ell), cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                    1));
+        }
         cudaFuncAttributes attr;
-        CK(cudaFuncGetAttributes(&attr, (const void*)verify_kernel<8>));
+        CK(cudaFuncGetAttributes(&attr, (const void*)verify_kernel<8, false>));
         int dev = 0, optin = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -419,9 +447,26 @@ void verify_launch(const VerifyArgs& args_in, int nblocks, cudaStream_t st) {
     }
     VerifyArgs args = args_in;
     args.stage_bytes = stage;
-    CK(cudaMemsetAsync(args.bar, 0, 2 * sizeof(unsigned), st));
-    void* params[] = {(void*)&args};
-    CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(nblocks), dim3(kVThreads), params, (size_t)stage, st));
+    if (cluster > 0) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cluster);
+        cfg.blockDim = dim3(kVThreads);
+        cfg.dynamicSmemBytes = (size_t)stage;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, verify_fn_t<true>(args.ell), args));
+    } else {
+        CK(cudaMemsetAsync(args.bar, 0, 2 * sizeof(unsigned), st));
+        void* params[] = {(void*)&args};
+        CK(cudaLaunchCooperativeKernel((const void*)verify_fn_t<false>(args.ell), dim3(nblocks), dim3(kVThreads),
+                                       params, (size_t)stage, st));
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

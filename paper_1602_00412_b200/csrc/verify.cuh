@@ -45,6 +45,7 @@ struct VerifyArgs {
 };
 
 int verify_grid_blocks(int device, int64_t d, int lp);  // cooperative grid for this B' size
-void verify_launch(const VerifyArgs& args, int nblocks, cudaStream_t st);
+int verify_cluster_size(int64_t d, int lp);            // > 0: one cluster of that many CTAs instead
+void verify_launch(const VerifyArgs& args, int nblocks, int cluster, cudaStream_t st);
 
 }  // namespace sfdg

@@ -1,0 +1,53 @@
+#!/usr/bin/env python
+"""trace_report.py -- summarise an SFDG_TRACE timeline (JSON lines from the sketcher).
+
+    SFDG_TRACE=/tmp/t.jsonl python -c '...sketch...'; python tools/trace_report.py /tmp/t.jsonl
+
+Reports, over the window from the first to the last device interval: the busy fraction of
+the dense-shrink chain, of verification (union over lanes; verifications are serialised),
+and of the shrink phase (union over lanes), plus per-phase mean durations.
+"""
+import json
+import sys
+from collections import defaultdict
+
+
+def union(iv):
+    iv = sorted(iv)
+    tot, cur_s, cur_e = 0.0, None, None
+    for s, e in iv:
+        if cur_e is None or s > cur_e:
+            if cur_e is not None:
+                tot += cur_e - cur_s
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    if cur_e is not None:
+        tot += cur_e - cur_s
+    return tot
+
+
+def main(path, last=0):
+    rows = [json.loads(l) for l in open(path) if l.strip()]
+    if last:  # only the last `last` flushes (e.g. the timed step of a bench run)
+        chain = sorted((r for r in rows if r["phase"] == "dense_shrink"), key=lambda r: r["gpu_end_us"])[-last:]
+        lo = min(r["gpu_start_us"] for r in chain)
+        first_ids = {r["flush"] for r in chain}
+        rows = [r for r in rows if r["gpu_end_us"] >= lo - 50e3 and (r["phase"] == "dense_shrink" and r in chain
+                or r["phase"] != "dense_shrink" and r["gpu_start_us"] >= lo - 20e3)]
+    by = defaultdict(list)
+    for r in rows:
+        by[r["phase"]].append((r["gpu_start_us"], r["gpu_end_us"]))
+    t0 = min(s for v in by.values() for s, _ in v)
+    t1 = max(e for v in by.values() for _, e in v)
+    span = t1 - t0
+    print(f"window {span / 1e3:.1f} ms, {len(by.get('dense_shrink', []))} chain steps")
+    for ph in sorted(by):
+        iv = by[ph]
+        d = [e - s for s, e in iv]
+        print(f"{ph:13s} n={len(iv):5d} mean {sum(d) / len(d):8.1f} us  sum {sum(d) / 1e3:8.1f} ms  "
+              f"union busy {100 * union(iv) / span:5.1f}%")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 0)
