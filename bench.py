@@ -406,6 +406,22 @@ def roofline_from_profile(prof: dict, st: dict, n: int, d: int, ell: int, nnz_st
                        "alg_bytes_per_launch": ks.get("alg_bytes_per_launch"),
                        "note": "c2 panels (8 MB) are L2-resident: achieved uses SURVEY 8(d) algorithmic bytes; "
                                "traffic = ncu dram bytes per launch (profiles/)"}
+    # The c2 panels are L2-resident, so the bound that actually applies is the L2 -> SM gather
+    # bandwidth: measured by tools/probe_l2 (the same access pattern without arithmetic).
+    l2 = None
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r01_l2_gather_peak.txt")):
+            if line.startswith("l2_gather_gbs"):
+                l2 = float(line.split()[1])
+    except Exception:
+        pass
+    if l2 and "spmm" in prof and prof["spmm"][1]:
+        ms, cnt = prof["spmm"]
+        gath = 8 * ell * nnz_f + 12 * nnz_f  # one ell-wide panel row per nonzero + the CSR entry
+        gbs = gath / (ms / cnt * 1e-3) / 1e9
+        out["roofline"]["l2_gather"] = {"achieved": round(gbs, 1), "peak": l2, "unit": "GB/s",
+                                        "frac": round(gbs / l2, 4), "bytes_per_launch": gath,
+                                        "peak_source": "profiles/r01_l2_gather_peak.txt (tools/probe_l2)"}
     out["dominant_kernel"] = {"class": dom, "share_of_step": kern[dom]["share"] if dom else None}
     return out
 
