@@ -31,10 +31,11 @@ def main(path, last=0):
     rows = [json.loads(l) for l in open(path) if l.strip()]
     if last:  # only the last `last` flushes (e.g. the timed step of a bench run)
         chain = sorted((r for r in rows if r["phase"] == "dense_shrink"), key=lambda r: r["gpu_end_us"])[-last:]
-        lo = min(r["gpu_start_us"] for r in chain)
-        first_ids = {r["flush"] for r in chain}
-        rows = [r for r in rows if r["gpu_end_us"] >= lo - 50e3 and (r["phase"] == "dense_shrink" and r in chain
-                or r["phase"] != "dense_shrink" and r["gpu_start_us"] >= lo - 20e3)]
+        t_lo = min(r["gpu_start_us"] for r in chain)
+        t_hi = max(r["gpu_end_us"] for r in chain)
+        # the same flush ids recur across sketcher resets: keep intervals inside the step
+        rows = [dict(r, gpu_start_us=max(r["gpu_start_us"], t_lo), gpu_end_us=min(r["gpu_end_us"], t_hi))
+                for r in rows if r["gpu_end_us"] > t_lo and r["gpu_start_us"] < t_hi]  # clipped to the step
     by = defaultdict(list)
     for r in rows:
         by[r["phase"]].append((r["gpu_start_us"], r["gpu_end_us"]))
