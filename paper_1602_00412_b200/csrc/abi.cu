@@ -696,7 +696,9 @@ class Sketcher {
                         std::lock_guard<std::mutex> g(verify_mu);  // keeps the ev_verify chain in order
                         // cluster verifiers run concurrently; grid ones are chained (co-residency)
                         e.verify_enqueue(L.cur.ver, delta_hat, e.Bp, e.lp,
-                                         serial_verify && e.verify_cluster == 0 ? ev_verify : nullptr);
+                                         serial_verify && e.verify_cluster == 0 && !e.verify_as_graph()
+                                             ? ev_verify
+                                             : nullptr);
                     }
                     trace_end(L);
                     L.cur.pos = e.pos;

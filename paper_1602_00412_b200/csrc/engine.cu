@@ -158,6 +158,13 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     }
     CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio));
     CK(cudaStreamCreateWithPriority(&st2, cudaStreamNonBlocking, prio));
+    {
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&vst, cudaStreamNonBlocking, hi));  // kernel-sequence verifier
+        CK(cudaEventCreateWithFlags(&ev_v0, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_v1, cudaEventDisableTiming));
+    }
     for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&ev_read_done[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_bprime, cudaEventDisableTiming));
     if (shared_rng) {
@@ -195,9 +202,13 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     CK(cudaMalloc(&ybuf, 2 * (size_t)d * sizeof(double)));
     verify_cluster = verify_cluster_size(d, lp);
     verify_blocks = verify_cluster > 0 ? verify_cluster : verify_grid_blocks(device, d, lp);
-    CK(cudaMalloc(&tpart, 2 * (size_t)verify_blocks * lp * sizeof(double)));
+    vg_blocks = verify_graph_blocks(device, d);
+    if (const char* e = std::getenv("SFDG_VERIFY_MODE")) use_vgraph = std::string(e) == "graph";
+    const int part_blocks = std::max(2 * verify_blocks, vg_blocks);
+    CK(cudaMalloc(&vstate, verify_state_bytes()));
+    CK(cudaMalloc(&tpart, (size_t)part_blocks * lp * sizeof(double)));
     CK(cudaMalloc(&tvec, (size_t)lp * sizeof(double)));
-    CK(cudaMalloc(&vpart, (size_t)verify_blocks * sizeof(double)));
+    CK(cudaMalloc(&vpart, (size_t)part_blocks * sizeof(double)));
     CK(cudaMalloc(&vout, 4 * sizeof(double)));
     CK(cudaMalloc(&bar, 2 * sizeof(unsigned)));
     CK(cudaMalloc(&d_udrop, 512 * sizeof(int)));
@@ -216,11 +227,14 @@ Engine::~Engine() {
     if (st) cudaStreamSynchronize(st);
     for (auto& kv : graphs)
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& kv : vgraphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     for (void* p : {(void*)Y, (void*)Yt, (void*)W, (void*)Mt[0], (void*)Mt[1], (void*)Bp, (void*)gram, (void*)rinv,
                     (void*)rfac,
                     (void*)dinv8, (void*)kc,
                     (void*)evals, (void*)evecs, (void*)S, (void*)x0, (void*)ybuf, (void*)u, (void*)tpart, (void*)tvec,
-                    (void*)vpart, (void*)vout, (void*)bar, (void*)d_err, (void*)d_scal, (void*)xtmp, (void*)d_udrop})
+                    (void*)vpart, (void*)vout, (void*)bar, (void*)d_err, (void*)d_scal, (void*)xtmp, (void*)d_udrop,
+                    (void*)vstate})
         if (p) cudaFree(p);
     if (h_scal) cudaFreeHost(h_scal);
     if (h_err) cudaFreeHost(h_err);
@@ -236,6 +250,12 @@ Engine::~Engine() {
         if (ev_read_done[i]) cudaEventDestroy(ev_read_done[i]);
     if (ev_bprime) cudaEventDestroy(ev_bprime);
     if (st2) cudaStreamDestroy(st2);
+    if (vst) {
+        cudaStreamSynchronize(vst);
+        cudaStreamDestroy(vst);
+    }
+    if (ev_v0) cudaEventDestroy(ev_v0);
+    if (ev_v1) cudaEventDestroy(ev_v1);
     if (st) cudaStreamDestroy(st);
 }
 
@@ -472,9 +492,55 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
     args.piece_end = plan_c.piece_end;
     args.counts = plan_c.counts;
     args.lpart = scr.take<double>(std::max<int64_t>(1, plan_c.cap_pieces));
-    if (serial) CK(cudaStreamWaitEvent(st, serial, 0));
-    verify_launch(args, verify_blocks, verify_cluster, st);
-    if (serial) CK(cudaEventRecord(serial, st));
+    if (verify_as_graph()) {
+        // kernel-sequence verifier: per-call scalars by a setup kernel, the steps replayed
+        // from a graph captured once per (step count, buffers); no serialisation needed
+        // on a high-priority stream: the steps are short dependent kernels that would
+        // otherwise queue behind the other lanes' SpMMs
+        static const bool prio = !(std::getenv("SFDG_VERIFY_PRIO") && std::atoi(std::getenv("SFDG_VERIFY_PRIO")) == 0);
+        cudaStream_t vs = prio ? vst : st;
+        if (prio) {
+            CK(cudaEventRecord(ev_v0, st));
+            CK(cudaStreamWaitEvent(vst, ev_v0, 0));
+        }
+        verify_setup(vstate, args.scale, args.steps, vs);
+        const std::array<uintptr_t, 18> key{
+            (uintptr_t)args.steps, (uintptr_t)args.m,     (uintptr_t)args.row_ptr, (uintptr_t)args.col,
+            (uintptr_t)args.val,   (uintptr_t)args.col_ptr, (uintptr_t)args.row_idx, (uintptr_t)args.cval,
+            (uintptr_t)args.bt,    (uintptr_t)args.ldb,   (uintptr_t)args.x0,      (uintptr_t)args.u,
+            (uintptr_t)args.ybuf,  (uintptr_t)args.tpart, (uintptr_t)args.t,       (uintptr_t)args.part,
+            (uintptr_t)args.out,   (uintptr_t)vstate};
+        auto it = vgraphs.find(key);
+        if (it == vgraphs.end()) {
+            const uint64_t l0 = g_launches.load();
+            cudaGraph_t graph = nullptr;
+            CK(cudaStreamBeginCapture(vs, cudaStreamCaptureModeThreadLocal));
+            try {
+                verify_sequence(args, vstate, vg_blocks, kSMs, vs);
+            } catch (...) {
+                cudaStreamEndCapture(vs, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            CK(cudaStreamEndCapture(vs, &graph));
+            GraphEntry g;
+            CK(cudaGraphInstantiate(&g.exec, graph, 0));
+            CK(cudaGraphDestroy(graph));
+            g.kernels = g_launches.load() - l0;
+            g_launches.fetch_sub(g.kernels, std::memory_order_relaxed);
+            it = vgraphs.emplace(key, g).first;
+        }
+        CK(cudaGraphLaunch(it->second.exec, vs));
+        g_launches.fetch_add(it->second.kernels, std::memory_order_relaxed);
+        if (prio) {
+            CK(cudaEventRecord(ev_v1, vst));
+            CK(cudaStreamWaitEvent(st, ev_v1, 0));
+        }
+    } else {
+        if (serial) CK(cudaStreamWaitEvent(st, serial, 0));
+        verify_launch(args, verify_blocks, verify_cluster, st);
+        if (serial) CK(cudaEventRecord(serial, st));
+    }
     CK(cudaMemcpyAsync(h_scal + 32, vout, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_err + 1, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
 }

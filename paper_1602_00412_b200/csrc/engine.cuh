@@ -91,6 +91,18 @@ class Engine {
     int* h_err = nullptr;
     int verify_blocks = 0;
     int verify_cluster = 0;  // > 0: the verifier is one cluster of this many CTAs (no grid barrier)
+    int vg_blocks = 0;       // column blocks of the kernel-sequence verifier
+    // SFDG_VERIFY_MODE=graph: the kernel-sequence verifier (concurrent across flushes). Off by
+    // default: on c2 its three dependent kernels per step queue behind the other lanes' work
+    // (2.5 ms per verification, 188 ms per stream) where the cooperative kernel holds its 32
+    // SMs (1.5 ms, 166 ms per stream, serialised).
+    bool use_vgraph = false;
+    void* vstate = nullptr;  // the kernel-sequence verifier's device state
+    cudaStream_t vst = nullptr;  // its high-priority stream (joined to st by events)
+    cudaEvent_t ev_v0 = nullptr, ev_v1 = nullptr;
+    // true when this flush's verification runs as the kernel sequence (concurrent-safe);
+    // the persistent kernels (skewed columns, or opted in) must be serialised by the caller
+    bool verify_as_graph() const { return use_vgraph && plan_c.host_long == 0; }
     // adaptive orthonormalisation schedule (simultaneous_iteration)
     bool adaptive = true;   // SFDG_ORTH_EVERY_SWEEP=1 forces the reference schedule
     int orth_interval = 1;  // sweeps per CholeskyQR2
@@ -124,6 +136,7 @@ class Engine {
         uint64_t kernels = 0;
     };
     std::map<std::array<uintptr_t, 12>, GraphEntry> graphs;
+    std::map<std::array<uintptr_t, 18>, GraphEntry> vgraphs;  // kernel-sequence verifier graphs
     bool use_graphs = true;  // SFDG_GRAPHS=0 disables
     // randsvd.cpp:18-51: Z (m x lp) left in Y.
     void simultaneous_iteration(int k, const PowerCfg& cfg);

@@ -16,6 +16,7 @@
 // B'^T is therefore streamed once per step (it is the bulk: d x ell FP64), not twice.
 // x = y / |y| is never materialised: it is y scaled by 1/|y| on the fly (the reference
 // divides; the two differ by at most one ulp per entry).
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -376,6 +377,245 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     }
 }
 
+
+// ---- the verifier as a kernel sequence (no persistent grid) -----------------------------
+// One power step = three kernels: vg_rows (u = A' x over every row, all SMs), vg_cols (y over
+// every column, the partials of the next t = B' y and of |y|^2 per block), vg_reduce (one
+// block: fixed-order totals, the accept / reject / continue decision, next t). Kernel
+// boundaries replace the grid barriers, so nothing spins and verifications of different
+// flushes overlap freely (no serialisation); the whole sequence for a given step count is
+// captured once as a CUDA graph. Per column / row the arithmetic is the persistent kernel's
+// (same lane order, same warp reductions); only the grouping of the block partials differs.
+// After a decision every later kernel returns at once (state->done).
+struct VState {
+    double scale, log_mag, xscale;
+    int done, verdict, step, steps;
+};
+
+constexpr int kGRowsThreads = 256;
+constexpr int kGColsThreads = 512;
+constexpr int kGColsWarps = kGColsThreads / 32;
+
+__global__ void vg_setup_kernel(VState* st, double scale, int steps) {
+    st->scale = scale;
+    st->log_mag = 0.0;
+    st->xscale = 0.0;
+    st->done = 0;
+    st->verdict = -1;
+    st->step = 0;
+    st->steps = steps;
+}
+
+// u = A' (x xscale): four rows per warp in flight, grid-stride over all rows
+__global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, const VState* __restrict__ st, int step) {
+    if (st->done) return;
+    const double* x = step == 0 ? a.x0 : a.ybuf + (size_t)((step - 1) & 1) * a.d;
+    const double xscale = st->xscale;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t rb = gw; rb < a.m; rb += 4 * nw) {
+        int k0[4], k1[4];
+        int len = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t r = rb + q * nw;
+            k0[q] = r < a.m ? a.row_ptr[r] : 0;
+            k1[q] = r < a.m ? a.row_ptr[r + 1] : 0;
+            len = max(len, k1[q] - k0[q]);
+        }
+        double sp[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int off = lane; off < len; off += 32) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = k0[q] + off;
+                if (k < k1[q]) sp[q] = fma(a.val[k], __ldcg(x + a.col[k]) * xscale, sp[q]);
+            }
+        }
+        const double tot = warp_sum4(sp);
+        const int q = lane >> 3;
+        const int64_t r = rb + q * nw;
+        if ((lane & 7) == 0 && r < a.m) a.u[r] = tot;
+    }
+}
+
+// columns (init = true: the x0 pass -- |x0|^2 and B' x0 partials, no y)
+template <int Q, bool INIT>
+__global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, const VState* __restrict__ st, int step) {
+    __shared__ double tloc[256];
+    __shared__ double wpart[kGColsWarps][257];
+    if (st->done) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int L = a.ell;
+    const int64_t cper = (a.d + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = blockIdx.x * cper, c1 = min((int64_t)a.d, c0 + cper);
+    double* y = a.ybuf + (size_t)(step & 1) * a.d;
+    if (!INIT)
+        for (int j = threadIdx.x; j < L; j += kGColsThreads) tloc[j] = __ldcg(a.t + j);
+    __syncthreads();
+    double tl[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) tl[q] = (!INIT && lane + 32 * q < L) ? tloc[lane + 32 * q] : 0.0;
+    double tn[kMaxQ];
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q) tn[q] = 0.0;
+    double nsq = 0.0;
+    bool bad = false;
+    const double scale = st->scale;
+    for (int64_t cb = c0 + wib; cb < c1; cb += 4 * kGColsWarps) {
+        if (INIT) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t c = cb + q * kGColsWarps;
+                if (c < c1) {
+                    const double xc = a.x0[c];
+                    nsq = fma(xc, xc, nsq);
+#pragma unroll
+                    for (int w = 0; w < Q; ++w) {
+                        const int j = lane + 32 * w;
+                        if (j < L) tn[w] = fma(a.bt[c * a.ldb + j], xc, tn[w]);
+                    }
+                }
+            }
+            continue;
+        }
+        int k0[4], k1[4];
+        int len = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t c = cb + q * kGColsWarps;
+            k0[q] = c < c1 ? a.col_ptr[c] : 0;
+            k1[q] = c < c1 ? a.col_ptr[c + 1] : 0;
+            len = max(len, k1[q] - k0[q]);
+        }
+        double brow[4][Q];
+        double dp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t c = cb + q * kGColsWarps;
+            dp[q] = 0.0;
+#pragma unroll
+            for (int w = 0; w < Q; ++w) {
+                const int j = lane + 32 * w;
+                brow[q][w] = (c < c1 && j < L) ? a.bt[c * a.ldb + j] : 0.0;
+                dp[q] = fma(-brow[q][w], tl[w], dp[q]);
+            }
+        }
+        for (int off = lane; off < len; off += 32) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = k0[q] + off;
+                if (k < k1[q]) dp[q] = fma(a.cval[k], __ldcg(a.u + a.row_idx[k]), dp[q]);
+            }
+        }
+        const double tot = warp_sum4(dp);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t c = cb + q * kGColsWarps;
+            const double yc = scale * __shfl_sync(0xffffffffu, tot, 8 * q);  // shrink.cpp:124
+            if (c < c1) {
+                if (!isfinite(yc)) bad = true;
+                if (lane == 0) y[c] = yc;
+                nsq = fma(yc, yc, nsq);
+#pragma unroll
+                for (int w = 0; w < Q; ++w) tn[w] = fma(brow[q][w], yc, tn[w]);
+            }
+        }
+    }
+    if (bad) atomicOr(a.err, ERR_NONFINITE_VERIFY);
+    // block partials (fixed warp order) -> tpart[block], part[block]
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q)
+        if (lane + 32 * q < L) wpart[wib][lane + 32 * q] = tn[q];
+    if (lane == 0) wpart[wib][256] = nsq;
+    __syncthreads();
+    for (int j = threadIdx.x; j <= 256; j += kGColsThreads) {
+        if (j < L || j == 256) {
+            double sacc = 0.0;
+            for (int w = 0; w < kGColsWarps; ++w) sacc += wpart[w][j];
+            if (j < L) a.tpart[(size_t)blockIdx.x * L + j] = sacc;
+            else a.part[blockIdx.x] = sacc;
+        }
+    }
+}
+
+// one block: totals in fixed block order, the decision (shrink.cpp:88-99) and the next t
+__global__ void __launch_bounds__(512) vg_reduce_kernel(VerifyArgs a, VState* st, int step, int nblk) {
+    __shared__ int s_go;
+    if (st->done) return;
+    const int L = a.ell;
+    if (threadIdx.x < 32) {
+        double sacc = 0.0;
+        for (int b = threadIdx.x; b < nblk; b += 32) sacc += __ldcg(a.part + b);
+        sacc = warp_sum(sacc);
+        if (threadIdx.x == 0) {
+            int go = 1;
+            if (step < 0) {  // after the x0 pass (la_core.cpp:177-186)
+                if (!(sacc > 0.0)) {
+                    atomicOr(a.err, ERR_RNG_U1_ZERO);  // all-zero draw: would need a redraw
+                    st->done = 1;
+                    st->verdict = 0;
+                    go = 0;
+                } else {
+                    st->xscale = 1.0 / sqrt(sacc);
+                }
+            } else {
+                if (*((volatile int*)a.err) & ERR_NONFINITE_VERIFY) {
+                    st->verdict = 0;
+                    st->done = 1;
+                    go = 0;
+                } else if (sacc == 0.0) {
+                    st->verdict = 1;
+                    st->done = 1;
+                    go = 0;
+                } else {
+                    const double nrm = sqrt(sacc);
+                    st->log_mag += log(nrm);
+                    st->step = step + 1;
+                    if (st->log_mag > 0.0 && nrm >= 1.0) {
+                        st->verdict = 0;
+                        st->done = 1;
+                        go = 0;
+                    } else {
+                        st->xscale = 1.0 / nrm;
+                    }
+                }
+            }
+            s_go = go;
+        }
+    }
+    __syncthreads();
+    if (!s_go) return;
+    const double xscale = st->xscale;
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+        double sacc = 0.0;
+        for (int b = 0; b < nblk; ++b) sacc += __ldcg(a.tpart + (size_t)b * L + j);
+        a.t[j] = sacc * xscale;
+    }
+}
+
+__global__ void vg_final_kernel(VerifyArgs a, const VState* st) {
+    const int verdict = st->verdict >= 0 ? st->verdict : (st->log_mag <= 0.0 ? 1 : 0);
+    a.out[0] = (double)verdict;
+    a.out[1] = st->log_mag;
+    a.out[2] = (double)st->step;
+}
+
+typedef void (*VgColsFn)(VerifyArgs, const VState*, int);
+template <bool INIT>
+VgColsFn vg_cols_fn(int ell) {
+    switch ((ell + 31) / 32) {
+        case 1: return vg_cols_kernel<1, INIT>;
+        case 2: return vg_cols_kernel<2, INIT>;
+        case 3: return vg_cols_kernel<3, INIT>;
+        case 4: return vg_cols_kernel<4, INIT>;
+        case 5: return vg_cols_kernel<5, INIT>;
+        case 6: return vg_cols_kernel<6, INIT>;
+        case 7: return vg_cols_kernel<7, INIT>;
+        default: return vg_cols_kernel<8, INIT>;
+    }
+}
+
 typedef void (*VerifyFn)(VerifyArgs);
 template <bool CL>
 VerifyFn verify_fn_t(int ell) {
@@ -468,6 +708,31 @@ void verify_launch(const VerifyArgs& args_in, int nblocks, int cluster, cudaStre
                                        params, (size_t)stage, st));
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+int verify_graph_blocks(int device, int64_t d) {
+    static int sms = 0;
+    if (!sms) CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms, (d + 63) / 64));
+}
+
+size_t verify_state_bytes() { return sizeof(VState); }
+
+void verify_sequence(const VerifyArgs& a, void* state, int nblk, int sms, cudaStream_t st) {
+    VState* s = static_cast<VState*>(state);
+    const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(8 * sms, (a.m + 31) / 32));
+    LAUNCH(vg_cols_fn<true>(a.ell), nblk, kGColsThreads, 0, st, a, s, 0);
+    LAUNCH(vg_reduce_kernel, 1, 512, 0, st, a, s, -1, nblk);
+    for (int step = 0; step < a.steps; ++step) {
+        LAUNCH(vg_rows_kernel, rgrid, kGRowsThreads, 0, st, a, s, step);
+        LAUNCH(vg_cols_fn<false>(a.ell), nblk, kGColsThreads, 0, st, a, s, step);
+        LAUNCH(vg_reduce_kernel, 1, 512, 0, st, a, s, step, nblk);
+    }
+    LAUNCH(vg_final_kernel, 1, 1, 0, st, a, s);
+}
+
+void verify_setup(void* state, double scale, int steps, cudaStream_t st) {
+    LAUNCH(vg_setup_kernel, 1, 1, 0, st, static_cast<VState*>(state), scale, steps);
 }
 
 }  // namespace sfdg

@@ -48,4 +48,14 @@ int verify_grid_blocks(int device, int64_t d, int lp);  // cooperative grid for 
 int verify_cluster_size(int64_t d, int lp);            // > 0: one cluster of that many CTAs instead
 void verify_launch(const VerifyArgs& args, int nblocks, int cluster, cudaStream_t st);
 
+// The verifier as a kernel sequence (three kernels per power step, no persistent grid; see
+// verify.cu). verify_setup writes the per-call scalars (2 / Delta, steps) into `state`
+// (verify_state_bytes() of device memory); verify_sequence enqueues the steps (the caller
+// captures it once per step count as a CUDA graph). tpart: nblk * ell, part: nblk. Columns
+// must have no long-column pieces (has_long == 0).
+int verify_graph_blocks(int device, int64_t d);
+size_t verify_state_bytes();
+void verify_setup(void* state, double scale, int steps, cudaStream_t st);
+void verify_sequence(const VerifyArgs& args, void* state, int nblk, int sms, cudaStream_t st);
+
 }  // namespace sfdg

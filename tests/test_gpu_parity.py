@@ -213,6 +213,29 @@ def test_simultaneous_iteration_near_rank_deficient(oracle):
     assert np.max(np.abs(z @ z.T - zo @ zo.T)) <= 1e-6
 
 
+@pytest.mark.parametrize("env", [{"SFDG_VERIFY_MODE": "graph"}, {"SFDG_VERIFY_CLUSTER": "16"},
+                                 {"SFDG_VERIFY_MODE": "graph", "SFDG_VERIFY_PRIO": "0"}])
+def test_alternative_verifiers_match_oracle(oracle, env):
+    """The opt-in verifier variants (kernel sequence captured as a graph, concurrent across
+    flushes; one 16-CTA cluster with hardware barriers) take the same decisions: sketch and
+    counters equal the oracle's on the c1 prefix (every flush verified)."""
+    rp, cs, vs = S.generate("c1", (0, 4000))
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        b, st = sketch_gpu(rp, cs, vs, 1000, 50, 13)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    bo, so = oracle.sketch(rp, cs, vs, 1000, 50, seed=13)
+    assert btb_rel(b, bo) <= BTB_TOL
+    for key in ("flushes", "attempts", "verifier_i", "delta_spent"):
+        assert st[key] == so[key], key
+
+
 def test_widely_spread_spectrum_stream_vs_oracle(oracle):
     """+-1 rows with two nonzeros (the CLI generator, n 1000, d 100, z 2, seed 2): per-flush
     spectra with lambda_4 / lambda_1 ~ 0.03. Skipping orthonormalisations let CholeskyQR drop
