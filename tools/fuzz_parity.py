@@ -6,7 +6,8 @@ cover (+-1 and integer values, head/tail and Zipf columns, duplicated rows, exac
 low-rank rows, tiny d, ell = 1 and ell = d, delta / power overrides) and checks every run with
 the north_star gates: B^T B within 1e-8 relative Frobenius of the oracle's, counters exact.
 
-    python tools/fuzz_parity.py [--cases 200] [--seed 0] [--max-d 300] [--big] [--out report.json]
+    python tools/fuzz_parity.py [--cases 200] [--seed 0] [--max-d 300] [--big] [--mode sfd|fd|merge]
+                                [--out report.json]
 
 Test infrastructure (uses oracle/); prints one line per failure and a JSON summary.
 """
@@ -140,6 +141,57 @@ def run_case(O, c):
     return res
 
 
+def run_fd_case(O, c):
+    """FdSketcher (sketch.cpp:47-78) on the same streams, densified: B^T B and shrink_count."""
+    rp, cs, vs = make_stream(c)
+    n, d = len(rp) - 1, c["d"]
+    a = np.zeros((n, d))
+    for i in range(n):
+        a[i, cs[rp[i]:rp[i + 1]]] = vs[rp[i]:rp[i + 1]]
+    res = {"case": c, "mode": "fd"}
+    try:
+        bo, co = O.fd_sketch(a, c["ell"])
+    except Exception as e:  # noqa: BLE001
+        bo, co = None, repr(e)
+    try:
+        f = P.FdSketcher(c["ell"], d)
+        if c["seed"] % 2:
+            f.append_csr(rp, cs, vs)
+        else:
+            f.append_rows(a)
+        b = f.finalize()
+        cg = f.shrink_count()
+        f.close()
+    except Exception as e:  # noqa: BLE001
+        b, cg = None, repr(e)
+    if bo is None or b is None:
+        res["ok"] = (bo is None) == (b is None)
+        res["oracle"], res["gpu"] = str(co), str(cg)
+        return res
+    res["btb"] = btb_rel(b, bo)
+    res["counters"] = {"shrink_count": (cg, co)}
+    res["ok"] = res["btb"] <= 1e-8 and cg == co
+    return res
+
+
+def run_merge_case(O, c):
+    """merge (sketch.cpp:80-83) of two shard sketches of the stream (seeds s, s + 1)."""
+    rp, cs, vs = make_stream(c)
+    n = len(rp) - 1
+    h = n // 2
+    parts = []
+    for k, (r0, r1) in enumerate(((0, h), (h, n))):
+        sub = (rp[r0:r1 + 1] - rp[r0], cs[rp[r0]:rp[r1]], vs[rp[r0]:rp[r1]])
+        bo, _ = O.sketch(*sub, c["d"], c["ell"], seed=c["seed"] + k)
+        parts.append(bo)
+    res = {"case": c, "mode": "merge"}
+    mo = O.merge(parts[0], parts[1], c["ell"])
+    mg = P.merge(parts[0], parts[1], c["ell"])
+    res["btb"] = btb_rel(mg, mo)
+    res["ok"] = res["btb"] <= 1e-8
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=200)
@@ -148,6 +200,8 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--big", action="store_true", help="ell 65..256, d 300..max-d, q 1..4")
     ap.add_argument("--case", default="", help="rerun one case given as its JSON dict")
+    ap.add_argument("--mode", default="sfd", choices=["sfd", "fd", "merge"],
+                    help="sfd: SfdSketcher streams; fd: FdSketcher; merge: merge of two shard sketches")
     a = ap.parse_args()
     O = Oracle()
     if a.case:
@@ -158,7 +212,7 @@ def main():
     fails, worst, t0 = [], 0.0, time.time()
     for i in range(a.cases):
         c = draw_case(g, a.max_d, a.big)
-        r = run_case(O, c)
+        r = {"sfd": run_case, "fd": run_fd_case, "merge": run_merge_case}[a.mode](O, c)
         worst = max(worst, r.get("btb", 0.0))
         if not r["ok"]:
             fails.append(r)
