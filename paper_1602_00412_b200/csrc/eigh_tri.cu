@@ -1017,7 +1017,9 @@ bool launch_tridiag_rows(const TriArgs& a, cudaStream_t st) {
     if (env && env[0] == 'p') return false;  // packed single-CTA kernel (A/B testing)
     const int n = a.n;
     const int nt = (n + 31) / 32;
+    static const int min_c = getenv("SFDG_TRIDIAG_MINC") ? atoi(getenv("SFDG_TRIDIAG_MINC")) : 1;  // A/B testing
     for (int C = 1; C <= 16; C *= 2) {
+        if (C < min_c) continue;
         const int rows = (n + C - 1) / C;
         const size_t smem = ((size_t)rows * n + 4 * (size_t)n) * sizeof(double);
         if (smem > 220 * 1024) continue;
