@@ -973,6 +973,258 @@ void backtransform(const double* vh, const double* tau, int n, int nval, const i
     else launch_backtransform<32>(vh, tau, n, nval, trivial, X, ldx, st);
 }
 
+// Single-CTA fused tridiagonalisation on the packed lower triangle (row i holds columns
+// 0..i at i(i+1)/2), for matrices whose full square would need a cluster (n ~ 167..220):
+// the whole step stays inside one SM, with block barriers (~26 ns) instead of cluster
+// barriers (~240 ns, tools/probe_cbar) and no DSMEM broadcasts. Step k (algebra of
+// tridiag_rows_kernel / dsytd2, the update of step k-1 applied lazily):
+//   S0 (all threads): p_{k-1,j} = tau_{k-1} (rowdot_j + sum_w colpart_w,j), fixed order.
+//   S1 (warp 0): c_{k-1} = tau_{k-1}/2 p_{k-1}^T v_{k-1}, w_{k-1} = p_{k-1} - c v_{k-1};
+//      apply update k-1 to column k; Householder (dlarfg) on column k -> v_k, tau_k.
+//   S2 (every warp, rows i > k, lanes over columns k < j <= i): a_ij -= v_i w_j + w_i v_j
+//      (update k-1) and, from the updated value, the row part sum_j a_ij v_kj of p_k,i
+//      (4-row transposed warp reduction) and the column part a_ij v_ki of p_k,j (per-lane
+//      registers, one colpart row per warp) -- the symmetric matvec over the packed triangle.
+// Three block barriers per step; each stored element is read and written once per step.
+struct TriPackedLayout {
+    size_t L, wpart, rd, pf, wv, vb, total;  // offsets in doubles
+};
+__host__ __device__ inline TriPackedLayout tri_packed_layout(int n, int nw) {
+    TriPackedLayout o;
+    o.L = 0;
+    o.wpart = ((size_t)n * (n + 1) / 2 + 1) & ~(size_t)1;  // 16-byte aligned rows
+    o.rd = o.wpart + (size_t)nw * n;
+    o.pf = o.rd + n;
+    o.wv = o.pf + n;
+    o.vb = o.wv + n;  // 2 x n
+    o.total = o.vb + 2 * (size_t)n;
+    return o;
+}
+
+template <int NT, int NTHR>
+__global__ void __launch_bounds__(NTHR) tridiag_packed_kernel(TriArgs a) {
+    constexpr int NW = NTHR / 32;
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    __shared__ double s_tau;
+    const int n = a.n;
+    const TriPackedLayout lay = tri_packed_layout(n, NW);
+    double* L = sm + lay.L;
+    double* wpart = sm + lay.wpart;
+    double* rd = sm + lay.rd;
+    double* pf = sm + lay.pf;
+    double* wv = sm + lay.wv;
+    double* vb = sm + lay.vb;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto tri = [](int i) { return i * (i + 1) / 2; };
+    double off = 0.0;
+    for (int i = warp; i < n; i += NW) {
+        double* Li = L + tri(i);
+        for (int j = lane; j <= i; j += 32) {
+            const double v = a.K[(size_t)i * a.ldk + j];
+            Li[j] = v;
+            if (j != i) off += 2.0 * v * v;
+        }
+    }
+    for (int j = tid; j < n; j += NTHR) {
+        pf[j] = 0.0;
+        wv[j] = 0.0;
+        rd[j] = 0.0;
+        vb[j] = 0.0;
+        vb[n + j] = 0.0;
+    }
+    double tol_sq = a.tol_sq;
+    if (a.d_fsq) {
+        const double ot = 1e-12 * fmax(*a.d_fsq, 1.0);
+        tol_sq = ot * ot;
+    }
+    off = block_sum(off, red);
+    if (!(off > tol_sq) || n == 1) {  // the reference's Jacobi would not rotate at all (la_core.cpp:33)
+        for (int i = tid; i < n; i += NTHR) {
+            a.d[i] = L[tri(i) + i];
+            if (i + 1 < n) a.e[i] = 0.0;
+        }
+        if (tid == 0) *a.trivial = 1;
+        return;
+    }
+    if (tid == 0) *a.trivial = 0;
+    double tau_prev = 0.0;
+    for (int k = 0; k + 1 < n; ++k) {
+        double* vp = vb + (k & 1 ? 0 : n);  // v_{k-1}
+        double* vc = vb + (k & 1 ? n : 0);  // v_k
+        // ---- S0: p_{k-1} for j >= k
+        if (k > 0) {
+            for (int j = k + tid; j < n; j += NTHR) {
+                double s = rd[j];
+#pragma unroll 4
+                for (int w = 0; w < NW; ++w) s += wpart[(size_t)w * n + j];
+                pf[j] = s * tau_prev;
+            }
+        }
+        __syncthreads();
+        // ---- S1 (warp 0): w_{k-1}, column k, reflector k
+        if (warp == 0) {
+            double pj[NT], vj[NT];
+            double dsum = 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int i = k + lane + 32 * t;
+                pj[t] = i < n ? pf[i] : 0.0;
+                vj[t] = i < n ? vp[i] : 0.0;
+                dsum = fma(pj[t], vj[t], dsum);
+            }
+            dsum = warp_sum(dsum);
+            const double c = 0.5 * tau_prev * dsum;
+            double wj[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int i = k + lane + 32 * t;
+                wj[t] = pj[t] - c * vj[t];
+                if (i < n) wv[i] = wj[t];
+            }
+            const double wk = __shfl_sync(0xffffffffu, wj[0], 0);  // w_{k-1,k}
+            const double vk = __shfl_sync(0xffffffffu, vj[0], 0);  // v_{k-1,k}
+            double x[NT];
+            double xs = 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int i = k + lane + 32 * t;
+                x[t] = 0.0;
+                if (i < n) {
+                    double* p = L + tri(i) + k;
+                    const double val = *p - vj[t] * wk - wj[t] * vk;
+                    *p = val;
+                    x[t] = val;
+                    if (i >= k + 2) xs = fma(val, val, xs);
+                }
+            }
+            xs = warp_sum(xs);
+            const double alpha = __shfl_sync(0xffffffffu, x[0], 1);
+            double tau = 0.0, beta = alpha, scal = 0.0;
+            if (xs > 0.0) {
+                beta = -copysign(sqrt(alpha * alpha + xs), alpha);
+                tau = (beta - alpha) * fast_rcp(beta);
+                scal = fast_rcp(alpha - beta);
+            }
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int i = k + lane + 32 * t;
+                if (i < n) {
+                    const double v = i == k ? 0.0 : (i == k + 1) ? 1.0 : x[t] * scal;
+                    vc[i] = v;
+                    if (i > k) a.vh[(size_t)k * n + i] = v;
+                }
+            }
+            if (lane == 0) {
+                s_tau = tau;
+                a.d[k] = x[0];
+                a.e[k] = beta;
+                a.tau[k] = tau;
+            }
+        }
+        __syncthreads();
+        // ---- S2: rows i > k
+        {
+            const double tau = s_tau;
+            double rv[NT], rw[NT], rc[NT], cp[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = k + 1 + lane + 32 * t;
+                const bool on = j < n;
+                rv[t] = on ? vp[j] : 0.0;
+                rw[t] = on ? wv[j] : 0.0;
+                rc[t] = on ? vc[j] : 0.0;
+                cp[t] = 0.0;
+            }
+            for (int i0 = k + 1 + warp; i0 < n; i0 += 4 * NW) {
+                double sr[4];
+                const int ilast = min(n - 1, i0 + 3 * NW);
+                const int tcnt = (ilast - k - 1) / 32 + 1;  // column chunks the longest row needs
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int i = i0 + r * NW;
+                    sr[r] = 0.0;
+                    if (i < n) {
+                        const double vi = vp[i], wi = wv[i], ci = vc[i];
+                        double* Li = L + tri(i);
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) {
+                            if (t < tcnt) {
+                                const int j = k + 1 + lane + 32 * t;
+                                if (j <= i) {
+                                    const double val = Li[j] - vi * rw[t] - wi * rv[t];
+                                    Li[j] = val;
+                                    sr[r] = fma(val, rc[t], sr[r]);
+                                    if (j < i) cp[t] = fma(val, ci, cp[t]);
+                                }
+                            }
+                        }
+                    }
+                }
+                const bool h16 = lane & 16, h8 = lane & 8;
+                double a0 = h16 ? sr[2] : sr[0], a1 = h16 ? sr[3] : sr[1];
+                a0 += __shfl_xor_sync(0xffffffffu, h16 ? sr[0] : sr[2], 16);
+                a1 += __shfl_xor_sync(0xffffffffu, h16 ? sr[1] : sr[3], 16);
+                double c0 = h8 ? a1 : a0;
+                c0 += __shfl_xor_sync(0xffffffffu, h8 ? a0 : a1, 8);
+                c0 += __shfl_xor_sync(0xffffffffu, c0, 4);
+                c0 += __shfl_xor_sync(0xffffffffu, c0, 2);
+                c0 += __shfl_xor_sync(0xffffffffu, c0, 1);
+                const int i = i0 + (lane >> 3) * NW;
+                if ((lane & 7) == 0 && i < n) rd[i] = c0;
+            }
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = k + 1 + lane + 32 * t;
+                if (j < n) wpart[(size_t)warp * n + j] = cp[t];
+            }
+            tau_prev = tau;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        a.d[n - 1] = L[tri(n - 1) + n - 1];
+        a.tau[n - 1] = 0.0;
+    }
+}
+
+template <int NT, int NTHR>
+void launch_packed(const TriArgs& a, size_t smem, cudaStream_t st) {
+    auto* fn = tridiag_packed_kernel<NT, NTHR>;
+    static bool attr = false;
+    if (!attr) {
+        allow_max_dynamic_smem(fn);
+        attr = true;
+    }
+    static const int excl = getenv("SFDG_TRIDIAG_EXCLUSIVE") ? atoi(getenv("SFDG_TRIDIAG_EXCLUSIVE")) : 1;
+    if (excl) {
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, (const void*)fn));
+        smem = std::max(smem, (size_t)fa.maxDynamicSharedSizeBytes);
+    }
+    LAUNCH(fn, 1, NTHR, smem, st, a);
+}
+
+// The fused packed kernel (opt-in, SFDG_TRIDIAG=f, n <= ~226). Measured on the B200
+// (tools/kbench, eigh top-100): n = 200 1090 us against 944 us for the 2-CTA cluster row
+// kernel, n = 100 414 us against 320 us for the 1-CTA row kernel -- the third barrier and
+// the S0 reduction per step cost more than the cluster barrier they replace, so the row
+// kernels stay the default.
+bool launch_tridiag_packed(const TriArgs& a, cudaStream_t st) {
+    static const char* env = getenv("SFDG_TRIDIAG");
+    if (!(env && env[0] == 'f')) return false;
+    const int n = a.n;
+    if (n < 2) return false;
+    const int nt = (n + 31) / 32;
+    if (nt > 8) return false;
+    const size_t s16 = tri_packed_layout(n, 16).total * sizeof(double);
+    const size_t s8 = tri_packed_layout(n, 8).total * sizeof(double);
+    if (s16 <= 224 * 1024) launch_packed<8, 512>(a, s16, st);
+    else if (s8 <= 224 * 1024) launch_packed<8, 256>(a, s8, st);
+    else return false;
+    return true;
+}
+
 template <int C, int NT, int NTHR>
 void launch_rows(const TriRowsArgs& ra, size_t smem, cudaStream_t st) {
     auto* fn = tridiag_rows_kernel<C, NT, NTHR>;
@@ -1074,7 +1326,7 @@ void eigh_tri(const double* K, int n, int ldk, double off_tol, const double* d_f
     }
     {
         ProfScope prof("eigh_tridiag", st);
-        if (!launch_tridiag_rows(a, st)) {
+        if (!launch_tridiag_packed(a, st) && !launch_tridiag_rows(a, st)) {
             const size_t smem = use_smem ? (packed + 2 * (size_t)n) * sizeof(double) : 0;
             if (use_smem) LAUNCH(tridiag_kernel<true>, 1, kTriThreads, smem, st, a);
             else LAUNCH(tridiag_kernel<false>, 1, kTriThreads, 0, st, a);

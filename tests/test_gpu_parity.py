@@ -152,6 +152,18 @@ def test_eigh_clustered_spectrum(n):
     assert np.max(np.abs(vecs @ np.diag(vals) @ vecs.T - k)) <= 1e-11 * 10
 
 
+def test_fused_packed_tridiagonalisation_eigh():
+    """SFDG_TRIDIAG=f (the opt-in single-CTA packed-triangle kernel, every n it fits) through
+    the eigh parity cases above, in a child process (the switch is read once per process)."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "-k", "eigh_vs_oracle or eigh_clustered or eigh_degenerate or eigh_equal", __file__],
+                       env={**os.environ, "SFDG_TRIDIAG": "f"}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
 def test_eigh_degenerate_and_diagonal():
     k = np.diag([3.0, 1.0, 3.0, 0.0, 2.0])
     vals, vecs = P.eigh(k, 1e-12)
