@@ -338,6 +338,17 @@ def main():
                        "h2d_bytes_per_step": int(nnz * 12 + (n + stats["flushes"]) * 4),
                        "d2h_bytes_per_step": int(ell * d * 8)}
     line.update(roofline_from_profile(prof, pstats, n, d, ell, nnz))
+    rl2 = line.get("roofline", {}).get("l2_gather")
+    if rl2 and "spmm" in prof and prof["spmm"][1]:
+        # Whole-step bound: the SpMM launches of one step move this many bytes L2 -> SM (one
+        # ell-wide FP64 panel row per nonzero), so at the measured gather peak the step cannot
+        # take less than floor_ms even with every other kernel hidden under them.
+        nsp = prof["spmm"][1]
+        gb = nsp * rl2["bytes_per_launch"] / 1e9
+        floor_ms = 1e3 * gb / rl2["peak"]
+        line["step_floor"] = {"bound": "l2_gather", "what": "SpMM gather bytes of one step at the measured "
+                              "L2 gather peak", "spmm_launches": nsp, "gbytes": round(gb, 2),
+                              "floor_ms": round(floor_ms, 2), "frac": round(floor_ms / ms_step, 4)}
     if accuracy is not None:
         line["accuracy"] = accuracy
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -40,7 +40,7 @@ static __thread frame* g_frame;
 
 const char* or_last_error(void) { return g_err; }
 
-static void raise_err(int code, const char* fmt, ...) {
+static _Noreturn void raise_err(int code, const char* fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof g_err, fmt, ap);

@@ -204,7 +204,9 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     verify_blocks = verify_cluster > 0 ? verify_cluster : verify_grid_blocks(device, d, lp);
     vg_blocks = verify_graph_blocks(device, d);
     if (const char* e = std::getenv("SFDG_VERIFY_MODE")) use_vgraph = std::string(e) == "graph";
-    const int part_blocks = std::max(2 * verify_blocks, vg_blocks);
+    int sms_here = 0;
+    CK(cudaDeviceGetAttribute(&sms_here, cudaDevAttrMultiProcessorCount, device));
+    const int part_blocks = std::max(2 * std::max(verify_blocks, sms_here), vg_blocks);  // resident grids: <= 1 per SM
     CK(cudaMalloc(&vstate, verify_state_bytes()));
     CK(cudaMalloc(&tpart, (size_t)part_blocks * lp * sizeof(double)));
     CK(cudaMalloc(&tvec, (size_t)lp * sizeof(double)));
@@ -537,8 +539,16 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
             CK(cudaStreamWaitEvent(st, ev_v1, 0));
         }
     } else {
+        int nb = verify_blocks;
+        if (verify_cluster == 0) {
+            const int rb = verify_resident_blocks(device, a.m, d, ell, a.nnz, verify_blocks);
+            if (rb > 0) {
+                nb = rb;
+                args.resident = 1;
+            }
+        }
         if (serial) CK(cudaStreamWaitEvent(st, serial, 0));
-        verify_launch(args, verify_blocks, verify_cluster, st);
+        verify_launch(args, nb, verify_cluster, st);
         if (serial) CK(cudaEventRecord(serial, st));
     }
     CK(cudaMemcpyAsync(h_scal + 32, vout, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));

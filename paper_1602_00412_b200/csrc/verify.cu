@@ -177,6 +177,22 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     const uint32_t* CI = a.col + rbase;
     const double *RV = a.val + rbase, *CV = a.cval + cbase;
     int rsub = rbase, csub = cbase;
+    // Resident: the block's B'^T rows (nc x L, 8 nc L bytes) stay in shared memory, so the
+    // per-step stream of B'^T (the bulk of a step's bytes) comes from SMEM instead of L2.
+    const size_t need_csr = (need + 15) & ~(size_t)15;
+    const bool resident = a.resident && staged && need_csr + 8 * (size_t)nc * L <= (size_t)a.stage_bytes;
+    const double* BT = a.bt;
+    int64_t ldbt = a.ldb, bt0 = 0;  // row c of B'^T at BT + (c - bt0) * ldbt
+    if (resident) {
+        double* s_b = reinterpret_cast<double*>(vsm + need_csr);
+        for (int e = threadIdx.x; e < nc * L; e += kVThreads) {
+            const int c = e / L, j = e - c * L;
+            s_b[e] = a.bt[(c0 + c) * a.ldb + j];
+        }
+        BT = s_b;
+        ldbt = L;
+        bt0 = c0;
+    }
     if (staged) {
         double* s_rv = reinterpret_cast<double*>(vsm);
         double* s_cv = s_rv + knr;
@@ -216,7 +232,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
                 const int j = lane + 32 * q;
-                if (j < L) tn[q] = fma(a.bt[c * a.ldb + j], xc, tn[q]);
+                if (j < L) tn[q] = fma(BT[(c - bt0) * ldbt + j], xc, tn[q]);
             }
         }
         block_partials(tn, ns, L, wpart, a.tpart, a.part);
@@ -320,7 +336,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
 #pragma unroll
                 for (int w = 0; w < Q; ++w) {
                     const int j = lane + 32 * w;
-                    brow[q][w] = (c < c1 && j < L) ? a.bt[c * a.ldb + j] : 0.0;
+                    brow[q][w] = (c < c1 && j < L) ? BT[(c - bt0) * ldbt + j] : 0.0;
                     dp[q] = fma(-brow[q][w], tl[w], dp[q]);  // - (B'^T t)_c partial
                 }
             }
@@ -649,6 +665,41 @@ int verify_grid_blocks(int device, int64_t d, int lp) {
     int nb = (int)std::max<int64_t>(32, std::min<int64_t>(sms, by_size));
     if (const char* e = std::getenv("SFDG_VERIFY_BLOCKS")) nb = std::max(1, std::min(sms, std::atoi(e)));
     return nb;
+}
+
+namespace {
+int stage_bytes_for(int device) {
+    static int cached = -1;
+    if (cached < 0) {
+        cudaFuncAttributes attr;
+        CK(cudaFuncGetAttributes(&attr, (const void*)verify_kernel<8, false>));
+        int optin = 0;
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        cached = optin - (int)attr.sharedSizeBytes - 1024;
+    }
+    return cached;
+}
+}  // namespace
+
+// Opt-in (SFDG_VERIFY_RESIDENT=1). Measured on c2 (SFDG_TRACE of the timed step, 1 B200): a
+// resident verification takes 1233 us against 1687 us streaming (57 blocks against 32), but
+// the extra SMs it holds stretch the lanes' shrink phase 5023 -> 5271 us, and the stream
+// gets slower overall (170.0 against 166.0 ms); c3-c5 B'^T does not fit at all.
+int verify_resident_blocks(int device, int64_t m, int64_t d, int ell, int64_t nnz, int min_blocks) {
+    const char* e = std::getenv("SFDG_VERIFY_RESIDENT");
+    if (!e || std::atoi(e) == 0) return 0;
+    if (std::getenv("SFDG_VERIFY_BLOCKS")) return 0;  // explicit grid: streaming kernel
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const double stage = (double)stage_bytes_for(device);
+    for (int nb = std::max(1, min_blocks); nb <= sms; ++nb) {
+        // per block: CSR + CSC slices (12 B per entry each, +25% for uneven rows / columns),
+        // their offsets, and the B'^T rows of its columns
+        const double rows = std::ceil((double)m / nb), cols = std::ceil((double)d / nb);
+        const double need = 1.25 * 24.0 * (double)nnz / nb + 4.0 * (rows + cols + 2) + 16 + 8.0 * cols * ell;
+        if (need <= stage) return nb;
+    }
+    return 0;
 }
 
 int verify_cluster_size(int64_t d, int lp) {

@@ -33,6 +33,7 @@ struct VerifyArgs {
     int* err;
     double* out;  // [accepted, log_mag, steps_run]
     int stage_bytes;  // dynamic shared memory for the block's CSR/CSC slices (0 = read from global)
+    int resident;     // 1: also keep the block's B'^T rows in shared memory for all steps
     // Columns longer than 2 kPiece (skewed data: Zipf columns) are split into pieces that every
     // warp of the grid shares (the CSC SegPlan of the SpMM), summed per column in fixed order.
     int has_long;
@@ -45,6 +46,9 @@ struct VerifyArgs {
 };
 
 int verify_grid_blocks(int device, int64_t d, int lp);  // cooperative grid for this B' size
+// Smallest grid (>= the streaming grid, <= one block per SM) whose blocks can hold their
+// B'^T rows and CSR/CSC slices in shared memory for the whole verification; 0 = none.
+int verify_resident_blocks(int device, int64_t m, int64_t d, int ell, int64_t nnz, int min_blocks);
 int verify_cluster_size(int64_t d, int lp);            // > 0: one cluster of that many CTAs instead
 void verify_launch(const VerifyArgs& args, int nblocks, int cluster, cudaStream_t st);
 

@@ -226,10 +226,12 @@ def test_simultaneous_iteration_near_rank_deficient(oracle):
 
 
 @pytest.mark.parametrize("env", [{"SFDG_VERIFY_MODE": "graph"}, {"SFDG_VERIFY_CLUSTER": "16"},
-                                 {"SFDG_VERIFY_MODE": "graph", "SFDG_VERIFY_PRIO": "0"}])
+                                 {"SFDG_VERIFY_MODE": "graph", "SFDG_VERIFY_PRIO": "0"},
+                                 {"SFDG_VERIFY_RESIDENT": "1"}])
 def test_alternative_verifiers_match_oracle(oracle, env):
     """The opt-in verifier variants (kernel sequence captured as a graph, concurrent across
-    flushes; one 16-CTA cluster with hardware barriers) take the same decisions: sketch and
+    flushes; one 16-CTA cluster with hardware barriers; B'^T resident in shared memory over a
+    wider grid) take the same decisions: sketch and
     counters equal the oracle's on the c1 prefix (every flush verified)."""
     rp, cs, vs = S.generate("c1", (0, 4000))
     old = {k: os.environ.get(k) for k in env}
