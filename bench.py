@@ -345,10 +345,14 @@ def main():
         # take less than floor_ms even with every other kernel hidden under them.
         nsp = prof["spmm"][1]
         gb = nsp * rl2["bytes_per_launch"] / 1e9
-        floor_ms = 1e3 * gb / rl2["peak"]
-        line["step_floor"] = {"bound": "l2_gather", "what": "SpMM gather bytes of one step at the measured "
-                              "L2 gather peak", "spmm_launches": nsp, "gbytes": round(gb, 2),
-                              "floor_ms": round(floor_ms, 2), "frac": round(floor_ms / ms_step, 4)}
+        bw = rl2.get("sustained_peak", rl2["peak"])
+        floor_ms = 1e3 * gb / bw
+        line["step_floor"] = {"bound": "l2_gather", "what": "SpMM gather bytes of one step at the sustained "
+                              "L2 gather bandwidth", "spmm_launches": nsp, "gbytes": round(gb, 2),
+                              "floor_ms": round(floor_ms, 2), "frac": round(floor_ms / ms_step, 4),
+                              "serial_launch_ms": round(nsp * rl2["bytes_per_launch"] / (rl2["peak"] * 1e9) * 1e3, 2),
+                              "note": "serial_launch_ms = the same launches back to back at the probe's "
+                                      "same-size launch time; the lanes overlap launches, the ramp is the cost"}
     if accuracy is not None:
         line["accuracy"] = accuracy
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -426,13 +430,26 @@ def roofline_from_profile(prof: dict, st: dict, n: int, d: int, ell: int, nnz_st
                 l2 = float(line.split()[1])
     except Exception:
         pass
+    # Sustained rate of the same pattern in long launches (16x the gathers): a c2-sized launch
+    # spends ~6.7 us of its ~10.6 us in launch ramp and tail (profiles/r01c_l2_gather_sustained.txt).
+    l2s = None
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "r01c_l2_gather_sustained.txt")):
+            if line.startswith("l2_gather_sustained_gbs"):
+                l2s = float(line.split()[1])
+    except Exception:
+        pass
     if l2 and "spmm" in prof and prof["spmm"][1]:
         ms, cnt = prof["spmm"]
         gath = 8 * ell * nnz_f + 12 * nnz_f  # one ell-wide panel row per nonzero + the CSR entry
         gbs = gath / (ms / cnt * 1e-3) / 1e9
         out["roofline"]["l2_gather"] = {"achieved": round(gbs, 1), "peak": l2, "unit": "GB/s",
                                         "frac": round(gbs / l2, 4), "bytes_per_launch": gath,
-                                        "peak_source": "profiles/r01_l2_gather_peak.txt (tools/probe_l2)"}
+                                        "peak_source": "profiles/r01_l2_gather_peak.txt (tools/probe_l2: the same "
+                                                       "gathers in one launch of the same size)"}
+        if l2s:
+            out["roofline"]["l2_gather"].update({"sustained_peak": l2s, "frac_of_sustained": round(gbs / l2s, 4),
+                                                 "sustained_source": "profiles/r01c_l2_gather_sustained.txt"})
     out["dominant_kernel"] = {"class": dom, "share_of_step": kern[dom]["share"] if dom else None}
     return out
 

@@ -48,12 +48,16 @@ __global__ void __launch_bounds__(256, 5) gather(const int* __restrict__ idx, in
     out[(size_t)warp * 64 + lane] = acc0.x + acc0.y + acc1.x + acc1.y;
 }
 
-int main() {
-    const int rows = 10000, ld = 104, ncols = 104, per_warp = 10, ngroups = 10000;
+int main(int argc, char** argv) {
+    // argv[1]: gathers per launch in units of 1e5 (default 1 = one c2 SpMM's worth); larger
+    // values measure the sustained rate without the launch ramp-up and tail of a ~10 us kernel
+    const int scale = argc > 1 ? std::atoi(argv[1]) : 1;
+    const int rows = 10000, ld = 104, ncols = 104, per_warp = 10, ngroups = 10000 * scale;
     const size_t gathers = (size_t)per_warp * ngroups;
     std::vector<int> h_idx(gathers);
     srand(1);
     for (auto& v : h_idx) v = rand() % rows;
+    std::printf("gathers per launch: %zu\n", gathers);
     int* d_idx;
     double *tab, *out, *seq_idx_tab;
     CK(cudaMalloc(&d_idx, gathers * sizeof(int)));
