@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kCholThreads) chol_factor_kernel(const double*
                                                                    double* __restrict__ stats, int* __restrict__ err,
                                                                    int err_bit, double* __restrict__ gscratch,
                                                                    int use_smem, int polar, int* __restrict__ udrop) {
+    pdl_entry();
     extern __shared__ double sm[];
     const int lda = use_smem ? k + 4 : k;
     double* A = use_smem ? sm : gscratch;
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(kTrsmThreads) trsm_apply_kernel(const double* 
                                                                   const double* __restrict__ dinv8,
                                                                   double* __restrict__ X, int ldx,
                                                                   const double* __restrict__ stats, int rows) {
+    pdl_entry();
     if (stats && stats[4] != 0.0) return;
     extern __shared__ double sm[];
     const int kp = (k + 7) / 8 * 8;
@@ -418,6 +420,7 @@ __global__ void __launch_bounds__(kTrsmThreads) trsm_panel_kernel(const double* 
                                                                   const double* __restrict__ dinv8,
                                                                   double* __restrict__ X, int ldx,
                                                                   const double* __restrict__ stats, int rows) {
+    pdl_entry();
     if (stats && stats[4] != 0.0) return;
     extern __shared__ double sm[];
     const int kp = (k + 7) / 8 * 8;
@@ -507,6 +510,7 @@ __global__ void __cluster_dims__(kXC, 1, 1) __launch_bounds__(kXThreads)
     exact_orth_kernel(const double* __restrict__ Y, int ldy, double* __restrict__ Q, int ldq, int m, int k,
                       const int* __restrict__ udrop, const double* __restrict__ stats, double* __restrict__ tmp,
                       int force) {
+    pdl_entry();
     if (!force && !(stats[6] > 0.0)) return;  // uniform over the cluster
     __shared__ double wred[kXWarps][kXMaxK];
     __shared__ double part[2][kXMaxK];

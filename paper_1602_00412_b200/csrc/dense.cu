@@ -50,6 +50,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 template <int VEC>
 __global__ void __launch_bounds__(128) gram_tn_kernel(const double* __restrict__ X, int n, int k, int ldx,
                                                       int rows_per_chunk, int T, double* __restrict__ partial) {
+    pdl_entry();
     extern __shared__ double smg[];  // [stage][A|B][KT][LDT]
     int ti = 0, rem = blockIdx.x;  // linear upper-triangle tile index -> (ti, tj)
     while (rem >= T - ti) {
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(128) gram_tn_kernel(const double* __restrict__
 constexpr int kRedWarps = 8;
 __global__ void __launch_bounds__(32 * kRedWarps) gram_reduce_kernel(const double* __restrict__ partial, int nchunks,
                                                                      int k, double* __restrict__ out, int ldo) {
+    pdl_entry();
     __shared__ double sh[kRedWarps][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int total = k * k;
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(128) gemm_nn_kernel(const double* __restrict__
                                                       const double* __restrict__ S, int c, int lds,
                                                       double* __restrict__ C, int ldc,
                                                       const double* __restrict__ pred) {
+    pdl_entry();
     if (pred && *pred == 0.0) return;
     extern __shared__ double smg[];  // [stage][Xs TB x LDK | Ss KT x LDT]
     constexpr int XS = TB * LDK, SS = KT * LDT;
@@ -227,6 +230,7 @@ constexpr int kRedBlocks = 2 * kSMs;
 // Deterministic sum of squares: fixed grid, fixed per-thread stride order, fixed trees.
 __global__ void sumsq_partial_kernel(const double* __restrict__ X, int64_t rows, int cols, int ld,
                                      double* __restrict__ partial, int* __restrict__ err, int err_bit) {
+    pdl_entry();
     __shared__ double sh[32];
     double s = 0.0;
     bool bad = false;
@@ -250,6 +254,7 @@ __global__ void sumsq_partial_kernel(const double* __restrict__ X, int64_t rows,
 }
 
 __global__ void sum_partials_kernel(const double* __restrict__ partial, int n, double* __restrict__ out) {
+    pdl_entry();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double s = 0.0;
         for (int i = 0; i < n; ++i) s += partial[i];
@@ -259,6 +264,7 @@ __global__ void sum_partials_kernel(const double* __restrict__ partial, int n, d
 
 __global__ void transpose_kernel(const double* __restrict__ in, int rows, int cols, int ldi, double* __restrict__ out,
                                  int ldo) {
+    pdl_entry();
     __shared__ double tile[32][33];
     const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
     for (int j = threadIdx.y; j < 32; j += blockDim.y) {
@@ -274,12 +280,14 @@ __global__ void transpose_kernel(const double* __restrict__ in, int rows, int co
 
 __global__ void copy2d_kernel(const double* __restrict__ in, int rows, int cols, int ldi, double* __restrict__ out,
                               int ldo) {
+    pdl_entry();
     const int64_t total = (int64_t)rows * cols;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
         out[(e / cols) * ldo + e % cols] = in[(e / cols) * ldi + e % cols];
 }
 
 __global__ void fill2d_kernel(double* __restrict__ out, int rows, int cols, int ldo, double v) {
+    pdl_entry();
     const int64_t total = (int64_t)rows * cols;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
         out[(e / cols) * ldo + e % cols] = v;

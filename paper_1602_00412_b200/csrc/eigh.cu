@@ -74,6 +74,7 @@ struct JacArgs {
 // packed index of any element of a 2 x 2 block costs one compare and one add.
 template <bool SMEM, bool TABLE>
 __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(JacArgs a) {
+    pdl_entry();
     if (a.only_if && *a.only_if == 0) return;
     extern __shared__ double sm[];
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -204,6 +205,7 @@ constexpr int kChunk = 8;
 __global__ void __launch_bounds__(kVRows * 32) vapply_kernel(int n, int N, const double2* __restrict__ rotlog,
                                                              const int* __restrict__ nrounds, double* __restrict__ V,
                                                              const int* __restrict__ only_if) {
+    pdl_entry();
     if (only_if && *only_if == 0) return;
     extern __shared__ double sm[];
     const int P = N / 2;
@@ -248,6 +250,7 @@ __global__ void __launch_bounds__(kVRows * 32) vapply_kernel(int n, int N, const
 __global__ void sort_kernel(int n, int N, const double* __restrict__ diag, const double* __restrict__ V,
                             double* __restrict__ values, double* __restrict__ out, int ldo,
                             const int* __restrict__ only_if) {
+    pdl_entry();
     if (only_if && *only_if == 0) return;
     __shared__ int rank[1024];
     for (int i = threadIdx.x; i < n; i += blockDim.x) {

@@ -77,6 +77,7 @@ __device__ double block_sum(double v, double* red) {
 
 template <bool SMEM>
 __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(TriArgs a) {
+    pdl_entry();
     extern __shared__ double sm[];
     __shared__ double red[32];
     __shared__ int tri[1024];
@@ -195,6 +196,7 @@ struct TriRowsArgs {
 
 template <int C, int NT, int NTHR>
 __global__ void __launch_bounds__(NTHR) tridiag_rows_kernel(TriRowsArgs ra) {
+    pdl_entry();
     constexpr int NW = NTHR / 32;
     extern __shared__ double sm[];
     __shared__ double s_sc[2][2];  // [k & 1] = {tau_k, c_{k-1}}
@@ -396,6 +398,7 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
 constexpr int kShifts = SFDG_BISECT_SHIFTS;
 __global__ void bisect_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int nval,
                               const int* __restrict__ trivial, double* __restrict__ lam_desc) {
+    pdl_entry();
     extern __shared__ double sh[];
     double* d = sh;
     double* e2 = sh + n;
@@ -482,6 +485,7 @@ __global__ void inviter_kernel(const double* __restrict__ dg, const double* __re
                                const double* __restrict__ lam, const int* __restrict__ trivial,
                                double* __restrict__ X, int ldx, double* __restrict__ work_g,
                                const int* __restrict__ need) {
+    pdl_entry();
     extern __shared__ double sh_inv[];
     __shared__ double s_tn;
     double* d = sh_inv;
@@ -646,6 +650,7 @@ constexpr int kEPW = 16;
 __global__ void twisted_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int nval,
                                const double* __restrict__ lam, const int* __restrict__ trivial,
                                double* __restrict__ X, int ldx, int* __restrict__ need) {
+    pdl_entry();
     extern __shared__ double tw_s[];
     double* a = tw_s;          // n diagonal
     double* b2 = tw_s + n;     // n-1 squared off-diagonals
@@ -767,6 +772,7 @@ constexpr int kMaxCluster = 32;
 __global__ void cluster_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int n, int nval,
                                double* __restrict__ lam, const int* __restrict__ trivial, double* __restrict__ X,
                                int ldx, int* __restrict__ fallback) {
+    pdl_entry();
     __shared__ double Cm[1][kMaxCluster * kMaxCluster];
     __shared__ double Vm[1][kMaxCluster * kMaxCluster];
     const int lane = threadIdx.x & 31, w = 0;
@@ -900,6 +906,7 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double* __rest
                                                             const double* __restrict__ tau, int n, int nval,
                                                             const int* __restrict__ trivial, double* __restrict__ X,
                                                             int ldx, int R) {
+    pdl_entry();
     if (*trivial) return;
     extern __shared__ double vs[];  // R x n reflector rows, then R taus
     double* ts = vs + (size_t)R * n;
@@ -1003,6 +1010,7 @@ __host__ __device__ inline TriPackedLayout tri_packed_layout(int n, int nw) {
 
 template <int NT, int NTHR>
 __global__ void __launch_bounds__(NTHR) tridiag_packed_kernel(TriArgs a) {
+    pdl_entry();
     constexpr int NW = NTHR / 32;
     extern __shared__ double sm[];
     __shared__ double red[32];

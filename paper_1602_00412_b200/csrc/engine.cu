@@ -27,11 +27,17 @@ namespace sfdg {
 
 std::atomic<uint64_t> g_launches{0};
 
+bool pdl_enabled() {
+    static const bool on = !(std::getenv("SFDG_PDL") && std::atoi(std::getenv("SFDG_PDL")) == 0);
+    return on;
+}
+
 namespace {
 
 // out (R x R) = K restricted to the index map a -> a < n1 ? a : off + (a - n1)
 __global__ void compact_kernel(const double* __restrict__ K, int ldk, int n1, int off, int R, double* __restrict__ out,
                                double* __restrict__ trace_out) {
+    pdl_entry();
     __shared__ double sh[32];
     double tr = 0.0;
     for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < R * R; e += blockDim.x * gridDim.x) {
@@ -60,6 +66,7 @@ __global__ void compact_kernel(const double* __restrict__ K, int ldk, int n1, in
 // shrink.cpp:15-26). S is kcols x lds, zero elsewhere.
 __global__ void shrink_weights_kernel(const double* __restrict__ evals, const double* __restrict__ U, int R, int ell,
                                       int n1, int off, double* __restrict__ S, int kcols, int lds) {
+    pdl_entry();
     __shared__ double w[512];
     const double s0 = sqrt(fmax(evals[0], 0.0));
     const double sl = sqrt(fmax(evals[ell - 1], 0.0));
@@ -90,6 +97,7 @@ __global__ void shrink_weights_kernel(const double* __restrict__ evals, const do
 // dense_shrink tall path (shrink.cpp:53-60): B^T[t][i] = shrunk_i * V[t][i].
 __global__ void tall_shrink_kernel(const double* __restrict__ evals, const double* __restrict__ V, int dd, int ell,
                                    double* __restrict__ bt, int ldo, int lp) {
+    pdl_entry();
     const double sl = sqrt(fmax(evals[ell - 1], 0.0));
     const double floor_sq = __dmul_rn(sl, sl);
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < dd * lp; e += gridDim.x * blockDim.x) {
@@ -107,6 +115,7 @@ __global__ void tall_shrink_kernel(const double* __restrict__ evals, const doubl
 // densify (sparse.cpp:71-78) straight into transposed columns: Tt[col][off + row] = val
 __global__ void densify_t_kernel(const int* __restrict__ row_ptr, const uint32_t* __restrict__ col,
                                  const double* __restrict__ val, int m, double* __restrict__ Tt, int ld, int off) {
+    pdl_entry();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     for (int r = warp; r < m; r += nw)

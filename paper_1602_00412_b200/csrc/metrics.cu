@@ -24,6 +24,7 @@ constexpr int kMBlocks = 2 * kSMs;
 // part[b][j] = sum_{c in block b's rows} bt[c][j] * x[c * 2]   (t = B x, split over rows of B^T)
 __global__ void bt_x_partial_kernel(const double* __restrict__ bt, int ldb, int d, int L, const double* __restrict__ x2,
                                     double* __restrict__ part) {
+    pdl_entry();
     const int per = (d + gridDim.x - 1) / gridDim.x;
     const int c0 = blockIdx.x * per, c1 = min(d, c0 + per);
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
@@ -34,6 +35,7 @@ __global__ void bt_x_partial_kernel(const double* __restrict__ bt, int ldb, int 
 }
 
 __global__ void bt_x_reduce_kernel(const double* __restrict__ part, int nb, int L, double* __restrict__ t) {
+    pdl_entry();
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
         double s = 0.0;
         for (int b = 0; b < nb; ++b) s += part[(size_t)b * L + j];  // fixed order
@@ -44,6 +46,7 @@ __global__ void bt_x_reduce_kernel(const double* __restrict__ part, int nb, int 
 // z[c] = (A^T A x)[c] - (B^T t)[c]  (z2 column 0 holds A^T u); per-block partials of x.z, z.z
 __global__ void diff_dots_kernel(const double* __restrict__ bt, int ldb, int d, int L, const double* __restrict__ t,
                                  double* __restrict__ z2, const double* __restrict__ x2, double* __restrict__ part) {
+    pdl_entry();
     __shared__ double sd[32], sn[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double pd = 0.0, pn = 0.0;
@@ -75,6 +78,7 @@ __global__ void diff_dots_kernel(const double* __restrict__ bt, int ldb, int d, 
 
 // sc: [0] rayleigh, [1] |y|^2 of this step, [2] annihilated (sticky), [3] non-finite (sticky)
 __global__ void step_scalars_kernel(const double* __restrict__ part, int nb, double* __restrict__ sc) {
+    pdl_entry();
     if (threadIdx.x != 0) return;
     double dot = 0.0, nrm = 0.0;
     for (int b = 0; b < nb; ++b) {
@@ -94,6 +98,7 @@ __global__ void step_scalars_kernel(const double* __restrict__ part, int nb, dou
 // x = z / |z| (column 0 of the 2-wide panels), frozen once the reference would have stopped
 __global__ void normalize_kernel(const double* __restrict__ z2, double* __restrict__ x2, int d,
                                  const double* __restrict__ sc) {
+    pdl_entry();
     if (sc[2] != 0.0 || sc[3] != 0.0) return;
     const double inv = 1.0 / sqrt(sc[1]);
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d; c += gridDim.x * blockDim.x)
@@ -102,6 +107,7 @@ __global__ void normalize_kernel(const double* __restrict__ z2, double* __restri
 
 // |x0|^2 partials of the raw normals, then x = x0 / |x0| (unit_sphere_vector, la_core.cpp:174-189)
 __global__ void sumsq2_partial_kernel(const double* __restrict__ x2, int d, double* __restrict__ part) {
+    pdl_entry();
     __shared__ double sh[32];
     double s = 0.0;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d; c += gridDim.x * blockDim.x)
@@ -119,6 +125,7 @@ __global__ void sumsq2_partial_kernel(const double* __restrict__ x2, int d, doub
 
 __global__ void unit_scale_kernel(double* __restrict__ x2, int d, const double* __restrict__ part, int nb,
                                   int* __restrict__ err) {
+    pdl_entry();
     __shared__ double inv;
     if (threadIdx.x == 0) {
         double s = 0.0;

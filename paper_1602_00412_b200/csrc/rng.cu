@@ -41,6 +41,7 @@ __device__ __forceinline__ uint64_t temper(uint64_t x) {
 // G .. G + 156*steps - 1 (output word j = temper(x[312 + j])) into ring[j & mask].
 __global__ void __launch_bounds__(MT_M) mt_generate_kernel(uint64_t* __restrict__ window, uint64_t* __restrict__ ring,
                                                            uint64_t ring_mask, uint64_t first_word, int steps) {
+    pdl_entry();
     __shared__ uint64_t r[2 * MT_N];  // slot = local index mod 624
     const int t = threadIdx.x;
     r[t] = window[t];
@@ -80,6 +81,7 @@ __device__ __forceinline__ void box_muller_pair(uint64_t e1, uint64_t e2, double
 __global__ void box_muller_kernel(const uint64_t* __restrict__ ring, uint64_t ring_mask, uint64_t w0,
                                   int has_spare, const double* __restrict__ spare_in, uint64_t n, uint64_t cols,
                                   uint64_t ld, double* __restrict__ out, int* __restrict__ err) {
+    pdl_entry();
     const uint64_t s = has_spare ? 1 : 0;
     const uint64_t rest = n > s ? n - s : 0;
     const uint64_t pairs = (rest + 1) / 2;
@@ -106,12 +108,14 @@ __global__ void box_muller_kernel(const uint64_t* __restrict__ ring, uint64_t ri
 
 __global__ void spare_kernel(const uint64_t* __restrict__ ring, uint64_t ring_mask, uint64_t w, double* __restrict__ out,
                              int* __restrict__ err) {
+    pdl_entry();
     double c, sn;
     box_muller_pair(ring[(w - 2) & ring_mask], ring[(w - 1) & ring_mask], c, sn, err);
     *out = sn;
 }
 
 __global__ void zero_pad_kernel(double* __restrict__ out, uint64_t rows, uint64_t cols, uint64_t ld) {
+    pdl_entry();
     const uint64_t padw = ld - cols;
     const uint64_t total = rows * padw;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x)

@@ -25,6 +25,7 @@ constexpr int kScanItems = 4;  // 4096 elements per block
 // ---------------------------------------------------------------- exclusive scan
 __global__ void scan_block_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n,
                                   int64_t* __restrict__ block_sums) {
+    pdl_entry();
     __shared__ int64_t warp_tot[32];
     const int64_t base = (int64_t)blockIdx.x * kScanBlock * kScanItems;
     int64_t v[kScanItems];
@@ -66,6 +67,7 @@ __global__ void scan_block_kernel(const int64_t* __restrict__ in, int64_t* __res
 }
 
 __global__ void scan_add_kernel(int64_t* __restrict__ out, int64_t n, const int64_t* __restrict__ block_offs) {
+    pdl_entry();
     const int64_t base = (int64_t)blockIdx.x * kScanBlock * kScanItems;
     const int64_t add = block_offs[blockIdx.x];
     for (int i = threadIdx.x; i < kScanBlock * kScanItems; i += kScanBlock) {
@@ -82,6 +84,7 @@ constexpr int kRadixTile = kRadixWarps * kRadixItemsPerWarp;
 
 __global__ void radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift, int ntiles,
                                   int64_t* __restrict__ hist /* [256][ntiles] */) {
+    pdl_entry();
     __shared__ int cnt[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
@@ -97,6 +100,7 @@ __global__ void radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, 
 __global__ void radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                                      uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int64_t n,
                                      int shift, int ntiles, const int64_t* __restrict__ offs /* [256][ntiles] */) {
+    pdl_entry();
     __shared__ int cnt[kRadixWarps][256];
     for (int i = threadIdx.x; i < kRadixWarps * 256; i += blockDim.x) (&cnt[0][0])[i] = 0;
     __syncthreads();
@@ -146,12 +150,14 @@ __global__ void radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const
 }
 
 __global__ void iota_kernel(uint32_t* __restrict__ v, int64_t n) {
+    pdl_entry();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         v[i] = (uint32_t)i;
 }
 
 // row id of every stored entry (warp per row)
 __global__ void expand_rows_kernel(const int* __restrict__ row_ptr, int m, uint32_t* __restrict__ row_of) {
+    pdl_entry();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -162,6 +168,7 @@ __global__ void expand_rows_kernel(const int* __restrict__ row_ptr, int m, uint3
 __global__ void csc_fill_kernel(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ row_of,
                                 const double* __restrict__ val, int64_t n, int* __restrict__ row_idx,
                                 double* __restrict__ cval) {
+    pdl_entry();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t k = perm[i];
         row_idx[i] = (int)row_of[k];
@@ -171,6 +178,7 @@ __global__ void csc_fill_kernel(const uint32_t* __restrict__ perm, const uint32_
 
 // col_ptr[c] = first position with key >= c (sorted keys)
 __global__ void col_ptr_kernel(const uint32_t* __restrict__ skeys, int64_t n, int d, int* __restrict__ col_ptr) {
+    pdl_entry();
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= d; c += gridDim.x * blockDim.x) {
         int64_t lo = 0, hi = n;
         while (lo < hi) {
@@ -185,6 +193,7 @@ __global__ void col_ptr_kernel(const uint32_t* __restrict__ skeys, int64_t n, in
 // ---------------------------------------------------------------- segment plans
 __global__ void plan_count_kernel(const int* __restrict__ ptr, int nrows, int piece, int64_t* __restrict__ is_long,
                                   int64_t* __restrict__ npieces) {
+    pdl_entry();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
         const int len = ptr[r + 1] - ptr[r];
         const bool lg = len > 2 * piece;
@@ -197,6 +206,7 @@ __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int pie
                                  const int64_t* __restrict__ long_off, const int64_t* __restrict__ piece_off,
                                  int* __restrict__ long_rows, int* __restrict__ long_first, int* __restrict__ piece_beg,
                                  int* __restrict__ piece_end, int* __restrict__ counts /* [nlong, npieces] */) {
+    pdl_entry();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
         const int len = ptr[r + 1] - ptr[r];
         if (len > 2 * piece) {
@@ -276,6 +286,7 @@ __global__ void __launch_bounds__(256, (J <= 2 ? 5 : 1)) spmm_rows_kernel(const 
                                                                         const double* __restrict__ val,
                                  int nrows, int piece, const double* __restrict__ in, int ld, int ncols,
                                  double* __restrict__ out, int ldo) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -299,6 +310,7 @@ __global__ void spmm_pieces_kernel(const int* __restrict__ piece_beg, const int*
                                    const int* __restrict__ counts, const int* __restrict__ idx,
                                    const double* __restrict__ val, const double* __restrict__ in, int ld, int ncols,
                                    double* __restrict__ partial /* [npieces][ld] */) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -319,6 +331,7 @@ __global__ void spmm_pieces_kernel(const int* __restrict__ piece_beg, const int*
 __global__ void spmm_fixup_kernel(const int* __restrict__ long_rows, const int* __restrict__ long_first,
                                   const int* __restrict__ counts, const double* __restrict__ partial, int ld,
                                   int ncols, double* __restrict__ out, int ldo) {
+    pdl_entry();
     const int nl = counts[0];
     const int npieces = counts[1];
     for (int li = blockIdx.x; li < nl; li += gridDim.x) {
@@ -339,6 +352,7 @@ __global__ void spmm_fixup_kernel(const int* __restrict__ long_rows, const int* 
 __global__ void validate_rows_kernel(const int64_t* __restrict__ row_ptr, int64_t nrows, const uint32_t* __restrict__ cols,
                                      const double* __restrict__ vals, uint32_t d, unsigned long long* __restrict__ first_bad,
                                      int* __restrict__ kind) {
+    pdl_entry();
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -360,6 +374,7 @@ __global__ void validate_rows_kernel(const int64_t* __restrict__ row_ptr, int64_
 
 // ---------------------------------------------------------------- misc
 __global__ void rebase_rows_kernel(const int64_t* __restrict__ src, int64_t base, int m, int* __restrict__ dst) {
+    pdl_entry();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += gridDim.x * blockDim.x)
         dst[i] = (int)(src[i] - base);
 }

@@ -150,6 +150,7 @@ __device__ __forceinline__ double warp_sum4(const double (&v)[4]) {
 // of two spinning grids.
 template <int Q, bool CL>
 __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
+    pdl_entry();
     extern __shared__ __align__(16) unsigned char vsm[];
     __shared__ double sh[8];
     __shared__ double tloc[256];             // current t = B' x
@@ -413,6 +414,7 @@ constexpr int kGColsThreads = 512;
 constexpr int kGColsWarps = kGColsThreads / 32;
 
 __global__ void vg_setup_kernel(VState* st, double scale, int steps) {
+    pdl_entry();
     st->scale = scale;
     st->log_mag = 0.0;
     st->xscale = 0.0;
@@ -424,6 +426,7 @@ __global__ void vg_setup_kernel(VState* st, double scale, int steps) {
 
 // u = A' (x xscale): four rows per warp in flight, grid-stride over all rows
 __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, const VState* __restrict__ st, int step) {
+    pdl_entry();
     if (st->done) return;
     const double* x = step == 0 ? a.x0 : a.ybuf + (size_t)((step - 1) & 1) * a.d;
     const double xscale = st->xscale;
@@ -458,6 +461,7 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, co
 // columns (init = true: the x0 pass -- |x0|^2 and B' x0 partials, no y)
 template <int Q, bool INIT>
 __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, const VState* __restrict__ st, int step) {
+    pdl_entry();
     __shared__ double tloc[256];
     __shared__ double wpart[kGColsWarps][257];
     if (st->done) return;
@@ -557,6 +561,7 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
 
 // one block: totals in fixed block order, the decision (shrink.cpp:88-99) and the next t
 __global__ void __launch_bounds__(512) vg_reduce_kernel(VerifyArgs a, VState* st, int step, int nblk) {
+    pdl_entry();
     __shared__ int s_go;
     if (st->done) return;
     const int L = a.ell;
@@ -611,6 +616,7 @@ __global__ void __launch_bounds__(512) vg_reduce_kernel(VerifyArgs a, VState* st
 }
 
 __global__ void vg_final_kernel(VerifyArgs a, const VState* st) {
+    pdl_entry();
     const int verdict = st->verdict >= 0 ? st->verdict : (st->log_mag <= 0.0 ? 1 : 0);
     a.out[0] = (double)verdict;
     a.out[1] = st->log_mag;
