@@ -188,6 +188,13 @@ __global__ void __launch_bounds__(kTriThreads) tridiag_kernel(TriArgs a) {
 //      the same pass p_k,i = tau_k sum_j a_ij v_k,j; broadcast p_k,i.
 // Two (cluster) barriers per step; each element is read and written once per step, with
 // lanes over columns (conflict-free rows). Algebra as tridiag_kernel (dsytd2).
+#ifdef SFDG_TRI_PROBE  // tools/tri_probe: per-step clock64 stamps of the single-CTA row kernel
+__device__ long long g_tri_probe[8 * 1100];
+#define TPROBE(i, cond) \
+    if (cond) g_tri_probe[8 * k + (i)] = clock64();
+#else
+#define TPROBE(i, cond)
+#endif
 struct TriRowsArgs {
     TriArgs a;
     int C;      // CTAs in the cluster
@@ -252,6 +259,7 @@ __global__ void __launch_bounds__(NTHR) tridiag_rows_kernel(TriRowsArgs ra) {
         const int cur = k & 1, prv = cur ^ 1;
         const double* vp = vbuf + prv * n;
         const double* pp = pbuf + prv * n;
+        TPROBE(0, tid == 0)
         // ---- S1: owner warp of row k
         if ((int)rank == k % C && wl == (k / C) % NW) {
             double dsum = 0.0;
@@ -306,8 +314,10 @@ __global__ void __launch_bounds__(NTHR) tridiag_rows_kernel(TriRowsArgs ra) {
                 a.e[k] = beta;
                 a.tau[k] = tau;
             }
+            TPROBE(1, lane == 0)
         }
         bar();
+        TPROBE(2, tid == 0)
         // ---- S2: rows i > k: update of step k-1, p_k = tau_k A v_k
         {
             const double tau = s_sc[cur][0], cprev = s_sc[cur][1];
@@ -367,7 +377,10 @@ __global__ void __launch_bounds__(NTHR) tridiag_rows_kernel(TriRowsArgs ra) {
                 }
             }
         }
+        TPROBE(3, tid == 0)
+        TPROBE(4, tid == 32 * (NW - 1))
         bar();
+        TPROBE(5, tid == 0)
     }
     if ((int)rank == (n - 1) % C && tid == 0) {
         a.d[n - 1] = A[(size_t)((n - 1) / C) * n + n - 1];
