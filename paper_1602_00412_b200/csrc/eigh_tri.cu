@@ -389,6 +389,222 @@ __global__ void __launch_bounds__(NTHR) tridiag_rows_kernel(TriRowsArgs ra) {
     }
 }
 
+// Register-resident variant of tridiag_rows_kernel (same row distribution, same algebra and
+// summation order, same two barriers per step): each warp keeps its rows of the matrix in
+// registers, A[s][t] = row (rank + C (wl + NW s)), columns 32 t + lane. The trailing update
+// of S2 was bound by shared-memory traffic (every live element loaded and stored once per
+// step, tools/tri_probe: S2 ~2.5x the S1 time at n = 100-160); here it is register FMAs.
+// RPW slots x NT chunks <= 32 doubles per lane: n <= 128 on 1 CTA, n <= 256 on a 4-CTA
+// cluster, n <= 512 on 16 CTAs. Shared memory only holds the v / p exchange vectors.
+template <int C, int NT, int RPW>
+__global__ void __launch_bounds__(512) tridiag_regs_kernel(TriRowsArgs ra) {
+    pdl_entry();
+    constexpr int NTHR = 512, NW = NTHR / 32;
+    extern __shared__ double sm[];
+    __shared__ double s_sc[2][2];  // [k & 1] = {tau_k, c_{k-1}}
+    __shared__ double s_off[16];
+    __shared__ double red[32];
+    const TriArgs& a = ra.a;
+    const int n = a.n;
+    const unsigned rank = C > 1 ? cluster_rank() : 0u;
+    const int tid = threadIdx.x, lane = tid & 31, wl = tid >> 5;
+    const int nloc = (n - (int)rank + C - 1) / C;  // rows rank, rank + C, ...
+    double* vbuf = sm;          // 2 x n
+    double* pbuf = sm + 2 * n;  // 2 x n
+    auto bar = [&]() {
+        if (C > 1) cluster_barrier();
+        else __syncthreads();
+    };
+    double A[RPW][NT];
+    double off = 0.0;
+#pragma unroll
+    for (int s = 0; s < RPW; ++s) {
+        const int li = wl + NW * s;
+        const int i = (int)rank + C * li;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int j = 32 * t + lane;
+            const bool on = li < nloc && j < n;
+            const double v = on ? a.K[(size_t)i * a.ldk + j] : 0.0;
+            A[s][t] = v;
+            if (on && j != i) off += v * v;
+        }
+    }
+    for (int j = tid; j < 4 * n; j += NTHR) vbuf[j] = 0.0;
+    if (tid < 4) (&s_sc[0][0])[tid] = 0.0;
+    off = block_sum(off, red);
+    if (tid == 0)
+        for (int r = 0; r < C; ++r) (C > 1 ? cluster_map(s_off, r) : s_off)[rank] = off;
+    bar();
+    off = 0.0;
+    for (int r = 0; r < C; ++r) off += s_off[r];  // same order on every CTA
+    double tol_sq = a.tol_sq;
+    if (a.d_fsq) {
+        const double ot = 1e-12 * fmax(*a.d_fsq, 1.0);
+        tol_sq = ot * ot;
+    }
+    if (!(off > tol_sq) || n == 1) {  // the reference's Jacobi would not rotate at all (la_core.cpp:33)
+#pragma unroll
+        for (int s = 0; s < RPW; ++s) {
+            const int li = wl + NW * s;
+            const int i = (int)rank + C * li;
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+                if (li < nloc && 32 * t + lane == i) {
+                    a.d[i] = A[s][t];
+                    if (i + 1 < n) a.e[i] = 0.0;
+                }
+        }
+        if (rank == 0 && tid == 0) *a.trivial = 1;
+        return;
+    }
+    if (rank == 0 && tid == 0) *a.trivial = 0;
+    for (int k = 0; k + 1 < n; ++k) {
+        const int cur = k & 1, prv = cur ^ 1;
+        const double* vp = vbuf + prv * n;
+        const double* pp = pbuf + prv * n;
+        TPROBE(0, tid == 0)
+        // ---- S1: owner warp of row k (slot sk of warp (k / C) % NW on CTA k % C)
+        if ((int)rank == k % C && wl == (k / C) % NW) {
+            const int sk = (k / C) / NW;
+            double dsum = 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = 32 * t + lane;
+                if (j >= k && j < n) dsum += pp[j] * vp[j];
+            }
+            dsum = warp_sum(dsum);
+            const double cprev = 0.5 * s_sc[prv][0] * dsum;
+            const double vk = vp[k], wk = pp[k] - cprev * vp[k];
+            double x[NT];
+            double xs = 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = 32 * t + lane;
+                double ak = 0.0;
+#pragma unroll
+                for (int s = 0; s < RPW; ++s)
+                    if (s == sk) ak = A[s][t];
+                x[t] = 0.0;
+                if (j >= k && j < n) {
+                    const double vj = vp[j];
+                    const double val = ak - vk * (pp[j] - cprev * vj) - wk * vj;
+                    x[t] = val;
+                    if (j >= k + 2) xs += val * val;
+                }
+            }
+            xs = warp_sum(xs);
+            double xa = 0.0, xd = 0.0;  // columns k + 1 and k of the updated row, on their lanes
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                if (t == (k + 1) >> 5) xa = x[t];
+                if (t == k >> 5) xd = x[t];
+            }
+            const double alpha = __shfl_sync(0xffffffffu, xa, (k + 1) & 31);
+            double tau = 0.0, beta = alpha, scal = 0.0;
+            if (xs > 0.0) {
+                beta = -copysign(sqrt(alpha * alpha + xs), alpha);
+                tau = (beta - alpha) * fast_rcp(beta);
+                scal = fast_rcp(alpha - beta);
+            }
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int j = 32 * t + lane;
+                if (j >= k + 1 && j < n) {
+                    const double v = (j == k + 1) ? 1.0 : x[t] * scal;
+                    for (int r = 0; r < C; ++r) (C > 1 ? cluster_map(vbuf, r) : vbuf)[cur * n + j] = v;
+                    a.vh[(size_t)k * n + j] = v;
+                }
+            }
+            if (lane == (k & 31)) a.d[k] = xd;
+            if (lane == 0) {
+                for (int r = 0; r < C; ++r) {
+                    double* sc = C > 1 ? cluster_map(&s_sc[cur][0], r) : &s_sc[cur][0];
+                    sc[0] = tau;
+                    sc[1] = cprev;
+                }
+                a.e[k] = beta;
+                a.tau[k] = tau;
+            }
+            TPROBE(1, lane == 0)
+        }
+        bar();
+        TPROBE(2, tid == 0)
+        // ---- S2: rows i > k: update of step k-1, p_k = tau_k A v_k (groups of four slots)
+        {
+            const double tau = s_sc[cur][0], cprev = s_sc[cur][1];
+            const double* vc = vbuf + cur * n;
+#pragma unroll
+            for (int g = 0; g < (RPW + 3) / 4; ++g) {
+                const int li_hi = wl + NW * min(4 * g + 3, RPW - 1);  // last slot of the group
+                const int li_lo = wl + NW * 4 * g;
+                if (li_lo >= nloc || (int)rank + C * li_hi <= k) continue;  // warp-uniform
+                double vi[4], wi[4], sr[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int li = wl + NW * (4 * g + r);
+                    const int i = (int)rank + C * li;
+                    const bool live = 4 * g + r < RPW && li < nloc && i > k;
+                    vi[r] = live ? vp[i] : 0.0;
+                    wi[r] = live ? pp[i] - cprev * vp[i] : 0.0;
+                    sr[r] = 0.0;
+                }
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    const int j = 32 * t + lane;
+                    if (j > k && j < n) {
+                        const double rv = vp[j], rw = pp[j] - cprev * vp[j], rc = vc[j];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int s = 4 * g + r;
+                            if (s < RPW) {
+                                const int li = wl + NW * s;
+                                if (li < nloc && (int)rank + C * li > k) {
+                                    const double val = A[s][t] - vi[r] * rw - wi[r] * rv;
+                                    A[s][t] = val;
+                                    sr[r] += val * rc;
+                                }
+                            }
+                        }
+                    }
+                }
+                const bool h16 = lane & 16, h8 = lane & 8;
+                double a0 = h16 ? sr[2] : sr[0], a1 = h16 ? sr[3] : sr[1];
+                a0 += __shfl_xor_sync(0xffffffffu, h16 ? sr[0] : sr[2], 16);
+                a1 += __shfl_xor_sync(0xffffffffu, h16 ? sr[1] : sr[3], 16);
+                double c0 = h8 ? a1 : a0;
+                c0 += __shfl_xor_sync(0xffffffffu, h8 ? a0 : a1, 8);
+                c0 += __shfl_xor_sync(0xffffffffu, c0, 4);
+                c0 += __shfl_xor_sync(0xffffffffu, c0, 2);
+                c0 += __shfl_xor_sync(0xffffffffu, c0, 1);
+                const int r = lane >> 3, sub = lane & 7;
+                const int s = 4 * g + r;
+                const int li = wl + NW * s;
+                const int i = (int)rank + C * li;
+                if (s < RPW && li < nloc && i > k)
+                    for (int q = sub; q < C; q += 8) (C > 1 ? cluster_map(pbuf, q) : pbuf)[cur * n + i] = c0 * tau;
+            }
+        }
+        TPROBE(3, tid == 0)
+        TPROBE(4, tid == 32 * (NW - 1))
+        bar();
+        TPROBE(5, tid == 0)
+    }
+    // the last diagonal entry, from the register of its owner lane
+#pragma unroll
+    for (int s = 0; s < RPW; ++s) {
+        const int li = wl + NW * s;
+        const int i = (int)rank + C * li;
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+            if (i == n - 1 && li < nloc && 32 * t + lane == n - 1) {
+                a.d[n - 1] = A[s][t];
+                a.tau[n - 1] = 0.0;
+                if (n >= 2) a.tau[n - 2] = 0.0;
+            }
+    }
+}
+
 // Sturm count: eigenvalues of T smaller than x (dlaebz recurrence with pivmin guard).
 __device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
     double q = d[0] - x;
@@ -1283,6 +1499,63 @@ void launch_rows(const TriRowsArgs& ra, size_t smem, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+template <int C, int NT, int RPW>
+void launch_regs(const TriRowsArgs& ra, cudaStream_t st) {
+    auto* fn = tridiag_regs_kernel<C, NT, RPW>;
+    static bool attr = false;
+    if (!attr) {
+        allow_max_dynamic_smem(fn);
+        CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    size_t smem = 4 * (size_t)ra.a.n * sizeof(double);
+    static const int excl = getenv("SFDG_TRIDIAG_EXCLUSIVE") ? atoi(getenv("SFDG_TRIDIAG_EXCLUSIVE")) : 1;
+    if (excl) {  // keep other kernels' blocks off these SMs (latency-bound chain kernel)
+        cudaFuncAttributes fa;
+        CK(cudaFuncGetAttributes(&fa, (const void*)fn));
+        smem = std::max(smem, (size_t)fa.maxDynamicSharedSizeBytes);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, fn, ra));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// Register-resident row kernel for 128 < n <= 512 (SFDG_TRIDIAG=c selects the shared-memory
+// row kernel below, which it reproduces bit for bit; SFDG_TRIDIAG=r forces it for n <= 128
+// too). Measured (tools/kbench, eigh top-100): n = 200 881 us against 930 us for the 2-CTA
+// shared-memory kernel; n = 100 312 us against 302 us, so small n keeps the shared-memory
+// kernel. tools/tri_probe shows why the gain is small: the trailing update costs the same
+// ~3000-4600 cycles per step from registers as from shared memory -- the step is bound by
+// dependent-instruction latency with 4 warps per scheduler, not by shared-memory traffic.
+bool launch_tridiag_regs(const TriArgs& a, cudaStream_t st) {
+    static const char* env = getenv("SFDG_TRIDIAG");
+    if (env && (env[0] == 'c' || env[0] == 'p' || env[0] == 'f')) return false;
+    const int n = a.n;
+    TriRowsArgs ra{a, 1, n};
+    if (n <= 128) {
+        if (!(env && env[0] == 'r')) return false;
+        launch_regs<1, 4, 8>(ra, st);
+    } else if (n <= 256) {
+        ra.C = 4;
+        launch_regs<4, 8, 4>(ra, st);
+    } else if (n <= 512) {
+        ra.C = 16;
+        launch_regs<16, 16, 2>(ra, st);
+    } else return false;
+    return true;
+}
+
 // Row-distributed tridiagonalisation when the full matrix fits the shared memory of a
 // cluster of <= 16 CTAs (n <= ~670); false -> the caller uses the packed kernel.
 bool launch_tridiag_rows(const TriArgs& a, cudaStream_t st) {
@@ -1347,7 +1620,7 @@ void eigh_tri(const double* K, int n, int ldk, double off_tol, const double* d_f
     }
     {
         ProfScope prof("eigh_tridiag", st);
-        if (!launch_tridiag_packed(a, st) && !launch_tridiag_rows(a, st)) {
+        if (!launch_tridiag_packed(a, st) && !launch_tridiag_regs(a, st) && !launch_tridiag_rows(a, st)) {
             const size_t smem = use_smem ? (packed + 2 * (size_t)n) * sizeof(double) : 0;
             if (use_smem) LAUNCH(tridiag_kernel<true>, 1, kTriThreads, smem, st, a);
             else LAUNCH(tridiag_kernel<false>, 1, kTriThreads, 0, st, a);

@@ -164,6 +164,31 @@ def test_fused_packed_tridiagonalisation_eigh():
     assert " passed" in r.stdout
 
 
+def test_register_tridiagonalisation_matches_shared_memory_kernel():
+    """The register-resident row kernel (default for 128 < n <= 512, forced for all n by
+    SFDG_TRIDIAG=r) and the shared-memory row kernel (SFDG_TRIDIAG=c) run the same arithmetic
+    in the same order: eigenpairs are bit-identical. Child processes (the switch is read once)."""
+    import subprocess
+    import sys
+    import tempfile
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1602_00412_b200 as P\n"
+            "out = {}\n"
+            "for n in (2, 7, 33, 100, 129, 200, 256, 300):\n"
+            "    a = np.random.default_rng(n).standard_normal((n + 3, n)); k = a.T @ a\n"
+            "    v, e = P.eigh(k, 1e-12 * (a ** 2).sum()); out['v%%d' %% n] = v; out['e%%d' %% n] = e\n"
+            "np.savez(sys.argv[1], **out)\n") % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as td:
+        res = {}
+        for mode in ("r", "c"):
+            path = os.path.join(td, mode + ".npz")
+            r = subprocess.run([sys.executable, "-c", code, path], env={**os.environ, "SFDG_TRIDIAG": mode},
+                               capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stderr[-2000:]
+            res[mode] = np.load(path)
+        for key in res["r"].files:
+            assert np.array_equal(res["r"][key], res["c"][key]), key
+
+
 def test_eigh_degenerate_and_diagonal():
     k = np.diag([3.0, 1.0, 3.0, 0.0, 2.0])
     vals, vecs = P.eigh(k, 1e-12)
