@@ -417,6 +417,7 @@ def roofline_from_profile(prof: dict, st: dict, n: int, d: int, ell: int, nnz_st
     out["roofline"] = {"bound": "hbm", "kernel": "spmm (CSR/CSC gather, ell-wide panels)",
                        "achieved": ks.get("achieved_gbs"), "peak": hbm, "unit": "GB/s",
                        "frac": ks.get("frac_of_measured_hbm"), "traffic": traffic,
+                       "frac_of_nominal_8tbs": round(ks["achieved_gbs"] / 8000.0, 4) if ks.get("achieved_gbs") else None,
                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)",
                        "alg_bytes_per_launch": ks.get("alg_bytes_per_launch"),
                        "note": "c2 panels (8 MB) are L2-resident: achieved uses SURVEY 8(d) algorithmic bytes; "
