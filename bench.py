@@ -290,6 +290,7 @@ def main():
     clk = clocks.stop()
     t_e2e = None
     if not a.no_e2e:
+        sk.reset(seed)
         step_host()  # warm the host path
         t_e2e = timed(step_host, a.steps)
 

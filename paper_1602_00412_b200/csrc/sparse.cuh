@@ -25,7 +25,10 @@ class Scratch {
             used = 0;
         }
         if (cur == chunks.size()) {
-            size_t sz = std::max<size_t>(bytes, chunks.empty() ? (size_t)64 << 20 : chunks.back().size * 2);
+            // exactly the request (>= 64 MB): the take sequence of a phase repeats, so after the
+            // first pass every take finds its chunk again. (Doubling the last chunk over-allocated
+            // by GBs at c5, where single takes are 1-4 GB, and ran a 180 GB device out of memory.)
+            size_t sz = std::max<size_t>(bytes, (size_t)64 << 20);
             Chunk c{nullptr, sz};
             CK(cudaMalloc(&c.ptr, sz));
             chunks.push_back(c);
