@@ -388,6 +388,7 @@ void Engine::sweep_block(int interval, int m) {
         // checked by the caller), so the same graph serves every later flush of this lane
         const uint64_t l0 = g_launches.load();
         cudaGraph_t graph = nullptr;
+        scr.headroom((size_t)256 << 20);  // the capture must not allocate
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         try {
             body();
@@ -525,6 +526,7 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
         if (it == vgraphs.end()) {
             const uint64_t l0 = g_launches.load();
             cudaGraph_t graph = nullptr;
+            scr.headroom((size_t)256 << 20);  // the capture must not allocate
             CK(cudaStreamBeginCapture(vs, cudaStreamCaptureModeThreadLocal));
             try {
                 verify_sequence(args, vstate, vg_blocks, kSMs, vs);

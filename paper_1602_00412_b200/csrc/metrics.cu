@@ -182,6 +182,7 @@ double device_cov_err(Engine& e, const double* b_host, int ell, size_t iteration
     };
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    gscr.headroom((size_t)256 << 20);  // the capture must not allocate
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     step();
     CK(cudaStreamEndCapture(st, &graph));

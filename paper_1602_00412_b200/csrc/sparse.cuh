@@ -25,10 +25,12 @@ class Scratch {
             used = 0;
         }
         if (cur == chunks.size()) {
-            // exactly the request (>= 64 MB): the take sequence of a phase repeats, so after the
-            // first pass every take finds its chunk again. (Doubling the last chunk over-allocated
-            // by GBs at c5, where single takes are 1-4 GB, and ran a 180 GB device out of memory.)
-            size_t sz = std::max<size_t>(bytes, (size_t)64 << 20);
+            // Double the last chunk, but never with more than 1 GB of slack beyond the request:
+            // plain doubling over-allocated by many GB at c5 (single takes of 1-4 GB) and ran a
+            // 180 GB device out of memory; some slack keeps later, slightly larger take sequences
+            // (and stream captures, which must not allocate) inside existing chunks.
+            const size_t last2 = chunks.empty() ? (size_t)64 << 20 : chunks.back().size * 2;
+            size_t sz = std::max<size_t>(bytes, std::min<size_t>(last2, bytes + ((size_t)1 << 30)));
             Chunk c{nullptr, sz};
             CK(cudaMalloc(&c.ptr, sz));
             chunks.push_back(c);
@@ -42,6 +44,14 @@ class Scratch {
     void reset() {
         cur = 0;
         used = 0;
+    }
+    // Before a stream capture (which must not cudaMalloc): make sure takes totalling up to
+    // `bytes` after this point find existing chunks. The position is unchanged.
+    void headroom(size_t bytes) {
+        const size_t c0 = cur, u0 = used;
+        take<char>((int64_t)bytes);
+        cur = c0;
+        used = u0;
     }
     void release() {
         for (auto& c : chunks) cudaFree(c.ptr);
