@@ -926,3 +926,16 @@ def test_proj_err_device_vs_oracle(oracle):
         want = oracle.proj_err(rp, cs, vs, 1000, b, k, t)
         assert got is not None and abs(got - want) <= 1e-9 * want
     assert P.proj_err((rp, cs, vs), 1000, b, 5, 1e-30) is None
+
+
+def test_cov_err_after_sketch_in_one_process():
+    """bench.py's accuracy path at reduced size: a whole sketch, then the device cov_err on the
+    same stream in the same process (its power step is captured as a CUDA graph, and a stream
+    capture must not allocate scratch -- a regression caught by the bench, not the tests)."""
+    d, ell = 10000, 100
+    rp, cs, vs = S.generate("c2", (0, 200000))
+    s = P.SfdSketcher(P.SketchConfig(ell=ell, d=d, seed=1), device=0)
+    s.append_csr(rp, cs, vs)
+    b = s.finalize()
+    ce, _ = P.cov_err((rp, cs, vs), d, b, P.RngState(4242), iterations=50, device=0)
+    assert 0.0 <= ce <= 1.0 / (KALPHA * ell)
