@@ -1,21 +1,29 @@
 #!/usr/bin/env python
 """bench.py -- nnz sketched/s (and rows/s) of the SFD sketch path on B200.
 
-Workload (BASELINE.json configs[1], "c2"): n = 1e6 rows, d = 1e4, ell = 100, FP64,
-rank-20 + noise, Bernoulli 0.1% (~1e7 nnz), seed 1 -- seeded synthetic data of that
-recipe (paper_1602_00412_b200/synthetic.py). One step = sketching the whole stream
-(100 flushes: SparseShrink + verify + DenseShrink each) with SfdSketcher and finalize().
+Workload (default): BASELINE.json configs[3] ("c4"), the largest configuration that runs on
+one GPU -- n = 5e6 rows, d = 5e4, ell = 128, FP64, Geometric(mean 50) row lengths, power-law
+(s = 0.9) items, mean-centred 1-5 ratings (~2.5e8 nnz), seed 3 -- as seeded synthetic data of
+that recipe (paper_1602_00412_b200/synthetic.py; the reference ships no data set). One step =
+sketching the whole stream (100 flushes: SparseShrink + verify + DenseShrink each) with
+SfdSketcher and finalize(). `--config c2` (configs[1]) and the others select the other families.
 
   value : inputs already resident in HBM (append_csr_device), B left on device
   e2e   : the public host API (append_csr from pinned host CSR, finalize() to host),
           host->device copies inside the timed region
-Multi-GPU (torchrun, one rank per GPU): weak scaling -- every rank sketches its own
-c2-sized stream (seed 1 + rank), then the ranks' sketches are merged in a log2 tree
-(NCCL send/recv + device merge-shrink). Time = max over ranks.
 
---impl reference: the reference C++ implementation (oracle/_ref, built from the
-unmodified /root/reference sources) on all host cores (one process per core, each
-sketching one flush worth of c2 rows), same metric and units.
+Multi-GPU (torchrun, one rank per GPU): one stream cut into contiguous row
+shards, rank r sketching its shard with seed + r, then the log2 merge tree (NCCL send/recv of
+B^T + device merge-shrink, lower rank stacked first); time = max over ranks.
+  c1-c4: weak scaling -- the family's stream has world x n rows, n per rank;
+  c5   : configs[4] itself (5e7 rows, the 8-GPU sharded stream), split over the ranks (strong).
+
+--impl reference: the unmodified reference C++ (oracle/_ref, built from /root/reference) on
+every host core, same config dict and metric. One c4 flush takes ~25 min on a core, so each
+step times one power sweep of simultaneous_iteration (randsvd.cpp:39-48, the reference's own
+rmatvec / matvec / orthonormalize on a flush buffer) per process and extrapolates a flush as
+q+1 sweeps (the projection / svd_top / dense_shrink tail, ~3% of a reference flush, is not
+counted, which favours the reference).
 """
 from __future__ import annotations
 
@@ -35,6 +43,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "nnz sketched/sec (and rows/s) at ell, 1/2/4/8 B200; SpMM HBM GB/s vs peak"
 UNIT = "nnz/s"
+CONFIG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
+DEFAULT_CONFIG = "c4"  # the largest single-GPU configuration in BASELINE.json
+FP64_PEAK_TFLOPS = 36.9  # DMMA (mma.sync m8n8k4 f64) measured on this pool: profiles/r01_fp64_peak.txt
+REF_BUDGET_S = 200.0  # reference arm: wall-clock budget of all timed samples together
 
 
 def parse():
@@ -43,12 +55,36 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="sfdg", choices=["sfdg", "reference"])
-    p.add_argument("--config", default="c2")
-    p.add_argument("--rows", type=int, default=0, help="limit rows per stream (debug only)")
+    p.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIG_INDEX))
+    p.add_argument("--rows", type=int, default=0, help="limit rows per shard (debug only)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-accuracy", action="store_true", help="skip the whole-stream cov_err check")
+    p.add_argument("--no-isolated", action="store_true", help="skip the one-lane profiled step")
     return p.parse_args()
+
+
+def workload(name: str, world: int, rows_limit: int):
+    """(stream, scaling, config dict) -- identical for both arms (same_config)."""
+    from paper_1602_00412_b200 import synthetic as S
+    base = S.CONFIGS[name]
+    if name == "c5":
+        n, scaling = base.n, "strong"
+        shard = "configs[4]'s 5e7-row stream split into contiguous row shards"
+    else:
+        n, scaling = base.n * world, "weak"
+        shard = f"one {world} x {base.n}-row stream of the family, a contiguous {base.n}-row shard per rank"
+    if rows_limit:
+        n = min(n, rows_limit * world)
+    stream = S.StreamConfig(name, n, base.d, base.ell, base.seed)
+    cfg = {"workload": f"{name} = BASELINE.json configs[{CONFIG_INDEX[name]}]: n={n} d={base.d} ell={base.ell} "
+                       f"FP64, data seed {base.seed}; step = full-stream SfdSketcher.append + finalize"
+                       + (" + log2 merge tree" if world > 1 else ""),
+           "config_index": CONFIG_INDEX[name], "n": n, "d": base.d, "ell": base.ell, "seed": base.seed,
+           "shards": world, "parallelism": f"row shards x{world} ({shard}), sketch seed {base.seed}+rank"
+                                           + (", log2 NCCL merge-shrink tree" if world > 1 else ""),
+           "l2_flush": "256 MB device write between timed steps (inputs 3 GB > 126 MB L2)"}
+    return stream, scaling, cfg
 
 
 # ------------------------------------------------------------------ clocks
@@ -101,70 +137,105 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ------------------------------------------------------------------ reference arm
-def _ref_worker(args):
-    name, r0, r1, ell, seed = args
+# ------------------------------------------------------------------ reference (CPU) samples
+def power_q(m: int) -> int:
+    """power_iteration_count (randsvd.cpp:10-16) with the default epsilon 1/4, c_q = 1."""
+    return max(1, math.ceil(math.log(max(m, 1) / 0.25) / 0.25))
+
+
+_REF_CACHE = {}
+
+
+def _sweep_job(args):
+    """One reference power sweep over the first `rows` rows of flush `f` of config `name`,
+    from a seeded Gaussian Y. Returns (seconds, nnz, rows)."""
+    name, f, rows = args
     from oracle.oracle import Reference
     from paper_1602_00412_b200 import synthetic as S
-    rp, cs, vs = S.generate(name, (r0, r1))
-    R = Reference()
-    t = time.perf_counter()
-    R.sketch(rp, cs, vs, S.CONFIGS[name].d, ell, seed=seed)
-    return time.perf_counter() - t, int(rp[-1]), r1 - r0
-
-
-def reference_sample(name: str, procs: int, rows_per_proc: int):
-    """Run the unmodified reference on `procs` host cores in parallel; returns (seconds, nnz, rows)."""
-    import multiprocessing as mp
-    from paper_1602_00412_b200 import synthetic as S
     cfg = S.CONFIGS[name]
-    span = max(1, cfg.n - rows_per_proc + 1)  # wrap so every job is a full in-range sample
-    jobs = [(name, (p * rows_per_proc) % span, (p * rows_per_proc) % span + rows_per_proc, cfg.ell, cfg.seed)
-            for p in range(procs)]
+    key = (name, f, rows)
+    if key not in _REF_CACHE:
+        _REF_CACHE.clear()
+        r0 = (f * cfg.d) % max(1, cfg.n - cfg.d + 1)
+        _REF_CACHE[key] = S.generate(name, (r0, r0 + rows))
+    rp, cs, vs = _REF_CACHE[key]
+    y = np.random.default_rng(f).standard_normal((rows, cfg.ell))
+    _, secs = Reference().power_sweep(rp, cs, vs, cfg.d, y)
+    return secs, int(rp[-1]), rows
+
+
+def reference_sweeps(name: str, procs: int, flush0: int, rows: int, pool=None):
+    """Sweeps on `procs` processes in parallel (flushes flush0 .. flush0 + procs - 1).
+    Returns (wall seconds, per-process results)."""
+    jobs = [(name, flush0 + p, rows) for p in range(procs)]
     t = time.perf_counter()
-    if procs == 1:
-        res = [_ref_worker(jobs[0])]
-    else:
-        with mp.get_context("fork").Pool(procs) as pool:
-            res = pool.map(_ref_worker, jobs)
-    wall = time.perf_counter() - t
-    return wall, sum(r[1] for r in res), sum(r[2] for r in res)
+    res = pool.map(_sweep_job, jobs) if pool is not None else [_sweep_job(j) for j in jobs]
+    return time.perf_counter() - t, res
+
+
+def sweep_rate(name: str, res) -> tuple[float, float]:
+    """Extrapolated reference throughput of the processes in `res` running side by side: each
+    sketches a flush in (q + 1) sweeps over its nonzeros, so its rate is nnz / ((q+1) t)."""
+    from paper_1602_00412_b200 import synthetic as S
+    q = power_q(S.CONFIGS[name].d)  # every flush of the five configs has m = d rows (SURVEY F4)
+    nnz_s = sum(r[1] / ((q + 1) * r[0]) for r in res)
+    rows_s = sum(r[2] / ((q + 1) * r[0]) for r in res)
+    return nnz_s, rows_s
+
+
+def sample_rows(name: str, budget_s: int | float, procs: int, pool=None) -> tuple[int, float]:
+    """Rows per sweep sample so that one sample takes about budget_s: a 1/16-flush calibration
+    sweep, scaled linearly (MGS and the SpMV pair are linear in the rows) with a 1.5x margin
+    for the cache effects that make small samples faster per row."""
+    from paper_1602_00412_b200 import synthetic as S
+    m = S.CONFIGS[name].d
+    cal = max(64, m // 16)
+    _, res = reference_sweeps(name, procs, 10_000, cal, pool)
+    t_full = 1.5 * max(r[0] for r in res) * m / cal
+    return (m if t_full <= budget_s else max(cal, int(m * budget_s / t_full))), t_full
 
 
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
+    import multiprocessing as mp
     from paper_1602_00412_b200 import synthetic as S
-    cfg = S.CONFIGS[a.config]
+    name = a.config
+    cfg = S.CONFIGS[name]
+    _, scaling, config = workload(name, world, a.rows)
     procs = os.cpu_count() or 1
-    flush_rows = cfg.d  # every flush of this config fires on rows == d (SURVEY F4)
-    for _ in range(a.warmup):
-        reference_sample("c1", procs, 1000)  # warm the processes/caches on a tiny sample
-    total_t, total_nnz, total_rows = 0.0, 0, 0
-    for _ in range(a.steps):
-        t, nnz, rows = reference_sample(a.config, procs, flush_rows)
-        total_t += t
-        total_nnz += nnz
-        total_rows += rows
-    v = total_nnz / total_t
+    q = power_q(cfg.d)
+    with mp.get_context("fork").Pool(procs) as pool:
+        for w in range(a.warmup):  # warm the processes (library load, page cache) on tiny sweeps
+            reference_sweeps(name, procs, 20_000 + w * procs, 256, pool)
+        rows, t_full = sample_rows(name, REF_BUDGET_S / max(1, a.steps), procs, pool)
+        vals, rvals, walls = [], [], []
+        for k in range(a.steps):
+            wall, res = reference_sweeps(name, procs, k * procs, rows, pool)
+            v, rv = sweep_rate(name, res)
+            vals.append(v)
+            rvals.append(rv)
+            walls.append(wall)
+    v = float(np.mean(vals))
+    sample = (f"{a.steps} steps x {procs} processes x one power sweep (randsvd.cpp:39-48 through the unmodified "
+              f"reference's SparseBuffer::rmatvec/matvec and orthonormalize, oracle/_ref) over {rows} of the {cfg.d} "
+              f"rows of a {name} flush buffer; a flush extrapolated as q+1 = {q + 1} sweeps (EXTRAPOLATED; the "
+              f"flush tail and the row-sampling's cache effects both favour the reference); est. full sweep "
+              f"{t_full:.1f} s/core")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": 1e3 * total_t / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "rows_per_sec": total_rows / total_t,
-            "config": {"workload": f"{a.config}: n={cfg.n} d={cfg.d} ell={cfg.ell} seed={cfg.seed} (BASELINE.json "
-                                   f"configs[1]); reference sample per step = one flush ({flush_rows} rows) on each "
-                                   f"of {procs} host processes", "l2_flush": "n/a (CPU)"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "reference",
-                             "sample": f"{a.steps} steps x {procs} processes x 1 flush ({flush_rows} rows of "
-                                       f"{a.config}), oracle/_ref = unmodified reference core/src, -O3"},
+            "warmup": a.warmup, "ms_per_step": 1e3 * float(np.mean(walls)), "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "rows_per_sec": float(np.mean(rvals)), "config": config, "extrapolated": True,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------------ our arm
-def merge_tree(P, torch, dist, s, d, ell, device, rank, world):
+def merge_tree(torch, dist, s, d, ell, device, rank, world):
     """log2 tree (paper_1602_00412_b200/shards.py): at level L, rank r with
     r % 2^(L+1) == 2^L sends its B^T (d x ell, FP64) to r - 2^L, which merge-shrinks it into
     its own sketch (sketch.cpp:80-83, sfdg_sketcher_merge_device: no allocation on the timed
@@ -210,12 +281,13 @@ def main():
     device = local
     torch.cuda.set_device(device)
 
-    cfg = S.CONFIGS[a.config]
-    n = min(cfg.n, a.rows) if a.rows else cfg.n
-    seed = cfg.seed + rank
-    rp, cs, vs = S.generate(S.StreamConfig(cfg.name, cfg.n, cfg.d, cfg.ell, seed), (0, n))
+    stream, scaling, config = workload(a.config, world, a.rows)
+    d, ell = stream.d, stream.ell
+    r0, r1 = S.shard_rows(stream.n, world, rank)
+    seed = stream.seed + rank
+    rp, cs, vs = S.generate_parallel(stream, (r0, r1))
+    n = r1 - r0
     nnz = int(rp[-1])
-    d, ell = cfg.d, cfg.ell
 
     # device-resident copy (value) and pinned host copy (e2e)
     d_cols = torch.from_numpy(cs.view(np.int32)).to(f"cuda:{device}")
@@ -228,17 +300,17 @@ def main():
 
     sk = P.SfdSketcher(P.SketchConfig(ell=ell, d=d, seed=seed), device=device)
 
-    def step_device():
-        sk.append_csr_device(rp, d_cols.data_ptr(), d_vals.data_ptr())
-        sk.finalize_device()
+    def step_device(s=sk):
+        s.append_csr_device(rp, d_cols.data_ptr(), d_vals.data_ptr())
+        s.finalize_device()
         if world > 1:
-            merge_tree(P, torch, dist, sk, d, ell, device, rank, world)
+            merge_tree(torch, dist, s, d, ell, device, rank, world)
 
     def step_host():
         sk.append_csr(rp, h_cs, h_vs)
         b = sk.finalize()  # B to host (the public API result)
         if world > 1:
-            merge_tree(P, torch, dist, sk, d, ell, device, rank, world)
+            merge_tree(torch, dist, sk, d, ell, device, rank, world)
         return b
 
     def barrier():
@@ -300,68 +372,70 @@ def main():
     P.profile_begin()
     step_device()
     prof = P.profile_end()
-    pstats = sk.stats()
+    iso = None
+    if rank == 0 and not a.no_isolated:
+        # the same step with one flush in flight: each launch runs without the other lanes'
+        # kernels beside it (its standalone duration; the pipelined step overlaps four flushes)
+        os.environ["SFDG_LANES"] = "1"
+        s1 = P.SfdSketcher(P.SketchConfig(ell=ell, d=d, seed=seed), device=device)
+        del os.environ["SFDG_LANES"]
+        torch.cuda.synchronize(device)
+        P.profile_begin()
+        step_device(s1)
+        iso = P.profile_end()
+        s1.close()
     accuracy = None
     if rank == 0 and world == 1 and not a.no_accuracy:
         # the paper's guarantee checked on the whole stream, on the device (SURVEY 8(d) accuracy
         # gate; cov_err = bench.cpp:171-183 with its default 1000 power steps, untimed)
+        sk.reset(seed)
+        step_device()
         b = sk.sketch()
         t0 = time.time()
         ce, _ = P.cov_err((rp, cs, vs), d, b, P.RngState(4242), iterations=1000, device=device)
         alpha = 6.0 / 41.0
         fsq = float(np.dot(vs, vs))
-        # the north_star bound at k = the planted rank: |A^T A - B^T B|_2 <= |A - A_k|_F^2 / (ell - k),
-        # with |A - A_k|_F^2 from exact_tail (bench.cpp:68-137) on the device
+        # the north_star bound |A^T A - B^T B|_2 <= |A - A_k|_F^2 / (ell - k) at k = the planted
+        # rank (c1, c2, c5), with |A - A_k|_F^2 from exact_tail (bench.cpp:68-137) on the device;
+        # the rating / text families have no planted rank: k = 0
         kp = {"c1": 10, "c2": 20, "c5": 32}.get(a.config, 0)
-        tail, _, sweeps, _ = P.exact_tail((rp, cs, vs), d, kp, P.RngState(4243), device=device)
+        tail = P.exact_tail((rp, cs, vs), d, kp, P.RngState(4243), device=device)[0] if kp else fsq
         accuracy = {"cov_err": ce, "definition": "|A^T A - B^T B|_2 / |A|_F^2 over the whole stream (1000 "
                                                  "power steps on the device, bench.cpp:171-183)",
                     "alpha_bound_k0": 1.0 / (alpha * ell), "within_alpha_bound": bool(ce <= 1.0 / (alpha * ell)),
                     "fd_bound_k0": 1.0 / ell, "within_fd_bound": bool(ce <= 1.0 / ell),
-                    "k_planted": kp, "tail_k_over_fsq": tail / fsq, "exact_tail_sweeps": sweeps,
+                    "k": kp, "tail_k_over_fsq": tail / fsq,
                     "north_star_bound_k": tail / fsq / (ell - kp),
                     "within_north_star_bound": bool(ce <= tail / fsq / (ell - kp)),
                     "seconds": round(time.time() - t0, 3)}
 
-    value = world * nnz * a.steps / t_dev
+    value = nnz_total(torch, dist, nnz, world) * a.steps / t_dev
+    rows_total = stream.n if world > 1 else n
     ms_step = 1e3 * t_dev / a.steps
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "rows_per_sec": world * n * a.steps / t_dev,
-            "config": {"workload": f"{a.config}: n={n} d={d} ell={ell} seed={cfg.seed}+rank, nnz={nnz}/rank "
-                                   f"(BASELINE.json configs[1]); step = full-stream SfdSketcher + finalize"
-                                   + (" + log2 merge tree" if world > 1 else ""),
-                       "l2_flush": "256 MB write between timed steps", "parallelism": f"shards x{world}",
-                       "flushes_per_step": stats["flushes"], "attempts_per_step": stats["attempts"]},
-            "gpu_launches": int(launches), "clocks": clk}
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "rows_per_sec": rows_total * a.steps / t_dev, "config": config,
+            "nnz_per_step": int(value * t_dev / a.steps), "flushes_per_step_rank0": stats["flushes"],
+            "attempts_per_step_rank0": stats["attempts"], "gpu_launches": int(launches), "clocks": clk}
     if t_e2e is not None:
-        line["e2e"] = {"value": world * nnz * a.steps / t_e2e, "unit": UNIT,
+        line["e2e"] = {"value": line["nnz_per_step"] * a.steps / t_e2e, "unit": UNIT,
                        "h2d_bytes_per_step": int(nnz * 12 + (n + stats["flushes"]) * 4),
-                       "d2h_bytes_per_step": int(ell * d * 8)}
-    line.update(roofline_from_profile(prof, pstats, n, d, ell, nnz))
-    rl2 = line.get("roofline", {}).get("l2_gather")
-    if rl2 and "spmm" in prof and prof["spmm"][1]:
-        # Whole-step bound: the SpMM launches of one step move this many bytes L2 -> SM (one
-        # ell-wide FP64 panel row per nonzero), so at the measured gather peak the step cannot
-        # take less than floor_ms even with every other kernel hidden under them.
-        nsp = prof["spmm"][1]
-        gb = nsp * rl2["bytes_per_launch"] / 1e9
-        bw = rl2.get("sustained_peak", rl2["peak"])
-        floor_ms = 1e3 * gb / bw
-        line["step_floor"] = {"bound": "l2_gather", "what": "SpMM gather bytes of one step at the sustained "
-                              "L2 gather bandwidth", "spmm_launches": nsp, "gbytes": round(gb, 2),
-                              "floor_ms": round(floor_ms, 2), "frac": round(floor_ms / ms_step, 4),
-                              "serial_launch_ms": round(nsp * rl2["bytes_per_launch"] / (rl2["peak"] * 1e9) * 1e3, 2),
-                              "note": "serial_launch_ms = the same launches back to back at the probe's "
-                                      "same-size launch time; the lanes overlap launches, the ramp is the cost"}
+                       "d2h_bytes_per_step": int(ell * d * 8),
+                       "note": "bytes of rank 0's shard (every rank copies its own)"}
+    line.update(roofline_from_profile(prof, a.config, ms_step))
+    if iso:
+        line["roofline"]["isolated"] = isolated_roofline(iso)
     if accuracy is not None:
         line["accuracy"] = accuracy
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
-            t, nz, rows = reference_sample(a.config, 1, d)
-            line["cpu_baseline"] = {"value": nz / t, "unit": UNIT, "cores": 1, "kind": "reference",
-                                    "sample": f"first flush of {a.config} ({rows} rows, {nz} nnz) through the "
-                                              f"unmodified reference (oracle/_ref), 1 thread: {t:.1f} s"}
+            rows_s, t_full = sample_rows(a.config, 15.0, 1)
+            wall, res = reference_sweeps(a.config, 1, 0, rows_s)
+            v, _ = sweep_rate(a.config, res)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "reference",
+                                    "sample": f"one power sweep of the unmodified reference (oracle/_ref) over {rows_s} "
+                                              f"rows of the first {a.config} flush buffer, 1 thread, {res[0][0]:.1f} s; "
+                                              f"a flush extrapolated as q+1 = {power_q(d) + 1} sweeps (EXTRAPOLATED)"}
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
@@ -372,88 +446,83 @@ def main():
     return 0
 
 
-def roofline_from_profile(prof: dict, st: dict, n: int, d: int, ell: int, nnz_stream: int) -> dict:
-    """Roofline of the dominant kernel class from the profiled step (SURVEY sec 8(d) formulas)."""
-    peaks = {}
+def nnz_total(torch, dist, nnz, world):
+    """Stored entries over all ranks' shards (each rank sketches its own)."""
+    if world == 1:
+        return nnz
+    t = torch.tensor([float(nnz)], dtype=torch.float64,
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t)
+    return int(t.item())
+
+
+def _peaks():
     try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
     except Exception:
-        pass
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    fp64 = 36.9  # TFLOP/s, DMMA/DFMA measured on this pool: profiles/r01_fp64_peak.txt
-    flushes = max(1, st["flushes"])
-    m = d  # every flush of c2 has m = d rows (row trigger, SURVEY F4)
-    nnz_f = nnz_stream / flushes
-    kern = {}
-    total_ms = sum(v[0] for k, v in prof.items() if k != "rng_gen")
-    for k, (ms, cnt) in prof.items():
-        kern[k] = {"ms": round(ms, 4), "launches": cnt, "share": round(ms / total_ms, 4) if total_ms else None}
-    out = {"kernels": kern}
-    # SpMM: bytes = 12 nnz_f + 8 (m+1) + 8 ell d + 8 ell m per launch
-    if "spmm" in prof and prof["spmm"][1]:
-        ms, cnt = prof["spmm"]
-        byts = 12 * nnz_f + 8 * (m + 1) + 8 * ell * d + 8 * ell * m
-        gbs = byts / (ms / cnt * 1e-3) / 1e9
-        kern["spmm"].update({"alg_bytes_per_launch": byts, "achieved_gbs": round(gbs, 1),
-                             "frac_of_measured_hbm": round(gbs / hbm, 4)})
-    if "gram" in prof and prof["gram"][1]:
-        ms, cnt = prof["gram"]
-        att = max(1, st["attempts"])
-        n_orth = prof.get("chol", (0, 0))[1]  # one pass-1 factorisation per CholeskyQR2
-        # per CholeskyQR2: 2 Grams of m x ell; per attempt: W^T W (d x ell); per flush: [B;B'] (d x 2ell)
-        flops = n_orth * 2 * (2 * m * ell * ell) + att * 2 * d * ell * ell + flushes * 2 * d * (2 * ell) ** 2
-        tf = flops / (ms * 1e-3) / 1e12
-        kern["gram"].update({"alg_flops_total": flops, "achieved_tflops": round(tf, 3),
-                             "frac_of_fp64_peak": round(tf / fp64, 4)})
-    # The metric names the SpMM's HBM roofline, so the roofline object is the SpMM (K3),
-    # the path's memory-bound kernel; the largest time share is reported beside it.
-    dom = max((k for k in prof if k != "rng_gen"), key=lambda k: prof[k][0]) if prof else None
-    ks = kern.get("spmm", {})
-    traffic = None
+        return {"hbm_gbs": 6650.0}, "B200_PROFILING.md fallback 6.65 TB/s (MEASURED_PEAKS.json absent)"
+
+
+def _traffic(config: str):
+    """ncu dram bytes per SpMM launch for this configuration (profiles/ncu_summary.json), or None."""
     try:
         ncu = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = ncu.get("spmm_rows_kernel", {}).get("dram_bytes_per_launch")
+        return ncu.get("spmm_dram_bytes_per_launch", {}).get(config)
     except Exception:
-        pass
-    out["roofline"] = {"bound": "hbm", "kernel": "spmm (CSR/CSC gather, ell-wide panels)",
-                       "achieved": ks.get("achieved_gbs"), "peak": hbm, "unit": "GB/s",
-                       "frac": ks.get("frac_of_measured_hbm"), "traffic": traffic,
-                       "frac_of_nominal_8tbs": round(ks["achieved_gbs"] / 8000.0, 4) if ks.get("achieved_gbs") else None,
-                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)",
-                       "alg_bytes_per_launch": ks.get("alg_bytes_per_launch"),
-                       "note": "c2 panels (8 MB) are L2-resident: achieved uses SURVEY 8(d) algorithmic bytes; "
-                               "traffic = ncu dram bytes per launch (profiles/)"}
-    # The c2 panels are L2-resident, so the bound that actually applies is the L2 -> SM gather
-    # bandwidth: measured by tools/probe_l2 (the same access pattern without arithmetic).
-    l2 = None
-    try:
-        for line in open(os.path.join(ROOT, "profiles", "r01_l2_gather_peak.txt")):
-            if line.startswith("l2_gather_gbs"):
-                l2 = float(line.split()[1])
-    except Exception:
-        pass
-    # Sustained rate of the same pattern in long launches (16x the gathers): a c2-sized launch
-    # spends ~6.7 us of its ~10.6 us in launch ramp and tail (profiles/r01c_l2_gather_sustained.txt).
-    l2s = None
-    try:
-        for line in open(os.path.join(ROOT, "profiles", "r01c_l2_gather_sustained.txt")):
-            if line.startswith("l2_gather_sustained_gbs"):
-                l2s = float(line.split()[1])
-    except Exception:
-        pass
-    if l2 and "spmm" in prof and prof["spmm"][1]:
-        ms, cnt = prof["spmm"]
-        gath = 8 * ell * nnz_f + 12 * nnz_f  # one ell-wide panel row per nonzero + the CSR entry
-        gbs = gath / (ms / cnt * 1e-3) / 1e9
-        out["roofline"]["l2_gather"] = {"achieved": round(gbs, 1), "peak": l2, "unit": "GB/s",
-                                        "frac": round(gbs / l2, 4), "bytes_per_launch": gath,
-                                        "peak_source": "profiles/r01_l2_gather_peak.txt (tools/probe_l2: the same "
-                                                       "gathers in one launch of the same size)"}
-        if l2s:
-            out["roofline"]["l2_gather"].update({"sustained_peak": l2s, "frac_of_sustained": round(gbs / l2s, 4),
-                                                 "sustained_source": "profiles/r01c_l2_gather_sustained.txt"})
+        return None
+
+
+def roofline_from_profile(prof: dict, config: str, ms_step: float) -> dict:
+    """Roofline of the metric's kernel (the SpMM, HBM-bound) and the Gram (FP64 tensor) from
+    the profiled step: achieved = the algorithmic bytes / flops the library declared for
+    those launches (SURVEY 8(d) formulas) / their summed CUDA-event durations."""
+    peaks, src = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    kern = {}
+    total_ms = sum(v[0] for k, v in prof.items() if k != "rng_gen")
+    for k, (ms, cnt, fl, by) in prof.items():
+        kern[k] = {"ms": round(ms, 4), "launches": cnt, "share": round(ms / total_ms, 4) if total_ms else None}
+        if cnt and by:
+            kern[k]["alg_bytes_per_launch"] = by / cnt
+            kern[k]["achieved_gbs"] = round(by / (ms * 1e-3) / 1e9, 1)
+        if cnt and fl:
+            kern[k]["alg_flops_per_launch"] = fl / cnt
+            kern[k]["achieved_tflops"] = round(fl / (ms * 1e-3) / 1e12, 3)
+    out = {"kernels": kern}
+    sp = kern.get("spmm", {})
+    ach = sp.get("achieved_gbs")
+    out["roofline"] = {"bound": "hbm", "kernel": "spmm (CSR / CSC gather, ell-wide FP64 panels)",
+                       "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4) if ach else None,
+                       "traffic": _traffic(config), "peak_source": src,
+                       "alg_bytes_per_launch": sp.get("alg_bytes_per_launch"),
+                       "frac_of_nominal_8tbs": round(ach / 8000.0, 4) if ach else None,
+                       "note": "achieved = SURVEY 8(d) bytes 12 nnz + 8 (m+1) + 8 ell (m + d) per launch / average "
+                               "launch duration (CUDA events on the lane stream, four flushes in flight); traffic = "
+                               "ncu dram__bytes per launch for this config (profiles/ncu_summary.json)"}
+    g = kern.get("gram", {})
+    if g.get("achieved_tflops"):
+        out["roofline"]["gram"] = {"bound": "tensor (FP64 DMMA)", "achieved": g["achieved_tflops"],
+                                   "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                   "frac": round(g["achieved_tflops"] / FP64_PEAK_TFLOPS, 4),
+                                   "flops": "n k (k+1) per Gram (distinct dot products), declared per launch",
+                                   "peak_source": "profiles/r01_fp64_peak.txt (mma.sync m8n8k4 f64 probe)"}
+    dom = max((k for k in prof if k != "rng_gen"), key=lambda k: prof[k][0]) if prof else None
     out["dominant_kernel"] = {"class": dom, "share_of_step": kern[dom]["share"] if dom else None}
     return out
+
+
+def isolated_roofline(prof: dict) -> dict:
+    peaks, _ = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    res = {"what": "the same profiled step with one flush in flight (SFDG_LANES=1): standalone launch durations"}
+    for k, peak, unit in (("spmm", hbm, "GB/s"), ("gram", FP64_PEAK_TFLOPS, "TFLOP/s")):
+        if k not in prof or not prof[k][1]:
+            continue
+        ms, cnt, fl, by = prof[k]
+        ach = by / (ms * 1e-3) / 1e9 if unit == "GB/s" else fl / (ms * 1e-3) / 1e12
+        res[k] = {"achieved": round(ach, 2), "peak": peak, "unit": unit, "frac": round(ach / peak, 4),
+                  "us_per_launch": round(1e3 * ms / cnt, 2), "launches": cnt}
+    return res
 
 
 if __name__ == "__main__":

@@ -543,6 +543,17 @@ class Reference:
         self._chk(self.L.ref_cov_err(*args, _ptr(b, _dp), b.shape[0], rng.h, iterations, C.byref(out)))
         return out.value
 
+    def power_sweep(self, row_ptr, cols, vals, d, y):
+        """One simultaneous_iteration sweep (randsvd.cpp:39-48) from y (m x k): (y', seconds)."""
+        args, keep = self._csr(row_ptr, cols, vals, d)
+        y = _f64(y)
+        out = np.zeros_like(y)
+        secs = C.c_double()
+        self.L.ref_power_sweep.argtypes = [_i64p, _u32p, _dp, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp,
+                                           C.POINTER(C.c_double)]
+        self._chk(self.L.ref_power_sweep(*args, y.shape[1], _ptr(y, _dp), _ptr(out, _dp), C.byref(secs)))
+        return out, secs.value
+
     def sketch(self, row_ptr, cols, vals, d, ell, seed=0, delta=0.1, power: PowerConfig | None = None):
         args, keep = self._csr(row_ptr, cols, vals, d)
         out = np.zeros((ell, d))
@@ -551,6 +562,50 @@ class Reference:
                                     _ptr(stats, _dp)))
         return out, {"flushes": int(stats[0]), "attempts": int(stats[1]), "verifier_i": int(stats[2]),
                      "delta_spent": float(stats[3])}
+
+
+class RefSketcher:
+    """A live reference SfdSketcher (oracle/ref_shim.cpp ref_sketcher_*), appended row by row."""
+
+    def __init__(self, lib: Reference, ell, d, seed=0, delta=0.1):
+        L = lib.L
+        L.ref_sketcher_new.restype = C.c_void_p
+        L.ref_sketcher_new.argtypes = [C.c_size_t, C.c_size_t, C.c_double, C.c_uint64]
+        L.ref_sketcher_free.argtypes = [C.c_void_p]
+        L.ref_sketcher_append.argtypes = [C.c_void_p, _u32p, _dp, C.c_size_t]
+        L.ref_sketcher_sketch.argtypes = [C.c_void_p, _dp]
+        L.ref_sketcher_stats.argtypes = [C.c_void_p, _dp]
+        self.lib, self.ell, self.d = lib, ell, d
+        self.h = L.ref_sketcher_new(ell, d, delta, C.c_uint64(seed))
+        if not self.h:
+            _raise(1, L.ref_last_error().decode())
+
+    def __del__(self):
+        try:
+            self.lib.L.ref_sketcher_free(self.h)
+        except Exception:
+            pass
+
+    def append(self, indices, values):
+        cs = np.ascontiguousarray(indices, dtype=np.uint32)
+        vs = np.ascontiguousarray(values, dtype=np.float64)
+        if cs.size == 0:
+            cs, vs = np.zeros(1, np.uint32), np.zeros(1)
+            n = 0
+        else:
+            n = cs.size
+        self.lib._chk(self.lib.L.ref_sketcher_append(self.h, _ptr(cs, _u32p), _ptr(vs, _dp), n))
+
+    def sketch(self):
+        out = np.zeros((self.ell, self.d))
+        self.lib.L.ref_sketcher_sketch(self.h, _ptr(out, _dp))
+        return out
+
+    def stats(self):
+        st = np.zeros(7)
+        self.lib.L.ref_sketcher_stats(self.h, _ptr(st, _dp))
+        return {"flushes": int(st[0]), "attempts": int(st[1]), "verifier_i": int(st[2]), "delta_spent": float(st[3]),
+                "buf_rows": int(st[4]), "buf_nnz": int(st[5]), "buf_frob_sq": float(st[6])}
 
 
 class RefRng:

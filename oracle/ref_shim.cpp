@@ -6,6 +6,7 @@
 // oracle/sfd_oracle.h with a `ref_` prefix so tests can run both side by side.
 // Exceptions map to the same status codes: 1 invalid_argument, 2 numerical_error.
 
+#include <chrono>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -219,6 +220,70 @@ int ref_sketch(const int64_t* row_ptr, const uint32_t* cols, const double* vals,
         stats[2] = static_cast<double>(s.verifier().i);
         stats[3] = s.verifier().delta_spent;
     });
+}
+
+// One power sweep of simultaneous_iteration (randsvd.cpp:39-48: for every column, rmatvec then
+// matvec; the finiteness check; orthonormalize) over the reference's own SparseBuffer and
+// orthonormalize, from a given Y (m x k). *seconds = wall time of the sweep alone. Used by
+// bench.py's reference arm, which extrapolates a flush as (q + 1) sweeps.
+int ref_power_sweep(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t m, size_t d, size_t k,
+                    const double* y_in, double* y_out, double* seconds) {
+    return guarded([&] {
+        sfd::SparseBuffer a = to_buffer(row_ptr, cols, vals, m, d);
+        sfd::DenseMatrix y(m, k);
+        std::memcpy(y.data.data(), y_in, m * k * sizeof(double));
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<double> ycol(m);
+        sfd::DenseMatrix next(m, k);
+        for (size_t j = 0; j < k; ++j) {
+            for (size_t i = 0; i < m; ++i) ycol[i] = y(i, j);
+            std::vector<double> w = a.rmatvec(ycol);
+            std::vector<double> yc = a.matvec(w);
+            for (size_t i = 0; i < m; ++i) next(i, j) = yc[i];
+        }
+        if (!sfd::all_finite(next)) throw sfd::numerical_error("simultaneous_iteration: non-finite intermediate");
+        y = sfd::orthonormalize(next);
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        put(y, y_out);
+    });
+}
+
+// A live SfdSketcher (sketch.hpp:22-49) driven row by row, so tests can read the reference's
+// state after an append that throws (sketch.cpp:20-32: the exception leaves B, the counters
+// and the buffer as they were at the failing flush).
+void* ref_sketcher_new(size_t ell, size_t d, double delta, uint64_t seed) {
+    sfd::SketchConfig cfg;
+    cfg.ell = ell;
+    cfg.d = d;
+    cfg.delta = delta;
+    cfg.seed = seed;
+    try {
+        return new sfd::SfdSketcher(cfg);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void ref_sketcher_free(void* h) { delete static_cast<sfd::SfdSketcher*>(h); }
+int ref_sketcher_append(void* h, const uint32_t* cols, const double* vals, size_t len) {
+    return guarded([&] {
+        sfd::SparseRow r;
+        r.indices.assign(cols, cols + len);
+        r.values.assign(vals, vals + len);
+        static_cast<sfd::SfdSketcher*>(h)->append(r);
+    });
+}
+void ref_sketcher_sketch(void* h, double* out) { put(static_cast<sfd::SfdSketcher*>(h)->sketch(), out); }
+// [flushes, attempts, verifier_i, delta_spent, buffer_rows, buffer_nnz, buffer_frob_sq]
+void ref_sketcher_stats(void* h, double* st) {
+    auto* s = static_cast<sfd::SfdSketcher*>(h);
+    st[0] = static_cast<double>(s->flush_count());
+    st[1] = static_cast<double>(s->attempt_total());
+    st[2] = static_cast<double>(s->verifier().i);
+    st[3] = s->verifier().delta_spent;
+    st[4] = static_cast<double>(s->buffer().rows());
+    st[5] = static_cast<double>(s->buffer().nnz());
+    st[6] = s->buffer().frob_sq();
 }
 
 }  // extern "C"

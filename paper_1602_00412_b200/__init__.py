@@ -149,11 +149,12 @@ def profile_begin() -> None:
 
 
 def profile_end() -> dict:
-    """Stop timing; returns {kernel_class: (total_ms, launches)}."""
+    """Stop timing; returns {kernel_class: (total_ms, launches, flops, bytes)} -- the flops /
+    bytes are the algorithmic work the library declared for those launches."""
     import json
     buf = C.create_string_buffer(1 << 16)
     lib().sfdg_profile_end(buf, len(buf))
-    return {k: (v[0], v[1]) for k, v in json.loads(buf.value.decode()).items()}
+    return {k: (v[0], v[1], v[2], v[3]) for k, v in json.loads(buf.value.decode()).items()}
 
 
 def _check(code: int) -> None:
@@ -176,9 +177,27 @@ def _p(a: np.ndarray, t):
 
 
 def _csr(row_ptr, cols, vals):
+    """Host CSR in the C ABI's types. The C side trusts row_ptr for its reads, so the array
+    shapes are checked here: row_ptr non-decreasing from >= 0, row_ptr[-1] <= len(cols) ==
+    len(vals) (the reference rejects an index/value length mismatch, sparse.cpp:9-10), and
+    column ids representable as uint32 (a wider id must not wrap onto a valid column)."""
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
-    cs = np.ascontiguousarray(cols, dtype=np.uint32)
+    c_in = np.asarray(cols)
+    if c_in.size and c_in.dtype != np.uint32:
+        if c_in.dtype.kind not in "iu":
+            raise InvalidArgument("SparseRow: column indices must be integers")
+        if int(c_in.min()) < 0 or int(c_in.max()) > 0xFFFFFFFF:
+            raise InvalidArgument("SparseRow: index out of range")
+    cs = np.ascontiguousarray(c_in, dtype=np.uint32)
     vs = np.ascontiguousarray(vals, dtype=np.float64)
+    if rp.ndim != 1 or rp.size < 1:
+        raise InvalidArgument("row_ptr must be a 1-d array of n+1 offsets")
+    if cs.size != vs.size:
+        raise InvalidArgument("SparseRow: indices and values size mismatch")
+    if rp[0] < 0 or (rp.size > 1 and bool(np.any(np.diff(rp) < 0))):
+        raise InvalidArgument("row_ptr must be non-decreasing from a non-negative offset")
+    if int(rp[-1]) > cs.size:
+        raise InvalidArgument("row_ptr[-1] exceeds the number of stored entries")
     if cs.size == 0:  # keep valid pointers for empty inputs
         cs, vs = np.zeros(1, np.uint32), np.zeros(1)
     return rp, cs, vs

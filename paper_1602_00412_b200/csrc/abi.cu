@@ -222,45 +222,77 @@ class Sketcher {
         if (ev_verify) cudaEventDestroy(ev_verify);
     }
 
-    void append_host(const int64_t* rp, const uint32_t* cols, const double* vals, size_t nrows, size_t* done) {
+    // sync_errors (the public append): the call returns only when every flush it triggered
+    // has committed, so a numerical error surfaces here, reported at its trigger row with the
+    // reference's state (sketch.cpp:20-32: B and the counters of the last good flush, the
+    // failing flush's rows still buffered, rows after the trigger not appended). Without it
+    // (the file reader, which overlaps parsing with the device) flushes may still run on return.
+    void append_host(const int64_t* rp, const uint32_t* cols, const double* vals, size_t nrows, size_t* done,
+                     bool sync_errors = true) {
         chain->set_device();
         if (done) *done = 0;
-        size_t r = 0;
-        while (r < nrows) {
-            const size_t take = segment(rp, r, nrows);
-            // validate before committing (sparse.cpp:8-20); rows before a bad row stay in
-            size_t good = 0;
-            std::string err;
-            for (; good < take; ++good) {
-                const size_t i = r + good;
-                try {
-                    if (rp[i + 1] < rp[i]) throw invalid_argument("append_row: index/value length mismatch");
-                    validate_row(cols + rp[i], vals + rp[i], rp[i + 1] - rp[i], cfg.d);
-                } catch (const invalid_argument& e) {
-                    err = e.what();
-                    break;
+        // segment() binary-searches row_ptr for the trigger row, which needs it monotone: rows
+        // past a decreasing offset are never segmented (the per-row check below rejects it)
+        for (size_t i = 0; i < nrows; ++i)
+            if (rp[i + 1] < rp[i]) {
+                nrows = i + 1;
+                break;
+            }
+        failed_row = -1;
+        try {
+            size_t r = 0;
+            while (r < nrows) {
+                const size_t take = segment(rp, r, nrows);
+                // validate before committing (sparse.cpp:8-20); rows before a bad row stay in
+                size_t good = 0;
+                std::string err;
+                for (; good < take; ++good) {
+                    const size_t i = r + good;
+                    try {
+                        if (rp[i + 1] < rp[i]) throw invalid_argument("append_row: index/value length mismatch");
+                        validate_row(cols + rp[i], vals + rp[i], rp[i + 1] - rp[i], cfg.d);
+                    } catch (const invalid_argument& e) {
+                        err = e.what();
+                        break;
+                    }
                 }
+                if (good > 0) commit_host(rp, cols, vals, r, good);
+                if (good < take) {
+                    finish_copies();
+                    if (sync_errors) settle();  // a flush before the bad row fails first (row order)
+                    if (done) *done = r + good;
+                    throw invalid_argument(err);
+                }
+                r += take;
+                if (done) *done = r;
+                trigger_row = (int64_t)r - 1;  // the trigger can only fire at a segment's last row
+                maybe_flush();
             }
-            if (good > 0) commit_host(rp, cols, vals, r, good);
-            if (good < take) {
-                if (done) *done = r + good;
-                finish_copies();
-                throw invalid_argument(err);
-            }
-            r += take;
-            if (done) *done = r;
-            maybe_flush();
+            finish_copies();  // the caller may reuse its (possibly pinned) buffers on return
+            if (sync_errors) settle();
+            else pump();
+        } catch (const numerical_error&) {
+            finish_copies();
+            if (done && failed_row >= 0) *done = (size_t)failed_row + 1;
+            throw;
         }
-        finish_copies();  // the caller may reuse its (possibly pinned) buffers on return
-        pump();
     }
 
     void append_device(const int64_t* h_rp, const uint32_t* d_cols, const double* d_vals, size_t nrows, size_t* done) {
         chain->set_device();
         if (done) *done = 0;
         if (nrows == 0) return;
+        size_t bad_rp = nrows;  // first row with a decreasing offset: rows before it are committed
         for (size_t i = 0; i < nrows; ++i)
-            if (h_rp[i + 1] < h_rp[i]) throw invalid_argument("append_row: index/value length mismatch");
+            if (h_rp[i + 1] < h_rp[i]) {
+                bad_rp = i;
+                break;
+            }
+        if (bad_rp < nrows) {
+            if (bad_rp > 0) append_device(h_rp, d_cols, d_vals, bad_rp, done);
+            if (done) *done = bad_rp;
+            throw invalid_argument("append_row: index/value length mismatch");
+        }
         Engine& E = *lanes[fill].eng;  // idle apart from row copies
         E.scr.reset();
         int64_t* d_rp = E.scr.take<int64_t>((int64_t)nrows + 1);
@@ -270,16 +302,24 @@ class Sketcher {
                                                  E.st);
         E.scr.reset();
         const size_t limit = bad < 0 ? nrows : (size_t)bad;
-        size_t r = 0;
-        while (r < limit) {
-            const size_t take = segment(h_rp, r, limit);
-            commit_device(h_rp, d_cols, d_vals, r, take);
-            r += take;
-            if (done) *done = r;
-            maybe_flush();
+        failed_row = -1;
+        try {
+            size_t r = 0;
+            while (r < limit) {
+                const size_t take = segment(h_rp, r, limit);
+                commit_device(h_rp, d_cols, d_vals, r, take);
+                r += take;
+                if (done) *done = r;
+                trigger_row = (int64_t)r - 1;
+                maybe_flush();
+            }
+            finish_copies();
+            settle();
+        } catch (const numerical_error&) {
+            finish_copies();
+            if (done && failed_row >= 0) *done = (size_t)failed_row + 1;
+            throw;
         }
-        finish_copies();
-        pump();
         if (bad >= 0)
             throw invalid_argument((kind & ERR_BAD_INDEX) ? "append_row: column index out of range or not increasing"
                                                           : "append_row: non-finite value");
@@ -291,6 +331,7 @@ class Sketcher {
         Lane& F = lanes[fill];
         if (F.rows() > 0) {
             if (F.rows() >= cfg.ell) {
+                trigger_row = -1;
                 flush();
                 drain();
             } else {
@@ -450,6 +491,8 @@ class Sketcher {
         cudaEvent_t tr0 = nullptr, tr1 = nullptr;  // SFDG_TRACE: timed bounds of the queued phase
         double tr_enq = 0.0, tr_enq_end = 0.0;
         bool bp_pending = false;
+        int64_t trigger_row = -1;      // row of the append call whose trigger started this flush
+        std::exception_ptr failure;    // numerical error of this flush, raised when it is the head
         size_t rows() const { return rp.size() - 1; }
         void clear_rows() {
             rp.assign(1, 0);
@@ -555,6 +598,8 @@ class Sketcher {
     void flush() {
         Lane& L = lanes[fill];
         L.id = next_id++;
+        L.trigger_row = trigger_row;
+        L.failure = nullptr;
         L.phase = Lane::Preparing;
         run(L, [this, &L] {
             L.eng->scr.reset();
@@ -599,6 +644,7 @@ class Sketcher {
     void start_flush(Lane& L, const FlushState& st) {
         L.start = st;
         L.cur = st;
+        L.failure = nullptr;
         L.attempt = 0;
         L.interval = L.interval_base;
         L.checked = L.checked_base;
@@ -643,8 +689,19 @@ class Sketcher {
         return e && std::atoi(e) != 0;
     }
 
-    // Advance one lane whose queued phase has completed.
+    // Advance one lane whose queued phase has completed. A numerical error (retry cap,
+    // non-finite intermediate) is held on the lane: it is the reference's error only if the
+    // lane reaches the head of the queue with its start state confirmed (step()).
     void advance(Lane& L, size_t idx_in_flight) {
+        try {
+            advance_phase(L, idx_in_flight);
+        } catch (const numerical_error&) {
+            L.failure = std::current_exception();
+            L.phase = Lane::Done;
+        }
+    }
+
+    void advance_phase(Lane& L, size_t idx_in_flight) {
         Engine& e = *L.eng;
         switch (L.phase) {
             case Lane::Preparing: {
@@ -749,7 +806,7 @@ class Sketcher {
 
     // One round of progress; blocking = wait for the oldest pending phase if nothing moved.
     void step(bool blocking) {
-        bool moved = false;
+        bool moved = false, head_failed = false;
         try {
             for (size_t k = 0; k < inflight.size(); ++k) {
                 Lane& L = lanes[inflight[k]];
@@ -773,6 +830,10 @@ class Sketcher {
                     moved = true;
                     break;
                 }
+                if (L.failure) {
+                    head_failed = true;
+                    break;
+                }
                 commit(L);
                 inflight.pop_front();
                 moved = true;
@@ -781,6 +842,7 @@ class Sketcher {
             abort_inflight();
             throw;
         }
+        if (head_failed) fail_head();
         // Nothing moved: the caller spins. Polling every lane (rather than blocking on one
         // event) lets whichever lane finishes first get its next phase queued at once.
         if (!moved && blocking) std::this_thread::yield();
@@ -840,6 +902,49 @@ class Sketcher {
         while (!inflight.empty()) step(true);
     }
 
+    // End of a public append: every flush it triggered has committed and the chain's dense
+    // shrinks have run (their device errors, which cannot be rolled back, are raised here).
+    void settle() {
+        drain();
+        chain->check_errors();
+    }
+
+    // The head flush failed for real (sketch.cpp:25-32 throws out of append): the sketcher
+    // takes the reference's post-exception state -- B and the counters of the last committed
+    // flush, the Rng / verifier advanced by the failed attempts, the failing flush's rows
+    // back in the buffer, every later row dropped (never appended in the reference) -- and
+    // the error is rethrown with its trigger row in failed_row.
+    void fail_head() {
+        const int h = inflight.front();
+        Lane& L = lanes[h];
+        std::exception_ptr ep = L.failure;
+        for (auto& K : lanes)
+            if (K.worker) {
+                K.worker->wait();
+                K.worker->take_error();
+            }
+        for (auto& K : lanes) CK(cudaStreamSynchronize(K.eng->st));
+        chain->sync();
+        committed = L.cur;
+        for (int i : inflight)
+            if (i != h) {
+                lanes[i].phase = Lane::Idle;
+                lanes[i].clear_rows();
+            }
+        inflight.clear();
+        if (fill != h) {
+            lanes[fill].phase = Lane::Idle;
+            lanes[fill].clear_rows();
+        }
+        for (auto& K : lanes) CK(cudaMemsetAsync(K.eng->d_err, 0, sizeof(int), K.eng->st));
+        fill = h;
+        L.phase = Lane::Filling;  // keeps rp / nnz / frob and its device CSR
+        L.failure = nullptr;
+        failed_row = L.trigger_row;
+        copies_on.clear();
+        std::rethrow_exception(ep);
+    }
+
     void sync_all() {
         for (auto& L : lanes)
             if (L.worker) L.worker->wait();
@@ -889,6 +994,8 @@ class Sketcher {
     std::mutex verify_mu;
     bool serial_verify = !(std::getenv("SFDG_VERIFY_SERIAL") && std::atoi(std::getenv("SFDG_VERIFY_SERIAL")) == 0);
     FlushState committed;
+    int64_t trigger_row = -1;  // call-relative row whose trigger the next flush() records
+    int64_t failed_row = -1;   // trigger row of the flush whose numerical error was raised
     int fill = 0;
     uint64_t next_id = 0;
     int64_t nnz_trigger = 0;
@@ -1232,7 +1339,7 @@ int sfdg_sketch_file(const char* path, size_t plain_cols, const sfdg_sketch_conf
             read_row_stream(path, plain_cols, 0, &d, [&](const int64_t* rp, const uint32_t* cs, const double* vs,
                                                          size_t nrows) {
                 make();
-                sk->append_host(rp, cs, vs, nrows, nullptr);
+                sk->append_host(rp, cs, vs, nrows, nullptr, false);
             });
         } catch (...) {
             if (d_out) *d_out = d;

@@ -654,6 +654,7 @@ void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, doub
     if (k <= 0) return;
     if (k > 512) throw invalid_argument("chol_factor: k > 512 unsupported");
     ProfScope prof(polar ? "chol_polar" : "chol", st);
+    prof.work((double)k * k * k / 3.0, 16.0 * (double)k * k);
     const bool use_smem = k <= kSmemMaxK;
     double* gscr = nullptr;
     size_t smem = 2 * (size_t)k * sizeof(double);
@@ -663,11 +664,9 @@ void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, doub
         gscr = scr.take<double>((int64_t)k * k + 2 * k);
         smem = 0;
     }
-    static bool attr_set = false;
-    if (!attr_set) {
+    if (first_on_device((const void*)(chol_factor_kernel))) {
         allow_max_dynamic_smem(chol_factor_kernel);
         allow_max_dynamic_smem(trsm_apply_kernel);
-        attr_set = true;
     }
     LAUNCH(chol_factor_kernel, 1, kCholThreads, smem, st, G, k, ldg, R, dinv8, T, ldt, stats, d_err, err_bit, gscr,
            use_smem ? 1 : 0, polar ? 1 : 0, udrop);
@@ -679,11 +678,10 @@ void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const do
     const int kp = (k + 7) / 8 * 8;
     if (kp > 512) throw invalid_argument("trsm_apply: k > 512 unsupported");
     ProfScope prof("trsm", st);
+    prof.work((double)m * k * k, 16.0 * (double)m * k);  // X = Y R^-1: k^2 / 2 multiply-adds per row
     if (kp > kTrsmSmemK) {  // R streamed through shared memory one block-column panel at a time
-        static bool pattr = false;
-        if (!pattr) {
+        if (first_on_device((const void*)(trsm_panel_kernel))) {
             allow_max_dynamic_smem(trsm_panel_kernel);
-            pattr = true;
         }
         int rows = 128;
         auto pbytes = [&](int r) {

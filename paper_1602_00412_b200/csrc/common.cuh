@@ -98,8 +98,15 @@ class ProfScope {
     ProfScope(const ProfScope&) = delete;
     ProfScope& operator=(const ProfScope&) = delete;
 
+    // Algorithmic work of this launch (SURVEY 8(d) formulas), reported by sfdg_profile_end.
+    void work(double flops, double bytes) {
+        flops_ = flops;
+        bytes_ = bytes;
+    }
+
   private:
     const char* cls_ = nullptr;
+    double flops_ = 0.0, bytes_ = 0.0;
     cudaStream_t st_;
     cudaEvent_t e0_ = nullptr, e1_ = nullptr;
 };
@@ -118,6 +125,11 @@ inline void allow_max_dynamic_smem(F* func) {
     CK(cudaFuncSetAttribute((const void*)func, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             optin - (int)attr.sharedSizeBytes));
 }
+
+// True the first time `key` (a kernel's address) is seen on the calling thread's current
+// device; thread-safe. Function attributes such as the dynamic shared memory opt-in are per
+// device, so a process driving several GPUs (sfdg_sharded_sketch) must set them on each.
+bool first_on_device(const void* key);
 
 inline size_t round_up(size_t x, size_t m) { return (x + m - 1) / m * m; }
 inline unsigned ceil_div(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }

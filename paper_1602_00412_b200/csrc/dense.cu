@@ -304,6 +304,8 @@ void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scrat
         return;
     }
     ProfScope prof("gram", st);
+    // algorithmic: the k(k+1)/2 distinct dot products of length n, X read once
+    prof.work((double)n * k * (k + 1), 8.0 * ((double)n * k + (double)k * k));
     const int T = (k + TB - 1) / TB;
     const int ntiles = T * (T + 1) / 2;
     int target_chunks = std::max(1, (2 * kSMs + ntiles - 1) / ntiles);
@@ -311,11 +313,9 @@ void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scrat
     const int nchunks = (n + rows_per_chunk - 1) / rows_per_chunk;
     double* partial = scr.take<double>((int64_t)nchunks * k * k);
     const size_t smem = 2 * 2 * KT * LDT * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device((const void*)(gram_tn_kernel<2>))) {
         allow_max_dynamic_smem(gram_tn_kernel<2>);
         allow_max_dynamic_smem(gram_tn_kernel<1>);
-        attr = true;
     }
     if (vec16(X, ldx) && k % 2 == 0)
         LAUNCH(gram_tn_kernel<2>, dim3(ntiles, nchunks), 128, smem, st, X, n, k, ldx, rows_per_chunk, T, partial);
@@ -332,12 +332,11 @@ void gemm_nn(const double* X, int n, int k, int ldx, const double* S, int c, int
         return;
     }
     ProfScope prof("gemm", st);
+    prof.work(2.0 * n * (double)k * c, 8.0 * ((double)n * k + (double)k * c + (double)n * c));
     const size_t smem = 2 * (TB * LDK + KT * LDT) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device((const void*)(gemm_nn_kernel<2>))) {
         allow_max_dynamic_smem(gemm_nn_kernel<2>);
         allow_max_dynamic_smem(gemm_nn_kernel<1>);
-        attr = true;
     }
     if (vec16(X, ldx) && vec16(S, lds) && k % 2 == 0 && c % 2 == 0)
         LAUNCH(gemm_nn_kernel<2>, dim3(ceil_div(n, TB), ceil_div(c, TB)), 128, smem, st, X, n, k, ldx, S, c, lds, C,

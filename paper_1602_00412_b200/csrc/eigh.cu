@@ -311,12 +311,10 @@ void eigh(const double* K, int n, int ldk, double off_tol, const double* d_fsq, 
     a.V = scr.take<double>((int64_t)N * N);
     a.err = d_err;
     a.only_if = fallback;
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device((const void*)(jacobi_kernel<true, true>))) {
         allow_max_dynamic_smem(jacobi_kernel<true, true>);
         allow_max_dynamic_smem(jacobi_kernel<true, false>);
         allow_max_dynamic_smem(vapply_kernel);
-        attr = true;
     }
     const size_t table = (size_t)P * (P + 1) / 2 * sizeof(uint32_t);
     const bool use_table = use_smem && packed * sizeof(double) + table <= 200 * 1024;

@@ -1190,10 +1190,8 @@ __global__ void __launch_bounds__(256) backtransform_kernel(const double* __rest
 template <int NT>
 void launch_backtransform(const double* vh, const double* tau, int n, int nval, const int* trivial, double* X,
                           int ldx, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device((const void*)(backtransform_kernel<NT>))) {
         allow_max_dynamic_smem(backtransform_kernel<NT>);
-        attr = true;
     }
     const int R = std::max(1, std::min(n, (int)((96 * 1024) / (sizeof(double) * (n + 1)))));
     const size_t smem = (size_t)R * (n + 1) * sizeof(double);
@@ -1428,10 +1426,8 @@ __global__ void __launch_bounds__(NTHR) tridiag_packed_kernel(TriArgs a) {
 template <int NT, int NTHR>
 void launch_packed(const TriArgs& a, size_t smem, cudaStream_t st) {
     auto* fn = tridiag_packed_kernel<NT, NTHR>;
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device((const void*)(fn))) {
         allow_max_dynamic_smem(fn);
-        attr = true;
     }
     static const int excl = getenv("SFDG_TRIDIAG_EXCLUSIVE") ? atoi(getenv("SFDG_TRIDIAG_EXCLUSIVE")) : 1;
     if (excl) {
@@ -1465,19 +1461,13 @@ bool launch_tridiag_packed(const TriArgs& a, cudaStream_t st) {
 template <int C, int NT, int NTHR>
 void launch_rows(const TriRowsArgs& ra, size_t smem, cudaStream_t st) {
     auto* fn = tridiag_rows_kernel<C, NT, NTHR>;
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device((const void*)(fn))) {
         allow_max_dynamic_smem(fn);
         CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
     }
     // Exclusive SMs: asking for all the shared memory an SM has keeps other kernels' blocks
     // (the lanes' SpMMs) off the SMs this latency-bound chain kernel runs on.
-    static int excl = -1;
-    if (excl < 0) {
-        const char* e = getenv("SFDG_TRIDIAG_EXCLUSIVE");
-        excl = e ? atoi(e) : 1;
-    }
+    static const int excl = getenv("SFDG_TRIDIAG_EXCLUSIVE") ? atoi(getenv("SFDG_TRIDIAG_EXCLUSIVE")) : 1;
     if (excl) {
         cudaFuncAttributes fa;
         CK(cudaFuncGetAttributes(&fa, (const void*)fn));
@@ -1502,11 +1492,9 @@ void launch_rows(const TriRowsArgs& ra, size_t smem, cudaStream_t st) {
 template <int C, int NT, int RPW>
 void launch_regs(const TriRowsArgs& ra, cudaStream_t st) {
     auto* fn = tridiag_regs_kernel<C, NT, RPW>;
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device((const void*)(fn))) {
         allow_max_dynamic_smem(fn);
         CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
     }
     size_t smem = 4 * (size_t)ra.a.n * sizeof(double);
     static const int excl = getenv("SFDG_TRIDIAG_EXCLUSIVE") ? atoi(getenv("SFDG_TRIDIAG_EXCLUSIVE")) : 1;
@@ -1611,12 +1599,10 @@ void eigh_tri(const double* K, int n, int ldk, double off_tol, const double* d_f
     a.trivial = scr.take<int>(1);
     const int64_t inv_slots = (int64_t)ceil_div(nval, 64) * 64;
     double* work = scr.take<double>(inv_slots * (5 * (int64_t)n + (n + 31) / 32 + 1));
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device((const void*)(tridiag_kernel<true>))) {
         allow_max_dynamic_smem(tridiag_kernel<true>);
         allow_max_dynamic_smem(inviter_kernel);
         allow_max_dynamic_smem(twisted_kernel);
-        attr = true;
     }
     {
         ProfScope prof("eigh_tridiag", st);

@@ -377,8 +377,8 @@ void Engine::sweep_block(int interval, int m) {
                                         (uintptr_t)a.row_idx,  (uintptr_t)a.cval,     (uintptr_t)d};
     auto body = [&] {
         for (int i = 0; i < interval; ++i) {
-            spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st);
-            spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
+            spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st, m, ell);
+            spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell);
         }
         orthonormalize_light(m, ERR_NONFINITE_ITER);  // swaps Y and Yt (host side)
     };
@@ -418,7 +418,7 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     const size_t q = power_iteration_count((size_t)m, cfg);
     // G = gaussian_matrix(d, k) in W (la_core.cpp:167-172), pad columns zero
     rng->normals(pos, (uint64_t)d * k, (uint64_t)k, (uint64_t)lp, W, d_err, st);
-    spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
+    spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell);
     if (adaptive && q > 0) orthonormalize_light(m, ERR_NONFINITE_ITER);
     else orthonormalize(Y, m, ERR_NONFINITE_ITER);
     // Only span(Y) matters for B' (it enters through Z Z^T), so CholeskyQR2 runs every
@@ -438,8 +438,8 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
             last_since = interval;
             continue;
         }
-        spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st);
-        spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st);
+        spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st, m, ell);
+        spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell);
         if (++since >= interval || s + 1 == q) {
             if (adaptive && s + 1 < q) orthonormalize_light(m, ERR_NONFINITE_ITER);
             else orthonormalize(Y, m, ERR_NONFINITE_ITER);
@@ -455,7 +455,7 @@ void Engine::sparse_shrink(const PowerCfg& cfg, double* bpt, int ldb) {
     if (ell > d) throw invalid_argument("sparse_shrink: ell exceeds column count");
     simultaneous_iteration(ell, cfg);
     // W = A'^T Z = P^T (d x lp): project_rows (sparse.cpp:57-69) without the transpose
-    spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st);
+    spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st, m, ell);
     double* fsq = d_scal + 0;
     sumsq(W, d, lp, lp, fsq, d_err, ERR_NONFINITE_PROJ, scr, st);  // all_finite(P) (shrink.cpp:70)
     // svd_top(P, ell): PP^T = W^T W, eigen, right vectors and the shrink in one GEMM
@@ -504,6 +504,7 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
     args.piece_end = plan_c.piece_end;
     args.counts = plan_c.counts;
     args.lpart = scr.take<double>(std::max<int64_t>(1, plan_c.cap_pieces));
+    args.nnz = a.nnz;
     if (verify_as_graph()) {
         // kernel-sequence verifier: per-call scalars by a setup kernel, the steps replayed
         // from a graph captured once per (step count, buffers); no serialisation needed
@@ -557,6 +558,11 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
                 nb = rb;
                 args.resident = 1;
             }
+        }
+        if (verify_cluster == 0 && !args.resident && !(std::getenv("SFDG_VERIFY_BALANCE") && std::atoi(std::getenv("SFDG_VERIFY_BALANCE")) == 0)) {
+            int64_t* prefix = scr.take<int64_t>((int64_t)d + 1);
+            verify_column_costs(a.col_ptr, d, ell, prefix, scr, st);
+            args.ccost = prefix;
         }
         if (serial) CK(cudaStreamWaitEvent(st, serial, 0));
         verify_launch(args, nb, verify_cluster, st);

@@ -527,10 +527,15 @@ void SegPlan::release() {
 }
 
 void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, const SegPlan& plan, int64_t nnz,
-          const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st) {
+          const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st,
+          int64_t in_rows, int alg_cols) {
     if (nrows == 0) return;
     if (ncols % 2 != 0 || ld % 2 != 0 || ldo % 2 != 0) throw invalid_argument("spmm: panel widths must be even");
     ProfScope prof("spmm", st);
+    {
+        const double w = alg_cols > 0 ? alg_cols : ncols, ir = in_rows >= 0 ? (double)in_rows : (double)nrows;
+        prof.work(2.0 * (double)nnz * w, 12.0 * (double)nnz + 8.0 * (nrows + 1) + 8.0 * w * (ir + nrows));
+    }
     const int J = (ncols + 63) / 64;
     const unsigned grid = std::max(1u, std::min(16u * kSMs, ceil_div((size_t)nrows * 32, 256)));
     double* partial = scr.take<double>((2 * (nnz / kPiece) + 2) * (int64_t)ld);

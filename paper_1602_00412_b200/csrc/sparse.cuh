@@ -113,8 +113,12 @@ void exclusive_scan(const int64_t* d_in, int64_t* d_out, int64_t n, Scratch& scr
 void rebase_row_ptr(const int64_t* d_src, int64_t base, int m, int* d_dst, cudaStream_t st);
 void build_transpose(DevCsr& a, Scratch& scr, cudaStream_t st);
 // out (nrows x ncols, ldo) = sparse(ptr, idx, val) * in (ld), ncols even.
+// in_rows / alg_cols (profiling only): rows of the input panel and the unpadded panel width,
+// for the launch's declared algorithmic bytes 12 nnz + 8 (nrows + 1) + 8 alg_cols (in_rows + nrows)
+// (SURVEY 8(d)); -1 = nrows / ncols.
 void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, const SegPlan& plan, int64_t nnz,
-          const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st);
+          const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st,
+          int64_t in_rows = -1, int alg_cols = -1);
 // First invalid row (or -1) of a device-resident CSR batch; kind_out gets ERR_BAD_* bits.
 int64_t validate_rows_device(const int64_t* d_row_ptr, int64_t nrows, const uint32_t* d_cols, const double* d_vals,
                              uint32_t d, int* kind_out, Scratch& scr, cudaStream_t st);

@@ -16,6 +16,8 @@
 // B'^T is therefore streamed once per step (it is the bulk: d x ell FP64), not twice.
 // x = y / |y| is never materialised: it is y scaled by 1/|y| on the fly (the reference
 // divides; the two differ by at most one ulp per entry).
+#include <map>
+#include <mutex>
 #include <algorithm>
 #include <cstdlib>
 
@@ -163,9 +165,63 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
     };
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int L = a.ell;
-    const int64_t rper = (a.m + nb - 1) / nb, cper = (a.d + nb - 1) / nb;
-    const int64_t r0 = blockIdx.x * rper, r1 = min((int64_t)a.m, r0 + rper);
-    const int64_t c0 = blockIdx.x * cper, c1 = min((int64_t)a.d, c0 + cper);
+    // Cost-balanced contiguous ranges (every step waits for the slowest block at each grid
+    // barrier): rows by 4 nnz + 4 per row, columns by the per-flush cost prefix a.ccost
+    // (long columns count their pieces, not their entries: B0 sums those over the grid).
+    __shared__ int64_t s_rng[6];
+    if (threadIdx.x == 0) {
+        const int64_t tr = 4 * (int64_t)a.row_ptr[a.m] + 4 * a.m;
+        auto rfind = [&](int64_t target) {
+            int64_t lo = 0, hi = a.m;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (4 * (int64_t)a.row_ptr[mid] + 4 * mid < target) lo = mid + 1;
+                else hi = mid;
+            }
+            return lo;
+        };
+        s_rng[0] = rfind(tr * blockIdx.x / nb);
+        s_rng[1] = blockIdx.x + 1 == nb ? a.m : rfind(tr * (blockIdx.x + 1) / nb);
+        if (a.ccost) {
+            const int64_t tc = a.ccost[a.d];
+            auto cfind = [&](int64_t target) {
+                int64_t lo = 0, hi = a.d;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (a.ccost[mid] < target) lo = mid + 1;
+                    else hi = mid;
+                }
+                return lo;
+            };
+            s_rng[2] = cfind(tc * blockIdx.x / nb);
+            s_rng[3] = blockIdx.x + 1 == nb ? a.d : cfind(tc * (blockIdx.x + 1) / nb);
+        } else {
+            const int64_t cper = (a.d + nb - 1) / nb;
+            s_rng[2] = min((int64_t)a.d, (int64_t)blockIdx.x * cper);
+            s_rng[3] = min((int64_t)a.d, s_rng[2] + cper);
+        }
+        // this block's long columns: a contiguous range of the ascending long-column list
+        int64_t lo = 0, hi = 0;
+        if (a.has_long) {
+            const int nl = a.counts[0];
+            auto lfind = [&](int64_t c) {
+                int l = 0, h = nl;
+                while (l < h) {
+                    const int mid = (l + h) >> 1;
+                    if (a.long_cols[mid] < c) l = mid + 1;
+                    else h = mid;
+                }
+                return (int64_t)l;
+            };
+            lo = lfind(s_rng[2]);
+            hi = lfind(s_rng[3]);
+        }
+        s_rng[4] = lo;
+        s_rng[5] = hi;
+    }
+    __syncthreads();
+    const int64_t r0 = s_rng[0], r1 = s_rng[1], c0 = s_rng[2], c1 = s_rng[3];
+    const int64_t lc0 = s_rng[4], lc1 = s_rng[5];
     // The block's slices of A' (CSR rows r0..r1, CSC columns c0..c1) do not change across
     // the power-method steps: stage them in shared memory when they fit, so each step pays
     // one dependent round trip (the x / u gather) instead of three.
@@ -268,11 +324,14 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
                 len = max(len, k1[q] - k0[q]);
             }
             double sp[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int off = lane; off < len; off += 32) {
+            for (int off = lane; off < len; off += 64) {  // two gathers per row and lane in flight
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int k = k0[q] + off;
-                    if (k < k1[q]) sp[q] = fma(RV[k], __ldcg(xsrc + CI[k]) * xscale, sp[q]);
+                    double v0 = 0.0, v1 = 0.0;
+                    if (k < k1[q]) v0 = RV[k] * __ldcg(xsrc + CI[k]);
+                    if (k + 32 < k1[q]) v1 = RV[k + 32] * __ldcg(xsrc + CI[k + 32]);
+                    sp[q] = fma(v0 + v1, xscale, sp[q]);
                 }
             }
             const double tot = warp_sum4(sp);
@@ -306,6 +365,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
         bool bad = false;
         for (int64_t cb = c0 + wib; cb < c1; cb += 4 * kVWarps) {
             int k0[4], k1[4];
+            bool own[4];
             int len = 0;
             double lsum[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -313,18 +373,10 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
                 const int64_t c = cb + q * kVWarps;
                 k0[q] = c < c1 ? CP[c - c0] - csub : 0;
                 k1[q] = c < c1 ? CP[c - c0 + 1] - csub : 0;
-                if (a.has_long && k1[q] - k0[q] > 2 * kPiece) {  // its pieces were summed in B0
-                    int lo = 0, hi = a.counts[0];
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (a.long_cols[mid] < c) lo = mid + 1;
-                        else hi = mid;
-                    }
-                    const int first = a.long_first[lo];
-                    const int npc = (k1[q] - k0[q] + kPiece - 1) / kPiece;
-                    if (lane == 0)
-                        for (int p = 0; p < npc; ++p) lsum[q] += __ldcg(a.lpart + first + p);
+                own[q] = c < c1;
+                if (a.has_long && k1[q] - k0[q] > 2 * kPiece) {  // long: the loop below
                     k1[q] = k0[q];
+                    own[q] = false;
                 }
                 len = max(len, k1[q] - k0[q]);
             }
@@ -337,7 +389,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
 #pragma unroll
                 for (int w = 0; w < Q; ++w) {
                     const int j = lane + 32 * w;
-                    brow[q][w] = (c < c1 && j < L) ? BT[(c - bt0) * ldbt + j] : 0.0;
+                    brow[q][w] = (own[q] && j < L) ? BT[(c - bt0) * ldbt + j] : 0.0;
                     dp[q] = fma(-brow[q][w], tl[w], dp[q]);  // - (B'^T t)_c partial
                 }
             }
@@ -353,13 +405,36 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
             for (int q = 0; q < 4; ++q) {
                 const int64_t c = cb + q * kVWarps;
                 const double yc = a.scale * __shfl_sync(0xffffffffu, tot, 8 * q);  // shrink.cpp:124
-                if (c < c1) {
+                if (own[q]) {
                     if (!isfinite(yc)) bad = true;
                     if (lane == 0) y[c] = yc;
                     nsq = fma(yc, yc, nsq);
 #pragma unroll
                     for (int w = 0; w < Q; ++w) tn[w] = fma(brow[q][w], yc, tn[w]);
                 }
+            }
+        }
+        // long columns of this block: warp per column, its B0 piece partials summed by lanes
+        if (a.has_long) {
+            const int nl = a.counts[0], npc = a.counts[1];
+            for (int64_t li = lc0 + wib; li < lc1; li += kVWarps) {
+                const int64_t c = a.long_cols[li];
+                const int first = a.long_first[li], last = li + 1 < nl ? a.long_first[li + 1] : npc;
+                double dpv = 0.0;
+                for (int p = first + lane; p < last; p += 32) dpv += __ldcg(a.lpart + p);
+                double brow[Q];
+#pragma unroll
+                for (int w = 0; w < Q; ++w) {
+                    const int j = lane + 32 * w;
+                    brow[w] = j < L ? BT[(c - bt0) * ldbt + j] : 0.0;
+                    dpv = fma(-brow[w], tl[w], dpv);
+                }
+                const double yc = a.scale * warp_sum(dpv);
+                if (!isfinite(yc)) bad = true;
+                if (lane == 0) y[c] = yc;
+                nsq = fma(yc, yc, nsq);
+#pragma unroll
+                for (int w = 0; w < Q; ++w) tn[w] = fma(brow[w], yc, tn[w]);
             }
         }
         if (bad) atomicOr(a.err, ERR_NONFINITE_VERIFY);
@@ -653,15 +728,31 @@ VerifyFn verify_fn_t(int ell) {
     }
 }
 
+// Per-column cost for the cost-balanced column ranges: a CSC entry is a stream read plus a
+// dependent gather (4), a long column (> 2 kPiece entries, summed over the grid in B0) costs
+// its pieces, and every column streams its B'^T row (ell / 8).
+__global__ void vcost_kernel(const int* __restrict__ col_ptr, int64_t d, int ell, int64_t* __restrict__ cost) {
+    pdl_entry();
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < d; c += (int64_t)gridDim.x * blockDim.x) {
+        const int len = col_ptr[c + 1] - col_ptr[c];
+        const int eff = len > 2 * kPiece ? (len + kPiece - 1) / kPiece : len;
+        cost[c] = 4 * (int64_t)eff + ell / 8 + 4;
+    }
+}
+
 }  // namespace
 
+void verify_column_costs(const int* d_col_ptr, int64_t d, int ell, int64_t* d_prefix, Scratch& scr, cudaStream_t st) {
+    int64_t* cost = scr.take<int64_t>(d + 1);
+    LAUNCH(vcost_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)d, 256))), 256, 0, st, d_col_ptr, d, ell,
+           cost);
+    CK(cudaMemsetAsync(cost + d, 0, sizeof(int64_t), st));
+    exclusive_scan(cost, d_prefix, d + 1, scr, st);
+}
+
 int verify_grid_blocks(int device, int64_t d, int lp) {
-    static int cached_sms[64] = {0};
-    int sms = device >= 0 && device < 64 ? cached_sms[device] : 0;
-    if (!sms) {
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        if (device >= 0 && device < 64) cached_sms[device] = sms;
-    }
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     // Each step streams B'^T (8 d lp bytes) once over the grid. Small B' (c2: 8 MB): the power
     // method is latency bound (two grid barriers per step), so 32 blocks -- with several
     // flushes in flight the other SMs keep running SpMM / orthonormalisation (measured on c2:
@@ -675,15 +766,19 @@ int verify_grid_blocks(int device, int64_t d, int lp) {
 
 namespace {
 int stage_bytes_for(int device) {
-    static int cached = -1;
-    if (cached < 0) {
-        cudaFuncAttributes attr;
-        CK(cudaFuncGetAttributes(&attr, (const void*)verify_kernel<8, false>));
-        int optin = 0;
-        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-        cached = optin - (int)attr.sharedSizeBytes - 1024;
-    }
-    return cached;
+    // the kernel's static shared memory and the device opt-in limit; one value per device
+    static std::mutex mu;
+    static std::map<int, int> cached;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cached.find(device);
+    if (it != cached.end()) return it->second;
+    cudaFuncAttributes attr;
+    CK(cudaFuncGetAttributes(&attr, (const void*)verify_kernel<8, false>));
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    const int v = optin - (int)attr.sharedSizeBytes - 1024;
+    cached[device] = v;
+    return v;
 }
 }  // namespace
 
@@ -726,21 +821,23 @@ int verify_cluster_size(int64_t d, int lp) {
 
 void verify_launch(const VerifyArgs& args_in, int nblocks, int cluster, cudaStream_t st) {
     ProfScope prof("verify", st);
-    static int stage = -1;
-    if (stage < 0) {
+    if (first_on_device((const void*)verify_kernel<8, false>)) {
         for (int ell = 32; ell <= 256; ell += 32) {
             allow_max_dynamic_smem(verify_fn_t<false>(ell));
             allow_max_dynamic_smem(verify_fn_t<true>(ell));
             CK(cudaFuncSetAttribute((const void*)verify_fn_t<true>(ell), cudaFuncAttributeNonPortableClusterSizeAllowed,
                                     1));
         }
-        cudaFuncAttributes attr;
-        CK(cudaFuncGetAttributes(&attr, (const void*)verify_kernel<8, false>));
-        int dev = 0, optin = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        stage = optin - (int)attr.sharedSizeBytes - 1024;
-        if (const char* e = std::getenv("SFDG_VERIFY_STAGE")) stage = std::atoi(e) ? stage : 0;
+    }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    int stage = stage_bytes_for(dev);
+    if (const char* e = std::getenv("SFDG_VERIFY_STAGE")) stage = std::atoi(e) ? stage : 0;
+    if (cluster == 0 && !args_in.resident && args_in.nnz > 0) {
+        // no block's CSR / CSC slices will fit: launch without the dynamic shared memory, so
+        // the L1 keeps its full size for the x / u gathers
+        const double per_block = 1.25 * 24.0 * (double)args_in.nnz / nblocks + 4.0 * (double)(args_in.m + args_in.d + 2) / nblocks;
+        if (per_block > (double)stage) stage = 0;
     }
     VerifyArgs args = args_in;
     args.stage_bytes = stage;
@@ -768,8 +865,8 @@ void verify_launch(const VerifyArgs& args_in, int nblocks, int cluster, cudaStre
 }
 
 int verify_graph_blocks(int device, int64_t d) {
-    static int sms = 0;
-    if (!sms) CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     return (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms, (d + 63) / 64));
 }
 

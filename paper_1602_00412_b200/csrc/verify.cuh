@@ -16,6 +16,7 @@ struct VerifyArgs {
     const int* row_idx;
     const double* cval;
     int64_t m, d;
+    int64_t nnz;
     // B'^T: d x ell, row stride ldb (the right half of the [B | B']^T stack)
     const double* bt;
     int64_t ldb;
@@ -43,7 +44,12 @@ struct VerifyArgs {
     const int* piece_end;
     const int* counts;      // [n_long, n_pieces] (device)
     double* lpart;          // n_pieces partial sums
+    const int64_t* ccost;   // d + 1 column-cost prefix (verify_column_costs) or null: equal counts
 };
+
+class Scratch;
+// Exclusive prefix of the per-column costs that balance the persistent verifier's column ranges.
+void verify_column_costs(const int* d_col_ptr, int64_t d, int ell, int64_t* d_prefix, Scratch& scr, cudaStream_t st);
 
 int verify_grid_blocks(int device, int64_t d, int lp);  // cooperative grid for this B' size
 // Smallest grid (>= the streaming grid, <= one block per SM) whose blocks can hold their

@@ -178,6 +178,42 @@ def generate(name: str | StreamConfig, rows: tuple[int, int] | None = None):
     return _heavy(cfg, r0, r1)
 
 
+def _gen_job(args):
+    cfg, r0, r1 = args
+    return generate(cfg, (r0, r1))
+
+
+def generate_parallel(name: str | StreamConfig, rows: tuple[int, int] | None = None, procs: int | None = None):
+    """generate() over chunk-aligned row ranges in parallel processes; identical output
+    (every CHUNK-row chunk draws from its own seeded generator)."""
+    import os
+    import multiprocessing as mp
+
+    cfg = name if isinstance(name, StreamConfig) else CONFIGS[name]
+    r0, r1 = rows if rows is not None else (0, cfg.n)
+    r1 = min(r1, cfg.n)
+    procs = procs or min(32, os.cpu_count() or 1)
+    nchunks = (r1 - r0 + CHUNK - 1) // CHUNK
+    if procs <= 1 or nchunks < 4:
+        return generate(cfg, (r0, r1))
+    per = max(1, (nchunks + 4 * procs - 1) // (4 * procs)) * CHUNK
+    cuts = [r0] + list(range((r0 // CHUNK + 1) * CHUNK, r1, CHUNK))  # chunk boundaries inside (r0, r1)
+    bounds = [r0]
+    for c in cuts[1:]:
+        if c - bounds[-1] >= per:
+            bounds.append(c)
+    bounds.append(r1)
+    jobs = [(cfg, a, b) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+    with mp.get_context("spawn").Pool(min(procs, len(jobs))) as pool:  # the caller may hold CUDA / threads
+        parts = pool.map(_gen_job, jobs)
+    rps, base = [np.zeros(1, np.int64)], 0
+    for rp, _, _ in parts:
+        rps.append(rp[1:] + base)
+        base += int(rp[-1])
+    return (np.concatenate(rps), np.concatenate([p[1] for p in parts]).astype(np.uint32),
+            np.concatenate([p[2] for p in parts]))
+
+
 def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous row shard of rank `rank`."""
     per = (n + world - 1) // world
