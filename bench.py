@@ -185,13 +185,13 @@ def sweep_rate(name: str, res) -> tuple[float, float]:
 
 def sample_rows(name: str, budget_s: int | float, procs: int, pool=None) -> tuple[int, float]:
     """Rows per sweep sample so that one sample takes about budget_s: a 1/16-flush calibration
-    sweep, scaled linearly (MGS and the SpMV pair are linear in the rows) with a 1.5x margin
+    sweep, scaled linearly (MGS and the SpMV pair are linear in the rows) with a 2x margin
     for the cache effects that make small samples faster per row."""
     from paper_1602_00412_b200 import synthetic as S
     m = S.CONFIGS[name].d
     cal = max(64, m // 16)
     _, res = reference_sweeps(name, procs, 10_000, cal, pool)
-    t_full = 1.5 * max(r[0] for r in res) * m / cal
+    t_full = 2.0 * max(r[0] for r in res) * m / cal
     return (m if t_full <= budget_s else max(cal, int(m * budget_s / t_full))), t_full
 
 

@@ -212,6 +212,20 @@ int sfdg_simultaneous_iteration(const int64_t* row_ptr, const uint32_t* cols, co
 /* power_iteration_count (randsvd.cpp:10-16). */
 int sfdg_power_iteration_count(size_t m, const sfdg_power_config* power, size_t* q);
 
+/* A symmetric operator y = C x on R^d supplied by the caller (la_core.hpp:45 SymOp). It
+ * returns 0 on success; a nonzero return aborts the verification with SFDG_INVALID_ARGUMENT.
+ * x and y are d doubles: host memory, or memory of `device` when op_on_device != 0. */
+typedef int (*sfdg_symop_fn)(const double* x, double* y, size_t d, void* user);
+/* verify_spectral(apply, d, state, rng) (shrink.hpp:35, shrink.cpp:75-102) over a caller
+ * operator: state->i += 1, delta_i = delta / (2 i^2) added to delta_spent, steps =
+ * ceil(c_verify log2(d / delta_i)); x = unit_sphere_vector(d, rng) (la_core.cpp:174-189) drawn
+ * from the device generator at *rng (advanced in place); then the log-domain power method with
+ * the reference's exits (annihilation -> accept, |.| >= 1 while the log magnitude is positive
+ * -> reject, non-finite output -> SFDG_NUMERICAL_ERROR). *accepted = 1 / 0. With
+ * op_on_device the iterate never leaves the GPU (norms and rescaling on the device). */
+int sfdg_verify_spectral(sfdg_symop_fn op, void* user, int op_on_device, size_t d, sfdg_verifier_state* state,
+                         sfdg_rng_state* rng, int* accepted, int device);
+
 /* ---- device kernels exposed for parity tests (la_core.hpp:23-41) --------------- */
 
 /* gaussian_matrix(rows, cols, rng) (la_core.cpp:167-172) generated on the device. */

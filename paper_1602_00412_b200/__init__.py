@@ -25,7 +25,8 @@ import numpy as np
 
 __all__ = [
     "SketchConfig", "PowerConfig", "VerifierState", "RngState", "SfdSketcher", "merge", "merge_device",
-    "dense_shrink", "sparse_shrink", "boosted_sparse_shrink", "simultaneous_iteration", "power_iteration_count",
+    "dense_shrink", "sparse_shrink", "boosted_sparse_shrink", "verify_spectral", "simultaneous_iteration",
+    "power_iteration_count",
     "gaussian_matrix", "eigh", "orthonormalize", "csr_products", "device_count", "launch_count", "lib",
     "InvalidArgument", "NumericalError", "CudaError", "KALPHA", "LIB_PATH",
 ]
@@ -604,6 +605,48 @@ def boosted_sparse_shrink(csr, d: int, ell: int, state: VerifierState, rng, powe
     st = RngState(st.seed)
     st._update(c)
     return out, dh.value, att.value, st
+
+
+_SYMOP = C.CFUNCTYPE(C.c_int, _dp, _dp, C.c_size_t, C.c_void_p)
+
+
+def verify_spectral(op, d: int, state: VerifierState, rng, device: int = 0, on_device: bool = False) -> tuple:
+    """verify_spectral(apply, d, state, rng) (shrink.hpp:35, shrink.cpp:75-102) over a caller
+    operator. op(x) -> y: numpy arrays (on_device=False), or op(x_ptr, y_ptr, d) on raw device
+    pointers of `device` (on_device=True). Returns (accepted, RngState after); state updated."""
+    err = []
+
+    def _cb(xp, yp, n, _ctx):
+        try:
+            if on_device:
+                op(C.cast(xp, C.c_void_p).value, C.cast(yp, C.c_void_p).value, n)
+            else:
+                x = np.ctypeslib.as_array(xp, shape=(n,)).copy()
+                y = np.asarray(op(x), dtype=np.float64)
+                if y.shape != (n,):
+                    raise ValueError("verify_spectral: operator output has the wrong shape")
+                np.ctypeslib.as_array(yp, shape=(n,))[:] = y
+            return 0
+        except Exception as e:  # reported after the call
+            err.append(e)
+            return 1
+
+    cb = _SYMOP(_cb)
+    st = _rng_arg(rng)
+    c = st._c()
+    v = state._c()
+    acc = C.c_int()
+    L = lib()
+    L.sfdg_verify_spectral.argtypes = [_SYMOP, C.c_void_p, C.c_int, C.c_size_t, C.POINTER(_Verifier),
+                                       C.POINTER(_Rng), C.POINTER(C.c_int), C.c_int]
+    code = L.sfdg_verify_spectral(cb, None, 1 if on_device else 0, d, C.byref(v), C.byref(c), C.byref(acc), device)
+    if err:
+        raise err[0]
+    _check(code)
+    state._update(v)
+    st = RngState(st.seed)
+    st._update(c)
+    return bool(acc.value), st
 
 
 def simultaneous_iteration(csr, d: int, k: int, rng, power: PowerConfig | None = None, device: int = 0):

@@ -1602,6 +1602,120 @@ int sfdg_power_iteration_count(size_t m, const sfdg_power_config* power, size_t*
     return guard([&] { *q = power_iteration_count(m, to_power(power)); });
 }
 
+int sfdg_verify_spectral(sfdg_symop_fn op, void* user, int op_on_device, size_t d, sfdg_verifier_state* state,
+                         sfdg_rng_state* rng, int* accepted, int device) {
+    return guard([&] {
+        if (!op || !state || !rng || !accepted) throw invalid_argument("verify_spectral: null argument");
+        if (d < 1) throw invalid_argument("unit_sphere_vector: d must be positive");  // la_core.cpp:175
+        require_device(device);
+        CK(cudaSetDevice(device));
+        // shrink.cpp:76-82 (host arithmetic identical to the reference)
+        state->i += 1;
+        const double di = static_cast<double>(state->i);
+        const double delta_i = state->delta / (2.0 * di * di);
+        state->delta_spent += delta_i;
+        const size_t steps =
+            static_cast<size_t>(std::ceil(state->c_verify * std::log2(static_cast<double>(d) / delta_i)));
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        struct Res {
+            cudaStream_t st;
+            std::vector<void*> mem;
+            ~Res() {
+                cudaStreamSynchronize(st);
+                for (void* p : mem) cudaFree(p);
+                cudaStreamDestroy(st);
+            }
+        } res{st, {}};
+        auto dalloc = [&](size_t n) {
+            void* p = nullptr;
+            CK(cudaMalloc(&p, n * sizeof(double)));
+            res.mem.push_back(p);
+            return static_cast<double*>(p);
+        };
+        double* dx = dalloc(d);
+        double* dy = dalloc(d);
+        double* dscal = dalloc(2);
+        int* derr = reinterpret_cast<int*>(dalloc(1));
+        CK(cudaMemsetAsync(derr, 0, sizeof(int), st));
+        RngStream rs;
+        RngPos pos{rng->words, rng->has_spare != 0};
+        rs.init(rng->seed, 4 * d + 64, device);
+        if (pos.has_spare) rs.set_spare(pos, rng->spare, st);
+        Scratch scr;
+        std::vector<double> x(d), y(d);
+        // x = unit_sphere_vector(d, rng): d normals in draw order, redrawn while all zero
+        for (;;) {
+            rs.normals(pos, d, 1, 1, dx, derr, st);
+            double nrm_sq = 0.0;
+            if (op_on_device) {
+                sumsq(dx, (int64_t)d, 1, 1, dscal, nullptr, 0, scr, st);
+                CK(cudaMemcpyAsync(&nrm_sq, dscal, sizeof(double), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (nrm_sq > 0.0) {
+                    scale_vector(dx, (int64_t)d, 1.0 / std::sqrt(nrm_sq), st);
+                    break;
+                }
+            } else {
+                CK(cudaMemcpyAsync(x.data(), dx, d * sizeof(double), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                for (size_t i = 0; i < d; ++i) nrm_sq += x[i] * x[i];
+                if (nrm_sq > 0.0) {
+                    const double inv = 1.0 / std::sqrt(nrm_sq);
+                    for (double& v : x) v *= inv;
+                    break;
+                }
+            }
+        }
+        int herr = 0;
+        CK(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        rng->words = pos.words;
+        rng->has_spare = pos.has_spare ? 1 : 0;
+        rng->spare = pos.has_spare ? rs.spare_value(pos, st) : 0.0;
+        if (herr) throw numerical_error("rng: Box-Muller u1 == 0 redraw (probability 2^-53) is not reproduced on device");
+        // shrink.cpp:85-101
+        double log_mag = 0.0;
+        for (size_t t = 0; t < steps; ++t) {
+            double nrm_sq = 0.0;
+            if (op_on_device) {
+                CK(cudaStreamSynchronize(st));
+                if (op(dx, dy, d, user) != 0) throw invalid_argument("verify_spectral: operator callback failed");
+                CK(cudaDeviceSynchronize());  // the operator's own work, on any stream
+                sumsq(dy, (int64_t)d, 1, 1, dscal, derr, ERR_NONFINITE_VERIFY, scr, st);
+                CK(cudaMemcpyAsync(&nrm_sq, dscal, sizeof(double), cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                scr.reset();
+                if (herr) throw numerical_error("verify_spectral: non-finite operator output");
+            } else {
+                if (op(x.data(), y.data(), d, user) != 0) throw invalid_argument("verify_spectral: operator callback failed");
+                for (double v : y) {
+                    if (!std::isfinite(v)) throw numerical_error("verify_spectral: non-finite operator output");
+                    nrm_sq += v * v;
+                }
+            }
+            if (nrm_sq == 0.0) {  // iterate annihilated, norm estimate 0
+                *accepted = 1;
+                return;
+            }
+            const double nrm = std::sqrt(nrm_sq);
+            log_mag += std::log(nrm);
+            if (log_mag > 0.0 && nrm >= 1.0) {
+                *accepted = 0;
+                return;
+            }
+            if (op_on_device) {
+                copy2d(dy, (int)d, 1, 1, dx, 1, st);
+                scale_vector(dx, (int64_t)d, 1.0 / nrm, st);
+            } else {
+                for (size_t i = 0; i < d; ++i) x[i] = y[i] / nrm;
+            }
+        }
+        *accepted = log_mag <= 0.0 ? 1 : 0;
+    });
+}
+
 int sfdg_gaussian_matrix(sfdg_rng_state* rng, size_t rows, size_t cols, double* out, int device) {
     return guard([&] {
         if (rows < 1 || cols < 1) throw invalid_argument("gaussian_matrix: empty shape");

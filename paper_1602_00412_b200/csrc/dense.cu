@@ -354,6 +354,19 @@ void sumsq(const double* X, int64_t rows, int cols, int ld, double* d_out, int* 
     LAUNCH(sum_partials_kernel, 1, 32, 0, st, partial, kRedBlocks, d_out);
 }
 
+namespace {
+__global__ void scale_vector_kernel(double* __restrict__ x, int64_t n, double s) {
+    pdl_entry();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] *= s;
+}
+}  // namespace
+
+void scale_vector(double* x, int64_t n, double s, cudaStream_t st) {
+    if (n <= 0) return;
+    LAUNCH(scale_vector_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)n, 256))), 256, 0, st, x, n, s);
+}
+
 void transpose(const double* in, int rows, int cols, int ldi, double* out, int ldo, cudaStream_t st) {
     if (rows <= 0 || cols <= 0) return;
     LAUNCH(transpose_kernel, dim3(ceil_div(cols, 32), ceil_div(rows, 32)), dim3(32, 8), 0, st, in, rows, cols, ldi, out,

@@ -19,6 +19,8 @@ void gemm_nn(const double* X, int n, int k, int ldx, const double* S, int c, int
 void sumsq(const double* X, int64_t rows, int cols, int ld, double* d_out, int* d_err, int err_bit, Scratch& scr,
            cudaStream_t st);
 void transpose(const double* in, int rows, int cols, int ldi, double* out, int ldo, cudaStream_t st);
+// x[i] *= s for i < n.
+void scale_vector(double* x, int64_t n, double s, cudaStream_t st);
 void copy2d(const double* in, int rows, int cols, int ldi, double* out, int ldo, cudaStream_t st);
 void fill2d(double* out, int rows, int cols, int ldo, double v, cudaStream_t st);
 

@@ -230,6 +230,12 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     CK(cudaHostAlloc(&h_scal, 64 * sizeof(double), cudaHostAllocDefault));
     CK(cudaHostAlloc(&h_err, 4 * sizeof(int), cudaHostAllocDefault));
     CK(cudaHostAlloc(&h_counts, 4 * sizeof(int), cudaHostAllocDefault));
+    if (const char* e = std::getenv("SFDG_HOT")) hot_enabled = std::atoi(e) != 0;
+    if (hot_enabled) {
+        CK(cudaHostAlloc(&h_colptr, ((size_t)d + 1) * sizeof(int), cudaHostAllocDefault));
+        CK(cudaMalloc(&d_hot_cols, (size_t)std::max(1, hot_rows_capacity(lp)) * sizeof(int)));
+        CK(cudaMalloc(&d_slot, (size_t)d * sizeof(int)));
+    }
     CK(cudaStreamSynchronize(st));
 }
 
@@ -250,6 +256,9 @@ Engine::~Engine() {
     if (h_scal) cudaFreeHost(h_scal);
     if (h_err) cudaFreeHost(h_err);
     if (h_counts) cudaFreeHost(h_counts);
+    if (h_colptr) cudaFreeHost(h_colptr);
+    for (void* p : {(void*)d_hot_cols, (void*)d_slot, (void*)d_idx2})
+        if (p) cudaFree(p);
     a.release();
     plan_r.release();
     plan_c.release();
@@ -327,11 +336,49 @@ void Engine::prepare_async() {
     // one small read-back per flush lets every SpMM skip the long-row kernels when unused
     CK(cudaMemcpyAsync(h_counts, plan_r.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_counts + 2, plan_c.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (hot_enabled && a.nnz > 0)
+        CK(cudaMemcpyAsync(h_colptr, a.col_ptr, ((size_t)d + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+}
+
+// The flush's most frequent columns (ties: lower column id first) up to the shared memory the
+// CSR SpMM stages per CTA. Worth it only when they hold a real share of the entries (Zipf /
+// power-law columns: c3-c5 top 100-200 columns carry 30-40 %); uniform columns (c1, c2) skip it.
+void Engine::choose_hot() {
+    hot = HotSet{};
+    hot_share = 0.0;
+    if (!hot_enabled || a.nnz == 0) return;
+    const int cap = std::min(hot_rows_capacity(lp), d);
+    if (cap < 16) return;
+    std::vector<int> ids(d);
+    for (int c = 0; c < d; ++c) ids[c] = c;
+    auto cnt = [&](int c) { return h_colptr[c + 1] - h_colptr[c]; };
+    auto better = [&](int x, int y) { return cnt(x) != cnt(y) ? cnt(x) > cnt(y) : x < y; };
+    std::nth_element(ids.begin(), ids.begin() + (cap - 1), ids.end(), better);
+    std::sort(ids.begin(), ids.begin() + cap, better);
+    int64_t in_hot = 0;
+    for (int i = 0; i < cap; ++i) in_hot += cnt(ids[i]);
+    hot_share = (double)in_hot / (double)a.nnz;
+    if (hot_share < 0.1) return;
+    if (a.nnz > idx2_cap) {
+        if (d_idx2) CK(cudaFree(d_idx2));
+        idx2_cap = std::max<int64_t>(a.nnz, idx2_cap * 3 / 2);
+        CK(cudaMalloc(&d_idx2, idx2_cap * sizeof(int)));
+    }
+    CK(cudaMemcpyAsync(d_hot_cols, ids.data(), (size_t)cap * sizeof(int), cudaMemcpyHostToDevice, st));
+    hot_relabel(d_hot_cols, cap, a.col, a.nnz, d, d_slot, d_idx2, st);
+    CK(cudaStreamSynchronize(st));  // ids (host) goes out of scope
+    hot = HotSet{d_hot_cols, d_idx2, cap};
 }
 
 void Engine::prepare_finish() {
     plan_r.host_long = h_counts[0];
+    plan_r.host_pieces = h_counts[1];
     plan_c.host_long = h_counts[2];
+    plan_c.host_pieces = h_counts[3];
+    // the piece partials at their final addresses before any sweep block is captured
+    if (plan_r.host_long > 0) plan_r.ensure_partial(plan_r.host_pieces * lp);
+    if (plan_c.host_long > 0) plan_c.ensure_partial(plan_c.host_pieces * lp);
+    choose_hot();
 }
 
 void Engine::prepare() {
@@ -371,21 +418,31 @@ void Engine::orthonormalize_light(int m, int err_bit) {
 }
 
 void Engine::sweep_block(int interval, int m) {
-    const std::array<uintptr_t, 12> key{(uintptr_t)interval,   (uintptr_t)m,          (uintptr_t)Y,
-                                        (uintptr_t)Yt,         (uintptr_t)W,          (uintptr_t)a.row_ptr,
-                                        (uintptr_t)a.col,      (uintptr_t)a.val,      (uintptr_t)a.col_ptr,
-                                        (uintptr_t)a.row_idx,  (uintptr_t)a.cval,     (uintptr_t)d};
+    // every buffer the captured kernels touch, and the launch parameters baked into them
+    std::vector<uintptr_t> key{(uintptr_t)interval,  (uintptr_t)m,      (uintptr_t)Y,         (uintptr_t)Yt,
+                               (uintptr_t)W,         (uintptr_t)a.row_ptr, (uintptr_t)a.col,  (uintptr_t)a.val,
+                               (uintptr_t)a.col_ptr, (uintptr_t)a.row_idx, (uintptr_t)a.cval, (uintptr_t)d};
+    for (const SegPlan* pl : {&plan_r, &plan_c})
+        for (const void* p : {(const void*)pl->partial, (const void*)pl->arrive, (const void*)pl->piece_beg,
+                              (const void*)pl->piece_end, (const void*)pl->piece_li, (const void*)pl->long_rows,
+                              (const void*)pl->long_first, (const void*)pl->counts,
+                              (const void*)(uintptr_t)(pl->host_long != 0)})
+            key.push_back((uintptr_t)p);
+    key.push_back((uintptr_t)hot.n);
+    key.push_back((uintptr_t)hot.idx);
+    key.push_back((uintptr_t)hot.cols);
     auto body = [&] {
         for (int i = 0; i < interval; ++i) {
             spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st, m, ell);
-            spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell);
+            spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell, &hot);
         }
         orthonormalize_light(m, ERR_NONFINITE_ITER);  // swaps Y and Yt (host side)
     };
     auto it = graphs.find(key);
     if (it == graphs.end()) {
-        // capture once: the kernels read only fixed buffers and device scalars (no long rows,
-        // checked by the caller), so the same graph serves every later flush of this lane
+        // capture once: the kernels read only fixed buffers and device scalars (the long-row
+        // plans and their piece partials are per-lane buffers at fixed addresses), so the same
+        // graph serves every later flush of this lane
         const uint64_t l0 = g_launches.load();
         cudaGraph_t graph = nullptr;
         scr.headroom((size_t)256 << 20);  // the capture must not allocate
@@ -418,7 +475,7 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     const size_t q = power_iteration_count((size_t)m, cfg);
     // G = gaussian_matrix(d, k) in W (la_core.cpp:167-172), pad columns zero
     rng->normals(pos, (uint64_t)d * k, (uint64_t)k, (uint64_t)lp, W, d_err, st);
-    spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell);
+    spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell, &hot);
     if (adaptive && q > 0) orthonormalize_light(m, ERR_NONFINITE_ITER);
     else orthonormalize(Y, m, ERR_NONFINITE_ITER);
     // Only span(Y) matters for B' (it enters through Z Z^T), so CholeskyQR2 runs every
@@ -428,8 +485,7 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     const int interval = adaptive ? orth_interval : 1;
     // whole blocks (interval sweeps closed by a light pass) replay as a CUDA graph when no
     // long-row piece kernels are involved and profiling (per-launch events) is off
-    const bool graphs_ok = use_graphs && adaptive && !exact_check && plan_r.host_long == 0 && plan_c.host_long == 0 &&
-                           !g_prof_on.load(std::memory_order_relaxed);
+    const bool graphs_ok = use_graphs && adaptive && !exact_check && !g_prof_on.load(std::memory_order_relaxed);
     int since = 0;
     for (size_t s = 0; s < q;) {
         if (graphs_ok && since == 0 && s + (size_t)interval < q) {
@@ -439,7 +495,7 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
             continue;
         }
         spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st, m, ell);
-        spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell);
+        spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell, &hot);
         if (++since >= interval || s + 1 == q) {
             if (adaptive && s + 1 < q) orthonormalize_light(m, ERR_NONFINITE_ITER);
             else orthonormalize(Y, m, ERR_NONFINITE_ITER);
@@ -455,7 +511,7 @@ void Engine::sparse_shrink(const PowerCfg& cfg, double* bpt, int ldb) {
     if (ell > d) throw invalid_argument("sparse_shrink: ell exceeds column count");
     simultaneous_iteration(ell, cfg);
     // W = A'^T Z = P^T (d x lp): project_rows (sparse.cpp:57-69) without the transpose
-    spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st, m, ell);
+    spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st, a.m, ell);
     double* fsq = d_scal + 0;
     sumsq(W, d, lp, lp, fsq, d_err, ERR_NONFINITE_PROJ, scr, st);  // all_finite(P) (shrink.cpp:70)
     // svd_top(P, ell): PP^T = W^T W, eigen, right vectors and the shrink in one GEMM

@@ -124,6 +124,20 @@ class Engine {
     void prepare_async();
     void prepare_finish();
     int* h_counts = nullptr;  // pinned [4]
+    // Per-flush hot columns of the CSR SpMM (sparse.cuh HotSet): chosen on the host from the
+    // CSC column counts (h_colptr, copied by prepare_async) in prepare_finish. Opt-in
+    // (SFDG_HOT=1): measured slower on c3-c5 (tools/spmm_bench, profiles/r02_spmm_hot.txt) --
+    // the L1 already serves the hot rows (21 % hit rate of the plain gather), and the 200 KB of
+    // staged rows shrink it for everything else.
+    bool hot_enabled = false;
+    HotSet hot;
+    int* h_colptr = nullptr;  // pinned d + 1
+    int* d_hot_cols = nullptr;
+    int* d_slot = nullptr;    // d
+    int* d_idx2 = nullptr;    // relabelled CSR column indices
+    int64_t idx2_cap = 0;
+    double hot_share = 0.0;   // share of this flush's nonzeros in the hot columns
+    void choose_hot();
     // la_core.cpp:130-165 contract on Y (m x lp, first k columns meaningful): CholeskyQR2.
     void orthonormalize(double* Yp, int m, int err_bit);
     // Single CholeskyQR pass on Y (between sweeps of the adaptive schedule; swaps Y/Yt).
@@ -135,7 +149,7 @@ class Engine {
         cudaGraphExec_t exec = nullptr;
         uint64_t kernels = 0;
     };
-    std::map<std::array<uintptr_t, 12>, GraphEntry> graphs;
+    std::map<std::vector<uintptr_t>, GraphEntry> graphs;
     std::map<std::array<uintptr_t, 18>, GraphEntry> vgraphs;  // kernel-sequence verifier graphs
     bool use_graphs = true;  // SFDG_GRAPHS=0 disables
     // randsvd.cpp:18-51: Z (m x lp) left in Y.

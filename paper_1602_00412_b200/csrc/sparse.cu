@@ -205,7 +205,8 @@ __global__ void plan_count_kernel(const int* __restrict__ ptr, int nrows, int pi
 __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int piece, const int64_t* __restrict__ is_long,
                                  const int64_t* __restrict__ long_off, const int64_t* __restrict__ piece_off,
                                  int* __restrict__ long_rows, int* __restrict__ long_first, int* __restrict__ piece_beg,
-                                 int* __restrict__ piece_end, int* __restrict__ counts /* [nlong, npieces] */) {
+                                 int* __restrict__ piece_end, int* __restrict__ piece_li,
+                                 int* __restrict__ counts /* [nlong, npieces] */) {
     pdl_entry();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
         const int len = ptr[r + 1] - ptr[r];
@@ -218,6 +219,7 @@ __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int pie
             for (int p = 0; p < np; ++p) {
                 piece_beg[pf + p] = ptr[r] + p * piece;
                 piece_end[pf + p] = min(ptr[r] + (p + 1) * piece, ptr[r + 1]);
+                piece_li[pf + p] = li;
             }
         }
         if (r == nrows - 1) {
@@ -228,11 +230,21 @@ __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int pie
 }
 
 // ---------------------------------------------------------------- SpMM
-// J = number of 64-column chunks (lane owns columns 2*lane + 64*j, +1).
-template <int J>
+// J = number of 64-column chunks (lane owns columns 2*lane + 64*j, +1). HOT: idx is relabelled
+// (HotSet): entries < nh read the staged row in shared memory (hot + i * ldh), the others row
+// idx - nh of `in`. The same loads in the same order either way, so the sums are identical.
+template <int J, bool HOT>
 __device__ __forceinline__ void gather_range(int kb, int ke, const int* __restrict__ idx, const double* __restrict__ val,
                                              const double* __restrict__ in, int ld, int ncols, int lane,
-                                             double2 (&acc)[J]) {
+                                             double2 (&acc)[J], const double* hot, int nh, int ldh) {
+    auto row = [&](int ci) -> const double* {
+        if constexpr (HOT) return ci < nh ? hot + (size_t)ci * ldh : in + (size_t)(ci - nh) * ld;
+        else return in + (size_t)ci * ld;
+    };
+    auto load = [&](const double* p) -> double2 {
+        if constexpr (HOT) return *reinterpret_cast<const double2*>(p);  // generic: SMEM or global
+        else return __ldg(reinterpret_cast<const double2*>(p));
+    };
     for (int k0 = kb; k0 < ke; k0 += 32) {
         const int kk = k0 + lane;
         const int my_idx = kk < ke ? idx[kk] : 0;
@@ -240,11 +252,11 @@ __device__ __forceinline__ void gather_range(int kb, int ke, const int* __restri
         const int cnt = min(32, ke - k0);
         int e = 0;
         for (; e + 4 <= cnt; e += 4) {
-            int ci[4];
+            const double* rp[4];
             double cv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                ci[u] = __shfl_sync(0xffffffffu, my_idx, e + u);
+                rp[u] = row(__shfl_sync(0xffffffffu, my_idx, e + u));
                 cv[u] = __shfl_sync(0xffffffffu, my_val, e + u);
             }
             double2 x[4][J];
@@ -253,8 +265,7 @@ __device__ __forceinline__ void gather_range(int kb, int ke, const int* __restri
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
                     const int c = 2 * lane + 64 * j;
-                    x[u][j] = c < ncols ? __ldg(reinterpret_cast<const double2*>(in + (size_t)ci[u] * ld + c))
-                                        : make_double2(0.0, 0.0);
+                    x[u][j] = c < ncols ? load(rp[u] + c) : make_double2(0.0, 0.0);
                 }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -265,13 +276,13 @@ __device__ __forceinline__ void gather_range(int kb, int ke, const int* __restri
                 }
         }
         for (; e < cnt; ++e) {
-            const int ci = __shfl_sync(0xffffffffu, my_idx, e);
+            const double* r1 = row(__shfl_sync(0xffffffffu, my_idx, e));
             const double cv = __shfl_sync(0xffffffffu, my_val, e);
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int c = 2 * lane + 64 * j;
                 if (c < ncols) {
-                    const double2 x = __ldg(reinterpret_cast<const double2*>(in + (size_t)ci * ld + c));
+                    const double2 x = load(r1 + c);
                     acc[j].x = fma(cv, x.x, acc[j].x);
                     acc[j].y = fma(cv, x.y, acc[j].y);
                 }
@@ -280,23 +291,110 @@ __device__ __forceinline__ void gather_range(int kb, int ke, const int* __restri
     }
 }
 
-template <int J>
-__global__ void __launch_bounds__(256, (J <= 2 ? 5 : 1)) spmm_rows_kernel(const int* __restrict__ ptr,
-                                                                        const int* __restrict__ idx,
-                                                                        const double* __restrict__ val,
-                                 int nrows, int piece, const double* __restrict__ in, int ld, int ncols,
-                                 double* __restrict__ out, int ldo) {
-    pdl_entry();
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// The CTA's copy of the hot input rows: one 1-D TMA bulk copy (cp.async.bulk) per row into
+// shared memory, completion counted in bytes on an mbarrier.
+__device__ __forceinline__ void stage_hot_rows(double* hot, const int* __restrict__ cols, int nh, const double* in,
+                                               int ld, int ncols, uint64_t* bar) {
+    const unsigned bytes = (unsigned)ncols * 8u;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                         "r"(bytes * (unsigned)nh)
+                         : "memory");
+        __syncwarp();
+        for (int i = threadIdx.x; i < nh; i += 32)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                             smem_u32(hot + (size_t)i * ncols)),
+                         "l"(in + (size_t)cols[i] * ld), "r"(bytes), "r"(smem_u32(bar))
+                         : "memory");
+    }
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+// One launch for the whole product. Work item w < npieces is a kPiece-long piece of a long row:
+// its partial row goes to `partial`, and the piece that finishes a row last (per-row arrival
+// counter) sums that row's partials in piece order -- deterministic, no FP atomics. The other
+// items are the short rows, written directly. Pieces come first, so their dependent gather
+// chains start at the beginning of the launch instead of forming a tail.
+template <int J, bool HOT>
+constexpr int spmm_threads() {
+    return HOT ? (J <= 2 ? 1024 : 512) : 256;
+}
+template <int J, bool HOT>
+constexpr int spmm_min_blocks() {
+    return HOT ? 1 : (J <= 2 ? 5 : 2);
+}
+
+template <int J, bool HOT>
+__global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT>()) spmm_kernel(
+    const int* __restrict__ ptr, const int* __restrict__ idx, const double* __restrict__ val, int nrows,
+    const int* __restrict__ piece_beg, const int* __restrict__ piece_end, const int* __restrict__ piece_li,
+    const int* __restrict__ long_rows, const int* __restrict__ long_first, const int* __restrict__ counts,
+    int* __restrict__ arrive, int use_pieces, const double* __restrict__ in, int ld, int ncols,
+    double* __restrict__ out, int ldo, double* __restrict__ partial, const int* __restrict__ hot_cols, int nh) {
+    extern __shared__ __align__(128) double hot_sm[];
+    __shared__ uint64_t hot_bar;
+    if constexpr (HOT) {
+        pdl_entry();
+        stage_hot_rows(hot_sm, hot_cols, nh, in, ld, ncols, &hot_bar);
+    }
+    if constexpr (!HOT) pdl_entry();
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int r = warp; r < nrows; r += nw) {
-        const int kb = ptr[r], ke = ptr[r + 1];
-        if (ke - kb > 2 * piece) continue;  // handled by the piece kernels
+    const int np = use_pieces ? counts[1] : 0;
+    const int nl = use_pieces ? counts[0] : 0;
+    for (int w = warp; w < np + nrows; w += nw) {
         double2 acc[J];
 #pragma unroll
         for (int j = 0; j < J; ++j) acc[j] = make_double2(0.0, 0.0);
-        gather_range<J>(kb, ke, idx, val, in, ld, ncols, lane, acc);
+        if (w < np) {
+            gather_range<J, HOT>(piece_beg[w], piece_end[w], idx, val, in, ld, ncols, lane, acc, hot_sm, nh, ncols);
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int c = 2 * lane + 64 * j;
+                if (c < ncols) *reinterpret_cast<double2*>(partial + (size_t)w * ld + c) = acc[j];
+            }
+            __threadfence();
+            const int li = piece_li[w];
+            const int first = long_first[li], last = li + 1 < nl ? long_first[li + 1] : np;
+            int old = 0;
+            if (lane == 0) old = atomicAdd(arrive + li, 1);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old == last - first - 1) {  // every piece of this row is written: sum them in order
+                __threadfence();
+                const int r = long_rows[li];
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    const int c = 2 * lane + 64 * j;
+                    if (c < ncols) {
+                        double2 t = make_double2(0.0, 0.0);
+                        for (int p = first; p < last; ++p) {
+                            const double2 v = __ldcg(reinterpret_cast<const double2*>(partial + (size_t)p * ld + c));
+                            t.x += v.x;
+                            t.y += v.y;
+                        }
+                        *reinterpret_cast<double2*>(out + (size_t)r * ldo + c) = t;
+                    }
+                }
+                if (lane == 0) arrive[li] = 0;  // ready for the next launch
+            }
+            continue;
+        }
+        const int r = w - np;
+        const int kb = ptr[r], ke = ptr[r + 1];
+        if (use_pieces && ke - kb > 2 * kPiece) continue;  // summed by its last piece
+        gather_range<J, HOT>(kb, ke, idx, val, in, ld, ncols, lane, acc, hot_sm, nh, ncols);
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const int c = 2 * lane + 64 * j;
@@ -305,44 +403,18 @@ __global__ void __launch_bounds__(256, (J <= 2 ? 5 : 1)) spmm_rows_kernel(const 
     }
 }
 
-template <int J>
-__global__ void spmm_pieces_kernel(const int* __restrict__ piece_beg, const int* __restrict__ piece_end,
-                                   const int* __restrict__ counts, const int* __restrict__ idx,
-                                   const double* __restrict__ val, const double* __restrict__ in, int ld, int ncols,
-                                   double* __restrict__ partial /* [npieces][ld] */) {
+__global__ void hot_slot_kernel(const int* __restrict__ cols, int n, int* __restrict__ slot) {
     pdl_entry();
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    const int np = counts[1];
-    for (int p = warp; p < np; p += nw) {
-        double2 acc[J];
-#pragma unroll
-        for (int j = 0; j < J; ++j) acc[j] = make_double2(0.0, 0.0);
-        gather_range<J>(piece_beg[p], piece_end[p], idx, val, in, ld, ncols, lane, acc);
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const int c = 2 * lane + 64 * j;
-            if (c < ncols) *reinterpret_cast<double2*>(partial + (size_t)p * ld + c) = acc[j];
-        }
-    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) slot[cols[i]] = i;
 }
 
-__global__ void spmm_fixup_kernel(const int* __restrict__ long_rows, const int* __restrict__ long_first,
-                                  const int* __restrict__ counts, const double* __restrict__ partial, int ld,
-                                  int ncols, double* __restrict__ out, int ldo) {
+__global__ void hot_relabel_kernel(const uint32_t* __restrict__ col, int64_t nnz, const int* __restrict__ slot, int n,
+                                   int* __restrict__ idx2) {
     pdl_entry();
-    const int nl = counts[0];
-    const int npieces = counts[1];
-    for (int li = blockIdx.x; li < nl; li += gridDim.x) {
-        const int first = long_first[li];
-        const int last = li + 1 < nl ? long_first[li + 1] : npieces;
-        const int r = long_rows[li];
-        for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
-            double s = 0.0;
-            for (int p = first; p < last; ++p) s += partial[(size_t)p * ld + c];
-            out[(size_t)r * ldo + c] = s;
-        }
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = col[k];
+        const int sl = slot[c];
+        idx2[k] = sl >= 0 ? sl : n + (int)c;
     }
 }
 
@@ -487,11 +559,14 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     host_long = -1;
     reserve_pieces(nnz);
     if (nrows > cap_rows) {
-        for (void* p : {(void*)long_rows, (void*)long_first}) if (p) cudaFree(p);
+        for (void* p : {(void*)long_rows, (void*)long_first, (void*)arrive}) if (p) cudaFree(p);
         CK(cudaMalloc(&long_rows, (size_t)nrows * sizeof(int)));
         CK(cudaMalloc(&long_first, (size_t)nrows * sizeof(int)));
+        CK(cudaMalloc(&arrive, (size_t)nrows * sizeof(int)));
+        CK(cudaMemsetAsync(arrive, 0, (size_t)nrows * sizeof(int), st));
         cap_rows = nrows;
     }
+    host_pieces = -1;
     if (!counts) CK(cudaMalloc(&counts, 2 * sizeof(int)));
     CK(cudaMemsetAsync(counts, 0, 2 * sizeof(int), st));
     if (nrows == 0) return;
@@ -505,30 +580,42 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     exclusive_scan(np, piece_off, nrows, scr, st);
     // pieces <= nnz / kPiece + nrows; size the piece arrays for the worst case of this call
     LAUNCH(plan_fill_kernel, g, 256, 0, st, d_ptr, nrows, kPiece, is_long, long_off, piece_off, long_rows, long_first,
-           piece_beg, piece_end, counts);
+           piece_beg, piece_end, piece_li, counts);
 }
 
 void SegPlan::reserve_pieces(int64_t nnz) {
     const int64_t need = 2 * (nnz / kPiece) + 2;
     if (need > cap_pieces) {
-        for (void* p : {(void*)piece_beg, (void*)piece_end}) if (p) cudaFree(p);
+        for (void* p : {(void*)piece_beg, (void*)piece_end, (void*)piece_li}) if (p) cudaFree(p);
         cap_pieces = need;
         CK(cudaMalloc(&piece_beg, cap_pieces * sizeof(int)));
         CK(cudaMalloc(&piece_end, cap_pieces * sizeof(int)));
+        CK(cudaMalloc(&piece_li, cap_pieces * sizeof(int)));
     }
 }
 
+void SegPlan::ensure_partial(int64_t doubles) const {
+    if (doubles <= partial_cap) return;
+    if (partial) CK(cudaFree(partial));
+    partial_cap = std::max<int64_t>(doubles, partial_cap * 3 / 2);
+    CK(cudaMalloc(&partial, partial_cap * sizeof(double)));
+}
+
 void SegPlan::release() {
-    for (void* p : {(void*)long_rows, (void*)long_first, (void*)piece_beg, (void*)piece_end, (void*)counts})
+    if (partial) cudaFree(partial);
+    partial = nullptr;
+    partial_cap = 0;
+    for (void* p : {(void*)long_rows, (void*)long_first, (void*)piece_beg, (void*)piece_end, (void*)piece_li,
+                    (void*)arrive, (void*)counts})
         if (p) cudaFree(p);
-    long_rows = long_first = piece_beg = piece_end = counts = nullptr;
+    long_rows = long_first = piece_beg = piece_end = piece_li = arrive = counts = nullptr;
     cap_rows = 0;
     cap_pieces = 0;
 }
 
 void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, const SegPlan& plan, int64_t nnz,
           const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st,
-          int64_t in_rows, int alg_cols) {
+          int64_t in_rows, int alg_cols, const HotSet* hot) {
     if (nrows == 0) return;
     if (ncols % 2 != 0 || ld % 2 != 0 || ldo % 2 != 0) throw invalid_argument("spmm: panel widths must be even");
     ProfScope prof("spmm", st);
@@ -537,17 +624,48 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
         prof.work(2.0 * (double)nnz * w, 12.0 * (double)nnz + 8.0 * (nrows + 1) + 8.0 * w * (ir + nrows));
     }
     const int J = (ncols + 63) / 64;
-    const unsigned grid = std::max(1u, std::min(16u * kSMs, ceil_div((size_t)nrows * 32, 256)));
-    double* partial = scr.take<double>((2 * (nnz / kPiece) + 2) * (int64_t)ld);
-    const unsigned pgrid = 4 * kSMs;
+    const int use_pieces = plan.host_long != 0 ? 1 : 0;
+    const int64_t pieces = plan.host_pieces >= 0 ? plan.host_pieces : 2 * (nnz / kPiece) + 2;
+    // a function of nrows only, so a captured sweep block replays unchanged for any piece count
+    const unsigned grid = std::max(1u, std::min(16u * kSMs, ceil_div((size_t)nrows * 2 * 32, 256)));
+    if (use_pieces) plan.ensure_partial(std::max<int64_t>(pieces, 1) * ld);
+    double* partial = use_pieces ? plan.partial : nullptr;
+    const bool use_hot = hot && hot->n > 0;
+    if (use_hot) {
+        int dev = 0, sms = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const size_t smem = (size_t)hot->n * ncols * sizeof(double);
+        switch (J) {
+#define SPMM_HOT(JJ)                                                                                                  \
+    case JJ: {                                                                                                        \
+        auto* fn = spmm_kernel<JJ, true>;                                                                             \
+        if (first_on_device((const void*)fn)) allow_max_dynamic_smem(fn);                                            \
+        LAUNCH(fn, (unsigned)sms, (spmm_threads<JJ, true>()), smem, st, d_ptr, hot->idx, d_val, nrows, plan.piece_beg, \
+               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, use_pieces,  \
+               d_in, ld, ncols, d_out, ldo, partial, hot->cols, hot->n);                                              \
+        break;                                                                                                        \
+    }
+            SPMM_HOT(1)
+            SPMM_HOT(2)
+            SPMM_HOT(3)
+            SPMM_HOT(4)
+            SPMM_HOT(5)
+            SPMM_HOT(6)
+            SPMM_HOT(7)
+            SPMM_HOT(8)
+#undef SPMM_HOT
+            default:
+                throw invalid_argument("spmm: panel wider than 512 columns");
+        }
+        return;
+    }
     switch (J) {
 #define SPMM_CASE(JJ)                                                                                              \
     case JJ:                                                                                                       \
-        LAUNCH(spmm_rows_kernel<JJ>, grid, 256, 0, st, d_ptr, d_idx, d_val, nrows, kPiece, d_in, ld, ncols, d_out, \
-               ldo);                                                                                               \
-        if (plan.host_long != 0)                                                                                   \
-            LAUNCH(spmm_pieces_kernel<JJ>, pgrid, 256, 0, st, plan.piece_beg, plan.piece_end, plan.counts, d_idx, \
-                   d_val, d_in, ld, ncols, partial);                                                               \
+        LAUNCH((spmm_kernel<JJ, false>), grid, 256, 0, st, d_ptr, d_idx, d_val, nrows, plan.piece_beg,             \
+               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, use_pieces, \
+               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0);                                      \
         break;
         SPMM_CASE(1)
         SPMM_CASE(2)
@@ -561,9 +679,20 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
         default:
             throw invalid_argument("spmm: panel wider than 512 columns");
     }
-    if (plan.host_long != 0)
-        LAUNCH(spmm_fixup_kernel, 2 * kSMs, 128, 0, st, plan.long_rows, plan.long_first, plan.counts, partial, ld,
-               ncols, d_out, ldo);
+}
+
+int hot_rows_capacity(int ncols) {
+    // 200 KB of the 227 KB a CTA may use (static smem and the L1 keep the rest)
+    return (int)((200u * 1024u) / ((unsigned)ncols * sizeof(double)));
+}
+
+void hot_relabel(const int* d_cols_hot, int n, const uint32_t* col, int64_t nnz, int d, int* slot, int* idx2,
+                 cudaStream_t st) {
+    CK(cudaMemsetAsync(slot, 0xff, (size_t)d * sizeof(int), st));
+    if (n > 0) LAUNCH(hot_slot_kernel, ceil_div(n, 256), 256, 0, st, d_cols_hot, n, slot);
+    if (nnz > 0)
+        LAUNCH(hot_relabel_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)nnz, 256))), 256, 0, st, col, nnz,
+               slot, n, idx2);
 }
 
 int64_t validate_rows_device(const int64_t* d_row_ptr, int64_t nrows, const uint32_t* d_cols, const double* d_vals,

@@ -91,16 +91,26 @@ struct DevCsr {
     ~DevCsr() { release(); }
 };
 
-// Long-row split plan for the gather SpMM (rows longer than 2*kPiece).
-constexpr int kPiece = 256;
+// Long-row split plan for the gather SpMM: rows longer than 2*kPiece are cut into kPiece-long
+// pieces, processed by the same launch as the short rows (pieces first, so their latency
+// chains overlap the rest) and summed per row, in piece order, by the piece that finishes last.
+constexpr int kPiece = 128;
 struct SegPlan {
     int rows = 0;
     int* long_rows = nullptr;
     int* long_first = nullptr;
     int* piece_beg = nullptr;
     int* piece_end = nullptr;
+    int* piece_li = nullptr;  // long-row index of each piece
+    int* arrive = nullptr;    // per long row: pieces finished in the current launch (self-resetting)
     int* counts = nullptr;  // device [nlong, npieces]
     int host_long = -1;     // long rows as known on the host (-1: unknown -> always run the piece path)
+    int64_t host_pieces = -1;  // pieces as known on the host (-1: unknown -> worst-case partial buffer)
+    // Partial rows of the pieces: a retained buffer (not scratch), so its address is fixed for
+    // the sweep-block CUDA graphs; grown by ensure_partial() outside any capture.
+    mutable double* partial = nullptr;
+    mutable int64_t partial_cap = 0;
+    void ensure_partial(int64_t doubles) const;
     int cap_rows = 0;
     int64_t cap_pieces = 0;
     void build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st);
@@ -109,6 +119,19 @@ struct SegPlan {
     ~SegPlan() { release(); }
 };
 
+// The most frequent columns of a flush (per-flush frequency ranking): their input-panel rows
+// are staged once per CTA in shared memory by TMA bulk copies, so every nonzero in those
+// columns reads the panel row from SMEM instead of gathering it through L2. idx is the CSR
+// column array relabelled for it: hot column -> its slot (< n), other column c -> n + c.
+struct HotSet {
+    const int* cols = nullptr;  // n column ids, device
+    const int* idx = nullptr;   // relabelled CSR column indices, device
+    int n = 0;
+};
+
+// Shared memory the hot rows of a panel `ncols` wide may use, and the resulting row count.
+int hot_rows_capacity(int ncols);
+
 void exclusive_scan(const int64_t* d_in, int64_t* d_out, int64_t n, Scratch& scr, cudaStream_t st);
 void rebase_row_ptr(const int64_t* d_src, int64_t base, int m, int* d_dst, cudaStream_t st);
 void build_transpose(DevCsr& a, Scratch& scr, cudaStream_t st);
@@ -116,9 +139,13 @@ void build_transpose(DevCsr& a, Scratch& scr, cudaStream_t st);
 // in_rows / alg_cols (profiling only): rows of the input panel and the unpadded panel width,
 // for the launch's declared algorithmic bytes 12 nnz + 8 (nrows + 1) + 8 alg_cols (in_rows + nrows)
 // (SURVEY 8(d)); -1 = nrows / ncols.
+// hot (optional): stage those input rows in shared memory (see HotSet); results are bit-identical.
 void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, const SegPlan& plan, int64_t nnz,
           const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st,
-          int64_t in_rows = -1, int alg_cols = -1);
+          int64_t in_rows = -1, int alg_cols = -1, const HotSet* hot = nullptr);
+// slot (d ints) = -1 except slot[cols[i]] = i; idx2[k] = slot[col[k]] >= 0 ? slot : n + col[k].
+void hot_relabel(const int* d_cols_hot, int n, const uint32_t* col, int64_t nnz, int d, int* slot, int* idx2,
+                 cudaStream_t st);
 // First invalid row (or -1) of a device-resident CSR batch; kind_out gets ERR_BAD_* bits.
 int64_t validate_rows_device(const int64_t* d_row_ptr, int64_t nrows, const uint32_t* d_cols, const double* d_vals,
                              uint32_t d, int* kind_out, Scratch& scr, cudaStream_t st);

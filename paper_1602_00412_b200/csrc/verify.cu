@@ -345,11 +345,15 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
             const int np = a.counts[1];
             const int gw = blockIdx.x * kVWarps + wib, tw = nb * kVWarps;
             for (int p = gw; p < np; p += tw) {
-                double sp = 0.0;
-                for (int k = a.piece_beg[p] + lane; k < a.piece_end[p]; k += 32)
-                    sp = fma(a.cval[k], __ldcg(a.u + a.row_idx[k]), sp);
-                sp = warp_sum(sp);
-                if (lane == 0) a.lpart[p] = sp;
+                const int kb = a.piece_beg[p], ke = a.piece_end[p];
+                double sp[4] = {0.0, 0.0, 0.0, 0.0};  // four gathers per lane in flight
+                for (int k = kb + lane; k < ke; k += 128) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (k + 32 * u < ke) sp[u] = fma(a.cval[k + 32 * u], __ldcg(a.u + a.row_idx[k + 32 * u]), sp[u]);
+                }
+                const double t = warp_sum((sp[0] + sp[1]) + (sp[2] + sp[3]));
+                if (lane == 0) a.lpart[p] = t;
             }
             step_sync();
         }
@@ -393,11 +397,14 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
                     dp[q] = fma(-brow[q][w], tl[w], dp[q]);  // - (B'^T t)_c partial
                 }
             }
-            for (int off = lane; off < len; off += 32) {
+            for (int off = lane; off < len; off += 64) {  // two gathers per column and lane in flight
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int k = k0[q] + off;
-                    if (k < k1[q]) dp[q] = fma(CV[k], __ldcg(a.u + RI[k]), dp[q]);
+                    double v0 = 0.0, v1 = 0.0;
+                    if (k < k1[q]) v0 = CV[k] * __ldcg(a.u + RI[k]);
+                    if (k + 32 < k1[q]) v1 = CV[k + 32] * __ldcg(a.u + RI[k + 32]);
+                    dp[q] += v0 + v1;
                 }
             }
             const double tot = warp_sum4(dp);  // (A'^T u - B'^T t)_c on lanes 8q..8q+7
@@ -759,7 +766,8 @@ int verify_grid_blocks(int device, int64_t d, int lp) {
     // 146 blocks 322, 74 blocks 199, 32 blocks 182 ms per stream). Large B' (c3-c5: 0.16-2 GB
     // per step) is bandwidth bound per SM: one block per 512 KB of B', up to every SM.
     const int64_t by_size = (8 * d * (int64_t)lp) / (512 * 1024);
-    int nb = (int)std::max<int64_t>(32, std::min<int64_t>(sms, by_size));
+    // past the small-B' regime every SM: the cost-balanced ranges keep the blocks even
+    int nb = by_size > 32 ? sms : 32;
     if (const char* e = std::getenv("SFDG_VERIFY_BLOCKS")) nb = std::max(1, std::min(sms, std::atoi(e)));
     return nb;
 }

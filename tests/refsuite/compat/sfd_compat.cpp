@@ -123,9 +123,29 @@ DenseMatrix sparse_shrink(const SparseBuffer& a, std::size_t ell, const PowerCon
     return out;
 }
 
-bool verify_spectral(const SymOp&, std::size_t, VerifierState&, Rng&) {
-    throw std::logic_error("verify_spectral: host operators are not offloaded (the device verifier runs inside "
-                           "boosted_sparse_shrink)");
+// The caller's std::function operator runs on the host through sfdg_verify_spectral's
+// callback; the draw of x and the step bookkeeping are the library's.
+bool verify_spectral(const SymOp& apply, std::size_t d, VerifierState& state, Rng& rng) {
+    struct Ctx {
+        const SymOp* op;
+        std::vector<double> x;
+    } ctx{&apply, std::vector<double>(d)};
+    auto cb = [](const double* x, double* y, size_t n, void* user) -> int {
+        Ctx* c = static_cast<Ctx*>(user);
+        c->x.assign(x, x + n);
+        const std::vector<double> out = (*c->op)(c->x);
+        if (out.size() != n) return 1;
+        std::copy(out.begin(), out.end(), y);
+        return 0;
+    };
+    sfdg_verifier_state vs{state.i, state.delta, state.c_verify, state.delta_spent};
+    sfdg_rng_state st = rng.device_state();
+    int accepted = 0;
+    check(sfdg_verify_spectral(cb, &ctx, 0, d, &vs, &st, &accepted, kDevice));
+    rng.set_device_state(st);
+    state.i = vs.i;
+    state.delta_spent = vs.delta_spent;
+    return accepted != 0;
 }
 
 ShrinkReport boosted_sparse_shrink(const SparseBuffer& a, std::size_t ell, VerifierState& state,

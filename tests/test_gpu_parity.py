@@ -939,3 +939,26 @@ def test_cov_err_after_sketch_in_one_process():
     b = s.finalize()
     ce, _ = P.cov_err((rp, cs, vs), d, b, P.RngState(4242), iterations=50, device=0)
     assert 0.0 <= ce <= 1.0 / (KALPHA * ell)
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0]])
+def test_sharded_sketch_c5_family_vs_oracle_tree(oracle, devices):
+    """The 8-GPU configuration's family (Poisson(20)+1 rows, Zipf 1.05 columns, planted
+    signal) at a d the oracle finishes in seconds: 4 contiguous shards with seeds 4 + g over
+    the device list, merged in the log2 tree, against the oracle replaying the same shards,
+    seeds and tree (parity is per shard count)."""
+    from paper_1602_00412_b200 import shards as SH
+    d, ell, n, shards = 2000, 48, 12000, 4
+    rp, cs, vs = S.generate(S.StreamConfig("c5", n, d, ell, 4), (0, n))
+    cfg = P.SketchConfig(ell=ell, d=d, seed=4)
+    b, st = P.sharded_sketch(rp, cs, vs, cfg, shards, devices=devices)
+    per = (n + shards - 1) // shards
+    parts = []
+    for g in range(shards):
+        r0, r1 = min(n, g * per), min(n, (g + 1) * per)
+        bo, so = oracle.sketch(rp[r0:r1 + 1] - rp[r0], cs[rp[r0]:rp[r1]], vs[rp[r0]:rp[r1]], d, ell, seed=4 + g)
+        parts.append(bo)
+        assert (st[g]["flushes"], st[g]["attempts"], st[g]["verifier_i"]) == (so["flushes"], so["attempts"],
+                                                                             so["verifier_i"])
+    want = SH.replay_tree(parts, lambda a, c: oracle.merge(a, c, ell))
+    assert btb_rel(b, want) <= BTB_TOL

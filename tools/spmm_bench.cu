@@ -5,6 +5,7 @@
 // `achieved`), and the L2 -> SM gather rate (one ell-wide panel row per stored entry).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -87,7 +88,42 @@ int main(int argc, char** argv) {
         s2.reset();
         spmm(a.col_ptr, a.row_idx, a.cval, d, pc, a.nnz, Y, lp, lp, W, lp, s2, st);
     });
-    for (auto [name, t] : {std::pair<const char*, double>{"csr (Y = A'W)", t_csr}, {"csc (W = A'^T Y)", t_csc}})
+    // hot-column staging for the CSR direction (the engine's per-flush choice, Engine::choose_hot)
+    const int cap = std::min(hot_rows_capacity(lp), d);
+    std::vector<int> cp(d + 1), ids(d);
+    cudaMemcpy(cp.data(), a.col_ptr, (d + 1) * 4, cudaMemcpyDeviceToHost);
+    for (int c = 0; c < d; ++c) ids[c] = c;
+    auto cnt = [&](int c) { return cp[c + 1] - cp[c]; };
+    auto better = [&](int x, int y) { return cnt(x) != cnt(y) ? cnt(x) > cnt(y) : x < y; };
+    std::nth_element(ids.begin(), ids.begin() + (cap - 1), ids.end(), better);
+    std::sort(ids.begin(), ids.begin() + cap, better);
+    long long in_hot = 0;
+    for (int i = 0; i < cap; ++i) in_hot += cnt(ids[i]);
+    int *hcols, *slot, *idx2;
+    cudaMalloc(&hcols, cap * 4);
+    cudaMalloc(&slot, (size_t)d * 4);
+    cudaMalloc(&idx2, nnz * 4);
+    cudaMemcpy(hcols, ids.data(), cap * 4, cudaMemcpyHostToDevice);
+    hot_relabel(hcols, cap, a.col, nnz, d, slot, idx2, st);
+    HotSet hs{hcols, idx2, cap};
+    double* Y2;
+    cudaMalloc(&Y2, (size_t)m * lp * 8);
+    const double t_hot = time_us(st, reps, [&] {
+        s2.reset();
+        spmm(a.row_ptr, (const int*)a.col, a.val, m, pr, a.nnz, W, lp, lp, Y2, lp, s2, st, -1, -1, &hs);
+    });
+    s2.reset();
+    spmm(a.row_ptr, (const int*)a.col, a.val, m, pr, a.nnz, W, lp, lp, Y, lp, s2, st);
+    cudaStreamSynchronize(st);
+    std::vector<double> h1((size_t)m * lp), h2((size_t)m * lp);
+    cudaMemcpy(h1.data(), Y, h1.size() * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h2.data(), Y2, h2.size() * 8, cudaMemcpyDeviceToHost);
+    size_t diff = 0;
+    for (size_t i = 0; i < h1.size(); ++i) diff += h1[i] != h2[i];
+    printf("hot columns: %d staged rows hold %.1f%% of the entries; hot result differs in %zu of %zu values\n", cap,
+           100.0 * in_hot / nnz, diff, h1.size());
+    for (auto [name, t] : {std::pair<const char*, double>{"csr (Y = A'W)", t_csr}, {"csr + hot smem", t_hot},
+                           {"csc (W = A'^T Y)", t_csc}})
         printf("%-18s %9.2f us  alg %7.1f GB/s (frac %.3f of %.0f)  gather %7.1f GB/s\n", name, t, alg / t / 1e3,
                alg / t / 1e3 / hbm, hbm, gath / t / 1e3);
     printf("cuda: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
