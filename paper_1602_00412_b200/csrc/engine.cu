@@ -554,6 +554,7 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
     args.err = d_err;
     args.out = vout;
     args.has_long = plan_c.host_long != 0 ? 1 : 0;
+    args.piece = plan_c.piece;
     args.long_cols = plan_c.long_rows;
     args.long_first = plan_c.long_first;
     args.piece_beg = plan_c.piece_beg;
@@ -617,7 +618,7 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
         }
         if (verify_cluster == 0 && !args.resident && !(std::getenv("SFDG_VERIFY_BALANCE") && std::atoi(std::getenv("SFDG_VERIFY_BALANCE")) == 0)) {
             int64_t* prefix = scr.take<int64_t>((int64_t)d + 1);
-            verify_column_costs(a.col_ptr, d, ell, prefix, scr, st);
+            verify_column_costs(a.col_ptr, d, ell, plan_c.piece, prefix, scr, st);
             args.ccost = prefix;
         }
         if (serial) CK(cudaStreamWaitEvent(st, serial, 0));

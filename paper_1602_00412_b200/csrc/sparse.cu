@@ -191,22 +191,41 @@ __global__ void col_ptr_kernel(const uint32_t* __restrict__ skeys, int64_t n, in
 }
 
 // ---------------------------------------------------------------- segment plans
+// Warp-aggregated slot in bin b: one atomic per distinct bin among the active lanes (row lengths
+// cluster on a few values, so per-lane atomics would serialise on a handful of addresses).
+__device__ __forceinline__ int64_t bin_slot(int64_t* bins, int b) {
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, b);
+    const int leader = __ffs(peers) - 1;
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (lane == leader)
+        base = atomicAdd(reinterpret_cast<unsigned long long*>(bins + b), (unsigned long long)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    return (int64_t)base + __popc(peers & ((1u << lane) - 1u));
+}
+
+// short rows are binned by length, longest first (bin 2 piece - len), for the SpMM's row order
 __global__ void plan_count_kernel(const int* __restrict__ ptr, int nrows, int piece, int64_t* __restrict__ is_long,
-                                  int64_t* __restrict__ npieces) {
+                                  int64_t* __restrict__ npieces, int64_t* __restrict__ bins) {
     pdl_entry();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
         const int len = ptr[r + 1] - ptr[r];
         const bool lg = len > 2 * piece;
         is_long[r] = lg ? 1 : 0;
         npieces[r] = lg ? (len + piece - 1) / piece : 0;
+        if (!lg) bin_slot(bins, 2 * piece - len);
     }
 }
 
+// Pieces of the long rows in row order; the short rows scattered into their length bins (the
+// order inside a bin is arbitrary: it only decides which warp computes a row).
 __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int piece, const int64_t* __restrict__ is_long,
                                  const int64_t* __restrict__ long_off, const int64_t* __restrict__ piece_off,
                                  int* __restrict__ long_rows, int* __restrict__ long_first, int* __restrict__ piece_beg,
                                  int* __restrict__ piece_end, int* __restrict__ piece_li,
-                                 int* __restrict__ counts /* [nlong, npieces] */) {
+                                 int* __restrict__ counts /* [nlong, npieces, nshort] */, int64_t* __restrict__ bin_off,
+                                 int* __restrict__ order) {
     pdl_entry();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
         const int len = ptr[r + 1] - ptr[r];
@@ -221,10 +240,13 @@ __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int pie
                 piece_end[pf + p] = min(ptr[r] + (p + 1) * piece, ptr[r + 1]);
                 piece_li[pf + p] = li;
             }
+        } else {
+            order[bin_slot(bin_off, 2 * piece - len)] = r;
         }
         if (r == nrows - 1) {
             counts[0] = (int)(long_off[r] + is_long[r]);
             counts[1] = (int)(piece_off[r] + (len > 2 * piece ? (len + piece - 1) / piece : 0));
+            counts[2] = nrows - counts[0];
         }
     }
 }
@@ -233,7 +255,7 @@ __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int pie
 // J = number of 64-column chunks (lane owns columns 2*lane + 64*j, +1). HOT: idx is relabelled
 // (HotSet): entries < nh read the staged row in shared memory (hot + i * ldh), the others row
 // idx - nh of `in`. The same loads in the same order either way, so the sums are identical.
-template <int J, bool HOT>
+template <int J, bool HOT, int NB>
 __device__ __forceinline__ void gather_range(int kb, int ke, const int* __restrict__ idx, const double* __restrict__ val,
                                              const double* __restrict__ in, int ld, int ncols, int lane,
                                              double2 (&acc)[J], const double* hot, int nh, int ldh) {
@@ -251,24 +273,24 @@ __device__ __forceinline__ void gather_range(int kb, int ke, const int* __restri
         const double my_val = kk < ke ? val[kk] : 0.0;
         const int cnt = min(32, ke - k0);
         int e = 0;
-        for (; e + 4 <= cnt; e += 4) {
-            const double* rp[4];
-            double cv[4];
+        for (; e + NB <= cnt; e += NB) {
+            const double* rp[NB];
+            double cv[NB];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < NB; ++u) {
                 rp[u] = row(__shfl_sync(0xffffffffu, my_idx, e + u));
                 cv[u] = __shfl_sync(0xffffffffu, my_val, e + u);
             }
-            double2 x[4][J];
+            double2 x[NB][J];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < NB; ++u)
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
                     const int c = 2 * lane + 64 * j;
                     x[u][j] = c < ncols ? load(rp[u] + c) : make_double2(0.0, 0.0);
                 }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < NB; ++u)
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
                     acc[j].x = fma(cv[u], x[u][j].x, acc[j].x);
@@ -321,18 +343,25 @@ __device__ __forceinline__ void stage_hot_rows(double* hot, const int* __restric
         : "memory");
 }
 
-// One launch for the whole product. Work item w < npieces is a kPiece-long piece of a long row:
-// its partial row goes to `partial`, and the piece that finishes a row last (per-row arrival
+// One launch for the whole product. Work item w < npieces is a piece of a long row: its
+// partial row goes to `partial`, and the piece that finishes a row last (per-row arrival
 // counter) sums that row's partials in piece order -- deterministic, no FP atomics. The other
-// items are the short rows, written directly. Pieces come first, so their dependent gather
-// chains start at the beginning of the launch instead of forming a tail.
+// items are the short rows in the plan's longest-first order, written directly. Pieces come
+// first, so their dependent gather chains start at the beginning of the launch instead of
+// forming a tail.
+// Occupancy / loads in flight (tools/spmm_lab.cu on the c2-c5 flush buffers): ell <= 128
+// (J <= 2) four panel rows in flight per warp at 4 blocks per SM; wider panels two rows at 3.
 template <int J, bool HOT>
 constexpr int spmm_threads() {
     return HOT ? (J <= 2 ? 1024 : 512) : 256;
 }
 template <int J, bool HOT>
 constexpr int spmm_min_blocks() {
-    return HOT ? 1 : (J <= 2 ? 5 : 2);
+    return HOT ? 1 : (J <= 2 ? 4 : 3);
+}
+template <int J>
+__host__ __device__ constexpr int spmm_batch() {
+    return J <= 2 ? 4 : 2;
 }
 
 template <int J, bool HOT>
@@ -340,7 +369,7 @@ __global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT
     const int* __restrict__ ptr, const int* __restrict__ idx, const double* __restrict__ val, int nrows,
     const int* __restrict__ piece_beg, const int* __restrict__ piece_end, const int* __restrict__ piece_li,
     const int* __restrict__ long_rows, const int* __restrict__ long_first, const int* __restrict__ counts,
-    int* __restrict__ arrive, int use_pieces, const double* __restrict__ in, int ld, int ncols,
+    int* __restrict__ arrive, const int* __restrict__ order, int use_pieces, const double* __restrict__ in, int ld, int ncols,
     double* __restrict__ out, int ldo, double* __restrict__ partial, const int* __restrict__ hot_cols, int nh) {
     extern __shared__ __align__(128) double hot_sm[];
     __shared__ uint64_t hot_bar;
@@ -354,12 +383,15 @@ __global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const int np = use_pieces ? counts[1] : 0;
     const int nl = use_pieces ? counts[0] : 0;
-    for (int w = warp; w < np + nrows; w += nw) {
+    const int ns = counts[2];  // short rows (all rows when there are no long ones)
+    constexpr int NB = spmm_batch<J>();
+    for (int w = warp; w < np + ns; w += nw) {
         double2 acc[J];
 #pragma unroll
         for (int j = 0; j < J; ++j) acc[j] = make_double2(0.0, 0.0);
         if (w < np) {
-            gather_range<J, HOT>(piece_beg[w], piece_end[w], idx, val, in, ld, ncols, lane, acc, hot_sm, nh, ncols);
+            gather_range<J, HOT, NB>(piece_beg[w], piece_end[w], idx, val, in, ld, ncols, lane, acc, hot_sm, nh,
+                                     ncols);
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int c = 2 * lane + 64 * j;
@@ -378,8 +410,21 @@ __global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT
                 for (int j = 0; j < J; ++j) {
                     const int c = 2 * lane + 64 * j;
                     if (c < ncols) {
+                        // in piece order, eight partial rows in flight
                         double2 t = make_double2(0.0, 0.0);
-                        for (int p = first; p < last; ++p) {
+                        int p = first;
+                        for (; p + 8 <= last; p += 8) {
+                            double2 v[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                v[u] = __ldcg(reinterpret_cast<const double2*>(partial + (size_t)(p + u) * ld + c));
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                t.x += v[u].x;
+                                t.y += v[u].y;
+                            }
+                        }
+                        for (; p < last; ++p) {
                             const double2 v = __ldcg(reinterpret_cast<const double2*>(partial + (size_t)p * ld + c));
                             t.x += v.x;
                             t.y += v.y;
@@ -391,10 +436,9 @@ __global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT
             }
             continue;
         }
-        const int r = w - np;
+        const int r = order[w - np];
         const int kb = ptr[r], ke = ptr[r + 1];
-        if (use_pieces && ke - kb > 2 * kPiece) continue;  // summed by its last piece
-        gather_range<J, HOT>(kb, ke, idx, val, in, ld, ncols, lane, acc, hot_sm, nh, ncols);
+        gather_range<J, HOT, NB>(kb, ke, idx, val, in, ld, ncols, lane, acc, hot_sm, nh, ncols);
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const int c = 2 * lane + 64 * j;
@@ -553,38 +597,51 @@ void build_transpose(DevCsr& a, Scratch& scr, cudaStream_t st) {
     LAUNCH(col_ptr_kernel, ceil_div(d + 1, 256), 256, 0, st, k0, n, d, a.col_ptr);
 }
 
+int spmm_piece_length(int64_t nnz) {
+    const int64_t per_warp = nnz / (16 * kSMs * 8);  // the SpMM grid: <= 16 x 148 blocks of 8 warps
+    int piece = kPiece;
+    while (piece < 2048 && 2 * (int64_t)piece <= per_warp / 2) piece *= 2;
+    return piece;
+}
+
 void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st) {
     ProfScope prof("csc_build", st);
     rows = nrows;
     host_long = -1;
+    piece = spmm_piece_length(nnz);
     reserve_pieces(nnz);
     if (nrows > cap_rows) {
-        for (void* p : {(void*)long_rows, (void*)long_first, (void*)arrive}) if (p) cudaFree(p);
+        for (void* p : {(void*)long_rows, (void*)long_first, (void*)arrive, (void*)order}) if (p) cudaFree(p);
         CK(cudaMalloc(&long_rows, (size_t)nrows * sizeof(int)));
         CK(cudaMalloc(&long_first, (size_t)nrows * sizeof(int)));
         CK(cudaMalloc(&arrive, (size_t)nrows * sizeof(int)));
+        CK(cudaMalloc(&order, (size_t)nrows * sizeof(int)));
         CK(cudaMemsetAsync(arrive, 0, (size_t)nrows * sizeof(int), st));
         cap_rows = nrows;
     }
     host_pieces = -1;
-    if (!counts) CK(cudaMalloc(&counts, 2 * sizeof(int)));
-    CK(cudaMemsetAsync(counts, 0, 2 * sizeof(int), st));
+    if (!counts) CK(cudaMalloc(&counts, 3 * sizeof(int)));
+    CK(cudaMemsetAsync(counts, 0, 3 * sizeof(int), st));
     if (nrows == 0) return;
     int64_t* is_long = scr.take<int64_t>(nrows);
     int64_t* np = scr.take<int64_t>(nrows);
     int64_t* long_off = scr.take<int64_t>(nrows);
     int64_t* piece_off = scr.take<int64_t>(nrows);
+    const int nbins = 2 * piece + 1;  // short rows have 0 .. 2 piece entries
+    int64_t* bins = scr.take<int64_t>(nbins);
+    int64_t* bin_off = scr.take<int64_t>(nbins);
+    CK(cudaMemsetAsync(bins, 0, nbins * sizeof(int64_t), st));
     const unsigned g = std::max(1u, std::min(8u * kSMs, ceil_div(nrows, 256)));
-    LAUNCH(plan_count_kernel, g, 256, 0, st, d_ptr, nrows, kPiece, is_long, np);
+    LAUNCH(plan_count_kernel, g, 256, 0, st, d_ptr, nrows, piece, is_long, np, bins);
     exclusive_scan(is_long, long_off, nrows, scr, st);
     exclusive_scan(np, piece_off, nrows, scr, st);
-    // pieces <= nnz / kPiece + nrows; size the piece arrays for the worst case of this call
-    LAUNCH(plan_fill_kernel, g, 256, 0, st, d_ptr, nrows, kPiece, is_long, long_off, piece_off, long_rows, long_first,
-           piece_beg, piece_end, piece_li, counts);
+    exclusive_scan(bins, bin_off, nbins, scr, st);
+    // pieces <= nnz / piece + nrows; size the piece arrays for the worst case of this call
+    LAUNCH(plan_fill_kernel, g, 256, 0, st, d_ptr, nrows, piece, is_long, long_off, piece_off, long_rows, long_first,
+           piece_beg, piece_end, piece_li, counts, bin_off, order);
 }
-
 void SegPlan::reserve_pieces(int64_t nnz) {
-    const int64_t need = 2 * (nnz / kPiece) + 2;
+    const int64_t need = 2 * (nnz / kPiece) + 2;  // any piece length >= kPiece
     if (need > cap_pieces) {
         for (void* p : {(void*)piece_beg, (void*)piece_end, (void*)piece_li}) if (p) cudaFree(p);
         cap_pieces = need;
@@ -606,9 +663,9 @@ void SegPlan::release() {
     partial = nullptr;
     partial_cap = 0;
     for (void* p : {(void*)long_rows, (void*)long_first, (void*)piece_beg, (void*)piece_end, (void*)piece_li,
-                    (void*)arrive, (void*)counts})
+                    (void*)arrive, (void*)order, (void*)counts})
         if (p) cudaFree(p);
-    long_rows = long_first = piece_beg = piece_end = piece_li = arrive = counts = nullptr;
+    long_rows = long_first = piece_beg = piece_end = piece_li = arrive = order = counts = nullptr;
     cap_rows = 0;
     cap_pieces = 0;
 }
@@ -625,7 +682,7 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
     }
     const int J = (ncols + 63) / 64;
     const int use_pieces = plan.host_long != 0 ? 1 : 0;
-    const int64_t pieces = plan.host_pieces >= 0 ? plan.host_pieces : 2 * (nnz / kPiece) + 2;
+    const int64_t pieces = plan.host_pieces >= 0 ? plan.host_pieces : 2 * (nnz / plan.piece) + 2;
     // a function of nrows only, so a captured sweep block replays unchanged for any piece count
     const unsigned grid = std::max(1u, std::min(16u * kSMs, ceil_div((size_t)nrows * 2 * 32, 256)));
     if (use_pieces) plan.ensure_partial(std::max<int64_t>(pieces, 1) * ld);
@@ -642,7 +699,7 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
         auto* fn = spmm_kernel<JJ, true>;                                                                             \
         if (first_on_device((const void*)fn)) allow_max_dynamic_smem(fn);                                            \
         LAUNCH(fn, (unsigned)sms, (spmm_threads<JJ, true>()), smem, st, d_ptr, hot->idx, d_val, nrows, plan.piece_beg, \
-               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, use_pieces,  \
+               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.order, use_pieces,  \
                d_in, ld, ncols, d_out, ldo, partial, hot->cols, hot->n);                                              \
         break;                                                                                                        \
     }
@@ -664,7 +721,7 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
 #define SPMM_CASE(JJ)                                                                                              \
     case JJ:                                                                                                       \
         LAUNCH((spmm_kernel<JJ, false>), grid, 256, 0, st, d_ptr, d_idx, d_val, nrows, plan.piece_beg,             \
-               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, use_pieces, \
+               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.order, use_pieces, \
                d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0);                                      \
         break;
         SPMM_CASE(1)

@@ -91,19 +91,30 @@ struct DevCsr {
     ~DevCsr() { release(); }
 };
 
-// Long-row split plan for the gather SpMM: rows longer than 2*kPiece are cut into kPiece-long
-// pieces, processed by the same launch as the short rows (pieces first, so their latency
-// chains overlap the rest) and summed per row, in piece order, by the piece that finishes last.
+// Work plan of the gather SpMM over one CSR (or CSC) operand, built once per flush.
+// Rows longer than 2*piece are cut into piece-long pieces, processed by the same launch as the
+// short rows (pieces first, so their latency chains overlap the rest) and summed per row, in
+// piece order, by the piece that finishes last. The short rows follow in descending length
+// (`order`, a counting sort by length): with skewed row lengths (geometric / lognormal rows,
+// Zipf columns) a static warp-to-row assignment in natural order leaves a tail of long rows
+// on a few warps, longest-first keeps the warps even (c4 CSR: 201 -> 145 us per launch,
+// tools/spmm_lab.cu). The order only changes which warp computes a row, never the row's
+// arithmetic, so results do not depend on it.
+// piece: 128 entries, doubled while a piece stays under half the grid's per-warp share of the
+// entries (c3: 512, c5: 1024), so the partial rows of very long rows stay few.
 constexpr int kPiece = 128;
+int spmm_piece_length(int64_t nnz);
 struct SegPlan {
     int rows = 0;
+    int piece = kPiece;
     int* long_rows = nullptr;
     int* long_first = nullptr;
     int* piece_beg = nullptr;
     int* piece_end = nullptr;
     int* piece_li = nullptr;  // long-row index of each piece
     int* arrive = nullptr;    // per long row: pieces finished in the current launch (self-resetting)
-    int* counts = nullptr;  // device [nlong, npieces]
+    int* order = nullptr;     // the short rows, longest first
+    int* counts = nullptr;  // device [nlong, npieces, nshort]
     int host_long = -1;     // long rows as known on the host (-1: unknown -> always run the piece path)
     int64_t host_pieces = -1;  // pieces as known on the host (-1: unknown -> worst-case partial buffer)
     // Partial rows of the pieces: a retained buffer (not scratch), so its address is fixed for

@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
                 k0[q] = c < c1 ? CP[c - c0] - csub : 0;
                 k1[q] = c < c1 ? CP[c - c0 + 1] - csub : 0;
                 own[q] = c < c1;
-                if (a.has_long && k1[q] - k0[q] > 2 * kPiece) {  // long: the loop below
+                if (a.has_long && k1[q] - k0[q] > 2 * a.piece) {  // long: the loop below
                     k1[q] = k0[q];
                     own[q] = false;
                 }
@@ -736,23 +736,25 @@ VerifyFn verify_fn_t(int ell) {
 }
 
 // Per-column cost for the cost-balanced column ranges: a CSC entry is a stream read plus a
-// dependent gather (4), a long column (> 2 kPiece entries, summed over the grid in B0) costs
+// dependent gather (4), a long column (> 2 piece entries, summed over the grid in B0) costs
 // its pieces, and every column streams its B'^T row (ell / 8).
-__global__ void vcost_kernel(const int* __restrict__ col_ptr, int64_t d, int ell, int64_t* __restrict__ cost) {
+__global__ void vcost_kernel(const int* __restrict__ col_ptr, int64_t d, int ell, int piece,
+                             int64_t* __restrict__ cost) {
     pdl_entry();
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < d; c += (int64_t)gridDim.x * blockDim.x) {
         const int len = col_ptr[c + 1] - col_ptr[c];
-        const int eff = len > 2 * kPiece ? (len + kPiece - 1) / kPiece : len;
+        const int eff = len > 2 * piece ? (len + piece - 1) / piece : len;
         cost[c] = 4 * (int64_t)eff + ell / 8 + 4;
     }
 }
 
 }  // namespace
 
-void verify_column_costs(const int* d_col_ptr, int64_t d, int ell, int64_t* d_prefix, Scratch& scr, cudaStream_t st) {
+void verify_column_costs(const int* d_col_ptr, int64_t d, int ell, int piece, int64_t* d_prefix, Scratch& scr,
+                         cudaStream_t st) {
     int64_t* cost = scr.take<int64_t>(d + 1);
     LAUNCH(vcost_kernel, std::max(1u, std::min(8u * kSMs, ceil_div((size_t)d, 256))), 256, 0, st, d_col_ptr, d, ell,
-           cost);
+           piece, cost);
     CK(cudaMemsetAsync(cost + d, 0, sizeof(int64_t), st));
     exclusive_scan(cost, d_prefix, d + 1, scr, st);
 }

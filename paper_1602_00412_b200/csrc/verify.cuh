@@ -38,6 +38,7 @@ struct VerifyArgs {
     // Columns longer than 2 kPiece (skewed data: Zipf columns) are split into pieces that every
     // warp of the grid shares (the CSC SegPlan of the SpMM), summed per column in fixed order.
     int has_long;
+    int piece;              // the plan's piece length: a column is long above 2 piece entries
     const int* long_cols;   // ascending column ids
     const int* long_first;  // first piece of each long column
     const int* piece_beg;
@@ -49,7 +50,8 @@ struct VerifyArgs {
 
 class Scratch;
 // Exclusive prefix of the per-column costs that balance the persistent verifier's column ranges.
-void verify_column_costs(const int* d_col_ptr, int64_t d, int ell, int64_t* d_prefix, Scratch& scr, cudaStream_t st);
+void verify_column_costs(const int* d_col_ptr, int64_t d, int ell, int piece, int64_t* d_prefix, Scratch& scr,
+                         cudaStream_t st);
 
 int verify_grid_blocks(int device, int64_t d, int lp);  // cooperative grid for this B' size
 // Smallest grid (>= the streaming grid, <= one block per SM) whose blocks can hold their
