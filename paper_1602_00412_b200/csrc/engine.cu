@@ -212,6 +212,10 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     verify_cluster = verify_cluster_size(d, lp);
     verify_blocks = verify_cluster > 0 ? verify_cluster : verify_grid_blocks(device, d, lp);
     vg_blocks = verify_graph_blocks(device, d);
+    // Large B' (c3-c5: the persistent grid would take every SM, 512 threads x 128 registers,
+    // i.e. each SM's whole register file, for the entire verification): the kernel sequence,
+    // which leaves room for the other lanes' kernels. Small B' (c1, c2): the persistent kernel.
+    use_vgraph = (8 * (int64_t)d * lp) / (512 * 1024) > 32;
     if (const char* e = std::getenv("SFDG_VERIFY_MODE")) use_vgraph = std::string(e) == "graph";
     int sms_here = 0;
     CK(cudaDeviceGetAttribute(&sms_here, cudaDevAttrMultiProcessorCount, device));
@@ -251,7 +255,7 @@ Engine::~Engine() {
                     (void*)dinv8, (void*)kc,
                     (void*)evals, (void*)evecs, (void*)S, (void*)x0, (void*)ybuf, (void*)u, (void*)tpart, (void*)tvec,
                     (void*)vpart, (void*)vout, (void*)bar, (void*)d_err, (void*)d_scal, (void*)xtmp, (void*)d_udrop,
-                    (void*)vstate})
+                    (void*)vstate, (void*)varrive})
         if (p) cudaFree(p);
     if (h_scal) cudaFreeHost(h_scal);
     if (h_err) cudaFreeHost(h_err);
@@ -563,6 +567,26 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
     args.lpart = scr.take<double>(std::max<int64_t>(1, plan_c.cap_pieces));
     args.nnz = a.nnz;
     if (verify_as_graph()) {
+        if (a.m > varrive_cap) {
+            if (varrive) CK(cudaFree(varrive));
+            CK(cudaMalloc(&varrive, (size_t)a.m * sizeof(int)));
+            CK(cudaMemsetAsync(varrive, 0, (size_t)a.m * sizeof(int), st));
+            varrive_cap = a.m;
+        }
+        args.r_counts = plan_r.counts;
+        args.r_piece_beg = plan_r.piece_beg;
+        args.r_piece_end = plan_r.piece_end;
+        args.r_piece_li = plan_r.piece_li;
+        args.r_long_rows = plan_r.long_rows;
+        args.r_long_first = plan_r.long_first;
+        args.r_order = plan_r.order;
+        args.r_part = scr.take<double>(std::max<int64_t>(1, plan_r.cap_pieces));
+        args.r_arrive = varrive;
+        if (!(std::getenv("SFDG_VERIFY_BALANCE") && std::atoi(std::getenv("SFDG_VERIFY_BALANCE")) == 0)) {
+            int64_t* prefix = scr.take<int64_t>((int64_t)d + 1);
+            verify_column_costs(a.col_ptr, d, ell, plan_c.piece, prefix, scr, st);
+            args.ccost = prefix;
+        }
         // kernel-sequence verifier: per-call scalars by a setup kernel, the steps replayed
         // from a graph captured once per (step count, buffers); no serialisation needed
         // on a high-priority stream: the steps are short dependent kernels that would
@@ -574,12 +598,17 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
             CK(cudaStreamWaitEvent(vst, ev_v0, 0));
         }
         verify_setup(vstate, args.scale, args.steps, vs);
-        const std::array<uintptr_t, 18> key{
-            (uintptr_t)args.steps, (uintptr_t)args.m,     (uintptr_t)args.row_ptr, (uintptr_t)args.col,
-            (uintptr_t)args.val,   (uintptr_t)args.col_ptr, (uintptr_t)args.row_idx, (uintptr_t)args.cval,
-            (uintptr_t)args.bt,    (uintptr_t)args.ldb,   (uintptr_t)args.x0,      (uintptr_t)args.u,
-            (uintptr_t)args.ybuf,  (uintptr_t)args.tpart, (uintptr_t)args.t,       (uintptr_t)args.part,
-            (uintptr_t)args.out,   (uintptr_t)vstate};
+        const std::array<uintptr_t, 37> key{
+            (uintptr_t)args.steps,     (uintptr_t)args.m,          (uintptr_t)args.row_ptr,   (uintptr_t)args.col,
+            (uintptr_t)args.val,       (uintptr_t)args.col_ptr,    (uintptr_t)args.row_idx,   (uintptr_t)args.cval,
+            (uintptr_t)args.bt,        (uintptr_t)args.ldb,        (uintptr_t)args.x0,        (uintptr_t)args.u,
+            (uintptr_t)args.ybuf,      (uintptr_t)args.tpart,      (uintptr_t)args.t,         (uintptr_t)args.part,
+            (uintptr_t)args.out,       (uintptr_t)vstate,          (uintptr_t)args.has_long,  (uintptr_t)args.piece,
+            (uintptr_t)args.long_cols, (uintptr_t)args.long_first, (uintptr_t)args.piece_beg, (uintptr_t)args.piece_end,
+            (uintptr_t)args.counts,    (uintptr_t)args.lpart,      (uintptr_t)args.ccost,     (uintptr_t)args.err,
+            (uintptr_t)args.r_counts,  (uintptr_t)args.r_piece_beg, (uintptr_t)args.r_piece_end, (uintptr_t)args.r_piece_li,
+            (uintptr_t)args.r_long_rows, (uintptr_t)args.r_long_first, (uintptr_t)args.r_order, (uintptr_t)args.r_part,
+            (uintptr_t)args.r_arrive};
         auto it = vgraphs.find(key);
         if (it == vgraphs.end()) {
             const uint64_t l0 = g_launches.load();

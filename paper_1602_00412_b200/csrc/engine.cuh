@@ -90,6 +90,8 @@ class Engine {
     double* h_scal = nullptr;  // pinned mirror
     int* h_err = nullptr;
     int verify_blocks = 0;
+    int* varrive = nullptr;  // arrival counters of the kernel-sequence verifier's long-row pieces
+    int64_t varrive_cap = 0;
     int verify_cluster = 0;  // > 0: the verifier is one cluster of this many CTAs (no grid barrier)
     int vg_blocks = 0;       // column blocks of the kernel-sequence verifier
     // SFDG_VERIFY_MODE=graph: the kernel-sequence verifier (concurrent across flushes). Off by
@@ -102,7 +104,7 @@ class Engine {
     cudaEvent_t ev_v0 = nullptr, ev_v1 = nullptr;
     // true when this flush's verification runs as the kernel sequence (concurrent-safe);
     // the persistent kernels (skewed columns, or opted in) must be serialised by the caller
-    bool verify_as_graph() const { return use_vgraph && plan_c.host_long == 0; }
+    bool verify_as_graph() const { return use_vgraph; }
     // adaptive orthonormalisation schedule (simultaneous_iteration)
     bool adaptive = true;   // SFDG_ORTH_EVERY_SWEEP=1 forces the reference schedule
     int orth_interval = 1;  // sweeps per CholeskyQR2
@@ -150,7 +152,7 @@ class Engine {
         uint64_t kernels = 0;
     };
     std::map<std::vector<uintptr_t>, GraphEntry> graphs;
-    std::map<std::array<uintptr_t, 18>, GraphEntry> vgraphs;  // kernel-sequence verifier graphs
+    std::map<std::array<uintptr_t, 37>, GraphEntry> vgraphs;  // kernel-sequence verifier graphs
     bool use_graphs = true;  // SFDG_GRAPHS=0 disables
     // randsvd.cpp:18-51: Z (m x lp) left in Y.
     void simultaneous_iteration(int k, const PowerCfg& cfg);

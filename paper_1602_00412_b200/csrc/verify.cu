@@ -478,9 +478,10 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
 
 
 // ---- the verifier as a kernel sequence (no persistent grid) -----------------------------
-// One power step = three kernels: vg_rows (u = A' x over every row, all SMs), vg_cols (y over
-// every column, the partials of the next t = B' y and of |y|^2 per block), vg_reduce (one
-// block: fixed-order totals, the accept / reject / continue decision, next t). Kernel
+// One power step = two or three kernels: vg_rows (the decision on the previous pass, the next
+// t = B' x, and u = A' x over every row, all SMs), vg_pieces (skewed columns only: the long
+// columns' pieces), vg_cols (y over every column, the partials of the next t and of |y|^2 per
+// block). Kernel
 // boundaries replace the grid barriers, so nothing spins and verifications of different
 // flushes overlap freely (no serialisation); the whole sequence for a given step count is
 // captured once as a CUDA graph. Per column / row the arithmetic is the persistent kernel's
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
 struct VState {
     double scale, log_mag, xscale;
     int done, verdict, step, steps;
+    double lm[2];  // log magnitude after pass k at lm[k & 1] (pass -1: 0)
 };
 
 constexpr int kGRowsThreads = 256;
@@ -504,39 +506,168 @@ __global__ void vg_setup_kernel(VState* st, double scale, int steps) {
     st->verdict = -1;
     st->step = 0;
     st->steps = steps;
+    st->lm[0] = st->lm[1] = 0.0;
 }
 
-// u = A' (x xscale): four rows per warp in flight, grid-stride over all rows
-__global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, const VState* __restrict__ st, int step) {
-    pdl_entry();
-    if (st->done) return;
-    const double* x = step == 0 ? a.x0 : a.ybuf + (size_t)((step - 1) & 1) * a.d;
-    const double xscale = st->xscale;
+// The accept / reject / continue decision after pass s - 1 (s = 0: after the x0 pass), from the
+// per-block |.|^2 partials of that pass (shrink.cpp:88-99 / la_core.cpp:177-186). Run by warp 0
+// of every block of a launch: each sums the partials in the same fixed order, so all blocks take
+// the same decision without a grid barrier; block 0 commits it to the state. Returns 1 to
+// continue, with the scale of the next x in *xs.
+__device__ int vg_decide(const VerifyArgs& a, VState* st, int s, int nblk, double* xs) {
     const int lane = threadIdx.x & 31;
+    if (*((volatile int*)&st->done)) return 0;
+    double tot = 0.0;
+    for (int b = lane; b < nblk; b += 32) tot += __ldcg(a.part + b);
+    tot = warp_sum(tot);
+    const bool commit = blockIdx.x == 0 && lane == 0;
+    if (s == 0) {
+        if (!(tot > 0.0)) {
+            if (commit) {
+                atomicOr(a.err, ERR_RNG_U1_ZERO);  // all-zero draw: would need a redraw
+                st->done = 1;
+                st->verdict = 0;
+            }
+            return 0;
+        }
+        *xs = 1.0 / sqrt(tot);
+        return 1;
+    }
+    if (*((volatile int*)a.err) & ERR_NONFINITE_VERIFY) {
+        if (commit) {
+            st->verdict = 0;
+            st->done = 1;
+        }
+        return 0;
+    }
+    if (tot == 0.0) {  // iterate annihilated (shrink.cpp:92)
+        if (commit) {
+            st->verdict = 1;
+            st->done = 1;
+        }
+        return 0;
+    }
+    const double nrm = sqrt(tot);
+    const double lm = st->lm[s & 1] + log(nrm);
+    if (commit) {
+        st->lm[(s - 1) & 1] = lm;
+        st->log_mag = lm;
+        st->step = s;
+    }
+    if (lm > 0.0 && nrm >= 1.0) {
+        if (commit) {
+            st->verdict = 0;
+            st->done = 1;
+        }
+        return 0;
+    }
+    *xs = 1.0 / nrm;
+    return 1;
+}
+
+// Step `step`: the decision after the previous pass (vg_decide), t = B' x for this pass from the
+// previous pass's block partials (entry j by warp j % 8 of block j / 8), and u = A' (x xscale):
+// long-row pieces first (warp per piece, the last piece of a row sums them in piece order), then
+// the short rows longest first, eight lanes per row with four entries each in flight.
+__global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VState* st, int step, int nblk) {
+    pdl_entry();
+    __shared__ double s_xs;
+    __shared__ int s_go;
+    if (threadIdx.x < 32) {
+        double xs = 0.0;
+        const int go = vg_decide(a, st, step, nblk, &xs);
+        if (threadIdx.x == 0) {
+            s_go = go;
+            s_xs = xs;
+        }
+    }
+    __syncthreads();
+    if (!s_go) return;
+    const double xscale = s_xs;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int L = a.ell;
+    {
+        const int j = blockIdx.x * (kGRowsThreads / 32) + wib;
+        if (j < L) {
+            double sacc = 0.0;
+            for (int b = lane; b < nblk; b += 32) sacc += __ldcg(a.tpart + (size_t)b * L + j);
+            sacc = warp_sum(sacc);
+            if (lane == 0) a.t[j] = sacc * xscale;
+        }
+    }
+    const double* x = step == 0 ? a.x0 : a.ybuf + (size_t)((step - 1) & 1) * a.d;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t rb = gw; rb < a.m; rb += 4 * nw) {
-        int k0[4], k1[4];
-        int len = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int64_t r = rb + q * nw;
-            k0[q] = r < a.m ? a.row_ptr[r] : 0;
-            k1[q] = r < a.m ? a.row_ptr[r + 1] : 0;
-            len = max(len, k1[q] - k0[q]);
-        }
+    int np = 0, ns = (int)a.m;
+    if (a.r_counts) {
+        np = a.r_counts[1];
+        ns = a.r_counts[2];
+    }
+    for (int64_t p = gw; p < np; p += nw) {
+        const int kb = a.r_piece_beg[p], ke = a.r_piece_end[p];
         double sp[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int off = lane; off < len; off += 32) {
+        for (int k = kb + lane; k < ke; k += 128) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int k = k0[q] + off;
-                if (k < k1[q]) sp[q] = fma(a.val[k], __ldcg(x + a.col[k]) * xscale, sp[q]);
+            for (int u = 0; u < 4; ++u)
+                if (k + 32 * u < ke) sp[u] = fma(a.val[k + 32 * u], __ldcg(x + a.col[k + 32 * u]) * xscale, sp[u]);
+        }
+        const double t = warp_sum((sp[0] + sp[1]) + (sp[2] + sp[3]));
+        if (lane == 0) a.r_part[p] = t;
+        __threadfence();
+        const int li = a.r_piece_li[p];
+        const int nl = a.r_counts[0];
+        const int first = a.r_long_first[li], last = li + 1 < nl ? a.r_long_first[li + 1] : np;
+        int old = 0;
+        if (lane == 0) old = atomicAdd(a.r_arrive + li, 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == last - first - 1) {  // every piece of this row is written: sum them in order
+            __threadfence();
+            if (lane == 0) {
+                double tot = 0.0;
+                for (int q = first; q < last; ++q) tot += __ldcg(a.r_part + q);
+                a.u[a.r_long_rows[li]] = tot;
+                a.r_arrive[li] = 0;  // ready for the next launch
             }
         }
-        const double tot = warp_sum4(sp);
-        const int q = lane >> 3;
-        const int64_t r = rb + q * nw;
-        if ((lane & 7) == 0 && r < a.m) a.u[r] = tot;
+    }
+    const int sub = lane & 7;
+    const int64_t g0 = gw * 4 + (lane >> 3), ng = nw * 4;
+    for (int64_t gi = g0; gi < ns; gi += ng) {
+        const int r = a.r_counts ? a.r_order[gi] : (int)gi;
+        const int kb = a.row_ptr[r], ke = a.row_ptr[r + 1];
+        double sp[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = kb + sub; k < ke; k += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k + 8 * u < ke) sp[u] = fma(a.val[k + 8 * u], __ldcg(x + a.col[k + 8 * u]) * xscale, sp[u]);
+        }
+        double t = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        if (sub == 0) a.u[r] = t;
+    }
+}
+
+// long-column pieces (skewed columns): lpart[p] = sum of piece p's entries against u, warp per
+// piece over the whole grid (the persistent kernel's phase B0)
+__global__ void __launch_bounds__(kGRowsThreads) vg_pieces_kernel(VerifyArgs a, const VState* __restrict__ st) {
+    pdl_entry();
+    if (st->done) return;
+    const int lane = threadIdx.x & 31;
+    const int np = a.counts[1];
+    const int gw = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int tw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+    for (int p = gw; p < np; p += tw) {
+        const int kb = a.piece_beg[p], ke = a.piece_end[p];
+        double sp[4] = {0.0, 0.0, 0.0, 0.0};  // four gathers per lane in flight
+        for (int k = kb + lane; k < ke; k += 128) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k + 32 * u < ke) sp[u] = fma(a.cval[k + 32 * u], __ldcg(a.u + a.row_idx[k + 32 * u]), sp[u]);
+        }
+        const double t = warp_sum((sp[0] + sp[1]) + (sp[2] + sp[3]));
+        if (lane == 0) a.lpart[p] = t;
     }
 }
 
@@ -547,10 +678,54 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
     __shared__ double tloc[256];
     __shared__ double wpart[kGColsWarps][257];
     if (st->done) return;
+    __shared__ int64_t s_rng[4];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int L = a.ell;
-    const int64_t cper = (a.d + gridDim.x - 1) / gridDim.x;
-    const int64_t c0 = blockIdx.x * cper, c1 = min((int64_t)a.d, c0 + cper);
+    const bool lng = !INIT && a.has_long;
+    if (threadIdx.x == 0) {
+        // cost-balanced column range (a.ccost) or equal counts; then this block's long columns,
+        // a contiguous range of the ascending long-column list
+        int64_t c0 = 0, c1 = 0;
+        if (a.ccost) {
+            const int64_t tc = a.ccost[a.d];
+            auto cfind = [&](int64_t target) {
+                int64_t lo = 0, hi = a.d;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (a.ccost[mid] < target) lo = mid + 1;
+                    else hi = mid;
+                }
+                return lo;
+            };
+            c0 = cfind(tc * blockIdx.x / gridDim.x);
+            c1 = blockIdx.x + 1 == gridDim.x ? a.d : cfind(tc * (blockIdx.x + 1) / gridDim.x);
+        } else {
+            const int64_t cper = (a.d + gridDim.x - 1) / gridDim.x;
+            c0 = min((int64_t)a.d, (int64_t)blockIdx.x * cper);
+            c1 = min((int64_t)a.d, c0 + cper);
+        }
+        int64_t lo = 0, hi = 0;
+        if (lng) {
+            const int nl = a.counts[0];
+            auto lfind = [&](int64_t c) {
+                int l = 0, h = nl;
+                while (l < h) {
+                    const int mid = (l + h) >> 1;
+                    if (a.long_cols[mid] < c) l = mid + 1;
+                    else h = mid;
+                }
+                return (int64_t)l;
+            };
+            lo = lfind(c0);
+            hi = lfind(c1);
+        }
+        s_rng[0] = c0;
+        s_rng[1] = c1;
+        s_rng[2] = lo;
+        s_rng[3] = hi;
+    }
+    __syncthreads();
+    const int64_t c0 = s_rng[0], c1 = s_rng[1], lc0 = s_rng[2], lc1 = s_rng[3];
     double* y = a.ybuf + (size_t)(step & 1) * a.d;
     if (!INIT)
         for (int j = threadIdx.x; j < L; j += kGColsThreads) tloc[j] = __ldcg(a.t + j);
@@ -582,24 +757,30 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
             continue;
         }
         int k0[4], k1[4];
+        bool own[4];
         int len = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int64_t c = cb + q * kGColsWarps;
             k0[q] = c < c1 ? a.col_ptr[c] : 0;
             k1[q] = c < c1 ? a.col_ptr[c + 1] : 0;
+            own[q] = c < c1;
+            if (lng && k1[q] - k0[q] > 2 * a.piece) {  // long: its pieces, below
+                k1[q] = k0[q];
+                own[q] = false;
+            }
             len = max(len, k1[q] - k0[q]);
         }
         double brow[4][Q];
         double dp[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const int64_t c = cb + q * kGColsWarps;
             dp[q] = 0.0;
+            const int64_t c = cb + q * kGColsWarps;
 #pragma unroll
             for (int w = 0; w < Q; ++w) {
                 const int j = lane + 32 * w;
-                brow[q][w] = (c < c1 && j < L) ? a.bt[c * a.ldb + j] : 0.0;
+                brow[q][w] = (own[q] && j < L) ? a.bt[c * a.ldb + j] : 0.0;
                 dp[q] = fma(-brow[q][w], tl[w], dp[q]);
             }
         }
@@ -615,13 +796,36 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
         for (int q = 0; q < 4; ++q) {
             const int64_t c = cb + q * kGColsWarps;
             const double yc = scale * __shfl_sync(0xffffffffu, tot, 8 * q);  // shrink.cpp:124
-            if (c < c1) {
+            if (own[q]) {
                 if (!isfinite(yc)) bad = true;
                 if (lane == 0) y[c] = yc;
                 nsq = fma(yc, yc, nsq);
 #pragma unroll
                 for (int w = 0; w < Q; ++w) tn[w] = fma(brow[q][w], yc, tn[w]);
             }
+        }
+    }
+    // long columns of this block: warp per column, its piece partials (vg_pieces) summed by lanes
+    if (lng) {
+        const int nl = a.counts[0], npc = a.counts[1];
+        for (int64_t li = lc0 + wib; li < lc1; li += kGColsWarps) {
+            const int64_t c = a.long_cols[li];
+            const int first = a.long_first[li], last = li + 1 < nl ? a.long_first[li + 1] : npc;
+            double dpv = 0.0;
+            for (int p = first + lane; p < last; p += 32) dpv += __ldcg(a.lpart + p);
+            double brow[Q];
+#pragma unroll
+            for (int w = 0; w < Q; ++w) {
+                const int j = lane + 32 * w;
+                brow[w] = j < L ? a.bt[c * a.ldb + j] : 0.0;
+                dpv = fma(-brow[w], tl[w], dpv);
+            }
+            const double yc = scale * warp_sum(dpv);
+            if (!isfinite(yc)) bad = true;
+            if (lane == 0) y[c] = yc;
+            nsq = fma(yc, yc, nsq);
+#pragma unroll
+            for (int w = 0; w < Q; ++w) tn[w] = fma(brow[w], yc, tn[w]);
         }
     }
     if (bad) atomicOr(a.err, ERR_NONFINITE_VERIFY);
@@ -641,68 +845,20 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
     }
 }
 
-// one block: totals in fixed block order, the decision (shrink.cpp:88-99) and the next t
-__global__ void __launch_bounds__(512) vg_reduce_kernel(VerifyArgs a, VState* st, int step, int nblk) {
+// after the last pass: its decision, then the verdict (shrink.cpp:101)
+__global__ void vg_final_kernel(VerifyArgs a, VState* st, int nblk) {
     pdl_entry();
-    __shared__ int s_go;
-    if (st->done) return;
-    const int L = a.ell;
     if (threadIdx.x < 32) {
-        double sacc = 0.0;
-        for (int b = threadIdx.x; b < nblk; b += 32) sacc += __ldcg(a.part + b);
-        sacc = warp_sum(sacc);
+        double xs = 0.0;
+        vg_decide(a, st, st->steps, nblk, &xs);
         if (threadIdx.x == 0) {
-            int go = 1;
-            if (step < 0) {  // after the x0 pass (la_core.cpp:177-186)
-                if (!(sacc > 0.0)) {
-                    atomicOr(a.err, ERR_RNG_U1_ZERO);  // all-zero draw: would need a redraw
-                    st->done = 1;
-                    st->verdict = 0;
-                    go = 0;
-                } else {
-                    st->xscale = 1.0 / sqrt(sacc);
-                }
-            } else {
-                if (*((volatile int*)a.err) & ERR_NONFINITE_VERIFY) {
-                    st->verdict = 0;
-                    st->done = 1;
-                    go = 0;
-                } else if (sacc == 0.0) {
-                    st->verdict = 1;
-                    st->done = 1;
-                    go = 0;
-                } else {
-                    const double nrm = sqrt(sacc);
-                    st->log_mag += log(nrm);
-                    st->step = step + 1;
-                    if (st->log_mag > 0.0 && nrm >= 1.0) {
-                        st->verdict = 0;
-                        st->done = 1;
-                        go = 0;
-                    } else {
-                        st->xscale = 1.0 / nrm;
-                    }
-                }
-            }
-            s_go = go;
+            __threadfence_block();
+            const int verdict = st->verdict >= 0 ? st->verdict : (st->log_mag <= 0.0 ? 1 : 0);
+            a.out[0] = (double)verdict;
+            a.out[1] = st->log_mag;
+            a.out[2] = (double)st->step;
         }
     }
-    __syncthreads();
-    if (!s_go) return;
-    const double xscale = st->xscale;
-    for (int j = threadIdx.x; j < L; j += blockDim.x) {
-        double sacc = 0.0;
-        for (int b = 0; b < nblk; ++b) sacc += __ldcg(a.tpart + (size_t)b * L + j);
-        a.t[j] = sacc * xscale;
-    }
-}
-
-__global__ void vg_final_kernel(VerifyArgs a, const VState* st) {
-    pdl_entry();
-    const int verdict = st->verdict >= 0 ? st->verdict : (st->log_mag <= 0.0 ? 1 : 0);
-    a.out[0] = (double)verdict;
-    a.out[1] = st->log_mag;
-    a.out[2] = (double)st->step;
 }
 
 typedef void (*VgColsFn)(VerifyArgs, const VState*, int);
@@ -884,15 +1040,15 @@ size_t verify_state_bytes() { return sizeof(VState); }
 
 void verify_sequence(const VerifyArgs& a, void* state, int nblk, int sms, cudaStream_t st) {
     VState* s = static_cast<VState*>(state);
-    const unsigned rgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(8 * sms, (a.m + 31) / 32));
+    const unsigned rgrid = (unsigned)std::max<int64_t>((a.ell + 7) / 8, std::min<int64_t>(8 * sms, (a.m + 31) / 32));
+    const unsigned pgrid = (unsigned)(4 * sms);  // grid-stride over the pieces (count read on the device)
     LAUNCH(vg_cols_fn<true>(a.ell), nblk, kGColsThreads, 0, st, a, s, 0);
-    LAUNCH(vg_reduce_kernel, 1, 512, 0, st, a, s, -1, nblk);
     for (int step = 0; step < a.steps; ++step) {
-        LAUNCH(vg_rows_kernel, rgrid, kGRowsThreads, 0, st, a, s, step);
+        LAUNCH(vg_rows_kernel, rgrid, kGRowsThreads, 0, st, a, s, step, nblk);
+        if (a.has_long) LAUNCH(vg_pieces_kernel, pgrid, kGRowsThreads, 0, st, a, s);
         LAUNCH(vg_cols_fn<false>(a.ell), nblk, kGColsThreads, 0, st, a, s, step);
-        LAUNCH(vg_reduce_kernel, 1, 512, 0, st, a, s, step, nblk);
     }
-    LAUNCH(vg_final_kernel, 1, 1, 0, st, a, s);
+    LAUNCH(vg_final_kernel, 1, 32, 0, st, a, s, nblk);
 }
 
 void verify_setup(void* state, double scale, int steps, cudaStream_t st) {

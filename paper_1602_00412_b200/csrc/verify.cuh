@@ -46,6 +46,18 @@ struct VerifyArgs {
     const int* counts;      // [n_long, n_pieces] (device)
     double* lpart;          // n_pieces partial sums
     const int64_t* ccost;   // d + 1 column-cost prefix (verify_column_costs) or null: equal counts
+    // CSR work plan of the kernel-sequence verifier's u = A' x (the SpMM's row SegPlan): pieces of
+    // the long rows, summed in piece order by the piece that finishes last, then the short rows
+    // longest first. Null r_counts: every row in natural order (no pieces).
+    const int* r_counts;    // [nlong, npieces, nshort] (device)
+    const int* r_piece_beg;
+    const int* r_piece_end;
+    const int* r_piece_li;
+    const int* r_long_rows;
+    const int* r_long_first;
+    const int* r_order;
+    double* r_part;         // npieces partial sums
+    int* r_arrive;          // nlong arrival counters (zero between launches: self-resetting)
 };
 
 class Scratch;
@@ -63,8 +75,8 @@ void verify_launch(const VerifyArgs& args, int nblocks, int cluster, cudaStream_
 // The verifier as a kernel sequence (three kernels per power step, no persistent grid; see
 // verify.cu). verify_setup writes the per-call scalars (2 / Delta, steps) into `state`
 // (verify_state_bytes() of device memory); verify_sequence enqueues the steps (the caller
-// captures it once per step count as a CUDA graph). tpart: nblk * ell, part: nblk. Columns
-// must have no long-column pieces (has_long == 0).
+// captures it once per step count as a CUDA graph). tpart: nblk * ell, part: nblk. Long columns
+// (has_long) are summed from their pieces (one more kernel per step).
 int verify_graph_blocks(int device, int64_t d);
 size_t verify_state_bytes();
 void verify_setup(void* state, double scale, int steps, cudaStream_t st);

@@ -634,11 +634,15 @@ def test_covariance_bound_random_streams(oracle):
 
 
 # ---------------------------------------------------------------- BASELINE families at reduced d
+@pytest.mark.parametrize("mode", ["grid", "graph"])
 @pytest.mark.parametrize("family,d,ell,rows", [("c3", 1500, 40, 3000), ("c4", 1200, 32, 2400), ("c5", 2000, 48, 4000),
                                                ("c2", 3000, 60, 6000)])
-def test_baseline_family_streams_vs_oracle(oracle, family, d, ell, rows):
+def test_baseline_family_streams_vs_oracle(oracle, family, d, ell, rows, mode, monkeypatch):
     """Same generator family (Zipf / power-law columns, skewed row lengths, centred ratings,
-    planted signal) at a d the CPU oracle finishes in seconds; two full flushes each."""
+    planted signal) at a d the CPU oracle finishes in seconds; two full flushes each. Both
+    verifiers: the persistent grid kernel and the kernel sequence (the default for large B';
+    c3 here has rows and columns longer than 2 pieces, so both of its piece paths run)."""
+    monkeypatch.setenv("SFDG_VERIFY_MODE", mode)
     cfg = S.StreamConfig(family, rows, d, ell, 7)
     rp, cs, vs = S.generate(cfg, (0, rows))
     b, st = sketch_gpu(rp, cs, vs, d, ell, 11)
