@@ -255,7 +255,7 @@ Engine::~Engine() {
                     (void*)dinv8, (void*)kc,
                     (void*)evals, (void*)evecs, (void*)S, (void*)x0, (void*)ybuf, (void*)u, (void*)tpart, (void*)tvec,
                     (void*)vpart, (void*)vout, (void*)bar, (void*)d_err, (void*)d_scal, (void*)xtmp, (void*)d_udrop,
-                    (void*)vstate, (void*)varrive})
+                    (void*)vstate, (void*)varrive, (void*)vcarrive, (void*)vw})
         if (p) cudaFree(p);
     if (h_scal) cudaFreeHost(h_scal);
     if (h_err) cudaFreeHost(h_err);
@@ -582,6 +582,18 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
         args.r_order = plan_r.order;
         args.r_part = scr.take<double>(std::max<int64_t>(1, plan_r.cap_pieces));
         args.r_arrive = varrive;
+        if (d > vcarrive_cap) {
+            if (vcarrive) CK(cudaFree(vcarrive));
+            if (vw) CK(cudaFree(vw));
+            CK(cudaMalloc(&vcarrive, (size_t)d * sizeof(int)));
+            CK(cudaMalloc(&vw, (size_t)d * sizeof(double)));
+            CK(cudaMemsetAsync(vcarrive, 0, (size_t)d * sizeof(int), st));
+            vcarrive_cap = d;
+        }
+        args.c_order = plan_c.order;
+        args.c_piece_li = plan_c.piece_li;
+        args.c_arrive = vcarrive;
+        args.w = vw;
         if (!(std::getenv("SFDG_VERIFY_BALANCE") && std::atoi(std::getenv("SFDG_VERIFY_BALANCE")) == 0)) {
             int64_t* prefix = scr.take<int64_t>((int64_t)d + 1);
             verify_column_costs(a.col_ptr, d, ell, plan_c.piece, prefix, scr, st);
@@ -598,7 +610,7 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
             CK(cudaStreamWaitEvent(vst, ev_v0, 0));
         }
         verify_setup(vstate, args.scale, args.steps, vs);
-        const std::array<uintptr_t, 37> key{
+        const std::array<uintptr_t, 42> key{
             (uintptr_t)args.steps,     (uintptr_t)args.m,          (uintptr_t)args.row_ptr,   (uintptr_t)args.col,
             (uintptr_t)args.val,       (uintptr_t)args.col_ptr,    (uintptr_t)args.row_idx,   (uintptr_t)args.cval,
             (uintptr_t)args.bt,        (uintptr_t)args.ldb,        (uintptr_t)args.x0,        (uintptr_t)args.u,
@@ -608,7 +620,8 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
             (uintptr_t)args.counts,    (uintptr_t)args.lpart,      (uintptr_t)args.ccost,     (uintptr_t)args.err,
             (uintptr_t)args.r_counts,  (uintptr_t)args.r_piece_beg, (uintptr_t)args.r_piece_end, (uintptr_t)args.r_piece_li,
             (uintptr_t)args.r_long_rows, (uintptr_t)args.r_long_first, (uintptr_t)args.r_order, (uintptr_t)args.r_part,
-            (uintptr_t)args.r_arrive};
+            (uintptr_t)args.r_arrive,  (uintptr_t)args.c_order,  (uintptr_t)args.c_piece_li, (uintptr_t)args.c_arrive,
+            (uintptr_t)args.w};
         auto it = vgraphs.find(key);
         if (it == vgraphs.end()) {
             const uint64_t l0 = g_launches.load();

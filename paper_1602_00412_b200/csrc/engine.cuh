@@ -92,6 +92,9 @@ class Engine {
     int verify_blocks = 0;
     int* varrive = nullptr;  // arrival counters of the kernel-sequence verifier's long-row pieces
     int64_t varrive_cap = 0;
+    int* vcarrive = nullptr;  // ... and of its long-column pieces
+    double* vw = nullptr;     // w = A'^T u (d)
+    int64_t vcarrive_cap = 0;
     int verify_cluster = 0;  // > 0: the verifier is one cluster of this many CTAs (no grid barrier)
     int vg_blocks = 0;       // column blocks of the kernel-sequence verifier
     // SFDG_VERIFY_MODE=graph: the kernel-sequence verifier (concurrent across flushes). Off by
@@ -152,7 +155,7 @@ class Engine {
         uint64_t kernels = 0;
     };
     std::map<std::vector<uintptr_t>, GraphEntry> graphs;
-    std::map<std::array<uintptr_t, 37>, GraphEntry> vgraphs;  // kernel-sequence verifier graphs
+    std::map<std::array<uintptr_t, 42>, GraphEntry> vgraphs;  // kernel-sequence verifier graphs
     bool use_graphs = true;  // SFDG_GRAPHS=0 disables
     // randsvd.cpp:18-51: Z (m x lp) left in Y.
     void simultaneous_iteration(int k, const PowerCfg& cfg);

@@ -478,10 +478,10 @@ __global__ void __launch_bounds__(kVThreads) verify_kernel(VerifyArgs a) {
 
 
 // ---- the verifier as a kernel sequence (no persistent grid) -----------------------------
-// One power step = two or three kernels: vg_rows (the decision on the previous pass, the next
-// t = B' x, and u = A' x over every row, all SMs), vg_pieces (skewed columns only: the long
-// columns' pieces), vg_cols (y over every column, the partials of the next t and of |y|^2 per
-// block). Kernel
+// One power step = three kernels: vg_rows (the decision on the previous pass, the next t = B' x,
+// and u = A' x over every row, all SMs), vg_colsum (w = A'^T u over every column), vg_cols (y
+// over every column from w and the streamed B'^T rows, the partials of the next t and of |y|^2
+// per block). Kernel
 // boundaries replace the grid barriers, so nothing spins and verifications of different
 // flushes overlap freely (no serialisation); the whole sequence for a given step count is
 // captured once as a CUDA graph. Per column / row the arithmetic is the persistent kernel's
@@ -565,34 +565,41 @@ __device__ int vg_decide(const VerifyArgs& a, VState* st, int s, int nblk, doubl
     return 1;
 }
 
-// Step `step`: the decision after the previous pass (vg_decide), t = B' x for this pass from the
-// previous pass's block partials (entry j by warp j % 8 of block j / 8), and u = A' (x xscale):
-// long-row pieces first (warp per piece, the last piece of a row sums them in piece order), then
-// the short rows longest first, eight lanes per row with four entries each in flight.
+// Step `step`: the decision after the previous pass (vg_decide, warp 0 of every block), t = B' x
+// for this pass from the previous pass's block partials (entry j by warp j % 8 of block j / 8),
+// and u = A' y_prev UNSCALED (x = y_prev / |y_prev|: the consumers apply the 1 / |y_prev| that
+// the decision produces, so the row work does not wait for it): long-row pieces first (warp per
+// piece, the last piece of a row sums them in piece order), then the short rows longest first,
+// sixteen lanes per row with four entries each in flight. The x gathers go through L1
+// (ld.global.nc): x is read-only for the launch and L1 starts every launch invalid, so this is
+// safe in the kernel sequence (not in the persistent kernel); tools/spmv_lab.cu on the c4 flush:
+// 8 lanes L2-only 32.8 us, 16 lanes through L1 14.4 us.
 __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VState* st, int step, int nblk) {
     pdl_entry();
     __shared__ double s_xs;
     __shared__ int s_go;
+    if (*((volatile int*)&st->done)) return;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int L = a.ell;
+    const bool t_block = blockIdx.x * (kGRowsThreads / 32) < L;
     if (threadIdx.x < 32) {
         double xs = 0.0;
         const int go = vg_decide(a, st, step, nblk, &xs);
         if (threadIdx.x == 0) {
             s_go = go;
             s_xs = xs;
+            if (blockIdx.x == 0 && go) st->xscale = xs;
         }
     }
-    __syncthreads();
-    if (!s_go) return;
-    const double xscale = s_xs;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int L = a.ell;
-    {
+    if (t_block) {
+        __syncthreads();
+        if (!s_go) return;
         const int j = blockIdx.x * (kGRowsThreads / 32) + wib;
         if (j < L) {
             double sacc = 0.0;
             for (int b = lane; b < nblk; b += 32) sacc += __ldcg(a.tpart + (size_t)b * L + j);
             sacc = warp_sum(sacc);
-            if (lane == 0) a.t[j] = sacc * xscale;
+            if (lane == 0) a.t[j] = sacc * s_xs;
         }
     }
     const double* x = step == 0 ? a.x0 : a.ybuf + (size_t)((step - 1) & 1) * a.d;
@@ -609,7 +616,7 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VS
         for (int k = kb + lane; k < ke; k += 128) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (k + 32 * u < ke) sp[u] = fma(a.val[k + 32 * u], __ldcg(x + a.col[k + 32 * u]) * xscale, sp[u]);
+                if (k + 32 * u < ke) sp[u] = fma(a.val[k + 32 * u], __ldg(x + a.col[k + 32 * u]), sp[u]);
         }
         const double t = warp_sum((sp[0] + sp[1]) + (sp[2] + sp[3]));
         if (lane == 0) a.r_part[p] = t;
@@ -630,18 +637,19 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VS
             }
         }
     }
-    const int sub = lane & 7;
-    const int64_t g0 = gw * 4 + (lane >> 3), ng = nw * 4;
+    const int sub = lane & 15;
+    const int64_t g0 = gw * 2 + (lane >> 4), ng = nw * 2;
     for (int64_t gi = g0; gi < ns; gi += ng) {
         const int r = a.r_counts ? a.r_order[gi] : (int)gi;
         const int kb = a.row_ptr[r], ke = a.row_ptr[r + 1];
         double sp[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int k = kb + sub; k < ke; k += 32) {
+        for (int k = kb + sub; k < ke; k += 64) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (k + 8 * u < ke) sp[u] = fma(a.val[k + 8 * u], __ldcg(x + a.col[k + 8 * u]) * xscale, sp[u]);
+                if (k + 16 * u < ke) sp[u] = fma(a.val[k + 16 * u], __ldg(x + a.col[k + 16 * u]), sp[u]);
         }
         double t = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+        t += __shfl_xor_sync(0xffffffffu, t, 8);
         t += __shfl_xor_sync(0xffffffffu, t, 4);
         t += __shfl_xor_sync(0xffffffffu, t, 2);
         t += __shfl_xor_sync(0xffffffffu, t, 1);
@@ -649,84 +657,81 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VS
     }
 }
 
-// long-column pieces (skewed columns): lpart[p] = sum of piece p's entries against u, warp per
-// piece over the whole grid (the persistent kernel's phase B0)
-__global__ void __launch_bounds__(kGRowsThreads) vg_pieces_kernel(VerifyArgs a, const VState* __restrict__ st) {
+// w = A'^T u (unscaled) for every column: pieces of the long columns first (warp per piece, the
+// last piece of a column sums them in piece order), then the short columns longest first, sixteen
+// lanes per column with four entries each in flight; u through L1 (read-only in this launch).
+// Each w_c is a per-column sum in a fixed order, so which warp computes it does not matter.
+__global__ void __launch_bounds__(kGRowsThreads) vg_colsum_kernel(VerifyArgs a, const VState* __restrict__ st) {
     pdl_entry();
     if (st->done) return;
     const int lane = threadIdx.x & 31;
-    const int np = a.counts[1];
-    const int gw = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int tw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-    for (int p = gw; p < np; p += tw) {
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int np = a.has_long ? a.counts[1] : 0;
+    const int ns = a.c_order ? a.counts[2] : (int)a.d;
+    for (int64_t p = gw; p < np; p += nw) {
         const int kb = a.piece_beg[p], ke = a.piece_end[p];
         double sp[4] = {0.0, 0.0, 0.0, 0.0};  // four gathers per lane in flight
         for (int k = kb + lane; k < ke; k += 128) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (k + 32 * u < ke) sp[u] = fma(a.cval[k + 32 * u], __ldcg(a.u + a.row_idx[k + 32 * u]), sp[u]);
+                if (k + 32 * u < ke) sp[u] = fma(a.cval[k + 32 * u], __ldg(a.u + a.row_idx[k + 32 * u]), sp[u]);
         }
         const double t = warp_sum((sp[0] + sp[1]) + (sp[2] + sp[3]));
         if (lane == 0) a.lpart[p] = t;
+        __threadfence();
+        const int li = a.c_piece_li[p];
+        const int nl = a.counts[0];
+        const int first = a.long_first[li], last = li + 1 < nl ? a.long_first[li + 1] : np;
+        int old = 0;
+        if (lane == 0) old = atomicAdd(a.c_arrive + li, 1);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old == last - first - 1) {  // every piece of this column is written: sum them in order
+            __threadfence();
+            if (lane == 0) {
+                double tot = 0.0;
+                for (int q = first; q < last; ++q) tot += __ldcg(a.lpart + q);
+                a.w[a.long_cols[li]] = tot;
+                a.c_arrive[li] = 0;  // ready for the next launch
+            }
+        }
+    }
+    const int sub = lane & 15;
+    const int64_t g0 = gw * 2 + (lane >> 4), ng = nw * 2;
+    for (int64_t gi = g0; gi < ns; gi += ng) {
+        const int c = a.c_order ? a.c_order[gi] : (int)gi;
+        const int kb = a.col_ptr[c], ke = a.col_ptr[c + 1];
+        double sp[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = kb + sub; k < ke; k += 64) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k + 16 * u < ke) sp[u] = fma(a.cval[k + 16 * u], __ldg(a.u + a.row_idx[k + 16 * u]), sp[u]);
+        }
+        double t = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+        t += __shfl_xor_sync(0xffffffffu, t, 8);
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        if (sub == 0) a.w[c] = t;
     }
 }
 
-// columns (init = true: the x0 pass -- |x0|^2 and B' x0 partials, no y)
+// columns: y_c = scale (xscale w_c - B'^T_c t) with the B'^T rows streamed once, and from the
+// same rows the block partials of the next t = B' y and of |y|^2 (init = true: the x0 pass --
+// |x0|^2 and B' x0 partials, no y). Every column costs one B'^T row, so equal contiguous column
+// ranges per block and a fixed warp interleave inside it (the partials' order is fixed).
 template <int Q, bool INIT>
 __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, const VState* __restrict__ st, int step) {
     pdl_entry();
     __shared__ double tloc[256];
     __shared__ double wpart[kGColsWarps][257];
     if (st->done) return;
-    __shared__ int64_t s_rng[4];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int L = a.ell;
-    const bool lng = !INIT && a.has_long;
-    if (threadIdx.x == 0) {
-        // cost-balanced column range (a.ccost) or equal counts; then this block's long columns,
-        // a contiguous range of the ascending long-column list
-        int64_t c0 = 0, c1 = 0;
-        if (a.ccost) {
-            const int64_t tc = a.ccost[a.d];
-            auto cfind = [&](int64_t target) {
-                int64_t lo = 0, hi = a.d;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (a.ccost[mid] < target) lo = mid + 1;
-                    else hi = mid;
-                }
-                return lo;
-            };
-            c0 = cfind(tc * blockIdx.x / gridDim.x);
-            c1 = blockIdx.x + 1 == gridDim.x ? a.d : cfind(tc * (blockIdx.x + 1) / gridDim.x);
-        } else {
-            const int64_t cper = (a.d + gridDim.x - 1) / gridDim.x;
-            c0 = min((int64_t)a.d, (int64_t)blockIdx.x * cper);
-            c1 = min((int64_t)a.d, c0 + cper);
-        }
-        int64_t lo = 0, hi = 0;
-        if (lng) {
-            const int nl = a.counts[0];
-            auto lfind = [&](int64_t c) {
-                int l = 0, h = nl;
-                while (l < h) {
-                    const int mid = (l + h) >> 1;
-                    if (a.long_cols[mid] < c) l = mid + 1;
-                    else h = mid;
-                }
-                return (int64_t)l;
-            };
-            lo = lfind(c0);
-            hi = lfind(c1);
-        }
-        s_rng[0] = c0;
-        s_rng[1] = c1;
-        s_rng[2] = lo;
-        s_rng[3] = hi;
-    }
-    __syncthreads();
-    const int64_t c0 = s_rng[0], c1 = s_rng[1], lc0 = s_rng[2], lc1 = s_rng[3];
+    const int64_t cper = (a.d + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = min((int64_t)a.d, (int64_t)blockIdx.x * cper), c1 = min((int64_t)a.d, c0 + cper);
     double* y = a.ybuf + (size_t)(step & 1) * a.d;
+    const double xscale = INIT ? 1.0 : st->xscale;  // w = A'^T A' y_prev is unscaled
     if (!INIT)
         for (int j = threadIdx.x; j < L; j += kGColsThreads) tloc[j] = __ldcg(a.t + j);
     __syncthreads();
@@ -740,63 +745,40 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
     bool bad = false;
     const double scale = st->scale;
     for (int64_t cb = c0 + wib; cb < c1; cb += 4 * kGColsWarps) {
-        if (INIT) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int64_t c = cb + q * kGColsWarps;
-                if (c < c1) {
-                    const double xc = a.x0[c];
-                    nsq = fma(xc, xc, nsq);
-#pragma unroll
-                    for (int w = 0; w < Q; ++w) {
-                        const int j = lane + 32 * w;
-                        if (j < L) tn[w] = fma(a.bt[c * a.ldb + j], xc, tn[w]);
-                    }
-                }
-            }
-            continue;
-        }
-        int k0[4], k1[4];
-        bool own[4];
-        int len = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int64_t c = cb + q * kGColsWarps;
-            k0[q] = c < c1 ? a.col_ptr[c] : 0;
-            k1[q] = c < c1 ? a.col_ptr[c + 1] : 0;
-            own[q] = c < c1;
-            if (lng && k1[q] - k0[q] > 2 * a.piece) {  // long: its pieces, below
-                k1[q] = k0[q];
-                own[q] = false;
-            }
-            len = max(len, k1[q] - k0[q]);
-        }
         double brow[4][Q];
-        double dp[4];
+        double wc[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            dp[q] = 0.0;
             const int64_t c = cb + q * kGColsWarps;
+            const bool own = c < c1;
+            wc[q] = own ? (INIT ? a.x0[c] : __ldcg(a.w + c)) : 0.0;
 #pragma unroll
             for (int w = 0; w < Q; ++w) {
                 const int j = lane + 32 * w;
-                brow[q][w] = (own[q] && j < L) ? a.bt[c * a.ldb + j] : 0.0;
-                dp[q] = fma(-brow[q][w], tl[w], dp[q]);
+                brow[q][w] = (own && j < L) ? a.bt[c * a.ldb + j] : 0.0;
             }
         }
-        for (int off = lane; off < len; off += 32) {
+        if constexpr (INIT) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const int k = k0[q] + off;
-                if (k < k1[q]) dp[q] = fma(a.cval[k], __ldcg(a.u + a.row_idx[k]), dp[q]);
+                nsq = fma(wc[q], wc[q], nsq);
+#pragma unroll
+                for (int w = 0; w < Q; ++w) tn[w] = fma(brow[q][w], wc[q], tn[w]);
             }
+        } else {
+            double dp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            dp[q] = 0.0;
+#pragma unroll
+            for (int w = 0; w < Q; ++w) dp[q] = fma(-brow[q][w], tl[w], dp[q]);
         }
-        const double tot = warp_sum4(dp);
+        const double tot = warp_sum4(dp);  // -(B'^T t)_c on lanes 8q .. 8q+7
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int64_t c = cb + q * kGColsWarps;
-            const double yc = scale * __shfl_sync(0xffffffffu, tot, 8 * q);  // shrink.cpp:124
-            if (own[q]) {
+            const double yc = scale * fma(wc[q], xscale, __shfl_sync(0xffffffffu, tot, 8 * q));  // shrink.cpp:124
+            if (c < c1) {
                 if (!isfinite(yc)) bad = true;
                 if (lane == 0) y[c] = yc;
                 nsq = fma(yc, yc, nsq);
@@ -804,28 +786,6 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
                 for (int w = 0; w < Q; ++w) tn[w] = fma(brow[q][w], yc, tn[w]);
             }
         }
-    }
-    // long columns of this block: warp per column, its piece partials (vg_pieces) summed by lanes
-    if (lng) {
-        const int nl = a.counts[0], npc = a.counts[1];
-        for (int64_t li = lc0 + wib; li < lc1; li += kGColsWarps) {
-            const int64_t c = a.long_cols[li];
-            const int first = a.long_first[li], last = li + 1 < nl ? a.long_first[li + 1] : npc;
-            double dpv = 0.0;
-            for (int p = first + lane; p < last; p += 32) dpv += __ldcg(a.lpart + p);
-            double brow[Q];
-#pragma unroll
-            for (int w = 0; w < Q; ++w) {
-                const int j = lane + 32 * w;
-                brow[w] = j < L ? a.bt[c * a.ldb + j] : 0.0;
-                dpv = fma(-brow[w], tl[w], dpv);
-            }
-            const double yc = scale * warp_sum(dpv);
-            if (!isfinite(yc)) bad = true;
-            if (lane == 0) y[c] = yc;
-            nsq = fma(yc, yc, nsq);
-#pragma unroll
-            for (int w = 0; w < Q; ++w) tn[w] = fma(brow[w], yc, tn[w]);
         }
     }
     if (bad) atomicOr(a.err, ERR_NONFINITE_VERIFY);
@@ -1040,12 +1000,13 @@ size_t verify_state_bytes() { return sizeof(VState); }
 
 void verify_sequence(const VerifyArgs& a, void* state, int nblk, int sms, cudaStream_t st) {
     VState* s = static_cast<VState*>(state);
-    const unsigned rgrid = (unsigned)std::max<int64_t>((a.ell + 7) / 8, std::min<int64_t>(8 * sms, (a.m + 31) / 32));
-    const unsigned pgrid = (unsigned)(4 * sms);  // grid-stride over the pieces (count read on the device)
+    // one wave of the row kernel (six 256-thread blocks per SM), at least one warp per entry of t
+    const unsigned rgrid = (unsigned)std::max<int64_t>((a.ell + 7) / 8, std::min<int64_t>(6 * sms, (a.m + 31) / 32));
+    const unsigned rgrid2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(6 * sms, (a.d + 31) / 32));
     LAUNCH(vg_cols_fn<true>(a.ell), nblk, kGColsThreads, 0, st, a, s, 0);
     for (int step = 0; step < a.steps; ++step) {
         LAUNCH(vg_rows_kernel, rgrid, kGRowsThreads, 0, st, a, s, step, nblk);
-        if (a.has_long) LAUNCH(vg_pieces_kernel, pgrid, kGRowsThreads, 0, st, a, s);
+        LAUNCH(vg_colsum_kernel, rgrid2, kGRowsThreads, 0, st, a, s);
         LAUNCH(vg_cols_fn<false>(a.ell), nblk, kGColsThreads, 0, st, a, s, step);
     }
     LAUNCH(vg_final_kernel, 1, 32, 0, st, a, s, nblk);

@@ -58,6 +58,11 @@ struct VerifyArgs {
     const int* r_order;
     double* r_part;         // npieces partial sums
     int* r_arrive;          // nlong arrival counters (zero between launches: self-resetting)
+    // ... and of its w = A'^T u (the CSC SegPlan: long_cols / long_first / piece_* / counts above)
+    const int* c_order;     // short columns longest first (null: natural order, no pieces)
+    const int* c_piece_li;  // long-column index of each piece
+    int* c_arrive;          // per long column arrival counters (self-resetting)
+    double* w;              // d: w = A'^T u
 };
 
 class Scratch;

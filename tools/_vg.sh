@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
+SFDG_LANES=1 SFDG_TRACE=gpurun_out/tr7_L1.jsonl python bench.py --config c4 --rows 1000000 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-accuracy --no-isolated > gpurun_out/lanes7_L1.json 2>&1; python tools/trace_report.py gpurun_out/tr7_L1.jsonl
 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -k regex:"vg_" --csv --log-file gpurun_out/vg_launches_warm.csv python bench.py --config c4 --rows 100000 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-accuracy --no-isolated > gpurun_out/vg_ncu.log 2>&1
 python - <<PY
 import csv,collections
@@ -10,4 +11,3 @@ for r in rows:
         agg[r[ii["Kernel Name"]][:40]].append(float(r[ii["Metric Value"]].replace(",","")))
 for k,v in agg.items(): print(k, len(v), "mean %.1f us"%(sum(v)/len(v)/1e3), "max %.1f"%(max(v)/1e3))
 PY
-ncu --set full --import-source on --clock-control none --cache-control none -k regex:"vg_rows|vg_cols_kernel<4, 0>|vg_reduce|vg_pieces" -s 20 -c 4 -o gpurun_out/vg_full python bench.py --config c4 --rows 100000 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-accuracy --no-isolated > gpurun_out/vg_full.log 2>&1
