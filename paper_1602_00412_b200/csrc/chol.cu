@@ -20,6 +20,8 @@
 //    emits T for gemm_nn when max|E| <= kPolarMax and otherwise falls back to the
 //    Cholesky path, so accuracy never depends on the guess.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "dense.cuh"
@@ -649,6 +651,163 @@ __global__ void __cluster_dims__(kXC, 1, 1) __launch_bounds__(kXThreads)
 }
 }  // namespace
 
+namespace {
+
+// ---- Q = Y R^-1 as inverse + GEMM (the default for k % 8 == 0) -----------------------------
+// The substitution kernels above walk k / 8 dependent block columns per 8-row tile, a DMMA
+// latency chain that leaves the FP64 pipe mostly idle (c4: 161 us for 5e4 x 128). Instead:
+// trinv_kernel forms T = R^-1 once per factorisation (one CTA, warp b owns block column b and
+// back-substitutes its 8 x 8 blocks bottom-up: T_bb = inv(R_bb) from dinv8, T_ab =
+// -inv(R_aa) sum_{a<c<=b} R_ac T_cb), then tsmm_kernel applies X = Y T as a triangular GEMM on
+// DMMA. A dropped column j has a zero column in dinv8, hence zero column j and zero row j in T
+// (R's dropped row is e_j), exactly the substitution's X_j = 0 with Y_j not contributing.
+// Same span, same drop decisions; the products round differently (~u kappa(R)), which the
+// second CholeskyQR pass absorbs like any other rounding.
+template <bool SM>
+__global__ void __launch_bounds__(1024) trinv_kernel(const double* __restrict__ R, int k,
+                                                     const double* __restrict__ dinv8, double* __restrict__ T,
+                                                     int ldt, const double* __restrict__ stats) {
+    pdl_entry();
+    if (stats && stats[4] != 0.0) return;  // polar second pass: nothing to apply
+    extern __shared__ double tsm[];        // SM: block column b's tiles (rows 0..b) at 64 b (b+1) / 2
+    const int nb = k / 8;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {  // lower triangle (block-wise) = 0
+        const int i = e / k, j = e % k;
+        if (i / 8 > j / 8) T[(size_t)i * ldt + j] = 0.0;
+    }
+    for (int b = w; b < nb; b += nw) {
+        // tile (a, b): 8 x 8 row-major
+        auto tile = [&](int a) -> double* { return SM ? tsm + 32 * b * (b + 1) + 64 * a : T + (size_t)(8 * a) * ldt + 8 * b; };
+        const int tld = SM ? 8 : ldt;
+        auto tload = [&](const double* p) { return SM ? *p : __ldcg(p); };
+        {
+            double* tb = tile(b);
+            for (int e = lane; e < 64; e += 32) tb[(e >> 3) * tld + (e & 7)] = dinv8[(size_t)(8 * b + (e >> 3)) * 8 + (e & 7)];
+        }
+        __syncwarp();
+        for (int a = b - 1; a >= 0; --a) {
+            double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;  // acc = sum_c R_ac T_cb, two chains
+            for (int c = a + 1; c <= b; ++c) {
+                const double* tc = tile(c);
+                dmma884(c0, c1, __ldg(R + (size_t)(8 * a + g) * k + 8 * c + t), tload(tc + t * tld + g));
+                dmma884(e0, e1, __ldg(R + (size_t)(8 * a + g) * k + 8 * c + 4 + t), tload(tc + (4 + t) * tld + g));
+            }
+            c0 += e0;
+            c1 += e1;
+            // acc as the B operand of inv(R_aa) acc: through the tile's own slot (row g, cols 2t..)
+            double* ta = tile(a);
+            ta[g * tld + 2 * t] = c0;
+            ta[g * tld + 2 * t + 1] = c1;
+            __syncwarp();
+            double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 8; ks += 4)
+                dmma884(x0, x1, dinv8[(size_t)(8 * a + g) * 8 + ks + t], tload(ta + (ks + t) * tld + g));
+            __syncwarp();
+            ta[g * tld + 2 * t] = -x0;
+            ta[g * tld + 2 * t + 1] = -x1;
+            __syncwarp();
+        }
+        if (SM)
+            for (int e = lane; e < 64 * (b + 1); e += 32) {
+                const int a = e >> 6, i = (e >> 3) & 7, j = e & 7;
+                T[(size_t)(8 * a + i) * ldt + 8 * b + j] = tsm[32 * b * (b + 1) + e];
+            }
+    }
+}
+
+// X (m x n) = Y (m x n) T (n x n), T upper block-triangular (8 x 8 blocks), n % 8 == 0, n <= 256.
+// CTA: 64 rows x all n columns, 8 warps; warp w owns the 8-column blocks w, 15 - w, 16 + w,
+// 31 - w (a snake, so the triangle's work is even across warps) for all 8 row tiles. T and Y
+// stream through shared memory in 16-deep k-chunks (cp.async, two stages); a block skips the
+// chunks below its diagonal.
+constexpr int kMmRows = 64, kMmKc = 16, kMmYld = kMmKc + 4;
+__device__ __forceinline__ void cpa16(double* smem, const double* gmem, bool ok) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 16 : 0));
+}
+template <int NBW>
+__global__ void __launch_bounds__(256, NBW <= 2 ? 2 : 1) tsmm_kernel(const double* __restrict__ Y, int m, int n, int ld,
+                                                      const double* __restrict__ T, int ldt, double* __restrict__ X,
+                                                      int ldx, const double* __restrict__ stats) {
+    pdl_entry();
+    if (stats && stats[4] != 0.0) return;
+    extern __shared__ double mm[];
+    const int tld = n + 4;  // conflict-free B-fragment reads (n % 16 == 0 or 8 -> tld % 16 == 4 or 12)
+    const size_t stage_sz = (size_t)kMmRows * kMmYld + (size_t)kMmKc * tld;
+    const int r0 = blockIdx.x * kMmRows;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int nb = n / 8;
+    int blk[NBW];
+#pragma unroll
+    for (int q = 0; q < NBW; ++q) {
+        const int b = 8 * q + ((q & 1) ? 7 - w : w);
+        blk[q] = b < nb ? b : -1;
+    }
+    auto load = [&](int stage, int kc) {
+        double* Ys = mm + stage * stage_sz;
+        double* Ts = Ys + kMmRows * kMmYld;
+        for (int e = threadIdx.x; e < kMmRows * (kMmKc / 2); e += 256) {
+            const int r = e / (kMmKc / 2), c = 2 * (e % (kMmKc / 2));
+            const bool ok = r0 + r < m;
+            cpa16(Ys + r * kMmYld + c, ok ? Y + (size_t)(r0 + r) * ld + kc + c : Y, ok);
+        }
+        for (int e = threadIdx.x; e < kMmKc * (n / 2); e += 256) {
+            const int r = e / (n / 2), c = 2 * (e % (n / 2));
+            cpa16(Ts + r * tld + c, T + (size_t)(kc + r) * ldt + c, true);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    double acc[8][NBW][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int q = 0; q < NBW; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+    int stage = 0;
+    load(0, 0);
+    for (int kc = 0; kc < n; kc += kMmKc) {
+        if (kc + kMmKc < n) {
+            load(stage ^ 1, kc + kMmKc);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        __syncthreads();
+        const double* Ys = mm + stage * stage_sz;
+        const double* Ts = Ys + kMmRows * kMmYld;
+#pragma unroll
+        for (int ks = 0; ks < kMmKc; ks += 4) {
+            double a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = Ys[(8 * i + g) * kMmYld + ks + t];
+#pragma unroll
+            for (int q = 0; q < NBW; ++q) {
+                if (blk[q] < 0 || kc + ks > 8 * blk[q] + 7) continue;  // below the diagonal: T = 0
+                const double bq = Ts[(ks + t) * tld + 8 * blk[q] + g];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) dmma884(acc[i][q][0], acc[i][q][1], a[i], bq);
+            }
+        }
+        __syncthreads();
+        stage ^= 1;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = r0 + 8 * i + g;
+        if (row >= m) continue;
+#pragma unroll
+        for (int q = 0; q < NBW; ++q)
+            if (blk[q] >= 0)
+                *reinterpret_cast<double2*>(X + (size_t)row * ldx + 8 * blk[q] + 2 * t) =
+                    make_double2(acc[i][q][0], acc[i][q][1]);
+    }
+}
+
+}  // namespace
+
 void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, double* T, int ldt, double* stats,
                  int* d_err, int err_bit, Scratch& scr, cudaStream_t st, bool polar, int* udrop) {
     if (k <= 0) return;
@@ -673,12 +832,30 @@ void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, doub
 }
 
 void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const double* dinv8, double* X, int ldx,
-                const double* stats, cudaStream_t st) {
+                const double* stats, cudaStream_t st, double* tinv) {
     if (m <= 0 || k <= 0) return;
     const int kp = (k + 7) / 8 * 8;
     if (kp > 512) throw invalid_argument("trsm_apply: k > 512 unsupported");
     ProfScope prof("trsm", st);
     prof.work((double)m * k * k, 16.0 * (double)m * k);  // X = Y R^-1: k^2 / 2 multiply-adds per row
+    static const bool subst = std::getenv("SFDG_TRSM") && std::string(std::getenv("SFDG_TRSM")) == "subst";
+    if (tinv && k % 8 == 0 && k <= 256 && ld % 2 == 0 && ldx % 2 == 0 && !subst) {
+        const int nb = k / 8;
+        const size_t tsmem = (size_t)32 * nb * (nb + 1) * sizeof(double);
+        const bool in_smem = tsmem <= 200 * 1024;
+        const unsigned threads = (unsigned)std::min(1024, 32 * nb);
+        if (first_on_device((const void*)(trinv_kernel<true>))) {
+            allow_max_dynamic_smem(trinv_kernel<true>);
+            allow_max_dynamic_smem(tsmm_kernel<2>);
+            allow_max_dynamic_smem(tsmm_kernel<4>);
+        }
+        if (in_smem) LAUNCH(trinv_kernel<true>, 1, threads, tsmem, st, R, k, dinv8, tinv, k, stats);
+        else LAUNCH(trinv_kernel<false>, 1, threads, 0, st, R, k, dinv8, tinv, k, stats);
+        const size_t msmem = 2 * ((size_t)kMmRows * kMmYld + (size_t)kMmKc * (k + 4)) * sizeof(double);
+        if (nb <= 16) LAUNCH(tsmm_kernel<2>, ceil_div(m, kMmRows), 256, msmem, st, Y, m, k, ld, tinv, k, X, ldx, stats);
+        else LAUNCH(tsmm_kernel<4>, ceil_div(m, kMmRows), 256, msmem, st, Y, m, k, ld, tinv, k, X, ldx, stats);
+        return;
+    }
     if (kp > kTrsmSmemK) {  // R streamed through shared memory one block-column panel at a time
         if (first_on_device((const void*)(trsm_panel_kernel))) {
             allow_max_dynamic_smem(trsm_panel_kernel);

@@ -34,8 +34,10 @@ void fill2d(double* out, int rows, int cols, int ldo, double v, cudaStream_t st)
 // 1e-6, else the Cholesky path. trsm_apply: X = Y R^-1 (skipped when stats[4] != 0).
 void chol_factor(const double* G, int k, int ldg, double* R, double* dinv8, double* T, int ldt, double* stats,
                  int* d_err, int err_bit, Scratch& scr, cudaStream_t st, bool polar, int* udrop = nullptr);
+// tinv (k x k workspace, optional): apply as T = R^-1 formed once + a DMMA GEMM (k % 8 == 0,
+// k <= 256) instead of the row-wise substitution; SFDG_TRSM=subst forces the substitution.
 void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const double* dinv8, double* X, int ldx,
-                const double* stats, cudaStream_t st);
+                const double* stats, cudaStream_t st, double* tinv = nullptr);
 // The reference's orthonormalize (la_core.cpp:130-165) exactly, for the columns CholeskyQR
 // cannot decide: when stats[6] > 0 (or force), re-derives the drop of every uncertain column
 // (udrop[j]) from its explicit residual against the CholeskyQR result Q (two classical

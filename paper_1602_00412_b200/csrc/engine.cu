@@ -201,6 +201,7 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     const int kmax = std::max(2 * lp, 8);
     CK(cudaMalloc(&gram, (size_t)kmax * kmax * sizeof(double)));
     CK(cudaMalloc(&rinv, (size_t)lp * lp * sizeof(double)));
+    CK(cudaMalloc(&tinvb, (size_t)lp * lp * sizeof(double)));
     CK(cudaMalloc(&rfac, (size_t)lp * lp * sizeof(double)));
     CK(cudaMalloc(&dinv8, (size_t)lp * 8 * sizeof(double)));
     CK(cudaMalloc(&kc, (size_t)kmax * kmax * sizeof(double)));
@@ -250,7 +251,7 @@ Engine::~Engine() {
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     for (auto& kv : vgraphs)
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    for (void* p : {(void*)Y, (void*)Yt, (void*)W, (void*)Mt[0], (void*)Mt[1], (void*)Bp, (void*)gram, (void*)rinv,
+    for (void* p : {(void*)Y, (void*)Yt, (void*)W, (void*)Mt[0], (void*)Mt[1], (void*)Bp, (void*)gram, (void*)rinv, (void*)tinvb,
                     (void*)rfac,
                     (void*)dinv8, (void*)kc,
                     (void*)evals, (void*)evecs, (void*)S, (void*)x0, (void*)ybuf, (void*)u, (void*)tpart, (void*)tvec,
@@ -399,11 +400,11 @@ void Engine::orthonormalize(double* Yp, int m, int err_bit) {
     gram_tn(Yp, m, lp, lp, gram, lp, scr, st);
     chol_factor(gram, lp, lp, rfac, dinv8, nullptr, 0, st1, d_err, err_bit, scr, st, false,
                 exact_check ? d_udrop : nullptr);
-    trsm_apply(Yp, m, lp, lp, rfac, dinv8, Yt, lp, nullptr, st);
+    trsm_apply(Yp, m, lp, lp, rfac, dinv8, Yt, lp, nullptr, st, tinvb);
     if (exact_check) exact_orth(Yp, lp, Yt, lp, m, lp, d_udrop, st1, xtmp, st);
     gram_tn(Yt, m, lp, lp, gram, lp, scr, st);
     chol_factor(gram, lp, lp, rfac, dinv8, rinv, lp, st2, d_err, err_bit, scr, st, true);
-    trsm_apply(Yt, m, lp, lp, rfac, dinv8, Yp, lp, st2, st);
+    trsm_apply(Yt, m, lp, lp, rfac, dinv8, Yp, lp, st2, st, tinvb);
     gemm_nn(Yt, m, lp, lp, rinv, lp, lp, Yp, lp, st, st2 + 4);
 }
 
@@ -416,7 +417,7 @@ void Engine::orthonormalize_light(int m, int err_bit) {
     gram_tn(Y, m, lp, lp, gram, lp, scr, st);
     chol_factor(gram, lp, lp, rfac, dinv8, nullptr, 0, st1, d_err, err_bit, scr, st, false,
                 exact_check ? d_udrop : nullptr);
-    trsm_apply(Y, m, lp, lp, rfac, dinv8, Yt, lp, nullptr, st);
+    trsm_apply(Y, m, lp, lp, rfac, dinv8, Yt, lp, nullptr, st, tinvb);
     if (exact_check) exact_orth(Y, lp, Yt, lp, m, lp, d_udrop, st1, xtmp, st);
     std::swap(Y, Yt);
 }

@@ -79,6 +79,7 @@ class Engine {
     double* Mt[2] = {nullptr, nullptr};                 // d x 2lp : [B^T | B'^T]
     double* Bp = nullptr;                               // d x lp : this lane's B'^T (no stack)
     int cur = 0;
+    double* tinvb = nullptr;  // R^-1 of the current CholeskyQR pass (trsm_apply's inverse + GEMM path)
     double *gram = nullptr, *rinv = nullptr, *rfac = nullptr, *dinv8 = nullptr, *kc = nullptr, *evals = nullptr, *evecs = nullptr, *S = nullptr;
     double *x0 = nullptr, *ybuf = nullptr, *u = nullptr, *tpart = nullptr, *tvec = nullptr, *vpart = nullptr;
     double* vout = nullptr;
