@@ -47,6 +47,9 @@ CONFIG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
 DEFAULT_CONFIG = "c4"  # the largest single-GPU configuration in BASELINE.json
 FP64_PEAK_TFLOPS = 36.9  # DMMA (mma.sync m8n8k4 f64) measured on this pool: profiles/r01_fp64_peak.txt
 REF_BUDGET_S = 200.0  # reference arm: wall-clock budget of all timed samples together
+# sustained L2 -> SM gather bandwidth of the SpMM access pattern (ell-wide FP64 panel rows at random
+# row ids), measured on this pool: tools/probe_l2 16, profiles/r01c_l2_gather_sustained.txt
+L2_GATHER_GBS = 19567.3
 
 
 def parse():
@@ -422,9 +425,10 @@ def main():
                        "h2d_bytes_per_step": int(nnz * 12 + (n + stats["flushes"]) * 4),
                        "d2h_bytes_per_step": int(ell * d * 8),
                        "note": "bytes of rank 0's shard (every rank copies its own)"}
-    line.update(roofline_from_profile(prof, a.config, ms_step))
+    gather = 8.0 * ((ell + 7) // 8 * 8) * nnz / max(1, stats["flushes"])  # panel bytes one SpMM launch gathers
+    line.update(roofline_from_profile(prof, a.config, ms_step, gather))
     if iso:
-        line["roofline"]["isolated"] = isolated_roofline(iso)
+        line["roofline"]["isolated"] = isolated_roofline(iso, gather)
     if accuracy is not None:
         line["accuracy"] = accuracy
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -472,7 +476,17 @@ def _traffic(config: str):
         return None
 
 
-def roofline_from_profile(prof: dict, config: str, ms_step: float) -> dict:
+def l2_gather_roofline(ms: float, cnt: int, gather: float) -> dict:
+    """The SpMM's own bound: every stored entry pulls one ell-wide FP64 panel row (lp * 8 bytes)
+    from L2 (the panels of c1-c4 are L2-resident; L1 hits make > 1 possible), against the
+    measured sustained L2 -> SM gather rate."""
+    ach = gather / (ms * 1e-3 / cnt) / 1e9
+    return {"bound": "l2 gather", "achieved": round(ach, 1), "peak": L2_GATHER_GBS, "unit": "GB/s",
+            "frac": round(ach / L2_GATHER_GBS, 4), "gather_bytes_per_launch": gather,
+            "peak_source": "tools/probe_l2 16 (profiles/r01c_l2_gather_sustained.txt)"}
+
+
+def roofline_from_profile(prof: dict, config: str, ms_step: float, gather: float = 0.0) -> dict:
     """Roofline of the metric's kernel (the SpMM, HBM-bound) and the Gram (FP64 tensor) from
     the profiled step: achieved = the algorithmic bytes / flops the library declared for
     those launches (SURVEY 8(d) formulas) / their summed CUDA-event durations."""
@@ -499,6 +513,8 @@ def roofline_from_profile(prof: dict, config: str, ms_step: float) -> dict:
                        "note": "achieved = SURVEY 8(d) bytes 12 nnz + 8 (m+1) + 8 ell (m + d) per launch / average "
                                "launch duration (CUDA events on the lane stream, four flushes in flight); traffic = "
                                "ncu dram__bytes per launch for this config (profiles/ncu_summary.json)"}
+    if gather and sp.get("launches"):
+        out["roofline"]["l2_gather"] = l2_gather_roofline(sp["ms"], sp["launches"], gather)
     g = kern.get("gram", {})
     if g.get("achieved_tflops"):
         out["roofline"]["gram"] = {"bound": "tensor (FP64 DMMA)", "achieved": g["achieved_tflops"],
@@ -511,7 +527,7 @@ def roofline_from_profile(prof: dict, config: str, ms_step: float) -> dict:
     return out
 
 
-def isolated_roofline(prof: dict) -> dict:
+def isolated_roofline(prof: dict, gather: float = 0.0) -> dict:
     peaks, _ = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     res = {"what": "the same profiled step with one flush in flight (SFDG_LANES=1): standalone launch durations"}
@@ -522,6 +538,8 @@ def isolated_roofline(prof: dict) -> dict:
         ach = by / (ms * 1e-3) / 1e9 if unit == "GB/s" else fl / (ms * 1e-3) / 1e12
         res[k] = {"achieved": round(ach, 2), "peak": peak, "unit": unit, "frac": round(ach / peak, 4),
                   "us_per_launch": round(1e3 * ms / cnt, 2), "launches": cnt}
+        if k == "spmm" and gather:
+            res[k]["l2_gather"] = l2_gather_roofline(ms, cnt, gather)
     return res
 
 

@@ -481,6 +481,7 @@ class Sketcher {
         int interval = 1, interval_base = 1, interval_used = 1;
         bool checked = false, checked_base = false;  // Engine::exact_check for the attempt / flush start
         bool uncertain_seen = false;                 // a checked attempt met uncertain drops
+        bool probe = false;  // no kappa history: the attempt measures its own (Engine::probe)
         RngPos pos0;
         size_t attempt = 0;
         double delta_hat = 0.0, kappa_last = 0.0;
@@ -665,6 +666,7 @@ class Sketcher {
             Engine& e = *L.eng;
             e.orth_interval = L.interval_used;
             e.exact_check = L.checked;
+            e.probe = L.probe && L.interval_used > 1;
             e.pos = L.cur.pos;
             e.scr.reset();
             if (wait_bp) CK(cudaStreamWaitEvent(e.st, L.ev_bp_free, 0));
@@ -711,6 +713,7 @@ class Sketcher {
                 L.interval_base =
                     (L.id >= lag && h.valid) ? next_orth_interval(h.kappa_last, h.last_since) : kFirstInterval;
                 L.checked_base = L.id >= lag && h.valid && h.checked;
+                L.probe = !(L.id >= lag && h.valid);
                 const FlushState st = idx_in_flight == 0 ? committed : predicted_end(lanes[inflight[idx_in_flight - 1]]);
                 start_flush(L, st);
                 break;
@@ -720,14 +723,16 @@ class Sketcher {
                 const double kappa_last = e.h_scal[16 + 3], kappa_max = e.h_scal[16 + 5];
                 const int err = e.h_err[0];
                 const double uncertain = e.h_scal[16 + 7] + e.h_scal[24 + 7];
-                if (!L.checked && (uncertain > 0.0 || (L.interval_used > 1 && (kappa_max > kKappaUnsafe ||
+                const int used = e.adaptive ? e.orth_interval : 1;  // a probe may have changed it
+                if (!L.checked && (uncertain > 0.0 || (used > 1 && (kappa_max > kKappaUnsafe ||
                                                                                  (err & ERR_NONFINITE_ITER))))) {
                     // redo from the same draws with the every-sweep schedule and exact drop
                     // decisions (as Engine::boosted)
                     CK(cudaMemsetAsync(e.d_err, 0, sizeof(int), e.st));
                     L.cur.pos = L.pos0;
                     L.interval = 1;
-                    L.checked = true;
+                    L.probe = false;
+                    L.checked = uncertain > 0.0;  // exact drop decisions only where CholeskyQR cannot vouch
                     --L.attempt;
                     enqueue_attempt(L);
                     break;
@@ -1012,7 +1017,7 @@ class FdSketch {
   public:
     FdSketch(size_t ell_, size_t d_, int device) : ell(ell_), d(d_) {
         if (ell < 1 || ell > d) throw invalid_argument("FdSketcher: requires 1 <= ell <= d");  // sketch.cpp:48-49
-        if (ell > (size_t)kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 256] for this build");
+        if (ell > (size_t)kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 512] for this build");
         if (d >= (size_t)INT32_MAX) throw invalid_argument("FdSketcher: d must be < 2^31");
         e = std::make_unique<Engine>(device, (int)d, (int)ell, 0, 1, 1);
     }
@@ -1151,7 +1156,7 @@ void dense_shrink_host(const double* a, size_t rows, size_t cols, size_t ell, do
     for (size_t i = 0; i < rows * cols; ++i)
         if (!std::isfinite(a[i])) throw invalid_argument("dense_shrink: non-finite input");
     if (rows > cols && ell > cols) throw invalid_argument("dense_shrink: ell exceeds column count");
-    if (ell > (size_t)kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 256] for this build");
+    if (ell > (size_t)kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 512] for this build");
     Engine e(device, (int)cols, (int)ell, 0, 1, 1);
     double* A = e.scr.take<double>((int64_t)rows * cols);
     double* Xt = e.scr.take<double>((int64_t)cols * rows);
@@ -1537,7 +1542,7 @@ int sfdg_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* val
                  size_t ell, size_t iterations, sfdg_rng_state* rng, double* out, int device) {
     return guard([&] {
         if (!row_ptr || !b || !rng || !out) throw invalid_argument("cov_err: null argument");
-        if (ell < 1 || ell > (size_t)kMaxEll) throw invalid_argument("cov_err: sketch rows must be in [1, 256]");
+        if (ell < 1 || ell > (size_t)kMaxEll) throw invalid_argument("cov_err: sketch rows must be in [1, 512]");
         if (d < 1 || d >= (size_t)INT32_MAX) throw invalid_argument("cov_err: dimension mismatch");
         validate_csr(row_ptr, cols, vals, n, d);
         require_device(device);
@@ -1565,7 +1570,7 @@ int sfdg_exact_tail(const int64_t* row_ptr, const uint32_t* cols, const double* 
         }
         if (k > std::min(n, d)) throw invalid_argument("exact_tail: k exceeds matrix rank bound");
         const size_t block = std::min(k + 10, std::min(n, d));
-        if (block > (size_t)kMaxEll) throw invalid_argument("exact_tail: k + 10 must be <= 256 for this build");
+        if (block > (size_t)kMaxEll) throw invalid_argument("exact_tail: k + 10 must be <= 512 for this build");
         require_device(device);
         const int64_t nnz = row_ptr[n] - row_ptr[0];
         Engine e(device, (int)d, (int)block, rng->seed, (uint64_t)std::max<int64_t>(nnz, 1), (int)n);
@@ -1585,7 +1590,7 @@ int sfdg_proj_err(const int64_t* row_ptr, const uint32_t* cols, const double* va
     return guard([&] {
         if (!row_ptr || !b || !out || !has_value) throw invalid_argument("proj_err: null argument");
         if (k < 1 || k > ell) throw invalid_argument("proj_err: k out of range");
-        if (ell > (size_t)kMaxEll) throw invalid_argument("proj_err: sketch rows must be in [1, 256]");
+        if (ell > (size_t)kMaxEll) throw invalid_argument("proj_err: sketch rows must be in [1, 512]");
         if (ell > d) throw invalid_argument("svd_top: expects m <= d");
         validate_csr(row_ptr, cols, vals, n, d);
         require_device(device);
@@ -1766,7 +1771,7 @@ int sfdg_eigh(const double* sym, size_t n, double off_tol, double* values, doubl
 int sfdg_orthonormalize(const double* in, size_t n, size_t k, double* out, int device) {
     return guard([&] {
         if (n < k) throw invalid_argument("orthonormalize: needs n >= k");
-        if (k < 1 || k > (size_t)kMaxEll) throw invalid_argument("orthonormalize: k must be in [1, 256]");
+        if (k < 1 || k > (size_t)kMaxEll) throw invalid_argument("orthonormalize: k must be in [1, 512]");
         require_device(device);
         Engine e(device, 8, (int)k, 0, 1, (int)n);
         CK(cudaMemsetAsync(e.Y, 0, n * e.lp * sizeof(double), e.st));

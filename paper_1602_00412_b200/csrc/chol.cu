@@ -506,7 +506,9 @@ __global__ void __launch_bounds__(kTrsmThreads) trsm_panel_kernel(const double* 
 constexpr int kXC = 8;
 constexpr int kXThreads = 512;
 constexpr int kXWarps = kXThreads / 32;
-constexpr int kXMaxK = 256;
+constexpr int kXMaxK = 512;
+// dynamic shared memory: per-warp partials, two cluster exchange vectors, the totals
+size_t exact_orth_smem(int k) { return (size_t)(kXWarps + 3) * (size_t)((k + 31) / 32 * 32) * sizeof(double); }
 
 __global__ void __cluster_dims__(kXC, 1, 1) __launch_bounds__(kXThreads)
     exact_orth_kernel(const double* __restrict__ Y, int ldy, double* __restrict__ Q, int ldq, int m, int k,
@@ -514,9 +516,11 @@ __global__ void __cluster_dims__(kXC, 1, 1) __launch_bounds__(kXThreads)
                       int force) {
     pdl_entry();
     if (!force && !(stats[6] > 0.0)) return;  // uniform over the cluster
-    __shared__ double wred[kXWarps][kXMaxK];
-    __shared__ double part[2][kXMaxK];
-    __shared__ double h[kXMaxK];
+    extern __shared__ double xsm[];
+    const int KM = (k + 31) / 32 * 32;
+    double* wred = xsm;                        // [kXWarps][KM]
+    double* part = wred + (size_t)kXWarps * KM;  // [2][KM]
+    double* h = part + 2 * (size_t)KM;           // [KM]
     const unsigned rank = cluster_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int chunk = (m + kXC - 1) / kXC;
@@ -527,17 +531,17 @@ __global__ void __cluster_dims__(kXC, 1, 1) __launch_bounds__(kXThreads)
     auto reduce = [&](const double* acc, int n) {
         const int nc = (n + 31) / 32;
         for (int c = 0; c < nc; ++c)
-            if (32 * c + lane < n) wred[warp][32 * c + lane] = acc[c];
+            if (32 * c + lane < n) wred[(size_t)warp * KM + 32 * c + lane] = acc[c];
         __syncthreads();
         for (int p = tid; p < n; p += kXThreads) {
             double v = 0.0;
-            for (int w = 0; w < kXWarps; ++w) v += wred[w][p];
-            part[pb][p] = v;
+            for (int w = 0; w < kXWarps; ++w) v += wred[(size_t)w * KM + p];
+            part[(size_t)pb * KM + p] = v;
         }
         cluster_barrier();
         for (int p = tid; p < n; p += kXThreads) {
             double v = 0.0;
-            for (unsigned r = 0; r < kXC; ++r) v += cluster_map(&part[pb][0], r)[p];
+            for (unsigned r = 0; r < kXC; ++r) v += cluster_map(part + (size_t)pb * KM, r)[p];
             h[p] = v;
         }
         pb ^= 1;
@@ -880,9 +884,11 @@ void trsm_apply(const double* Y, int m, int k, int ld, const double* R, const do
 void exact_orth(const double* Y, int ldy, double* Q, int ldq, int m, int k, const int* udrop, const double* stats,
                 double* tmp, cudaStream_t st, bool force) {
     if (m <= 0 || k <= 0) return;
-    if (k > kXMaxK) throw invalid_argument("exact_orth: k > 256 unsupported");
+    if (k > kXMaxK) throw invalid_argument("exact_orth: k > 512 unsupported");
     ProfScope prof("exact_orth", st);
-    LAUNCH(exact_orth_kernel, kXC, kXThreads, 0, st, Y, ldy, Q, ldq, m, k, udrop, stats, tmp, force ? 1 : 0);
+    if (first_on_device((const void*)exact_orth_kernel)) allow_max_dynamic_smem(exact_orth_kernel);
+    LAUNCH(exact_orth_kernel, kXC, kXThreads, exact_orth_smem(k), st, Y, ldy, Q, ldq, m, k, udrop, stats, tmp,
+           force ? 1 : 0);
 }
 
 }  // namespace sfdg

@@ -154,7 +154,7 @@ void raise_device_flags(int e) {
 Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, int m_cap_, RngStream* shared_rng,
                bool stack, bool high_priority)
     : device(device_), d(d_), ell(ell_) {
-    if (ell < 1 || ell > kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 256] for this build");
+    if (ell < 1 || ell > kMaxEll) throw invalid_argument("sfdg: ell must be in [1, 512] for this build");
     lp = (int)round_up((size_t)ell, 8);
     if (const char* e = std::getenv("SFDG_ORTH_EVERY_SWEEP")) adaptive = std::atoi(e) == 0;
     if (const char* e = std::getenv("SFDG_GRAPHS")) use_graphs = std::atoi(e) != 0;
@@ -218,6 +218,7 @@ Engine::Engine(int device_, int d_, int ell_, uint64_t seed, uint64_t nnz_cap, i
     // which leaves room for the other lanes' kernels. Small B' (c1, c2): the persistent kernel.
     use_vgraph = (8 * (int64_t)d * lp) / (512 * 1024) > 32;
     if (const char* e = std::getenv("SFDG_VERIFY_MODE")) use_vgraph = std::string(e) == "graph";
+    if (ell > 256) use_vgraph = true;  // the persistent verifier keeps ell <= 256 per warp in registers
     int sms_here = 0;
     CK(cudaDeviceGetAttribute(&sms_here, cudaDevAttrMultiProcessorCount, device));
     const int part_blocks = std::max(2 * std::max(verify_blocks, sms_here), vg_blocks);  // resident grids: <= 1 per SM
@@ -487,12 +488,27 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
     // `interval` sweeps (adaptive, see boosted()) and always after the last sweep; in
     // between Y <- A'(A'^T Y) unnormalised. interval = 1 is the reference's schedule
     // (randsvd.cpp:38-49).
+    size_t s = 0;
+    if (adaptive && probe && !exact_check && q > 1) {
+        // No conditioning history for this flush: measure it. One sweep from the orthonormal
+        // Y0 closed by a light pass gives kappa(Y1) = the per-sweep growth g of this buffer
+        // (a pure function of the attempt's own data: the same on every lane count); the rest
+        // of the attempt runs at the interval that keeps cond(Y) <= kKappaTarget.
+        spmm(a.col_ptr, a.row_idx, a.cval, d, plan_c, a.nnz, Y, lp, lp, W, lp, scr, st, m, ell);
+        spmm(a.row_ptr, (const int*)a.col, a.val, m, plan_r, a.nnz, W, lp, lp, Y, lp, scr, st, d, ell, &hot);
+        orthonormalize_light(m, ERR_NONFINITE_ITER);
+        CK(cudaMemcpyAsync(h_scal + 48, d_scal + 16 + 3, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        orth_interval = next_orth_interval(h_scal[48], 1);
+        last_since = 1;
+        s = 1;
+    }
     const int interval = adaptive ? orth_interval : 1;
     // whole blocks (interval sweeps closed by a light pass) replay as a CUDA graph when no
     // long-row piece kernels are involved and profiling (per-launch events) is off
     const bool graphs_ok = use_graphs && adaptive && !exact_check && !g_prof_on.load(std::memory_order_relaxed);
     int since = 0;
-    for (size_t s = 0; s < q;) {
+    for (; s < q;) {
         if (graphs_ok && since == 0 && s + (size_t)interval < q) {
             sweep_block(interval, m);
             s += (size_t)interval;
@@ -706,8 +722,8 @@ size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* d
     for (size_t attempt = 1; attempt <= kRetryCap; ++attempt) {
         const RngPos pos0 = pos;
         if (exact_check) orth_interval = 1;
-        const int interval_used = adaptive ? orth_interval : 1;
         attempt_enqueue(cfg, bpt, ldb);
+        const int interval_used = adaptive ? orth_interval : 1;  // after a probe: the measured one
         // prefetch the next attempt's draws while we wait (side stream)
         rng->prefetch(pos.words + 2 * ((uint64_t)d * ell + 2 * d) + 8);
         CK(cudaStreamSynchronize(st));
@@ -722,7 +738,7 @@ size_t Engine::boosted(Verifier& v, const PowerCfg& cfg, double a_fsq, double* d
             CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
             pos = pos0;
             orth_interval = 1;
-            exact_check = true;
+            exact_check = uncertain > 0.0;  // exact drop decisions only where CholeskyQR cannot vouch
             --attempt;
             continue;
         }

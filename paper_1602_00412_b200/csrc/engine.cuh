@@ -19,7 +19,7 @@ namespace sfdg {
 
 constexpr double kAlpha = 6.0 / 41.0;  // core/include/sfd/common.hpp:10
 constexpr size_t kRetryCap = 64;       // core/src/shrink.cpp:12
-constexpr int kMaxEll = 256;           // 2*ell <= 512 fits every kernel's tile plan
+constexpr int kMaxEll = 512;           // 2*ell <= 1024: the eigensolver and CholeskyQR limits
 constexpr double kKappaTarget = 1e4;   // cond(Y) allowed to build up between CholeskyQR2 passes
 constexpr double kKappaUnsafe = 1e7;   // above this CholeskyQR2 may lose orthogonality: redo
 constexpr int kMaxInterval = 8;
@@ -117,6 +117,9 @@ class Engine {
     // column drops re-decided by the reference's rule. Set for attempts replayed after an
     // uncertain drop (with orth_interval = 1, the reference's schedule).
     bool exact_check = false;
+    // No kappa history (a stream's first flushes): simultaneous_iteration measures the growth
+    // over its first sweep (one host read-back) and picks the interval from it.
+    bool probe = false;
 
     void set_device() const;
     void ensure_rows(int m);

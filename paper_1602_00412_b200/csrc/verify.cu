@@ -720,11 +720,19 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_colsum_kernel(VerifyArgs a, 
 // same rows the block partials of the next t = B' y and of |y|^2 (init = true: the x0 pass --
 // |x0|^2 and B' x0 partials, no y). Every column costs one B'^T row, so equal contiguous column
 // ranges per block and a fixed warp interleave inside it (the partials' order is fixed).
+// Q > 8 (256 < ell <= 512): 256 threads and two columns in flight per warp keep the B'^T
+// rows, t and the partials in registers (2 x 16 + 2 x 16 doubles) and the static shared memory
+// under 48 KB.
+template <int Q>
+__host__ __device__ constexpr int vg_cols_threads() { return Q > 8 ? 256 : kGColsThreads; }
+
 template <int Q, bool INIT>
-__global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, const VState* __restrict__ st, int step) {
+__global__ void __launch_bounds__(vg_cols_threads<Q>()) vg_cols_kernel(VerifyArgs a, const VState* __restrict__ st, int step) {
     pdl_entry();
-    __shared__ double tloc[256];
-    __shared__ double wpart[kGColsWarps][257];
+    constexpr int NT = vg_cols_threads<Q>(), NW = NT / 32, QL = 32 * Q;
+    constexpr int RF = Q > 8 ? 2 : 4;  // columns in flight per warp
+    __shared__ double tloc[QL];
+    __shared__ double wpart[NW][QL + 1];
     if (st->done) return;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int L = a.ell;
@@ -733,23 +741,23 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
     double* y = a.ybuf + (size_t)(step & 1) * a.d;
     const double xscale = INIT ? 1.0 : st->xscale;  // w = A'^T A' y_prev is unscaled
     if (!INIT)
-        for (int j = threadIdx.x; j < L; j += kGColsThreads) tloc[j] = __ldcg(a.t + j);
+        for (int j = threadIdx.x; j < L; j += NT) tloc[j] = __ldcg(a.t + j);
     __syncthreads();
     double tl[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) tl[q] = (!INIT && lane + 32 * q < L) ? tloc[lane + 32 * q] : 0.0;
-    double tn[kMaxQ];
+    double tn[Q];
 #pragma unroll
-    for (int q = 0; q < kMaxQ; ++q) tn[q] = 0.0;
+    for (int q = 0; q < Q; ++q) tn[q] = 0.0;
     double nsq = 0.0;
     bool bad = false;
     const double scale = st->scale;
-    for (int64_t cb = c0 + wib; cb < c1; cb += 4 * kGColsWarps) {
-        double brow[4][Q];
-        double wc[4];
+    for (int64_t cb = c0 + wib; cb < c1; cb += RF * NW) {
+        double brow[RF][Q];
+        double wc[RF];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int64_t c = cb + q * kGColsWarps;
+        for (int q = 0; q < RF; ++q) {
+            const int64_t c = cb + q * NW;
             const bool own = c < c1;
             wc[q] = own ? (INIT ? a.x0[c] : __ldcg(a.w + c)) : 0.0;
 #pragma unroll
@@ -760,23 +768,22 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
         }
         if constexpr (INIT) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < RF; ++q) {
                 nsq = fma(wc[q], wc[q], nsq);
 #pragma unroll
                 for (int w = 0; w < Q; ++w) tn[w] = fma(brow[q][w], wc[q], tn[w]);
             }
         } else {
-            double dp[4];
+            double dp[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            dp[q] = 0.0;
+        for (int q = 0; q < RF; ++q) {
 #pragma unroll
             for (int w = 0; w < Q; ++w) dp[q] = fma(-brow[q][w], tl[w], dp[q]);
         }
         const double tot = warp_sum4(dp);  // -(B'^T t)_c on lanes 8q .. 8q+7
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int64_t c = cb + q * kGColsWarps;
+        for (int q = 0; q < RF; ++q) {
+            const int64_t c = cb + q * NW;
             const double yc = scale * fma(wc[q], xscale, __shfl_sync(0xffffffffu, tot, 8 * q));  // shrink.cpp:124
             if (c < c1) {
                 if (!isfinite(yc)) bad = true;
@@ -791,14 +798,14 @@ __global__ void __launch_bounds__(kGColsThreads) vg_cols_kernel(VerifyArgs a, co
     if (bad) atomicOr(a.err, ERR_NONFINITE_VERIFY);
     // block partials (fixed warp order) -> tpart[block], part[block]
 #pragma unroll
-    for (int q = 0; q < kMaxQ; ++q)
+    for (int q = 0; q < Q; ++q)
         if (lane + 32 * q < L) wpart[wib][lane + 32 * q] = tn[q];
-    if (lane == 0) wpart[wib][256] = nsq;
+    if (lane == 0) wpart[wib][QL] = nsq;
     __syncthreads();
-    for (int j = threadIdx.x; j <= 256; j += kGColsThreads) {
-        if (j < L || j == 256) {
+    for (int j = threadIdx.x; j <= QL; j += NT) {
+        if (j < L || j == QL) {
             double sacc = 0.0;
-            for (int w = 0; w < kGColsWarps; ++w) sacc += wpart[w][j];
+            for (int w = 0; w < NW; ++w) sacc += wpart[w][j];
             if (j < L) a.tpart[(size_t)blockIdx.x * L + j] = sacc;
             else a.part[blockIdx.x] = sacc;
         }
@@ -832,9 +839,14 @@ VgColsFn vg_cols_fn(int ell) {
         case 5: return vg_cols_kernel<5, INIT>;
         case 6: return vg_cols_kernel<6, INIT>;
         case 7: return vg_cols_kernel<7, INIT>;
-        default: return vg_cols_kernel<8, INIT>;
+        case 8: return vg_cols_kernel<8, INIT>;
+        case 9: case 10: return vg_cols_kernel<10, INIT>;
+        case 11: case 12: return vg_cols_kernel<12, INIT>;
+        case 13: case 14: return vg_cols_kernel<14, INIT>;
+        default: return vg_cols_kernel<16, INIT>;
     }
 }
+unsigned vg_cols_nthreads(int ell) { return (ell + 31) / 32 > 8 ? 256u : (unsigned)kGColsThreads; }
 
 typedef void (*VerifyFn)(VerifyArgs);
 template <bool CL>
@@ -946,6 +958,7 @@ int verify_cluster_size(int64_t d, int lp) {
 }
 
 void verify_launch(const VerifyArgs& args_in, int nblocks, int cluster, cudaStream_t st) {
+    if (args_in.ell > 32 * kMaxQ) throw invalid_argument("verify: the persistent verifier holds ell <= 256 (wider: kernel sequence)");
     ProfScope prof("verify", st);
     if (first_on_device((const void*)verify_kernel<8, false>)) {
         for (int ell = 32; ell <= 256; ell += 32) {
@@ -1003,11 +1016,11 @@ void verify_sequence(const VerifyArgs& a, void* state, int nblk, int sms, cudaSt
     // one wave of the row kernel (six 256-thread blocks per SM), at least one warp per entry of t
     const unsigned rgrid = (unsigned)std::max<int64_t>((a.ell + 7) / 8, std::min<int64_t>(6 * sms, (a.m + 31) / 32));
     const unsigned rgrid2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(6 * sms, (a.d + 31) / 32));
-    LAUNCH(vg_cols_fn<true>(a.ell), nblk, kGColsThreads, 0, st, a, s, 0);
+    LAUNCH(vg_cols_fn<true>(a.ell), nblk, vg_cols_nthreads(a.ell), 0, st, a, s, 0);
     for (int step = 0; step < a.steps; ++step) {
         LAUNCH(vg_rows_kernel, rgrid, kGRowsThreads, 0, st, a, s, step, nblk);
         LAUNCH(vg_colsum_kernel, rgrid2, kGRowsThreads, 0, st, a, s);
-        LAUNCH(vg_cols_fn<false>(a.ell), nblk, kGColsThreads, 0, st, a, s, step);
+        LAUNCH(vg_cols_fn<false>(a.ell), nblk, vg_cols_nthreads(a.ell), 0, st, a, s, step);
     }
     LAUNCH(vg_final_kernel, 1, 32, 0, st, a, s, nblk);
 }
