@@ -40,7 +40,7 @@ def test_orthonormalize_wide_drops_dependent_columns(oracle):
     a = rng.standard_normal((900, 300))
     a[:, 270] = a[:, 3] - 2.0 * a[:, 280]
     a[:, 299] = 0.0
-    a[:, 290] = a[:, 10] + a[:, 20] + 1e-9 * a[:, 30]  # nearly dependent: kept by the reference
+    a[:, 290] = a[:, 10] + a[:, 20] + 1e-9 * rng.standard_normal(900)  # nearly dependent: kept by the reference
     q = P.orthonormalize(a)
     qo = oracle.orthonormalize(a)
     assert np.array_equal(np.abs(q).sum(axis=0) == 0, np.abs(qo).sum(axis=0) == 0)
