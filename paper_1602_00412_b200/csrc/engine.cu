@@ -135,7 +135,10 @@ size_t power_iteration_count(size_t m, const PowerCfg& cfg) {
 int next_orth_interval(double kappa_last, int last_since) {
     if (!(kappa_last >= 1.0)) return 1;
     const double g = std::pow(std::max(kappa_last, 1.0), 1.0 / std::max(last_since, 1));
-    const int iv = g <= 1.001 ? kMaxInterval : (int)std::floor(std::log(kKappaTarget) / std::log(g));
+    // SFDG_KAPPA_TARGET: A/B testing of the target (results stay within the parity gates; the
+    // kKappaUnsafe replay still guards every attempt)
+    static const double target = std::getenv("SFDG_KAPPA_TARGET") ? std::atof(std::getenv("SFDG_KAPPA_TARGET")) : kKappaTarget;
+    const int iv = g <= 1.001 ? kMaxInterval : (int)std::floor(std::log(target) / std::log(g));
     return std::max(1, std::min(kMaxInterval, iv));
 }
 
