@@ -13,6 +13,8 @@
 //    the right-vector recovery V = A^T U / sigma (la_core.cpp:113-126) fused with the
 //    shrink row scale (shrink.cpp:15-26).
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "dense.cuh"
@@ -110,6 +112,130 @@ __global__ void __launch_bounds__(128) gram_tn_kernel(const double* __restrict__
         }
         __syncthreads();
         stage ^= 1;
+    }
+    double* P = partial + (size_t)chunk * k * k;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const int row = i0 + wm * 32 + mi * 8 + g;
+            const int col = j0 + wn * 32 + ni * 8 + 2 * t;
+            if (row < k) {
+                if (col < k) P[(size_t)row * k + col] = acc[mi][ni][0];
+                if (col + 1 < k) P[(size_t)row * k + col + 1] = acc[mi][ni][1];
+            }
+        }
+}
+
+// ---- TMA-staged Gram (opt-in, SFDG_GRAM=tma: measured slower than cp.async, see gram_tn) ------
+// The same tiles, chunks and DMMA order as gram_tn_kernel (bit-identical partials), but each
+// stage's 2 x KT row segments (<= 512 B each, contiguous in X) arrive by 1-D TMA bulk copies
+// (cp.async.bulk, SASS UBLKCP) issued by one warp and counted in bytes on the stage's
+// mbarrier, three stages deep: the other warps issue only LDS + DMMA, no per-element LDGSTS.
+// Columns past k in an edge tile are zeroed once; rows past the chunk end in the last stage
+// are zeroed by the consumers before they read.
+constexpr int kGStages = 3;
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(128) gram_tma_kernel(const double* __restrict__ X, int n, int k, int ldx,
+                                                      int rows_per_chunk, int T, double* __restrict__ partial) {
+    extern __shared__ __align__(128) double smg[];  // [stage][A|B][KT][LDT]
+    __shared__ __align__(8) uint64_t full[kGStages];
+    int ti = 0, rem = blockIdx.x;
+    while (rem >= T - ti) {
+        rem -= T - ti;
+        ++ti;
+    }
+    const int tj = ti + rem;
+    const int i0 = ti * TB, j0 = tj * TB;
+    const int chunk = blockIdx.y;
+    const int r0 = chunk * rows_per_chunk;
+    const int r1 = min(n, r0 + rows_per_chunk);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = w & 1, wn = w >> 1;
+    auto tile = [&](int stage, int ab) { return smg + (size_t)((stage * 2 + ab) * KT) * LDT; };
+    const int ca = min(TB, k - i0), cb = min(TB, k - j0);  // valid columns of the A / B tiles
+    // zero the columns no copy will write (edge tiles), then the barriers; all before PDL wait
+    if (ca < TB || cb < TB)
+        for (int e = threadIdx.x; e < kGStages * 2 * KT * TB; e += 128) {
+            const int c = e % TB, r = (e / TB) % KT, ab = (e / (TB * KT)) % 2, stg = e / (2 * TB * KT);
+            if (c >= (ab ? cb : ca)) tile(stg, ab)[r * LDT + c] = 0.0;
+        }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kGStages; ++i) mbar_init(&full[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // zeros before any async write
+    __syncthreads();
+    pdl_entry();
+    const int nst = (r1 - r0 + KT - 1) / KT;
+    auto issue = [&](int s) {  // warp 0: stage s's row segments
+        if (w != 0 || s >= nst) return;
+        const int kb = r0 + s * KT, nr = min(KT, r1 - kb);
+        const int stg = s % kGStages;
+        if (lane == 0) mbar_expect_tx(&full[stg], (unsigned)(nr * (ca + cb) * 8));
+        __syncwarp();
+        if (lane < nr) {
+            const double* row = X + (size_t)(kb + lane) * ldx;
+            bulk_g2s(tile(stg, 0) + lane * LDT, row + i0, (unsigned)ca * 8u, &full[stg]);
+            bulk_g2s(tile(stg, 1) + lane * LDT, row + j0, (unsigned)cb * 8u, &full[stg]);
+        }
+    };
+    for (int s = 0; s < kGStages - 1; ++s) issue(s);
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int s = 0; s < nst; ++s) {
+        issue(s + kGStages - 1);  // its buffer was released by the barrier that ended step s - 1
+        const int stg = s % kGStages;
+        mbar_wait(&full[stg], (unsigned)((s / kGStages) & 1));
+        const int nr = min(KT, r1 - (r0 + s * KT));
+        double* As = tile(stg, 0);
+        double* Bs = tile(stg, 1);
+        if (nr < KT) {  // last stage of the chunk: rows past its end count as zero
+            for (int e = threadIdx.x; e < (KT - nr) * TB; e += 128) {
+                const int r = nr + e / TB, c = e % TB;
+                As[r * LDT + c] = 0.0;
+                Bs[r * LDT + c] = 0.0;
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int ks = 0; ks < KT; ks += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = As[(ks + t) * LDT + wm * 32 + mi * 8 + g];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(ks + t) * LDT + wn * 32 + ni * 8 + g];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        __syncthreads();  // stage stg free for the copy issued at the top of step s + 1
     }
     double* P = partial + (size_t)chunk * k * k;
 #pragma unroll
@@ -308,7 +434,13 @@ void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scrat
     prof.work((double)n * k * (k + 1), 8.0 * ((double)n * k + (double)k * k));
     const int T = (k + TB - 1) / TB;
     const int ntiles = T * (T + 1) / 2;
-    int target_chunks = std::max(1, (2 * kSMs + ntiles - 1) / ntiles);
+    // split-K chunks: two waves of tile-chunks, and up to six for tall X (>= 8192 rows per chunk
+    // at two waves) -- kbench, 1 B200: 1e6 x 256 4.13 ms at two waves, 3.03 ms at six; 5e4 x 128
+    // 46.9 us at two, 50-56 us at more (profiles/r02c_gram_ab.txt). SFDG_GRAM_WAVES overrides.
+    static const int waves_env = std::getenv("SFDG_GRAM_WAVES") ? std::max(1, std::atoi(std::getenv("SFDG_GRAM_WAVES"))) : 0;
+    const int64_t lo = (2 * (int64_t)kSMs + ntiles - 1) / ntiles, hi = (6 * (int64_t)kSMs + ntiles - 1) / ntiles;
+    int target_chunks = waves_env ? std::max(1, (waves_env * kSMs + ntiles - 1) / ntiles)
+                                  : (int)std::max<int64_t>(1, std::max(lo, std::min(hi, (int64_t)n / 8192)));
     int rows_per_chunk = (int)round_up(std::max<int64_t>(KT * 4, ((int64_t)n + target_chunks - 1) / target_chunks), KT);
     const int nchunks = (n + rows_per_chunk - 1) / rows_per_chunk;
     double* partial = scr.take<double>((int64_t)nchunks * k * k);
@@ -317,7 +449,16 @@ void gram_tn(const double* X, int n, int k, int ldx, double* out, int ldo, Scrat
         allow_max_dynamic_smem(gram_tn_kernel<2>);
         allow_max_dynamic_smem(gram_tn_kernel<1>);
     }
-    if (vec16(X, ldx) && k % 2 == 0)
+    // SFDG_GRAM=tma: stages by TMA bulk copies (bit-identical; measured slower: three 35 KB
+    // stages leave two CTAs per SM and 64 512-byte copies per stage, 7.2 against 4.1 ms at
+    // 1e6 x 256, profiles/r02c_gram_ab.txt), so per-thread cp.async stays the default
+    const char* gsel = std::getenv("SFDG_GRAM");
+    const bool tma = gsel && std::string(gsel) == "tma";
+    if (tma && vec16(X, ldx) && k % 2 == 0) {
+        if (first_on_device((const void*)gram_tma_kernel)) allow_max_dynamic_smem(gram_tma_kernel);
+        const size_t tsmem = (size_t)kGStages * 2 * KT * LDT * sizeof(double);
+        LAUNCH(gram_tma_kernel, dim3(ntiles, nchunks), 128, tsmem, st, X, n, k, ldx, rows_per_chunk, T, partial);
+    } else if (vec16(X, ldx) && k % 2 == 0)
         LAUNCH(gram_tn_kernel<2>, dim3(ntiles, nchunks), 128, smem, st, X, n, k, ldx, rows_per_chunk, T, partial);
     else
         LAUNCH(gram_tn_kernel<1>, dim3(ntiles, nchunks), 128, smem, st, X, n, k, ldx, rows_per_chunk, T, partial);

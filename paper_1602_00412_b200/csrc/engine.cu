@@ -17,6 +17,7 @@
 // in one d x 2lp buffer so [B; B'] never has to be materialised for dense_shrink.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -503,6 +504,8 @@ void Engine::simultaneous_iteration(int k, const PowerCfg& cfg) {
         CK(cudaMemcpyAsync(h_scal + 48, d_scal + 16 + 3, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         orth_interval = next_orth_interval(h_scal[48], 1);
+        static const bool dbg = std::getenv("SFDG_DEBUG_KAPPA") != nullptr;
+        if (dbg) std::fprintf(stderr, "sfdg probe: m=%d kappa after one sweep %.3e -> interval %d\n", m, h_scal[48], orth_interval);
         last_since = 1;
         s = 1;
     }
@@ -663,7 +666,10 @@ void Engine::verify_enqueue(Verifier& v, double delta_hat, const double* bpt, in
             g_launches.fetch_sub(g.kernels, std::memory_order_relaxed);
             it = vgraphs.emplace(key, g).first;
         }
-        CK(cudaGraphLaunch(it->second.exec, vs));
+        {
+            ProfScope prof("verify", vs);  // the whole captured sequence (3 kernels per power step)
+            CK(cudaGraphLaunch(it->second.exec, vs));
+        }
         g_launches.fetch_add(it->second.kernels, std::memory_order_relaxed);
         if (prio) {
             CK(cudaEventRecord(ev_v1, vst));

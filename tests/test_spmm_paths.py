@@ -35,3 +35,25 @@ def test_graphs_on_and_off_are_bit_identical(monkeypatch):
     monkeypatch.setenv("SFDG_GRAPHS", "0")
     b_n, st_n = _sketch(rp, cs, vs, 3000, 64, 1)
     assert np.array_equal(b_g, b_n) and st_g == st_n
+
+
+@pytest.mark.parametrize("family,d,ell,rows", [("c4", 3000, 64, 6000), ("c2", 4000, 100, 12000), ("c5", 2000, 200, 4000)])
+def test_gram_tma_and_cp_async_are_bit_identical(monkeypatch, family, d, ell, rows):
+    """The Gram's stages arrive by per-thread cp.async (default) or TMA bulk copies
+    (SFDG_GRAM=tma): the same tiles, chunks and DMMA order, so the same bits -- including edge
+    tiles (lp = 104 / 200: a 40- / 8-column last tile) and chunk tails."""
+    rp, cs, vs = S.generate(S.StreamConfig(family, rows, d, ell, 7), (0, rows))
+    b_c, st_c = _sketch(rp, cs, vs, d, ell, 2)
+    monkeypatch.setenv("SFDG_GRAM", "tma")
+    b_t, st_t = _sketch(rp, cs, vs, d, ell, 2)
+    assert np.array_equal(b_t, b_c) and st_t == st_c
+
+
+def test_gram_tma_dense_shrink_and_orthonormalize(monkeypatch):
+    g = np.random.default_rng(11)
+    a = g.standard_normal((333, 1001))  # 2 lp-wide Grams with odd row counts
+    y = g.standard_normal((20011, 136))
+    d_c, q_c = P.dense_shrink(a, 150), P.orthonormalize(y)
+    monkeypatch.setenv("SFDG_GRAM", "tma")
+    d_t, q_t = P.dense_shrink(a, 150), P.orthonormalize(y)
+    assert np.array_equal(d_t, d_c) and np.array_equal(q_t, q_c)

@@ -114,6 +114,20 @@ int main(int argc, char** argv) {
                chol_factor(G, lp, lp, R, R + lp * lp / 2, K, lp, st4, err, 1, s2, st, true);
            }));
     printf("gemm m x lp %8.2f us\n", time_us(st, reps, [&] { gemm_nn(Y, m, lp, lp, R, lp, lp, Y2, lp, st); }));
+    {  // CholeskyQR apply: X = Y R^-1 (trinv + triangular DMMA GEMM, the engine's default)
+        double *Rf, *D8, *Tinv;
+        cudaMalloc(&Rf, (size_t)lp * lp * 8);
+        cudaMalloc(&D8, (size_t)lp * 8 * 8);
+        cudaMalloc(&Tinv, (size_t)lp * lp * 8);
+        gram_tn(Y, m, lp, lp, G, lp, s2, st);
+        chol_factor(G, lp, lp, Rf, D8, nullptr, 0, st4, err, 1, s2, st, false);
+        printf("trsm m x lp %8.2f us\n", time_us(st, reps, [&] {
+                   trsm_apply(Y, m, lp, lp, Rf, D8, Y2, lp, nullptr, st, Tinv);
+               }));
+        cudaFree(Rf);
+        cudaFree(D8);
+        cudaFree(Tinv);
+    }
     for (int n : {ell, 2 * ell}) {
         double* vals_d;
         double* vecs;
