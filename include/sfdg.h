@@ -88,7 +88,8 @@ int sfdg_device_count(int* count);
 
 /* ---- SfdSketcher (sketch.hpp:22-49; sketch.cpp:9-45) -------------------------- */
 
-/* SfdSketcher(const SketchConfig&): validates (1 <= ell <= d, 0 < delta < 1). */
+/* SfdSketcher(const SketchConfig&): validates (1 <= ell <= d, 0 < delta < 1); this build also
+ * requires ell <= 512 (SFDG_INVALID_ARGUMENT above: the eigensolver / CholeskyQR limits). */
 int sfdg_sketcher_create(const sfdg_sketch_config* cfg, int device, sfdg_sketcher** out);
 int sfdg_sketcher_destroy(sfdg_sketcher* h);
 
@@ -184,7 +185,7 @@ int sfdg_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* val
                  const double* b, size_t ell, size_t iterations, sfdg_rng_state* rng, double* out, int device);
 /* exact_tail(a, k, rng) (bench.hpp:51-55, bench.cpp:68-137): the ground-truth tail
  * |A - A_k|_F^2 and the top-k singular values of the whole stream by block power iteration
- * (block k + 10 <= 256, <= 1000 sweeps, the reference's convergence tests); *sweeps_out = the
+ * (block k + 10 <= 512, <= 1000 sweeps, the reference's convergence tests); *sweeps_out = the
  * sweeps run (nullable). k = 0 returns |A|_F^2. rng advanced in place. */
 int sfdg_exact_tail(const int64_t* row_ptr, const uint32_t* cols, const double* vals, size_t n, size_t d, size_t k,
                     sfdg_rng_state* rng, double* sigma_out, double* tail_out, size_t* sweeps_out, int device);
