@@ -303,10 +303,10 @@ def main():
 
     sk = P.SfdSketcher(P.SketchConfig(ell=ell, d=d, seed=seed), device=device)
 
-    def step_device(s=sk):
+    def step_device(s=sk, merge=True):
         s.append_csr_device(rp, d_cols.data_ptr(), d_vals.data_ptr())
         s.finalize_device()
-        if world > 1:
+        if world > 1 and merge:  # every rank takes part in the tree, or none does
             merge_tree(torch, dist, s, d, ell, device, rank, world)
 
     def step_host():
@@ -384,7 +384,7 @@ def main():
         del os.environ["SFDG_LANES"]
         torch.cuda.synchronize(device)
         P.profile_begin()
-        step_device(s1)
+        step_device(s1, merge=False)  # rank 0 alone: its shard's sketch, no tree
         iso = P.profile_end()
         s1.close()
     accuracy = None

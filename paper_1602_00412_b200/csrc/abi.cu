@@ -516,7 +516,9 @@ class Sketcher {
     };
 
     // Flushes in flight: 4, or fewer when 4 lanes' working sets (CSR + CSC of ell*d nnz,
-    // Y/Yt of d x lp, W/B' of d x lp, a share of the Rng ring) would exceed 30% of the HBM.
+    // Y/Yt of d x lp, W/B' of d x lp, a share of the Rng ring) would exceed 20% of the HBM.
+    // Lanes that big have panels far beyond L2: their SpMMs are HBM-bound and extra lanes only
+    // contend (c5 shard, 16 GB per lane: 2 lanes 6.70 s, 3 lanes 6.89 s, 4 lanes 6.94 s).
     // SFDG_LANES overrides (1 = one flush at a time); the results are the same either way.
     int lane_count() const {
         if (const char* e = std::getenv("SFDG_LANES")) return std::max(1, std::min((int)kLag, std::atoi(e)));
@@ -524,7 +526,7 @@ class Sketcher {
         const double per_lane = 24.0 * ((double)cfg.ell * cfg.d + cfg.d) + 32.0 * cfg.d * lp + 8.0 * cfg.d * (cfg.ell + 1);
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
-        const int fit = (int)std::floor(0.3 * (double)total_b / std::max(per_lane, 1.0));
+        const int fit = (int)std::floor(0.2 * (double)total_b / std::max(per_lane, 1.0));
         return std::max(1, std::min(kDefaultLanes, fit));
     }
 

@@ -82,6 +82,34 @@ inline void launch_kernel(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
+// Same launch with an L2 access-policy window: [base, base + bytes) persisting in L2, the
+// kernel's other accesses streaming (SpMM panels far larger than L2: the hot columns' rows).
+template <class... KArgs, class... Args>
+inline void launch_kernel_l2win(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                const void* base, size_t bytes, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[na].val.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    at[na].val.accessPolicyWindow.num_bytes = bytes;
+    at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    CK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                                                \
     do {                                                                                              \
         ::sfdg::launch_kernel(kernel, dim3(grid), dim3(block), (size_t)(smem), (stream), __VA_ARGS__); \

@@ -20,7 +20,7 @@ namespace sfdg {
 constexpr double kAlpha = 6.0 / 41.0;  // core/include/sfd/common.hpp:10
 constexpr size_t kRetryCap = 64;       // core/src/shrink.cpp:12
 constexpr int kMaxEll = 512;           // 2*ell <= 1024: the eigensolver and CholeskyQR limits
-constexpr double kKappaTarget = 1e4;   // cond(Y) allowed to build up between CholeskyQR2 passes
+constexpr double kKappaTarget = 1e5;   // cond(Y) allowed to build up between CholeskyQR2 passes
 constexpr double kKappaUnsafe = 1e7;   // above this CholeskyQR2 may lose orthogonality: redo
 constexpr int kMaxInterval = 8;
 

@@ -12,6 +12,9 @@
 //    W = A'^T Y (rmatvec/project_rows, sparse.cpp:45-69).
 #include <algorithm>
 
+#include <mutex>
+#include <set>
+#include <cstdlib>
 #include "common.cuh"
 #include "sparse.cuh"
 
@@ -670,6 +673,28 @@ void SegPlan::release() {
     cap_pieces = 0;
 }
 
+namespace {
+// Persisting-L2 window for a gathered panel of `panel` bytes (0 = none): only when SFDG_L2_WINDOW
+// asks for one and the panel is at least twice the L2, capped by the device's window and
+// persisting-carve-out limits (the carve-out is set once per device).
+size_t l2_window_bytes(size_t panel) {
+    static const size_t want = std::getenv("SFDG_L2_WINDOW") ? (size_t)std::atoll(std::getenv("SFDG_L2_WINDOW")) << 20 : 0;
+    if (want == 0 || panel == 0) return 0;
+    int dev = 0, l2 = 0, maxwin = 0, maxpers = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    if (panel < 2 * (size_t)l2) return 0;
+    CK(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    CK(cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    const size_t bytes = std::min({want, (size_t)maxwin, (size_t)maxpers, panel});
+    static std::mutex mu;
+    static std::set<int> done;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.insert(dev).second) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(want, (size_t)maxpers)));
+    return bytes;
+}
+}  // namespace
+
 void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, const SegPlan& plan, int64_t nnz,
           const double* d_in, int ld, int ncols, double* d_out, int ldo, Scratch& scr, cudaStream_t st,
           int64_t in_rows, int alg_cols, const HotSet* hot) {
@@ -716,6 +741,33 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
                 throw invalid_argument("spmm: panel wider than 512 columns");
         }
         return;
+    }
+    // SFDG_L2_WINDOW=<MB> (A/B testing): for the gather of a panel much larger than L2 in the CSR
+    // direction (rows of W by column id), keep its first MB -- the most frequent columns when the
+    // ids are frequency ranked -- persisting in L2
+    const size_t win = l2_window_bytes(in_rows >= 0 && hot ? (size_t)in_rows * ld * sizeof(double) : 0);
+    if (win > 0) {
+        switch (J) {
+#define SPMM_WIN(JJ)                                                                                               \
+    case JJ:                                                                                                       \
+        ::sfdg::launch_kernel_l2win((spmm_kernel<JJ, false>), dim3(grid), dim3(256), 0, st, (const void*)d_in, win,  \
+               d_ptr, d_idx, d_val, nrows, plan.piece_beg,                                                          \
+               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.order, use_pieces, \
+               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0);                                      \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                                                      \
+        return;
+            SPMM_WIN(1)
+            SPMM_WIN(2)
+            SPMM_WIN(3)
+            SPMM_WIN(4)
+            SPMM_WIN(5)
+            SPMM_WIN(6)
+            SPMM_WIN(7)
+            SPMM_WIN(8)
+#undef SPMM_WIN
+            default:
+                throw invalid_argument("spmm: panel wider than 512 columns");
+        }
     }
     switch (J) {
 #define SPMM_CASE(JJ)                                                                                              \
