@@ -629,9 +629,11 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VS
         old = __shfl_sync(0xffffffffu, old, 0);
         if (old == last - first - 1) {  // every piece of this row is written: sum them in order
             __threadfence();
+            // the whole warp sums the row's pieces: lane-strided, then a fixed shuffle tree
+            double tot = 0.0;
+            for (int q = first + lane; q < last; q += 32) tot += __ldcg(a.r_part + q);
+            tot = warp_sum(tot);
             if (lane == 0) {
-                double tot = 0.0;
-                for (int q = first; q < last; ++q) tot += __ldcg(a.r_part + q);
                 a.u[a.r_long_rows[li]] = tot;
                 a.r_arrive[li] = 0;  // ready for the next launch
             }
@@ -688,9 +690,10 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_colsum_kernel(VerifyArgs a, 
         old = __shfl_sync(0xffffffffu, old, 0);
         if (old == last - first - 1) {  // every piece of this column is written: sum them in order
             __threadfence();
+            double tot = 0.0;
+            for (int q = first + lane; q < last; q += 32) tot += __ldcg(a.lpart + q);
+            tot = warp_sum(tot);
             if (lane == 0) {
-                double tot = 0.0;
-                for (int q = first; q < last; ++q) tot += __ldcg(a.lpart + q);
                 a.w[a.long_cols[li]] = tot;
                 a.c_arrive[li] = 0;  // ready for the next launch
             }

@@ -2,7 +2,7 @@
 # c3 full-size parity + the c4 verifier's warm kernel durations against its traced wall time
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_fullsize_parity.py -q -p no:cacheprovider -k c3 --durations=5 2>&1 | tail -8
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_verify_spectral.py -q -p no:cacheprovider -x -k "verif" 2>&1 | tail -3
 SFDG_LANES=1 SFDG_TRACE=gpurun_out/tr_vg.jsonl timeout 600 python bench.py --config c4 --rows 300000 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-accuracy --no-isolated > gpurun_out/vg_l1.json 2>&1
 python tools/trace_report.py gpurun_out/tr_vg.jsonl
 SFDG_LANES=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -k regex:"vg_" --csv --log-file gpurun_out/vg_warm.csv python bench.py --config c4 --rows 150000 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-accuracy --no-isolated > gpurun_out/vg_ncu.log 2>&1
