@@ -295,10 +295,11 @@ def main():
     # device-resident copy (value) and pinned host copy (e2e)
     d_cols = torch.from_numpy(cs.view(np.int32)).to(f"cuda:{device}")
     d_vals = torch.from_numpy(vs).to(f"cuda:{device}")
-    h_cols = torch.from_numpy(cs.view(np.int32)).pin_memory()
-    h_vals = torch.from_numpy(vs).pin_memory()
-    h_cs = h_cols.numpy().view(np.uint32)
-    h_vs = h_vals.numpy()
+    if not a.no_e2e:  # pinned host copies only for the e2e leg (c5 full stream: 12.6 GB)
+        h_cols = torch.from_numpy(cs.view(np.int32)).pin_memory()
+        h_vals = torch.from_numpy(vs).pin_memory()
+        h_cs = h_cols.numpy().view(np.uint32)
+        h_vs = h_vals.numpy()
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")  # > 126 MB L2
 
     sk = P.SfdSketcher(P.SketchConfig(ell=ell, d=d, seed=seed), device=device)
