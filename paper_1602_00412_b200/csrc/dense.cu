@@ -392,15 +392,21 @@ __global__ void transpose_kernel(const double* __restrict__ in, int rows, int co
                                  int ldo) {
     pdl_entry();
     __shared__ double tile[32][33];
-    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
-    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-        const int r = by + j, c = bx + threadIdx.x;
-        if (r < rows && c < cols) tile[j][threadIdx.x] = in[(size_t)r * ldi + c];
-    }
-    __syncthreads();
-    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
-        const int r = bx + j, c = by + threadIdx.x;  // out row = in col
-        if (r < cols && c < rows) out[(size_t)r * ldo + c] = tile[threadIdx.x][j];
+    // 32 x 32 tiles in a flat block-stride loop: any rows x cols (a d-row panel has d / 32 tile
+    // rows, past the 65535 limit of a grid's y dimension at d > 2.1e6)
+    const int64_t tc = (cols + 31) / 32, ntile = tc * (((int64_t)rows + 31) / 32);
+    for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+        const int bx = (int)(t % tc) * 32, by = (int)(t / tc) * 32;
+        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+            const int r = by + j, c = bx + threadIdx.x;
+            if (r < rows && c < cols) tile[j][threadIdx.x] = in[(size_t)r * ldi + c];
+        }
+        __syncthreads();
+        for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+            const int r = bx + j, c = by + threadIdx.x;  // out row = in col
+            if (r < cols && c < rows) out[(size_t)r * ldo + c] = tile[threadIdx.x][j];
+        }
+        __syncthreads();
     }
 }
 
@@ -510,8 +516,9 @@ void scale_vector(double* x, int64_t n, double s, cudaStream_t st) {
 
 void transpose(const double* in, int rows, int cols, int ldi, double* out, int ldo, cudaStream_t st) {
     if (rows <= 0 || cols <= 0) return;
-    LAUNCH(transpose_kernel, dim3(ceil_div(cols, 32), ceil_div(rows, 32)), dim3(32, 8), 0, st, in, rows, cols, ldi, out,
-           ldo);
+    const size_t ntile = (size_t)ceil_div((size_t)cols, 32) * (size_t)ceil_div((size_t)rows, 32);
+    LAUNCH(transpose_kernel, (unsigned)std::min<size_t>(ntile, 16 * kSMs * 8), dim3(32, 8), 0, st, in, rows, cols, ldi,
+           out, ldo);
 }
 
 void copy2d(const double* in, int rows, int cols, int ldi, double* out, int ldo, cudaStream_t st) {

@@ -85,3 +85,31 @@ def test_wide_ell_stream_vs_oracle(oracle, family, d, ell, rows):
 def test_ell_above_build_limit_rejected():
     with pytest.raises(P.InvalidArgument):
         P.SfdSketcher(P.SketchConfig(ell=513, d=2000, seed=0))
+
+
+def test_large_d_stream_vs_oracle(oracle):
+    """A wide, very sparse stream (d = 2e7 columns, ell = 3): panels of 2e7 x 8 doubles, the
+    draw of d x ell = 6e7 normals per attempt, column ids above 2^24 -- the column and panel
+    indexing at sizes the BASELINE configs do not reach (c5: d = 1e6)."""
+    d, ell, rows = 20_000_000, 3, 40
+    g = np.random.default_rng(9)
+    rp = [0]
+    cs, vs = [], []
+    for _ in range(rows):
+        c = np.sort(g.choice(d, size=g.integers(1, 6), replace=False))
+        cs.append(c)
+        vs.append(g.standard_normal(c.size))
+        rp.append(rp[-1] + c.size)
+    rp, cs, vs = np.array(rp, np.int64), np.concatenate(cs).astype(np.uint32), np.concatenate(vs)
+    s = P.SfdSketcher(P.SketchConfig(ell=ell, d=d, seed=5))
+    s.append_csr(rp, cs, vs)
+    b = s.finalize()
+    st = s.stats()
+    s.close()
+    bo, so = oracle.sketch(rp, cs, vs, d, ell, seed=5)
+    for key in ("flushes", "attempts", "verifier_i", "delta_spent"):
+        assert st[key] == so[key], key
+    # B^T B is d x d here: compare through the 2 ell x 2 ell form of the difference
+    r = np.linalg.qr(np.vstack([b, bo]).T, mode="r")
+    x = r[:, :ell] @ r[:, :ell].T - r[:, ell:] @ r[:, ell:].T
+    assert np.linalg.norm(x) <= BTB_TOL * np.linalg.norm(bo @ bo.T)

@@ -27,10 +27,12 @@ def union(iv):
     return tot
 
 
-def main(path, last=0):
+def main(path, last=0, skip=-1):
     rows = [json.loads(l) for l in open(path) if l.strip()]
-    if last:  # only the last `last` flushes (e.g. the timed step of a bench run)
-        chain = sorted((r for r in rows if r["phase"] == "dense_shrink"), key=lambda r: r["gpu_end_us"])[-last:]
+    if last:  # only the last `last` flushes (e.g. the timed step of a bench run), or `last`
+        # flushes after the first `skip` ones (a bench run's timed step between warm-up and profile)
+        chain = sorted((r for r in rows if r["phase"] == "dense_shrink"), key=lambda r: r["gpu_end_us"])
+        chain = chain[-last:] if skip < 0 else chain[skip:skip + last]
         t_lo = min(r["gpu_start_us"] for r in chain)
         t_hi = max(r["gpu_end_us"] for r in chain)
         # the same flush ids recur across sketcher resets: keep intervals inside the step
@@ -51,4 +53,4 @@ def main(path, last=0):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 0, int(sys.argv[3]) if len(sys.argv) > 3 else -1)
