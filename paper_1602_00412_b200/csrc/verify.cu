@@ -574,6 +574,7 @@ __device__ int vg_decide(const VerifyArgs& a, VState* st, int s, int nblk, doubl
 // (ld.global.nc): x is read-only for the launch and L1 starts every launch invalid, so this is
 // safe in the kernel sequence (not in the persistent kernel); tools/spmv_lab.cu on the c4 flush:
 // 8 lanes L2-only 32.8 us, 16 lanes through L1 14.4 us.
+template <int G>
 __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VState* st, int step, int nblk) {
     pdl_entry();
     __shared__ double s_xs;
@@ -639,22 +640,21 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VS
             }
         }
     }
-    const int sub = lane & 15;
-    const int64_t g0 = gw * 2 + (lane >> 4), ng = nw * 2;
+    // G lanes per row (32 / G rows per warp in flight), four entries per lane in flight
+    const int sub = lane & (G - 1);
+    const int64_t g0 = gw * (32 / G) + lane / G, ng = nw * (32 / G);
     for (int64_t gi = g0; gi < ns; gi += ng) {
         const int r = a.r_counts ? a.r_order[gi] : (int)gi;
         const int kb = a.row_ptr[r], ke = a.row_ptr[r + 1];
         double sp[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int k = kb + sub; k < ke; k += 64) {
+        for (int k = kb + sub; k < ke; k += 4 * G) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (k + 16 * u < ke) sp[u] = fma(a.val[k + 16 * u], __ldg(x + a.col[k + 16 * u]), sp[u]);
+                if (k + G * u < ke) sp[u] = fma(a.val[k + G * u], __ldg(x + a.col[k + G * u]), sp[u]);
         }
         double t = (sp[0] + sp[1]) + (sp[2] + sp[3]);
-        t += __shfl_xor_sync(0xffffffffu, t, 8);
-        t += __shfl_xor_sync(0xffffffffu, t, 4);
-        t += __shfl_xor_sync(0xffffffffu, t, 2);
-        t += __shfl_xor_sync(0xffffffffu, t, 1);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (sub == 0) a.u[r] = t;
     }
 }
@@ -663,6 +663,7 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VS
 // last piece of a column sums them in piece order), then the short columns longest first, sixteen
 // lanes per column with four entries each in flight; u through L1 (read-only in this launch).
 // Each w_c is a per-column sum in a fixed order, so which warp computes it does not matter.
+template <int G>
 __global__ void __launch_bounds__(kGRowsThreads) vg_colsum_kernel(VerifyArgs a, const VState* __restrict__ st) {
     pdl_entry();
     if (st->done) return;
@@ -699,22 +700,20 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_colsum_kernel(VerifyArgs a, 
             }
         }
     }
-    const int sub = lane & 15;
-    const int64_t g0 = gw * 2 + (lane >> 4), ng = nw * 2;
+    const int sub = lane & (G - 1);
+    const int64_t g0 = gw * (32 / G) + lane / G, ng = nw * (32 / G);
     for (int64_t gi = g0; gi < ns; gi += ng) {
         const int c = a.c_order ? a.c_order[gi] : (int)gi;
         const int kb = a.col_ptr[c], ke = a.col_ptr[c + 1];
         double sp[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int k = kb + sub; k < ke; k += 64) {
+        for (int k = kb + sub; k < ke; k += 4 * G) {
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (k + 16 * u < ke) sp[u] = fma(a.cval[k + 16 * u], __ldg(a.u + a.row_idx[k + 16 * u]), sp[u]);
+                if (k + G * u < ke) sp[u] = fma(a.cval[k + G * u], __ldg(a.u + a.row_idx[k + G * u]), sp[u]);
         }
         double t = (sp[0] + sp[1]) + (sp[2] + sp[3]);
-        t += __shfl_xor_sync(0xffffffffu, t, 8);
-        t += __shfl_xor_sync(0xffffffffu, t, 4);
-        t += __shfl_xor_sync(0xffffffffu, t, 2);
-        t += __shfl_xor_sync(0xffffffffu, t, 1);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (sub == 0) a.w[c] = t;
     }
 }
@@ -1020,9 +1019,13 @@ void verify_sequence(const VerifyArgs& a, void* state, int nblk, int sms, cudaSt
     const unsigned rgrid = (unsigned)std::max<int64_t>((a.ell + 7) / 8, std::min<int64_t>(6 * sms, (a.m + 31) / 32));
     const unsigned rgrid2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(6 * sms, (a.d + 31) / 32));
     LAUNCH(vg_cols_fn<true>(a.ell), nblk, vg_cols_nthreads(a.ell), 0, st, a, s, 0);
+    // SFDG_VG_LANES=8|16|32: lanes per row / column in the two SpMVs (A/B testing)
+    static const int G = std::getenv("SFDG_VG_LANES") ? std::atoi(std::getenv("SFDG_VG_LANES")) : 16;
+    auto rows_fn = G == 8 ? vg_rows_kernel<8> : G == 32 ? vg_rows_kernel<32> : vg_rows_kernel<16>;
+    auto cols_fn = G == 8 ? vg_colsum_kernel<8> : G == 32 ? vg_colsum_kernel<32> : vg_colsum_kernel<16>;
     for (int step = 0; step < a.steps; ++step) {
-        LAUNCH(vg_rows_kernel, rgrid, kGRowsThreads, 0, st, a, s, step, nblk);
-        LAUNCH(vg_colsum_kernel, rgrid2, kGRowsThreads, 0, st, a, s);
+        LAUNCH(rows_fn, rgrid, kGRowsThreads, 0, st, a, s, step, nblk);
+        LAUNCH(cols_fn, rgrid2, kGRowsThreads, 0, st, a, s);
         LAUNCH(vg_cols_fn<false>(a.ell), nblk, vg_cols_nthreads(a.ell), 0, st, a, s, step);
     }
     LAUNCH(vg_final_kernel, 1, 32, 0, st, a, s, nblk);
