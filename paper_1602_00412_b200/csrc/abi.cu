@@ -516,9 +516,10 @@ class Sketcher {
     };
 
     // Flushes in flight: 4, or fewer when 4 lanes' working sets (CSR + CSC of ell*d nnz,
-    // Y/Yt of d x lp, W/B' of d x lp, a share of the Rng ring) would exceed 20% of the HBM.
-    // Lanes that big have panels far beyond L2: their SpMMs are HBM-bound and extra lanes only
-    // contend (c5 shard, 16 GB per lane: 2 lanes 6.70 s, 3 lanes 6.89 s, 4 lanes 6.94 s).
+    // Y/Yt of d x lp, W/B' of d x lp, a share of the Rng ring) would exceed 20% of the HBM;
+    // 2 when an ell-wide panel (d x lp doubles) is larger than the L2: those SpMMs gather from
+    // HBM and extra lanes only contend for it (c5 shard: 2 lanes 6.70 s, 3 lanes 6.89 s, 4 lanes
+    // 6.94 s; c3, 6 flushes: 1098 / 1105 / 1146 ms; c4, panels in L2: 3, 4, 6 lanes equal).
     // SFDG_LANES overrides (1 = one flush at a time); the results are the same either way.
     int lane_count() const {
         if (const char* e = std::getenv("SFDG_LANES")) return std::max(1, std::min((int)kLag, std::atoi(e)));
@@ -527,7 +528,11 @@ class Sketcher {
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
         const int fit = (int)std::floor(0.2 * (double)total_b / std::max(per_lane, 1.0));
-        return std::max(1, std::min(kDefaultLanes, fit));
+        int dev = 0, l2 = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+        const int cap = 8.0 * cfg.d * lp > (double)l2 ? 2 : kDefaultLanes;
+        return std::max(1, std::min(cap, fit));
     }
 
     size_t buf_rows() const { return lanes[fill].rows(); }
