@@ -57,6 +57,35 @@ __global__ void __launch_bounds__(256) grp_kernel(const int* __restrict__ ptr, c
     }
 }
 
+// the rows stored in the processing (LPT) order: start offsets in the permuted storage, so the
+// chain is start -> entries -> x; the output index is an independent load
+template <int G, int U>
+__global__ void __launch_bounds__(256) perm_kernel(const int* __restrict__ pptr, const int* __restrict__ col,
+                                                   const double* __restrict__ val, const int* __restrict__ order,
+                                                   int n, const double* __restrict__ x, double* __restrict__ u) {
+    const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / G;
+    for (int64_t gi = gw; gi < n; gi += ng) {
+        const int kb = pptr[gi], ke = pptr[gi + 1];
+        const int r = order[gi];
+        double sp[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) sp[q] = 0.0;
+        for (int k = kb + sub; k < ke; k += G * U) {
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (k + G * q < ke) sp[q] = fma(val[k + G * q], __ldg(x + col[k + G * q]), sp[q]);
+        }
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < U; ++q) t += sp[q];
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (sub == 0) u[r] = t;
+    }
+}
+
 template <class T>
 static T* dev(const std::vector<T>& h) {
     T* d = nullptr;
@@ -160,6 +189,32 @@ int main(int argc, char** argv) {
             {"grp32 U4 ldg LPT", grp_kernel<32, true, 4>, 32, true},  {"grp32 U2 ldcg LPT", grp_kernel<32, false, 2>, 32, true},
             {"grp4 U4 ldg LPT", grp_kernel<4, true, 4>, 4, true},     {"grp2 U8 ldg LPT", grp_kernel<2, true, 8>, 2, true},
         };
+        {  // permuted storage in LPT order
+            std::vector<int> pptr(O->n + 1, 0), pidx;
+            std::vector<double> pv;
+            for (int gi = 0; gi < O->n; ++gi) {
+                const int r = ord[gi];
+                for (int k = O->ptr[r]; k < O->ptr[r + 1]; ++k) {
+                    pidx.push_back(O->idx[k]);
+                    pv.push_back(O->v[k]);
+                }
+                pptr[gi + 1] = (int)pidx.size();
+            }
+            int *dpp = dev(pptr), *dpi = dev(pidx);
+            double* dpv = dev(pv);
+            for (int bps : {4, 6, 8}) {
+                const int grid = bps * sms;
+                CKL(cudaMemset(du, 0, O->n * 8));
+                double t = time_us(reps, [&] { perm_kernel<16, 4><<<grid, 256>>>(dpp, dpi, dpv, dord, O->n, dx, du); });
+                printf("[%s] %-22s %d blk/SM  %7.1f us  maxrel %.1e\n", O->name, "perm16 U4 ldg LPT", bps, t, check());
+                CKL(cudaMemset(du, 0, O->n * 8));
+                t = time_us(reps, [&] { perm_kernel<8, 4><<<grid, 256>>>(dpp, dpi, dpv, dord, O->n, dx, du); });
+                printf("[%s] %-22s %d blk/SM  %7.1f us  maxrel %.1e\n", O->name, "perm8 U4 ldg LPT", bps, t, check());
+            }
+            cudaFree(dpp);
+            cudaFree(dpi);
+            cudaFree(dpv);
+        }
         for (const V& v : vs) {
             for (int bps : {4, 6, 8}) {
                 const int grid = bps * sms;
