@@ -341,8 +341,9 @@ void Engine::load_csr(const int64_t* row_ptr, const uint32_t* cols, const double
 
 void Engine::prepare_async() {
     build_transpose(a, scr, st);
-    plan_r.build(a.row_ptr, a.m, a.nnz, scr, st);
-    plan_c.build(a.col_ptr, a.d, a.nnz, scr, st);
+    // CSR pieces gather W rows by column, CSC pieces Y rows by row
+    plan_r.build(a.row_ptr, a.m, a.nnz, scr, st, (const int*)a.col, d, (size_t)d * lp * sizeof(double));
+    plan_c.build(a.col_ptr, a.d, a.nnz, scr, st, a.row_idx, a.m, (size_t)a.m * lp * sizeof(double));
     // one small read-back per flush lets every SpMM skip the long-row kernels when unused
     CK(cudaMemcpyAsync(h_counts, plan_r.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_counts + 2, plan_c.counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -436,7 +437,7 @@ void Engine::sweep_block(int interval, int m) {
         for (const void* p : {(const void*)pl->partial, (const void*)pl->arrive, (const void*)pl->piece_beg,
                               (const void*)pl->piece_end, (const void*)pl->piece_li, (const void*)pl->long_rows,
                               (const void*)pl->long_first, (const void*)pl->counts,
-                              (const void*)(uintptr_t)(pl->host_long != 0)})
+                              (const void*)(uintptr_t)(pl->host_long != 0), (const void*)pl->piece_order()})
             key.push_back((uintptr_t)p);
     key.push_back((uintptr_t)hot.n);
     key.push_back((uintptr_t)hot.idx);

@@ -254,6 +254,31 @@ __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int pie
     }
 }
 
+// Pieces by the first input index they gather, in kPieceBuckets coarse buckets (counting sort;
+// the order inside a bucket is arbitrary). Only which warp runs a piece, and when, changes: the
+// partials are indexed by piece and summed in piece order, so results do not depend on it.
+constexpr int kPieceBuckets = 1024;
+__global__ void piece_order_kernel(const int* __restrict__ counts, const int* __restrict__ key,
+                                   int64_t* __restrict__ bin_off, int* __restrict__ porder) {
+    pdl_entry();
+    const int np = counts[1];
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x)
+        porder[bin_slot(bin_off, key[p])] = p;
+}
+
+// Key of a piece: the coarse bucket of the first input index it gathers.
+__global__ void piece_key_kernel(const int* __restrict__ counts, const int* __restrict__ piece_beg,
+                                 const int* __restrict__ idx, int range, int* __restrict__ key,
+                                 int64_t* __restrict__ bins) {
+    pdl_entry();
+    const int np = counts[1];
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+        const int k = (int)min((int64_t)kPieceBuckets - 1, (int64_t)idx[piece_beg[p]] * kPieceBuckets / range);
+        key[p] = k;
+        bin_slot(bins, k);
+    }
+}
+
 // ---------------------------------------------------------------- SpMM
 // J = number of 64-column chunks (lane owns columns 2*lane + 64*j, +1). HOT: idx is relabelled
 // (HotSet): entries < nh read the staged row in shared memory (hot + i * ldh), the others row
@@ -373,7 +398,8 @@ __global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT
     const int* __restrict__ piece_beg, const int* __restrict__ piece_end, const int* __restrict__ piece_li,
     const int* __restrict__ long_rows, const int* __restrict__ long_first, const int* __restrict__ counts,
     int* __restrict__ arrive, const int* __restrict__ order, int use_pieces, const double* __restrict__ in, int ld, int ncols,
-    double* __restrict__ out, int ldo, double* __restrict__ partial, const int* __restrict__ hot_cols, int nh) {
+    double* __restrict__ out, int ldo, double* __restrict__ partial, const int* __restrict__ hot_cols, int nh,
+    const int* __restrict__ porder) {
     extern __shared__ __align__(128) double hot_sm[];
     __shared__ uint64_t hot_bar;
     if constexpr (HOT) {
@@ -393,15 +419,16 @@ __global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT
 #pragma unroll
         for (int j = 0; j < J; ++j) acc[j] = make_double2(0.0, 0.0);
         if (w < np) {
-            gather_range<J, HOT, NB>(piece_beg[w], piece_end[w], idx, val, in, ld, ncols, lane, acc, hot_sm, nh,
+            const int pc = porder ? porder[w] : w;  // the piece this warp runs
+            gather_range<J, HOT, NB>(piece_beg[pc], piece_end[pc], idx, val, in, ld, ncols, lane, acc, hot_sm, nh,
                                      ncols);
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int c = 2 * lane + 64 * j;
-                if (c < ncols) *reinterpret_cast<double2*>(partial + (size_t)w * ld + c) = acc[j];
+                if (c < ncols) *reinterpret_cast<double2*>(partial + (size_t)pc * ld + c) = acc[j];
             }
             __threadfence();
-            const int li = piece_li[w];
+            const int li = piece_li[pc];
             const int first = long_first[li], last = li + 1 < nl ? long_first[li + 1] : np;
             int old = 0;
             if (lane == 0) old = atomicAdd(arrive + li, 1);
@@ -607,12 +634,13 @@ int spmm_piece_length(int64_t nnz) {
     return piece;
 }
 
-void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st) {
+void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st, const int* d_idx,
+                    int idx_range, size_t panel_bytes) {
     ProfScope prof("csc_build", st);
     rows = nrows;
     host_long = -1;
     piece = spmm_piece_length(nnz);
-    reserve_pieces(nnz);
+    reserve_pieces(2 * (nnz / kPiece) + 2);  // any piece length >= kPiece
     if (nrows > cap_rows) {
         for (void* p : {(void*)long_rows, (void*)long_first, (void*)arrive, (void*)order}) if (p) cudaFree(p);
         CK(cudaMalloc(&long_rows, (size_t)nrows * sizeof(int)));
@@ -623,6 +651,7 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
         cap_rows = nrows;
     }
     host_pieces = -1;
+    has_porder = false;
     if (!counts) CK(cudaMalloc(&counts, 3 * sizeof(int)));
     CK(cudaMemsetAsync(counts, 0, 3 * sizeof(int), st));
     if (nrows == 0) return;
@@ -642,15 +671,40 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     // pieces <= nnz / piece + nrows; size the piece arrays for the worst case of this call
     LAUNCH(plan_fill_kernel, g, 256, 0, st, d_ptr, nrows, piece, is_long, long_off, piece_off, long_rows, long_first,
            piece_beg, piece_end, piece_li, counts, bin_off, order);
+    // Pieces in the order of the first input index they gather (porder), for panels larger
+    // than the L2 (c3, c5): the grid then works on pieces of many long rows over nearby panel
+    // rows at a time (c5 CSC: DRAM 41.6 -> 36.8 GB per launch, L2 hits 3 -> 10 %; c3 stream
+    // 3725 -> 3454 ms; c5 shard 6160 -> 5893 ms). An L2-resident panel (c4) gains nothing and its
+    // standalone launch got slower (146 -> 156 us). Cutting long rows at window boundaries of
+    // the gathered index as well (tools/porder_ab.sh) kept the L2 hit rate at 10 % and was slower:
+    // 7000 warps x `piece` entries in flight span a third of the panel whatever the window.
+    // SFDG_PIECE_ORDER=0 / 1 forces it off / on (A/B testing).
+    const char* po_env = std::getenv("SFDG_PIECE_ORDER");
+    int l2 = 0, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    const bool pord = po_env ? std::atoi(po_env) != 0 : panel_bytes > (size_t)l2;
+    has_porder = pord && d_idx && idx_range > 0 && nnz > 2 * piece;
+    if (has_porder) {
+        int* key = scr.take<int>(cap_pieces);
+        int64_t* pb = scr.take<int64_t>(kPieceBuckets);
+        int64_t* po = scr.take<int64_t>(kPieceBuckets);
+        CK(cudaMemsetAsync(pb, 0, kPieceBuckets * sizeof(int64_t), st));
+        const unsigned gp = std::max(1u, std::min(8u * kSMs, ceil_div((size_t)cap_pieces, 256)));
+        LAUNCH(piece_key_kernel, gp, 256, 0, st, counts, piece_beg, d_idx, idx_range, key, pb);
+        exclusive_scan(pb, po, kPieceBuckets, scr, st);
+        LAUNCH(piece_order_kernel, gp, 256, 0, st, counts, key, po, porder);
+    }
 }
-void SegPlan::reserve_pieces(int64_t nnz) {
-    const int64_t need = 2 * (nnz / kPiece) + 2;  // any piece length >= kPiece
+
+void SegPlan::reserve_pieces(int64_t need) {
     if (need > cap_pieces) {
-        for (void* p : {(void*)piece_beg, (void*)piece_end, (void*)piece_li}) if (p) cudaFree(p);
+        for (void* p : {(void*)piece_beg, (void*)piece_end, (void*)piece_li, (void*)porder}) if (p) cudaFree(p);
         cap_pieces = need;
         CK(cudaMalloc(&piece_beg, cap_pieces * sizeof(int)));
         CK(cudaMalloc(&piece_end, cap_pieces * sizeof(int)));
         CK(cudaMalloc(&piece_li, cap_pieces * sizeof(int)));
+        CK(cudaMalloc(&porder, cap_pieces * sizeof(int)));
     }
 }
 
@@ -666,9 +720,9 @@ void SegPlan::release() {
     partial = nullptr;
     partial_cap = 0;
     for (void* p : {(void*)long_rows, (void*)long_first, (void*)piece_beg, (void*)piece_end, (void*)piece_li,
-                    (void*)arrive, (void*)order, (void*)counts})
+                    (void*)arrive, (void*)order, (void*)counts, (void*)porder})
         if (p) cudaFree(p);
-    long_rows = long_first = piece_beg = piece_end = piece_li = arrive = order = counts = nullptr;
+    long_rows = long_first = piece_beg = piece_end = piece_li = arrive = order = counts = porder = nullptr;
     cap_rows = 0;
     cap_pieces = 0;
 }
@@ -725,7 +779,7 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
         if (first_on_device((const void*)fn)) allow_max_dynamic_smem(fn);                                            \
         LAUNCH(fn, (unsigned)sms, (spmm_threads<JJ, true>()), smem, st, d_ptr, hot->idx, d_val, nrows, plan.piece_beg, \
                plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.order, use_pieces,  \
-               d_in, ld, ncols, d_out, ldo, partial, hot->cols, hot->n);                                              \
+               d_in, ld, ncols, d_out, ldo, partial, hot->cols, hot->n, plan.piece_order());                     \
         break;                                                                                                        \
     }
             SPMM_HOT(1)
@@ -753,7 +807,7 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
         ::sfdg::launch_kernel_l2win((spmm_kernel<JJ, false>), dim3(grid), dim3(256), 0, st, (const void*)d_in, win,  \
                d_ptr, d_idx, d_val, nrows, plan.piece_beg,                                                          \
                plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.order, use_pieces, \
-               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0);                                      \
+               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0, plan.piece_order());            \
         g_launches.fetch_add(1, std::memory_order_relaxed);                                                      \
         return;
             SPMM_WIN(1)
@@ -774,7 +828,7 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
     case JJ:                                                                                                       \
         LAUNCH((spmm_kernel<JJ, false>), grid, 256, 0, st, d_ptr, d_idx, d_val, nrows, plan.piece_beg,             \
                plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.order, use_pieces, \
-               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0);                                      \
+               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0, plan.piece_order());            \
         break;
         SPMM_CASE(1)
         SPMM_CASE(2)

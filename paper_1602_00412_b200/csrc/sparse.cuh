@@ -114,6 +114,12 @@ struct SegPlan {
     int* piece_li = nullptr;  // long-row index of each piece
     int* arrive = nullptr;    // per long row: pieces finished in the current launch (self-resetting)
     int* order = nullptr;     // the short rows, longest first
+    // Processing order of the pieces (null: piece order): by the first input index a piece
+    // gathers (the row of a CSC piece, the column of a CSR piece) in coarse buckets, so the grid
+    // works on pieces of many long rows over the same window of the input panel at a time
+    int* porder = nullptr;
+    bool has_porder = false;  // porder filled by the last build
+    const int* piece_order() const { return has_porder ? porder : nullptr; }
     int* counts = nullptr;  // device [nlong, npieces, nshort]
     int host_long = -1;     // long rows as known on the host (-1: unknown -> always run the piece path)
     int64_t host_pieces = -1;  // pieces as known on the host (-1: unknown -> worst-case partial buffer)
@@ -124,8 +130,11 @@ struct SegPlan {
     void ensure_partial(int64_t doubles) const;
     int cap_rows = 0;
     int64_t cap_pieces = 0;
-    void build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st);
-    void reserve_pieces(int64_t nnz);
+    // d_idx / idx_range (optional): the gathered index array and its range, for porder, which
+    // is built when the gathered panel (panel_bytes) is larger than the L2
+    void build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st, const int* d_idx = nullptr,
+               int idx_range = 0, size_t panel_bytes = 0);
+    void reserve_pieces(int64_t need);  // piece arrays for >= need pieces
     void release();
     ~SegPlan() { release(); }
 };

@@ -57,3 +57,17 @@ def test_gram_tma_dense_shrink_and_orthonormalize(monkeypatch):
     monkeypatch.setenv("SFDG_GRAM", "tma")
     d_t, q_t = P.dense_shrink(a, 150), P.orthonormalize(y)
     assert np.array_equal(d_t, d_c) and np.array_equal(q_t, q_c)
+
+
+@pytest.mark.parametrize("family,d,ell,rows", [("c4", 3000, 64, 6000), ("c3", 2500, 96, 5000), ("c5", 4000, 128, 8000)])
+def test_piece_order_is_bit_identical(monkeypatch, family, d, ell, rows):
+    """Pieces of long rows / columns run in the order of the first input index they gather
+    (default for panels larger than L2; forced on here) or in piece order (SFDG_PIECE_ORDER=0):
+    which warp runs a piece, and when, changes; the partials are summed in piece order either
+    way, so the sketches are the same bits."""
+    rp, cs, vs = S.generate(S.StreamConfig(family, rows, d, ell, 8), (0, rows))
+    monkeypatch.setenv("SFDG_PIECE_ORDER", "1")
+    b_o, st_o = _sketch(rp, cs, vs, d, ell, 4)
+    monkeypatch.setenv("SFDG_PIECE_ORDER", "0")
+    b_n, st_n = _sketch(rp, cs, vs, d, ell, 4)
+    assert np.array_equal(b_o, b_n) and st_o == st_n
