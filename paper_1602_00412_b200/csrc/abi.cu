@@ -1549,12 +1549,13 @@ int sfdg_cov_err(const int64_t* row_ptr, const uint32_t* cols, const double* val
                  size_t ell, size_t iterations, sfdg_rng_state* rng, double* out, int device) {
     return guard([&] {
         if (!row_ptr || !b || !rng || !out) throw invalid_argument("cov_err: null argument");
-        if (ell < 1 || ell > (size_t)kMaxEll) throw invalid_argument("cov_err: sketch rows must be in [1, 512]");
+        if (ell < 1) throw invalid_argument("cov_err: sketch rows must be positive");
         if (d < 1 || d >= (size_t)INT32_MAX) throw invalid_argument("cov_err: dimension mismatch");
         validate_csr(row_ptr, cols, vals, n, d);
         require_device(device);
         const int64_t nnz = row_ptr[n] - row_ptr[0];
-        Engine e(device, (int)d, (int)ell, rng->seed, (uint64_t)std::max<int64_t>(nnz, 1), 1);
+        // the power step only needs the stream's CSR / CSC and 2-wide panels: any sketch height
+        Engine e(device, (int)d, 1, rng->seed, (uint64_t)std::max<int64_t>(nnz, 1), 1);
         rng_in(e, rng);
         e.load_csr(row_ptr, cols, vals, (int)n, nnz, /*panels=*/false);
         e.prepare();

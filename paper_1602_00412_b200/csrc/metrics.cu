@@ -145,7 +145,7 @@ double device_cov_err(Engine& e, const double* b_host, int ell, size_t iteration
     if (iterations < 1) throw invalid_argument("spectral_norm_sym: iterations must be >= 1");
     if (a_fsq == 0.0) return 0.0;  // bench.cpp:176
     const int d = e.d, m = e.a.m;
-    const int lp = e.lp;
+    const int lp = (int)round_up((size_t)ell, 8);  // the sketch's own width: any ell (the engine's is 2-wide)
     cudaStream_t st = e.st;
     Scratch& scr = e.scr;
     // B^T (d x lp) on the device

@@ -113,3 +113,13 @@ def test_large_d_stream_vs_oracle(oracle):
     r = np.linalg.qr(np.vstack([b, bo]).T, mode="r")
     x = r[:, :ell] @ r[:, :ell].T - r[:, ell:] @ r[:, ell:].T
     assert np.linalg.norm(x) <= BTB_TOL * np.linalg.norm(bo @ bo.T)
+
+
+def test_cov_err_any_sketch_height_vs_oracle(oracle):
+    """cov_err (bench.cpp:171-183) has no limit on the sketch's height: a 700-row B (above this
+    build's sketching limit of 512) against the oracle, same draws."""
+    rp, cs, vs = S.generate("c1", (0, 1500))
+    b = np.random.default_rng(12).standard_normal((700, 1000)) * 0.05
+    got, _ = P.cov_err((rp, cs, vs), 1000, b, P.RngState(31), iterations=150)
+    want = oracle.cov_err(rp, cs, vs, 1000, b, oracle.rng(31), 150)
+    assert abs(got - want) <= 1e-9 * abs(want)
