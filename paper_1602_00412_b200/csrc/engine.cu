@@ -434,7 +434,7 @@ void Engine::sweep_block(int interval, int m) {
                                (uintptr_t)W,         (uintptr_t)a.row_ptr, (uintptr_t)a.col,  (uintptr_t)a.val,
                                (uintptr_t)a.col_ptr, (uintptr_t)a.row_idx, (uintptr_t)a.cval, (uintptr_t)d};
     for (const SegPlan* pl : {&plan_r, &plan_c})
-        for (const void* p : {(const void*)pl->partial, (const void*)pl->arrive, (const void*)pl->piece_beg,
+        for (const void* p : {(const void*)pl->partial, (const void*)pl->arrive, (const void*)pl->garrive, (const void*)pl->piece_beg,
                               (const void*)pl->piece_end, (const void*)pl->piece_li, (const void*)pl->long_rows,
                               (const void*)pl->long_first, (const void*)pl->counts,
                               (const void*)(uintptr_t)(pl->host_long != 0), (const void*)pl->piece_order()})

@@ -379,6 +379,38 @@ __device__ __forceinline__ void stage_hot_rows(double* hot, const int* __restric
 // forming a tail.
 // Occupancy / loads in flight (tools/spmm_lab.cu on the c2-c5 flush buffers): ell <= 128
 // (J <= 2) four panel rows in flight per warp at 4 blocks per SM; wider panels two rows at 3.
+// dst[c] = sum of the partial rows p = first, first + step, ... < last, in that order, eight
+// rows in flight (read through L2: other SMs wrote them).
+template <int J>
+__device__ __forceinline__ void sum_partials(const double* partial, int ld, int first, int last, int step, int ncols,
+                                             int lane, double* dst) {
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int c = 2 * lane + 64 * j;
+        if (c < ncols) {
+            double2 t = make_double2(0.0, 0.0);
+            int p = first;
+            for (; p + 8 * step <= last; p += 8 * step) {
+                double2 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    v[u] = __ldcg(reinterpret_cast<const double2*>(partial + (size_t)(p + u * step) * ld + c));
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    t.x += v[u].x;
+                    t.y += v[u].y;
+                }
+            }
+            for (; p < last; p += step) {
+                const double2 v = __ldcg(reinterpret_cast<const double2*>(partial + (size_t)p * ld + c));
+                t.x += v.x;
+                t.y += v.y;
+            }
+            *reinterpret_cast<double2*>(dst + c) = t;
+        }
+    }
+}
+
 template <int J, bool HOT>
 constexpr int spmm_threads() {
     return HOT ? (J <= 2 ? 1024 : 512) : 256;
@@ -397,9 +429,9 @@ __global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT
     const int* __restrict__ ptr, const int* __restrict__ idx, const double* __restrict__ val, int nrows,
     const int* __restrict__ piece_beg, const int* __restrict__ piece_end, const int* __restrict__ piece_li,
     const int* __restrict__ long_rows, const int* __restrict__ long_first, const int* __restrict__ counts,
-    int* __restrict__ arrive, const int* __restrict__ order, int use_pieces, const double* __restrict__ in, int ld, int ncols,
+    int* __restrict__ arrive, int* __restrict__ garrive, const int* __restrict__ order, int use_pieces, const double* __restrict__ in, int ld, int ncols,
     double* __restrict__ out, int ldo, double* __restrict__ partial, const int* __restrict__ hot_cols, int nh,
-    const int* __restrict__ porder) {
+    const int* __restrict__ porder, int* __restrict__ ticket) {
     extern __shared__ __align__(128) double hot_sm[];
     __shared__ uint64_t hot_bar;
     if constexpr (HOT) {
@@ -414,7 +446,33 @@ __global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT
     const int nl = use_pieces ? counts[0] : 0;
     const int ns = counts[2];  // short rows (all rows when there are no long ones)
     constexpr int NB = spmm_batch<J>();
-    for (int w = warp; w < np + ns; w += nw) {
+    // Pieces either statically strided over the grid's warps or, with a ticket counter (gathered
+    // panels larger than L2), taken in order as warps become free: the pieces in flight then stay
+    // a window of consecutive pieces -- with the pieces in the order of the first index they
+    // gather, a window of the panel -- whatever the individual piece durations. The warp that
+    // leaves the piece phase last resets the counters for the next launch.
+    const bool dyn = ticket != nullptr && np > 0;
+    bool grabbing = dyn;
+    int sw = warp;
+    for (;;) {
+        int w;
+        if (grabbing) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(ticket, 1);
+            w = __shfl_sync(0xffffffffu, t, 0);
+            if (w >= np) {
+                grabbing = false;
+                if (lane == 0 && atomicAdd(ticket + 1, 1) == nw - 1) {
+                    ticket[0] = 0;
+                    ticket[1] = 0;
+                }
+                continue;
+            }
+        } else {
+            w = dyn ? np + sw : sw;
+            if (w >= np + ns) break;
+            sw += nw;
+        }
         double2 acc[J];
 #pragma unroll
         for (int j = 0; j < J; ++j) acc[j] = make_double2(0.0, 0.0);
@@ -430,40 +488,31 @@ __global__ void __launch_bounds__(spmm_threads<J, HOT>(), spmm_min_blocks<J, HOT
             __threadfence();
             const int li = piece_li[pc];
             const int first = long_first[li], last = li + 1 < nl ? long_first[li + 1] : np;
+            // Two-level sum, both levels in piece order (deterministic, no FP atomics): the piece
+            // that finishes a group of kPieceGroup consecutive pieces last sums the group, and the
+            // group that finishes the row last sums the group sums. A row of one group is summed
+            // straight into `out`.
+            const int gfirst = first + (pc - first) / kPieceGroup * kPieceGroup;
+            const int glast = min(gfirst + kPieceGroup, last);
             int old = 0;
+            if (lane == 0) old = atomicAdd(garrive + gfirst, 1);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old != glast - gfirst - 1) continue;
+            __threadfence();
+            if (lane == 0) garrive[gfirst] = 0;  // ready for the next launch
+            const bool single = last - first <= kPieceGroup;
+            const int r = long_rows[li];
+            sum_partials<J>(partial, ld, gfirst, glast, 1, ncols, lane,
+                            single ? out + (size_t)r * ldo : partial + (size_t)gfirst * ld);
+            if (single) continue;
+            __threadfence();
             if (lane == 0) old = atomicAdd(arrive + li, 1);
             old = __shfl_sync(0xffffffffu, old, 0);
-            if (old == last - first - 1) {  // every piece of this row is written: sum them in order
-                __threadfence();
-                const int r = long_rows[li];
-#pragma unroll
-                for (int j = 0; j < J; ++j) {
-                    const int c = 2 * lane + 64 * j;
-                    if (c < ncols) {
-                        // in piece order, eight partial rows in flight
-                        double2 t = make_double2(0.0, 0.0);
-                        int p = first;
-                        for (; p + 8 <= last; p += 8) {
-                            double2 v[8];
-#pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                v[u] = __ldcg(reinterpret_cast<const double2*>(partial + (size_t)(p + u) * ld + c));
-#pragma unroll
-                            for (int u = 0; u < 8; ++u) {
-                                t.x += v[u].x;
-                                t.y += v[u].y;
-                            }
-                        }
-                        for (; p < last; ++p) {
-                            const double2 v = __ldcg(reinterpret_cast<const double2*>(partial + (size_t)p * ld + c));
-                            t.x += v.x;
-                            t.y += v.y;
-                        }
-                        *reinterpret_cast<double2*>(out + (size_t)r * ldo + c) = t;
-                    }
-                }
-                if (lane == 0) arrive[li] = 0;  // ready for the next launch
-            }
+            const int ngroups = (last - first + kPieceGroup - 1) / kPieceGroup;
+            if (old != ngroups - 1) continue;
+            __threadfence();
+            if (lane == 0) arrive[li] = 0;
+            sum_partials<J>(partial, ld, first, last, kPieceGroup, ncols, lane, out + (size_t)r * ldo);
             continue;
         }
         const int r = order[w - np];
@@ -634,13 +683,46 @@ int spmm_piece_length(int64_t nnz) {
     return piece;
 }
 
+int spmm_big_piece_length(int piece, int64_t nnz, int64_t in_rows, size_t panel_bytes, size_t l2_bytes) {
+    // The pieces in flight are the resident warps' (kSMs x 3 blocks x 8 warps, one piece each);
+    // taken by ticket in the order of the first panel row they gather, they cover a window of
+    // about warps x piece / (entries per panel row) panel rows. That window has to stay in the
+    // L2 next to the streamed CSR / CSC arrays and the partial rows: a quarter of the L2.
+    // c5 CSC (2 GB panel, 21 entries per panel row): 64 entries, DRAM 36.7 -> 20.2 GB and 6.17 ->
+    // 3.90 ms per launch; c3 (160 MB panel, 110 entries per row) keeps its 512
+    // (profiles/r02f_piece_big_ab.txt). SFDG_PIECE_BIG=<entries> overrides (A/B testing).
+    static const int want = std::getenv("SFDG_PIECE_BIG") ? std::atoi(std::getenv("SFDG_PIECE_BIG")) : 0;
+    if (want >= 8) return want;
+    if (in_rows <= 0 || panel_bytes == 0) return piece;
+    const double row_bytes = (double)panel_bytes / (double)in_rows;
+    const double window_rows = 0.25 * (double)l2_bytes / row_bytes;
+    const double per_row = (double)nnz / (double)in_rows;
+    const double fit = window_rows * per_row / (double)(kSMs * 24);
+    int p = 32;
+    while (2 * p <= piece && 2.0 * p <= fit) p *= 2;
+    return p;
+}
+
+// SFDG_SPMM_BLOCKS=<k> (A/B testing): at most k blocks per SM in the SpMM grid (default 16)
+static unsigned spmm_blocks_per_sm() {
+    static const int want = std::getenv("SFDG_SPMM_BLOCKS") ? std::atoi(std::getenv("SFDG_SPMM_BLOCKS")) : 0;
+    return want >= 1 ? (unsigned)want : 16u;
+}
+
 void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cudaStream_t st, const int* d_idx,
                     int idx_range, size_t panel_bytes) {
     ProfScope prof("csc_build", st);
     rows = nrows;
     host_long = -1;
     piece = spmm_piece_length(nnz);
-    reserve_pieces(2 * (nnz / kPiece) + 2);  // any piece length >= kPiece
+    int l2 = 0, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    // A gathered panel larger than the L2: the pieces in flight (resident warps x piece entries)
+    // must cover a window of the panel that fits in the L2, or the long rows' gathers all come
+    // from HBM (see spmm_big_piece_length()).
+    if (panel_bytes > (size_t)l2) piece = spmm_big_piece_length(piece, nnz, idx_range, panel_bytes, (size_t)l2);
+    reserve_pieces(2 * (nnz / std::min(piece, kPiece)) + 2);  // any piece length >= min(piece, kPiece)
     if (nrows > cap_rows) {
         for (void* p : {(void*)long_rows, (void*)long_first, (void*)arrive, (void*)order}) if (p) cudaFree(p);
         CK(cudaMalloc(&long_rows, (size_t)nrows * sizeof(int)));
@@ -653,6 +735,11 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     host_pieces = -1;
     has_porder = false;
     if (!counts) CK(cudaMalloc(&counts, 3 * sizeof(int)));
+    if (!ticket) {
+        CK(cudaMalloc(&ticket, 2 * sizeof(int)));
+        CK(cudaMemset(ticket, 0, 2 * sizeof(int)));  // self-resetting afterwards
+    }
+    big = panel_bytes > (size_t)l2;
     CK(cudaMemsetAsync(counts, 0, 3 * sizeof(int), st));
     if (nrows == 0) return;
     int64_t* is_long = scr.take<int64_t>(nrows);
@@ -672,17 +759,14 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     LAUNCH(plan_fill_kernel, g, 256, 0, st, d_ptr, nrows, piece, is_long, long_off, piece_off, long_rows, long_first,
            piece_beg, piece_end, piece_li, counts, bin_off, order);
     // Pieces in the order of the first input index they gather (porder), for panels larger
-    // than the L2 (c3, c5): the grid then works on pieces of many long rows over nearby panel
-    // rows at a time (c5 CSC: DRAM 41.6 -> 36.8 GB per launch, L2 hits 3 -> 10 %; c3 stream
-    // 3725 -> 3454 ms; c5 shard 6160 -> 5893 ms). An L2-resident panel (c4) gains nothing and its
-    // standalone launch got slower (146 -> 156 us). Cutting long rows at window boundaries of
-    // the gathered index as well (tools/porder_ab.sh) kept the L2 hit rate at 10 % and was slower:
-    // 7000 warps x `piece` entries in flight span a third of the panel whatever the window.
+    // than the L2 (c3, c5): taken by ticket in that order (spmm()), the pieces in flight are the
+    // pieces of many long rows over one window of panel rows, sized to fit the L2 by
+    // spmm_big_piece_length(). With statically strided pieces of the default length the order
+    // alone gave c5 CSC DRAM 41.6 -> 36.8 GB per launch (L2 hits 3 -> 10 %); the ticket and the
+    // 64-entry pieces 20.2 GB (39 %), 6.17 -> 3.90 ms. An L2-resident panel (c4) gains nothing and
+    // its standalone launch got slower (146 -> 156 us).
     // SFDG_PIECE_ORDER=0 / 1 forces it off / on (A/B testing).
     const char* po_env = std::getenv("SFDG_PIECE_ORDER");
-    int l2 = 0, dev = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
     const bool pord = po_env ? std::atoi(po_env) != 0 : panel_bytes > (size_t)l2;
     has_porder = pord && d_idx && idx_range > 0 && nnz > 2 * piece;
     if (has_porder) {
@@ -699,8 +783,10 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
 
 void SegPlan::reserve_pieces(int64_t need) {
     if (need > cap_pieces) {
-        for (void* p : {(void*)piece_beg, (void*)piece_end, (void*)piece_li, (void*)porder}) if (p) cudaFree(p);
+        for (void* p : {(void*)piece_beg, (void*)piece_end, (void*)piece_li, (void*)porder, (void*)garrive}) if (p) cudaFree(p);
         cap_pieces = need;
+        CK(cudaMalloc(&garrive, cap_pieces * sizeof(int)));
+        CK(cudaMemset(garrive, 0, cap_pieces * sizeof(int)));  // self-resetting afterwards
         CK(cudaMalloc(&piece_beg, cap_pieces * sizeof(int)));
         CK(cudaMalloc(&piece_end, cap_pieces * sizeof(int)));
         CK(cudaMalloc(&piece_li, cap_pieces * sizeof(int)));
@@ -720,9 +806,10 @@ void SegPlan::release() {
     partial = nullptr;
     partial_cap = 0;
     for (void* p : {(void*)long_rows, (void*)long_first, (void*)piece_beg, (void*)piece_end, (void*)piece_li,
-                    (void*)arrive, (void*)order, (void*)counts, (void*)porder})
+                    (void*)arrive, (void*)order, (void*)counts, (void*)porder, (void*)garrive, (void*)ticket})
         if (p) cudaFree(p);
-    long_rows = long_first = piece_beg = piece_end = piece_li = arrive = order = counts = porder = nullptr;
+    ticket = nullptr;
+    long_rows = long_first = piece_beg = piece_end = piece_li = arrive = order = counts = porder = garrive = nullptr;
     cap_rows = 0;
     cap_pieces = 0;
 }
@@ -763,9 +850,13 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
     const int use_pieces = plan.host_long != 0 ? 1 : 0;
     const int64_t pieces = plan.host_pieces >= 0 ? plan.host_pieces : 2 * (nnz / plan.piece) + 2;
     // a function of nrows only, so a captured sweep block replays unchanged for any piece count
-    const unsigned grid = std::max(1u, std::min(16u * kSMs, ceil_div((size_t)nrows * 2 * 32, 256)));
+    const unsigned grid = std::max(1u, std::min(spmm_blocks_per_sm() * kSMs, ceil_div((size_t)nrows * 2 * 32, 256)));
     if (use_pieces) plan.ensure_partial(std::max<int64_t>(pieces, 1) * ld);
     double* partial = use_pieces ? plan.partial : nullptr;
+    // pieces by ticket for gathered panels larger than L2 (SFDG_SPMM_DYN=0 / 1 forces it off / on
+    // for every panel: A/B testing; the sums do not depend on it)
+    static const int dyn_env = std::getenv("SFDG_SPMM_DYN") ? std::atoi(std::getenv("SFDG_SPMM_DYN")) : -1;
+    int* ticket = use_pieces && (dyn_env < 0 ? plan.big : dyn_env != 0) ? plan.ticket : nullptr;
     const bool use_hot = hot && hot->n > 0;
     if (use_hot) {
         int dev = 0, sms = 0;
@@ -778,8 +869,8 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
         auto* fn = spmm_kernel<JJ, true>;                                                                             \
         if (first_on_device((const void*)fn)) allow_max_dynamic_smem(fn);                                            \
         LAUNCH(fn, (unsigned)sms, (spmm_threads<JJ, true>()), smem, st, d_ptr, hot->idx, d_val, nrows, plan.piece_beg, \
-               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.order, use_pieces,  \
-               d_in, ld, ncols, d_out, ldo, partial, hot->cols, hot->n, plan.piece_order());                     \
+               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.garrive, plan.order, use_pieces,  \
+               d_in, ld, ncols, d_out, ldo, partial, hot->cols, hot->n, plan.piece_order(), ticket);                     \
         break;                                                                                                        \
     }
             SPMM_HOT(1)
@@ -806,8 +897,8 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
     case JJ:                                                                                                       \
         ::sfdg::launch_kernel_l2win((spmm_kernel<JJ, false>), dim3(grid), dim3(256), 0, st, (const void*)d_in, win,  \
                d_ptr, d_idx, d_val, nrows, plan.piece_beg,                                                          \
-               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.order, use_pieces, \
-               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0, plan.piece_order());            \
+               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.garrive, plan.order, use_pieces, \
+               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0, plan.piece_order(), ticket);            \
         g_launches.fetch_add(1, std::memory_order_relaxed);                                                      \
         return;
             SPMM_WIN(1)
@@ -827,8 +918,8 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
 #define SPMM_CASE(JJ)                                                                                              \
     case JJ:                                                                                                       \
         LAUNCH((spmm_kernel<JJ, false>), grid, 256, 0, st, d_ptr, d_idx, d_val, nrows, plan.piece_beg,             \
-               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.order, use_pieces, \
-               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0, plan.piece_order());            \
+               plan.piece_end, plan.piece_li, plan.long_rows, plan.long_first, plan.counts, plan.arrive, plan.garrive, plan.order, use_pieces, \
+               d_in, ld, ncols, d_out, ldo, partial, (const int*)nullptr, 0, plan.piece_order(), ticket);            \
         break;
         SPMM_CASE(1)
         SPMM_CASE(2)

@@ -101,9 +101,14 @@ struct DevCsr {
 // tools/spmm_lab.cu). The order only changes which warp computes a row, never the row's
 // arithmetic, so results do not depend on it.
 // piece: 128 entries, doubled while a piece stays under half the grid's per-warp share of the
-// entries (c3: 512, c5: 1024), so the partial rows of very long rows stay few.
+// entries (up to 512 at c3-c5), so the partial rows of very long rows stay few; for a gathered
+// panel larger than L2, shortened again so the pieces in flight cover an L2-sized window of it
+// (spmm_big_piece_length: c5 CSC 64). A long row's partials are summed in two levels.
 constexpr int kPiece = 128;
+constexpr int kPieceGroup = 64;  // pieces per first-level sum of a long row's partials
 int spmm_piece_length(int64_t nnz);
+// for gathered panels larger than the L2: the pieces in flight must cover an L2-sized window
+int spmm_big_piece_length(int piece, int64_t nnz, int64_t in_rows, size_t panel_bytes, size_t l2_bytes);
 struct SegPlan {
     int rows = 0;
     int piece = kPiece;
@@ -112,7 +117,8 @@ struct SegPlan {
     int* piece_beg = nullptr;
     int* piece_end = nullptr;
     int* piece_li = nullptr;  // long-row index of each piece
-    int* arrive = nullptr;    // per long row: pieces finished in the current launch (self-resetting)
+    int* arrive = nullptr;    // per long row: piece groups finished in the current launch (self-resetting)
+    int* garrive = nullptr;   // per group of kPieceGroup pieces (at its first piece): pieces finished
     int* order = nullptr;     // the short rows, longest first
     // Processing order of the pieces (null: piece order): by the first input index a piece
     // gathers (the row of a CSC piece, the column of a CSR piece) in coarse buckets, so the grid
@@ -121,6 +127,8 @@ struct SegPlan {
     bool has_porder = false;  // porder filled by the last build
     const int* piece_order() const { return has_porder ? porder : nullptr; }
     int* counts = nullptr;  // device [nlong, npieces, nshort]
+    int* ticket = nullptr;  // device [next piece, warps done]: pieces by ticket (big panels)
+    bool big = false;       // the gathered panel is larger than the L2 (set by build)
     int host_long = -1;     // long rows as known on the host (-1: unknown -> always run the piece path)
     int64_t host_pieces = -1;  // pieces as known on the host (-1: unknown -> worst-case partial buffer)
     // Partial rows of the pieces: a retained buffer (not scratch), so its address is fixed for

@@ -94,6 +94,35 @@ def test_csr_products_long_rows_and_columns():
     assert np.array_equal(y, y2) and np.array_equal(w, w2)
 
 
+@pytest.mark.parametrize("k", [16, 130, 200])
+def test_csr_products_many_pieces_two_level_sum(k):
+    """A row and a column of more than kPieceGroup (64) pieces of 128 entries: their partial rows
+    are summed in two levels (groups of 64 pieces, then the group sums), a second long row /
+    column with one group plus a remainder, and one of exactly 64 pieces (a single group)."""
+    rng = np.random.default_rng(17)
+    m, d = 21000, 21000
+    rows = [np.sort(rng.choice(d, 4, replace=False)) for _ in range(m)]
+    rows[3] = np.arange(0, 20000)           # 157 pieces: two full groups + a remainder
+    rows[11] = np.arange(5, 5 + 64 * 128)   # exactly one group
+    rows[12] = np.arange(1, 1 + 9001)       # 71 pieces: one group + 7
+    for i in range(0, 20500):               # column 7: 20500 entries; column 9: 9000
+        rows[i] = np.union1d(rows[i], [7] if i >= 9000 else [7, 9])
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    cs = np.concatenate(rows).astype(np.uint32)
+    vs = rng.standard_normal(cs.size)
+    x, z = rng.standard_normal((d, k)), rng.standard_normal((m, k))
+    y, w = P.csr_products((rp, cs, vs), d, x=x, z=z)
+    import scipy.sparse as sp
+
+    a = sp.csr_matrix((vs, cs.astype(np.int64), rp), shape=(m, d))
+    ya, wa = a @ x, a.T @ z
+    assert np.max(np.abs(y - ya)) <= 1e-11 * np.abs(ya).max()
+    assert np.max(np.abs(w - wa)) <= 1e-11 * np.abs(wa).max()
+    y2, w2 = P.csr_products((rp, cs, vs), d, x=x, z=z)  # deterministic, counters reset
+    assert np.array_equal(y, y2) and np.array_equal(w, w2)
+
+
 def test_csr_products_empty_rows_and_buffer():
     rp = np.array([0, 0, 2, 2, 3], np.int64)
     cs = np.array([1, 4, 0], np.uint32)

@@ -71,3 +71,47 @@ def test_piece_order_is_bit_identical(monkeypatch, family, d, ell, rows):
     monkeypatch.setenv("SFDG_PIECE_ORDER", "0")
     b_n, st_n = _sketch(rp, cs, vs, d, ell, 4)
     assert np.array_equal(b_o, b_n) and st_o == st_n
+
+
+@pytest.mark.parametrize("family,d,ell,rows", [("c4", 3000, 64, 6000), ("c5", 4000, 128, 8000)])
+def test_pieces_by_ticket_are_bit_identical(monkeypatch, family, d, ell, rows):
+    """Pieces taken by ticket as warps become free (default for panels larger than L2; forced on
+    here, with the first-index order) or statically strided: only which warp runs a piece, and
+    when, changes -- the two-level sums keep the piece order -- so the sketches are the same bits,
+    launch after launch (the ticket and arrival counters reset themselves)."""
+    rp, cs, vs = S.generate(S.StreamConfig(family, rows, d, ell, 9), (0, rows))
+    monkeypatch.setenv("SFDG_PIECE_ORDER", "1")
+    monkeypatch.setenv("SFDG_SPMM_DYN", "1")
+    b_t, st_t = _sketch(rp, cs, vs, d, ell, 5)
+    monkeypatch.setenv("SFDG_SPMM_DYN", "0")
+    b_s, st_s = _sketch(rp, cs, vs, d, ell, 5)
+    assert np.array_equal(b_t, b_s) and st_t == st_s
+
+
+def test_products_with_a_panel_larger_than_l2():
+    """A'^T Z with a Z panel larger than the L2 (300k rows x 64 columns = 154 MB): the CSC plan
+    shortens its pieces so the pieces in flight cover an L2-sized window, takes them by ticket in
+    first-row order and sums columns of more than 64 pieces in two levels. Against scipy, and the
+    same bits on a second run."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(23)
+    m, d, k = 300_000, 5000, 64
+    per = 5
+    cols = rng.integers(20, d, size=(m, per))
+    hot = rng.random((m, 3)) < np.array([0.9, 0.2, 0.02])  # columns 0, 1, 2: 270k / 60k / 6k entries
+    rows = []
+    for i in range(m):
+        r = np.unique(cols[i])
+        rows.append(np.concatenate([np.nonzero(hot[i])[0], r]))
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    cs = np.concatenate(rows).astype(np.uint32)
+    vs = rng.standard_normal(cs.size)
+    z = rng.standard_normal((m, k))
+    a = sp.csr_matrix((vs, cs.astype(np.int64), rp), shape=(m, d))
+    wa = a.T @ z
+    _, w = P.csr_products((rp, cs, vs), d, z=z)
+    assert np.max(np.abs(w - wa)) <= 1e-11 * np.abs(wa).max()
+    _, w2 = P.csr_products((rp, cs, vs), d, z=z)
+    assert np.array_equal(w, w2)
