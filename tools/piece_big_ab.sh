@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 OUT=gpurun_out/piece_big_ab.txt
 : > $OUT
 for V in ${1:-0:16:0 128:16:1 64:16:1}; do
-  IFS=: read P B D <<< "$V"; export SFDG_SPMM_DYN=$D
+  IFS=: read P B D <<< "$V"; if [ "$D" = x ]; then unset SFDG_SPMM_DYN; else export SFDG_SPMM_DYN=$D; fi
   SFDG_PIECE_BIG=$P SFDG_SPMM_BLOCKS=$B SFDG_LANES=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
     --clock-control none -k regex:"spmm_kernel" -s 8 -c 2 --csv --log-file gpurun_out/pb_c5_${P}_${B}_${D}.csv \
     python bench.py --config c5 --rows 1000000 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-accuracy --no-isolated > /dev/null 2>&1
