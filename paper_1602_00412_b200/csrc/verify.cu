@@ -565,20 +565,21 @@ __device__ int vg_decide(const VerifyArgs& a, VState* st, int s, int nblk, doubl
     return 1;
 }
 
-// Lane-strided sum of part[first .. last) with eight loads per lane in flight (a column of
+// Lane-strided sum of part[first], part[first + step], ... (< last) with eight loads per lane in flight (a column of
 // thousands of pieces -- c5's most frequent item has 13 700 -- is summed by one warp: a dependent
 // load per iteration made that a 300 us tail). Fixed order: deterministic.
-__device__ __forceinline__ double lane_strided_sum(const double* part, int first, int last, int lane) {
+__device__ __forceinline__ double lane_strided_sum(const double* part, int first, int last, int step, int lane) {
     double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    int q = first + lane;
-    for (; q + 32 * 7 < last; q += 256) {
+    const int64_t st = 32 * (int64_t)step;
+    int64_t q = first + (int64_t)lane * step;
+    for (; q + 7 * st < last; q += 8 * st) {
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + q + 32 * u);
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + q + u * st);
 #pragma unroll
         for (int u = 0; u < 8; ++u) s[u] += v[u];
     }
-    for (; q < last; q += 32) s[0] += __ldcg(part + q);
+    for (; q < last; q += st) s[0] += __ldcg(part + q);
     return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
@@ -648,7 +649,9 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_rows_kernel(VerifyArgs a, VS
         if (old == last - first - 1) {  // every piece of this row is written: sum them in order
             __threadfence();
             // the whole warp sums the row's pieces: lane-strided, then a fixed shuffle tree
-            const double tot = warp_sum(lane_strided_sum(a.r_part, first, last, lane));
+            double tot = 0.0;
+            for (int q = first + lane; q < last; q += 32) tot += __ldcg(a.r_part + q);
+            tot = warp_sum(tot);
             if (lane == 0) {
                 a.u[a.r_long_rows[li]] = tot;
                 a.r_arrive[li] = 0;  // ready for the next launch
@@ -687,8 +690,17 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_colsum_kernel(VerifyArgs a, 
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int np = a.has_long ? a.counts[1] : 0;
     const int ns = a.c_order ? a.counts[2] : (int)a.d;
+    // A long column's pieces in runs of vrun consecutive pieces (about 512 entries) per warp: the
+    // SpMM's pieces may be as short as 64 entries (panels larger than L2), and a scalar gather per
+    // entry does not pay a partial, a fence and an arrival per such piece (c5: 568 -> 290 us).
+    const int vrun = max(1, 512 / max(a.piece, 1));
     for (int64_t p = gw; p < np; p += nw) {
-        const int kb = a.piece_beg[p], ke = a.piece_end[p];
+        const int li = a.c_piece_li[p];
+        const int nl = a.counts[0];
+        const int first = a.long_first[li], last = li + 1 < nl ? a.long_first[li + 1] : np;
+        if ((p - first) % vrun != 0) continue;  // not the head of a run
+        const int pend = min((int)p + vrun, last);
+        const int kb = a.piece_beg[p], ke = a.piece_end[pend - 1];
         double sp[4] = {0.0, 0.0, 0.0, 0.0};  // four gathers per lane in flight
         for (int k = kb + lane; k < ke; k += 128) {
 #pragma unroll
@@ -698,15 +710,12 @@ __global__ void __launch_bounds__(kGRowsThreads) vg_colsum_kernel(VerifyArgs a, 
         const double t = warp_sum((sp[0] + sp[1]) + (sp[2] + sp[3]));
         if (lane == 0) a.lpart[p] = t;
         __threadfence();
-        const int li = a.c_piece_li[p];
-        const int nl = a.counts[0];
-        const int first = a.long_first[li], last = li + 1 < nl ? a.long_first[li + 1] : np;
         int old = 0;
         if (lane == 0) old = atomicAdd(a.c_arrive + li, 1);
         old = __shfl_sync(0xffffffffu, old, 0);
-        if (old == last - first - 1) {  // every piece of this column is written: sum them in order
+        if (old == (last - first + vrun - 1) / vrun - 1) {  // every run of this column is written: sum them in order
             __threadfence();
-            const double tot = warp_sum(lane_strided_sum(a.lpart, first, last, lane));
+            const double tot = warp_sum(lane_strided_sum(a.lpart, first, last, vrun, lane));
             if (lane == 0) {
                 a.w[a.long_cols[li]] = tot;
                 a.c_arrive[li] = 0;  // ready for the next launch
