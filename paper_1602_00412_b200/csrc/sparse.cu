@@ -208,37 +208,22 @@ __device__ __forceinline__ int64_t bin_slot(int64_t* bins, int b) {
     return (int64_t)base + __popc(peers & ((1u << lane) - 1u));
 }
 
-// Piece length of a long row of `len` entries: `piece`, or (win > 0: gathered panels larger than
-// L2) the power of two <= piece that keeps a piece's entries within about `win` of the
-// `in_rows` panel rows -- a sparse long row's entries are spread over the whole panel, so its
-// pieces must be shorter than a dense one's to stay inside the window the grid is working on.
-__device__ __forceinline__ int piece_of(int len, int piece, int64_t win, int64_t in_rows) {
-    if (win <= 0) return piece;
-    const int64_t t = (int64_t)len * win / in_rows;
-    int p = 8;
-    while (2 * p <= piece && 2 * p <= t) p *= 2;
-    return p;
-}
-
 // short rows are binned by length, longest first (bin 2 piece - len), for the SpMM's row order
-__global__ void plan_count_kernel(const int* __restrict__ ptr, int nrows, int piece, int64_t win, int64_t in_rows,
-                                  int64_t* __restrict__ is_long, int64_t* __restrict__ npieces,
-                                  int64_t* __restrict__ bins) {
+__global__ void plan_count_kernel(const int* __restrict__ ptr, int nrows, int piece, int64_t* __restrict__ is_long,
+                                  int64_t* __restrict__ npieces, int64_t* __restrict__ bins) {
     pdl_entry();
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
         const int len = ptr[r + 1] - ptr[r];
         const bool lg = len > 2 * piece;
         is_long[r] = lg ? 1 : 0;
-        const int pl = lg ? piece_of(len, piece, win, in_rows) : piece;
-        npieces[r] = lg ? (len + pl - 1) / pl : 0;
+        npieces[r] = lg ? (len + piece - 1) / piece : 0;
         if (!lg) bin_slot(bins, 2 * piece - len);
     }
 }
 
 // Pieces of the long rows in row order; the short rows scattered into their length bins (the
 // order inside a bin is arbitrary: it only decides which warp computes a row).
-__global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int piece, int64_t win, int64_t in_rows,
-                                 const int64_t* __restrict__ is_long,
+__global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int piece, const int64_t* __restrict__ is_long,
                                  const int64_t* __restrict__ long_off, const int64_t* __restrict__ piece_off,
                                  int* __restrict__ long_rows, int* __restrict__ long_first, int* __restrict__ piece_beg,
                                  int* __restrict__ piece_end, int* __restrict__ piece_li,
@@ -252,11 +237,10 @@ __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int pie
             const int pf = (int)piece_off[r];
             long_rows[li] = r;
             long_first[li] = pf;
-            const int pl = piece_of(len, piece, win, in_rows);
-            const int np = (len + pl - 1) / pl;
+            const int np = (len + piece - 1) / piece;
             for (int p = 0; p < np; ++p) {
-                piece_beg[pf + p] = ptr[r] + p * pl;
-                piece_end[pf + p] = min(ptr[r] + (p + 1) * pl, ptr[r + 1]);
+                piece_beg[pf + p] = ptr[r] + p * piece;
+                piece_end[pf + p] = min(ptr[r] + (p + 1) * piece, ptr[r + 1]);
                 piece_li[pf + p] = li;
             }
         } else {
@@ -264,8 +248,7 @@ __global__ void plan_fill_kernel(const int* __restrict__ ptr, int nrows, int pie
         }
         if (r == nrows - 1) {
             counts[0] = (int)(long_off[r] + is_long[r]);
-            const int pl = piece_of(len, piece, win, in_rows);
-            counts[1] = (int)(piece_off[r] + (len > 2 * piece ? (len + pl - 1) / pl : 0));
+            counts[1] = (int)(piece_off[r] + (len > 2 * piece ? (len + piece - 1) / piece : 0));
             counts[2] = nrows - counts[0];
         }
     }
@@ -739,12 +722,7 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     // must cover a window of the panel that fits in the L2, or the long rows' gathers all come
     // from HBM (see spmm_big_piece_length()).
     if (panel_bytes > (size_t)l2) piece = spmm_big_piece_length(piece, nnz, idx_range, panel_bytes, (size_t)l2);
-    // SFDG_PIECE_VAR=1 (A/B testing): a sparse long row's pieces shortened to the same window
-    static const bool var_env = std::getenv("SFDG_PIECE_VAR") && std::atoi(std::getenv("SFDG_PIECE_VAR")) != 0;
-    int64_t var_win = 0;
-    if (var_env && panel_bytes > (size_t)l2 && idx_range > 0)
-        var_win = std::max<int64_t>(1, (int64_t)(0.25 * (double)l2 / ((double)panel_bytes / (double)idx_range)));
-    reserve_pieces(2 * (nnz / (var_win > 0 ? 8 : std::min(piece, kPiece))) + 2);  // any piece length the plan may use
+    reserve_pieces(2 * (nnz / std::min(piece, kPiece)) + 2);  // any piece length >= min(piece, kPiece)
     if (nrows > cap_rows) {
         for (void* p : {(void*)long_rows, (void*)long_first, (void*)arrive, (void*)order}) if (p) cudaFree(p);
         CK(cudaMalloc(&long_rows, (size_t)nrows * sizeof(int)));
@@ -760,6 +738,7 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     if (!ticket) {
         CK(cudaMalloc(&ticket, 2 * sizeof(int)));
         CK(cudaMemset(ticket, 0, 2 * sizeof(int)));  // self-resetting afterwards
+        CK(cudaDeviceSynchronize());  // the lane streams do not order against the null stream's memset
     }
     big = panel_bytes > (size_t)l2;
     CK(cudaMemsetAsync(counts, 0, 3 * sizeof(int), st));
@@ -773,12 +752,12 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     int64_t* bin_off = scr.take<int64_t>(nbins);
     CK(cudaMemsetAsync(bins, 0, nbins * sizeof(int64_t), st));
     const unsigned g = std::max(1u, std::min(8u * kSMs, ceil_div(nrows, 256)));
-    LAUNCH(plan_count_kernel, g, 256, 0, st, d_ptr, nrows, piece, var_win, (int64_t)idx_range, is_long, np, bins);
+    LAUNCH(plan_count_kernel, g, 256, 0, st, d_ptr, nrows, piece, is_long, np, bins);
     exclusive_scan(is_long, long_off, nrows, scr, st);
     exclusive_scan(np, piece_off, nrows, scr, st);
     exclusive_scan(bins, bin_off, nbins, scr, st);
     // pieces <= nnz / piece + nrows; size the piece arrays for the worst case of this call
-    LAUNCH(plan_fill_kernel, g, 256, 0, st, d_ptr, nrows, piece, var_win, (int64_t)idx_range, is_long, long_off, piece_off, long_rows, long_first,
+    LAUNCH(plan_fill_kernel, g, 256, 0, st, d_ptr, nrows, piece, is_long, long_off, piece_off, long_rows, long_first,
            piece_beg, piece_end, piece_li, counts, bin_off, order);
     // Pieces in the order of the first input index they gather (porder), for panels larger
     // than the L2 (c3, c5): taken by ticket in that order (spmm()), the pieces in flight are the
@@ -809,6 +788,7 @@ void SegPlan::reserve_pieces(int64_t need) {
         cap_pieces = need;
         CK(cudaMalloc(&garrive, cap_pieces * sizeof(int)));
         CK(cudaMemset(garrive, 0, cap_pieces * sizeof(int)));  // self-resetting afterwards
+        CK(cudaDeviceSynchronize());  // the lane streams do not order against the null stream's memset
         CK(cudaMalloc(&piece_beg, cap_pieces * sizeof(int)));
         CK(cudaMalloc(&piece_end, cap_pieces * sizeof(int)));
         CK(cudaMalloc(&piece_li, cap_pieces * sizeof(int)));
@@ -870,7 +850,7 @@ void spmm(const int* d_ptr, const int* d_idx, const double* d_val, int nrows, co
     }
     const int J = (ncols + 63) / 64;
     const int use_pieces = plan.host_long != 0 ? 1 : 0;
-    const int64_t pieces = plan.host_pieces >= 0 ? plan.host_pieces : std::max<int64_t>(plan.cap_pieces, 2 * (nnz / plan.piece) + 2);
+    const int64_t pieces = plan.host_pieces >= 0 ? plan.host_pieces : 2 * (nnz / plan.piece) + 2;
     // a function of nrows only, so a captured sweep block replays unchanged for any piece count
     const unsigned grid = std::max(1u, std::min(spmm_blocks_per_sm() * kSMs, ceil_div((size_t)nrows * 2 * 32, 256)));
     if (use_pieces) plan.ensure_partial(std::max<int64_t>(pieces, 1) * ld);

@@ -1,6 +1,7 @@
 #!/bin/bash
 # Piece length / grid size of the SpMM for gathered panels larger than L2 (c5, c3): ncu DRAM bytes
 # and duration of one CSR and one CSC launch, then whole-step times.
+# (the fourth field, var, drove an experiment whose code was removed: leave it 0)
 # Usage: piece_big_ab.sh "<piece:blocks:dyn> ..." [c3]   (piece 0 = default length; dyn 1 = pieces by ticket)
 cd ${GRAFT_REPO_ROOT:-.}
 mkdir -p gpurun_out
