@@ -723,6 +723,10 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     // from HBM (see spmm_big_piece_length()).
     if (panel_bytes > (size_t)l2) piece = spmm_big_piece_length(piece, nnz, idx_range, panel_bytes, (size_t)l2);
     reserve_pieces(2 * (nnz / std::min(piece, kPiece)) + 2);  // any piece length >= min(piece, kPiece)
+    if (garrive_fresh) {
+        CK(cudaMemsetAsync(garrive, 0, cap_pieces * sizeof(int), st));
+        garrive_fresh = false;
+    }
     if (nrows > cap_rows) {
         for (void* p : {(void*)long_rows, (void*)long_first, (void*)arrive, (void*)order}) if (p) cudaFree(p);
         CK(cudaMalloc(&long_rows, (size_t)nrows * sizeof(int)));
@@ -737,8 +741,7 @@ void SegPlan::build(const int* d_ptr, int nrows, int64_t nnz, Scratch& scr, cuda
     if (!counts) CK(cudaMalloc(&counts, 3 * sizeof(int)));
     if (!ticket) {
         CK(cudaMalloc(&ticket, 2 * sizeof(int)));
-        CK(cudaMemset(ticket, 0, 2 * sizeof(int)));  // self-resetting afterwards
-        CK(cudaDeviceSynchronize());  // the lane streams do not order against the null stream's memset
+        CK(cudaMemsetAsync(ticket, 0, 2 * sizeof(int), st));  // on the plan's stream; self-resetting afterwards
     }
     big = panel_bytes > (size_t)l2;
     CK(cudaMemsetAsync(counts, 0, 3 * sizeof(int), st));
@@ -787,8 +790,7 @@ void SegPlan::reserve_pieces(int64_t need) {
         for (void* p : {(void*)piece_beg, (void*)piece_end, (void*)piece_li, (void*)porder, (void*)garrive}) if (p) cudaFree(p);
         cap_pieces = need;
         CK(cudaMalloc(&garrive, cap_pieces * sizeof(int)));
-        CK(cudaMemset(garrive, 0, cap_pieces * sizeof(int)));  // self-resetting afterwards
-        CK(cudaDeviceSynchronize());  // the lane streams do not order against the null stream's memset
+        garrive_fresh = true;  // build() zeroes it on the plan's stream; self-resetting afterwards
         CK(cudaMalloc(&piece_beg, cap_pieces * sizeof(int)));
         CK(cudaMalloc(&piece_end, cap_pieces * sizeof(int)));
         CK(cudaMalloc(&piece_li, cap_pieces * sizeof(int)));

@@ -119,6 +119,7 @@ struct SegPlan {
     int* piece_li = nullptr;  // long-row index of each piece
     int* arrive = nullptr;    // per long row: piece groups finished in the current launch (self-resetting)
     int* garrive = nullptr;   // per group of kPieceGroup pieces (at its first piece): pieces finished
+    bool garrive_fresh = false;  // newly allocated: zeroed by the next build() on its stream
     int* order = nullptr;     // the short rows, longest first
     // Processing order of the pieces (null: piece order): by the first input index a piece
     // gathers (the row of a CSC piece, the column of a CSR piece) in coarse buckets, so the grid
